@@ -1,0 +1,439 @@
+// ps_adjust.cu -- multiple-testing adjustment on the device.
+//
+// Replaces adjust.py:23-87.  The family (strict upper triangle for symmetric
+// matrices, every cell otherwise) is compacted to its defined (non-NaN)
+// p-values, sorted ascending by an LSD radix sort over order-preserving 64-bit
+// keys, scaled by fl(scale / i) exactly as numpy's `values[order] * (scale /
+// arange(1, m+1))`, reverse-cumulative-minimised, clipped at 1 and scattered
+// back (mirrored, NaN diagonal).  Tied p-values receive identical adjusted
+// values whatever their order, so an unstable compaction and the radix sort's
+// tie order cannot change a bit of the result (adjust is bit-exact given the
+// same p matrix).  Bonferroni is min(1, m p).
+//
+// HBM-bound: each non-trivial radix pass streams 8 B key + 4 B index in and
+// out; passes whose digit is constant across the family are skipped.
+#include "ps_internal.cuh"
+#include <math_constants.h>
+#include <algorithm>
+#include <vector>
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;  // per thread per tile
+constexpr int kTile = kSortThreads * kSortItems;
+constexpr int kRadixBits = 8;
+constexpr int kBuckets = 1 << kRadixBits;
+
+__device__ __forceinline__ uint64_t key_of(double v) {
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double val_of(uint64_t k) {
+  uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+// Compact the defined members of the family into (key, flat index).
+__global__ void extract_kernel(const double* __restrict__ p, int64_t rows, int64_t cols,
+                               int symmetric, uint64_t* __restrict__ keys,
+                               uint32_t* __restrict__ idx, unsigned long long* __restrict__ count) {
+  const int64_t n = rows * cols;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    bool take = false;
+    double v = 0.0;
+    if (i < n) {
+      const int64_t r = i / cols, c = i - r * cols;
+      if (!symmetric || c > r) {
+        v = p[i];
+        take = !(v != v);
+      }
+    }
+    const uint32_t ball = __ballot_sync(PS_FULL, take);
+    unsigned long long off = 0;
+    if ((threadIdx.x & 31) == 0 && ball) off = atomicAdd(count, (unsigned long long)__popc(ball));
+    off = __shfl_sync(PS_FULL, off, 0);
+    if (take) {
+      const uint64_t pos = off + __popc(ball & lanemask_lt());
+      keys[pos] = key_of(v);
+      idx[pos] = (uint32_t)i;
+    }
+  }
+}
+
+__global__ void extract_vec_kernel(const double* __restrict__ p, int64_t n, uint64_t* __restrict__ keys,
+                                   uint32_t* __restrict__ idx, unsigned long long* __restrict__ count) {
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    double v = i < n ? p[i] : PS_NAN;
+    const bool take = !(v != v);
+    const uint32_t ball = __ballot_sync(PS_FULL, take);
+    unsigned long long off = 0;
+    if ((threadIdx.x & 31) == 0 && ball) off = atomicAdd(count, (unsigned long long)__popc(ball));
+    off = __shfl_sync(PS_FULL, off, 0);
+    if (take) {
+      const uint64_t pos = off + __popc(ball & lanemask_lt());
+      keys[pos] = key_of(v);
+      idx[pos] = (uint32_t)i;
+    }
+  }
+}
+
+// All eight digit histograms in one read of the keys (for pass skipping).
+__global__ void digit_hist_all_kernel(const uint64_t* __restrict__ keys, const unsigned long long* count_ptr,
+                                      unsigned long long* __restrict__ hist /* 8 x 256 */) {
+  __shared__ unsigned int h[8][kBuckets];
+  for (int i = threadIdx.x; i < 8 * kBuckets; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t m = (int64_t)*count_ptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) atomicAdd(&h[d][(k >> (8 * d)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * kBuckets; i += blockDim.x)
+    if ((&h[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&h[0][0])[i]);
+}
+
+// Per-tile digit counts for one pass: tile_hist[digit * ntiles + tile].
+__global__ void __launch_bounds__(kSortThreads)
+tile_hist_kernel(const uint64_t* __restrict__ keys, int64_t m, int shift, uint32_t* __restrict__ tile_hist,
+                 int64_t ntiles) {
+  __shared__ uint32_t h[kBuckets];
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t t0 = blockIdx.x * (int64_t)kTile;
+  for (int q = 0; q < kSortItems; ++q) {
+    const int64_t i = t0 + (int64_t)q * kSortThreads + threadIdx.x;
+    if (i < m) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kBuckets; d += blockDim.x) tile_hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+// Exclusive scan of a uint32 array (digit-major tile histograms) in place,
+// three-level: per-block scans, then a scan of block sums, then fix-up.
+__global__ void scan_block_kernel(uint32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ sums) {
+  __shared__ uint32_t s[1024];
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  uint32_t v = i < n ? a[i] : 0u;
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint32_t t = threadIdx.x >= (unsigned)o ? s[threadIdx.x - o] : 0u;
+    __syncthreads();
+    s[threadIdx.x] += t;
+    __syncthreads();
+  }
+  if (i < n) a[i] = s[threadIdx.x] - v;
+  if (threadIdx.x == 1023) sums[blockIdx.x] = s[1023];
+}
+__global__ void scan_add_kernel(uint32_t* __restrict__ a, int64_t n, const uint32_t* __restrict__ sums) {
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  if (i < n) a[i] += sums[blockIdx.x];
+}
+
+// Stable scatter of one tile: warps own contiguous runs of the tile and walk
+// them in order, so equal digits keep their input order (LSD correctness).
+__global__ void __launch_bounds__(kSortThreads)
+scatter_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+               uint32_t* __restrict__ vout, int64_t m, int shift, const uint32_t* __restrict__ tile_off,
+               int64_t ntiles) {
+  constexpr int NW = kSortThreads / 32;
+  constexpr int PER_WARP = kTile / NW;  // contiguous items per warp
+  __shared__ uint32_t wcnt[NW][kBuckets];
+  __shared__ uint32_t base[kBuckets];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NW * kBuckets; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  for (int d = threadIdx.x; d < kBuckets; d += blockDim.x) base[d] = tile_off[(int64_t)d * ntiles + blockIdx.x];
+  __syncthreads();
+  const int64_t w0 = blockIdx.x * (int64_t)kTile + (int64_t)warp * PER_WARP;
+  // pass 1: per-warp digit counts
+  for (int r = 0; r < PER_WARP; r += 32) {
+    const int64_t i = w0 + r + lane;
+    const bool ok = i < m;
+    const uint32_t d = ok ? (uint32_t)((kin[i] >> shift) & 0xff) : 0u;
+    const uint32_t peers = __match_any_sync(PS_FULL, ok ? d : 0xffffffffu);
+    if (ok && (peers & lanemask_lt()) == 0) wcnt[warp][d] += __popc(peers);
+  }
+  __syncthreads();
+  // exclusive scan over warps per digit
+  for (int d = threadIdx.x; d < kBuckets; d += blockDim.x) {
+    uint32_t run = base[d];
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = wcnt[w][d];
+      wcnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // pass 2: stable placement
+  for (int r = 0; r < PER_WARP; r += 32) {
+    const int64_t i = w0 + r + lane;
+    const bool ok = i < m;
+    uint64_t k = 0;
+    uint32_t v = 0, d = 0;
+    if (ok) {
+      k = kin[i];
+      v = vin[i];
+      d = (uint32_t)((k >> shift) & 0xff);
+    }
+    const uint32_t peers = __match_any_sync(PS_FULL, ok ? d : 0xffffffffu);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    uint32_t start = 0;
+    if (ok) start = wcnt[warp][d];
+    __syncwarp();
+    if (ok) {
+      const uint32_t pos = start + rank;
+      kout[pos] = k;
+      vout[pos] = v;
+      if ((peers >> lane) == 1u) wcnt[warp][d] = start + __popc(peers);  // highest lane of the group
+    }
+    __syncwarp();
+  }
+}
+
+// ranked[i] = val(key[i]) * fl(scale / (i+1)); then block-wise suffix minima.
+__global__ void rank_scale_kernel(const uint64_t* __restrict__ keys, int64_t m, double scale,
+                                  double* __restrict__ ranked, double* __restrict__ block_min) {
+  __shared__ double s[1024];
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  double v = CUDART_INF;
+  if (i < m) v = val_of(keys[i]) * (scale / (double)(i + 1));
+  s[threadIdx.x] = v;
+  __syncthreads();
+  // inclusive suffix-min within the block
+  for (int o = 1; o < 1024; o <<= 1) {
+    double t = threadIdx.x + o < 1024 ? s[threadIdx.x + o] : CUDART_INF;
+    __syncthreads();
+    s[threadIdx.x] = fmin(s[threadIdx.x], t);
+    __syncthreads();
+  }
+  if (i < m) ranked[i] = s[threadIdx.x];
+  if (threadIdx.x == 0) block_min[blockIdx.x] = s[0];
+}
+// suffix-min over block minima (exclusive, i.e. min of later blocks), in place
+__global__ void block_suffix_min_kernel(double* __restrict__ bm, int64_t nb) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double run = CUDART_INF;
+  for (int64_t b = nb - 1; b >= 0; --b) {
+    const double v = bm[b];
+    bm[b] = run;
+    run = fmin(run, v);
+  }
+}
+__global__ void bh_scatter_kernel(const double* __restrict__ ranked, const double* __restrict__ bm,
+                                  const uint32_t* __restrict__ idx, int64_t m, int64_t cols, int symmetric,
+                                  double* __restrict__ out) {
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  if (i >= m) return;
+  double v = fmin(ranked[i], bm[blockIdx.x]);
+  v = fmin(1.0, v);
+  const int64_t f = idx[i];
+  out[f] = v;
+  if (symmetric) {
+    const int64_t r = f / cols, c = f - r * cols;
+    out[c * cols + r] = v;
+  }
+}
+__global__ void bonferroni_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                                  const unsigned long long* __restrict__ count, int64_t cols, int symmetric,
+                                  double* __restrict__ out) {
+  const int64_t m = (int64_t)*count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = (double)m * val_of(keys[i]);
+    v = fmin(1.0, v);
+    const int64_t f = idx[i];
+    out[f] = v;
+    if (symmetric) {
+      const int64_t r = f / cols, c = f - r * cols;
+      out[c * cols + r] = v;
+    }
+  }
+}
+
+int scan_u32(uint32_t* a, int64_t n, cudaStream_t s) {
+  const int64_t nb = ps_ceil_div(n, 1024);
+  uint32_t* sums = nullptr;
+  PS_CUDA(ps_alloc(&sums, (size_t)nb, s));
+  scan_block_kernel<<<(unsigned)nb, 1024, 0, s>>>(a, n, sums);
+  PS_LAUNCHED();
+  if (nb > 1) {
+    int rc = scan_u32(sums, nb, s);
+    if (rc) return rc;
+    scan_add_kernel<<<(unsigned)nb, 1024, 0, s>>>(a, n, sums);
+    PS_LAUNCHED();
+  }
+  ps_free(sums, s);
+  return PS_OK;
+}
+
+// host-side BY factor: numpy's pairwise summation of 1/i (adjust.py:34-36).
+double numpy_pairwise_harmonic(int64_t m) {
+  // numpy sums float64 arrays with pairwise summation: blocks of <= 128
+  // elements are summed with 8 interleaved accumulators, larger ranges are
+  // split in halves (n2 = n/2 rounded down to a multiple of 8).
+  struct Rec {
+    static double sum(int64_t lo, int64_t n) {
+      if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r += 1.0 / (double)(lo + i + 1);
+        return r;
+      }
+      if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = 1.0 / (double)(lo + j + 1);
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+          for (int j = 0; j < 8; ++j) r[j] += 1.0 / (double)(lo + i + j + 1);
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += 1.0 / (double)(lo + i + 1);
+        return res;
+      }
+      int64_t n2 = n / 2;
+      n2 -= n2 % 8;
+      return sum(lo, n2) + sum(lo + n2, n - n2);
+    }
+  };
+  return Rec::sum(0, m);
+}
+
+int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int64_t cols,
+                int symmetric, int method, double* out, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  unsigned long long m_host = 0;
+  PS_CUDA(cudaMemcpyAsync(&m_host, d_count, sizeof(m_host), cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  const int64_t m = (int64_t)m_host;
+  if (m == 0) return PS_OK;
+  if (method == PS_ADJ_BONFERRONI) {
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(m, 256), (int64_t)ds->num_sms * 8);
+    bonferroni_kernel<<<blocks, 256, 0, s>>>(keys, idx, d_count, cols, symmetric, out);
+    PS_LAUNCHED();
+    return PS_OK;
+  }
+  // digit histograms -> which passes are non-trivial
+  unsigned long long* d_hist = nullptr;
+  PS_CUDA(ps_alloc(&d_hist, 8 * kBuckets, s));
+  PS_CUDA(cudaMemsetAsync(d_hist, 0, 8 * kBuckets * sizeof(unsigned long long), s));
+  {
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(m, 256), (int64_t)ds->num_sms * 4);
+    digit_hist_all_kernel<<<blocks, 256, 0, s>>>(keys, d_count, d_hist);
+    PS_LAUNCHED();
+  }
+  std::vector<unsigned long long> hist(8 * kBuckets);
+  PS_CUDA(cudaMemcpyAsync(hist.data(), d_hist, hist.size() * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  ps_free(d_hist, s);
+
+  uint64_t* k2 = nullptr;
+  uint32_t* v2 = nullptr;
+  const int64_t ntiles = ps_ceil_div(m, kTile);
+  uint32_t* tile_hist = nullptr;
+  PS_CUDA(ps_alloc(&k2, (size_t)m, s));
+  PS_CUDA(ps_alloc(&v2, (size_t)m, s));
+  PS_CUDA(ps_alloc(&tile_hist, (size_t)(ntiles * kBuckets), s));
+  uint64_t* kin = keys;
+  uint32_t* vin = idx;
+  uint64_t* kout = k2;
+  uint32_t* vout = v2;
+  for (int pass = 0; pass < 8; ++pass) {
+    bool trivial = false;
+    for (int d = 0; d < kBuckets; ++d)
+      if (hist[pass * kBuckets + d] == (unsigned long long)m) trivial = true;
+    if (trivial) continue;
+    const int shift = pass * kRadixBits;
+    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, m, shift, tile_hist, ntiles);
+    PS_LAUNCHED();
+    int rc = scan_u32(tile_hist, ntiles * kBuckets, s);
+    if (rc) return rc;
+    scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, s>>>(kin, vin, kout, vout, m, shift, tile_hist,
+                                                             ntiles);
+    PS_LAUNCHED();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  double scale = (double)m;
+  if (method == PS_ADJ_BY) scale *= numpy_pairwise_harmonic(m);
+  const int64_t nb = ps_ceil_div(m, 1024);
+  double* ranked = nullptr;
+  double* bm = nullptr;
+  PS_CUDA(ps_alloc(&ranked, (size_t)m, s));
+  PS_CUDA(ps_alloc(&bm, (size_t)nb, s));
+  rank_scale_kernel<<<(unsigned)nb, 1024, 0, s>>>(kin, m, scale, ranked, bm);
+  PS_LAUNCHED();
+  block_suffix_min_kernel<<<1, 32, 0, s>>>(bm, nb);
+  PS_LAUNCHED();
+  bh_scatter_kernel<<<(unsigned)nb, 1024, 0, s>>>(ranked, bm, vin, m, cols, symmetric, out);
+  PS_LAUNCHED();
+  ps_free(ranked, s);
+  ps_free(bm, s);
+  ps_free(k2, s);
+  ps_free(v2, s);
+  ps_free(tile_hist, s);
+  return PS_OK;
+}
+
+}  // namespace
+
+int ps_adjust_run(const double* p, int64_t rows, int64_t cols, int method, int symmetric, double* out,
+                  cudaStream_t s) {
+  if (method < 0 || method > 2) return ps_fail(PS_ERR_UNKNOWN_METHOD, "unknown adjustment method");
+  if (symmetric && rows != cols)
+    return ps_fail(PS_ERR_NON_SQUARE, "symmetric adjustment needs a square matrix");
+  const int64_t n = rows * cols;
+  if (n >= (int64_t)UINT32_MAX) return ps_fail(PS_ERR_INVALID, "family larger than 2^32 cells");
+  int rc = ps_fill_nan(out, n, s);
+  if (rc) return rc;
+  if (n == 0) return PS_OK;
+  ps_device_state* ds = ps_state();
+  const int64_t fam = symmetric ? rows * (rows - 1) / 2 : n;
+  if (fam == 0) return PS_OK;
+  uint64_t* keys = nullptr;
+  uint32_t* idx = nullptr;
+  unsigned long long* d_count = nullptr;
+  PS_CUDA(ps_alloc(&keys, (size_t)fam, s));
+  PS_CUDA(ps_alloc(&idx, (size_t)fam, s));
+  PS_CUDA(ps_alloc(&d_count, 1, s));
+  PS_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  const int blocks = (int)std::min<int64_t>(ps_ceil_div(n, 256), (int64_t)ds->num_sms * 8);
+  extract_kernel<<<blocks, 256, 0, s>>>(p, rows, cols, symmetric, keys, idx, d_count);
+  PS_LAUNCHED();
+  rc = adjust_core(keys, idx, d_count, cols, symmetric, method, out, s);
+  ps_free(keys, s);
+  ps_free(idx, s);
+  ps_free(d_count, s);
+  return rc;
+}
+
+int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s) {
+  if (method < 0 || method > 2) return ps_fail(PS_ERR_UNKNOWN_METHOD, "unknown adjustment method");
+  if (n >= (int64_t)UINT32_MAX) return ps_fail(PS_ERR_INVALID, "family larger than 2^32 cells");
+  int rc = ps_fill_nan(out, n, s);
+  if (rc || n == 0) return rc;
+  ps_device_state* ds = ps_state();
+  uint64_t* keys = nullptr;
+  uint32_t* idx = nullptr;
+  unsigned long long* d_count = nullptr;
+  PS_CUDA(ps_alloc(&keys, (size_t)n, s));
+  PS_CUDA(ps_alloc(&idx, (size_t)n, s));
+  PS_CUDA(ps_alloc(&d_count, 1, s));
+  PS_CUDA(cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s));
+  const int blocks = (int)std::min<int64_t>(ps_ceil_div(n, 256), (int64_t)ds->num_sms * 8);
+  extract_vec_kernel<<<blocks, 256, 0, s>>>(p, n, keys, idx, d_count);
+  PS_LAUNCHED();
+  rc = adjust_core(keys, idx, d_count, n, 0, method, out, s);
+  ps_free(keys, s);
+  ps_free(idx, s);
+  ps_free(d_count, s);
+  return rc;
+}
+
+extern "C" double ps_by_factor(int64_t m) { return numpy_pairwise_harmonic(m); }

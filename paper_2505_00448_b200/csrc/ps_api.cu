@@ -1,0 +1,415 @@
+// ps_api.cu -- the C ABI (include/pairstat_b200.h): device state, prepared
+// matrices, block entry points and the host-buffer run() used by Python.
+#include "ps_internal.cuh"
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+std::recursive_mutex g_lock;
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+ps_device_state g_states[64];
+
+struct Guard {
+  std::lock_guard<std::recursive_mutex> lk{g_lock};
+};
+
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+int init_state(ps_device_state* st, int dev) {
+  if (st->device == dev) return PS_OK;
+  PS_CUDA(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  PS_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10) return ps_fail(PS_ERR_NO_DEVICE, "pair engine needs an sm_100 (B200) device");
+  st->num_sms = prop.multiProcessorCount;
+  PS_CUDA(cudaMalloc(&st->d_err, sizeof(int)));
+  PS_CUDA(cudaMemset(st->d_err, 0, sizeof(int)));
+  PS_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+  // keep freed workspace cached in the stream-ordered pool between calls
+  cudaMemPool_t pool;
+  PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = UINT64_MAX;
+  PS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  st->device = dev;
+  return PS_OK;
+}
+
+int ensure_state() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return ps_fail(PS_ERR_NO_DEVICE, "no CUDA device visible");
+  }
+  const int dev = current_device();
+  return init_state(&g_states[dev], dev);
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Read and reset the device error word (synchronises the stream).
+int drain_errors(cudaStream_t s) {
+  ps_device_state* st = ps_state();
+  int err = 0;
+  PS_CUDA(cudaMemcpyAsync(&err, st->d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  if (err) {
+    PS_CUDA(cudaMemsetAsync(st->d_err, 0, sizeof(int), s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    return ps_fail(err, "raised by a device kernel");
+  }
+  return PS_OK;
+}
+
+}  // namespace
+
+ps_device_state* ps_state() { return &g_states[current_device()]; }
+void ps_count_launch(int n) { g_launches += n; }
+int ps_fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+int ps_cuda_check(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return PS_ERR_CUDA;
+}
+
+extern "C" {
+
+const char* ps_version(void) { return "paper_2505_00448_b200 0.1.0 (sm_100a)"; }
+const char* ps_last_error(void) { return g_last_error.c_str(); }
+int64_t ps_kernel_launches(void) { return g_launches.load(); }
+void ps_reset_kernel_launches(void) { g_launches = 0; }
+
+int ps_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *count = n;
+  return PS_OK;
+}
+
+int ps_set_device(int device) {
+  Guard g;
+  PS_CUDA(cudaSetDevice(device));
+  return ensure_state();
+}
+
+int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_presort, void* stream,
+                     ps_matrix** out) {
+  Guard g;
+  *out = nullptr;
+  int rc = ensure_state();
+  if (rc) return rc;
+  if (!desc || desc->n_features <= 0 || desc->n_samples <= 0)
+    return ps_fail(PS_ERR_INVALID, "expected a non-empty matrix");
+  cudaStream_t s = as_stream(stream);
+  ps_matrix* m = new ps_matrix();
+  m->device = current_device();
+  m->kind = desc->kind;
+  m->F = desc->n_features;
+  m->S = desc->n_samples;
+  m->W = ps_ceil_div(m->S, 32);
+  const double sent = desc->na_sentinel;
+  m->sentinel_is_nan = std::isnan(sent) ? 1 : 0;
+  std::memcpy(&m->sentinel_bits, &sent, sizeof(double));
+  const int64_t src_ld = desc->ld > 0 ? desc->ld : m->S;
+  if (m->kind != PS_KIND_CONTINUOUS) {
+    if (!desc->category_counts) {
+      delete m;
+      return ps_fail(PS_ERR_INVALID, "label matrix without category counts");
+    }
+    m->h_cat = new int64_t[m->F];
+    std::memcpy(m->h_cat, desc->category_counts, sizeof(int64_t) * m->F);
+    int64_t cmax = 0;
+    for (int64_t f = 0; f < m->F; ++f) cmax = std::max(cmax, m->h_cat[f]);
+    if (cmax > 254) {
+      delete[] m->h_cat;
+      delete m;
+      return ps_fail(PS_ERR_INVALID, "category counts above 254 are not supported by the device path");
+    }
+    m->cmax = (int)cmax;
+    std::vector<int32_t> c32(m->h_cat, m->h_cat + m->F);
+    rc = ps_alloc(&m->d_cat, (size_t)m->F, s) == cudaSuccess ? 0 : PS_ERR_CUDA;
+    if (!rc) rc = cudaMemcpyAsync(m->d_cat, c32.data(), sizeof(int32_t) * m->F, cudaMemcpyHostToDevice, s)
+                      == cudaSuccess ? 0 : PS_ERR_CUDA;
+    if (!rc) rc = cudaStreamSynchronize(s) == cudaSuccess ? 0 : PS_ERR_CUDA;
+    if (rc) {
+      ps_matrix_destroy(m);
+      return ps_fail(PS_ERR_CUDA, "category count upload failed");
+    }
+  }
+  if (values_on_device && (src_ld % 32) == 0 && (reinterpret_cast<uintptr_t>(desc->values) % 256) == 0) {
+    // use the caller's device buffer in place (must be zero-padded to ld)
+    m->d_vals = const_cast<double*>(desc->values);
+    m->ld = src_ld;
+    m->owns_vals = false;
+  } else {
+    m->ld = ps_round_up(m->S, 32);
+    if (ps_alloc(&m->d_vals, (size_t)(m->F * m->ld), s) != cudaSuccess) {
+      ps_matrix_destroy(m);
+      return ps_fail(PS_ERR_CUDA, "out of device memory for the input matrix");
+    }
+    cudaError_t e = cudaSuccess;
+    if (m->ld != m->S) e = cudaMemsetAsync(m->d_vals, 0, sizeof(double) * m->F * m->ld, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
+                            sizeof(double) * m->S, m->F,
+                            values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      ps_matrix_destroy(m);
+      return ps_cuda_check(e, "input upload");
+    }
+  }
+  rc = ps_prepare_matrix(m, s);
+  if (!rc && want_presort) rc = ps_presort_matrix(m, s);
+  if (rc) {
+    ps_matrix_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return PS_OK;
+}
+
+int ps_matrix_destroy(ps_matrix* m) {
+  if (!m) return PS_OK;
+  Guard g;
+  cudaStream_t s = ps_state()->stream;
+  if (m->owns_vals) ps_free(m->d_vals, s);
+  ps_free(m->d_mask, s);
+  ps_free(m->d_center, s);
+  ps_free(m->d_count, s);
+  ps_free(m->d_cat, s);
+  ps_free(m->d_codes, s);
+  ps_free(m->d_zero, s);
+  ps_free(m->d_bad, s);
+  ps_free(m->d_order, s);
+  ps_free(m->d_gs, s);
+  ps_free(m->d_ge, s);
+  ps_free(m->d_tied, s);
+  ps_free(m->d_inv, s);
+  delete[] m->h_cat;
+  delete m;
+  return PS_OK;
+}
+
+static int need_kind(ps_matrix* m, bool continuous, const char* what) {
+  if (!m) return ps_fail(PS_ERR_INVALID, std::string(what) + ": missing matrix");
+  if (continuous != (m->kind == PS_KIND_CONTINUOUS))
+    return ps_fail(PS_ERR_INVALID, std::string(what) + ": wrong matrix kind");
+  return PS_OK;
+}
+
+int ps_pearson_block(ps_matrix* a, int64_t lo, int64_t hi, double* out_stat, double* out_p,
+                     double* out_r2, void* stream) {
+  Guard g;
+  int rc = need_kind(a, true, "pearson");
+  if (!rc) rc = ps_pearson_run(a, lo, hi, out_stat, out_p, out_r2, as_stream(stream));
+  return rc;
+}
+
+int ps_spearman_block(ps_matrix* a, int64_t lo, int64_t hi, double* out_stat, double* out_p,
+                      double* out_rho, void* stream) {
+  Guard g;
+  int rc = need_kind(a, true, "spearman");
+  if (!rc && !a->has_presort) rc = ps_presort_matrix(a, as_stream(stream));
+  if (!rc) rc = ps_spearman_run(a, lo, hi, out_stat, out_p, out_rho, as_stream(stream));
+  return rc;
+}
+
+int ps_chi2_block(ps_matrix* a, int64_t lo, int64_t hi, double* out_stat, double* out_p,
+                  double* out_phi, double* out_v, void* stream) {
+  Guard g;
+  int rc = need_kind(a, false, "chi2");
+  if (!rc) rc = ps_chi2_run(a, lo, hi, out_stat, out_p, out_phi, out_v, as_stream(stream));
+  return rc;
+}
+
+int ps_ttest_block(ps_matrix* labels, ps_matrix* values, int64_t lo, int64_t hi, int student,
+                   double* out_stat, double* out_p, double* out_d, void* stream) {
+  Guard g;
+  int rc = need_kind(labels, false, "ttest");
+  if (!rc) rc = need_kind(values, true, "ttest");
+  if (!rc)
+    rc = ps_group_moment_run(PS_TEST_TTEST, labels, values, lo, hi, student, out_stat, out_p, out_d,
+                             as_stream(stream));
+  return rc;
+}
+
+int ps_anova_block(ps_matrix* labels, ps_matrix* values, int64_t lo, int64_t hi, double* out_stat,
+                   double* out_p, double* out_eta, void* stream) {
+  Guard g;
+  int rc = need_kind(labels, false, "anova");
+  if (!rc) rc = need_kind(values, true, "anova");
+  if (!rc)
+    rc = ps_group_moment_run(PS_TEST_ANOVA, labels, values, lo, hi, 1, out_stat, out_p, out_eta,
+                             as_stream(stream));
+  return rc;
+}
+
+int ps_mwu_block(ps_matrix* labels, ps_matrix* values, int64_t lo, int64_t hi, int u_mode,
+                 double* out_stat, double* out_p, double* out_r, void* stream) {
+  Guard g;
+  int rc = need_kind(labels, false, "mwu");
+  if (!rc) rc = need_kind(values, true, "mwu");
+  if (!rc && !values->has_presort) rc = ps_presort_matrix(values, as_stream(stream));
+  if (!rc)
+    rc = ps_rank_mixed_run(PS_TEST_MWU, labels, values, lo, hi, u_mode, out_stat, out_p, out_r,
+                           as_stream(stream));
+  return rc;
+}
+
+int ps_kruskal_block(ps_matrix* labels, ps_matrix* values, int64_t lo, int64_t hi, double* out_stat,
+                     double* out_p, double* out_eta, void* stream) {
+  Guard g;
+  int rc = need_kind(labels, false, "kruskal");
+  if (!rc) rc = need_kind(values, true, "kruskal");
+  if (!rc && !values->has_presort) rc = ps_presort_matrix(values, as_stream(stream));
+  if (!rc)
+    rc = ps_rank_mixed_run(PS_TEST_KRUSKAL, labels, values, lo, hi, 0, out_stat, out_p, out_eta,
+                           as_stream(stream));
+  return rc;
+}
+
+int ps_adjust_device(const double* p, int64_t rows, int64_t cols, int method, int symmetric,
+                     double* out, void* stream) {
+  Guard g;
+  int rc = ensure_state();
+  if (!rc) rc = ps_adjust_run(p, rows, cols, method, symmetric, out, as_stream(stream));
+  return rc;
+}
+
+int ps_adjust_family_device(const double* p, int64_t n, int method, double* out, void* stream) {
+  Guard g;
+  int rc = ensure_state();
+  if (!rc) rc = ps_adjust_family_run(p, n, method, out, as_stream(stream));
+  return rc;
+}
+
+int ps_sync(void* stream) {
+  Guard g;
+  int rc = ensure_state();
+  if (!rc) rc = drain_errors(as_stream(stream));
+  return rc;
+}
+
+// Host-buffer end-to-end run: engine.run (engine.py:415-557) on the device.
+int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_variant, int u_mode,
+           double* const* outs, double* const* adj_outs) {
+  Guard g;
+  int rc = ensure_state();
+  if (rc) return rc;
+  ps_device_state* st = ps_state();
+  cudaStream_t s = st->stream;
+  const bool homogeneous = test == PS_TEST_PEARSON || test == PS_TEST_SPEARMAN || test == PS_TEST_CHI2;
+  if (!homogeneous && !b) return ps_fail(PS_ERR_INVALID, "mixed test needs a second matrix");
+  const bool presort_a = test == PS_TEST_SPEARMAN;
+  const bool presort_b = test == PS_TEST_MWU || test == PS_TEST_KRUSKAL;
+  ps_matrix* ma = nullptr;
+  ps_matrix* mb = nullptr;
+  rc = ps_matrix_create(a, 0, presort_a, s, &ma);
+  if (!rc && !homogeneous) rc = ps_matrix_create(b, 0, presort_b, s, &mb);
+  if (rc) {
+    ps_matrix_destroy(ma);
+    return rc;
+  }
+  const int64_t rows = ma->F, cols = homogeneous ? ma->F : mb->F;
+  const int64_t cells = rows * cols;
+  bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
+  double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* d_adj = nullptr;
+  for (int k = 0; k < 4 && !rc; ++k) {
+    const bool want = (outs && outs[k]) || (k == 1 && any_adj);
+    if (!want) continue;
+    if (ps_alloc(&d_out[k], (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
+    if (!rc) rc = ps_fill_nan(d_out[k], cells, s);
+  }
+  if (!rc) {
+    switch (test) {
+      case PS_TEST_PEARSON: rc = ps_pearson_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s); break;
+      case PS_TEST_SPEARMAN: rc = ps_spearman_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s); break;
+      case PS_TEST_CHI2: rc = ps_chi2_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], d_out[3], s); break;
+      case PS_TEST_TTEST:
+        rc = ps_group_moment_run(PS_TEST_TTEST, ma, mb, 0, cells, t_variant == 0, d_out[0], d_out[1],
+                                 d_out[2], s);
+        break;
+      case PS_TEST_ANOVA:
+        rc = ps_group_moment_run(PS_TEST_ANOVA, ma, mb, 0, cells, 1, d_out[0], d_out[1], d_out[2], s);
+        break;
+      case PS_TEST_MWU:
+        rc = ps_rank_mixed_run(PS_TEST_MWU, ma, mb, 0, cols, u_mode, d_out[0], d_out[1], d_out[2], s);
+        break;
+      case PS_TEST_KRUSKAL:
+        rc = ps_rank_mixed_run(PS_TEST_KRUSKAL, ma, mb, 0, cols, 0, d_out[0], d_out[1], d_out[2], s);
+        break;
+      default: rc = ps_fail(PS_ERR_INVALID, "unknown test");
+    }
+  }
+  if (!rc) rc = drain_errors(s);
+  for (int k = 0; k < 4 && !rc; ++k) {
+    if (outs && outs[k] && d_out[k]) {
+      cudaError_t e = cudaMemcpyAsync(outs[k], d_out[k], sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) rc = ps_cuda_check(e, "result download");
+    }
+  }
+  if (!rc && any_adj) {
+    if (ps_alloc(&d_adj, (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
+    for (int k = 0; k < 3 && !rc; ++k) {
+      if (!adj_outs[k]) continue;
+      rc = ps_adjust_run(d_out[1], rows, cols, k, homogeneous ? 1 : 0, d_adj, s);
+      if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(adj_outs[k], d_adj, sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) rc = ps_cuda_check(e, "adjusted download");
+      }
+    }
+  }
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = ps_cuda_check(e, "run");
+  }
+  for (int k = 0; k < 4; ++k) ps_free(d_out[k], s);
+  ps_free(d_adj, s);
+  ps_matrix_destroy(ma);
+  ps_matrix_destroy(mb);
+  if (rc) cudaStreamSynchronize(s);
+  return rc;
+}
+
+int ps_adjust(const double* p, int64_t rows, int64_t cols, int method, int symmetric, double* out) {
+  Guard g;
+  int rc = ensure_state();
+  if (rc) return rc;
+  cudaStream_t s = ps_state()->stream;
+  const int64_t n = rows * cols;
+  double* dp = nullptr;
+  double* dout = nullptr;
+  if (ps_alloc(&dp, (size_t)std::max<int64_t>(n, 1), s) != cudaSuccess ||
+      ps_alloc(&dout, (size_t)std::max<int64_t>(n, 1), s) != cudaSuccess)
+    return ps_fail(PS_ERR_CUDA, "out of device memory");
+  cudaError_t e = cudaMemcpyAsync(dp, p, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust upload");
+  if (!rc) rc = ps_adjust_run(dp, rows, cols, method, symmetric, dout, s);
+  if (!rc) {
+    e = cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust download");
+  }
+  cudaStreamSynchronize(s);
+  ps_free(dp, s);
+  ps_free(dout, s);
+  return rc;
+}
+
+}  // extern "C"

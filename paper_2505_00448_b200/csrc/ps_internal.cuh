@@ -1,0 +1,94 @@
+// ps_internal.cuh -- device-resident matrix handle and kernel entry points
+// shared between the per-test translation units and the C-ABI layer.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <cuda_runtime.h>
+#include "ps_common.cuh"
+
+// Device copy of one input matrix, prepared once per run (the device half of
+// the reference's make_matrix + _presort_matrix, datamodel.py:144-196,
+// engine.py:379-400).
+struct ps_matrix {
+  int kind = PS_KIND_CONTINUOUS;
+  int device = 0;
+  int64_t F = 0, S = 0;
+  int64_t ld = 0;         // row stride of d_vals (doubles), multiple of 32
+  int64_t W = 0;          // mask words per row = ceil(S/32)
+  int64_t ldc = 0;        // row stride of d_codes (bytes), multiple of 16
+  uint64_t sentinel_bits = 0;
+  int sentinel_is_nan = 1;
+  bool owns_vals = true;
+  double* d_vals = nullptr;       // F x ld raw fp64 values (zero beyond S)
+  uint32_t* d_mask = nullptr;     // F x W presence bits (bit s%32 of word s/32)
+  double* d_center = nullptr;     // F per-feature pivot (mean of present values)
+  int32_t* d_count = nullptr;     // F present counts
+  // label kinds
+  int64_t* h_cat = nullptr;       // host copy of category counts
+  int32_t* d_cat = nullptr;       // F category counts (device)
+  int cmax = 0;
+  uint8_t* d_codes = nullptr;     // F x ldc: trunc(label) or 0xFE (present, out of range) / 0xFF (missing)
+  uint32_t* d_zero = nullptr;     // F x W bits: present && value == 0.0 (ttest / mwu grouping)
+  uint32_t* d_bad = nullptr;      // F x W bits: present && label out of [0, c_f)
+  // presort tables (rank tests)
+  bool has_presort = false;
+  int32_t* d_len = nullptr;       // F present counts (== d_count)
+  uint32_t* d_order = nullptr;    // F x S: sample ids of present entries, ascending value, stable
+  uint32_t* d_gs = nullptr;       // F x S: tie-group start position of sorted position p
+  uint32_t* d_ge = nullptr;       // F x S: tie-group end position (exclusive)
+  uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
+  uint16_t* d_inv = nullptr;      // F x S: sorted position of sample s, 0xFFFF if missing (S <= 65535)
+};
+
+// Per-device library state.
+struct ps_device_state {
+  int device = -1;
+  int num_sms = 148;
+  int* d_err = nullptr;           // device error word
+  cudaStream_t stream = nullptr;  // library stream used by ps_run
+};
+
+ps_device_state* ps_state();                 // current device's state
+void ps_count_launch(int n = 1);             // kernel-launch accounting
+int ps_fail(int code, const std::string& msg);
+int ps_cuda_check(cudaError_t e, const char* what);
+
+#define PS_CUDA(call)                                              \
+  do {                                                             \
+    cudaError_t _e = (call);                                       \
+    if (_e != cudaSuccess) return ps_cuda_check(_e, #call);        \
+  } while (0)
+
+#define PS_LAUNCHED()                                                      \
+  do {                                                                     \
+    ps_count_launch();                                                     \
+    cudaError_t _e = cudaGetLastError();                                   \
+    if (_e != cudaSuccess) return ps_cuda_check(_e, "kernel launch");     \
+  } while (0)
+
+// Workspace allocation on the stream-ordered pool.
+template <typename T>
+inline cudaError_t ps_alloc(T** p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, count * sizeof(T) + 16, s);
+}
+inline void ps_free(void* p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+}
+
+// Kernel-family entry points (implemented per translation unit).
+int ps_prepare_matrix(ps_matrix* m, cudaStream_t s);
+int ps_presort_matrix(ps_matrix* m, cudaStream_t s);
+int ps_fill_nan(double* p, int64_t n, cudaStream_t s);
+int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
+                   cudaStream_t s);
+int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
+                    cudaStream_t s);
+int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi,
+                double* v, cudaStream_t s);
+int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi,
+                        int student, double* stat, double* p, double* eff, cudaStream_t s);
+int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode,
+                      double* stat, double* p, double* eff, cudaStream_t s);
+int ps_adjust_run(const double* p, int64_t rows, int64_t cols, int method, int symmetric,
+                  double* out, cudaStream_t s);
+int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s);

@@ -1,0 +1,407 @@
+// ps_pearson.cu -- all-pairs Pearson with pairwise deletion on FP64 tensor cores.
+//
+// Replaces the reference's _pearson_block -> _pearson_rows -> _pearson_finish
+// (engine.py:145-166, continuous.py:29-49, :77-103).  The two masked passes per
+// pair become one masked-moment contraction over upper-triangular 64x64 tiles
+// of features: with x' = (x - c_f) on present cells and 0 elsewhere, and m the
+// 0/1 presence,
+//     Sxy = X' X'^T,  Sx = X' M^T,  Sxx = X'^2 M^T,  Sy = M X'^T,  Syy = M X'^2^T
+// run as DMMA.8x8x4 (mma.sync m8n8k4 f64 -- the only FP64 tensor path on
+// sm_100a; tcgen05 has no f64 kind), and the pair count n = popc(m_g & m_h) on
+// the integer pipe.  Centred sums then follow from
+//     sxx = Sxx - Sx^2/n, syy = Syy - Sy^2/n, sxy = Sxy - Sx Sy/n.
+// The epilogue (r, clamp, p = 2 beta_sym_sf(|r|, n/2 - 1), r^2) is fused into
+// the same CTA.  Pairs where cancellation could flip the reference's
+// degenerate-variance decision (sxx or syy <= 1e-3 of its raw second moment,
+// or non-finite) are re-evaluated by an exact replay of the reference's
+// sequential two-pass loop, so the NaN pattern is identical.
+//
+// Algorithmic work: 10 FP64 flops per pair-sample (5 masked MACs).
+#include "ps_internal.cuh"
+#include "ps_specfun.cuh"
+#include <algorithm>
+
+namespace {
+
+constexpr int T = 64;            // features per tile edge
+constexpr int KC = 32;           // samples per k-chunk (one mask word)
+constexpr int XS = KC + 4;       // padded smem row stride (doubles): 2 wavefronts per fragment load
+constexpr int NWARP = 8;         // 4 x 2 warps, 16 x 32 pairs each
+constexpr int WM = 2, WN = 4;    // 8x8 accumulator blocks per warp (rows x cols)
+constexpr int NTHR = NWARP * 32;
+constexpr double kReplayTau = 1e-3;
+
+struct Stage {
+  double xi[T][XS];
+  double xj[T][XS];
+  uint32_t mi[T];
+  uint32_t mj[T];
+};
+constexpr int NSTAGE = 3;
+constexpr size_t kSmemBytes = NSTAGE * sizeof(Stage);
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+struct Outs {
+  double* stat;
+  double* p;
+  double* r2;
+  int2* replay;
+  int* replay_count;
+  int replay_cap;
+  int* err;
+};
+
+__device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
+  if (o) {
+    o[g * F + h] = v;
+    o[h * F + g] = v;
+  }
+}
+
+// Moments -> outputs for one upper-triangular pair (g <= h).
+__device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx, double sy,
+                               double qx, double qy, double xy, const Outs& o) {
+  double r = PS_NAN, p = PS_NAN;
+  if (n > 1) {
+    const double fn = (double)n;
+    const bool diag = g == h;
+    const double sxx = qx - sx * sx / fn;
+    const double syy = diag ? sxx : qy - sy * sy / fn;
+    if (!(sxx > kReplayTau * qx) || !(syy > kReplayTau * (diag ? qx : qy))) {
+      int slot = atomicAdd(o.replay_count, 1);
+      if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
+      return;  // the replay kernel writes this pair
+    }
+    const double sxy = diag ? sxx : xy - sx * sy / fn;
+    r = sxy / sqrt(sxx * syy);
+    if (r > 1.0) r = 1.0;
+    else if (r < -1.0) r = -1.0;
+    if (n != 2) {
+      p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, o.err);
+      if (p > 1.0) p = 1.0;
+    }
+  }
+  put(o.stat, F, g, h, r);
+  put(o.p, F, g, h, p);
+  put(o.r2, F, g, h, r * r);
+}
+
+// grid.x = tiles in range x nsplit.  Each CTA accumulates one 64x64 tile over
+// its share of the k-chunks.
+__global__ void __launch_bounds__(NTHR, 1)
+pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
+                    int64_t W, const double* __restrict__ center, int64_t F, int64_t NT,
+                    int64_t tile0, int64_t lo, int64_t hi, int nsplit, int64_t chunks_per_split,
+                    Outs o, double* __restrict__ ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Stage* st = reinterpret_cast<Stage*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = warp >> 1, wj = warp & 1;
+  const int64_t tile = tile0 + blockIdx.x / nsplit;
+  const int split = blockIdx.x % nsplit;
+  int64_t I, J;
+  ps_tri_tile(tile, NT, &I, &J);
+  const int64_t row0 = I * T, col0 = J * T;
+  const int64_t c_begin = (int64_t)split * chunks_per_split;
+  const int64_t c_end = min(W, c_begin + chunks_per_split);
+
+  // per-lane fragment rows/cols and their pivots
+  const int fr = lane >> 2, fk = lane & 3;
+  double ci[WM], cj[WN];
+#pragma unroll
+  for (int q = 0; q < WM; ++q) {
+    const int64_t gr = row0 + wi * 8 * WM + q * 8 + fr;
+    ci[q] = gr < F ? center[gr] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < WN; ++q) {
+    const int64_t gc = col0 + wj * 8 * WN + q * 8 + fr;
+    cj[q] = gc < F ? center[gc] : 0.0;
+  }
+
+  double axy[WM][WN][2], asx[WM][WN][2], asxx[WM][WN][2], asy[WM][WN][2], asyy[WM][WN][2];
+  int an[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        axy[i][j][e] = asx[i][j][e] = asxx[i][j][e] = asy[i][j][e] = asyy[i][j][e] = 0.0;
+        an[i][j][e] = 0;
+      }
+
+  // global -> shared via cp.async (no register staging), NSTAGE-deep ring
+  constexpr int LQ = (T * KC / 2) / NTHR;  // 16-byte copies per thread per operand tile
+  auto issue = [&](int64_t c, Stage& sd) {
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) {
+      const int idx = tid + q * NTHR;
+      const int r = idx >> 4, c2 = idx & 15;
+      const int64_t gi = min(row0 + r, F - 1), gj = min(col0 + r, F - 1);
+      const int64_t off = c * KC + c2 * 2;
+      const unsigned si = (unsigned)__cvta_generic_to_shared(&sd.xi[r][c2 * 2]);
+      const unsigned sj = (unsigned)__cvta_generic_to_shared(&sd.xj[r][c2 * 2]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(si), "l"(vals + gi * ld + off));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sj), "l"(vals + gj * ld + off));
+    }
+    if (tid < 2 * T) {
+      const int64_t gr = (tid < T ? row0 : col0) + (tid & (T - 1));
+      // rows past F get an all-zero mask, so their (clamped) values never count
+      const uint32_t w = gr < F ? mask[gr * W + c] : 0u;
+      if (tid < T) sd.mi[tid] = w;
+      else sd.mj[tid - T] = w;
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+
+  for (int q = 0; q < NSTAGE - 1; ++q) {
+    if (c_begin + q < c_end) issue(c_begin + q, st[q]);
+    else asm volatile("cp.async.commit_group;");
+  }
+  for (int64_t c = c_begin; c < c_end; ++c) {
+    const int cur = (int)((c - c_begin) % NSTAGE);
+    asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2));
+    __syncthreads();
+    {
+      const int64_t cn = c + NSTAGE - 1;
+      if (cn < c_end) issue(cn, st[(int)((cn - c_begin) % NSTAGE)]);
+      else asm volatile("cp.async.commit_group;");
+    }
+    const Stage& s = st[cur];
+    uint32_t mrow[WM], mcol[WN];
+#pragma unroll
+    for (int q = 0; q < WM; ++q) mrow[q] = s.mi[wi * 8 * WM + q * 8 + fr];
+#pragma unroll
+    for (int q = 0; q < WN; ++q) mcol[q] = s.mj[wj * 8 * WN + q * 8 + fr];
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int k = kk * 4 + fk;
+      double xa[WM], ma[WM], xa2[WM], xb[WN], mb[WN], xb2[WN];
+#pragma unroll
+      for (int q = 0; q < WM; ++q) {
+        const bool pa = (mrow[q] >> k) & 1u;
+        const double va = s.xi[wi * 8 * WM + q * 8 + fr][k];
+        xa[q] = pa ? va - ci[q] : 0.0;
+        ma[q] = pa ? 1.0 : 0.0;
+        xa2[q] = xa[q] * xa[q];
+      }
+#pragma unroll
+      for (int q = 0; q < WN; ++q) {
+        const bool pb = (mcol[q] >> k) & 1u;
+        const double vb = s.xj[wj * 8 * WN + q * 8 + fr][k];
+        xb[q] = pb ? vb - cj[q] : 0.0;
+        mb[q] = pb ? 1.0 : 0.0;
+        xb2[q] = xb[q] * xb[q];
+      }
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) {
+          dmma(axy[i][j][0], axy[i][j][1], xa[i], xb[j]);
+          dmma(asx[i][j][0], asx[i][j][1], xa[i], mb[j]);
+          dmma(asxx[i][j][0], asxx[i][j][1], xa2[i], mb[j]);
+          dmma(asy[i][j][0], asy[i][j][1], ma[i], xb[j]);
+          dmma(asyy[i][j][0], asyy[i][j][1], ma[i], xb2[j]);
+        }
+    }
+    // pair counts for the lane's accumulator positions (integer pipe)
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      const uint32_t a = mrow[i];
+#pragma unroll
+      for (int j = 0; j < WN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) an[i][j][e] += __popc(a & s.mj[wj * 8 * WN + j * 8 + 2 * fk + e]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+
+  if (nsplit > 1) {
+    // partial moments -> workspace [tile-in-range][split][6][T][T]
+    double* w = ws + ((blockIdx.x / nsplit) * (int64_t)nsplit + split) * 6 * T * T;
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int j = 0; j < WN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = wi * 8 * WM + i * 8 + fr, cc = wj * 8 * WN + j * 8 + 2 * fk + e;
+          const int o2 = r * T + cc;
+          w[0 * T * T + o2] = (double)an[i][j][e];
+          w[1 * T * T + o2] = asx[i][j][e];
+          w[2 * T * T + o2] = asy[i][j][e];
+          w[3 * T * T + o2] = asxx[i][j][e];
+          w[4 * T * T + o2] = asyy[i][j][e];
+          w[5 * T * T + o2] = axy[i][j][e];
+        }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t g = row0 + wi * 8 * WM + i * 8 + fr;
+        const int64_t h = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
+        if (g < lo || g >= hi || h < g || h >= F) continue;
+        pearson_finish(g, h, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e],
+                       asyy[i][j][e], axy[i][j][e], o);
+      }
+}
+
+// Split-K reduction (fixed split order => deterministic) + epilogue.
+__global__ void pearson_splitk_finish_kernel(const double* __restrict__ ws, int64_t F, int64_t NT,
+                                             int64_t tile0, int64_t ntiles, int nsplit, int64_t lo,
+                                             int64_t hi, Outs o) {
+  const int64_t total = ntiles * T * T;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tl = idx / (T * T);
+    const int rc = (int)(idx % (T * T));
+    int64_t I, J;
+    ps_tri_tile(tile0 + tl, NT, &I, &J);
+    const int64_t g = I * T + rc / T, h = J * T + rc % T;
+    if (g < lo || g >= hi || h < g || h >= F) continue;
+    double m[6] = {0, 0, 0, 0, 0, 0};
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const double* w = ws + (tl * nsplit + sp) * 6 * T * T + rc;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) m[q] += w[q * T * T];
+    }
+    pearson_finish(g, h, F, (int)m[0], m[1], m[2], m[3], m[4], m[5], o);
+  }
+}
+
+// Exact replay of the reference's sequential two-pass loop (continuous.py:77-103)
+// for pairs the fast path could not decide.  One thread per pair.
+__global__ void pearson_replay_kernel(const double* __restrict__ vals, int64_t ld,
+                                      const uint32_t* __restrict__ mask, int64_t W, int64_t S,
+                                      int64_t F, const int2* __restrict__ list,
+                                      const int* __restrict__ count_ptr, int cap, int64_t lo,
+                                      int64_t hi, Outs o) {
+  // The list length is only known on the device; an overflowing list falls
+  // back to re-deciding every pair in range (pathological inputs only).
+  const int count = *count_ptr;
+  if (count == 0) return;
+  const int all_pairs = count > cap;
+  const int64_t n_items = all_pairs ? (hi - lo) * F : count;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < n_items;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g, h;
+    if (all_pairs) {
+      g = lo + it / F;
+      h = it % F;
+      if (h < g) continue;
+    } else {
+      g = list[it].x;
+      h = list[it].y;
+    }
+    const double* xg = vals + g * ld;
+    const double* xh = vals + h * ld;
+    const uint32_t* mg = mask + g * W;
+    const uint32_t* mh = mask + h * W;
+    int64_t n = 0;
+    double sum_x = 0.0, sum_y = 0.0;
+    for (int64_t s = 0; s < S; ++s) {
+      if ((mg[s >> 5] & mh[s >> 5]) >> (s & 31) & 1u) {
+        ++n;
+        sum_x += xg[s];
+        sum_y += xh[s];
+      }
+    }
+    double r = PS_NAN, p = PS_NAN;
+    if (n > 1) {
+      const double mx = sum_x / (double)n, my = sum_y / (double)n;
+      double sxx = 0.0, syy = 0.0, sxy = 0.0;
+      for (int64_t s = 0; s < S; ++s) {
+        if ((mg[s >> 5] & mh[s >> 5]) >> (s & 31) & 1u) {
+          const double dx = xg[s] - mx, dy = xh[s] - my;
+          sxx += dx * dx;
+          syy += dy * dy;
+          sxy += dx * dy;
+        }
+      }
+      if (sxx > 0.0 && syy > 0.0) {
+        r = sxy / sqrt(sxx * syy);
+        if (r > 1.0) r = 1.0;
+        else if (r < -1.0) r = -1.0;
+        if (n != 2) {
+          p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * (double)n - 1.0, o.err);
+          if (p > 1.0) p = 1.0;
+        }
+      }
+    }
+    put(o.stat, F, g, h, r);
+    put(o.p, F, g, h, p);
+    put(o.r2, F, g, h, r * r);
+  }
+}
+
+}  // namespace
+
+int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
+                   cudaStream_t s) {
+  const int64_t F = a->F;
+  lo = std::max<int64_t>(0, lo);
+  hi = std::min<int64_t>(F, hi);
+  if (hi <= lo || (!stat && !p && !r2)) return PS_OK;
+  ps_device_state* ds = ps_state();
+  const int64_t NT = ps_ceil_div(F, T);
+  const int64_t I0 = lo / T, I1 = (hi - 1) / T;
+  const int64_t tile0 = ps_tri_offset(I0, NT);
+  const int64_t ntiles = ps_tri_offset(I1 + 1, NT) - tile0;
+  const int64_t W = a->W;
+  // split-K so that small problems still fill the machine (>= 2 CTAs per SM)
+  int nsplit = 1;
+  const int64_t want = 2LL * ds->num_sms;
+  if (ntiles < want) {
+    nsplit = (int)std::min<int64_t>(ps_ceil_div(want, ntiles), std::max<int64_t>(1, W / 4));
+    nsplit = std::max(1, nsplit);
+  }
+  const int64_t cps = ps_ceil_div(W, nsplit);
+  nsplit = (int)ps_ceil_div(W, cps);
+
+  const int64_t npairs = (hi - lo) * F;  // upper bound on pairs touched
+  const int cap = (int)std::min<int64_t>(npairs, 1 << 22);
+  Outs o{stat, p, r2, nullptr, nullptr, cap, ds->d_err};
+  double* ws = nullptr;
+  PS_CUDA(ps_alloc(&o.replay, (size_t)cap, s));
+  PS_CUDA(ps_alloc(&o.replay_count, 1, s));
+  PS_CUDA(cudaMemsetAsync(o.replay_count, 0, sizeof(int), s));
+  if (nsplit > 1) PS_CUDA(ps_alloc(&ws, (size_t)(ntiles * nsplit * 6 * T * T), s));
+
+  static bool attr_set = false;
+  if (!attr_set) {
+    PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmemBytes));
+    attr_set = true;
+  }
+  const int64_t grid = ntiles * nsplit;
+  pearson_tile_kernel<<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
+      a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws);
+  PS_LAUNCHED();
+  if (nsplit > 1) {
+    const int64_t total = ntiles * T * T;
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 256), (int64_t)ds->num_sms * 8);
+    pearson_splitk_finish_kernel<<<blocks, 256, 0, s>>>(ws, F, NT, tile0, ntiles, nsplit, lo, hi,
+                                                        o);
+    PS_LAUNCHED();
+  }
+  {
+    const int blocks = ds->num_sms * 4;
+    pearson_replay_kernel<<<blocks, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, W, a->S, F, o.replay,
+                                                o.replay_count, cap, lo, hi, o);
+    PS_LAUNCHED();
+  }
+  ps_free(o.replay, s);
+  ps_free(o.replay_count, s);
+  ps_free(ws, s);
+  return PS_OK;
+}

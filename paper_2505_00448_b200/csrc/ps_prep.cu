@@ -1,0 +1,118 @@
+// ps_prep.cu -- one pass over each input matrix on the device: packed validity
+// mask (reference present_mask, datamodel.py:86-104), per-feature present
+// count and pivot (mean of present values, used to centre the moment
+// contractions), and for label kinds the uint8 label codes the contingency /
+// group kernels consume.  HBM-bound: reads 8 B/cell once, writes 1/8 B/cell
+// of mask (+1 B/cell of codes for labels).
+#include "ps_internal.cuh"
+#include <math_constants.h>
+#include <algorithm>
+#include <limits>
+
+namespace {
+
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads)
+prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t W,
+                 uint64_t sent_bits, int sent_nan, uint32_t* __restrict__ mask,
+                 double* __restrict__ center, int32_t* __restrict__ count,
+                 // label outputs (nullptr for continuous)
+                 const int32_t* __restrict__ cat, uint8_t* __restrict__ codes, int64_t ldc,
+                 uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits) {
+  const int64_t f = blockIdx.x;
+  const double* row = vals + f * ld;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cf = cat ? cat[f] : 0;
+  double sum = 0.0;
+  int cnt = 0;
+  for (int64_t base = (int64_t)warp * 32; base < S; base += (int64_t)kPrepThreads) {
+    const int64_t s = base + lane;
+    double v = 0.0;
+    bool pres = false;
+    if (s < S) {
+      v = row[s];
+      pres = ps_is_present(v, sent_bits, sent_nan);
+    }
+    const uint32_t word = __ballot_sync(PS_FULL, pres);
+    if (pres) { sum += v; }
+    cnt += pres ? 1 : 0;
+    if (codes) {
+      uint8_t code = 0xFF;
+      bool bad = false;
+      if (pres) {
+        // int(label) in the reference truncates toward zero (categorical.py:87).
+        if (v != v || v <= -1.0 || v >= (double)cf) {
+          bad = true;
+        } else {
+          code = (uint8_t)(int)trunc(v);
+        }
+        if (bad) code = 0xFE;
+      }
+      if (s < S) codes[f * ldc + s] = code;
+      const uint32_t zw = __ballot_sync(PS_FULL, pres && v == 0.0);
+      const uint32_t bw = __ballot_sync(PS_FULL, bad);
+      if (lane == 0) {
+        zero_bits[f * W + (base >> 5)] = zw;
+        bad_bits[f * W + (base >> 5)] = bw;
+      }
+    }
+    if (lane == 0) mask[f * W + (base >> 5)] = word;
+  }
+  // block reduction of (sum, cnt); order is fixed, so the pivot is reproducible.
+  __shared__ double ssum[kPrepThreads / 32];
+  __shared__ int scnt[kPrepThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(PS_FULL, sum, o);
+    cnt += __shfl_xor_sync(PS_FULL, cnt, o);
+  }
+  if (lane == 0) { ssum[warp] = sum; scnt[warp] = cnt; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    int c = 0;
+    for (int w = 0; w < kPrepThreads / 32; ++w) { t += ssum[w]; c += scnt[w]; }
+    count[f] = c;
+    // pivot: any finite value works for centring; use the mean when finite.
+    double piv = c > 0 ? t / (double)c : 0.0;
+    if (!isfinite(piv)) piv = 0.0;
+    center[f] = piv;
+  }
+}
+
+__global__ void fill_kernel(double* __restrict__ p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace
+
+int ps_fill_nan(double* p, int64_t n, cudaStream_t s) {
+  if (!p || n <= 0) return PS_OK;
+  int blocks = (int)std::min<int64_t>(ps_ceil_div(n, 256), (int64_t)ps_state()->num_sms * 16);
+  fill_kernel<<<blocks, 256, 0, s>>>(p, n, std::numeric_limits<double>::quiet_NaN());
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_prepare_matrix(ps_matrix* m, cudaStream_t s) {
+  PS_CUDA(ps_alloc(&m->d_mask, (size_t)(m->F * m->W), s));
+  PS_CUDA(ps_alloc(&m->d_center, (size_t)m->F, s));
+  PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
+  const bool labels = m->kind != PS_KIND_CONTINUOUS;
+  if (labels) {
+    m->ldc = ps_round_up(m->S, 16);
+    PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
+    PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
+    PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));
+  }
+  if (m->F > 0) {
+    prep_rows_kernel<<<(unsigned)m->F, kPrepThreads, 0, s>>>(
+        m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask,
+        m->d_center, m->d_count, labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero,
+        m->d_bad);
+    PS_LAUNCHED();
+  }
+  return PS_OK;
+}

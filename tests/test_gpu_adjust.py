@@ -1,0 +1,54 @@
+"""Device BH / BY / Bonferroni vs the restated reference adjust (adjust.py:23-87).
+
+Given the same p matrix the device result is bit-identical (survey Appendix B).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal
+
+pytestmark = pytest.mark.gpu
+
+import paper_2505_00448_b200 as ps
+
+
+@pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
+def test_adjust_vector_families(oracle, method):
+    rng = np.random.default_rng(55)
+    for size in [1, 2, 3, 7, 100, 1000, 4097, 20000, 200001]:
+        v = rng.random(size)
+        ties = rng.random(size) < 0.3
+        v[ties] = np.round(v[ties], 1)
+        v[rng.random(size) < 0.1] = np.nan
+        got = ps.adjust(v.reshape(1, -1), method, symmetric=False).ravel()
+        want = oracle.adjust_family(v, method)
+        assert bitwise_equal(got, want), (method, size)
+
+
+@pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
+def test_adjust_symmetric(oracle, method):
+    rng = np.random.default_rng(7)
+    n = 301
+    up = rng.random(n * (n - 1) // 2) ** 3
+    up[rng.random(up.size) < 0.1] = np.nan
+    m = np.zeros((n, n))
+    r, c = np.triu_indices(n, 1)
+    m[r, c] = up
+    m[c, r] = up
+    np.fill_diagonal(m, 0.0)
+    got = ps.adjust(m, method, symmetric=True)
+    want = oracle.adjust(m, method, symmetric=True)
+    assert bitwise_equal(got, want)
+    assert np.isnan(np.diag(got)).all()
+
+
+def test_adjust_all_nan_and_errors():
+    m = np.full((4, 4), np.nan)
+    assert np.isnan(ps.adjust(m, "bh", symmetric=True)).all()
+    with pytest.raises(ps.UnknownMethod, match="holm"):
+        ps.adjust(m, "holm", symmetric=True)
+    with pytest.raises(ps.NonSquareSymmetric, match="square"):
+        ps.adjust(np.zeros((2, 3)), "bh", symmetric=True)
