@@ -1,0 +1,271 @@
+// ps_presort.cu -- per-feature stable sort of the present values.
+//
+// Replaces _presort_matrix -> _presort_block -> _presort (engine.py:379-400,
+// :133-142; ranking.py:30-53: stable mergesort of the present entries).  One
+// CTA per feature runs an LSD radix sort over order-preserving 64-bit keys in
+// global scratch (8-bit digits, passes whose digit is constant are skipped).
+// Keys are canonicalised so that the sort agrees with numpy's: -0.0 and +0.0
+// compare equal (and keep sample order), NaN (present under a numeric
+// sentinel) sorts after +inf.  Initial order = sample order and every pass is
+// stable, so ties keep ascending sample order exactly like the reference.
+//
+// Outputs per feature f (present count n_f):
+//   order[f][p]  sample id of sorted position p (p < n_f)
+//   inv[f][s]    sorted position of sample s, 0xFFFF when s is missing
+//   gs/ge[f][p]  [start, end) of the tie group of position p, where ties are
+//                float '==' runs (ranking.py:56-89): NaN never ties
+//   tied[f]      1 if some tie group has more than one member
+#include "ps_internal.cuh"
+#include <algorithm>
+
+namespace {
+
+constexpr int NT = 512;
+constexpr int NW = NT / 32;
+constexpr int ITEMS = 4;                 // rounds of 32 per warp per tile
+constexpr int TILE = NT * ITEMS;         // 2048 keys per tile
+constexpr int PER_WARP = TILE / NW;      // 128 contiguous keys per warp
+
+__device__ __forceinline__ uint64_t sort_key(double v) {
+  uint64_t b = (uint64_t)__double_as_longlong(v);
+  if (v != v) b = 0x7ff8000000000000ull;       // canonical NaN, sorts last
+  if ((b << 1) == 0) b = 0;                    // -0.0 ties with +0.0
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ bool key_is_nan(uint64_t k) {
+  // canonical NaN key: 0x7ff8... | sign flip
+  return k == (0x7ff8000000000000ull | 0x8000000000000000ull);
+}
+
+// Block-wide exclusive scan of one int per thread; returns the block total.
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_buf, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(PS_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_buf[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < NW ? warp_buf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(PS_FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NW) warp_buf[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  const int before = warp > 0 ? warp_buf[warp - 1] : 0;
+  total = warp_buf[NW - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+__global__ void __launch_bounds__(NT)
+presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
+               int64_t W, int64_t S, uint64_t* __restrict__ keyA, uint32_t* __restrict__ idxA,
+               uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, uint32_t* __restrict__ order,
+               uint16_t* __restrict__ inv, uint32_t* __restrict__ gs, uint32_t* __restrict__ ge,
+               uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
+  __shared__ int warp_buf[NW];
+  __shared__ uint32_t hist[8][256];
+  __shared__ uint32_t wcnt[NW][256];
+  __shared__ uint32_t bucket[256];
+  __shared__ int s_any_tie;
+  const int64_t f = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* row = vals + f * ld;
+  const uint32_t* mrow = mask + f * W;
+  uint64_t* kA = keyA + f * S;
+  uint32_t* iA = idxA + f * S;
+  uint64_t* kB = keyB + f * S;
+  uint32_t* iB = idxB + f * S;
+
+  for (int i = threadIdx.x; i < 8 * 256; i += NT) (&hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_any_tie = 0;
+  __syncthreads();
+
+  // 1. stable compaction of the present entries (sample order) + digit histograms
+  int n = 0;
+  for (int64_t base = 0; base < S; base += NT) {
+    const int64_t s = base + threadIdx.x;
+    const bool pres = s < S && ((mrow[s >> 5] >> (s & 31)) & 1u);
+    int tot;
+    const int pos = block_excl_scan(pres ? 1 : 0, warp_buf, tot);
+    if (pres) {
+      const uint64_t k = sort_key(row[s]);
+      kA[n + pos] = k;
+      iA[n + pos] = (uint32_t)s;
+#pragma unroll
+      for (int d = 0; d < 8; ++d) atomicAdd(&hist[d][(k >> (8 * d)) & 0xff], 1u);
+    }
+    n += tot;
+  }
+  __syncthreads();
+
+  // 2. LSD passes (stable), skipping constant digits
+  for (int d = 0; d < 8; ++d) {
+    bool trivial = false;
+    for (int b = 0; b < 256; ++b)
+      if (hist[d][b] == (uint32_t)n) trivial = true;
+    if (trivial || n <= 1) continue;
+    const int shift = 8 * d;
+    // bucket starts: exclusive scan of hist[d] by warp 0
+    if (warp == 0) {
+      uint32_t run = 0;
+      for (int b0 = 0; b0 < 256; b0 += 32) {
+        uint32_t v = hist[d][b0 + lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
+          if (lane >= o) x += y;
+        }
+        bucket[b0 + lane] = run + x - v;
+        run += __shfl_sync(PS_FULL, x, 31);
+      }
+    }
+    __syncthreads();
+    for (int t0 = 0; t0 < n; t0 += TILE) {
+      for (int i = threadIdx.x; i < NW * 256; i += NT) (&wcnt[0][0])[i] = 0;
+      __syncthreads();
+      const int w0 = t0 + warp * PER_WARP;
+      for (int r = 0; r < PER_WARP; r += 32) {
+        const int i = w0 + r + lane;
+        const bool ok = i < n;
+        const uint32_t dg = ok ? (uint32_t)((kA[i] >> shift) & 0xff) : 0u;
+        const uint32_t peers = __match_any_sync(PS_FULL, ok ? dg : 0xffffffffu);
+        if (ok && (peers & lanemask_lt()) == 0) wcnt[warp][dg] += __popc(peers);
+      }
+      __syncthreads();
+      if (threadIdx.x < 256) {
+        const int b = threadIdx.x;
+        uint32_t run = bucket[b];
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t c = wcnt[w][b];
+          wcnt[w][b] = run;
+          run += c;
+        }
+        bucket[b] = run;
+      }
+      __syncthreads();
+      for (int r = 0; r < PER_WARP; r += 32) {
+        const int i = w0 + r + lane;
+        const bool ok = i < n;
+        uint64_t k = 0;
+        uint32_t v = 0, dg = 0;
+        if (ok) {
+          k = kA[i];
+          v = iA[i];
+          dg = (uint32_t)((k >> shift) & 0xff);
+        }
+        const uint32_t peers = __match_any_sync(PS_FULL, ok ? dg : 0xffffffffu);
+        uint32_t start = ok ? wcnt[warp][dg] : 0u;
+        __syncwarp();
+        if (ok) {
+          const uint32_t pos = start + __popc(peers & lanemask_lt());
+          kB[pos] = k;
+          iB[pos] = v;
+          if ((peers >> lane) == 1u) wcnt[warp][dg] = start + __popc(peers);
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    // swap A <-> B
+    uint64_t* tk = kA; kA = kB; kB = tk;
+    uint32_t* ti = iA; iA = iB; iB = ti;
+    __syncthreads();
+  }
+
+  // 3. outputs: order, inverse permutation, tie groups
+  uint32_t* ord = order + f * S;
+  uint16_t* iv = inv + f * S;
+  for (int64_t s = threadIdx.x; s < S; s += NT) iv[s] = 0xFFFF;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += NT) {
+    const uint32_t s = iA[p];
+    ord[p] = s;
+    iv[s] = (uint16_t)p;
+  }
+  // gs: inclusive max-scan of (boundary ? p : 0); ge: next boundary (or n)
+  uint32_t* gsr = gs + f * S;
+  uint32_t* ger = ge + f * S;
+  int carry_gs = 0;
+  for (int base = 0; base < n; base += NT) {
+    const int p = base + threadIdx.x;
+    bool bnd = false;
+    if (p < n) {
+      bnd = p == 0 || kA[p] != kA[p - 1] || key_is_nan(kA[p]);
+      if (!bnd) s_any_tie = 1;
+    }
+    int x = (p < n && bnd) ? p : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(PS_FULL, x, o);
+      if (lane >= o) x = max(x, y);
+    }
+    if (lane == 31) warp_buf[warp] = x;
+    __syncthreads();
+    int pre = carry_gs;
+    for (int w = 0; w < warp; ++w) pre = max(pre, warp_buf[w]);
+    x = max(x, pre);
+    if (p < n) gsr[p] = (uint32_t)x;
+    int last = carry_gs;
+    for (int w = 0; w < NW; ++w) last = max(last, warp_buf[w]);
+    __syncthreads();
+    carry_gs = last;
+  }
+  __syncthreads();
+  // ge[p] = gs of the first position after p's group: walk groups by start
+  for (int p = threadIdx.x; p < n; p += NT) {
+    // group end: the next boundary after p; boundaries are where gs[q] == q
+    // (scan forward; groups are short in the common case, long runs are
+    // handled by the per-group owner below)
+    if ((int)gsr[p] == p) {
+      int q = p + 1;
+      while (q < n && (int)gsr[q] != q) ++q;
+      for (int t = p; t < q; ++t) ger[t] = (uint32_t)q;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tied[f] = s_any_tie ? 1 : 0;
+    lens[f] = n;
+  }
+}
+
+}  // namespace
+
+int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
+  if (m->has_presort) return PS_OK;
+  if (m->S > 65535)
+    return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
+  const int64_t FS = m->F * m->S;
+  uint64_t *kA = nullptr, *kB = nullptr;
+  uint32_t *iA = nullptr, *iB = nullptr;
+  PS_CUDA(ps_alloc(&kA, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&kB, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&iA, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&iB, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_order, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_inv, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_gs, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_ge, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
+  PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
+  presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,
+                                               m->d_order, m->d_inv, m->d_gs, m->d_ge, m->d_tied,
+                                               m->d_len);
+  PS_LAUNCHED();
+  ps_free(kA, s);
+  ps_free(kB, s);
+  ps_free(iA, s);
+  ps_free(iB, s);
+  // host copy of the tie flags steers kernel specialisation
+  m->has_presort = true;
+  return PS_OK;
+}

@@ -41,7 +41,7 @@ __device__ __forceinline__ double ln_gamma(double x, int* err) {
   return lanczos_lg(x);
 }
 
-__device__ __noinline__ double beta_cf(double a, double b, double x, int* err) {
+static __device__ __noinline__ double beta_cf(double a, double b, double x, int* err) {
   const double tiny = 1e-300, eps = 1e-15;
   const double qab = a + b, qap = a + 1.0, qam = a - 1.0;
   double c = 1.0;
@@ -84,7 +84,7 @@ __device__ __forceinline__ double reg_inc_beta(double x, double a, double b, int
   return 1.0 - front * beta_cf(b, a, 1.0 - x, err) / b;
 }
 
-__device__ __noinline__ double reg_inc_gamma_upper(double a, double x, int* err) {
+static __device__ __noinline__ double reg_inc_gamma_upper(double a, double x, int* err) {
   const double tiny = 1e-300, eps = 1e-15;
   if (a <= 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
   if (x < 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
