@@ -161,6 +161,12 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
 int64_t ps_kernel_launches(void);
 void ps_reset_kernel_launches(void);
 
+/* Kernel-level timing: when enabled, the dominant kernel of each block call
+ * ("pearson_tile", "spearman_walk", "chi2_gemm", "group_gemm", "rank_mixed_walk")
+ * is bracketed by CUDA events on its launch stream.  collect() sums them. */
+void ps_profile_enable(int on);
+int ps_profile_collect(const char* name, double* total_ms, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

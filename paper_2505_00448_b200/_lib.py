@@ -57,6 +57,8 @@ EXPORTED = (
     "ps_run",
     "ps_kernel_launches",
     "ps_reset_kernel_launches",
+    "ps_profile_enable",
+    "ps_profile_collect",
 )
 
 
@@ -116,6 +118,16 @@ def _declare(lib: ctypes.CDLL) -> None:
         ctypes.POINTER(ctypes.c_void_p),
     ]
     lib.ps_kernel_launches.restype = ctypes.c_int64
+    lib.ps_profile_enable.argtypes = [i32]
+    lib.ps_profile_collect.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_int64)]
+
+
+def profile_collect(name: str) -> tuple[float, int]:
+    ms = ctypes.c_double(0.0)
+    cnt = ctypes.c_int64(0)
+    load().ps_profile_collect(name.encode(), ctypes.byref(ms), ctypes.byref(cnt))
+    return ms.value, cnt.value
 
 
 def load() -> ctypes.CDLL:

@@ -71,7 +71,31 @@ int drain_errors(cudaStream_t s) {
   return PS_OK;
 }
 
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+bool g_prof = false;
+std::vector<ProfRec> g_prof_recs;
+ProfRec* g_prof_open = nullptr;
+
 }  // namespace
+
+void ps_prof_begin(const char* name, cudaStream_t s) {
+  if (!g_prof) return;
+  ProfRec r;
+  r.name = name;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+  g_prof_recs.push_back(r);
+  g_prof_open = &g_prof_recs.back();
+}
+void ps_prof_end(cudaStream_t s) {
+  if (!g_prof || !g_prof_open) return;
+  cudaEventRecord(g_prof_open->b, s);
+  g_prof_open = nullptr;
+}
 
 ps_device_state* ps_state() { return &g_states[current_device()]; }
 void ps_count_launch(int n) { g_launches += n; }
@@ -90,6 +114,38 @@ const char* ps_version(void) { return "paper_2505_00448_b200 0.1.0 (sm_100a)"; }
 const char* ps_last_error(void) { return g_last_error.c_str(); }
 int64_t ps_kernel_launches(void) { return g_launches.load(); }
 void ps_reset_kernel_launches(void) { g_launches = 0; }
+
+void ps_profile_enable(int on) {
+  Guard g;
+  g_prof = on != 0;
+}
+
+// Sum of event-timed milliseconds and launch count of kernel `name` since the
+// last collect (synchronises on the recorded events); clears the records.
+int ps_profile_collect(const char* name, double* total_ms, int64_t* count) {
+  Guard g;
+  double t = 0.0;
+  int64_t c = 0;
+  std::vector<ProfRec> keep;
+  for (auto& r : g_prof_recs) {
+    if (r.name == name) {
+      cudaEventSynchronize(r.b);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, r.a, r.b);
+      t += ms;
+      ++c;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    } else {
+      keep.push_back(r);
+    }
+  }
+  g_prof_recs.swap(keep);
+  g_prof_open = nullptr;
+  *total_ms = t;
+  *count = c;
+  return PS_OK;
+}
 
 int ps_device_count(int* count) {
   int n = 0;

@@ -66,6 +66,11 @@ int ps_cuda_check(cudaError_t e, const char* what);
     if (_e != cudaSuccess) return ps_cuda_check(_e, "kernel launch");     \
   } while (0)
 
+// Kernel-level profiling: when enabled, the dominant kernel of each test
+// records CUDA events on its launch stream (bench.py reads them back).
+void ps_prof_begin(const char* name, cudaStream_t s);
+void ps_prof_end(cudaStream_t s);
+
 // Workspace allocation on the stream-ordered pool.
 template <typename T>
 inline cudaError_t ps_alloc(T** p, size_t count, cudaStream_t s) {

@@ -384,8 +384,10 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     attr_set = true;
   }
   const int64_t grid = ntiles * nsplit;
+  ps_prof_begin("pearson_tile", s);
   pearson_tile_kernel<<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
       a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws);
+  ps_prof_end(s);
   PS_LAUNCHED();
   if (nsplit > 1) {
     const int64_t total = ntiles * T * T;

@@ -333,8 +333,10 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   PS_CUDA(ps_alloc(&ps.sxy4, (size_t)(F * F), s));
   PS_CUDA(ps_alloc(&queue, 1, s));
   PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+  ps_prof_begin("spearman_walk", s);
   spearman_walk_kernel<<<grid, STH, smem, s>>>(a->d_order, a->d_inv, a->d_gs, a->d_ge, a->d_tied,
                                               a->d_len, S, F, lo, hi, queue, ps);
+  ps_prof_end(s);
   PS_LAUNCHED();
   const int64_t total = (hi - lo) * F;
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
