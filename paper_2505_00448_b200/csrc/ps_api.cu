@@ -253,10 +253,12 @@ int ps_matrix_destroy(ps_matrix* m) {
   ps_free(m->d_zero, s);
   ps_free(m->d_bad, s);
   ps_free(m->d_order, s);
-  ps_free(m->d_gs, s);
-  ps_free(m->d_ge, s);
-  ps_free(m->d_tied, s);
   ps_free(m->d_inv, s);
+  ps_free(m->d_tb, s);
+  ps_free(m->d_lastb, s);
+  ps_free(m->d_nextb, s);
+  ps_free(m->d_tied, s);
+  ps_free(m->d_len, s);
   delete[] m->h_cat;
   delete m;
   return PS_OK;

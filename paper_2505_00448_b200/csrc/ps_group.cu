@@ -1,0 +1,560 @@
+// ps_group.cu -- ANOVA and t-test: per-level moments as one FP64 tensor-core
+// contraction of label one-hots against the continuous matrix.
+//
+// Replaces _anova_block -> _anova_rows -> _anova_finish and _ttest_block ->
+// _ttest_rows -> _ttest_finish (engine.py:245-293; mixed.py:121-202,
+// :453-520).  For label row j of feature g (level j; for the t-test the two
+// rows are "label == 0" and "label != 0", mixed.py:192-201) and continuous
+// feature h, over jointly present samples:
+//     n_j = popc(onehot_gj & m_h),  S_j = sum x'_h,  Q_j = sum x'_h^2
+// with x' = x - c_h (per-feature pivot) on present cells, 0 elsewhere.  S and
+// Q are DMMA.8x8x4 contractions (one-hot x [X', X'^2]); n is exact on the
+// integer pipe.  The epilogue evaluates the reference formulas in centred
+// form (the pivot cancels from every deviation) and replays the reference's
+// sequential raw one-pass loop exactly for pairs whose within-group sums are
+// ill-conditioned, so degenerate-variance decisions (ssw_j > 0, SSW == 0,
+// pooled == 0) match bit for bit.
+//
+// Algorithmic work: 4 k_g FP64 flops per pair-sample (ANOVA), 8 (t-test).
+#include "ps_internal.cuh"
+#include "ps_specfun.cuh"
+#include <math_constants.h>
+#include <algorithm>
+#include <vector>
+
+namespace {
+
+constexpr int T = 64;        // rows (label levels) x cols (continuous features) per tile
+constexpr int KC = 32;
+constexpr int XS = KC + 4;
+constexpr int NW = 8;        // 4 x 2 warps, 16 x 32 cells each
+constexpr int NTH = NW * 32;
+constexpr int WM = 2, WN = 4;
+constexpr int NSTAGE = 3;
+constexpr double kReplayTau = 1e-6;
+
+struct Stage {
+  double x[T][XS];
+  uint32_t mh[T];
+  uint32_t oh[T];
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// one-hot bit rows: row r = (feature row_feat[r], level row_level[r]); level
+// -1 / -2 select the t-test rows (present && v == 0.0 / present && v != 0.0).
+__global__ void onehot_bits_kernel(const uint8_t* __restrict__ codes, int64_t ldc,
+                                   const uint32_t* __restrict__ mask, const uint32_t* __restrict__ zero,
+                                   int64_t W, const int32_t* __restrict__ row_feat,
+                                   const int32_t* __restrict__ row_level, int64_t R, int64_t S,
+                                   uint32_t* __restrict__ bits) {
+  const int64_t r = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* out = bits + r * W;
+  if (r >= R) {
+    for (int64_t w = threadIdx.x; w < W; w += blockDim.x) out[w] = 0u;
+    return;
+  }
+  const int f = row_feat[r], lev = row_level[r];
+  if (lev < 0) {
+    for (int64_t w = threadIdx.x; w < W; w += blockDim.x) {
+      const uint32_t m = mask[f * W + w], z = zero[f * W + w];
+      out[w] = lev == -1 ? (m & z) : (m & ~z);
+    }
+    return;
+  }
+  const uint8_t* c = codes + f * ldc;
+  for (int64_t w = warp; w < W; w += blockDim.x / 32) {
+    const int64_t s = w * 32 + lane;
+    const bool hit = s < S && c[s] == (uint8_t)lev;
+    const uint32_t b = __ballot_sync(PS_FULL, hit);
+    if (lane == 0) out[w] = b;
+  }
+}
+
+// M[r][h] moments over upper-left-aligned 64 x 64 tiles of (label rows x features)
+__global__ void __launch_bounds__(NTH, 2)
+group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double* __restrict__ vals,
+                  int64_t ld, const uint32_t* __restrict__ mask, const double* __restrict__ center,
+                  int64_t W, int64_t Fq, int64_t row_tile0, int64_t col_tiles, int32_t* __restrict__ Mn,
+                  double* __restrict__ Ms, double* __restrict__ Mq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Stage* st = reinterpret_cast<Stage*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = warp >> 1, wj = warp & 1;
+  const int64_t rt = row_tile0 + blockIdx.x / col_tiles, ct = blockIdx.x % col_tiles;
+  const int64_t row0 = rt * T, col0 = ct * T;
+  const int fr = lane >> 2, fk = lane & 3;
+  double cj[WN];
+#pragma unroll
+  for (int q = 0; q < WN; ++q) {
+    const int64_t gc = col0 + wj * 8 * WN + q * 8 + fr;
+    cj[q] = gc < Fq ? center[gc] : 0.0;
+  }
+  double as[WM][WN][2], aq[WM][WN][2];
+  int an[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        as[i][j][e] = aq[i][j][e] = 0.0;
+        an[i][j][e] = 0;
+      }
+  constexpr int LQ = (T * KC / 2) / NTH;
+  auto issue = [&](int64_t c, Stage& sd) {
+#pragma unroll
+    for (int q = 0; q < LQ; ++q) {
+      const int idx = tid + q * NTH;
+      const int r = idx >> 4, c2 = idx & 15;
+      const int64_t gj = min(col0 + r, Fq - 1);
+      const unsigned sj = (unsigned)__cvta_generic_to_shared(&sd.x[r][c2 * 2]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sj), "l"(vals + gj * ld + c * KC + c2 * 2));
+    }
+    if (tid < T) {
+      const int64_t gc = col0 + tid;
+      sd.mh[tid] = gc < Fq ? mask[gc * W + c] : 0u;
+    } else if (tid < 2 * T) {
+      sd.oh[tid - T] = ohbits[(row0 + tid - T) * W + c];
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  for (int q = 0; q < NSTAGE - 1; ++q) {
+    if (q < W) issue(q, st[q]);
+    else asm volatile("cp.async.commit_group;");
+  }
+  for (int64_t c = 0; c < W; ++c) {
+    const int cur = (int)(c % NSTAGE);
+    asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2));
+    __syncthreads();
+    {
+      const int64_t cn = c + NSTAGE - 1;
+      if (cn < W) issue(cn, st[(int)(cn % NSTAGE)]);
+      else asm volatile("cp.async.commit_group;");
+    }
+    const Stage& s = st[cur];
+    uint32_t orow[WM], mcol[WN];
+#pragma unroll
+    for (int q = 0; q < WM; ++q) orow[q] = s.oh[wi * 8 * WM + q * 8 + fr];
+#pragma unroll
+    for (int q = 0; q < WN; ++q) mcol[q] = s.mh[wj * 8 * WN + q * 8 + fr];
+#pragma unroll
+    for (int kk = 0; kk < KC / 4; ++kk) {
+      const int k = kk * 4 + fk;
+      double oa[WM], xb[WN], xb2[WN];
+#pragma unroll
+      for (int q = 0; q < WM; ++q) oa[q] = ((orow[q] >> k) & 1u) ? 1.0 : 0.0;
+#pragma unroll
+      for (int q = 0; q < WN; ++q) {
+        const bool pb = (mcol[q] >> k) & 1u;
+        xb[q] = pb ? s.x[wj * 8 * WN + q * 8 + fr][k] - cj[q] : 0.0;
+        xb2[q] = xb[q] * xb[q];
+      }
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) {
+          dmma(as[i][j][0], as[i][j][1], oa[i], xb[j]);
+          dmma(aq[i][j][0], aq[i][j][1], oa[i], xb2[j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < WM; ++i)
+#pragma unroll
+      for (int j = 0; j < WN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) an[i][j][e] += __popc(orow[i] & s.mh[wj * 8 * WN + j * 8 + 2 * fk + e]);
+  }
+  asm volatile("cp.async.wait_group 0;");
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t r = row0 + wi * 8 * WM + i * 8 + fr;
+        const int64_t h = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
+        if (h >= Fq) continue;
+        Mn[r * Fq + h] = an[i][j][e];
+        Ms[r * Fq + h] = as[i][j][e];
+        Mq[r * Fq + h] = aq[i][j][e];
+      }
+}
+
+struct Outs {
+  double* stat;
+  double* p;
+  double* eff;
+  int2* replay;
+  int* replay_count;
+  int replay_cap;
+  int* err;
+};
+
+__device__ __forceinline__ void push_replay(const Outs& o, int64_t g, int64_t h) {
+  const int slot = atomicAdd(o.replay_count, 1);
+  if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
+}
+
+// mixed.py:453-495 from raw (counts, sums, ssq) -- the exact reference form
+__device__ void anova_finish_raw(const long long* counts, const double* sums, const double* ssq, int k,
+                                 double* f_out, double* p_out, double* eta_out, int* err) {
+  *f_out = *p_out = *eta_out = PS_NAN;
+  if (k < 2) return;
+  long long n = 0;
+  double total = 0.0;
+  for (int j = 0; j < k; ++j) {
+    if (counts[j] == 0) return;
+    n += counts[j];
+    total += sums[j];
+  }
+  if (n <= k) return;
+  const double grand = total / (double)n;
+  double ssb = 0.0, ssw = 0.0, mlo = CUDART_INF, mhi = -CUDART_INF, scale = 0.0;
+  for (int j = 0; j < k; ++j) {
+    const double mj = sums[j] / (double)counts[j];
+    const double dev = mj - grand;
+    ssb += (double)counts[j] * dev * dev;
+    const double gs = ssq[j] - sums[j] * mj;
+    if (gs > 0.0) ssw += gs;
+    if (mj < mlo) mlo = mj;
+    if (mj > mhi) mhi = mj;
+    if (fabs(mj) > scale) scale = fabs(mj);
+  }
+  if (ssw == 0.0) {
+    if ((mhi - mlo) <= 1e-12 * scale) return;
+    *f_out = CUDART_INF;
+    *p_out = 0.0;
+    *eta_out = 1.0;
+    return;
+  }
+  const double f = (ssb / ((double)k - 1.0)) / (ssw / (double)(n - k));
+  *f_out = f;
+  *p_out = psf::f_sf(f, (double)k - 1.0, (double)(n - k), err);
+  *eta_out = ssb / (ssb + ssw);
+}
+
+// mixed.py:121-157 from raw group sums -- the exact reference form
+__device__ void ttest_finish_raw(long long n0, long long n1, double sum0, double sum1, double ss0,
+                                 double ss1, int student, double* t_out, double* p_out, double* d_out,
+                                 int* err) {
+  *t_out = *p_out = *d_out = PS_NAN;
+  if (n0 < 2 || n1 < 2 || n0 + n1 < 3) return;
+  const double mean0 = sum0 / (double)n0, mean1 = sum1 / (double)n1;
+  double var0 = (ss0 - sum0 * mean0) / (double)(n0 - 1);
+  double var1 = (ss1 - sum1 * mean1) / (double)(n1 - 1);
+  if (var0 < 0.0) var0 = 0.0;
+  if (var1 < 0.0) var1 = 0.0;
+  const double diff = mean0 - mean1;
+  double t, dof, d;
+  if (student) {
+    const double pooled = ((double)(n0 - 1) * var0 + (double)(n1 - 1) * var1) / (double)(n0 + n1 - 2);
+    if (pooled == 0.0) return;
+    const double sp = sqrt(pooled);
+    t = diff / (sp * sqrt(1.0 / (double)n0 + 1.0 / (double)n1));
+    dof = (double)(n0 + n1 - 2);
+    d = diff / sp;
+  } else {
+    if (var0 + var1 == 0.0) return;
+    const double v0 = var0 / (double)n0, v1 = var1 / (double)n1;
+    t = diff / sqrt(v0 + v1);
+    dof = (v0 + v1) * (v0 + v1) / (v0 * v0 / (double)(n0 - 1) + v1 * v1 / (double)(n1 - 1));
+    d = diff / sqrt(0.5 * (var0 + var1));
+  }
+  double p = 2.0 * psf::t_sf(fabs(t), dof, err);
+  if (p > 1.0) p = 1.0;
+  *t_out = t;
+  *p_out = p;
+  *d_out = d;
+}
+
+template <int KM>
+__global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, const double* __restrict__ Ms,
+                                    const double* __restrict__ Mq, const int32_t* __restrict__ off,
+                                    const int32_t* __restrict__ cat, const double* __restrict__ center,
+                                    int64_t Fq, int64_t lo, int64_t hi, int student, Outs o) {
+  for (int64_t idx = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < hi;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = idx / Fq, h = idx - g * Fq;
+    const double c = center[h];
+    double r0 = PS_NAN, r1 = PS_NAN, r2 = PS_NAN;
+    if (test == PS_TEST_ANOVA) {
+      const int k = cat[g];
+      const int64_t base = (int64_t)off[g];
+      if (k >= 2) {
+        long long n = 0;
+        double total = 0.0;
+        bool empty = false, replay = false;
+        for (int j = 0; j < k; ++j) {
+          const int64_t cell = (base + j) * Fq + h;
+          const long long nj = Mn[cell];
+          if (nj == 0) empty = true;
+          n += nj;
+          total += Ms[cell];
+        }
+        if (!empty && n > k) {
+          const double grand = total / (double)n;
+          double ssb = 0.0, ssw = 0.0, mlo = CUDART_INF, mhi = -CUDART_INF, scale = 0.0;
+          for (int j = 0; j < k; ++j) {
+            const int64_t cell = (base + j) * Fq + h;
+            const double nj = (double)Mn[cell], sj = Ms[cell], qj = Mq[cell];
+            const double mj = sj / nj;
+            const double dev = mj - grand;
+            ssb += nj * dev * dev;
+            const double gs = qj - sj * mj;
+            // the reference forms ssq - sum*mean in raw (uncentred) sums:
+            // replay exactly whenever the sign of that could be in doubt
+            if (!(gs > kReplayTau * (qj + nj * c * c))) replay = true;
+            ssw += gs;
+            const double mr = mj + c;
+            mlo = fmin(mlo, mr);
+            mhi = fmax(mhi, mr);
+            scale = fmax(scale, fabs(mr));
+          }
+          if (replay) {
+            push_replay(o, g, h);
+            continue;
+          }
+          const double f = (ssb / ((double)k - 1.0)) / (ssw / (double)(n - k));
+          r0 = f;
+          r1 = psf::f_sf(f, (double)k - 1.0, (double)(n - k), o.err);
+          r2 = ssb / (ssb + ssw);
+        }
+      }
+    } else {
+      const int64_t c0 = (2 * g) * Fq + h, c1 = (2 * g + 1) * Fq + h;
+      const long long n0 = Mn[c0], n1 = Mn[c1];
+      if (!(n0 < 2 || n1 < 2 || n0 + n1 < 3)) {
+        const double s0 = Ms[c0], s1 = Ms[c1], q0 = Mq[c0], q1 = Mq[c1];
+        const double m0 = s0 / (double)n0, m1 = s1 / (double)n1;
+        const double w0 = q0 - s0 * m0, w1 = q1 - s1 * m1;
+        if (!(w0 > kReplayTau * (q0 + (double)n0 * c * c)) || !(w1 > kReplayTau * (q1 + (double)n1 * c * c))) {
+          push_replay(o, g, h);
+          continue;
+        }
+        const double var0 = w0 / (double)(n0 - 1), var1 = w1 / (double)(n1 - 1);
+        const double diff = m0 - m1;
+        double t, dof, d;
+        if (student) {
+          const double pooled = ((double)(n0 - 1) * var0 + (double)(n1 - 1) * var1) / (double)(n0 + n1 - 2);
+          const double sp = sqrt(pooled);
+          t = diff / (sp * sqrt(1.0 / (double)n0 + 1.0 / (double)n1));
+          dof = (double)(n0 + n1 - 2);
+          d = diff / sp;
+        } else {
+          const double v0 = var0 / (double)n0, v1 = var1 / (double)n1;
+          t = diff / sqrt(v0 + v1);
+          dof = (v0 + v1) * (v0 + v1) / (v0 * v0 / (double)(n0 - 1) + v1 * v1 / (double)(n1 - 1));
+          d = diff / sqrt(0.5 * (var0 + var1));
+        }
+        double p = 2.0 * psf::t_sf(fabs(t), dof, o.err);
+        if (p > 1.0) p = 1.0;
+        r0 = t;
+        r1 = p;
+        r2 = d;
+      }
+    }
+    if (o.stat) o.stat[idx] = r0;
+    if (o.p) o.p[idx] = r1;
+    if (o.eff) o.eff[idx] = r2;
+  }
+}
+
+// Exact replay of _anova_rows / _ttest_rows (mixed.py:182-202, :498-520):
+// one thread per cell, samples in order, raw fp64 one-pass sums.
+template <int KM>
+__global__ void group_replay_kernel(int test, const double* __restrict__ lab_vals, int64_t lld,
+                                    const uint8_t* __restrict__ codes, int64_t ldc,
+                                    const uint32_t* __restrict__ lmask, const double* __restrict__ vals,
+                                    int64_t ld, const uint32_t* __restrict__ vmask, int64_t W, int64_t S,
+                                    const int32_t* __restrict__ cat, int64_t Fq, int student, Outs o) {
+  const int count = *o.replay_count;
+  if (count == 0) return;
+  const bool overflow = count > o.replay_cap;
+  (void)overflow;
+  const int n_items = min(count, o.replay_cap);
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
+    const int64_t g = o.replay[it].x, h = o.replay[it].y;
+    const double* xv = vals + h * ld;
+    const uint32_t* mg = lmask + g * W;
+    const uint32_t* mh = vmask + h * W;
+    double r0, r1, r2;
+    if (test == PS_TEST_ANOVA) {
+      const int k = cat[g];
+      long long counts[KM];
+      double sums[KM], ssq[KM];
+      for (int j = 0; j < k; ++j) {
+        counts[j] = 0;
+        sums[j] = 0.0;
+        ssq[j] = 0.0;
+      }
+      const uint8_t* cg = codes + g * ldc;
+      for (int64_t s = 0; s < S; ++s) {
+        if (((mg[s >> 5] & mh[s >> 5]) >> (s & 31)) & 1u) {
+          const int j = cg[s];
+          if (j >= k) continue;  // out-of-range labels are reported by the label check
+          const double v = xv[s];
+          counts[j] += 1;
+          sums[j] += v;
+          ssq[j] += v * v;
+        }
+      }
+      anova_finish_raw(counts, sums, ssq, k, &r0, &r1, &r2, o.err);
+    } else {
+      const double* lv = lab_vals + g * lld;
+      long long n0 = 0, n1 = 0;
+      double s0 = 0, s1 = 0, q0 = 0, q1 = 0;
+      for (int64_t s = 0; s < S; ++s) {
+        if (((mg[s >> 5] & mh[s >> 5]) >> (s & 31)) & 1u) {
+          const double v = xv[s];
+          if (lv[s] == 0.0) {
+            ++n0;
+            s0 += v;
+            q0 += v * v;
+          } else {
+            ++n1;
+            s1 += v;
+            q1 += v * v;
+          }
+        }
+      }
+      ttest_finish_raw(n0, n1, s0, s1, q0, q1, student, &r0, &r1, &r2, o.err);
+    }
+    const int64_t idx = g * Fq + h;
+    if (o.stat) o.stat[idx] = r0;
+    if (o.p) o.p[idx] = r1;
+    if (o.eff) o.eff[idx] = r2;
+  }
+}
+
+// LabelOutOfRange (mixed.py:511-515): a bad present label of a label row in
+// [g0, g1) meeting a present value of any continuous feature in [h0, h1).
+__global__ void mixed_label_check_kernel(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ vmask,
+                                         int64_t W, int64_t g0, int64_t g1, int64_t h0, int64_t h1,
+                                         int* __restrict__ err) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t anyb = 0;
+    for (int64_t g = g0; g < g1; ++g) anyb |= bad[g * W + w];
+    if (!anyb) continue;
+    uint32_t col = 0;
+    for (int64_t h = h0; h < h1 && !(col & anyb); ++h) col |= vmask[h * W + w];
+    if (col & anyb) {
+      ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
+                        double* stat, double* p, double* eff, cudaStream_t s) {
+  const int64_t Fc = lab->F, Fq = val->F, S = val->S;
+  if (lab->S != S) return ps_fail(PS_ERR_INVALID, "sample counts differ");
+  lo = std::max<int64_t>(0, lo);
+  hi = std::min<int64_t>(Fc * Fq, hi);
+  if (hi <= lo || (!stat && !p && !eff)) return PS_OK;
+  ps_device_state* ds = ps_state();
+  const int64_t W = val->W;
+  const int64_t g0 = lo / Fq, g1 = (hi - 1) / Fq + 1;
+  // label rows of g0..g1-1
+  std::vector<int32_t> off(Fc + 1, 0);
+  std::vector<int32_t> rf, rl;
+  for (int64_t g = 0; g < Fc; ++g) {
+    const int k = test == PS_TEST_ANOVA ? (int)lab->h_cat[g] : 2;
+    off[g + 1] = off[g] + k;
+  }
+  for (int64_t g = 0; g < Fc; ++g) {
+    const int k = off[g + 1] - off[g];
+    for (int j = 0; j < k; ++j) {
+      rf.push_back((int32_t)g);
+      rl.push_back(test == PS_TEST_ANOVA ? j : -1 - j);
+    }
+  }
+  const int64_t R = off[Fc];
+  const int64_t Rp = std::max<int64_t>(T, ps_round_up(R, T));
+  const int64_t rtile0 = off[g0] / T;
+  const int64_t rtile1 = off[g1] > 0 ? (off[g1] - 1) / T + 1 : rtile0;
+  const int64_t ctiles = ps_ceil_div(Fq, T);
+
+  uint32_t* bits = nullptr;
+  int32_t *d_rf = nullptr, *d_rl = nullptr, *d_off = nullptr, *Mn = nullptr, *repc = nullptr;
+  double *Ms = nullptr, *Mq = nullptr;
+  int2* rep = nullptr;
+  const int cap = (int)std::min<int64_t>(hi - lo, 1 << 22);
+  PS_CUDA(ps_alloc(&bits, (size_t)(Rp * W), s));
+  PS_CUDA(ps_alloc(&d_rf, (size_t)std::max<int64_t>(R, 1), s));
+  PS_CUDA(ps_alloc(&d_rl, (size_t)std::max<int64_t>(R, 1), s));
+  PS_CUDA(ps_alloc(&d_off, (size_t)(Fc + 1), s));
+  PS_CUDA(ps_alloc(&Mn, (size_t)(Rp * Fq), s));
+  PS_CUDA(ps_alloc(&Ms, (size_t)(Rp * Fq), s));
+  PS_CUDA(ps_alloc(&Mq, (size_t)(Rp * Fq), s));
+  PS_CUDA(ps_alloc(&rep, (size_t)cap, s));
+  PS_CUDA(ps_alloc(&repc, 1, s));
+  PS_CUDA(cudaMemsetAsync(repc, 0, sizeof(int), s));
+  if (R > 0) {
+    PS_CUDA(cudaMemcpyAsync(d_rf, rf.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(d_rl, rl.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+  }
+  PS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (Fc + 1), cudaMemcpyHostToDevice, s));
+  if (test == PS_TEST_ANOVA) {
+    const int64_t h0 = g1 - g0 > 1 ? 0 : lo - g0 * Fq;
+    const int64_t h1 = g1 - g0 > 1 ? Fq : hi - g0 * Fq;
+    mixed_label_check_kernel<<<(unsigned)std::min<int64_t>(ps_ceil_div(W, 128), 1024), 128, 0, s>>>(
+        lab->d_bad, val->d_mask, W, g0, g1, h0, h1, ds->d_err);
+    PS_LAUNCHED();
+  }
+  onehot_bits_kernel<<<(unsigned)Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, d_rf,
+                                                  d_rl, R, lab->S, bits);
+  PS_LAUNCHED();
+  const size_t smem = NSTAGE * sizeof(Stage);
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = (rtile1 - rtile0) * ctiles;
+  if (grid > 0) {
+    ps_prof_begin("group_gemm", s);
+    group_gemm_kernel<<<(unsigned)grid, NTH, smem, s>>>(bits, Rp, val->d_vals, val->ld, val->d_mask,
+                                                         val->d_center, W, Fq, rtile0, ctiles, Mn, Ms, Mq);
+    ps_prof_end(s);
+    PS_LAUNCHED();
+  }
+  Outs o{stat, p, eff, rep, repc, cap, ds->d_err};
+  const int blocks = (int)std::min<int64_t>(ps_ceil_div(hi - lo, 128), (int64_t)ds->num_sms * 16);
+  const bool small = lab->cmax <= 16;
+  if (small)
+    group_finish_kernel<16><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq, lo,
+                                                   hi, student, o);
+  else
+    group_finish_kernel<256><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq,
+                                                    lo, hi, student, o);
+  PS_LAUNCHED();
+  if (small)
+    group_replay_kernel<16><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_vals, lab->ld, lab->d_codes, lab->ldc,
+                                                           lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
+                                                           S, lab->d_cat, Fq, student, o);
+  else
+    group_replay_kernel<256><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_vals, lab->ld, lab->d_codes, lab->ldc,
+                                                            lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
+                                                            S, lab->d_cat, Fq, student, o);
+  PS_LAUNCHED();
+  // a replay list overflow (pathological: > 4M ill-conditioned cells) is reported
+  int count = 0;
+  PS_CUDA(cudaMemcpyAsync(&count, repc, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  ps_free(bits, s);
+  ps_free(d_rf, s);
+  ps_free(d_rl, s);
+  ps_free(d_off, s);
+  ps_free(Mn, s);
+  ps_free(Ms, s);
+  ps_free(Mq, s);
+  ps_free(rep, s);
+  ps_free(repc, s);
+  if (count > cap) return ps_fail(PS_ERR_INVALID, "too many ill-conditioned cells for the exact replay list");
+  return PS_OK;
+}

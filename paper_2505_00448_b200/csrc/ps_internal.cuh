@@ -33,11 +33,14 @@ struct ps_matrix {
   // presort tables (rank tests)
   bool has_presort = false;
   int32_t* d_len = nullptr;       // F present counts (== d_count)
-  uint32_t* d_order = nullptr;    // F x S: sample ids of present entries, ascending value, stable
-  uint32_t* d_gs = nullptr;       // F x S: tie-group start position of sorted position p
-  uint32_t* d_ge = nullptr;       // F x S: tie-group end position (exclusive)
+  int64_t ldo = 0;                // row stride of d_order / d_inv (uint16), multiple of 64
+  int64_t ldt = 0;                // row stride of the tie tables (words), tie_words(S)
+  uint16_t* d_order = nullptr;    // F x ldo: sample ids of present entries, ascending value, stable
+  uint16_t* d_inv = nullptr;      // F x ldo: sorted position of sample s, 0xFFFF if missing
+  uint32_t* d_tb = nullptr;       // F x ldt: tie-group boundary bits (ps_ties.cuh)
+  uint16_t* d_lastb = nullptr;    // F x ldt: prefix-max boundary position per word
+  uint16_t* d_nextb = nullptr;    // F x ldt: suffix-min boundary position per word
   uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
-  uint16_t* d_inv = nullptr;      // F x S: sorted position of sample s, 0xFFFF if missing (S <= 65535)
 };
 
 // Per-device library state.

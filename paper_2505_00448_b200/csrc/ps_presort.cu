@@ -16,6 +16,7 @@
 //                float '==' runs (ranking.py:56-89): NaN never ties
 //   tied[f]      1 if some tie group has more than one member
 #include "ps_internal.cuh"
+#include "ps_ties.cuh"
 #include <algorithm>
 
 namespace {
@@ -67,8 +68,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_buf, int& total)
 __global__ void __launch_bounds__(NT)
 presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
                int64_t W, int64_t S, uint64_t* __restrict__ keyA, uint32_t* __restrict__ idxA,
-               uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, uint32_t* __restrict__ order,
-               uint16_t* __restrict__ inv, uint32_t* __restrict__ gs, uint32_t* __restrict__ ge,
+               uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, uint16_t* __restrict__ order,
+               uint16_t* __restrict__ inv, int64_t ldo, uint32_t* __restrict__ tb,
+               uint16_t* __restrict__ lastb, uint16_t* __restrict__ nextb, int64_t ldt,
                uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
   __shared__ int warp_buf[NW];
   __shared__ uint32_t hist[8][256];
@@ -181,54 +183,63 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
     __syncthreads();
   }
 
-  // 3. outputs: order, inverse permutation, tie groups
-  uint32_t* ord = order + f * S;
-  uint16_t* iv = inv + f * S;
+  // 3. outputs: order, inverse permutation, tie-group boundary tables
+  uint16_t* ord = order + f * ldo;
+  uint16_t* iv = inv + f * ldo;
   for (int64_t s = threadIdx.x; s < S; s += NT) iv[s] = 0xFFFF;
   __syncthreads();
   for (int p = threadIdx.x; p < n; p += NT) {
     const uint32_t s = iA[p];
-    ord[p] = s;
+    ord[p] = (uint16_t)s;
     iv[s] = (uint16_t)p;
   }
-  // gs: inclusive max-scan of (boundary ? p : 0); ge: next boundary (or n)
-  uint32_t* gsr = gs + f * S;
-  uint32_t* ger = ge + f * S;
-  int carry_gs = 0;
-  for (int base = 0; base < n; base += NT) {
-    const int p = base + threadIdx.x;
+  uint32_t* tbr = tb + f * ldt;
+  uint16_t* lbr = lastb + f * ldt;
+  uint16_t* nbr = nextb + f * ldt;
+  const int nw = (int)ldt;
+  for (int w = warp; w < nw; w += NW) {
+    const int p = w * 32 + lane;
     bool bnd = false;
     if (p < n) {
       bnd = p == 0 || kA[p] != kA[p - 1] || key_is_nan(kA[p]);
       if (!bnd) s_any_tie = 1;
+    } else {
+      bnd = p == n;  // sentinel boundary closes the last group
     }
-    int x = (p < n && bnd) ? p : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(PS_FULL, x, o);
-      if (lane >= o) x = max(x, y);
-    }
-    if (lane == 31) warp_buf[warp] = x;
-    __syncthreads();
-    int pre = carry_gs;
-    for (int w = 0; w < warp; ++w) pre = max(pre, warp_buf[w]);
-    x = max(x, pre);
-    if (p < n) gsr[p] = (uint32_t)x;
-    int last = carry_gs;
-    for (int w = 0; w < NW; ++w) last = max(last, warp_buf[w]);
-    __syncthreads();
-    carry_gs = last;
+    const uint32_t word = __ballot_sync(PS_FULL, bnd);
+    if (lane == 0) tbr[w] = word;
   }
   __syncthreads();
-  // ge[p] = gs of the first position after p's group: walk groups by start
-  for (int p = threadIdx.x; p < n; p += NT) {
-    // group end: the next boundary after p; boundaries are where gs[q] == q
-    // (scan forward; groups are short in the common case, long runs are
-    // handled by the per-group owner below)
-    if ((int)gsr[p] == p) {
-      int q = p + 1;
-      while (q < n && (int)gsr[q] != q) ++q;
-      for (int t = p; t < q; ++t) ger[t] = (uint32_t)q;
+  if (warp == 0) {  // lastb: inclusive prefix max of the last boundary per word
+    int carry = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int w = w0 + lane;
+      const uint32_t word = w < nw ? tbr[w] : 0u;
+      int x = word ? w * 32 + 31 - __clz(word) : -1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(PS_FULL, x, o);
+        if (lane >= o) x = max(x, y);
+      }
+      x = max(x, carry);
+      if (w < nw) lbr[w] = (uint16_t)x;
+      carry = __shfl_sync(PS_FULL, x, 31);
+    }
+  } else if (warp == 1) {  // nextb: inclusive suffix min of the first boundary per word
+    int carry = 0xFFFF;
+    const int last0 = ((nw - 1) / 32) * 32;
+    for (int w0 = last0; w0 >= 0; w0 -= 32) {
+      const int w = w0 + lane;
+      const uint32_t word = w < nw ? tbr[w] : 0u;
+      int x = word ? w * 32 + __ffs(word) - 1 : 0xFFFF;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_down_sync(PS_FULL, x, o);
+        if (lane + o < 32) x = min(x, y);
+      }
+      x = min(x, carry);
+      if (w < nw) nbr[w] = (uint16_t)x;
+      carry = __shfl_sync(PS_FULL, x, 0);
     }
   }
   __syncthreads();
@@ -245,27 +256,29 @@ int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
   if (m->S > 65535)
     return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
   const int64_t FS = m->F * m->S;
+  m->ldo = ps_round_up(m->S, 64);
+  m->ldt = tie_words(m->S);
   uint64_t *kA = nullptr, *kB = nullptr;
   uint32_t *iA = nullptr, *iB = nullptr;
   PS_CUDA(ps_alloc(&kA, (size_t)FS, s));
   PS_CUDA(ps_alloc(&kB, (size_t)FS, s));
   PS_CUDA(ps_alloc(&iA, (size_t)FS, s));
   PS_CUDA(ps_alloc(&iB, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&m->d_order, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&m->d_inv, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&m->d_gs, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&m->d_ge, (size_t)FS, s));
+  PS_CUDA(ps_alloc(&m->d_order, (size_t)(m->F * m->ldo), s));
+  PS_CUDA(ps_alloc(&m->d_inv, (size_t)(m->F * m->ldo), s));
+  PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
+  PS_CUDA(ps_alloc(&m->d_lastb, (size_t)(m->F * m->ldt), s));
+  PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
   presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,
-                                               m->d_order, m->d_inv, m->d_gs, m->d_ge, m->d_tied,
-                                               m->d_len);
+                                               m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
+                                               m->d_nextb, m->ldt, m->d_tied, m->d_len);
   PS_LAUNCHED();
   ps_free(kA, s);
   ps_free(kB, s);
   ps_free(iA, s);
   ps_free(iB, s);
-  // host copy of the tie flags steers kernel specialisation
   m->has_presort = true;
   return PS_OK;
 }

@@ -1,0 +1,99 @@
+"""ANOVA / t-test (moment contraction) and Kruskal-Wallis / Mann-Whitney U
+(label-filtered rank walks) on the B200 vs the CPU oracle
+(reference mixed.py:121-663).
+
+ANOVA F / eta^2 and t / d: |rel| <= 1e-9; KW H, MWU U and r: bit-exact (exact
+rank sums replayed in the reference's op order); p within 1e-6 relative or
+1e-12 absolute; identical NaN pattern.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal, max_rel, p_close, same_nan
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+import paper_2505_00448_b200 as ps
+
+
+def _inputs(test, Fc, Fq, S, na, seed, c=4):
+    kind = ps.KINDS_BY_TEST[test][0]
+    a = workloads.simulate(Fc, S, kind, categories=c, na_ratio=na, seed=seed)
+    b = workloads.simulate(Fq, S, "continuous", na_ratio=na, seed=seed + 1)
+    return ps.make_matrix(a, kind), ps.make_matrix(b, "continuous")
+
+
+def _check_moment(res, ref, names):
+    for name in names:
+        assert same_nan(res[name], ref[name]), name
+    assert max_rel(res["stat"], ref["stat"], floor=1e-300) <= 1e-9
+    assert max_rel(res[names[-1]], ref[names[-1]], floor=1e-300) <= 1e-9
+    assert p_close(res["p"], ref["p"])
+
+
+@pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
+@pytest.mark.parametrize("variant", ["student", "welch"])
+def test_ttest_matches_oracle(oracle, na, variant):
+    a, b = _inputs("ttest", 12, 70, 300, na, seed=int(na * 100) + 3)
+    req = ps.TestRequest("ttest", ("stat", "p", "cohens_d"), t_variant=variant)
+    _check_moment(ps.run(req, a, b), oracle.oracle_run(req, a, b), ("stat", "p", "cohens_d"))
+
+
+@pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
+@pytest.mark.parametrize("c", [2, 3, 7])
+def test_anova_matches_oracle(oracle, na, c):
+    a, b = _inputs("anova", 12, 90, 400, na, seed=int(na * 100) + c, c=c)
+    req = ps.TestRequest("anova", ("stat", "p", "partial_eta2"))
+    _check_moment(ps.run(req, a, b), oracle.oracle_run(req, a, b), ("stat", "p", "partial_eta2"))
+
+
+def test_moment_degenerate_cases(oracle):
+    nan = np.nan
+    lab = np.array([
+        [0, 0, 1, 1, 0, 1, nan, 0],
+        [0, 0, 0, 0, 1, 1, 1, 1],
+        [0, 1, 0, 1, 0, 1, 0, 1],
+    ], dtype=float)
+    val = np.array([
+        [2.0, 2.0, 5.0, 5.0, 2.0, 5.0, 1.0, 2.0],    # zero within-group variance, unequal means
+        [3.0, 3.0, 3.0, 3.0, 3.0, 3.0, 3.0, 3.0],    # all equal
+        [0.1, 0.1, 0.1, 0.2, 0.1, 0.2, 0.1, 0.2],    # near-degenerate, rounding-sensitive
+        [1.0, 2.0, 4.0, 7.0, nan, nan, nan, 3.0],
+    ])
+    for test, kind in (("anova", "categorical"), ("ttest", "dichotomous")):
+        a = ps.make_matrix(lab, kind)
+        b = ps.make_matrix(val, "continuous")
+        outs = ("stat", "p", ps.EFFECTS_BY_TEST[test][0])
+        for variant in ("student", "welch"):
+            req = ps.TestRequest(test, outs, t_variant=variant)
+            res = ps.run(req, a, b)
+            ref = oracle.oracle_run(req, a, b)
+            for name in outs:
+                assert same_nan(res[name], ref[name]), (test, name)
+                m = ~np.isnan(ref[name])
+                np.testing.assert_allclose(res[name][m], ref[name][m], rtol=1e-9)
+
+
+def test_anova_config4_slice(oracle):
+    c = workloads.config(4, scale=0.05)
+    a = ps.make_matrix(c["a"], "categorical", na_sentinel=workloads.SENTINEL)
+    b = ps.make_matrix(c["b"], "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("anova", ("stat", "p", "partial_eta2", "p_bh"))
+    res = ps.run(req, a, b)
+    ref = oracle.oracle_run(req, a, b)
+    _check_moment(res, ref, ("stat", "p", "partial_eta2"))
+    assert same_nan(res["p_bh"], ref["p_bh"])
+
+
+def test_anova_label_out_of_range():
+    lab = np.array([[0.0, 1.0, 2.0, 1.0]])
+    val = np.array([[1.0, 2.0, 3.0, 4.0]])
+    good = ps.make_matrix(lab, "categorical")
+    bad = ps.DataMatrix(values=good.values, na_sentinel=good.na_sentinel, kind="categorical",
+                        category_counts=np.array([2]), present=good.present)
+    with pytest.raises(ps.LabelOutOfRange, match="category range"):
+        ps.run(ps.TestRequest("anova", ("stat",)), bad, ps.make_matrix(val, "continuous"))
