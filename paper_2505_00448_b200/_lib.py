@@ -20,7 +20,7 @@ from .errors import PS_ERR_NO_DEVICE, raise_for_status
 
 PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
-LIB_PATH = PKG_DIR / "libpairstat_b200.so"
+LIB_PATH = Path(os.environ["PS_LIB"]) if os.environ.get("PS_LIB") else PKG_DIR / "libpairstat_b200.so"
 
 TEST_CODES = {
     "pearson": 0,

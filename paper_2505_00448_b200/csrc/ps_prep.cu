@@ -59,6 +59,8 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
     }
     if (lane == 0) mask[f * W + (base >> 5)] = word;
   }
+  if (codes)
+    for (int64_t s = S + threadIdx.x; s < ldc; s += kPrepThreads) codes[f * ldc + s] = 0xFF;
   // block reduction of (sum, cnt); order is fixed, so the pivot is reproducible.
   __shared__ double ssum[kPrepThreads / 32];
   __shared__ int scnt[kPrepThreads / 32];
@@ -102,7 +104,7 @@ int ps_prepare_matrix(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
   const bool labels = m->kind != PS_KIND_CONTINUOUS;
   if (labels) {
-    m->ldc = ps_round_up(m->S, 16);
+    m->ldc = ps_round_up(m->S + 1, 16);  // code[S] = 0xFF: sentinel for padded walks
     PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
     PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
     PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));

@@ -186,12 +186,18 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
   // 3. outputs: order, inverse permutation, tie-group boundary tables
   uint16_t* ord = order + f * ldo;
   uint16_t* iv = inv + f * ldo;
-  for (int64_t s = threadIdx.x; s < S; s += NT) iv[s] = 0xFFFF;
+  // positions past n hold the sentinel sample id S, whose inverse is 0xFFFF
+  // (absent), so walks over whole 32-position words need no bounds checks
+  for (int64_t s = threadIdx.x; s < ldo; s += NT) iv[s] = 0xFFFF;
   __syncthreads();
-  for (int p = threadIdx.x; p < n; p += NT) {
-    const uint32_t s = iA[p];
-    ord[p] = (uint16_t)s;
-    iv[s] = (uint16_t)p;
+  for (int64_t p = threadIdx.x; p < ldo; p += NT) {
+    if (p < n) {
+      const uint32_t s = iA[p];
+      ord[p] = (uint16_t)s;
+      iv[s] = (uint16_t)p;
+    } else {
+      ord[p] = (uint16_t)S;
+    }
   }
   uint32_t* tbr = tb + f * ldt;
   uint16_t* lbr = lastb + f * ldt;
@@ -256,7 +262,7 @@ int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
   if (m->S > 65535)
     return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
   const int64_t FS = m->F * m->S;
-  m->ldo = ps_round_up(m->S, 64);
+  m->ldo = ps_round_up(m->S + 1, 64);  // room for the sentinel sample id S
   m->ldt = tie_words(m->S);
   uint64_t *kA = nullptr, *kB = nullptr;
   uint32_t *iA = nullptr, *iB = nullptr;

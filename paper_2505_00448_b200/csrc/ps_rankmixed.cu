@@ -1,0 +1,511 @@
+// ps_rankmixed.cu -- Kruskal-Wallis and Mann-Whitney U: label-filtered rank
+// walks over one presort of each continuous feature.
+//
+// Replaces _kruskal_block -> _kruskal_rows -> _kruskal_finish and _mwu_block ->
+// _mwu_rows -> _mwu_finish (engine.py:296-352; mixed.py:231-247, :305-403,
+// :550-623).  The reference walks continuous feature h's sorted order,
+// compacting the samples whose label is present, and averages ranks over tied
+// runs.  Here one persistent CTA owns h (its 16-bit order and tie tables stay
+// in shared memory) and walks it once per label row g:
+//
+//   phase 1  keep bits over h's order: keep(p) = label_g[order_h[p]] present
+//            (ballot per 32 positions) + a block scan of word popcounts;
+//   phase 2  joint rank 2r = Pfx(gs) + Pfx(ge) + 1 of every kept position,
+//            accumulated per level in registers (exact integer rank sums and
+//            counts) plus the tie term sum(t^3 - t) over kept tie groups.
+//
+// g's label row (one byte per sample) is double-buffered in shared memory and
+// prefetched with cp.async during the previous pair.  Per-pair exact sums go
+// to a buffer; a one-thread-per-pair epilogue replays _kruskal_finish /
+// _mwu_finish in the reference's fp64 op order (H, U, r bit-identical), and a
+// cold-path kernel builds the exact U distribution (Gaussian-binomial
+// coefficients, the same integers as mixed.py:231-247) when the exact test
+// applies.  Out-of-range labels of kept samples raise LabelOutOfRange.
+//
+// Algorithmic work: ~12 B of shared-memory traffic per pair-sample.
+#include "ps_internal.cuh"
+#include "ps_specfun.cuh"
+#include "ps_ties.cuh"
+#include <math_constants.h>
+#include <algorithm>
+
+namespace {
+
+constexpr int RW = 16;  // warps per CTA
+constexpr int RTH = RW * 32;
+
+struct RankSums {
+  int KM;                       // levels stored per pair
+  int32_t* cnt;                 // [pair][KM]
+  unsigned long long* r2;       // [pair][KM] sums of 2r
+  long long* tie;               // [pair] sum over tie groups of t^3 - t
+};
+
+__device__ __forceinline__ uint32_t pfx_at(const uint32_t* K, const uint32_t* P, uint32_t x) {
+  const uint32_t w = x >> 5, b = x & 31u;
+  return P[w] + __popc(K[w] & ((1u << b) - 1u));
+}
+
+__device__ void scan_words(uint32_t* K, uint32_t* P, int nwords, uint32_t* wsum) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (nwords + RTH - 1) / RTH;
+  const int w0 = threadIdx.x * per;
+  uint32_t local = 0;
+  for (int i = 0; i < per; ++i) {
+    const int w = w0 + i;
+    if (w < nwords) local += __popc(K[w]);
+  }
+  uint32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v = lane < RW ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(PS_FULL, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < RW) wsum[lane] = v;
+  }
+  __syncthreads();
+  uint32_t run = (warp > 0 ? wsum[warp - 1] : 0u) + x - local;
+  for (int i = 0; i < per; ++i) {
+    const int w = w0 + i;
+    if (w < nwords) {
+      P[w] = run;
+      run += __popc(K[w]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    K[nwords] = 0u;
+    P[nwords] = wsum[RW - 1];
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+
+// Codes: 0..k-1 valid level, 0xFE present but out of range, 0xFF missing.
+template <int KM>
+__global__ void __launch_bounds__(RTH, 2)
+rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const uint32_t* __restrict__ tb,
+                       const uint16_t* __restrict__ lastb, const uint16_t* __restrict__ nextb, int64_t ldt,
+                       const uint8_t* __restrict__ tied, const int32_t* __restrict__ lens,
+                       const uint8_t* __restrict__ codes, int64_t ldc, const int32_t* __restrict__ cat,
+                       int64_t Fc, int64_t Fq, int64_t lo, int64_t hi, int check_labels,
+                       int* __restrict__ queue, RankSums out, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* cur = smem;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = cur;
+    cur += (bytes + 15) & ~size_t(15);
+    return p;
+  };
+  uint16_t* oh = reinterpret_cast<uint16_t*>(take(ldo * 2));
+  uint32_t* tbh = reinterpret_cast<uint32_t*>(take(ldt * 4));
+  uint16_t* lbh = reinterpret_cast<uint16_t*>(take(ldt * 2));
+  uint16_t* nbh = reinterpret_cast<uint16_t*>(take(ldt * 2));
+  uint32_t* K = reinterpret_cast<uint32_t*>(take(ldt * 4));
+  uint32_t* P = reinterpret_cast<uint32_t*>(take(ldt * 4));
+  uint8_t* cg_s[2];
+  cg_s[0] = take(ldc);
+  cg_s[1] = take(ldc);
+  __shared__ uint32_t wsum[RW];
+  __shared__ unsigned long long red_r[RW][KM];
+  __shared__ uint32_t red_c[RW][KM];
+  __shared__ long long red_t[RW];
+  __shared__ int s_item;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  auto prefetch = [&](int64_t g, int b) {
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(cg_s[b]);
+    const unsigned char* src = codes + g * ldc;
+    for (int64_t c = threadIdx.x; c < ldc / 16; c += RTH) cp16(dst + c * 16, src + c * 16);
+    asm volatile("cp.async.commit_group;");
+  };
+
+  const int64_t items = hi - lo;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= items) break;
+    const int64_t h = lo + item;
+    const int nh = lens[h];
+    const bool th = tied[h] != 0;
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(order + h * ldo);
+      uint4* dst = reinterpret_cast<uint4*>(oh);
+      for (int64_t i = threadIdx.x; i < ldo / 8; i += RTH) dst[i] = src[i];
+      if (th) {
+        for (int64_t i = threadIdx.x; i < ldt; i += RTH) {
+          tbh[i] = tb[h * ldt + i];
+          lbh[i] = lastb[h * ldt + i];
+          nbh[i] = nextb[h * ldt + i];
+        }
+      }
+    }
+    prefetch(0, 0);
+    const int nw = (nh + 31) >> 5;
+    for (int64_t g = 0; g < Fc; ++g) {
+      const int buf = (int)(g & 1);
+      if (g + 1 < Fc) prefetch(g + 1, buf ^ 1);
+      else asm volatile("cp.async.commit_group;");
+      asm volatile("cp.async.wait_group 1;");
+      __syncthreads();
+      const uint8_t* cg = cg_s[buf];
+      const int k = cat[g];
+      // -------- phase 1: keep bits (label present) over h's order --------
+      bool bad = false;
+#pragma unroll 4
+      for (int word = warp; word < nw; word += RW) {
+        const int p = word * 32 + lane;
+        const uint32_t c = p < nh ? (uint32_t)cg[oh[p]] : 0xFFu;
+        bad |= c == 0xFEu;
+        const uint32_t B = __ballot_sync(PS_FULL, c != 0xFFu);
+        if (lane == 0) K[word] = B;
+      }
+      if (check_labels && __any_sync(PS_FULL, bad) && lane == 0) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
+      __syncthreads();
+      scan_words(K, P, nw, wsum);
+      // -------- phase 2: ranks, per-level sums, tie term --------
+      uint32_t acc[KM], cnt[KM];
+#pragma unroll
+      for (int j = 0; j < KM; ++j) acc[j] = cnt[j] = 0u;
+      long long tie = 0;
+      if (!th) {
+#pragma unroll 4
+        for (int word = warp; word < nw; word += RW) {
+          const int p = word * 32 + lane;
+          const uint32_t kw = K[word];
+          const uint32_t c = (kw >> lane) & 1u ? (uint32_t)cg[oh[p]] : 0xFFu;
+          const uint32_t r2 = 2u * (P[word] + __popc(kw & lanemask_lt()) + 1u);
+#pragma unroll
+          for (int j = 0; j < KM; ++j)
+            if (c == (uint32_t)j) {
+              acc[j] += r2;
+              cnt[j] += 1u;
+            }
+        }
+      } else {
+        for (int word = warp; word < nw; word += RW) {
+          const uint32_t p = (uint32_t)(word * 32 + lane);
+          const uint32_t kw = K[word];
+          if (p < (uint32_t)nh) {
+            const uint32_t gs = tie_start(tbh, lbh, p);
+            const uint32_t ge = tie_end(tbh, nbh, p);
+            const uint32_t a = pfx_at(K, P, gs), b = pfx_at(K, P, ge);
+            if (gs == p) {  // the group's first position owns its tie term
+              const long long t = (long long)(b - a);
+              if (t > 1) tie += t * t * t - t;
+            }
+            if ((kw >> lane) & 1u) {
+              const uint32_t c = cg[oh[p]];
+              const uint32_t r2 = a + b + 1u;
+#pragma unroll
+              for (int j = 0; j < KM; ++j)
+                if (c == (uint32_t)j) {
+                  acc[j] += r2;
+                  cnt[j] += 1u;
+                }
+            }
+          }
+        }
+      }
+      // -------- reduce to the pair's exact sums --------
+#pragma unroll
+      for (int j = 0; j < KM; ++j) {
+        unsigned long long a = acc[j];
+        uint32_t c = cnt[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(PS_FULL, a, o);
+          c += __shfl_xor_sync(PS_FULL, c, o);
+        }
+        if (lane == 0) {
+          red_r[warp][j] = a;
+          red_c[warp][j] = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tie += __shfl_xor_sync(PS_FULL, tie, o);
+      if (lane == 0) red_t[warp] = tie;
+      __syncthreads();
+      const int64_t pair = g * Fq + h;
+      if (threadIdx.x < KM) {
+        const int j = threadIdx.x;
+        unsigned long long a = 0;
+        uint32_t c = 0;
+        for (int w = 0; w < RW; ++w) {
+          a += red_r[w][j];
+          c += red_c[w][j];
+        }
+        if (j < k || j == 0) {
+          out.r2[pair * out.KM + j] = a;
+          out.cnt[pair * out.KM + j] = (int32_t)c;
+        }
+      } else if (threadIdx.x == 32) {
+        long long t = 0;
+        for (int w = 0; w < RW; ++w) t += red_t[w];
+        out.tie[pair] = t;
+      }
+    }
+    asm volatile("cp.async.wait_group 0;");
+  }
+}
+
+__device__ __forceinline__ void kruskal_finish(const RankSums& in, int64_t pair, int k, double* h_out,
+                                               double* p_out, double* eta_out, int* err) {
+  *h_out = *p_out = *eta_out = PS_NAN;
+  long long n = 0;
+  for (int j = 0; j < k; ++j) {
+    const long long c = in.cnt[pair * in.KM + j];
+    if (c == 0) return;
+    n += c;
+  }
+  if (n < 2) return;
+  const double fn = (double)n;
+  const double tie = (double)in.tie[pair];
+  const double tden = 1.0 - tie / (fn * fn * fn - fn);
+  if (tden <= 0.0) return;
+  double h = 0.0;
+  for (int j = 0; j < k; ++j) {
+    const double rs = (double)in.r2[pair * in.KM + j] * 0.5;  // exact half-integers
+    h += rs * rs / (double)in.cnt[pair * in.KM + j];
+  }
+  h = (12.0 / (fn * (fn + 1.0))) * h - 3.0 * (fn + 1.0);
+  h /= tden;
+  if (h < 0.0) h = 0.0;
+  *h_out = h;
+  if (k < 2) return;
+  *p_out = psf::chi2_sf(h, (double)k - 1.0, err);
+  if (n <= k) return;
+  *eta_out = (h - (double)k + 1.0) / (double)(n - k);
+}
+
+// mixed.py:305-363; returns 1 when the exact distribution is needed
+__device__ __forceinline__ int mwu_finish(long long n0, long long n1, double r0, double tie, int mode,
+                                          double* u_out, double* p_out, double* r_out, int* err) {
+  *u_out = *p_out = *r_out = PS_NAN;
+  if (n0 == 0 || n1 == 0) return 0;
+  const long long n = n0 + n1;
+  const double u = r0 - 0.5 * (double)n0 * (double)(n0 + 1);
+  const double mu = 0.5 * (double)n0 * (double)n1;
+  const double diff = u - mu;
+  bool use_exact = false;
+  if (mode == PS_U_EXACT) {
+    if (tie != 0.0) { ps_raise(err, PS_ERR_EXACT_WITH_TIES); return 0; }
+    if (n > 64) { ps_raise(err, PS_ERR_TABLE_TOO_LARGE); return 0; }
+    use_exact = true;
+  } else if (mode == PS_U_AUTO) {
+    use_exact = tie == 0.0 && (n0 < n1 ? n0 : n1) < 8 && n <= 64;
+  }
+  const double sigma_sq = ((double)(n0 * n1) / 12.0) * (((double)n + 1.0) - tie / ((double)n * ((double)n - 1.0)));
+  *u_out = u;
+  if (sigma_sq <= 0.0) return 0;
+  double z = (fabs(diff) - 0.5) / sqrt(sigma_sq);
+  if (z < 0.0) z = 0.0;
+  double r;
+  if (z == 0.0 || diff == 0.0) r = 0.0;
+  else if (diff > 0.0) r = z / sqrt((double)n);
+  else r = -z / sqrt((double)n);
+  *r_out = r;
+  if (use_exact) return 1;
+  double p = 2.0 * psf::normal_sf(z);
+  if (p > 1.0) p = 1.0;
+  *p_out = p;
+  return 0;
+}
+
+__device__ __forceinline__ void put_cell(double* o, int64_t idx, double v) {
+  if (o) o[idx] = v;
+}
+
+__global__ void rank_mixed_finish_kernel(int test, RankSums in, const int32_t* __restrict__ cat, int64_t Fc,
+                                         int64_t Fq, int64_t lo, int64_t hi, int mode, double* __restrict__ stat,
+                                         double* __restrict__ pout, double* __restrict__ eff,
+                                         int2* __restrict__ exact_list, int* __restrict__ exact_count,
+                                         int exact_cap, int* __restrict__ err) {
+  const int64_t total = Fc * (hi - lo);
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = it / (hi - lo), h = lo + it % (hi - lo);
+    const int64_t pair = g * Fq + h;
+    double a, b, c;
+    if (test == PS_TEST_KRUSKAL) {
+      kruskal_finish(in, pair, cat[g], &a, &b, &c, err);
+    } else {
+      const long long n0 = in.cnt[pair * in.KM + 0];
+      const long long n1 = in.cnt[pair * in.KM + 1];
+      const double r0 = (double)in.r2[pair * in.KM + 0] * 0.5;
+      if (mwu_finish(n0, n1, r0, (double)in.tie[pair], mode, &a, &b, &c, err)) {
+        const int slot = atomicAdd(exact_count, 1);
+        if (slot < exact_cap) exact_list[slot] = make_int2((int)g, (int)h);
+      }
+    }
+    put_cell(stat, pair, a);
+    put_cell(pout, pair, b);
+    put_cell(eff, pair, c);
+  }
+}
+
+// Cold path: exact two-sided U p-value (mixed.py:348-358).  The arrangement
+// counts f(n0, n1, u) are the coefficients of the Gaussian binomial
+// [n0+n1 choose n0]_q, built by P <- P (1 - q^(n1+i)) / (1 - q^i); every step
+// is an exact int64 polynomial, identical to the reference's DP table row.
+__global__ void mwu_exact_kernel(RankSums in, int64_t Fq, const int2* __restrict__ list,
+                                 const int* __restrict__ count_ptr, int cap, double* __restrict__ pout) {
+  __shared__ long long poly[1152];  // degree <= a (b + 1) <= 32 * 33 during the product
+  const int count = min(*count_ptr, cap);
+  for (int it = blockIdx.x; it < count; it += gridDim.x) {
+    const int64_t g = list[it].x, h = list[it].y;
+    const int64_t pair = g * Fq + h;
+    const long long n0 = in.cnt[pair * in.KM + 0];
+    const long long n1 = in.cnt[pair * in.KM + 1];
+    const double r0 = (double)in.r2[pair * in.KM + 0] * 0.5;
+    const int a = (int)(n0 < n1 ? n0 : n1), bb = (int)(n0 < n1 ? n1 : n0);
+    const int umax = (int)(n0 * n1);
+    if (threadIdx.x == 0) {
+      for (int u = 0; u <= a * (bb + 1); ++u) poly[u] = 0;
+      poly[0] = 1;
+      int deg = 0;
+      for (int i = 1; i <= a; ++i) {
+        const int m = bb + i;
+        // multiply by (1 - q^m)
+        for (int u = deg + m; u >= m; --u) poly[u] -= (u - m <= deg) ? poly[u - m] : 0;
+        deg += m;
+        // divide by (1 - q^i): exact
+        for (int u = i; u <= deg; ++u) poly[u] += poly[u - i];
+        deg -= i;
+      }
+      const double u = r0 - 0.5 * (double)n0 * (double)(n0 + 1);
+      const double lowv = u < (double)umax - u ? u : (double)umax - u;
+      const long long ulow = (long long)rint(lowv);
+      long long cum = 0, total = 0;
+      for (int v = 0; v <= umax; ++v) {
+        total += poly[v];
+        if (v <= ulow) cum += poly[v];
+      }
+      double p = 2.0 * (double)cum / (double)total;
+      if (p > 1.0) p = 1.0;
+      pout[pair] = p;
+    }
+    __syncthreads();
+  }
+}
+
+// MWU grouping codes from the dichotomous label bits: 0 if the label is 0.0,
+// 1 if present and non-zero (mixed.py:381), 0xFF if missing.
+__global__ void binary_codes_kernel(const uint32_t* __restrict__ mask, const uint32_t* __restrict__ zero,
+                                    int64_t W, int64_t S, int64_t ldc, uint8_t* __restrict__ out) {
+  const int64_t f = blockIdx.x;
+  for (int64_t s = threadIdx.x; s < ldc; s += blockDim.x) {
+    uint8_t c = 0xFF;
+    if (s < S) {
+      const uint32_t m = mask[f * W + (s >> 5)], z = zero[f * W + (s >> 5)];
+      const uint32_t bit = 1u << (s & 31);
+      if (m & bit) c = (z & bit) ? 0 : 1;
+    }
+    out[f * ldc + s] = c;
+  }
+}
+
+size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc) {
+  auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+  return r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2) + 2 * r16(ldt * 4) + 2 * r16(ldc);
+}
+
+template <int KM>
+int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo, int64_t hi, int check,
+                int* queue, RankSums rs, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  const size_t smem = walk_smem(val->ldo, val->ldt, lab->ldc);
+  if (smem > 226 * 1024) return ps_fail(PS_ERR_INVALID, "rank walk: sample count too large for shared memory");
+  auto kern = rank_mixed_walk_kernel<KM>;
+  PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RTH, smem));
+  per_sm = std::max(1, per_sm);
+  const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)ds->num_sms * per_sm);
+  ps_prof_begin("rank_mixed_walk", s);
+  kern<<<grid, RTH, smem, s>>>(val->d_order, val->ldo, val->d_tb, val->d_lastb, val->d_nextb, val->ldt,
+                               val->d_tied, val->d_len, codes, lab->ldc, lab->d_cat, lab->F, val->F, lo, hi,
+                               check, queue, rs, ds->d_err);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+}  // namespace
+
+int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode,
+                      double* stat, double* p, double* eff, cudaStream_t s) {
+  const int64_t Fc = lab->F, Fq = val->F;
+  if (lab->S != val->S) return ps_fail(PS_ERR_INVALID, "sample counts differ");
+  lo = std::max<int64_t>(0, lo);
+  hi = std::min<int64_t>(Fq, hi);
+  if (hi <= lo || (!stat && !p && !eff)) return PS_OK;
+  if (!val->has_presort) {
+    int rc = ps_presort_matrix(val, s);
+    if (rc) return rc;
+  }
+  ps_device_state* ds = ps_state();
+  const bool kw = test == PS_TEST_KRUSKAL;
+  const int kmax = kw ? std::max(1, lab->cmax) : 2;
+  int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 0;
+  if (KM == 0) return ps_fail(PS_ERR_INVALID, "kruskal: more than 16 label levels is not supported yet");
+  const int64_t npairs = Fc * Fq;
+  RankSums rs{KM, nullptr, nullptr, nullptr};
+  uint8_t* bcodes = nullptr;
+  int* queue = nullptr;
+  int2* exl = nullptr;
+  int* exc = nullptr;
+  const int excap = (int)std::min<int64_t>(Fc * (hi - lo), 1 << 20);
+  PS_CUDA(ps_alloc(&rs.cnt, (size_t)(npairs * KM), s));
+  PS_CUDA(ps_alloc(&rs.r2, (size_t)(npairs * KM), s));
+  PS_CUDA(ps_alloc(&rs.tie, (size_t)npairs, s));
+  PS_CUDA(ps_alloc(&queue, 1, s));
+  PS_CUDA(ps_alloc(&exl, (size_t)excap, s));
+  PS_CUDA(ps_alloc(&exc, 1, s));
+  PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+  PS_CUDA(cudaMemsetAsync(exc, 0, sizeof(int), s));
+  PS_CUDA(cudaMemsetAsync(rs.cnt, 0, sizeof(int32_t) * npairs * KM, s));
+  PS_CUDA(cudaMemsetAsync(rs.r2, 0, sizeof(unsigned long long) * npairs * KM, s));
+  const uint8_t* codes = lab->d_codes;
+  if (!kw) {
+    PS_CUDA(ps_alloc(&bcodes, (size_t)(Fc * lab->ldc), s));
+    binary_codes_kernel<<<(unsigned)Fc, 256, 0, s>>>(lab->d_mask, lab->d_zero, lab->W, lab->S, lab->ldc, bcodes);
+    PS_LAUNCHED();
+    codes = bcodes;
+  }
+  int rc = 0;
+  if (KM == 2) rc = launch_walk<2>(lab, val, codes, lo, hi, kw, queue, rs, s);
+  else if (KM == 8) rc = launch_walk<8>(lab, val, codes, lo, hi, kw, queue, rs, s);
+  else rc = launch_walk<16>(lab, val, codes, lo, hi, kw, queue, rs, s);
+  if (rc) return rc;
+  const int64_t total = Fc * (hi - lo);
+  const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
+  rank_mixed_finish_kernel<<<blocks, 128, 0, s>>>(test, rs, lab->d_cat, Fc, Fq, lo, hi, u_mode, stat, p, eff,
+                                                  exl, exc, excap, ds->d_err);
+  PS_LAUNCHED();
+  if (!kw && u_mode != PS_U_ASYMPTOTIC && p) {
+    mwu_exact_kernel<<<ds->num_sms, 32, 0, s>>>(rs, Fq, exl, exc, excap, p);
+    PS_LAUNCHED();
+  }
+  ps_free(rs.cnt, s);
+  ps_free(rs.r2, s);
+  ps_free(rs.tie, s);
+  ps_free(queue, s);
+  ps_free(exl, s);
+  ps_free(exc, s);
+  ps_free(bcodes, s);
+  return PS_OK;
+}

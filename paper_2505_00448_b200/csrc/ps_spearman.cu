@@ -45,52 +45,42 @@ struct PairSums {
   long long* sxy4;
 };
 
-__device__ __forceinline__ uint32_t pfx_at(const uint32_t* K, const uint32_t* P, uint32_t x) {
-  const uint32_t w = x >> 5, b = x & 31u;
-  return P[w] + __popc(K[w] & ((1u << b) - 1u));
+// All shared-memory regions are addressed as integer offsets into two views of
+// the one dynamic buffer, so every access compiles to LDS/STS (no generic
+// pointers, no per-access window conversion).
+extern __shared__ __align__(16) uint32_t sm32[];
+#define SM16 reinterpret_cast<uint16_t*>(sm32)
+
+// 32-bit shared-address accessors: one register holds the CTA window base,
+// so hot loops never re-derive it from a generic pointer.
+__device__ __forceinline__ uint32_t ld16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void st16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
+}
+__device__ __forceinline__ void st32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
-// exclusive block scan over word popcounts: P[w] = kept positions before word w
-__device__ void scan_words(uint32_t* K, uint32_t* P, int nwords, uint32_t* wsum) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (nwords + STH - 1) / STH;
-  const int w0 = threadIdx.x * per;
-  uint32_t local = 0;
-  for (int i = 0; i < per; ++i) {
-    const int w = w0 + i;
-    if (w < nwords) local += __popc(K[w]);
-  }
-  uint32_t x = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v = lane < SW ? wsum[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(PS_FULL, v, o);
-      if (lane >= o) v += y;
-    }
-    if (lane < SW) wsum[lane] = v;
-  }
-  __syncthreads();
-  uint32_t run = (warp > 0 ? wsum[warp - 1] : 0u) + x - local;
-  for (int i = 0; i < per; ++i) {
-    const int w = w0 + i;
-    if (w < nwords) {
-      P[w] = run;
-      run += __popc(K[w]);
-    }
-  }
-  if (threadIdx.x == 0) {
-    K[nwords] = 0u;
-    P[nwords] = wsum[SW - 1];
-  }
-  __syncthreads();
+// tie-group [start, end) of position p from shared tie tables (ps_ties.cuh)
+// (aT, aL, aN: byte addresses of the boundary words, lastb, nextb tables)
+__device__ __forceinline__ uint32_t tstart_a(uint32_t aT, uint32_t aL, uint32_t p) {
+  const uint32_t w = p >> 5, b = p & 31u;
+  const uint32_t m = ld32(aT + 4 * w) & (0xFFFFFFFFu >> (31u - b));
+  return m ? (w << 5) + 31u - __clz(m) : ld16(aL + 2 * (w - 1));
+}
+__device__ __forceinline__ uint32_t tend_a(uint32_t aT, uint32_t aN, uint32_t p) {
+  const uint32_t w = p >> 5, b = p & 31u;
+  const uint32_t m = b == 31u ? 0u : (ld32(aT + 4 * w) & (0xFFFFFFFFu << (b + 1u)));
+  return m ? (w << 5) + (uint32_t)__ffs(m) - 1u : ld16(aN + 2 * (w + 1));
 }
 
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
@@ -102,57 +92,100 @@ __device__ __forceinline__ unsigned long long sq_closed(unsigned long long n) {
   return 4ull * (n * (n + 1) * (2 * n + 1) / 6ull);
 }
 
-template <bool OGS>
-__global__ void __launch_bounds__(STH)
+// Shared-memory layout, in 32-bit words (all regions 16-byte aligned).
+struct WalkLayout {
+  uint32_t inv16, R16, tbh, lbh16, nbh16, par, K, Pl;
+  uint32_t og16[2], tbg[2], lbg16[2], nbg16[2];
+  uint32_t words;
+  __host__ __device__ WalkLayout(int64_t ldo, int64_t ldt, bool ogs, bool r2) {
+    uint32_t w = 0;
+    auto take = [&](int64_t bytes) {
+      const uint32_t o = w;
+      w += (uint32_t)(((bytes + 15) / 16) * 4);
+      return o;
+    };
+    inv16 = take(ldo * 2) * 2;
+    R16 = take(ldo * 2) * 2;
+    tbh = take(ldt * 4);
+    lbh16 = take(ldt * 2) * 2;
+    nbh16 = take(ldt * 2) * 2;
+    par = r2 ? 0 : take(ldt * 4);
+    K = take(ldt * 4);
+    Pl = take(ldt * 4);
+    for (int b = 0; b < 2; ++b) {
+      og16[b] = ogs ? take(ldo * 2) * 2 : 0;
+      tbg[b] = ogs ? take(ldt * 4) : 0;
+      lbg16[b] = ogs ? take(ldt * 2) * 2 : 0;
+      nbg16[b] = ogs ? take(ldt * 2) * 2 : 0;
+    }
+    words = w;
+  }
+};
+
+// After phase 1: turn per-warp totals into segment bases (exclusive scan in
+// registers: lane i of every warp holds the base of segment i).
+__device__ __forceinline__ void segment_bases(const uint32_t* wtot, uint32_t& segpre, uint32_t& ntot) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t v = lane < SW ? wtot[lane] : 0u;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  segpre = x - v;
+  ntot = __shfl_sync(PS_FULL, x, 31);
+}
+
+#ifdef PS_WALK_TIMING
+__device__ unsigned long long g_walk_cycles[16];
+#define WT(i)                                                         \
+  do {                                                                \
+    if (threadIdx.x == 0) {                                           \
+      const long long _t = clock64();                                 \
+      atomicAdd(&g_walk_cycles[i], (unsigned long long)(_t - _tw));   \
+      _tw = _t;                                                       \
+    }                                                                 \
+  } while (0)
+#else
+#define WT(i) \
+  do {        \
+  } while (0)
+#endif
+
+constexpr unsigned long long kClosed = ~0ull;  // "tie-free: use the closed form"
+
+template <bool OGS, bool R2>
+__global__ void __launch_bounds__(STH, 2)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
                      const int32_t* __restrict__ lens, int64_t F, int64_t lo, int64_t hi,
                      int* __restrict__ queue, PairSums out) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned char* cur = smem;
-  auto take = [&](size_t bytes) {
-    unsigned char* p = cur;
-    cur += (bytes + 15) & ~size_t(15);
-    return p;
-  };
-  uint16_t* inv_s = reinterpret_cast<uint16_t*>(take(ldo * 2));
-  uint16_t* R = reinterpret_cast<uint16_t*>(take(ldo * 2));
-  uint32_t* tbh = reinterpret_cast<uint32_t*>(take(ldt * 4));
-  uint16_t* lbh = reinterpret_cast<uint16_t*>(take(ldt * 2));
-  uint16_t* nbh = reinterpret_cast<uint16_t*>(take(ldt * 2));
-  uint32_t* par = reinterpret_cast<uint32_t*>(take(ldt * 4));
-  uint32_t* K = reinterpret_cast<uint32_t*>(take(ldt * 4));
-  uint32_t* P = reinterpret_cast<uint32_t*>(take(ldt * 4));
-  uint32_t* Kb = reinterpret_cast<uint32_t*>(take(ldt * 4));  // pass-B keep bits, set by pass A
-  uint16_t* og_s[2] = {nullptr, nullptr};
-  uint32_t* tbg_s[2] = {nullptr, nullptr};
-  uint16_t* lbg_s[2] = {nullptr, nullptr};
-  uint16_t* nbg_s[2] = {nullptr, nullptr};
-  if (OGS) {
-    for (int b = 0; b < 2; ++b) {
-      og_s[b] = reinterpret_cast<uint16_t*>(take(ldo * 2));
-      tbg_s[b] = reinterpret_cast<uint32_t*>(take(ldt * 4));
-      lbg_s[b] = reinterpret_cast<uint16_t*>(take(ldt * 2));
-      nbg_s[b] = reinterpret_cast<uint16_t*>(take(ldt * 2));
-    }
-  }
-  __shared__ uint32_t wsum[SW];
+  const WalkLayout L(ldo, ldt, OGS, R2);
+  __shared__ uint32_t wtot[SW];
   __shared__ unsigned long long red[SW][3];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm32);
+  const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + 4 * L.Pl;
+  const uint32_t aPar = sb + 4 * L.par;
+  const uint32_t aTbh = sb + 4 * L.tbh, aLbh = sb + 2 * L.lbh16, aNbh = sb + 2 * L.nbh16;
+  const uint32_t ltmask = lanemask_lt();
+  // absolute kept-prefix of position x: P[x/32] + popc(bits of K below x)
+  auto pfx = [&](uint32_t x) -> uint32_t {
+    const uint32_t w = x >> 5;
+    return ld32(aP + 4 * w) + __popc(ld32(aK + 4 * w) & ((1u << (x & 31u)) - 1u));
+  };
 
-  for (int64_t i = threadIdx.x; i < ldo; i += STH) R[i] = 0;
-  for (int64_t i = threadIdx.x; i < ldt; i += STH) {
-    par[i] = 0u;
-    Kb[i] = 0u;
-  }
+  for (int64_t i = threadIdx.x; i < ldo; i += STH) SM16[L.R16 + i] = 0;
+  if (!R2)
+    for (int64_t i = threadIdx.x; i < ldt; i += STH) sm32[L.par + i] = 0u;
 
-  // stage g's order (+ tie tables when tied) into buffer b
   auto prefetch = [&](int64_t g, int b) {
     const int ng = lens[g];
-    const int nch = (ng * 2 + 15) / 16;
-    const uint32_t so = (uint32_t)__cvta_generic_to_shared(og_s[b]);
+    const int nch = ((ng + 31) >> 5) * 4;  // whole 32-position words (sentinel padded)
+    const uint32_t so = sb + L.og16[b] * 2;
     const unsigned char* src = reinterpret_cast<const unsigned char*>(order + g * ldo);
     for (int c = threadIdx.x; c < nch; c += STH) cp16(so + c * 16, src + c * 16);
     if (tied[g]) {
@@ -160,13 +193,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       const unsigned char* t4 = reinterpret_cast<const unsigned char*>(tb + g * ldt);
       const unsigned char* l2 = reinterpret_cast<const unsigned char*>(lastb + g * ldt);
       const unsigned char* n2 = reinterpret_cast<const unsigned char*>(nextb + g * ldt);
-      const uint32_t st4 = (uint32_t)__cvta_generic_to_shared(tbg_s[b]);
-      const uint32_t sl2 = (uint32_t)__cvta_generic_to_shared(lbg_s[b]);
-      const uint32_t sn2 = (uint32_t)__cvta_generic_to_shared(nbg_s[b]);
-      for (int c = threadIdx.x; c < tch4; c += STH) cp16(st4 + c * 16, t4 + c * 16);
+      for (int c = threadIdx.x; c < tch4; c += STH) cp16(sb + L.tbg[b] * 4 + c * 16, t4 + c * 16);
       for (int c = threadIdx.x; c < tch2; c += STH) {
-        cp16(sl2 + c * 16, l2 + c * 16);
-        cp16(sn2 + c * 16, n2 + c * 16);
+        cp16(sb + L.lbg16[b] * 2 + c * 16, l2 + c * 16);
+        cp16(sb + L.nbg16[b] * 2 + c * 16, n2 + c * 16);
       }
     }
     asm volatile("cp.async.commit_group;");
@@ -184,109 +214,198 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
     const bool th = tied[h] != 0;
     {
       const uint4* src = reinterpret_cast<const uint4*>(inv + h * ldo);
-      uint4* dst = reinterpret_cast<uint4*>(inv_s);
+      uint4* dst = reinterpret_cast<uint4*>(&SM16[L.inv16]);
       for (int64_t i = threadIdx.x; i < ldo / 8; i += STH) dst[i] = src[i];
       if (th) {
         for (int64_t i = threadIdx.x; i < ldt; i += STH) {
-          tbh[i] = tb[h * ldt + i];
-          lbh[i] = lastb[h * ldt + i];
-          nbh[i] = nextb[h * ldt + i];
+          sm32[L.tbh + i] = tb[h * ldt + i];
+          SM16[L.lbh16 + i] = lastb[h * ldt + i];
+          SM16[L.nbh16 + i] = nextb[h * ldt + i];
         }
       }
     }
     const int64_t gmax = std::min<int64_t>(h, hi - 1);
     if (OGS && lo <= gmax) prefetch(lo, 0);
     __syncthreads();
+    const int nwb = (nh + 31) >> 5;
+    const int Lb = (nwb + SW - 1) / SW;
+    const int b0 = min(nwb, warp * Lb), b1 = min(nwb, b0 + Lb);
+#ifdef PS_WALK_TIMING
+    long long _tw = clock64();
+#endif
+    int ng_next = lo <= gmax ? lens[lo] : 0;
+    bool tg_next = lo <= gmax ? tied[lo] != 0 : false;
     for (int64_t g = lo; g <= gmax; ++g) {
       const int buf = (int)((g - lo) & 1);
-      const int ng = lens[g];
-      const bool tg = tied[g] != 0;
-      const uint16_t* og;
-      const uint32_t* tbg;
-      const uint16_t *lbg, *nbg;
+      const int ng = ng_next;
+      const bool tg = tg_next;
+      if (g + 1 <= gmax) {
+        ng_next = lens[g + 1];
+        tg_next = tied[g + 1] != 0;
+      }
       if (OGS) {
         if (g + 1 <= gmax) prefetch(g + 1, buf ^ 1);
         else asm volatile("cp.async.commit_group;");
         asm volatile("cp.async.wait_group 1;");
         __syncthreads();
-        og = og_s[buf];
-        tbg = tbg_s[buf];
-        lbg = lbg_s[buf];
-        nbg = nbg_s[buf];
-      } else {
-        og = order + g * ldo;
-        tbg = tb + g * ldt;
-        lbg = lastb + g * ldt;
-        nbg = nextb + g * ldt;
       }
+      WT(0);
+      const uint32_t aOg = sb + 2 * L.og16[buf];
+      const uint32_t aTbg = sb + 4 * L.tbg[buf], aLbg = sb + 2 * L.lbg16[buf], aNbg = sb + 2 * L.nbg16[buf];
+      const uint16_t* og_g = order + g * ldo;
       // ---------------- pass A, phase 1: keep bits over g's order ----------
       const int nwa = (ng + 31) >> 5;
+      const int La = (nwa + SW - 1) / SW;
+      const int a0 = min(nwa, warp * La), a1 = min(nwa, a0 + La);
+      {
+        // q = inv_h[order_g[p]]; with g's order staged in shared memory the
+        // gathered q overwrites it in place, so phase 2 reads it sequentially
+        uint32_t cnt = 0;
 #pragma unroll 4
-      for (int word = warp; word < nwa; word += SW) {
-        const int p = word * 32 + lane;
-        const uint32_t q = p < ng ? (uint32_t)inv_s[og[p]] : 0xFFFFu;
-        const uint32_t B = __ballot_sync(PS_FULL, q != 0xFFFFu);
-        if (lane == 0) K[word] = B;
+        for (int word = a0; word < a1; ++word) {
+          const uint32_t p = (uint32_t)(word * 32 + lane);
+          const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
+          const uint32_t q = ld16(aInv + 2 * s);
+          if (OGS) st16(aOg + 2 * p, q);
+          const uint32_t B = __ballot_sync(PS_FULL, q != 0xFFFFu);
+          if (lane == 0) {
+            st32(aK + 4 * word, B);
+            st32(aP + 4 * word, cnt);
+          }
+          cnt += __popc(B);
+        }
+        if (lane == 0) wtot[warp] = cnt;
       }
       __syncthreads();
-      scan_words(K, P, nwa, wsum);
-      const uint32_t n = P[nwa];
-      // ---------------- pass A, phase 2: ranks -> R[q], keep bits of B ------
+      WT(1);
+      uint32_t abase, n;
+      {
+        uint32_t segpre;
+        segment_bases(wtot, segpre, n);
+        abase = __shfl_sync(PS_FULL, segpre, warp);
+        if (tg) {  // absolute prefixes for arbitrary-position lookups
+          for (int w = a0 + lane; w < a1; w += 32) st32(aP + 4 * w, ld32(aP + 4 * w) + abase);
+          if (threadIdx.x == 0) {
+            st32(aK + 4 * nwa, 0u);
+            st32(aP + 4 * nwa, n);
+          }
+          __syncthreads();
+        }
+      }
+      WT(2);
+      // ---------------- pass A, phase 2: ranks -> R[q] -------------------
+      auto q_at = [&](uint32_t p) -> uint32_t { return OGS ? ld16(aOg + 2 * p) : ld16(aInv + 2 * (uint32_t)og_g[p]); };
       unsigned long long sa2 = 0;
       if (!tg) {
-        // tie-free: 2r = 2 (Pfx(p) + 1), always even
 #pragma unroll 4
-        for (int word = warp; word < nwa; word += SW) {
-          const int p = word * 32 + lane;
-          const uint32_t kw = K[word];
-          if ((kw >> lane) & 1u) {
-            const uint32_t q = inv_s[og[p]];
-            R[q] = (uint16_t)(P[word] + __popc(kw & lanemask_lt()) + 1u);
-            atomicOr(&Kb[q >> 5], 1u << (q & 31u));
-          }
+        for (int word = a0; word < a1; ++word) {
+          const uint32_t kw = ld32(aK + 4 * word);
+          const uint32_t r = abase + ld32(aP + 4 * word) + __popc(kw & ltmask) + 1u;
+          const uint32_t q = q_at((uint32_t)(word * 32 + lane));
+          if ((kw >> lane) & 1u) st16(aR + 2 * q, R2 ? 2u * r : r);
         }
       } else {
-        for (int word = warp; word < nwa; word += SW) {
+        const uint32_t* tbgg = tb + g * ldt;
+        const uint16_t* lbgg = lastb + g * ldt;
+        const uint16_t* nbgg = nextb + g * ldt;
+        for (int word = a0; word < a1; ++word) {
+          const uint32_t kw = ld32(aK + 4 * word);
           const uint32_t p = (uint32_t)(word * 32 + lane);
-          const uint32_t kw = K[word];
           if ((kw >> lane) & 1u) {
-            const uint32_t q = inv_s[og[p]];
-            const uint32_t r2 =
-                pfx_at(K, P, tie_start(tbg, lbg, p)) + pfx_at(K, P, tie_end(tbg, nbg, p)) + 1u;
+            uint32_t xs, xe;
+            if (OGS) {
+              xs = tstart_a(aTbg, aLbg, p);
+              xe = tend_a(aTbg, aNbg, p);
+            } else {
+              xs = tie_start(tbgg, lbgg, p);
+              xe = tie_end(tbgg, nbgg, p);
+            }
+            const uint32_t r2 = pfx(xs) + pfx(xe) + 1u;
+            const uint32_t q = q_at(p);
             sa2 += (unsigned long long)r2 * r2;
-            R[q] = (uint16_t)(r2 >> 1);
-            atomicOr(&Kb[q >> 5], 1u << (q & 31u));
-            if (r2 & 1u) atomicOr(&par[q >> 5], 1u << (q & 31u));
+            if (R2) {
+              st16(aR + 2 * q, r2);
+            } else {
+              st16(aR + 2 * q, r2 >> 1);
+              if (r2 & 1u) atomicOr(&sm32[L.par + (q >> 5)], 1u << (q & 31u));
+            }
           }
         }
       }
       __syncthreads();
-      // ---------------- pass B: h's order, keep bits already set by pass A ---
-      const int nwb = (nh + 31) >> 5;
-      scan_words(Kb, P, nwb, wsum);
+      WT(3);
+      // ---------------- pass B, phase 1: keep = R != 0 over h's order ------
+      {
+        uint32_t cnt = 0;
+#pragma unroll 4
+        for (int word = b0; word < b1; ++word) {
+          const bool keep = ld16(aR + 2 * (uint32_t)(word * 32 + lane)) != 0u;
+          const uint32_t B = __ballot_sync(PS_FULL, keep);
+          if (lane == 0) {
+            st32(aK + 4 * word, B);
+            st32(aP + 4 * word, cnt);
+          }
+          cnt += __popc(B);
+        }
+        if (lane == 0) wtot[warp] = cnt;
+      }
+      __syncthreads();
+      WT(4);
+      uint32_t bbase;
+      {
+        uint32_t segpre, tot;
+        segment_bases(wtot, segpre, tot);
+        bbase = __shfl_sync(PS_FULL, segpre, warp);
+        if (th) {
+          for (int w = b0 + lane; w < b1; w += 32) st32(aP + 4 * w, ld32(aP + 4 * w) + bbase);
+          if (threadIdx.x == 0) {
+            st32(aK + 4 * nwb, 0u);
+            st32(aP + 4 * nwb, tot);
+          }
+          __syncthreads();
+        }
+      }
+      // ---------------- pass B, phase 2: accumulate, clear R ---------------
       unsigned long long sab = 0, sbb = 0;
       if (!th) {
 #pragma unroll 4
-        for (int word = warp; word < nwb; word += SW) {
-          const uint32_t kw = Kb[word];
+        for (int word = b0; word < b1; ++word) {
+          const uint32_t kw = ld32(aK + 4 * word);
           const uint32_t q = (uint32_t)(word * 32 + lane);
-          const uint32_t r2g = 2u * (uint32_t)R[q] + (tg ? ((par[word] >> lane) & 1u) : 0u);
-          const uint32_t r2h = 2u * (P[word] + __popc(kw & lanemask_lt()) + 1u);
-          if ((kw >> lane) & 1u) sab += (unsigned long long)r2g * r2h;
+          const uint32_t v = ld16(aR + 2 * q);
+          uint32_t r2g = R2 ? v : 2u * v;
+          if (!R2 && tg) r2g += (ld32(aPar + 4 * word) >> lane) & 1u;
+          const uint32_t rh = bbase + ld32(aP + 4 * word) + __popc(kw & ltmask) + 1u;
+          if ((kw >> lane) & 1u) {
+            sab += (unsigned long long)r2g * rh;
+            st16(aR + 2 * q, 0u);
+          }
+          if (!R2 && tg) {
+            __syncwarp();
+            if (lane == 0) st32(aPar + 4 * word, 0u);
+          }
         }
+        sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
       } else {
-        for (int word = warp; word < nwb; word += SW) {
-          const uint32_t kw = Kb[word];
+        for (int word = b0; word < b1; ++word) {
+          const uint32_t kw = ld32(aK + 4 * word);
           const uint32_t q = (uint32_t)(word * 32 + lane);
           if ((kw >> lane) & 1u) {
-            const uint32_t r2g = 2u * (uint32_t)R[q] + (tg ? ((par[word] >> lane) & 1u) : 0u);
-            const uint32_t r2h =
-                pfx_at(Kb, P, tie_start(tbh, lbh, q)) + pfx_at(Kb, P, tie_end(tbh, nbh, q)) + 1u;
-            sbb += (unsigned long long)r2h * r2h;
+            const uint32_t v = ld16(aR + 2 * q);
+            uint32_t r2g = R2 ? v : 2u * v;
+            if (!R2 && tg) r2g += (ld32(aPar + 4 * word) >> lane) & 1u;
+            const uint32_t r2h = pfx(tstart_a(aTbh, aLbh, q)) + pfx(tend_a(aTbh, aNbh, q)) + 1u;
             sab += (unsigned long long)r2g * r2h;
+            sbb += (unsigned long long)r2h * r2h;
+            st16(aR + 2 * q, 0u);
+          }
+          if (!R2 && tg) {
+            __syncwarp();
+            if (lane == 0) st32(aPar + 4 * word, 0u);
           }
         }
       }
+      WT(5);
       // ---------------- reduce and store the exact sums ---------------------
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -300,28 +419,20 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         red[warp][2] = sbb;
       }
       __syncthreads();
-      for (int w = threadIdx.x; w < nwb; w += STH) {
-        Kb[w] = 0u;
-        if (tg) par[w] = 0u;
-      }
-      if (threadIdx.x == 0) {
-        unsigned long long a = 0, b = 0, c = 0;
-        for (int w = 0; w < SW; ++w) {
-          a += red[w][0];
-          b += red[w][1];
-          c += red[w][2];
-        }
-        const unsigned long long un = n;
-        if (!tg) a = sq_closed(un);
-        if (!th) c = sq_closed(un);
-        const long long nn = (long long)n;
-        const long long base = nn * (nn + 1) * (nn + 1);
+      if (threadIdx.x < 3) {
+        unsigned long long v = 0;
+        for (int w = 0; w < SW; ++w) v += red[w][threadIdx.x];
         const int64_t cell = g * F + h;
-        out.n[cell] = nn;
-        out.sxx4[cell] = (long long)a - base;
-        out.syy4[cell] = (long long)c - base;
-        out.sxy4[cell] = (long long)b - base;
+        if (threadIdx.x == 0) {
+          out.sxx4[cell] = (long long)(tg ? v : kClosed);
+          out.n[cell] = (long long)n;
+        } else if (threadIdx.x == 1) {
+          out.sxy4[cell] = (long long)v;
+        } else {
+          out.syy4[cell] = (long long)(th ? v : kClosed);
+        }
       }
+      WT(6);
     }
     if (OGS) asm volatile("cp.async.wait_group 0;");
   }
@@ -347,10 +458,19 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
     const long long n = in.n[cell];
     double rho = PS_NAN, p = PS_NAN;
     if (n > 1) {
+      // raw sums of (2r)(2r) -> exact 4 x centred sums (rank totals are
+      // preserved by tie averaging); tie-free walks use the closed form
+      const unsigned long long un = (unsigned long long)n;
+      const long long base = n * (n + 1) * (n + 1);
+      const unsigned long long ra = (unsigned long long)in.sxx4[cell];
+      const unsigned long long rc = (unsigned long long)in.syy4[cell];
+      const long long a4 = (long long)(ra == kClosed ? sq_closed(un) : ra) - base;
+      const long long c4 = (long long)(rc == kClosed ? sq_closed(un) : rc) - base;
+      const long long b4 = in.sxy4[cell] - base;
       // exact quarter-integers, identical to the reference's fp64 sums
-      const double sxx = (double)in.sxx4[cell] * 0.25;
-      const double syy = (double)in.syy4[cell] * 0.25;
-      const double sxy = (double)in.sxy4[cell] * 0.25;
+      const double sxx = (double)a4 * 0.25;
+      const double syy = (double)c4 * 0.25;
+      const double sxy = (double)b4 * 0.25;
       if (sxx > 0.0 && syy > 0.0) {
         rho = sxy / sqrt(sxx * syy);
         if (rho > 1.0) rho = 1.0;
@@ -373,12 +493,7 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
   }
 }
 
-size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs) {
-  auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
-  size_t b = 2 * r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2) + 4 * r16(ldt * 4);
-  if (ogs) b += 2 * (r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2));
-  return b;
-}
+size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs, bool r2) { return (size_t)WalkLayout(ldo, ldt, ogs, r2).words * 4; }
 
 }  // namespace
 
@@ -394,19 +509,6 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   }
   ps_device_state* ds = ps_state();
   const size_t limit = 227 * 1024 - 1024;
-  size_t smem = walk_smem(a->ldo, a->ldt, true);
-  const bool ogs = smem <= limit;
-  if (!ogs) smem = walk_smem(a->ldo, a->ldt, false);
-  if (smem > limit)
-    return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
-  auto kern = ogs ? spearman_walk_kernel<true> : spearman_walk_kernel<false>;
-  PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, STH, smem));
-  per_sm = std::max(1, per_sm);
-  const int64_t items = F - lo;
-  const int grid = (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
-
   PairSums ps{};
   int* queue = nullptr;
   PS_CUDA(ps_alloc(&ps.n, (size_t)(F * F), s));
@@ -415,11 +517,27 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   PS_CUDA(ps_alloc(&ps.sxy4, (size_t)(F * F), s));
   PS_CUDA(ps_alloc(&queue, 1, s));
   PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+  {
+  const bool r2 = a->S <= 32767;  // 2r fits 16 bits: no parity bits
+  size_t smem = walk_smem(a->ldo, a->ldt, true, r2);
+  const bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
+  if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2);
+  if (smem > limit)
+    return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
+  auto kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
+                  : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
+  PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, STH, smem));
+  per_sm = std::max(1, per_sm);
+  const int64_t items = F - lo;
+  const int grid = (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
   ps_prof_begin("spearman_walk", s);
   kern<<<grid, STH, smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
                                a->d_tied, a->d_len, F, lo, hi, queue, ps);
   ps_prof_end(s);
   PS_LAUNCHED();
+  }
   const int64_t total = (hi - lo) * F;
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
   spearman_finish_kernel<<<blocks, 128, 0, s>>>(ps, F, lo, hi, stat, p, rho, ds->d_err);
@@ -431,3 +549,10 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   ps_free(queue, s);
   return PS_OK;
 }
+
+#ifdef PS_WALK_TIMING
+extern "C" int ps_debug_walk_cycles(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_walk_cycles, sizeof(unsigned long long) * 16);
+  return 0;
+}
+#endif

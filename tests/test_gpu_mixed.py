@@ -97,3 +97,98 @@ def test_anova_label_out_of_range():
                         category_counts=np.array([2]), present=good.present)
     with pytest.raises(ps.LabelOutOfRange, match="category range"):
         ps.run(ps.TestRequest("anova", ("stat",)), bad, ps.make_matrix(val, "continuous"))
+
+
+@pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
+@pytest.mark.parametrize("c", [2, 3, 8, 13])
+def test_kruskal_matches_oracle(oracle, na, c):
+    a, b = _inputs("kruskal", 12, 60, 400, na, seed=int(na * 100) + c, c=c)
+    req = ps.TestRequest("kruskal", ("stat", "p", "eta2"))
+    res = ps.run(req, a, b)
+    ref = oracle.oracle_run(req, a, b)
+    for name in ("stat", "p", "eta2"):
+        assert same_nan(res[name], ref[name]), name
+    assert bitwise_equal(res["stat"], ref["stat"])
+    assert bitwise_equal(res["eta2"], ref["eta2"])
+    assert p_close(res["p"], ref["p"])
+
+
+@pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
+@pytest.mark.parametrize("mode", ["auto", "asymptotic"])
+def test_mwu_matches_oracle(oracle, na, mode):
+    a, b = _inputs("mwu", 12, 60, 400, na, seed=int(na * 100) + 17)
+    req = ps.TestRequest("mwu", ("stat", "p", "r"), u_mode=mode)
+    res = ps.run(req, a, b)
+    ref = oracle.oracle_run(req, a, b)
+    for name in ("stat", "p", "r"):
+        assert same_nan(res[name], ref[name]), name
+    assert bitwise_equal(res["stat"], ref["stat"])
+    assert bitwise_equal(res["r"], ref["r"])
+    assert p_close(res["p"], ref["p"])
+
+
+def test_rank_tests_with_ties(oracle):
+    rng = np.random.default_rng(8)
+    S = 3000
+    lab = rng.integers(0, 4, size=(9, S)).astype(float)
+    lab[rng.random(lab.shape) < 0.1] = np.nan
+    val = np.round(rng.normal(size=(20, S)), 1)   # heavy ties
+    val[3] = 1.0                                    # all tied -> NaN rows
+    val[rng.random(val.shape) < 0.15] = np.nan
+    a = ps.make_matrix(lab, "categorical")
+    b = ps.make_matrix(val, "continuous")
+    req = ps.TestRequest("kruskal", ("stat", "p", "eta2"))
+    res, ref = ps.run(req, a, b), oracle.oracle_run(req, a, b)
+    assert bitwise_equal(res["stat"], ref["stat"]) and same_nan(res["p"], ref["p"])
+    assert p_close(res["p"], ref["p"])
+    dich = ps.make_matrix(np.where(np.isnan(lab), np.nan, (lab > 1).astype(float)), "dichotomous")
+    req = ps.TestRequest("mwu", ("stat", "p", "r"))
+    res, ref = ps.run(req, dich, b), oracle.oracle_run(req, dich, b)
+    assert bitwise_equal(res["stat"], ref["stat"]) and bitwise_equal(res["r"], ref["r"])
+    assert same_nan(res["p"], ref["p"]) and p_close(res["p"], ref["p"])
+
+
+def test_mwu_exact_small_groups(oracle):
+    """Exact U distribution (mixed.py:231-247) on tie-free small groups."""
+    rng = np.random.default_rng(12)
+    S = 40
+    lab = np.zeros((6, S))
+    for i, n0 in enumerate([1, 3, 5, 7, 7, 20]):
+        lab[i, rng.permutation(S)[:n0]] = 1.0
+    val = rng.permutation(S * 3)[: S * 4].reshape(1, -1)[:, :S].astype(float)
+    val = np.vstack([val, rng.normal(size=(3, S))])
+    a = ps.make_matrix(lab, "dichotomous")
+    b = ps.make_matrix(val, "continuous")
+    for mode in ("auto", "exact"):
+        req = ps.TestRequest("mwu", ("stat", "p", "r"), u_mode=mode)
+        res, ref = ps.run(req, a, b), oracle.oracle_run(req, a, b)
+        assert bitwise_equal(res["stat"], ref["stat"])
+        # exact p-values are ratios of exact integer counts: bit-exact; in
+        # auto mode the larger groups take the normal approximation (erfc ulps)
+        if mode == "exact":
+            assert bitwise_equal(res["p"], ref["p"])
+        else:
+            assert p_close(res["p"], ref["p"])
+
+
+def test_mwu_exact_errors():
+    lab = np.array([[0, 0, 1, 1, 0, 1.0]])
+    tied = np.array([[1.0, 1.0, 2.0, 3.0, 4.0, 5.0]])
+    a = ps.make_matrix(lab, "dichotomous")
+    with pytest.raises(ps.ExactModeWithTies, match="tie-free"):
+        ps.run(ps.TestRequest("mwu", ("p",), u_mode="exact"), a, ps.make_matrix(tied, "continuous"))
+    big_lab = (np.arange(70) % 2).astype(float).reshape(1, -1)
+    big_val = np.arange(70, dtype=float).reshape(1, -1)
+    with pytest.raises(ps.TableTooLarge, match="cap"):
+        ps.run(ps.TestRequest("mwu", ("p",), u_mode="exact"), ps.make_matrix(big_lab, "dichotomous"),
+               ps.make_matrix(big_val, "continuous"))
+
+
+def test_kruskal_config4_slice(oracle):
+    c = workloads.config(4, scale=0.05)
+    a = ps.make_matrix(c["a"], "categorical", na_sentinel=workloads.SENTINEL)
+    b = ps.make_matrix(c["b"], "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("kruskal", ("stat", "p", "eta2", "p_bh"))
+    res, ref = ps.run(req, a, b), oracle.oracle_run(req, a, b)
+    assert bitwise_equal(res["stat"], ref["stat"])
+    assert p_close(res["p"], ref["p"]) and same_nan(res["p_bh"], ref["p_bh"])

@@ -46,5 +46,25 @@ def main():
     print("ok", test, shape, float(np.nanmean(outs[0].cpu().numpy())))
 
 
+
+
+def dump_walk_cycles():
+    import ctypes
+    import os
+
+    from paper_2505_00448_b200 import _lib
+
+    lib = _lib.load()
+    if not os.environ.get("PS_LIB") or not hasattr(lib, "ps_debug_walk_cycles"):
+        return
+    buf = (ctypes.c_ulonglong * 16)()
+    lib.ps_debug_walk_cycles(buf)
+    names = ["wait+prefetch", "passA phase1", "scanA", "passA phase2", "scanB", "passB", "reduce+final"]
+    tot = sum(buf[i] for i in range(7))
+    for i, n in enumerate(names):
+        print(f"{n:16s} {buf[i]:16d} {100.0 * buf[i] / max(tot, 1):6.1f}%")
+
+
 if __name__ == "__main__":
     main()
+    dump_walk_cycles()
