@@ -145,6 +145,12 @@ int ps_adjust_family_device(const double* p, int64_t n, int method, double* out,
  * since the last check (LabelOutOfRange, NonConvergence, ...). */
 int ps_sync(void* stream);
 
+/* Device special functions on a host batch (golden-grid tests): which =
+ * 0 ln_gamma(x), 1 reg_inc_beta(x,a,b), 2 reg_inc_gamma_upper(a,x),
+ * 3 normal_sf(z), 4 t_sf(t,dof), 5 chi2_sf(x,dof), 6 f_sf(f,d1,d2),
+ * 7 beta_sym_sf(r,a) -- specfun.py:41-314.  args is n x nargs row-major. */
+int ps_specfun_eval(int which, const double* args, int64_t n, int nargs, double* out);
+
 /* numpy-identical BY harmonic factor c(m) (exposed for tests). */
 double ps_by_factor(int64_t m);
 

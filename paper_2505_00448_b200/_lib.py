@@ -54,6 +54,7 @@ EXPORTED = (
     "ps_adjust_family_device",
     "ps_sync",
     "ps_by_factor",
+    "ps_specfun_eval",
     "ps_run",
     "ps_kernel_launches",
     "ps_reset_kernel_launches",
@@ -107,6 +108,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.ps_adjust_family_device.argtypes = [dp, i64, i32, dp, vp]
     lib.ps_sync.argtypes = [vp]
     lib.ps_by_factor.argtypes = [i64]
+    lib.ps_specfun_eval.argtypes = [i32, dp, i64, i32, dp]
     lib.ps_by_factor.restype = ctypes.c_double
     lib.ps_run.argtypes = [
         i32,
@@ -188,3 +190,24 @@ def describe(mat, values: np.ndarray | None = None) -> tuple[MatrixDesc, tuple]:
 
 def by_factor(m: int) -> float:
     return float(load().ps_by_factor(int(m)))
+
+
+SPECFUN_CODES = {
+    "ln_gamma": (0, 1),
+    "reg_inc_beta": (1, 3),
+    "reg_inc_gamma_upper": (2, 2),
+    "normal_sf": (3, 1),
+    "t_sf": (4, 2),
+    "chi2_sf": (5, 2),
+    "f_sf": (6, 3),
+    "beta_sym_sf": (7, 2),
+}
+
+
+def specfun(name: str, args) -> np.ndarray:
+    """Evaluate a device special function on a batch (tests / diagnostics)."""
+    which, nargs = SPECFUN_CODES[name]
+    a = np.ascontiguousarray(np.asarray(args, dtype=np.float64).reshape(-1, nargs))
+    out = np.empty(a.shape[0])
+    check(load().ps_specfun_eval(which, a.ctypes.data, a.shape[0], nargs, out.ctypes.data))
+    return out
