@@ -255,6 +255,205 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
   }
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory presort (S <= 20480): one CTA per feature holds its keys in
+// registers (warp-striped: warp w, item i, lane l <-> position
+// w*32*ITEMS + i*32 + l, so (i, lane) order IS sequence order) and runs a
+// stable LSD radix sort whose scatter goes through one shared exchange buffer
+// (10 B per element).  Digit passes whose byte is constant are skipped (AND ==
+// OR over all keys).  Global traffic: values + mask in, order/inv/tie tables
+// out -- no per-pass HBM round trips.
+// ---------------------------------------------------------------------------
+constexpr int QT = 512;
+constexpr int QW = QT / 32;
+
+template <int ITEMS>
+__global__ void __launch_bounds__(QT, 1)
+presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask, int64_t W,
+                    int64_t S, uint16_t* __restrict__ order, uint16_t* __restrict__ inv, int64_t ldo,
+                    uint32_t* __restrict__ tb, uint16_t* __restrict__ lastb, uint16_t* __restrict__ nextb,
+                    int64_t ldt, uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
+  constexpr int NMAX = QT * ITEMS;
+  extern __shared__ __align__(16) unsigned char qsm[];
+  uint64_t* skey = reinterpret_cast<uint64_t*>(qsm);
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(qsm + (size_t)NMAX * 8);
+  __shared__ uint16_t wcnt[QW][256];
+  __shared__ int warp_buf[QW];
+  __shared__ unsigned long long s_and, s_or;
+  __shared__ int s_any_tie;
+  const int64_t f = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* row = vals + f * ld;
+  const uint32_t* mrow = mask + f * W;
+
+  // 1. stable compaction of present entries (sample order) into smem
+  if (threadIdx.x == 0) {
+    s_and = ~0ull;
+    s_or = 0ull;
+    s_any_tie = 0;
+  }
+  int n = 0;
+  for (int64_t base = 0; base < S; base += QT) {
+    const int64_t s = base + threadIdx.x;
+    const bool pres = s < S && ((mrow[s >> 5] >> (s & 31)) & 1u);
+    int tot;
+    const int pos = block_excl_scan(pres ? 1 : 0, warp_buf, tot);
+    if (pres) {
+      skey[n + pos] = sort_key(row[s]);
+      sidx[n + pos] = (uint16_t)s;
+    }
+    n += tot;
+  }
+  __syncthreads();
+  // 2. registers (warp-striped), AND/OR of keys for pass skipping
+  uint64_t key[ITEMS];
+  uint32_t idx[ITEMS];
+  unsigned long long a = ~0ull, o = 0ull;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const int p = warp * 32 * ITEMS + i * 32 + lane;
+    key[i] = p < n ? skey[p] : ~0ull;  // padding sorts last
+    idx[i] = p < n ? sidx[p] : 0xFFFFu;
+    if (p < n) {
+      a &= key[i];
+      o |= key[i];
+    }
+  }
+#pragma unroll
+  for (int sft = 16; sft > 0; sft >>= 1) {
+    a &= __shfl_xor_sync(PS_FULL, a, sft);
+    o |= __shfl_xor_sync(PS_FULL, o, sft);
+  }
+  if (lane == 0) {
+    atomicAnd(&s_and, a);
+    atomicOr(&s_or, o);
+  }
+  __syncthreads();
+  const unsigned long long diff = s_and ^ s_or;
+  // 3. LSD passes over non-constant bytes
+  for (int d = 0; d < 8; ++d) {
+    const int shift = 8 * d;
+    if (((diff >> shift) & 0xffull) == 0 || n <= 1) continue;
+    for (int i = threadIdx.x; i < QW * 256; i += QT) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    uint32_t loc[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xff);
+      const uint32_t peers = __match_any_sync(PS_FULL, dg);
+      const uint32_t base = wcnt[warp][dg];
+      __syncwarp();
+      loc[i] = base + __popc(peers & lanemask_lt());
+      if ((peers >> lane) == 1u) wcnt[warp][dg] = (uint16_t)(base + __popc(peers));
+      __syncwarp();
+    }
+    __syncthreads();
+    // digit totals -> bucket starts -> per-warp starts (digit-major, warp order)
+    if (threadIdx.x < 256) {
+      uint32_t tot = 0;
+      for (int w = 0; w < QW; ++w) tot += wcnt[w][threadIdx.x];
+      // exclusive scan of totals across the 256 digits (8 warps)
+      uint32_t x = tot;
+#pragma unroll
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const uint32_t y = __shfl_up_sync(PS_FULL, x, sft);
+        if (lane >= sft) x += y;
+      }
+      if (lane == 31) warp_buf[warp] = (int)x;
+      // (warps 0..7 participate; others skip)
+      asm volatile("bar.sync 1, 256;");
+      uint32_t before = 0;
+      for (int w = 0; w < warp; ++w) before += (uint32_t)warp_buf[w];
+      uint32_t run = before + x - tot;
+      for (int w = 0; w < QW; ++w) {
+        const uint32_t c = wcnt[w][threadIdx.x];
+        wcnt[w][threadIdx.x] = (uint16_t)0;  // reused below as start offsets (fits: < 2^16)
+        wcnt[w][threadIdx.x] = (uint16_t)run;
+        run += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xff);
+      const uint32_t dst = (uint32_t)wcnt[warp][dg] + loc[i];
+      skey[dst] = key[i];
+      sidx[dst] = (uint16_t)idx[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int p = warp * 32 * ITEMS + i * 32 + lane;
+      key[i] = skey[p];
+      idx[i] = sidx[p];
+    }
+    __syncthreads();
+  }
+  // sorted keys are in smem (written by the compaction or the last pass)
+  // 4. outputs
+  uint16_t* ord = order + f * ldo;
+  uint16_t* iv = inv + f * ldo;
+  for (int64_t s = threadIdx.x; s < ldo; s += QT) iv[s] = 0xFFFF;
+  __syncthreads();
+  for (int p = threadIdx.x; p < (int)ldo; p += QT) ord[p] = p < n ? sidx[p] : (uint16_t)S;
+  for (int p = threadIdx.x; p < n; p += QT) iv[sidx[p]] = (uint16_t)p;
+  uint32_t* tbr = tb + f * ldt;
+  uint16_t* lbr = lastb + f * ldt;
+  uint16_t* nbr = nextb + f * ldt;
+  const int nw = (int)ldt;
+  for (int w = warp; w < nw; w += QW) {
+    const int p = w * 32 + lane;
+    bool bnd;
+    if (p < n) {
+      const uint64_t k = skey[p];
+      bnd = p == 0 || k != skey[p - 1] || key_is_nan(k);
+      if (!bnd) s_any_tie = 1;
+    } else {
+      bnd = p == n;
+    }
+    const uint32_t word = __ballot_sync(PS_FULL, bnd);
+    if (lane == 0) tbr[w] = word;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int w = w0 + lane;
+      const uint32_t word = w < nw ? tbr[w] : 0u;
+      int x = word ? w * 32 + 31 - __clz(word) : -1;
+#pragma unroll
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const int y = __shfl_up_sync(PS_FULL, x, sft);
+        if (lane >= sft) x = max(x, y);
+      }
+      x = max(x, carry);
+      if (w < nw) lbr[w] = (uint16_t)x;
+      carry = __shfl_sync(PS_FULL, x, 31);
+    }
+  } else if (warp == 1) {
+    int carry = 0xFFFF;
+    const int last0 = ((nw - 1) / 32) * 32;
+    for (int w0 = last0; w0 >= 0; w0 -= 32) {
+      const int w = w0 + lane;
+      const uint32_t word = w < nw ? tbr[w] : 0u;
+      int x = word ? w * 32 + __ffs(word) - 1 : 0xFFFF;
+#pragma unroll
+      for (int sft = 1; sft < 32; sft <<= 1) {
+        const int y = __shfl_down_sync(PS_FULL, x, sft);
+        if (lane + sft < 32) x = min(x, y);
+      }
+      x = min(x, carry);
+      if (w < nw) nbr[w] = (uint16_t)x;
+      carry = __shfl_sync(PS_FULL, x, 0);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tied[f] = s_any_tie ? 1 : 0;
+    lens[f] = n;
+  }
+}
+
 }  // namespace
 
 int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
@@ -277,10 +476,28 @@ int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
-  presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,
-                                               m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
-                                               m->d_nextb, m->ldt, m->d_tied, m->d_len);
-  PS_LAUNCHED();
+  const int items = (int)ps_ceil_div(m->S, QT);
+  auto smem_path = [&](auto kern, int it) -> int {
+    const size_t smem = (size_t)QT * it * 10;
+    PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)m->F, QT, smem, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, m->d_order, m->d_inv, m->ldo,
+                                          m->d_tb, m->d_lastb, m->d_nextb, m->ldt, m->d_tied, m->d_len);
+    PS_LAUNCHED();
+    return PS_OK;
+  };
+  int rc = -1;
+  if (items <= 8) rc = smem_path(presort_smem_kernel<8>, 8);
+  else if (items <= 16) rc = smem_path(presort_smem_kernel<16>, 16);
+  else if (items <= 24) rc = smem_path(presort_smem_kernel<24>, 24);
+  else if (items <= 32) rc = smem_path(presort_smem_kernel<32>, 32);
+  else if (items <= 40) rc = smem_path(presort_smem_kernel<40>, 40);
+  if (rc > 0) return rc;
+  if (rc < 0) {
+    presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,
+                                                 m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
+                                                 m->d_nextb, m->ldt, m->d_tied, m->d_len);
+    PS_LAUNCHED();
+  }
   ps_free(kA, s);
   ps_free(kB, s);
   ps_free(iA, s);
