@@ -89,7 +89,7 @@ def device_peaks(peaks: dict) -> dict:
             mb = {}
     out["dmma_tflops"] = mb.get("dmma_tflops", 37.0)
     out["imma_tops"] = mb.get("imma_mma_sync_tops", 1127.0)
-    out["tcgen05_i8_tops"] = mb.get("tcgen05_i8_tops", 4500.0)
+    out["tcgen05_i8_tops"] = mb.get("tcgen05_i8_tops", 4500.0)  # measured: tools/microbench/tc05_peak.cu
     # SMEM crossbar: 148 SMs x 128 B/clk at the max SM clock
     out["smem_gbs"] = 148 * 128 * out["sm_max_mhz"] * 1e6 / 1e9
     return out
@@ -411,9 +411,9 @@ def main():
             ks = cat_a
             ksum = float(ks.sum())
             per_launch = 2.0 * (ksum * ksum - float((ks * ks).sum())) / 2.0 * S / world
-            peak = peaks["imma_tops"]
+            peak = peaks["tcgen05_i8_tops"]
             achieved = per_launch / (launch_ms / 1e3) / 1e12
-            per_ps_desc = "2 k_g k_h int8 ops"
+            per_ps_desc = "2 k_g k_h int8 ops (tcgen05 kind::i8)"
         elif test == "anova":
             ksum = float(cat_a.sum())
             per_launch = 4.0 * ksum * b.shape[0] * S / world

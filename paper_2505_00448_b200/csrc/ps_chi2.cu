@@ -14,6 +14,8 @@
 // Algorithmic work: 2 k_g k_h int8 ops per pair-sample.
 #include "ps_internal.cuh"
 #include "ps_specfun.cuh"
+#include "ps_tc05.cuh"
+#include <cudaTypedefs.h>
 #include <algorithm>
 #include <vector>
 
@@ -167,6 +169,104 @@ onehot_gemm_kernel(const uint8_t* __restrict__ O, int64_t Sp, int64_t NTt, int64
     }
 }
 
+// ----------------------------------------------------------------- tcgen05 GEMM
+// Blackwell-native version of the same contraction: tcgen05.mma kind::i8 with
+// the int32 accumulator tile (128 x 256) in tensor memory.  Operands are
+// staged by cp.async into the canonical K-major SWIZZLE_128B layout (8-row x
+// 128-byte atoms), described to the tensor core by 64-bit smem descriptors;
+// one elected thread issues 4 MMAs (K = 32 bytes each) per 128-byte stage and
+// commits them to the stage's mbarrier, which gates the refill of that stage.
+// The epilogue drains TMEM with tcgen05.ld (32 lanes x 32 columns per warp
+// instruction) straight to the int32 table matrix.
+constexpr int TM = 128, TN = 256, TKB = 128;  // tile rows, cols, K bytes per stage
+constexpr int TSTAGES = 4;
+constexpr int TTH = 128;
+constexpr int TA_BYTES = TM * TKB, TB_BYTES = TN * TKB;
+constexpr int TSTAGE_BYTES = TA_BYTES + TB_BYTES;
+constexpr size_t kTc05Smem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
+
+// Warp roles: warps 0-3 epilogue (TMEM lanes 32w..32w+31), warp 4 TMA
+// producer, warp 5 MMA issuer.  full[s]: TMA bytes landed; empty[s]: the MMAs
+// reading stage s retired (tcgen05.commit); done: last MMA retired.
+constexpr int TTH_WS = 192;
+__global__ void __launch_bounds__(TTH_WS, 1)
+onehot_gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
+                        int64_t Sp, const int2* __restrict__ tiles, int32_t* __restrict__ C, int64_t ldC) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[TSTAGES], empty[TSTAGES], done;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int2 t = tiles[blockIdx.x];
+  const int64_t row0 = (int64_t)t.x * TM, col0 = (int64_t)t.y * TN;
+  const int nk = (int)(Sp / TKB);
+
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, TN);
+  if (tid == 32) {
+    for (int i = 0; i < TSTAGES; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], 1);
+    }
+    tc05::mbar_init(&done, 1);
+    tc05::fence_barrier_init();
+  }
+  if (tid == 4 * 32) {
+    tc05::prefetch_tmap(&tmapA);
+    tc05::prefetch_tmap(&tmapB);
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::fence_after_sync();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      for (int kc = 0; kc < nk; ++kc) {
+        const int st = kc % TSTAGES, n = kc / TSTAGES;
+        if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
+        const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
+        tc05::mbar_arrive_expect_tx(&full[st], TSTAGE_BYTES);
+        tc05::tma_load_2d(sa, &tmapA, kc * TKB, (int32_t)row0, &full[st]);
+        tc05::tma_load_2d(sb, &tmapB, kc * TKB, (int32_t)col0, &full[st]);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc05::idesc_i8(TM, TN, true);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int st = kc % TSTAGES, n = kc / TSTAGES;
+        tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
+        tc05::fence_after_sync();
+        const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < TKB / 32; ++kk)
+          tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), tc05::sw128_kmajor_desc(sb + kk * 32), idesc,
+                       (kc | kk) != 0 ? 1u : 0u);
+        tc05::commit(&empty[st]);
+      }
+      tc05::commit(&done);
+    }
+  } else {
+    // epilogue warps 0-3
+    tc05::mbar_wait(&done, 0);
+    tc05::fence_after_sync();
+    const int64_t r = row0 + warp * 32 + lane;
+    int32_t* crow = C + r * ldC + col0;
+#pragma unroll 1
+    for (int cc = 0; cc < TN / 32; ++cc) {
+      uint32_t v[32];
+      tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<int4*>(crow + cc * 32 + j) = make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+    }
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc05::tmem_dealloc(tmem, TN);
+}
+
 // ----------------------------------------------------------------- epilogue
 __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
   if (o) {
@@ -263,6 +363,33 @@ __global__ void label_check_kernel(const uint32_t* __restrict__ bad, const uint3
 
 }  // namespace
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D uint8 tensor map over the one-hot matrix: rows x Sp bytes, box TKB x rows_box, 128-B swizzle
+static int make_onehot_map(CUtensorMap* map, const uint8_t* O, int64_t rows, int64_t Sp, uint32_t rows_box) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)Sp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)Sp};
+  cuuint32_t box[2] = {(cuuint32_t)TKB, rows_box};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(O), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return PS_OK;
+}
+
 int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi, double* v,
                 cudaStream_t s) {
   const int64_t F = a->F, S = a->S;
@@ -277,8 +404,8 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
     off[f + 1] = off[f] + cat32[f];
   }
   const int64_t R = off[F];
-  const int64_t Rp = std::max<int64_t>(BM, ps_round_up(R, BM));
-  const int64_t Sp = ps_round_up(S, BK);
+  const int64_t Rp = std::max<int64_t>(TN, ps_round_up(R, TN));
+  const int64_t Sp = ps_round_up(S, TKB);
   std::vector<int32_t> row_feat(R), row_level(R);
   for (int64_t f = 0; f < F; ++f)
     for (int32_t l = 0; l < cat32[f]; ++l) {
@@ -306,17 +433,27 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   }
   onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
   PS_LAUNCHED();
-  // tiles of C needed by pairs with g in [lo, hi): tile rows covering off[lo]..off[hi]-1
-  const int64_t NTt = Rp / BM;
-  const int64_t I0 = off[lo] / BM;
-  const int64_t I1 = std::max<int64_t>(I0, (off[hi] - 1) / BM);
-  const int64_t tile0 = ps_tri_offset(I0, NTt);
-  const int64_t ntiles = ps_tri_offset(std::min<int64_t>(I1 + 1, NTt), NTt) - tile0;
-  const size_t smem = (size_t)GSTAGES * 2 * TILE_BYTES;
-  PS_CUDA(cudaFuncSetAttribute(onehot_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (R > 0 && ntiles > 0) {
+  // 128 x 256 tiles of C needed by pairs with g in [lo, hi): row tiles covering
+  // off[lo] .. off[hi]-1, column tiles from the diagonal rightwards
+  std::vector<int2> tl;
+  if (R > 0) {
+    const int64_t I0 = off[lo] / TM;
+    const int64_t I1 = std::max<int64_t>(I0, (off[hi] - 1) / TM);
+    for (int64_t I = I0; I <= I1; ++I)
+      for (int64_t J = (I * TM) / TN; J < Rp / TN; ++J) tl.push_back(make_int2((int)I, (int)J));
+  }
+  int2* d_tiles = nullptr;
+  if (!tl.empty()) {
+    PS_CUDA(ps_alloc(&d_tiles, tl.size(), s));
+    PS_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaFuncSetAttribute(onehot_gemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTc05Smem));
+    CUtensorMap mapA, mapB;
+    int rc = make_onehot_map(&mapA, O, Rp, Sp, TM);
+    if (!rc) rc = make_onehot_map(&mapB, O, Rp, Sp, TN);
+    if (rc) return rc;
     ps_prof_begin("chi2_gemm", s);
-    onehot_gemm_kernel<<<(unsigned)ntiles, GTH, smem, s>>>(O, Sp, NTt, tile0, C, Rp);
+    onehot_gemm_tc05_kernel<<<(unsigned)tl.size(), TTH_WS, kTc05Smem, s>>>(mapA, mapB, Sp, d_tiles, C, Rp);
     ps_prof_end(s);
     PS_LAUNCHED();
   }
@@ -333,5 +470,6 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   ps_free(d_off, s);
   ps_free(d_rf, s);
   ps_free(d_rl, s);
+  ps_free(d_tiles, s);
   return PS_OK;
 }

@@ -1,0 +1,63 @@
+// tcgen05 kind::i8 dense throughput (M=128, N=256, K=32 per instruction), operands
+// fixed in shared memory, accumulator in TMEM; one issuing thread per CTA, one CTA per SM.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_2505_00448_b200/csrc/ps_tc05.cuh"
+
+__global__ void __launch_bounds__(128, 1) peak_kernel(int iters, int* out) {
+  extern __shared__ __align__(1024) unsigned char sm_raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 48 * 1024; i += blockDim.x) sm[i] = (unsigned char)(i * 7);
+  if (threadIdx.x < 32) tc05::tmem_alloc(&tbase, 256);
+  if (threadIdx.x == 32) { tc05::mbar_init(&bar, 1); tc05::fence_barrier_init(); }
+  tc05::fence_proxy_async();
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::fence_after_sync();
+  const uint32_t sa = tc05::smem_u32(sm), sb = sa + 16 * 1024;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = tc05::idesc_i8(128, 256, true);
+    for (int it = 0; it < iters; ++it)
+      for (int kk = 0; kk < 4; ++kk)
+        tc05::mma_i8(tbase, tc05::sw128_kmajor_desc(sa + kk * 32), tc05::sw128_kmajor_desc(sb + kk * 32), idesc, 1u);
+    tc05::commit(&bar);
+    tc05::mbar_wait(&bar, 0);
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v[32];
+    tc05::tmem_ld32(tbase, v);
+    if (v[0] == 12345u) out[0] = 1;
+    tc05::tmem_dealloc(tbase, 256);
+  }
+}
+
+int main() {
+  int *d;
+  cudaMalloc(&d, 4);
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  cudaFuncSetAttribute(peak_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
+  const int iters = 20000;
+  peak_kernel<<<p.multiProcessorCount, 128, 50 * 1024>>>(100, d);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  double best = 0;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(a);
+    peak_kernel<<<p.multiProcessorCount, 128, 50 * 1024>>>(iters, d);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    const double ops = (double)p.multiProcessorCount * iters * 4 * 2.0 * 128 * 256 * 32;
+    if (ops / (ms * 1e-3) > best) best = ops / (ms * 1e-3);
+  }
+  printf("{\"tcgen05_i8_tops\": %.1f, \"err\": \"%s\"}\n", best / 1e12, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
