@@ -163,7 +163,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
                      const int32_t* __restrict__ lens, int64_t F, int64_t lo, int64_t hi,
                      int* __restrict__ queue, PairSums out) {
   const WalkLayout L(ldo, ldt, OGS, R2);
-  __shared__ uint32_t wtot[SW];
+  __shared__ uint32_t wtot[SW], wtotA[SW], wtotB[SW];
   __shared__ unsigned long long red[SW][3];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -257,6 +257,29 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       const int nwa = (ng + 31) >> 5;
       const int La = (nwa + SW - 1) / SW;
       const int a0 = min(nwa, warp * La), a1 = min(nwa, a0 + La);
+      // Tie-free g (and R holding 2r): one sweep.  R[q] = (warp << 11) | local
+      // rank within the warp's segment; the segment bases are folded in by
+      // pass B, so no prefix phase is needed here.
+      const bool encA = R2 && !tg && La * 32 <= 2047;
+      uint32_t segpreA = 0, n = 0, abase = 0;
+      unsigned long long sa2 = 0;
+      if (encA) {
+        uint32_t cnt = 0;
+#pragma unroll 4
+        for (int word = a0; word < a1; ++word) {
+          const uint32_t p = (uint32_t)(word * 32 + lane);
+          const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
+          const uint32_t q = ld16(aInv + 2 * s);
+          const bool keep = q != 0xFFFFu;
+          const uint32_t B = __ballot_sync(PS_FULL, keep);
+          if (keep) st16(aR + 2 * q, ((uint32_t)warp << 11) | (cnt + __popc(B & ltmask) + 1u));
+          cnt += __popc(B);
+        }
+        if (lane == 0) wtotA[warp] = cnt;
+        __syncthreads();
+        segment_bases(wtotA, segpreA, n);
+        WT(1);
+      } else {
       {
         // q = inv_h[order_g[p]]; with g's order staged in shared memory the
         // gathered q overwrites it in place, so phase 2 reads it sequentially
@@ -278,7 +301,6 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       }
       __syncthreads();
       WT(1);
-      uint32_t abase, n;
       {
         uint32_t segpre;
         segment_bases(wtot, segpre, n);
@@ -295,7 +317,6 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       WT(2);
       // ---------------- pass A, phase 2: ranks -> R[q] -------------------
       auto q_at = [&](uint32_t p) -> uint32_t { return OGS ? ld16(aOg + 2 * p) : ld16(aInv + 2 * (uint32_t)og_g[p]); };
-      unsigned long long sa2 = 0;
       if (!tg) {
 #pragma unroll 4
         for (int word = a0; word < a1; ++word) {
@@ -333,7 +354,36 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
       }
       __syncthreads();
+      }  // two-phase pass A
       WT(3);
+      // decode R -> 2 r_g (all lanes must execute: shuffles)
+      auto r2g_of = [&](uint32_t v, int word) -> uint32_t {
+        if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> 11)) + (v & 0x7FFu));
+        if (R2) return v;
+        return 2u * v + (tg ? ((ld32(aPar + 4 * word) >> lane) & 1u) : 0u);
+      };
+      const bool sweepB = R2 && !th;
+      unsigned long long sab = 0, sbb = 0, s0 = 0;
+      if (sweepB) {
+        // Tie-free h: one sweep; per warp sum r2g * local_h and sum r2g, the
+        // segment bases of h's order are folded in after the reduction.
+        uint32_t cnt = 0;
+#pragma unroll 4
+        for (int word = b0; word < b1; ++word) {
+          const uint32_t q = (uint32_t)(word * 32 + lane);
+          const uint32_t v = ld16(aR + 2 * q);
+          const bool keep = v != 0u;
+          const uint32_t B = __ballot_sync(PS_FULL, keep);
+          const uint32_t r2g = r2g_of(v, word);
+          if (keep) {
+            sab += (unsigned long long)r2g * (cnt + __popc(B & ltmask) + 1u);
+            s0 += r2g;
+            st16(aR + 2 * q, 0u);
+          }
+          cnt += __popc(B);
+        }
+        if (lane == 0) wtotB[warp] = cnt;
+      } else {
       // ---------------- pass B, phase 1: keep = R != 0 over h's order ------
       {
         uint32_t cnt = 0;
@@ -366,15 +416,13 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
       }
       // ---------------- pass B, phase 2: accumulate, clear R ---------------
-      unsigned long long sab = 0, sbb = 0;
       if (!th) {
 #pragma unroll 4
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(aK + 4 * word);
           const uint32_t q = (uint32_t)(word * 32 + lane);
           const uint32_t v = ld16(aR + 2 * q);
-          uint32_t r2g = R2 ? v : 2u * v;
-          if (!R2 && tg) r2g += (ld32(aPar + 4 * word) >> lane) & 1u;
+          const uint32_t r2g = r2g_of(v, word);
           const uint32_t rh = bbase + ld32(aP + 4 * word) + __popc(kw & ltmask) + 1u;
           if ((kw >> lane) & 1u) {
             sab += (unsigned long long)r2g * rh;
@@ -390,10 +438,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(aK + 4 * word);
           const uint32_t q = (uint32_t)(word * 32 + lane);
+          const uint32_t v = ld16(aR + 2 * q);
+          const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
           if ((kw >> lane) & 1u) {
-            const uint32_t v = ld16(aR + 2 * q);
-            uint32_t r2g = R2 ? v : 2u * v;
-            if (!R2 && tg) r2g += (ld32(aPar + 4 * word) >> lane) & 1u;
             const uint32_t r2h = pfx(tstart_a(aTbh, aLbh, q)) + pfx(tend_a(aTbh, aNbh, q)) + 1u;
             sab += (unsigned long long)r2g * r2h;
             sbb += (unsigned long long)r2h * r2h;
@@ -405,6 +452,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           }
         }
       }
+      }  // two-phase pass B
       WT(5);
       // ---------------- reduce and store the exact sums ---------------------
 #pragma unroll
@@ -412,11 +460,12 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         sa2 += __shfl_xor_sync(PS_FULL, sa2, o);
         sab += __shfl_xor_sync(PS_FULL, sab, o);
         sbb += __shfl_xor_sync(PS_FULL, sbb, o);
+        s0 += __shfl_xor_sync(PS_FULL, s0, o);
       }
       if (lane == 0) {
         red[warp][0] = sa2;
         red[warp][1] = sab;
-        red[warp][2] = sbb;
+        red[warp][2] = sweepB ? s0 : sbb;
       }
       __syncthreads();
       if (threadIdx.x < 3) {
@@ -427,9 +476,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           out.sxx4[cell] = (long long)(tg ? v : kClosed);
           out.n[cell] = (long long)n;
         } else if (threadIdx.x == 1) {
+          if (sweepB) {
+            // sum over warps of 2 * (sum r2g*local + base_w * sum r2g)
+            unsigned long long acc = 0, base = 0;
+            for (int w = 0; w < SW; ++w) {
+              acc += 2ull * (red[w][1] + base * red[w][2]);
+              base += wtotB[w];
+            }
+            v = acc;
+          }
           out.sxy4[cell] = (long long)v;
         } else {
-          out.syy4[cell] = (long long)(th ? v : kClosed);
+          out.syy4[cell] = (long long)(th ? v : kClosed);  // (sweepB implies !th)
         }
       }
       WT(6);
