@@ -117,10 +117,16 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
   uint8_t* cg_s[2];
   cg_s[0] = take(ldc);
   cg_s[1] = take(ldc);
+  // byte offsets into the dynamic buffer: indexing `smem[...]` directly keeps
+  // the gathers in the shared window (LDS), never generic loads
+  const uint32_t cg_off[2] = {(uint32_t)(cg_s[0] - smem), (uint32_t)(cg_s[1] - smem)};
+  const uint32_t oh_off = (uint32_t)(reinterpret_cast<unsigned char*>(oh) - smem) / 2;
+  const uint16_t* smem16 = reinterpret_cast<const uint16_t*>(smem);
   __shared__ uint32_t wsum[RW];
   __shared__ unsigned long long red_r[RW][KM];
   __shared__ uint32_t red_c[RW][KM];
   __shared__ long long red_t[RW];
+  __shared__ uint32_t wtot_s[RW];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -161,41 +167,53 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       else asm volatile("cp.async.commit_group;");
       asm volatile("cp.async.wait_group 1;");
       __syncthreads();
-      const uint8_t* cg = cg_s[buf];
+      const uint32_t cgo = cg_off[buf];
       const int k = cat[g];
-      // -------- phase 1: keep bits (label present) over h's order --------
-      bool bad = false;
-#pragma unroll 4
-      for (int word = warp; word < nw; word += RW) {
-        const int p = word * 32 + lane;
-        const uint32_t c = p < nh ? (uint32_t)cg[oh[p]] : 0xFFu;
-        bad |= c == 0xFEu;
-        const uint32_t B = __ballot_sync(PS_FULL, c != 0xFFu);
-        if (lane == 0) K[word] = B;
-      }
-      if (check_labels && __any_sync(PS_FULL, bad) && lane == 0) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
-      __syncthreads();
-      scan_words(K, P, nw, wsum);
-      // -------- phase 2: ranks, per-level sums, tie term --------
       uint32_t acc[KM], cnt[KM];
 #pragma unroll
       for (int j = 0; j < KM; ++j) acc[j] = cnt[j] = 0u;
       long long tie = 0;
+      bool bad = false;
       if (!th) {
+        // Tie-free h: ONE sweep over a contiguous segment per warp.  Ranks are
+        // segment-local (running kept count); per level we keep sum(local)
+        // and the count, and fold in the segment base after the reduction:
+        //   sum 2r = 2 (base_w * count + sum local).
+        const int L = (nw + RW - 1) / RW;
+        const int w0 = min(nw, warp * L), w1 = min(nw, w0 + L);
+        uint32_t run = 0;
+        // per lane and level: count in bits [20,32), sum of local ranks in [0,20)
+        // (a lane sees <= 128 positions of rank <= 4096 for S <= 65535)
 #pragma unroll 4
-        for (int word = warp; word < nw; word += RW) {
-          const int p = word * 32 + lane;
-          const uint32_t kw = K[word];
-          const uint32_t c = (kw >> lane) & 1u ? (uint32_t)cg[oh[p]] : 0xFFu;
-          const uint32_t r2 = 2u * (P[word] + __popc(kw & lanemask_lt()) + 1u);
+        for (int word = w0; word < w1; ++word) {
+          const uint32_t c = smem[cgo + smem16[oh_off + word * 32 + lane]];  // sentinel padded: 0xFF
+          bad |= c == 0xFEu;
+          const bool keep = c != 0xFFu;
+          const uint32_t B = __ballot_sync(PS_FULL, keep);
+          const uint32_t packed = (1u << 20) + run + __popc(B & lanemask_lt()) + 1u;
 #pragma unroll
-          for (int j = 0; j < KM; ++j)
-            if (c == (uint32_t)j) {
-              acc[j] += r2;
-              cnt[j] += 1u;
-            }
+          for (int j = 0; j < KM; ++j) acc[j] += c == (uint32_t)j ? packed : 0u;  // select, not a branch
+          run += __popc(B);
         }
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+          cnt[j] = acc[j] >> 20;
+          acc[j] &= 0xFFFFFu;
+        }
+        if (lane == 0) wtot_s[warp] = run;
       } else {
+      // -------- phase 1: keep bits (label present) over h's order --------
+#pragma unroll 4
+      for (int word = warp; word < nw; word += RW) {
+        const int p = word * 32 + lane;
+        const uint32_t c = p < nh ? (uint32_t)smem[cgo + smem16[oh_off + p]] : 0xFFu;
+        bad |= c == 0xFEu;
+        const uint32_t B = __ballot_sync(PS_FULL, c != 0xFFu);
+        if (lane == 0) K[word] = B;
+      }
+      __syncthreads();
+      scan_words(K, P, nw, wsum);
+      // -------- phase 2: ranks, per-level sums, tie term --------
         for (int word = warp; word < nw; word += RW) {
           const uint32_t p = (uint32_t)(word * 32 + lane);
           const uint32_t kw = K[word];
@@ -208,18 +226,19 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
               if (t > 1) tie += t * t * t - t;
             }
             if ((kw >> lane) & 1u) {
-              const uint32_t c = cg[oh[p]];
+              const uint32_t c = smem[cgo + smem16[oh_off + p]];
               const uint32_t r2 = a + b + 1u;
 #pragma unroll
-              for (int j = 0; j < KM; ++j)
-                if (c == (uint32_t)j) {
-                  acc[j] += r2;
-                  cnt[j] += 1u;
-                }
+              for (int j = 0; j < KM; ++j) {
+                const bool hit = c == (uint32_t)j;
+                acc[j] += hit ? r2 : 0u;
+                cnt[j] += hit ? 1u : 0u;
+              }
             }
           }
         }
       }
+      if (check_labels && __any_sync(PS_FULL, bad) && lane == 0) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
       // -------- reduce to the pair's exact sums --------
 #pragma unroll
       for (int j = 0; j < KM; ++j) {
@@ -244,9 +263,18 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
         const int j = threadIdx.x;
         unsigned long long a = 0;
         uint32_t c = 0;
-        for (int w = 0; w < RW; ++w) {
-          a += red_r[w][j];
-          c += red_c[w][j];
+        if (!th) {
+          unsigned long long base = 0;
+          for (int w = 0; w < RW; ++w) {
+            a += 2ull * (red_r[w][j] + base * red_c[w][j]);
+            c += red_c[w][j];
+            base += wtot_s[w];
+          }
+        } else {
+          for (int w = 0; w < RW; ++w) {
+            a += red_r[w][j];
+            c += red_c[w][j];
+          }
         }
         if (j < k || j == 0) {
           out.r2[pair * out.KM + j] = a;
