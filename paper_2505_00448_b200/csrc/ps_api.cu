@@ -220,14 +220,22 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
       return ps_fail(PS_ERR_CUDA, "out of device memory for the input matrix");
     }
     cudaError_t e = cudaSuccess;
-    if (m->ld != m->S) e = cudaMemsetAsync(m->d_vals, 0, sizeof(double) * m->F * m->ld, s);
-    if (e == cudaSuccess)
+    if (m->ld != m->S && values_on_device) e = cudaMemsetAsync(m->d_vals, 0, sizeof(double) * m->F * m->ld, s);
+    if (e == cudaSuccess && values_on_device)
       e = cudaMemcpy2DAsync(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
-                            sizeof(double) * m->S, m->F,
-                            values_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+                            sizeof(double) * m->S, m->F, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) {
       ps_matrix_destroy(m);
       return ps_cuda_check(e, "input upload");
+    }
+    if (!values_on_device) {
+      // pinned, double-buffered, all-core staging of the pageable input
+      rc = ps_stage_h2d_2d(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
+                           sizeof(double) * m->S, m->F, s);
+      if (rc) {
+        ps_matrix_destroy(m);
+        return rc;
+      }
     }
   }
   rc = ps_prepare_matrix(m, s);
@@ -417,21 +425,14 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     }
   }
   if (!rc) rc = drain_errors(s);
-  for (int k = 0; k < 4 && !rc; ++k) {
-    if (outs && outs[k] && d_out[k]) {
-      cudaError_t e = cudaMemcpyAsync(outs[k], d_out[k], sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
-      if (e != cudaSuccess) rc = ps_cuda_check(e, "result download");
-    }
-  }
+  for (int k = 0; k < 4 && !rc; ++k)
+    if (outs && outs[k] && d_out[k]) rc = ps_stage_d2h(outs[k], d_out[k], sizeof(double) * cells, s);
   if (!rc && any_adj) {
     if (ps_alloc(&d_adj, (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
     for (int k = 0; k < 3 && !rc; ++k) {
       if (!adj_outs[k]) continue;
       rc = ps_adjust_run(d_out[1], rows, cols, k, homogeneous ? 1 : 0, d_adj, s);
-      if (!rc) {
-        cudaError_t e = cudaMemcpyAsync(adj_outs[k], d_adj, sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) rc = ps_cuda_check(e, "adjusted download");
-      }
+      if (!rc) rc = ps_stage_d2h(adj_outs[k], d_adj, sizeof(double) * cells, s);
     }
   }
   if (!rc) {

@@ -99,4 +99,7 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
                       double* stat, double* p, double* eff, cudaStream_t s);
 int ps_adjust_run(const double* p, int64_t rows, int64_t cols, int method, int symmetric,
                   double* out, cudaStream_t s);
+int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                    cudaStream_t s);
+int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s);
