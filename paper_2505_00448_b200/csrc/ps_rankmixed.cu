@@ -123,8 +123,14 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
   const uint32_t oh_off = (uint32_t)(reinterpret_cast<unsigned char*>(oh) - smem) / 2;
   const uint16_t* smem16 = reinterpret_cast<const uint16_t*>(smem);
   __shared__ uint32_t wsum[RW];
-  __shared__ unsigned long long red_r[RW][KM];
-  __shared__ uint32_t red_c[RW][KM];
+  // KM <= 16: per-lane register accumulators reduced by shuffles; KM = 256:
+  // per-warp shared accumulators (shared atomics) for labels with many levels
+  constexpr bool BIG = KM > 16;
+  constexpr int NR = BIG ? 1 : KM;
+  __shared__ unsigned long long red_r[RW][NR];
+  __shared__ uint32_t red_c[RW][NR];
+  __shared__ uint32_t bsum[BIG ? RW : 1][BIG ? 256 : 1];
+  __shared__ uint32_t bcnt[BIG ? RW : 1][BIG ? 256 : 1];
   __shared__ long long red_t[RW];
   __shared__ uint32_t wtot_s[RW];
   __shared__ int s_item;
@@ -169,9 +175,16 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       __syncthreads();
       const uint32_t cgo = cg_off[buf];
       const int k = cat[g];
-      uint32_t acc[KM], cnt[KM];
+      uint32_t acc[NR], cnt[NR];
 #pragma unroll
-      for (int j = 0; j < KM; ++j) acc[j] = cnt[j] = 0u;
+      for (int j = 0; j < NR; ++j) acc[j] = cnt[j] = 0u;
+      if constexpr (BIG) {
+        for (int j = lane; j < k; j += 32) {
+          bsum[warp][j] = 0u;
+          bcnt[warp][j] = 0u;
+        }
+        __syncwarp();
+      }
       long long tie = 0;
       bool bad = false;
       if (!th) {
@@ -190,13 +203,21 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
           bad |= c == 0xFEu;
           const bool keep = c != 0xFFu;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
-          const uint32_t packed = (1u << 20) + run + __popc(B & lanemask_lt()) + 1u;
+          const uint32_t local = run + __popc(B & lanemask_lt()) + 1u;
+          if constexpr (BIG) {
+            if (c < (uint32_t)k) {
+              atomicAdd(&bsum[warp][c], local);
+              atomicAdd(&bcnt[warp][c], 1u);
+            }
+          } else {
+            const uint32_t packed = (1u << 20) + local;
 #pragma unroll
-          for (int j = 0; j < KM; ++j) acc[j] += c == (uint32_t)j ? packed : 0u;  // select, not a branch
+            for (int j = 0; j < KM; ++j) acc[j] += c == (uint32_t)j ? packed : 0u;  // select, not a branch
+          }
           run += __popc(B);
         }
 #pragma unroll
-        for (int j = 0; j < KM; ++j) {
+        for (int j = 0; j < NR; ++j) {
           cnt[j] = acc[j] >> 20;
           acc[j] &= 0xFFFFFu;
         }
@@ -228,11 +249,18 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
             if ((kw >> lane) & 1u) {
               const uint32_t c = smem[cgo + smem16[oh_off + p]];
               const uint32_t r2 = a + b + 1u;
+              if constexpr (BIG) {
+                if (c < (uint32_t)k) {
+                  atomicAdd(&bsum[warp][c], r2);
+                  atomicAdd(&bcnt[warp][c], 1u);
+                }
+              } else {
 #pragma unroll
-              for (int j = 0; j < KM; ++j) {
-                const bool hit = c == (uint32_t)j;
-                acc[j] += hit ? r2 : 0u;
-                cnt[j] += hit ? 1u : 0u;
+                for (int j = 0; j < KM; ++j) {
+                  const bool hit = c == (uint32_t)j;
+                  acc[j] += hit ? r2 : 0u;
+                  cnt[j] += hit ? 1u : 0u;
+                }
               }
             }
           }
@@ -241,7 +269,7 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       if (check_labels && __any_sync(PS_FULL, bad) && lane == 0) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
       // -------- reduce to the pair's exact sums --------
 #pragma unroll
-      for (int j = 0; j < KM; ++j) {
+      for (int j = 0; j < (BIG ? 0 : NR); ++j) {
         unsigned long long a = acc[j];
         uint32_t c = cnt[j];
 #pragma unroll
@@ -259,7 +287,25 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       if (lane == 0) red_t[warp] = tie;
       __syncthreads();
       const int64_t pair = g * Fq + h;
-      if (threadIdx.x < KM) {
+      if constexpr (BIG) {
+        for (int j = threadIdx.x; j < max(k, 1); j += RTH) {
+          unsigned long long a = 0;
+          uint32_t c = 0;
+          unsigned long long base = 0;
+          for (int w = 0; w < RW; ++w) {
+            a += th ? (unsigned long long)bsum[w][j] : 2ull * ((unsigned long long)bsum[w][j] + base * bcnt[w][j]);
+            c += bcnt[w][j];
+            base += wtot_s[w];
+          }
+          out.r2[pair * out.KM + j] = a;
+          out.cnt[pair * out.KM + j] = (int32_t)c;
+        }
+        if (threadIdx.x == 0) {
+          long long t = 0;
+          for (int w = 0; w < RW; ++w) t += red_t[w];
+          out.tie[pair] = t;
+        }
+      } else if (threadIdx.x < KM) {
         const int j = threadIdx.x;
         unsigned long long a = 0;
         uint32_t c = 0;
@@ -456,8 +502,11 @@ int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo
                 int* queue, RankSums rs, cudaStream_t s) {
   ps_device_state* ds = ps_state();
   const size_t smem = walk_smem(val->ldo, val->ldt, lab->ldc);
-  if (smem > 226 * 1024) return ps_fail(PS_ERR_INVALID, "rank walk: sample count too large for shared memory");
   auto kern = rank_mixed_walk_kernel<KM>;
+  cudaFuncAttributes fa{};
+  PS_CUDA(cudaFuncGetAttributes(&fa, kern));
+  if (smem + fa.sharedSizeBytes > 227 * 1024)
+    return ps_fail(PS_ERR_INVALID, "rank walk: sample count too large for shared memory");
   PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RTH, smem));
@@ -488,25 +537,25 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
   ps_device_state* ds = ps_state();
   const bool kw = test == PS_TEST_KRUSKAL;
   const int kmax = kw ? std::max(1, lab->cmax) : 2;
-  int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 0;
-  if (KM == 0) return ps_fail(PS_ERR_INVALID, "kruskal: more than 16 label levels is not supported yet");
+  const int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 256;
   const int64_t npairs = Fc * Fq;
-  RankSums rs{KM, nullptr, nullptr, nullptr};
+  // per-pair level stride: the template width, or the real level count for k > 16
+  RankSums rs{KM > 16 ? (kmax + 31) / 32 * 32 : KM, nullptr, nullptr, nullptr};
   uint8_t* bcodes = nullptr;
   int* queue = nullptr;
   int2* exl = nullptr;
   int* exc = nullptr;
   const int excap = (int)std::min<int64_t>(Fc * (hi - lo), 1 << 20);
-  PS_CUDA(ps_alloc(&rs.cnt, (size_t)(npairs * KM), s));
-  PS_CUDA(ps_alloc(&rs.r2, (size_t)(npairs * KM), s));
+  PS_CUDA(ps_alloc(&rs.cnt, (size_t)(npairs * rs.KM), s));
+  PS_CUDA(ps_alloc(&rs.r2, (size_t)(npairs * rs.KM), s));
   PS_CUDA(ps_alloc(&rs.tie, (size_t)npairs, s));
   PS_CUDA(ps_alloc(&queue, 1, s));
   PS_CUDA(ps_alloc(&exl, (size_t)excap, s));
   PS_CUDA(ps_alloc(&exc, 1, s));
   PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
   PS_CUDA(cudaMemsetAsync(exc, 0, sizeof(int), s));
-  PS_CUDA(cudaMemsetAsync(rs.cnt, 0, sizeof(int32_t) * npairs * KM, s));
-  PS_CUDA(cudaMemsetAsync(rs.r2, 0, sizeof(unsigned long long) * npairs * KM, s));
+  PS_CUDA(cudaMemsetAsync(rs.cnt, 0, sizeof(int32_t) * npairs * rs.KM, s));
+  PS_CUDA(cudaMemsetAsync(rs.r2, 0, sizeof(unsigned long long) * npairs * rs.KM, s));
   const uint8_t* codes = lab->d_codes;
   if (!kw) {
     PS_CUDA(ps_alloc(&bcodes, (size_t)(Fc * lab->ldc), s));
@@ -517,7 +566,8 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
   int rc = 0;
   if (KM == 2) rc = launch_walk<2>(lab, val, codes, lo, hi, kw, queue, rs, s);
   else if (KM == 8) rc = launch_walk<8>(lab, val, codes, lo, hi, kw, queue, rs, s);
-  else rc = launch_walk<16>(lab, val, codes, lo, hi, kw, queue, rs, s);
+  else if (KM == 16) rc = launch_walk<16>(lab, val, codes, lo, hi, kw, queue, rs, s);
+  else rc = launch_walk<256>(lab, val, codes, lo, hi, kw, queue, rs, s);
   if (rc) return rc;
   const int64_t total = Fc * (hi - lo);
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);

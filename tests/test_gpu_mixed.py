@@ -44,7 +44,7 @@ def test_ttest_matches_oracle(oracle, na, variant):
 
 
 @pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
-@pytest.mark.parametrize("c", [2, 3, 7])
+@pytest.mark.parametrize("c", [2, 3, 7, 30])
 def test_anova_matches_oracle(oracle, na, c):
     a, b = _inputs("anova", 12, 90, 400, na, seed=int(na * 100) + c, c=c)
     req = ps.TestRequest("anova", ("stat", "p", "partial_eta2"))
@@ -100,7 +100,7 @@ def test_anova_label_out_of_range():
 
 
 @pytest.mark.parametrize("na", [0.0, 0.1, 0.3, 0.5])
-@pytest.mark.parametrize("c", [2, 3, 8, 13])
+@pytest.mark.parametrize("c", [2, 3, 8, 13, 20, 60])
 def test_kruskal_matches_oracle(oracle, na, c):
     a, b = _inputs("kruskal", 12, 60, 400, na, seed=int(na * 100) + c, c=c)
     req = ps.TestRequest("kruskal", ("stat", "p", "eta2"))
@@ -110,6 +110,22 @@ def test_kruskal_matches_oracle(oracle, na, c):
         assert same_nan(res[name], ref[name]), name
     assert bitwise_equal(res["stat"], ref["stat"])
     assert bitwise_equal(res["eta2"], ref["eta2"])
+    assert p_close(res["p"], ref["p"])
+
+
+def test_kruskal_mixed_level_counts(oracle):
+    """Label features with 2..200 levels in one matrix (k > 16 takes the
+    shared-accumulator walk for every feature)."""
+    rows = [workloads.simulate(1, 600, "categorical", categories=c, na_ratio=0.2, seed=c)
+            for c in (2, 5, 17, 40, 200)]
+    a = ps.make_matrix(np.vstack(rows), "categorical")
+    b = ps.make_matrix(workloads.simulate(40, 600, "continuous", na_ratio=0.2, seed=5), "continuous")
+    req = ps.TestRequest("kruskal", ("stat", "p", "eta2"))
+    res = ps.run(req, a, b)
+    ref = oracle.oracle_run(req, a, b)
+    for name in ("stat", "p", "eta2"):
+        assert same_nan(res[name], ref[name]), name
+    assert bitwise_equal(res["stat"], ref["stat"])
     assert p_close(res["p"], ref["p"])
 
 
