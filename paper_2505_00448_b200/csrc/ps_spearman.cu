@@ -111,7 +111,7 @@ struct WalkLayout {
     nbh16 = take(ldt * 2) * 2;
     par = r2 ? 0 : take(ldt * 4);
     K = take(ldt * 4);
-    Pl = take(ldt * 4);
+    Pl = r2 ? take(ldt * 4) : take(ldt * 2) * 2;  // word prefixes; 16-bit when S > 32767 (fits 227 KB)
     for (int b = 0; b < 2; ++b) {
       og16[b] = ogs ? take(ldo * 2) * 2 : 0;
       tbg[b] = ogs ? take(ldt * 4) : 0;
@@ -168,14 +168,19 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm32);
-  const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + 4 * L.Pl;
+  const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + (R2 ? 4 : 2) * L.Pl;
   const uint32_t aPar = sb + 4 * L.par;
   const uint32_t aTbh = sb + 4 * L.tbh, aLbh = sb + 2 * L.lbh16, aNbh = sb + 2 * L.nbh16;
   const uint32_t ltmask = lanemask_lt();
+  auto ldP = [&](uint32_t w) -> uint32_t { return R2 ? ld32(aP + 4 * w) : ld16(aP + 2 * w); };
+  auto stP = [&](uint32_t w, uint32_t v) {
+    if (R2) st32(aP + 4 * w, v);
+    else st16(aP + 2 * w, v);
+  };
   // absolute kept-prefix of position x: P[x/32] + popc(bits of K below x)
   auto pfx = [&](uint32_t x) -> uint32_t {
     const uint32_t w = x >> 5;
-    return ld32(aP + 4 * w) + __popc(ld32(aK + 4 * w) & ((1u << (x & 31u)) - 1u));
+    return ldP(w) + __popc(ld32(aK + 4 * w) & ((1u << (x & 31u)) - 1u));
   };
 
   for (int64_t i = threadIdx.x; i < ldo; i += STH) SM16[L.R16 + i] = 0;
@@ -293,7 +298,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t B = __ballot_sync(PS_FULL, q != 0xFFFFu);
           if (lane == 0) {
             st32(aK + 4 * word, B);
-            st32(aP + 4 * word, cnt);
+            stP(word, cnt);
           }
           cnt += __popc(B);
         }
@@ -306,10 +311,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         segment_bases(wtot, segpre, n);
         abase = __shfl_sync(PS_FULL, segpre, warp);
         if (tg) {  // absolute prefixes for arbitrary-position lookups
-          for (int w = a0 + lane; w < a1; w += 32) st32(aP + 4 * w, ld32(aP + 4 * w) + abase);
+          for (int w = a0 + lane; w < a1; w += 32) stP(w, ldP(w) + abase);
           if (threadIdx.x == 0) {
             st32(aK + 4 * nwa, 0u);
-            st32(aP + 4 * nwa, n);
+            stP(nwa, n);
           }
           __syncthreads();
         }
@@ -321,7 +326,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
 #pragma unroll 4
         for (int word = a0; word < a1; ++word) {
           const uint32_t kw = ld32(aK + 4 * word);
-          const uint32_t r = abase + ld32(aP + 4 * word) + __popc(kw & ltmask) + 1u;
+          const uint32_t r = abase + ldP(word) + __popc(kw & ltmask) + 1u;
           const uint32_t q = q_at((uint32_t)(word * 32 + lane));
           if ((kw >> lane) & 1u) st16(aR + 2 * q, R2 ? 2u * r : r);
         }
@@ -393,7 +398,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t B = __ballot_sync(PS_FULL, keep);
           if (lane == 0) {
             st32(aK + 4 * word, B);
-            st32(aP + 4 * word, cnt);
+            stP(word, cnt);
           }
           cnt += __popc(B);
         }
@@ -407,10 +412,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         segment_bases(wtot, segpre, tot);
         bbase = __shfl_sync(PS_FULL, segpre, warp);
         if (th) {
-          for (int w = b0 + lane; w < b1; w += 32) st32(aP + 4 * w, ld32(aP + 4 * w) + bbase);
+          for (int w = b0 + lane; w < b1; w += 32) stP(w, ldP(w) + bbase);
           if (threadIdx.x == 0) {
             st32(aK + 4 * nwb, 0u);
-            st32(aP + 4 * nwb, tot);
+            stP(nwb, tot);
           }
           __syncthreads();
         }
@@ -423,7 +428,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t q = (uint32_t)(word * 32 + lane);
           const uint32_t v = ld16(aR + 2 * q);
           const uint32_t r2g = r2g_of(v, word);
-          const uint32_t rh = bbase + ld32(aP + 4 * word) + __popc(kw & ltmask) + 1u;
+          const uint32_t rh = bbase + ldP(word) + __popc(kw & ltmask) + 1u;
           if ((kw >> lane) & 1u) {
             sab += (unsigned long long)r2g * rh;
             st16(aR + 2 * q, 0u);

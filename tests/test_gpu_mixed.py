@@ -208,3 +208,16 @@ def test_kruskal_config4_slice(oracle):
     res, ref = ps.run(req, a, b), oracle.oracle_run(req, a, b)
     assert bitwise_equal(res["stat"], ref["stat"])
     assert p_close(res["p"], ref["p"]) and same_nan(res["p_bh"], ref["p_bh"])
+
+
+@pytest.mark.parametrize("test", ["kruskal", "mwu"])
+def test_rank_tests_large_sample_count(oracle, test):
+    """S = 50,000 (the config-5 Spearman sample count): 16-bit orders, the
+    walk's shared-memory plan at its largest."""
+    a, b = _inputs(test, 3, 8, 50000, 0.15, seed=77, c=5)
+    req = ps.TestRequest(test, ("stat", "p"))
+    res = ps.run(req, a, b)
+    ref = oracle.oracle_run(req, a, b)
+    assert same_nan(res["stat"], ref["stat"])
+    assert bitwise_equal(res["stat"], ref["stat"])
+    assert p_close(res["p"], ref["p"])

@@ -34,7 +34,7 @@ def test_spearman_matches_oracle(oracle, F, S, na):
     _check(ps.run(req, mat), oracle.oracle_run(req, mat))
 
 
-@pytest.mark.parametrize("S", [300, 2500, 12000, 25000])
+@pytest.mark.parametrize("S", [300, 2500, 12000, 25000, 40000, 50000])
 def test_spearman_ties_and_blocks(oracle, S):
     rng = np.random.default_rng(S)
     x = workloads.config_spearman_like(rng, 24, S)
