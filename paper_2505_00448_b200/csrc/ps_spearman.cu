@@ -63,6 +63,19 @@ __device__ __forceinline__ uint32_t ld32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint4 ld128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 ld64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void st64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y));
+}
 __device__ __forceinline__ void st16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 }
@@ -83,6 +96,31 @@ __device__ __forceinline__ uint32_t tend_a(uint32_t aT, uint32_t aN, uint32_t p)
   return m ? (w << 5) + (uint32_t)__ffs(m) - 1u : ld16(aN + 2 * (w + 1));
 }
 
+// Tie-averaged doubled rank 2r = Pfx(group start) + Pfx(group end) + 1 for
+// every lane of word w of a tied feature's order (Pfx: the pair's absolute
+// kept-prefix).  T = w's boundary bits, lb = lastb[w-1], nb = nextb[w+1],
+// kw = w's kept bits, Pw = Pfx(32 w).  The prefixes of the groups entering
+// and leaving the word are warp-uniform (two lookups per word); only a word
+// that holds a boundary needs per-lane in-word start / end bits.
+__device__ __forceinline__ uint32_t word_r2(uint32_t T, uint32_t sp, uint32_t ep, uint32_t kw, uint32_t Pw) {
+  if (T == 0u) return sp + ep + 1u;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t le = 0xFFFFFFFFu >> (31u - lane);
+  const uint32_t mS = T & le, mE = T & ~le;
+  const uint32_t ps = mS ? Pw + __popc(kw & ((1u << (31u - __clz(mS))) - 1u)) : sp;
+  const uint32_t pe = mE ? Pw + __popc(kw & ((1u << (__ffs(mE) - 1u)) - 1u)) : ep;
+  return ps + pe + 1u;
+}
+template <class PfxF>
+__device__ __forceinline__ uint32_t tied_r2(uint32_t T, uint32_t lb, uint32_t nb, uint32_t n, uint32_t kw,
+                                            uint32_t Pw, PfxF&& pfx) {
+  const uint32_t sp = (T & 1u) ? Pw : pfx(lb);  // group holding lane 0 starts at or before 32 w
+  // group holding lane 31 ends at nb (past the sentinel word nextb is
+  // unset: clamp; only lanes beyond the feature's length read it there)
+  const uint32_t ep = pfx(min(nb, n));
+  return word_r2(T, sp, ep, kw, Pw);
+}
+
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
 }
@@ -94,7 +132,7 @@ __device__ __forceinline__ unsigned long long sq_closed(unsigned long long n) {
 
 // Shared-memory layout, in 32-bit words (all regions 16-byte aligned).
 struct WalkLayout {
-  uint32_t inv16, R16, tbh, lbh16, nbh16, par, K, Pl;
+  uint32_t inv16, R16, tbh, lbh16, nbh16, par, K, Pl, SE;
   uint32_t og16[2], tbg[2], lbg16[2], nbg16[2];
   uint32_t words;
   __host__ __device__ WalkLayout(int64_t ldo, int64_t ldt, bool ogs, bool r2) {
@@ -110,8 +148,13 @@ struct WalkLayout {
     lbh16 = take(ldt * 2) * 2;
     nbh16 = take(ldt * 2) * 2;
     par = r2 ? 0 : take(ldt * 4);
-    K = take(ldt * 4);
-    Pl = r2 ? take(ldt * 4) : take(ldt * 2) * 2;  // word prefixes; 16-bit when S > 32767 (fits 227 KB)
+    // per word of the walked order: kept bits K, segment-relative prefix P and
+    // (R2 tied passes) the prefixes of the tie groups entering / leaving it;
+    // for R2 one 16-byte record {K, P, sp, ep} per word (one LDS.128), else
+    // K and a 16-bit P (S > 32767 must fit 227 KB)
+    K = r2 ? take(ldt * 16) : take(ldt * 4);
+    Pl = r2 ? 0 : take(ldt * 2) * 2;
+    SE = 0;
     for (int b = 0; b < 2; ++b) {
       og16[b] = ogs ? take(ldo * 2) * 2 : 0;
       tbg[b] = ogs ? take(ldt * 4) : 0;
@@ -138,14 +181,17 @@ __device__ __forceinline__ void segment_bases(const uint32_t* wtot, uint32_t& se
 }
 
 #ifdef PS_WALK_TIMING
-__device__ unsigned long long g_walk_cycles[16];
-#define WT(i)                                                         \
-  do {                                                                \
-    if (threadIdx.x == 0) {                                           \
-      const long long _t = clock64();                                 \
-      atomicAdd(&g_walk_cycles[i], (unsigned long long)(_t - _tw));   \
-      _tw = _t;                                                       \
-    }                                                                 \
+// cycles per phase, split by pair class (tied g) + 2 (tied h): [cls * 8 + phase],
+// pair counts per class at [32 + cls]
+__device__ unsigned long long g_walk_cycles[40];
+#define WT(i)                                                                  \
+  do {                                                                         \
+    if (threadIdx.x == 0) {                                                    \
+      const long long _t = clock64();                                          \
+      atomicAdd(&g_walk_cycles[_wcls * 8 + (i)], (unsigned long long)(_t - _tw)); \
+      if ((i) == 6) atomicAdd(&g_walk_cycles[32 + _wcls], 1ull);               \
+      _tw = _t;                                                                \
+    }                                                                          \
   } while (0)
 #else
 #define WT(i) \
@@ -168,19 +214,54 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm32);
-  const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + (R2 ? 4 : 2) * L.Pl;
+  const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + 2 * L.Pl;
   const uint32_t aPar = sb + 4 * L.par;
+  auto kA = [&](uint32_t w) -> uint32_t { return R2 ? aK + 16 * w : aK + 4 * w; };
+  auto stK = [&](uint32_t w, uint32_t v) { st32(kA(w), v); };
   const uint32_t aTbh = sb + 4 * L.tbh, aLbh = sb + 2 * L.lbh16, aNbh = sb + 2 * L.nbh16;
   const uint32_t ltmask = lanemask_lt();
-  auto ldP = [&](uint32_t w) -> uint32_t { return R2 ? ld32(aP + 4 * w) : ld16(aP + 2 * w); };
+  auto ldP = [&](uint32_t w) -> uint32_t { return R2 ? ld32(aK + 16 * w + 4) : ld16(aP + 2 * w); };
   auto stP = [&](uint32_t w, uint32_t v) {
-    if (R2) st32(aP + 4 * w, v);
+    if (R2) st32(aK + 16 * w + 4, v);
     else st16(aP + 2 * w, v);
+  };
+  auto stKP = [&](uint32_t w, uint32_t k, uint32_t pv) {  // phase 1, lane 0
+    if (R2) {
+      st64(aK + 16 * w, k, pv);
+    } else {
+      stK(w, k);
+      st16(aP + 2 * w, pv);
+    }
   };
   // absolute kept-prefix of position x: P[x/32] + popc(bits of K below x)
   auto pfx = [&](uint32_t x) -> uint32_t {
     const uint32_t w = x >> 5;
-    return ldP(w) + __popc(ld32(aK + 4 * w) & ((1u << (x & 31u)) - 1u));
+    return ldP(w) + __popc(ld32(kA(w)) & ((1u << (x & 31u)) - 1u));
+  };
+
+  // R2 tied passes: for each of this warp's words [w0, w1) of a feature of
+  // length nf, store (Pfx(start of the tie group entering the word),
+  // Pfx(end of the group leaving it)) -- one lane per word, so phase 2 reads
+  // two warp-uniform values instead of resolving group bounds per element.
+  // Word prefixes are segment-relative; the base of another warp's segment
+  // is lane s of segpre (segment_bases), so no block barrier is needed.
+  auto fill_spep = [&](int w0, int w1, int Lseg, uint32_t segpre, uint32_t tot, uint32_t nf, auto&& Tat,
+                       auto&& LBat, auto&& NBat) {
+    const uint32_t own = __shfl_sync(PS_FULL, segpre, warp);
+    auto pabs = [&](uint32_t x) -> uint32_t {  // all lanes (shuffle inside)
+      const uint32_t wx = min(x, nf - 1u) >> 5;
+      const uint32_t base = __shfl_sync(PS_FULL, segpre, (int)(wx / (uint32_t)Lseg));
+      const uint32_t v = ldP(wx) + base + __popc(ld32(kA(wx)) & ((1u << (x & 31u)) - 1u));
+      return x >= nf ? tot : v;
+    };
+    for (int wb = w0; wb < w1; wb += 32) {
+      const int w = min(wb + lane, w1 - 1);
+      const uint32_t T = Tat(w);
+      const uint32_t ps = pabs(LBat(w ? w - 1 : 0));
+      const uint32_t pe = pabs(min(NBat(w + 1), nf));
+      if (wb + lane < w1) st64(aK + 16 * w + 8, (T & 1u) ? ldP(w) + own : ps, pe);
+    }
+    __syncwarp();
   };
 
   for (int64_t i = threadIdx.x; i < ldo; i += STH) SM16[L.R16 + i] = 0;
@@ -254,6 +335,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         asm volatile("cp.async.wait_group 1;");
         __syncthreads();
       }
+#ifdef PS_WALK_TIMING
+      const int _wcls = (tg ? 1 : 0) + (th ? 2 : 0);
+#endif
       WT(0);
       const uint32_t aOg = sb + 2 * L.og16[buf];
       const uint32_t aTbg = sb + 4 * L.tbg[buf], aLbg = sb + 2 * L.lbg16[buf], aNbg = sb + 2 * L.nbg16[buf];
@@ -296,10 +380,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t q = ld16(aInv + 2 * s);
           if (OGS) st16(aOg + 2 * p, q);
           const uint32_t B = __ballot_sync(PS_FULL, q != 0xFFFFu);
-          if (lane == 0) {
-            st32(aK + 4 * word, B);
-            stP(word, cnt);
-          }
+          if (lane == 0) stKP(word, B, cnt);
           cnt += __popc(B);
         }
         if (lane == 0) wtot[warp] = cnt;
@@ -310,10 +391,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         uint32_t segpre;
         segment_bases(wtot, segpre, n);
         abase = __shfl_sync(PS_FULL, segpre, warp);
-        if (tg) {  // absolute prefixes for arbitrary-position lookups
+        if (tg && R2) {
+          if (OGS)
+            fill_spep(a0, a1, La, segpre, n, (uint32_t)ng, [&](int w) { return ld32(aTbg + 4 * w); },
+                      [&](int w) { return ld16(aLbg + 2 * w); }, [&](int w) { return ld16(aNbg + 2 * w); });
+          else
+            fill_spep(a0, a1, La, segpre, n, (uint32_t)ng, [&](int w) { return tb[g * ldt + w]; },
+                      [&](int w) { return (uint32_t)lastb[g * ldt + w]; },
+                      [&](int w) { return (uint32_t)nextb[g * ldt + w]; });
+        } else if (tg) {  // absolute prefixes for arbitrary-position lookups
           for (int w = a0 + lane; w < a1; w += 32) stP(w, ldP(w) + abase);
           if (threadIdx.x == 0) {
-            st32(aK + 4 * nwa, 0u);
+            stK(nwa, 0u);
             stP(nwa, n);
           }
           __syncthreads();
@@ -325,28 +414,44 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       if (!tg) {
 #pragma unroll 4
         for (int word = a0; word < a1; ++word) {
-          const uint32_t kw = ld32(aK + 4 * word);
+          const uint32_t kw = ld32(kA(word));
           const uint32_t r = abase + ldP(word) + __popc(kw & ltmask) + 1u;
           const uint32_t q = q_at((uint32_t)(word * 32 + lane));
           if ((kw >> lane) & 1u) st16(aR + 2 * q, R2 ? 2u * r : r);
+        }
+      } else if (R2) {
+        const uint32_t* tbgg = tb + g * ldt;
+#pragma unroll 2
+        for (int word = a0; word < a1; ++word) {
+          const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
+          const uint32_t kw = rec.x;
+          const uint32_t T = OGS ? ld32(aTbg + 4 * word) : tbgg[word];
+          const uint32_t r2 = word_r2(T, rec.z, rec.w, kw, rec.y + abase);
+          if ((kw >> lane) & 1u) {
+            const uint32_t q = q_at((uint32_t)(word * 32 + lane));
+            sa2 += (unsigned long long)r2 * r2;
+            st16(aR + 2 * q, r2);
+          }
         }
       } else {
         const uint32_t* tbgg = tb + g * ldt;
         const uint16_t* lbgg = lastb + g * ldt;
         const uint16_t* nbgg = nextb + g * ldt;
         for (int word = a0; word < a1; ++word) {
-          const uint32_t kw = ld32(aK + 4 * word);
+          const uint32_t kw = ld32(kA(word));
           const uint32_t p = (uint32_t)(word * 32 + lane);
+          uint32_t T, lb, nb;
+          if (OGS) {
+            T = ld32(aTbg + 4 * word);
+            lb = ld16(aLbg + 2 * (word ? word - 1 : 0));
+            nb = ld16(aNbg + 2 * (word + 1));
+          } else {
+            T = tbgg[word];
+            lb = lbgg[word ? word - 1 : 0];
+            nb = nbgg[word + 1];
+          }
+          const uint32_t r2 = tied_r2(T, lb, nb, (uint32_t)ng, kw, ldP(word), pfx);
           if ((kw >> lane) & 1u) {
-            uint32_t xs, xe;
-            if (OGS) {
-              xs = tstart_a(aTbg, aLbg, p);
-              xe = tend_a(aTbg, aNbg, p);
-            } else {
-              xs = tie_start(tbgg, lbgg, p);
-              xe = tie_end(tbgg, nbgg, p);
-            }
-            const uint32_t r2 = pfx(xs) + pfx(xe) + 1u;
             const uint32_t q = q_at(p);
             sa2 += (unsigned long long)r2 * r2;
             if (R2) {
@@ -396,10 +501,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         for (int word = b0; word < b1; ++word) {
           const bool keep = ld16(aR + 2 * (uint32_t)(word * 32 + lane)) != 0u;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
-          if (lane == 0) {
-            st32(aK + 4 * word, B);
-            stP(word, cnt);
-          }
+          if (lane == 0) stKP(word, B, cnt);
           cnt += __popc(B);
         }
         if (lane == 0) wtot[warp] = cnt;
@@ -411,10 +513,13 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         uint32_t segpre, tot;
         segment_bases(wtot, segpre, tot);
         bbase = __shfl_sync(PS_FULL, segpre, warp);
-        if (th) {
+        if (th && R2) {
+          fill_spep(b0, b1, Lb, segpre, tot, (uint32_t)nh, [&](int w) { return ld32(aTbh + 4 * w); },
+                    [&](int w) { return ld16(aLbh + 2 * w); }, [&](int w) { return ld16(aNbh + 2 * w); });
+        } else if (th) {
           for (int w = b0 + lane; w < b1; w += 32) stP(w, ldP(w) + bbase);
           if (threadIdx.x == 0) {
-            st32(aK + 4 * nwb, 0u);
+            stK(nwb, 0u);
             stP(nwb, tot);
           }
           __syncthreads();
@@ -424,7 +529,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       if (!th) {
 #pragma unroll 4
         for (int word = b0; word < b1; ++word) {
-          const uint32_t kw = ld32(aK + 4 * word);
+          const uint32_t kw = ld32(kA(word));
           const uint32_t q = (uint32_t)(word * 32 + lane);
           const uint32_t v = ld16(aR + 2 * q);
           const uint32_t r2g = r2g_of(v, word);
@@ -439,14 +544,30 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           }
         }
         sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
-      } else {
+      } else if (R2) {
+#pragma unroll 2
         for (int word = b0; word < b1; ++word) {
-          const uint32_t kw = ld32(aK + 4 * word);
+          const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
+          const uint32_t kw = rec.x;
           const uint32_t q = (uint32_t)(word * 32 + lane);
           const uint32_t v = ld16(aR + 2 * q);
           const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
+          const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
           if ((kw >> lane) & 1u) {
-            const uint32_t r2h = pfx(tstart_a(aTbh, aLbh, q)) + pfx(tend_a(aTbh, aNbh, q)) + 1u;
+            sab += (unsigned long long)r2g * r2h;
+            sbb += (unsigned long long)r2h * r2h;
+            st16(aR + 2 * q, 0u);
+          }
+        }
+      } else {
+        for (int word = b0; word < b1; ++word) {
+          const uint32_t kw = ld32(kA(word));
+          const uint32_t q = (uint32_t)(word * 32 + lane);
+          const uint32_t v = ld16(aR + 2 * q);
+          const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
+          const uint32_t r2h = tied_r2(ld32(aTbh + 4 * word), ld16(aLbh + 2 * (word ? word - 1 : 0)),
+                                       ld16(aNbh + 2 * (word + 1)), (uint32_t)nh, kw, ldP(word), pfx);
+          if ((kw >> lane) & 1u) {
             sab += (unsigned long long)r2g * r2h;
             sbb += (unsigned long long)r2h * r2h;
             st16(aR + 2 * q, 0u);
@@ -615,7 +736,7 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
 
 #ifdef PS_WALK_TIMING
 extern "C" int ps_debug_walk_cycles(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, g_walk_cycles, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out, g_walk_cycles, sizeof(unsigned long long) * 40);
   return 0;
 }
 #endif

@@ -57,12 +57,16 @@ def dump_walk_cycles():
     lib = _lib.load()
     if not os.environ.get("PS_LIB") or not hasattr(lib, "ps_debug_walk_cycles"):
         return
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 40)()
     lib.ps_debug_walk_cycles(buf)
     names = ["wait+prefetch", "passA phase1", "scanA", "passA phase2", "scanB", "passB", "reduce+final"]
-    tot = sum(buf[i] for i in range(7))
-    for i, n in enumerate(names):
-        print(f"{n:16s} {buf[i]:16d} {100.0 * buf[i] / max(tot, 1):6.1f}%")
+    tot = sum(buf[i] for i in range(32)) or 1
+    for cls, cname in enumerate(["untied", "tied g", "tied h", "tied both"]):
+        n = buf[32 + cls]
+        c = sum(buf[cls * 8 + i] for i in range(7))
+        print(f"{cname:10s} pairs {n:9d}  share {100.0 * c / tot:5.1f}%  cycles/pair {c / max(n, 1):9.0f}")
+        for i, nm in enumerate(names):
+            print(f"    {nm:16s} {buf[cls * 8 + i] / max(n, 1):9.0f}")
 
 
 if __name__ == "__main__":
