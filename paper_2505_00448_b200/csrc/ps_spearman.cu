@@ -45,6 +45,20 @@ struct PairSums {
   long long* sxy4;
 };
 
+// Per-warp partial sums of one chunk of g rows [c0, c1): the walk writes them
+// without a block-wide reduction (no barrier at the end of a pair), the
+// partials kernel folds them into PairSums.
+//   part[(g - c0) * F + h][slot][warp]: slot 0 sum (2r_g)^2 (tied g),
+//   slot 1 sum (2r_g)(r_h or 2r_h), slot 2 sum (2r_h)^2 (tied h) or, for the
+//   one-sweep tie-free h walk, sum 2r_g | (segment kept count << 40)
+//   meta[(g - c0) * F + h] = n | tied g << 40 | tied h << 41 | sweep << 42
+struct PairParts {
+  unsigned long long* part;
+  unsigned long long* meta;
+  int64_t c0;
+};
+constexpr int kSlots = 3;
+
 // All shared-memory regions are addressed as integer offsets into two views of
 // the one dynamic buffer, so every access compiles to LDS/STS (no generic
 // pointers, no per-access window conversion).
@@ -102,13 +116,17 @@ __device__ __forceinline__ uint32_t tend_a(uint32_t aT, uint32_t aN, uint32_t p)
 // kw = w's kept bits, Pw = Pfx(32 w).  The prefixes of the groups entering
 // and leaving the word are warp-uniform (two lookups per word); only a word
 // that holds a boundary needs per-lane in-word start / end bits.
+// (branch-free: selects only, so the word loops unroll)
 __device__ __forceinline__ uint32_t word_r2(uint32_t T, uint32_t sp, uint32_t ep, uint32_t kw, uint32_t Pw) {
-  if (T == 0u) return sp + ep + 1u;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t le = 0xFFFFFFFFu >> (31u - lane);
   const uint32_t mS = T & le, mE = T & ~le;
-  const uint32_t ps = mS ? Pw + __popc(kw & ((1u << (31u - __clz(mS))) - 1u)) : sp;
-  const uint32_t pe = mE ? Pw + __popc(kw & ((1u << (__ffs(mE) - 1u)) - 1u)) : ep;
+  // start bit s = highest set bit of mS; kept lanes below s: kw & (2^s - 1)
+  const uint32_t belowS = mS ? (0xFFFFFFFFu >> __clz(mS)) >> 1 : 0u;
+  // end bit e = lowest set bit of mE; kept lanes below e: kw & (2^e - 1)
+  const uint32_t belowE = (mE & (0u - mE)) - 1u;
+  const uint32_t ps = mS ? Pw + __popc(kw & belowS) : sp;
+  const uint32_t pe = mE ? Pw + __popc(kw & belowE) : ep;
   return ps + pe + 1u;
 }
 template <class PfxF>
@@ -207,10 +225,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
                      const int32_t* __restrict__ lens, int64_t F, int64_t lo, int64_t hi,
-                     int* __restrict__ queue, PairSums out) {
+                     int* __restrict__ queue, PairParts out) {
   const WalkLayout L(ldo, ldt, OGS, R2);
-  __shared__ uint32_t wtot[SW], wtotA[SW], wtotB[SW];
-  __shared__ unsigned long long red[SW][3];
+  __shared__ uint32_t wtot[SW], wtotA[SW];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm32);
@@ -333,8 +350,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         if (g + 1 <= gmax) prefetch(g + 1, buf ^ 1);
         else asm volatile("cp.async.commit_group;");
         asm volatile("cp.async.wait_group 1;");
-        __syncthreads();
       }
+      // the previous pair's pass B (reads / clears R, reads the word records)
+      // is complete in every warp before this pair's pass A writes them
+      __syncthreads();
 #ifdef PS_WALK_TIMING
       const int _wcls = (tg ? 1 : 0) + (th ? 2 : 0);
 #endif
@@ -421,7 +440,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
       } else if (R2) {
         const uint32_t* tbgg = tb + g * ldt;
-#pragma unroll 2
+#pragma unroll 4
         for (int word = a0; word < a1; ++word) {
           const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
           const uint32_t kw = rec.x;
@@ -474,6 +493,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       };
       const bool sweepB = R2 && !th;
       unsigned long long sab = 0, sbb = 0, s0 = 0;
+      uint32_t wtotB = 0;
       if (sweepB) {
         // Tie-free h: one sweep; per warp sum r2g * local_h and sum r2g, the
         // segment bases of h's order are folded in after the reduction.
@@ -492,7 +512,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           }
           cnt += __popc(B);
         }
-        if (lane == 0) wtotB[warp] = cnt;
+        wtotB = cnt;
       } else {
       // ---------------- pass B, phase 1: keep = R != 0 over h's order ------
       {
@@ -545,7 +565,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
         sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
       } else if (R2) {
-#pragma unroll 2
+#pragma unroll 4
         for (int word = b0; word < b1; ++word) {
           const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
           const uint32_t kw = rec.x;
@@ -553,11 +573,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t v = ld16(aR + 2 * q);
           const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
           const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
-          if ((kw >> lane) & 1u) {
-            sab += (unsigned long long)r2g * r2h;
-            sbb += (unsigned long long)r2h * r2h;
-            st16(aR + 2 * q, 0u);
-          }
+          const uint32_t r2hk = (kw >> lane) & 1u ? r2h : 0u;
+          sab += (unsigned long long)r2g * r2hk;  // r2g = 0 where not kept
+          sbb += (unsigned long long)r2hk * r2hk;
+          st16(aR + 2 * q, 0u);                   // unkept positions hold 0 already
         }
       } else {
         for (int word = b0; word < b1; ++word) {
@@ -580,45 +599,75 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       }
       }  // two-phase pass B
       WT(5);
-      // ---------------- reduce and store the exact sums ---------------------
+      // ---------------- per-warp partial sums -> global ---------------------
+      // (no block barrier: the next pair's top barrier orders R / record reuse)
+      unsigned long long c = sweepB ? s0 : sbb;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         sa2 += __shfl_xor_sync(PS_FULL, sa2, o);
         sab += __shfl_xor_sync(PS_FULL, sab, o);
-        sbb += __shfl_xor_sync(PS_FULL, sbb, o);
-        s0 += __shfl_xor_sync(PS_FULL, s0, o);
+        c += __shfl_xor_sync(PS_FULL, c, o);
       }
+      const int64_t cell = (g - out.c0) * F + h;
       if (lane == 0) {
-        red[warp][0] = sa2;
-        red[warp][1] = sab;
-        red[warp][2] = sweepB ? s0 : sbb;
+        unsigned long long* pp = out.part + cell * (kSlots * SW) + warp;
+        pp[0] = sa2;
+        pp[SW] = sab;
+        pp[2 * SW] = sweepB ? c | ((unsigned long long)wtotB << 40) : c;
       }
-      __syncthreads();
-      if (threadIdx.x < 3) {
-        unsigned long long v = 0;
-        for (int w = 0; w < SW; ++w) v += red[w][threadIdx.x];
-        const int64_t cell = g * F + h;
-        if (threadIdx.x == 0) {
-          out.sxx4[cell] = (long long)(tg ? v : kClosed);
-          out.n[cell] = (long long)n;
-        } else if (threadIdx.x == 1) {
-          if (sweepB) {
-            // sum over warps of 2 * (sum r2g*local + base_w * sum r2g)
-            unsigned long long acc = 0, base = 0;
-            for (int w = 0; w < SW; ++w) {
-              acc += 2ull * (red[w][1] + base * red[w][2]);
-              base += wtotB[w];
-            }
-            v = acc;
-          }
-          out.sxy4[cell] = (long long)v;
-        } else {
-          out.syy4[cell] = (long long)(th ? v : kClosed);  // (sweepB implies !th)
-        }
-      }
+      if (threadIdx.x == 0)
+        out.meta[cell] = (unsigned long long)n | ((unsigned long long)tg << 40) |
+                         ((unsigned long long)th << 41) | ((unsigned long long)sweepB << 42);
       WT(6);
     }
     if (OGS) asm volatile("cp.async.wait_group 0;");
+  }
+}
+
+// One warp per (g, h) cell of chunk [c0, c1): fold the SW per-warp partials
+// into the exact 4x sums (tie-free walks: the closed-form sentinel).
+__global__ void spearman_partials_kernel(PairParts in, int64_t F, int64_t c1, PairSums out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ncell = (c1 - in.c0) * F;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t cell = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); cell < ncell;
+       cell += nwarps) {
+    const int64_t g = in.c0 + cell / F, h = cell % F;
+    if (h < g) continue;  // warp-uniform
+    const unsigned long long meta = in.meta[cell];
+    const bool tg = (meta >> 40) & 1, th = (meta >> 41) & 1, sweep = (meta >> 42) & 1;
+    const unsigned long long* pp = in.part + cell * (kSlots * SW);
+    unsigned long long a = 0, b = 0, c = 0;
+    if (lane < SW) {
+      a = pp[lane];
+      b = pp[SW + lane];
+      c = pp[2 * SW + lane];
+    }
+    if (sweep) {
+      // sum_w 2 (sum r2g * local_h + base_w * sum r2g), base_w = kept count
+      // of the h segments before w
+      const unsigned long long s0 = c & ((1ull << 40) - 1), cnt = c >> 40;
+      unsigned long long x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(PS_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      b = lane < SW ? 2ull * (b + (x - cnt) * s0) : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(PS_FULL, a, o);
+      b += __shfl_xor_sync(PS_FULL, b, o);
+      c += __shfl_xor_sync(PS_FULL, c, o);
+    }
+    if (lane == 0) {
+      const int64_t o = g * F + h;
+      out.n[o] = (long long)(meta & ((1ull << 40) - 1));
+      out.sxx4[o] = (long long)(tg ? a : kClosed);
+      out.sxy4[o] = (long long)b;
+      out.syy4[o] = (long long)(th ? c : kClosed);
+    }
   }
 }
 
@@ -714,13 +763,29 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   int per_sm = 0;
   PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, STH, smem));
   per_sm = std::max(1, per_sm);
-  const int64_t items = F - lo;
-  const int grid = (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
-  ps_prof_begin("spearman_walk", s);
-  kern<<<grid, STH, smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
-                               a->d_tied, a->d_len, F, lo, hi, queue, ps);
-  ps_prof_end(s);
-  PS_LAUNCHED();
+  // g rows per chunk: the per-warp partials take kSlots * SW * 8 B per cell
+  const int64_t per_row = F * (int64_t)(kSlots * SW + 1) * 8;
+  const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(hi - lo, ((int64_t)2 << 30) / per_row));
+  PairParts pp{nullptr, nullptr, lo};
+  PS_CUDA(ps_alloc(&pp.part, (size_t)(rows * F * kSlots * SW), s));
+  PS_CUDA(ps_alloc(&pp.meta, (size_t)(rows * F), s));
+  for (int64_t c0 = lo; c0 < hi; c0 += rows) {
+    const int64_t c1 = std::min<int64_t>(hi, c0 + rows);
+    pp.c0 = c0;
+    if (c0 > lo) PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+    const int64_t items = F - c0;
+    const int grid = (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
+    ps_prof_begin("spearman_walk", s);
+    kern<<<grid, STH, smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
+                                 a->d_tied, a->d_len, F, c0, c1, queue, pp);
+    ps_prof_end(s);
+    PS_LAUNCHED();
+    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((c1 - c0) * F, 8), (int64_t)ds->num_sms * 32);
+    spearman_partials_kernel<<<pblocks, 256, 0, s>>>(pp, F, c1, ps);
+    PS_LAUNCHED();
+  }
+  ps_free(pp.part, s);
+  ps_free(pp.meta, s);
   }
   const int64_t total = (hi - lo) * F;
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
