@@ -365,10 +365,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       const int nwa = (ng + 31) >> 5;
       const int La = (nwa + SW - 1) / SW;
       const int a0 = min(nwa, warp * La), a1 = min(nwa, a0 + La);
-      // Tie-free g (and R holding 2r): one sweep.  R[q] = (warp << 11) | local
+      // Tie-free g: one sweep.  R[q] = (warp << 12) | local
       // rank within the warp's segment; the segment bases are folded in by
       // pass B, so no prefix phase is needed here.
-      const bool encA = R2 && !tg && La * 32 <= 2047;
+      const bool encA = !tg && La * 32 <= 4095;
       uint32_t segpreA = 0, n = 0, abase = 0;
       unsigned long long sa2 = 0;
       if (encA) {
@@ -380,7 +380,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           const uint32_t q = ld16(aInv + 2 * s);
           const bool keep = q != 0xFFFFu;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
-          if (keep) st16(aR + 2 * q, ((uint32_t)warp << 11) | (cnt + __popc(B & ltmask) + 1u));
+          if (keep) st16(aR + 2 * q, ((uint32_t)warp << 12) | (cnt + __popc(B & ltmask) + 1u));
           cnt += __popc(B);
         }
         if (lane == 0) wtotA[warp] = cnt;
@@ -487,11 +487,11 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       WT(3);
       // decode R -> 2 r_g (all lanes must execute: shuffles)
       auto r2g_of = [&](uint32_t v, int word) -> uint32_t {
-        if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> 11)) + (v & 0x7FFu));
+        if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu));
         if (R2) return v;
         return 2u * v + (tg ? ((ld32(aPar + 4 * word) >> lane) & 1u) : 0u);
       };
-      const bool sweepB = R2 && !th;
+      const bool sweepB = !th;
       unsigned long long sab = 0, sbb = 0, s0 = 0;
       uint32_t wtotB = 0;
       if (sweepB) {
@@ -511,6 +511,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             st16(aR + 2 * q, 0u);
           }
           cnt += __popc(B);
+          if (!R2 && tg) {  // parity bits of this word were read above
+            __syncwarp();
+            if (lane == 0) st32(aPar + 4 * word, 0u);
+          }
         }
         wtotB = cnt;
       } else {
