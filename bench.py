@@ -385,6 +385,8 @@ def main():
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
+        if os.environ.get("PS_BENCH_VERBOSE"):
+            print("step ms %.3f" % times[-1], file=sys.stderr)
     blocks.sync(stream)
     torch.cuda.synchronize()
     if world > 1:

@@ -32,6 +32,7 @@
 #include "ps_specfun.cuh"
 #include "ps_ties.cuh"
 #include <algorithm>
+#include <type_traits>
 
 namespace {
 
@@ -497,25 +498,32 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       if (sweepB) {
         // Tie-free h: one sweep; per warp sum r2g * local_h and sum r2g, the
         // segment bases of h's order are folded in after the reduction.
-        uint32_t cnt = 0;
+        uint32_t cnt = 0, s0l = 0;  // s0l: per lane <= 2S * (words per warp) < 2^32
+        auto sweep = [&](auto enc) {
 #pragma unroll 4
-        for (int word = b0; word < b1; ++word) {
-          const uint32_t q = (uint32_t)(word * 32 + lane);
-          const uint32_t v = ld16(aR + 2 * q);
-          const bool keep = v != 0u;
-          const uint32_t B = __ballot_sync(PS_FULL, keep);
-          const uint32_t r2g = r2g_of(v, word);
-          if (keep) {
-            sab += (unsigned long long)r2g * (cnt + __popc(B & ltmask) + 1u);
-            s0 += r2g;
-            st16(aR + 2 * q, 0u);
+          for (int word = b0; word < b1; ++word) {
+            const uint32_t q = (uint32_t)(word * 32 + lane);
+            const uint32_t v = ld16(aR + 2 * q);
+            const bool keep = v != 0u;
+            const uint32_t B = __ballot_sync(PS_FULL, keep);
+            uint32_t r2g;
+            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu)) << 1;
+            else r2g = r2g_of(v, word);
+            if (keep) {
+              sab += (unsigned long long)r2g * (cnt + __popc(B & ltmask) + 1u);
+              s0l += r2g;
+              st16(aR + 2 * q, 0u);
+            }
+            cnt += __popc(B);
+            if (!R2 && tg) {  // parity bits of this word were read above
+              __syncwarp();
+              if (lane == 0) st32(aPar + 4 * word, 0u);
+            }
           }
-          cnt += __popc(B);
-          if (!R2 && tg) {  // parity bits of this word were read above
-            __syncwarp();
-            if (lane == 0) st32(aPar + 4 * word, 0u);
-          }
-        }
+        };
+        if (encA) sweep(std::true_type{});
+        else sweep(std::false_type{});
+        s0 = s0l;
         wtotB = cnt;
       } else {
       // ---------------- pass B, phase 1: keep = R != 0 over h's order ------
@@ -569,19 +577,25 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
         sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
       } else if (R2) {
+        auto walk2 = [&](auto enc) {
 #pragma unroll 4
-        for (int word = b0; word < b1; ++word) {
-          const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
-          const uint32_t kw = rec.x;
-          const uint32_t q = (uint32_t)(word * 32 + lane);
-          const uint32_t v = ld16(aR + 2 * q);
-          const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
-          const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
-          const uint32_t r2hk = (kw >> lane) & 1u ? r2h : 0u;
-          sab += (unsigned long long)r2g * r2hk;  // r2g = 0 where not kept
-          sbb += (unsigned long long)r2hk * r2hk;
-          st16(aR + 2 * q, 0u);                   // unkept positions hold 0 already
-        }
+          for (int word = b0; word < b1; ++word) {
+            const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
+            const uint32_t kw = rec.x;
+            const uint32_t q = (uint32_t)(word * 32 + lane);
+            const uint32_t v = ld16(aR + 2 * q);
+            uint32_t r2g;  // all lanes (shuffle)
+            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu)) << 1;
+            else r2g = v;
+            const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
+            const uint32_t r2hk = (kw >> lane) & 1u ? r2h : 0u;
+            sab += (unsigned long long)r2g * r2hk;  // r2g is meaningless where not kept: r2hk = 0
+            sbb += (unsigned long long)r2hk * r2hk;
+            st16(aR + 2 * q, 0u);                   // unkept positions hold 0 already
+          }
+        };
+        if (encA) walk2(std::true_type{});
+        else walk2(std::false_type{});
       } else {
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(kA(word));
