@@ -144,6 +144,15 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
 }
 
+// Exact warp sum of 64-bit lane values: three 22-bit slices through the
+// integer warp-reduce unit (each slice sum < 2^27).
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
+  const uint32_t s0 = __reduce_add_sync(PS_FULL, (uint32_t)(x & 0x3FFFFFu));
+  const uint32_t s1 = __reduce_add_sync(PS_FULL, (uint32_t)((x >> 22) & 0x3FFFFFu));
+  const uint32_t s2 = __reduce_add_sync(PS_FULL, (uint32_t)(x >> 44));
+  return (unsigned long long)s0 + ((unsigned long long)s1 << 22) + ((unsigned long long)s2 << 44);
+}
+
 // sum_{k=1..n} (2k)^2: the rank-square total of a tie-free walk
 __device__ __forceinline__ unsigned long long sq_closed(unsigned long long n) {
   return 4ull * (n * (n + 1) * (2 * n + 1) / 6ull);
@@ -620,12 +629,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // ---------------- per-warp partial sums -> global ---------------------
       // (no block barrier: the next pair's top barrier orders R / record reuse)
       unsigned long long c = sweepB ? s0 : sbb;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sa2 += __shfl_xor_sync(PS_FULL, sa2, o);
-        sab += __shfl_xor_sync(PS_FULL, sab, o);
-        c += __shfl_xor_sync(PS_FULL, c, o);
-      }
+      if (tg) sa2 = warp_sum64(sa2);
+      sab = warp_sum64(sab);
+      c = warp_sum64(c);
       const int64_t cell = (g - out.c0) * F + h;
       if (lane == 0) {
         unsigned long long* pp = out.part + cell * (kSlots * SW) + warp;
