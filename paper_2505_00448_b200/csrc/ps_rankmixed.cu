@@ -270,21 +270,25 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       // -------- reduce to the pair's exact sums --------
 #pragma unroll
       for (int j = 0; j < (BIG ? 0 : NR); ++j) {
-        unsigned long long a = acc[j];
-        uint32_t c = cnt[j];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(PS_FULL, a, o);
-          c += __shfl_xor_sync(PS_FULL, c, o);
-        }
+        // per lane: sum of local ranks < 2^20 (tie-free sweep) or of 2r < 2^24
+        // (tied walk), so the warp sums fit 32 bits: integer warp reduce
+        const uint32_t a = __reduce_add_sync(PS_FULL, acc[j]);
+        const uint32_t c = __reduce_add_sync(PS_FULL, cnt[j]);
         if (lane == 0) {
           red_r[warp][j] = a;
           red_c[warp][j] = c;
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tie += __shfl_xor_sync(PS_FULL, tie, o);
-      if (lane == 0) red_t[warp] = tie;
+      {
+        // sum of t^3 - t (< 2^54): three 22-bit slices
+        const unsigned long long x = (unsigned long long)tie;
+        const uint32_t t0 = __reduce_add_sync(PS_FULL, (uint32_t)(x & 0x3FFFFFu));
+        const uint32_t t1 = __reduce_add_sync(PS_FULL, (uint32_t)((x >> 22) & 0x3FFFFFu));
+        const uint32_t t2 = __reduce_add_sync(PS_FULL, (uint32_t)(x >> 44));
+        if (lane == 0)
+          red_t[warp] = (long long)((unsigned long long)t0 + ((unsigned long long)t1 << 22) +
+                                    ((unsigned long long)t2 << 44));
+      }
       __syncthreads();
       const int64_t pair = g * Fq + h;
       if constexpr (BIG) {
