@@ -39,6 +39,7 @@ __device__ __forceinline__ bool key_is_nan(uint64_t k) {
 }
 
 // Block-wide exclusive scan of one int per thread; returns the block total.
+template <int NWARPS = NW>
 __device__ __forceinline__ int block_excl_scan(int v, int* warp_buf, int& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
@@ -50,17 +51,17 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_buf, int& total)
   if (lane == 31) warp_buf[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = lane < NW ? warp_buf[lane] : 0;
+    int w = lane < NWARPS ? warp_buf[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(PS_FULL, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < NW) warp_buf[lane] = w;  // inclusive
+    if (lane < NWARPS) warp_buf[lane] = w;  // inclusive
   }
   __syncthreads();
   const int before = warp > 0 ? warp_buf[warp - 1] : 0;
-  total = warp_buf[NW - 1];
+  total = warp_buf[NWARPS - 1];
   __syncthreads();
   return before + x - v;
 }
@@ -264,7 +265,7 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
 // OR over all keys).  Global traffic: values + mask in, order/inv/tie tables
 // out -- no per-pass HBM round trips.
 // ---------------------------------------------------------------------------
-constexpr int QT = 512;
+constexpr int QT = 1024;
 constexpr int QW = QT / 32;
 
 template <int ITEMS>
@@ -275,49 +276,40 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
                     int64_t ldt, uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
   constexpr int NMAX = QT * ITEMS;
   extern __shared__ __align__(16) unsigned char qsm[];
-  uint64_t* skey = reinterpret_cast<uint64_t*>(qsm);
+  uint64_t* skey = reinterpret_cast<uint64_t*>(qsm);  // full keys, once sorted
+  uint32_t* sk32 = reinterpret_cast<uint32_t*>(qsm);  // 32-bit pass keys (same bytes, earlier)
   uint16_t* sidx = reinterpret_cast<uint16_t*>(qsm + (size_t)NMAX * 8);
   __shared__ uint16_t wcnt[QW][256];
   __shared__ int warp_buf[QW];
   __shared__ unsigned long long s_and, s_or;
-  __shared__ int s_any_tie;
+  __shared__ int s_any_tie, s_long;
   const int64_t f = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* row = vals + f * ld;
   const uint32_t* mrow = mask + f * W;
 
-  // 1. stable compaction of present entries (sample order) into smem
+  // 1. stable compaction of present sample ids (sample order) into smem;
+  //    AND / OR over the keys for pass skipping
   if (threadIdx.x == 0) {
     s_and = ~0ull;
     s_or = 0ull;
     s_any_tie = 0;
+    s_long = 0;
   }
   int n = 0;
+  unsigned long long a = ~0ull, o = 0ull;
   for (int64_t base = 0; base < S; base += QT) {
     const int64_t s = base + threadIdx.x;
     const bool pres = s < S && ((mrow[s >> 5] >> (s & 31)) & 1u);
     int tot;
-    const int pos = block_excl_scan(pres ? 1 : 0, warp_buf, tot);
+    const int pos = block_excl_scan<QW>(pres ? 1 : 0, warp_buf, tot);
     if (pres) {
-      skey[n + pos] = sort_key(row[s]);
+      const uint64_t k = sort_key(row[s]);
+      a &= k;
+      o |= k;
       sidx[n + pos] = (uint16_t)s;
     }
     n += tot;
-  }
-  __syncthreads();
-  // 2. registers (warp-striped), AND/OR of keys for pass skipping
-  uint64_t key[ITEMS];
-  uint32_t idx[ITEMS];
-  unsigned long long a = ~0ull, o = 0ull;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int p = warp * 32 * ITEMS + i * 32 + lane;
-    key[i] = p < n ? skey[p] : ~0ull;  // padding sorts last
-    idx[i] = p < n ? sidx[p] : 0xFFFFu;
-    if (p < n) {
-      a &= key[i];
-      o |= key[i];
-    }
   }
 #pragma unroll
   for (int sft = 16; sft > 0; sft >>= 1) {
@@ -330,64 +322,119 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   }
   __syncthreads();
   const unsigned long long diff = s_and ^ s_or;
-  // 3. LSD passes over non-constant bytes
-  for (int d = 0; d < 8; ++d) {
-    const int shift = 8 * d;
-    if (((diff >> shift) & 0xffull) == 0 || n <= 1) continue;
-    for (int i = threadIdx.x; i < QW * 256; i += QT) (&wcnt[0][0])[i] = 0;
-    __syncthreads();
-    uint32_t loc[ITEMS];
+
+  // 2. Stable LSD radix sort on 32-bit halves of the key, registers
+  //    warp-striped (warp w, item i, lane l <-> position w*32*ITEMS + i*32 + l,
+  //    so (i, lane) order IS sequence order).  Round 0 sorts on the HIGH half
+  //    only (sign, exponent, top mantissa bits); the rare runs whose high
+  //    halves collide but whose full keys differ are then repaired by an
+  //    insertion sort on the full key.  A feature with a long colliding run
+  //    is re-sorted on both halves (round 1: low half, then high half).  The
+  //    32-bit pass keys are re-derived from the values through the sample id
+  //    (one gather per stage), so only 6 B per element move per pass.
+  uint32_t k32[ITEMS], idx[ITEMS];  // idx: sample id | in-warp offset << 16
+  for (int round = 0, st0 = 1; round < 2; ++round, st0 = 0) {
+    for (int st = st0; st < 2; ++st) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xff);
-      const uint32_t peers = __match_any_sync(PS_FULL, dg);
-      const uint32_t base = wcnt[warp][dg];
-      __syncwarp();
-      loc[i] = base + __popc(peers & lanemask_lt());
-      if ((peers >> lane) == 1u) wcnt[warp][dg] = (uint16_t)(base + __popc(peers));
-      __syncwarp();
-    }
-    __syncthreads();
-    // digit totals -> bucket starts -> per-warp starts (digit-major, warp order)
-    if (threadIdx.x < 256) {
-      uint32_t tot = 0;
-      for (int w = 0; w < QW; ++w) tot += wcnt[w][threadIdx.x];
-      // exclusive scan of totals across the 256 digits (8 warps)
-      uint32_t x = tot;
-#pragma unroll
-      for (int sft = 1; sft < 32; sft <<= 1) {
-        const uint32_t y = __shfl_up_sync(PS_FULL, x, sft);
-        if (lane >= sft) x += y;
+      for (int i = 0; i < ITEMS; ++i) {
+        const int p = warp * 32 * ITEMS + i * 32 + lane;
+        idx[i] = p < n ? sidx[p] : 0xFFFFu;
+        const uint64_t k = p < n ? sort_key(row[idx[i]]) : ~0ull;  // padding sorts last
+        k32[i] = st ? (uint32_t)(k >> 32) : (uint32_t)k;
+        if ((i & 7) == 7) asm volatile("" ::: "memory");  // <= 8 gathers in flight (registers)
       }
-      if (lane == 31) warp_buf[warp] = (int)x;
-      // (warps 0..7 participate; others skip)
-      asm volatile("bar.sync 1, 256;");
-      uint32_t before = 0;
-      for (int w = 0; w < warp; ++w) before += (uint32_t)warp_buf[w];
-      uint32_t run = before + x - tot;
-      for (int w = 0; w < QW; ++w) {
-        const uint32_t c = wcnt[w][threadIdx.x];
-        wcnt[w][threadIdx.x] = (uint16_t)0;  // reused below as start offsets (fits: < 2^16)
-        wcnt[w][threadIdx.x] = (uint16_t)run;
-        run += c;
+      __syncthreads();
+      for (int b = 0; b < 4; ++b) {
+        const int shift = 8 * b;
+        if (((diff >> (32 * st + shift)) & 0xffull) == 0 || n <= 1) continue;
+        for (int i = threadIdx.x; i < QW * 256; i += QT) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const uint32_t dg = (k32[i] >> shift) & 0xffu;
+          const uint32_t peers = __match_any_sync(PS_FULL, dg);
+          const uint32_t base = wcnt[warp][dg];
+          __syncwarp();
+          idx[i] = (idx[i] & 0xFFFFu) | ((base + __popc(peers & lanemask_lt())) << 16);
+          if ((peers >> lane) == 1u) wcnt[warp][dg] = (uint16_t)(base + __popc(peers));
+          __syncwarp();
+        }
+        __syncthreads();
+        // digit totals -> bucket starts -> per-warp starts (digit-major, warp order)
+        if (threadIdx.x < 256) {
+          uint32_t tot = 0;
+          for (int w = 0; w < QW; ++w) tot += wcnt[w][threadIdx.x];
+          // exclusive scan of totals across the 256 digits (8 warps)
+          uint32_t x = tot;
+#pragma unroll
+          for (int sft = 1; sft < 32; sft <<= 1) {
+            const uint32_t y = __shfl_up_sync(PS_FULL, x, sft);
+            if (lane >= sft) x += y;
+          }
+          if (lane == 31) warp_buf[warp] = (int)x;
+          // (warps 0..7 participate; others skip)
+          asm volatile("bar.sync 1, 256;");
+          uint32_t before = 0;
+          for (int w = 0; w < warp; ++w) before += (uint32_t)warp_buf[w];
+          uint32_t run = before + x - tot;
+          for (int w = 0; w < QW; ++w) {
+            const uint32_t c = wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = (uint16_t)run;  // start offsets (fit: < 2^16)
+            run += c;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const uint32_t dg = (k32[i] >> shift) & 0xffu;
+          const uint32_t dst = (uint32_t)wcnt[warp][dg] + (idx[i] >> 16);
+          sk32[dst] = k32[i];
+          sidx[dst] = (uint16_t)idx[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int p = warp * 32 * ITEMS + i * 32 + lane;
+          k32[i] = sk32[p];
+          idx[i] = sidx[p];
+        }
+        __syncthreads();
+      }
+    }
+    // full keys of the sorted order (overwrites the pass keys)
+    for (int p = threadIdx.x; p < n; p += QT) skey[p] = sort_key(row[sidx[p]]);
+    __syncthreads();
+    if (round == 1 || (uint32_t)diff == 0u) break;  // low halves all equal: sorted
+    // repair runs of equal high halves with differing full keys
+    for (int p = threadIdx.x; p < n; p += QT) {
+      const uint64_t k = skey[p];
+      if (p > 0 && (skey[p - 1] >> 32) == (k >> 32)) continue;  // not a run start
+      int e = p + 1;
+      bool mixed = false;
+      while (e < n && (skey[e] >> 32) == (k >> 32)) {
+        mixed |= skey[e] != k;
+        ++e;
+      }
+      if (!mixed) continue;
+      if (e - p > 64) {
+        s_long = 1;
+        continue;
+      }
+      for (int i = p + 1; i < e; ++i) {  // stable insertion sort of [p, e) by the full key
+        const uint64_t ki = skey[i];
+        const uint16_t xi = sidx[i];
+        int j = i - 1;
+        while (j >= p && skey[j] > ki) {
+          skey[j + 1] = skey[j];
+          sidx[j + 1] = sidx[j];
+          --j;
+        }
+        skey[j + 1] = ki;
+        sidx[j + 1] = xi;
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xff);
-      const uint32_t dst = (uint32_t)wcnt[warp][dg] + loc[i];
-      skey[dst] = key[i];
-      sidx[dst] = (uint16_t)idx[i];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int p = warp * 32 * ITEMS + i * 32 + lane;
-      key[i] = skey[p];
-      idx[i] = sidx[p];
-    }
-    __syncthreads();
+    if (!s_long) break;
   }
   // sorted keys are in smem (written by the compaction or the last pass)
   // 4. outputs
@@ -486,11 +533,11 @@ int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
     return PS_OK;
   };
   int rc = -1;
-  if (items <= 8) rc = smem_path(presort_smem_kernel<8>, 8);
+  if (items <= 4) rc = smem_path(presort_smem_kernel<4>, 4);
+  else if (items <= 8) rc = smem_path(presort_smem_kernel<8>, 8);
+  else if (items <= 12) rc = smem_path(presort_smem_kernel<12>, 12);
   else if (items <= 16) rc = smem_path(presort_smem_kernel<16>, 16);
-  else if (items <= 24) rc = smem_path(presort_smem_kernel<24>, 24);
-  else if (items <= 32) rc = smem_path(presort_smem_kernel<32>, 32);
-  else if (items <= 40) rc = smem_path(presort_smem_kernel<40>, 40);
+  else if (items <= 20) rc = smem_path(presort_smem_kernel<20>, 20);
   if (rc > 0) return rc;
   if (rc < 0) {
     presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,

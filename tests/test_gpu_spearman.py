@@ -87,3 +87,21 @@ def test_spearman_config2_slice(oracle):
     ref = oracle.oracle_run(req, mat)
     _check(res, ref)
     assert same_nan(res["p_bh"], ref["p_bh"])
+
+
+@pytest.mark.parametrize("S", [500, 6000, 20000])
+def test_spearman_keys_equal_in_high_bits(oracle, S):
+    """Values that agree in their high 32 bits but differ below: the presort
+    orders on the high half first, then repairs short colliding runs and
+    re-sorts features with long ones on the full key."""
+    rng = np.random.default_rng(S + 7)
+    x = workloads.config_spearman_like(rng, 10, S)
+    x[1] = 1.0 + rng.integers(0, 1000, S) * 2.0**-40        # one long colliding run
+    x[2] = np.round(x[2], 1) + rng.integers(0, 3, S) * 2.0**-45  # many short runs
+    x[3] = -1.0 - rng.integers(0, 50, S) * 2.0**-38          # negative keys
+    x[4, ::3] = 0.0
+    x[4, 1::3] = -0.0
+    x[5, ::7] = np.nan                                      # NaN values as data
+    mat = ps.make_matrix(x, "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("spearman", ("stat", "p", "rho"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
