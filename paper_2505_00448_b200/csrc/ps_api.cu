@@ -1,6 +1,9 @@
 // ps_api.cu -- the C ABI (include/pairstat_b200.h): device state, prepared
 // matrices, block entry points and the host-buffer run() used by Python.
 #include "ps_internal.cuh"
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -108,6 +111,22 @@ int ps_cuda_check(cudaError_t e, const char* what) {
   return PS_ERR_CUDA;
 }
 
+namespace {
+// PS_TRACE=1: per-phase wall times of ps_run on stderr (synchronising)
+struct Trace {
+  bool on = getenv("PS_TRACE") != nullptr;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[ps_run] %-10s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 extern "C" {
 
 const char* ps_version(void) { return "paper_2505_00448_b200 0.1.0 (sm_100a)"; }
@@ -173,6 +192,8 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
   if (!desc || desc->n_features <= 0 || desc->n_samples <= 0)
     return ps_fail(PS_ERR_INVALID, "expected a non-empty matrix");
   cudaStream_t s = as_stream(stream);
+  Trace tr;
+  tr.s = s;
   ps_matrix* m = new ps_matrix();
   m->device = current_device();
   m->kind = desc->kind;
@@ -238,8 +259,11 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
       }
     }
   }
+  tr.mark("  upload");
   rc = ps_prepare_matrix(m, s);
+  tr.mark("  prepare");
   if (!rc && want_presort) rc = ps_presort_matrix(m, s);
+  tr.mark("  presort");
   if (rc) {
     ps_matrix_destroy(m);
     return rc;
@@ -373,6 +397,7 @@ int ps_sync(void* stream) {
 }
 
 // Host-buffer end-to-end run: engine.run (engine.py:415-557) on the device.
+
 int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_variant, int u_mode,
            double* const* outs, double* const* adj_outs) {
   Guard g;
@@ -380,6 +405,8 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   if (rc) return rc;
   ps_device_state* st = ps_state();
   cudaStream_t s = st->stream;
+  Trace tr;
+  tr.s = s;
   const bool homogeneous = test == PS_TEST_PEARSON || test == PS_TEST_SPEARMAN || test == PS_TEST_CHI2;
   if (!homogeneous && !b) return ps_fail(PS_ERR_INVALID, "mixed test needs a second matrix");
   const bool presort_a = test == PS_TEST_SPEARMAN;
@@ -392,6 +419,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     ps_matrix_destroy(ma);
     return rc;
   }
+  tr.mark("matrices");
   const int64_t rows = ma->F, cols = homogeneous ? ma->F : mb->F;
   const int64_t cells = rows * cols;
   bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
@@ -425,8 +453,10 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     }
   }
   if (!rc) rc = drain_errors(s);
+  tr.mark("compute");
   for (int k = 0; k < 4 && !rc; ++k)
     if (outs && outs[k] && d_out[k]) rc = ps_stage_d2h(outs[k], d_out[k], sizeof(double) * cells, s);
+  tr.mark("d2h");
   if (!rc && any_adj) {
     if (ps_alloc(&d_adj, (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
     for (int k = 0; k < 3 && !rc; ++k) {
@@ -435,6 +465,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
       if (!rc) rc = ps_stage_d2h(adj_outs[k], d_adj, sizeof(double) * cells, s);
     }
   }
+  tr.mark("adjust");
   if (!rc) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = ps_cuda_check(e, "run");

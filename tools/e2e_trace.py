@@ -1,0 +1,24 @@
+"""Time run() end to end for one config with PS_TRACE phase marks."""
+import os
+import sys
+import time
+
+sys.path.insert(0, ".")
+os.environ["PS_TRACE"] = "1"
+import bench  # noqa: E402
+import workloads  # noqa: E402
+import paper_2505_00448_b200 as ps  # noqa: E402
+
+cfg = workloads.config(bench.parse_config(sys.argv[1]))
+test = sys.argv[2] if len(sys.argv) > 2 else cfg["tests"][0]
+a, b, ka, kb = bench.build_inputs(cfg, test)
+outputs = bench.OUTPUTS[bench.parse_config(sys.argv[1])]
+if cfg.get("config") == 4 or sys.argv[1] == "4":
+    outputs = ("stat", "p", "p_bh")
+mat_a = ps.make_matrix(a, ka, na_sentinel=workloads.SENTINEL)
+mat_b = ps.make_matrix(b, kb, na_sentinel=workloads.SENTINEL) if b is not None else None
+req = ps.TestRequest(test, outputs)
+for i in range(3):
+    t0 = time.perf_counter()
+    ps.run(req, mat_a, mat_b)
+    print("run total %.3f ms" % ((time.perf_counter() - t0) * 1e3), file=sys.stderr, flush=True)
