@@ -5,9 +5,9 @@
 // c_f rows to a one-hot matrix O (row off_f + a, sample s) = 1 iff f is present
 // at s with label a.  All contingency tables at once are C = O O^T
 // (int8 x int8 -> int32, exact): the table of (g, h) is the c_g x c_h block at
-// (off_g, off_h).  The GEMM runs on the tensor cores over upper-triangular
-// 128 x 128 tiles of C (IMMA m16n8k32 via mma.sync, ldmatrix-fed from a
-// swizzled 3-stage cp.async ring).  The epilogue (one thread per pair) replays
+// (off_g, off_h).  The GEMM runs on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM, TMA-fed) over upper-triangular
+// 256 x 256 tiles of C, stream-K scheduled (see below).  The epilogue (one thread per pair) replays
 // the reference's NaN rules and its i-major chi-square loop in the same fp64
 // operation order, so chi2 / phi / V are bit-identical; p = chi2_sf(chi2, dof).
 //
@@ -21,11 +21,6 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 64;  // BK in bytes (int8)
-constexpr int GW = 8;                        // warps: 2 (m) x 4 (n), warp tile 64 x 32
-constexpr int GTH = GW * 32;
-constexpr int GSTAGES = 3;
-constexpr int TILE_BYTES = BM * BK;          // 8 KB per operand per stage
 
 // ----------------------------------------------------------------- one-hot
 __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, const int32_t* __restrict__ row_feat,
@@ -62,159 +57,62 @@ __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, co
   }
 }
 
-// ----------------------------------------------------------------- GEMM
-__device__ __forceinline__ uint32_t swz(int row, int chunk) {  // 16-byte chunk swizzle
-  return (uint32_t)(row * BK + ((chunk ^ ((row >> 1) & 3)) << 4));
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-__device__ __forceinline__ void imma(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// C[i][j] = sum_s O[i][s] O[j][s] over upper-triangular tiles (I <= J).
-__global__ void __launch_bounds__(GTH)
-onehot_gemm_kernel(const uint8_t* __restrict__ O, int64_t Sp, int64_t NTt, int64_t tile0,
-                   int32_t* __restrict__ C, int64_t ldC) {
-  extern __shared__ __align__(128) unsigned char gsm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4
-  int64_t I, J;
-  ps_tri_tile(tile0 + blockIdx.x, NTt, &I, &J);
-  const int64_t row0 = I * BM, col0 = J * BN;
-  const uint8_t* A = O + row0 * Sp;
-  const uint8_t* B = O + col0 * Sp;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(gsm);
-  const int64_t nk = Sp / BK;
-
-  auto issue = [&](int64_t kc, int stage) {
-    const uint32_t sa = sbase + stage * 2 * TILE_BYTES, sb = sa + TILE_BYTES;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int idx = tid + q * GTH;  // 512 chunks of 16 B per operand
-      const int r = idx >> 2, ch = idx & 3;
-      const uint8_t* ga = A + r * Sp + kc * BK + ch * 16;
-      const uint8_t* gb = B + r * Sp + kc * BK + ch * 16;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + swz(r, ch)), "l"(ga));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + swz(r, ch)), "l"(gb));
-    }
-    asm volatile("cp.async.commit_group;");
-  };
-
-  int acc[4][4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0;
-
-  for (int q = 0; q < GSTAGES - 1; ++q) {
-    if (q < nk) issue(q, q);
-    else asm volatile("cp.async.commit_group;");
-  }
-  for (int64_t kc = 0; kc < nk; ++kc) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(GSTAGES - 2));
-    __syncthreads();
-    {
-      const int64_t kn = kc + GSTAGES - 1;
-      if (kn < nk) issue(kn, (int)(kn % GSTAGES));
-      else asm volatile("cp.async.commit_group;");
-    }
-    const int stage = (int)(kc % GSTAGES);
-    const uint32_t sa = sbase + stage * 2 * TILE_BYTES, sb = sa + TILE_BYTES;
-#pragma unroll
-    for (int kk = 0; kk < BK / 32; ++kk) {
-      uint32_t af[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int mi = lane >> 3;
-        const int r = wm * 64 + i * 16 + (lane & 7) + (mi & 1) * 8;
-        const int ch = kk * 2 + (mi >> 1);
-        ldsm_x4(sa + swz(r, ch), af[i][0], af[i][1], af[i][2], af[i][3]);
-      }
-      uint32_t bf[4][2];
-#pragma unroll
-      for (int j2 = 0; j2 < 2; ++j2) {
-        const int mi = lane >> 3;
-        const int r = wn * 32 + j2 * 16 + (lane & 7) + (mi >> 1) * 8;
-        const int ch = kk * 2 + (mi & 1);
-        ldsm_x4(sb + swz(r, ch), bf[j2 * 2][0], bf[j2 * 2][1], bf[j2 * 2 + 1][0], bf[j2 * 2 + 1][1]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) imma(acc[i][j], af[i], bf[j][0], bf[j][1]);
-    }
-  }
-  asm volatile("cp.async.wait_group 0;");
-  const int gr = lane >> 2, tg = lane & 3;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t r = row0 + wm * 64 + i * 16 + gr;
-      const int64_t c = col0 + wn * 32 + j * 8 + tg * 2;
-      *reinterpret_cast<int2*>(C + r * ldC + c) = make_int2(acc[i][j][0], acc[i][j][1]);
-      *reinterpret_cast<int2*>(C + (r + 8) * ldC + c) = make_int2(acc[i][j][2], acc[i][j][3]);
-    }
-}
-
 // ----------------------------------------------------------------- tcgen05 GEMM
-// Blackwell-native version of the same contraction: tcgen05.mma kind::i8 with
-// the int32 accumulator tile (128 x 256) in tensor memory.  Operands are
-// staged by cp.async into the canonical K-major SWIZZLE_128B layout (8-row x
-// 128-byte atoms), described to the tensor core by 64-bit smem descriptors;
-// one elected thread issues 4 MMAs (K = 32 bytes each) per 128-byte stage and
-// commits them to the stage's mbarrier, which gates the refill of that stage.
-// The epilogue drains TMEM with tcgen05.ld (32 lanes x 32 columns per warp
-// instruction) straight to the int32 table matrix.
-constexpr int TM = 128, TN = 256, TKB = 128;  // tile rows, cols, K bytes per stage
-constexpr int TSTAGES = 4;
-constexpr int TTH = 128;
+// C = O O^T on tcgen05.mma kind::i8.  A CTA tile is 256 x 256: two M = 128
+// accumulators (TMEM columns 0-255 and 256-511) share one 256-row B operand,
+// so each 128-byte K step moves 64 KB through TMA for 8 MMAs -- half the L2
+// traffic per MMA of a 128 x 256 tile (the contraction is L2-bandwidth bound
+// at that size).  Operands are TMA-loaded (SWIZZLE_128B, K-major 8-row x
+// 128-byte atoms) into a 3-stage ring; one elected thread issues the MMAs and
+// commits each stage to its `empty` mbarrier.
+//
+// Stream-K schedule: the (tile, K step) iteration space of all upper
+// triangular tiles is cut into gridDim.x equal contiguous ranges (one
+// persistent CTA per SM), so every SM does the same MMA work regardless of
+// how many tiles there are.  A CTA's range splits into segments at tile
+// boundaries; after each segment the 4 epilogue warps drain both
+// accumulators with tcgen05.ld and add them into C (fp32 red.global.add.v4:
+// counts < 2^24 are exact in fp32, and integer-valued adds commute, so the
+// result does not depend on the split).  C must be zeroed first.
+//
+// Warp roles: warps 0-3 epilogue (TMEM lanes 32w..32w+31), warp 4 TMA
+// producer, warp 5 MMA issuer.
+constexpr int TM = 256, TN = 256, TKB = 128;  // CTA tile rows, cols, K bytes per stage
+constexpr int TSTAGES = 3;
 constexpr int TA_BYTES = TM * TKB, TB_BYTES = TN * TKB;
 constexpr int TSTAGE_BYTES = TA_BYTES + TB_BYTES;
 constexpr size_t kTc05Smem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
-
-// Warp roles: warps 0-3 epilogue (TMEM lanes 32w..32w+31), warp 4 TMA
-// producer, warp 5 MMA issuer.  full[s]: TMA bytes landed; empty[s]: the MMAs
-// reading stage s retired (tcgen05.commit); done: last MMA retired.
 constexpr int TTH_WS = 192;
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(TTH_WS, 1)
-onehot_gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_constant__ CUtensorMap tmapB,
-                        int64_t Sp, const int2* __restrict__ tiles, int32_t* __restrict__ C, int64_t ldC) {
+onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, const int2* __restrict__ tiles,
+                      int64_t ntiles, float* __restrict__ C, int64_t ldC) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
-  __shared__ uint64_t full[TSTAGES], empty[TSTAGES], done;
+  __shared__ uint64_t full[TSTAGES], empty[TSTAGES], accfull, accempty;
   __shared__ uint32_t tmem_base_s;
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = tc05::smem_u32(tsm);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int2 t = tiles[blockIdx.x];
-  const int64_t row0 = (int64_t)t.x * TM, col0 = (int64_t)t.y * TN;
-  const int nk = (int)(Sp / TKB);
+  // this CTA's share of the (tile, K step) iteration space
+  const int64_t total = ntiles * nk;
+  const int64_t i0 = total * blockIdx.x / gridDim.x, i1 = total * (blockIdx.x + 1) / gridDim.x;
 
-  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, TN);
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
   if (tid == 32) {
     for (int i = 0; i < TSTAGES; ++i) {
       tc05::mbar_init(&full[i], 1);
       tc05::mbar_init(&empty[i], 1);
     }
-    tc05::mbar_init(&done, 1);
+    tc05::mbar_init(&accfull, 1);
+    tc05::mbar_init(&accempty, 128);
     tc05::fence_barrier_init();
   }
-  if (tid == 4 * 32) {
-    tc05::prefetch_tmap(&tmapA);
-    tc05::prefetch_tmap(&tmapB);
-  }
+  if (tid == 4 * 32) tc05::prefetch_tmap(&tmap);
   tc05::fence_before_sync();
   __syncthreads();
   tc05::fence_after_sync();
@@ -222,49 +120,81 @@ onehot_gemm_tc05_kernel(const __grid_constant__ CUtensorMap tmapA, const __grid_
 
   if (warp == 4) {
     if (lane == 0) {  // TMA producer
-      for (int kc = 0; kc < nk; ++kc) {
-        const int st = kc % TSTAGES, n = kc / TSTAGES;
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t q = it - i0;
+        const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
+        const int2 t = tiles[it / nk];
+        const int kc = (int)(it % nk);
         if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
         const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
         tc05::mbar_arrive_expect_tx(&full[st], TSTAGE_BYTES);
-        tc05::tma_load_2d(sa, &tmapA, kc * TKB, (int32_t)row0, &full[st]);
-        tc05::tma_load_2d(sb, &tmapB, kc * TKB, (int32_t)col0, &full[st]);
+        tc05::tma_load_2d(sa, &tmap, kc * TKB, t.x * TM, &full[st]);
+        tc05::tma_load_2d(sb, &tmap, kc * TKB, t.y * TN, &full[st]);
       }
     }
   } else if (warp == 5) {
     if (lane == 0) {  // MMA issuer
-      constexpr uint32_t idesc = tc05::idesc_i8(TM, TN, true);
-      for (int kc = 0; kc < nk; ++kc) {
-        const int st = kc % TSTAGES, n = kc / TSTAGES;
+      constexpr uint32_t idesc = tc05::idesc_i8(128, TN, true);
+      int seg = 0;
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t q = it - i0;
+        const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
+        const int kc = (int)(it % nk);
+        const bool first = it == i0 || kc == 0;
+        const bool last = it + 1 == i1 || kc == nk - 1;
+        if (first && seg > 0) {  // the epilogue has drained the previous segment
+          tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
         tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
         tc05::fence_after_sync();
         const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < TKB / 32; ++kk)
-          tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), tc05::sw128_kmajor_desc(sb + kk * 32), idesc,
-                       (kc | kk) != 0 ? 1u : 0u);
+        for (int kk = 0; kk < TKB / 32; ++kk) {
+          const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+          const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+          tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+          tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * TKB + kk * 32), bd, idesc, acc);
+        }
         tc05::commit(&empty[st]);
+        if (last) {
+          tc05::commit(&accfull);
+          ++seg;
+        }
       }
-      tc05::commit(&done);
     }
   } else {
-    // epilogue warps 0-3
-    tc05::mbar_wait(&done, 0);
-    tc05::fence_after_sync();
-    const int64_t r = row0 + warp * 32 + lane;
-    int32_t* crow = C + r * ldC + col0;
+    // epilogue warps 0-3: one pass per segment, in the MMA issuer's order
+    int seg = 0;
+    for (int64_t it = i0; it < i1;) {
+      const int64_t tile = it / nk;
+      const int64_t seg_end = std::min<int64_t>(i1, (tile + 1) * nk);
+      const int2 t = tiles[tile];
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
 #pragma unroll 1
-    for (int cc = 0; cc < TN / 32; ++cc) {
-      uint32_t v[32];
-      tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
+      for (int half = 0; half < 2; ++half) {
+        const int64_t r = (int64_t)t.x * TM + half * 128 + warp * 32 + lane;
+        float* crow = C + r * ldC + (int64_t)t.y * TN;
+#pragma unroll 1
+        for (int cc = 0; cc < TN / 32; ++cc) {
+          uint32_t v[32];
+          tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<int4*>(crow + cc * 32 + j) = make_int4((int)v[j], (int)v[j + 1], (int)v[j + 2], (int)v[j + 3]);
+          for (int j = 0; j < 32; j += 4)
+            red_add_v4(crow + cc * 32 + j, (float)(int)v[j], (float)(int)v[j + 1], (float)(int)v[j + 2],
+                       (float)(int)v[j + 3]);
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive(&accempty);
+      ++seg;
+      it = seg_end;
     }
   }
   tc05::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc05::tmem_dealloc(tmem, TN);
+  if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
 // ----------------------------------------------------------------- epilogue
@@ -278,7 +208,7 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
 // One thread per pair (g <= h): categorical.py:31-74 in the same op order.
 // Row/column sums are cached for up to CM levels; the table is read from C.
 template <int CM>
-__global__ void chi2_finish_kernel(const int32_t* __restrict__ C, int64_t ldC,
+__global__ void chi2_finish_kernel(const float* __restrict__ C, int64_t ldC,
                                    const int32_t* __restrict__ off, const int32_t* __restrict__ cat,
                                    int64_t F, int64_t lo, int64_t hi, double* __restrict__ stat,
                                    double* __restrict__ pout, double* __restrict__ phi_out,
@@ -290,12 +220,12 @@ __global__ void chi2_finish_kernel(const int32_t* __restrict__ C, int64_t ldC,
     if (h < g) continue;
     const int cg = cat[g], ch = cat[h];
     const bool diag = g == h;
-    const int32_t* T = C + (int64_t)off[g] * ldC + off[h];
+    const float* T = C + (int64_t)off[g] * ldC + off[h];  // exact integer counts
     // the diagonal pair's table is diagonal; its lower half lies outside the
     // computed upper-triangular tiles, so read only the diagonal
     auto tab = [&](int i, int j) -> long long {
       if (diag && i != j) return 0;
-      return T[(int64_t)i * ldC + j];
+      return (long long)T[(int64_t)i * ldC + j];
     };
     long long rs[CM], cs[CM];
     for (int j = 0; j < ch; ++j) cs[j] = 0;
@@ -413,10 +343,11 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
       row_level[off[f] + l] = l;
     }
   uint8_t* O = nullptr;
-  int32_t* C = nullptr;
+  float* C = nullptr;  // exact integer counts (< 2^24), accumulated by the stream-K GEMM
   int32_t *d_off = nullptr, *d_rf = nullptr, *d_rl = nullptr;
   PS_CUDA(ps_alloc(&O, (size_t)(Rp * Sp), s));
   PS_CUDA(ps_alloc(&C, (size_t)(Rp * Rp), s));
+  PS_CUDA(cudaMemsetAsync(C, 0, sizeof(float) * Rp * Rp, s));
   PS_CUDA(ps_alloc(&d_off, (size_t)(F + 1), s));
   PS_CUDA(ps_alloc(&d_rf, (size_t)std::max<int64_t>(R, 1), s));
   PS_CUDA(ps_alloc(&d_rl, (size_t)std::max<int64_t>(R, 1), s));
@@ -433,7 +364,7 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   }
   onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
   PS_LAUNCHED();
-  // 128 x 256 tiles of C needed by pairs with g in [lo, hi): row tiles covering
+  // 256 x 256 tiles of C needed by pairs with g in [lo, hi): row tiles covering
   // off[lo] .. off[hi]-1, column tiles from the diagonal rightwards
   std::vector<int2> tl;
   if (R > 0) {
@@ -446,14 +377,16 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   if (!tl.empty()) {
     PS_CUDA(ps_alloc(&d_tiles, tl.size(), s));
     PS_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, s));
-    PS_CUDA(cudaFuncSetAttribute(onehot_gemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PS_CUDA(cudaFuncSetAttribute(onehot_gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kTc05Smem));
-    CUtensorMap mapA, mapB;
-    int rc = make_onehot_map(&mapA, O, Rp, Sp, TM);
-    if (!rc) rc = make_onehot_map(&mapB, O, Rp, Sp, TN);
+    CUtensorMap map;
+    int rc = make_onehot_map(&map, O, Rp, Sp, TM);
     if (rc) return rc;
+    const int nk = (int)(Sp / TKB);
+    const int64_t iters = (int64_t)tl.size() * nk;
+    const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
     ps_prof_begin("chi2_gemm", s);
-    onehot_gemm_tc05_kernel<<<(unsigned)tl.size(), TTH_WS, kTc05Smem, s>>>(mapA, mapB, Sp, d_tiles, C, Rp);
+    onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, d_tiles, (int64_t)tl.size(), C, Rp);
     ps_prof_end(s);
     PS_LAUNCHED();
   }
