@@ -1,0 +1,36 @@
+#!/bin/bash
+# Re-measure every BASELINE config on one B200 and refresh profiles/:
+#   bench lines, ncu launch lists (time + DRAM bytes per launch), and
+#   ncu --set full reports of the dominant kernels.
+# usage (on the GPU box): bash tools/refresh_profiles.sh <round tag, e.g. r01> [full]
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/prof_$TAG
+mkdir -p $OUT
+CFGS=("1" "2" "3" "4 --test anova" "4 --test ttest" "4 --test kruskal" "4 --test mwu" "5" "5s")
+for c in "${CFGS[@]}"; do
+  n=$(echo $c | sed 's/ --test /_/')
+  extra="--no-cpu-baseline"
+  [ "$n" = "2" ] && extra=""
+  steps=5; [ "$n" = "5" ] && steps=3; [ "$n" = "5s" ] && steps=3
+  timeout 900 python bench.py --config $c --steps $steps --warmup 3 $extra > $OUT/bench_$n.jsonl 2> $OUT/bench_$n.err
+  tail -1 $OUT/bench_$n.jsonl | cut -c1-200
+done
+# launch lists (1 timed step; cold-cache, serialised: shares, not absolutes)
+for c in "${CFGS[@]}"; do
+  n=$(echo $c | sed 's/ --test /_/')
+  [ "$n" = "5" ] && continue
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none --csv --log-file $OUT/launches_$n.csv \
+    python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+  python tools/summarize_launches.py $OUT/launches_$n.csv $OUT/launches_$n.json > $OUT/launches_$n.txt 2>/dev/null
+done
+if [ "${2:-}" = "full" ]; then
+  for spec in "2:spearman_walk" "3:onehot_gemm_sk" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm" "5 --scale 0.15:pearson_tile"; do
+    c=${spec%%:*}; k=${spec##*:}
+    n=$(echo $c | sed 's/ --test /_/')
+    timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
+      -o $OUT/ncu_${n}_$k python tools/profile_one.py --config $c > $OUT/ncu_${n}.log 2>&1
+  done
+fi
+echo done
