@@ -39,6 +39,8 @@ int init_state(ps_device_state* st, int dev) {
   PS_CUDA(cudaMalloc(&st->d_err, sizeof(int)));
   PS_CUDA(cudaMemset(st->d_err, 0, sizeof(int)));
   PS_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+  PS_CUDA(cudaStreamCreateWithFlags(&st->aux, cudaStreamNonBlocking));
+  PS_CUDA(cudaEventCreateWithFlags(&st->aux_ev, cudaEventDisableTiming));
   // keep freed workspace cached in the stream-ordered pool between calls
   cudaMemPool_t pool;
   PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -229,6 +231,19 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
       return ps_fail(PS_ERR_CUDA, "category count upload failed");
     }
   }
+  if (!values_on_device && m->kind != PS_KIND_CONTINUOUS) {
+    // host labels: converted to device codes while staging; no fp64 copy
+    m->ld = ps_round_up(m->S, 32);
+    m->owns_vals = false;
+    rc = ps_prepare_labels_from_host(m, desc->values, src_ld, s);
+    tr.mark("  labels");
+    if (rc) {
+      ps_matrix_destroy(m);
+      return rc;
+    }
+    *out = m;
+    return PS_OK;
+  }
   if (values_on_device && (src_ld % 32) == 0 && (reinterpret_cast<uintptr_t>(desc->values) % 256) == 0) {
     // use the caller's device buffer in place (must be zero-padded to ld)
     m->d_vals = const_cast<double*>(desc->values);
@@ -250,13 +265,35 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
       return ps_cuda_check(e, "input upload");
     }
     if (!values_on_device) {
-      // pinned, double-buffered, all-core staging of the pageable input
-      rc = ps_stage_h2d_2d(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
-                           sizeof(double) * m->S, m->F, s);
+      // pinned, double-buffered, all-core staging of the pageable input; the
+      // validity pass and the presort of each uploaded chunk of rows run on
+      // the auxiliary stream while the next chunk is copied
+      ps_device_state* st = ps_state();
+      rc = ps_prepare_alloc(m, s);
+      if (!rc && want_presort) rc = ps_presort_begin(m, s);
+      if (!rc) {
+        auto on_rows = [&](int64_t r0, int64_t nr, cudaEvent_t ev) -> int {
+          PS_CUDA(cudaStreamWaitEvent(st->aux, ev, 0));
+          int c = ps_prepare_rows(m, r0, r0 + nr, st->aux);
+          if (!c && want_presort) c = ps_presort_rows(m, r0, r0 + nr, st->aux);
+          return c;
+        };
+        rc = ps_stage_h2d_2d(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
+                             sizeof(double) * m->S, m->F, s, on_rows);
+      }
+      if (!rc) {
+        cudaError_t e2 = cudaEventRecord(st->aux_ev, st->aux);
+        if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s, st->aux_ev, 0);
+        if (e2 != cudaSuccess) rc = ps_cuda_check(e2, "upload overlap");
+      }
+      if (!rc && want_presort) rc = ps_presort_end(m, s);
+      tr.mark("  upload+prep");
       if (rc) {
         ps_matrix_destroy(m);
         return rc;
       }
+      *out = m;
+      return PS_OK;
     }
   }
   tr.mark("  upload");

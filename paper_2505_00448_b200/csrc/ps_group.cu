@@ -368,7 +368,7 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
 // Exact replay of _anova_rows / _ttest_rows (mixed.py:182-202, :498-520):
 // one thread per cell, samples in order, raw fp64 one-pass sums.
 template <int KM>
-__global__ void group_replay_kernel(int test, const double* __restrict__ lab_vals, int64_t lld,
+__global__ void group_replay_kernel(int test, const uint32_t* __restrict__ zero_bits,
                                     const uint8_t* __restrict__ codes, int64_t ldc,
                                     const uint32_t* __restrict__ lmask, const double* __restrict__ vals,
                                     int64_t ld, const uint32_t* __restrict__ vmask, int64_t W, int64_t S,
@@ -406,13 +406,13 @@ __global__ void group_replay_kernel(int test, const double* __restrict__ lab_val
       }
       anova_finish_raw(counts, sums, ssq, k, &r0, &r1, &r2, o.err);
     } else {
-      const double* lv = lab_vals + g * lld;
+      const uint32_t* zg = zero_bits + g * W;  // present && label == 0.0
       long long n0 = 0, n1 = 0;
       double s0 = 0, s1 = 0, q0 = 0, q1 = 0;
       for (int64_t s = 0; s < S; ++s) {
         if (((mg[s >> 5] & mh[s >> 5]) >> (s & 31)) & 1u) {
           const double v = xv[s];
-          if (lv[s] == 0.0) {
+          if ((zg[s >> 5] >> (s & 31)) & 1u) {
             ++n0;
             s0 += v;
             q0 += v * v;
@@ -534,11 +534,11 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
                                                     lo, hi, student, o);
   PS_LAUNCHED();
   if (small)
-    group_replay_kernel<16><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_vals, lab->ld, lab->d_codes, lab->ldc,
+    group_replay_kernel<16><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_zero, lab->d_codes, lab->ldc,
                                                            lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
                                                            S, lab->d_cat, Fq, student, o);
   else
-    group_replay_kernel<256><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_vals, lab->ld, lab->d_codes, lab->ldc,
+    group_replay_kernel<256><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_zero, lab->d_codes, lab->ldc,
                                                             lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
                                                             S, lab->d_cat, Fq, student, o);
   PS_LAUNCHED();

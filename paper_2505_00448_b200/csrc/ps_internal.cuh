@@ -1,6 +1,7 @@
 // ps_internal.cuh -- device-resident matrix handle and kernel entry points
 // shared between the per-test translation units and the C-ABI layer.
 #pragma once
+#include <functional>
 #include <cstdint>
 #include <string>
 #include <cuda_runtime.h>
@@ -41,6 +42,7 @@ struct ps_matrix {
   uint16_t* d_lastb = nullptr;    // F x ldt: prefix-max boundary position per word
   uint16_t* d_nextb = nullptr;    // F x ldt: suffix-min boundary position per word
   uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
+  void* presort_scratch[4] = {nullptr, nullptr, nullptr, nullptr};  // global radix path (S > 20480)
 };
 
 // Per-device library state.
@@ -49,6 +51,8 @@ struct ps_device_state {
   int num_sms = 148;
   int* d_err = nullptr;           // device error word
   cudaStream_t stream = nullptr;  // library stream used by ps_run
+  cudaStream_t aux = nullptr;     // second stream: per-chunk prep / presort during uploads
+  cudaEvent_t aux_ev = nullptr;
 };
 
 ps_device_state* ps_state();                 // current device's state
@@ -85,7 +89,12 @@ inline void ps_free(void* p, cudaStream_t s) {
 
 // Kernel-family entry points (implemented per translation unit).
 int ps_prepare_matrix(ps_matrix* m, cudaStream_t s);
+int ps_prepare_alloc(ps_matrix* m, cudaStream_t s);
+int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
 int ps_presort_matrix(ps_matrix* m, cudaStream_t s);
+int ps_presort_begin(ps_matrix* m, cudaStream_t s);
+int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
+int ps_presort_end(ps_matrix* m, cudaStream_t s);
 int ps_fill_nan(double* p, int64_t n, cudaStream_t s);
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s);
@@ -99,7 +108,14 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
                       double* stat, double* p, double* eff, cudaStream_t s);
 int ps_adjust_run(const double* p, int64_t rows, int64_t cols, int method, int symmetric,
                   double* out, cudaStream_t s);
+// on_rows(r0, nr, ev): called after the copy of rows [r0, r0 + nr) was issued;
+// ev is recorded on the copy stream right after it
+typedef std::function<int(int64_t, int64_t, cudaEvent_t)> ps_rows_done_fn;
 int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
-                    cudaStream_t s);
+                    cudaStream_t s, const ps_rows_done_fn& on_rows = nullptr);
+int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
+                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, uint32_t* d_zero, int64_t W,
+                        cudaStream_t s);
+int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld, cudaStream_t s);
 int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s);

@@ -19,8 +19,8 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
                  double* __restrict__ center, int32_t* __restrict__ count,
                  // label outputs (nullptr for continuous)
                  const int32_t* __restrict__ cat, uint8_t* __restrict__ codes, int64_t ldc,
-                 uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits) {
-  const int64_t f = blockIdx.x;
+                 uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits, int64_t f0) {
+  const int64_t f = f0 + blockIdx.x;
   const double* row = vals + f * ld;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cf = cat ? cat[f] : 0;
@@ -82,6 +82,38 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
   }
 }
 
+// Label matrices staged from the host as codes: presence / out-of-range bit
+// words and present counts from the codes (pivot unused for labels: 0).
+__global__ void __launch_bounds__(kPrepThreads)
+label_bits_kernel(const uint8_t* __restrict__ codes, int64_t ldc, int64_t S, int64_t W,
+                  uint32_t* __restrict__ mask, uint32_t* __restrict__ bad_bits, int32_t* __restrict__ count,
+                  double* __restrict__ center) {
+  const int64_t f = blockIdx.x;
+  const uint8_t* c = codes + f * ldc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int cnt = 0;
+  for (int64_t base = (int64_t)warp * 32; base < S; base += (int64_t)kPrepThreads) {
+    const int64_t s = base + lane;
+    const uint8_t code = s < S ? c[s] : (uint8_t)0xFF;
+    const uint32_t word = __ballot_sync(PS_FULL, code != 0xFF);
+    const uint32_t bw = __ballot_sync(PS_FULL, code == 0xFE);
+    if (lane == 0) {
+      mask[f * W + (base >> 5)] = word;
+      bad_bits[f * W + (base >> 5)] = bw;
+      cnt += __popc(word);
+    }
+  }
+  __shared__ int scnt[kPrepThreads / 32];
+  if (lane == 0) scnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < kPrepThreads / 32; ++w) t += scnt[w];
+    count[f] = t;
+    center[f] = 0.0;
+  }
+}
+
 __global__ void fill_kernel(double* __restrict__ p, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -98,23 +130,49 @@ int ps_fill_nan(double* p, int64_t n, cudaStream_t s) {
   return PS_OK;
 }
 
-int ps_prepare_matrix(ps_matrix* m, cudaStream_t s) {
+// Host label matrix -> device codes + bits without a device copy of the values.
+int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_mask, (size_t)(m->F * m->W), s));
   PS_CUDA(ps_alloc(&m->d_center, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
-  const bool labels = m->kind != PS_KIND_CONTINUOUS;
-  if (labels) {
+  m->ldc = ps_round_up(m->S + 1, 16);
+  PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
+  PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
+  PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));
+  int rc = ps_stage_labels_h2d(src, (size_t)src_ld, m->F, m->S, m->sentinel_bits, m->sentinel_is_nan, m->h_cat,
+                               m->d_codes, m->ldc, m->d_zero, m->W, s);
+  if (rc) return rc;
+  label_bits_kernel<<<(unsigned)m->F, kPrepThreads, 0, s>>>(m->d_codes, m->ldc, m->S, m->W, m->d_mask, m->d_bad,
+                                                            m->d_count, m->d_center);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_prepare_alloc(ps_matrix* m, cudaStream_t s) {
+  PS_CUDA(ps_alloc(&m->d_mask, (size_t)(m->F * m->W), s));
+  PS_CUDA(ps_alloc(&m->d_center, (size_t)m->F, s));
+  PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
+  if (m->kind != PS_KIND_CONTINUOUS) {
     m->ldc = ps_round_up(m->S + 1, 16);  // code[S] = 0xFF: sentinel for padded walks
     PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
     PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
     PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));
   }
-  if (m->F > 0) {
-    prep_rows_kernel<<<(unsigned)m->F, kPrepThreads, 0, s>>>(
-        m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask,
-        m->d_center, m->d_count, labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero,
-        m->d_bad);
-    PS_LAUNCHED();
-  }
   return PS_OK;
+}
+
+int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
+  if (f1 <= f0) return PS_OK;
+  const bool labels = m->kind != PS_KIND_CONTINUOUS;
+  prep_rows_kernel<<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
+      m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
+      labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero, m->d_bad, f0);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_prepare_matrix(ps_matrix* m, cudaStream_t s) {
+  int rc = ps_prepare_alloc(m, s);
+  if (!rc) rc = ps_prepare_rows(m, 0, m->F, s);
+  return rc;
 }

@@ -72,13 +72,13 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
                uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, uint16_t* __restrict__ order,
                uint16_t* __restrict__ inv, int64_t ldo, uint32_t* __restrict__ tb,
                uint16_t* __restrict__ lastb, uint16_t* __restrict__ nextb, int64_t ldt,
-               uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
+               uint8_t* __restrict__ tied, int32_t* __restrict__ lens, int64_t f0) {
   __shared__ int warp_buf[NW];
   __shared__ uint32_t hist[8][256];
   __shared__ uint32_t wcnt[NW][256];
   __shared__ uint32_t bucket[256];
   __shared__ int s_any_tie;
-  const int64_t f = blockIdx.x;
+  const int64_t f = f0 + blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* row = vals + f * ld;
   const uint32_t* mrow = mask + f * W;
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(QT, 1)
 presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask, int64_t W,
                     int64_t S, uint16_t* __restrict__ order, uint16_t* __restrict__ inv, int64_t ldo,
                     uint32_t* __restrict__ tb, uint16_t* __restrict__ lastb, uint16_t* __restrict__ nextb,
-                    int64_t ldt, uint8_t* __restrict__ tied, int32_t* __restrict__ lens) {
+                    int64_t ldt, uint8_t* __restrict__ tied, int32_t* __restrict__ lens, int64_t f0) {
   constexpr int NMAX = QT * ITEMS;
   extern __shared__ __align__(16) unsigned char qsm[];
   uint64_t* skey = reinterpret_cast<uint64_t*>(qsm);  // full keys, once sorted
@@ -283,7 +283,7 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   __shared__ int warp_buf[QW];
   __shared__ unsigned long long s_and, s_or;
   __shared__ int s_any_tie, s_long;
-  const int64_t f = blockIdx.x;
+  const int64_t f = f0 + blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* row = vals + f * ld;
   const uint32_t* mrow = mask + f * W;
@@ -503,19 +503,13 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
 
 }  // namespace
 
-int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
-  if (m->has_presort) return PS_OK;
+// Presort in three steps so the per-feature sorts can follow the input
+// upload chunk by chunk (ps_matrix_create overlaps them with the H2D copy).
+int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
   if (m->S > 65535)
     return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
-  const int64_t FS = m->F * m->S;
   m->ldo = ps_round_up(m->S + 1, 64);  // room for the sentinel sample id S
   m->ldt = tie_words(m->S);
-  uint64_t *kA = nullptr, *kB = nullptr;
-  uint32_t *iA = nullptr, *iB = nullptr;
-  PS_CUDA(ps_alloc(&kA, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&kB, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&iA, (size_t)FS, s));
-  PS_CUDA(ps_alloc(&iB, (size_t)FS, s));
   PS_CUDA(ps_alloc(&m->d_order, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_inv, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
@@ -523,32 +517,61 @@ int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
+  if (ps_ceil_div(m->S, QT) > 20) {  // global-memory radix path: per-feature scratch
+    const int64_t FS = m->F * m->S;
+    uint64_t *kA = nullptr, *kB = nullptr;
+    uint32_t *iA = nullptr, *iB = nullptr;
+    PS_CUDA(ps_alloc(&kA, (size_t)FS, s));
+    PS_CUDA(ps_alloc(&kB, (size_t)FS, s));
+    PS_CUDA(ps_alloc(&iA, (size_t)FS, s));
+    PS_CUDA(ps_alloc(&iB, (size_t)FS, s));
+    m->presort_scratch[0] = kA;
+    m->presort_scratch[1] = kB;
+    m->presort_scratch[2] = iA;
+    m->presort_scratch[3] = iB;
+  }
+  return PS_OK;
+}
+
+int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
+  const int64_t nf = f1 - f0;
+  if (nf <= 0) return PS_OK;
   const int items = (int)ps_ceil_div(m->S, QT);
   auto smem_path = [&](auto kern, int it) -> int {
     const size_t smem = (size_t)QT * it * 10;
     PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)m->F, QT, smem, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, m->d_order, m->d_inv, m->ldo,
-                                          m->d_tb, m->d_lastb, m->d_nextb, m->ldt, m->d_tied, m->d_len);
+    kern<<<(unsigned)nf, QT, smem, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, m->d_order, m->d_inv, m->ldo,
+                                        m->d_tb, m->d_lastb, m->d_nextb, m->ldt, m->d_tied, m->d_len, f0);
     PS_LAUNCHED();
     return PS_OK;
   };
-  int rc = -1;
-  if (items <= 4) rc = smem_path(presort_smem_kernel<4>, 4);
-  else if (items <= 8) rc = smem_path(presort_smem_kernel<8>, 8);
-  else if (items <= 12) rc = smem_path(presort_smem_kernel<12>, 12);
-  else if (items <= 16) rc = smem_path(presort_smem_kernel<16>, 16);
-  else if (items <= 20) rc = smem_path(presort_smem_kernel<20>, 20);
-  if (rc > 0) return rc;
-  if (rc < 0) {
-    presort_kernel<<<(unsigned)m->F, NT, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->S, kA, iA, kB, iB,
-                                                 m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
-                                                 m->d_nextb, m->ldt, m->d_tied, m->d_len);
-    PS_LAUNCHED();
+  if (items <= 4) return smem_path(presort_smem_kernel<4>, 4);
+  if (items <= 8) return smem_path(presort_smem_kernel<8>, 8);
+  if (items <= 12) return smem_path(presort_smem_kernel<12>, 12);
+  if (items <= 16) return smem_path(presort_smem_kernel<16>, 16);
+  if (items <= 20) return smem_path(presort_smem_kernel<20>, 20);
+  presort_kernel<<<(unsigned)nf, NT, 0, s>>>(
+      m->d_vals, m->ld, m->d_mask, m->W, m->S, static_cast<uint64_t*>(m->presort_scratch[0]),
+      static_cast<uint32_t*>(m->presort_scratch[2]), static_cast<uint64_t*>(m->presort_scratch[1]),
+      static_cast<uint32_t*>(m->presort_scratch[3]), m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
+      m->d_nextb, m->ldt, m->d_tied, m->d_len, f0);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_presort_end(ps_matrix* m, cudaStream_t s) {
+  for (void*& p : m->presort_scratch) {
+    ps_free(p, s);
+    p = nullptr;
   }
-  ps_free(kA, s);
-  ps_free(kB, s);
-  ps_free(iA, s);
-  ps_free(iB, s);
   m->has_presort = true;
   return PS_OK;
+}
+
+int ps_presort_matrix(ps_matrix* m, cudaStream_t s) {
+  if (m->has_presort) return PS_OK;
+  int rc = ps_presort_begin(m, s);
+  if (!rc) rc = ps_presort_rows(m, 0, m->F, s);
+  if (!rc) rc = ps_presort_end(m, s);
+  return rc;
 }

@@ -238,11 +238,15 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
         for (int word = warp; word < nw; word += RW) {
           const uint32_t p = (uint32_t)(word * 32 + lane);
           const uint32_t kw = K[word];
+          // prefixes of the tie groups entering / leaving the word (uniform),
+          // then per-lane group bounds from the word's boundary bits
+          const uint32_t T = tbh[word], Pw = P[word];
+          const uint32_t sp = (T & 1u) ? Pw : pfx_at(K, P, lbh[word ? word - 1 : 0]);
+          const uint32_t ep = pfx_at(K, P, min((uint32_t)nbh[word + 1], (uint32_t)nh));
+          uint32_t a, b;
+          word_group_pfx(T, sp, ep, kw, Pw, a, b);
           if (p < (uint32_t)nh) {
-            const uint32_t gs = tie_start(tbh, lbh, p);
-            const uint32_t ge = tie_end(tbh, nbh, p);
-            const uint32_t a = pfx_at(K, P, gs), b = pfx_at(K, P, ge);
-            if (gs == p) {  // the group's first position owns its tie term
+            if ((T >> lane) & 1u) {  // the group's first position owns its tie term
               const long long t = (long long)(b - a);
               if (t > 1) tie += t * t * t - t;
             }

@@ -117,18 +117,10 @@ __device__ __forceinline__ uint32_t tend_a(uint32_t aT, uint32_t aN, uint32_t p)
 // kw = w's kept bits, Pw = Pfx(32 w).  The prefixes of the groups entering
 // and leaving the word are warp-uniform (two lookups per word); only a word
 // that holds a boundary needs per-lane in-word start / end bits.
-// (branch-free: selects only, so the word loops unroll)
 __device__ __forceinline__ uint32_t word_r2(uint32_t T, uint32_t sp, uint32_t ep, uint32_t kw, uint32_t Pw) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t le = 0xFFFFFFFFu >> (31u - lane);
-  const uint32_t mS = T & le, mE = T & ~le;
-  // start bit s = highest set bit of mS; kept lanes below s: kw & (2^s - 1)
-  const uint32_t belowS = mS ? (0xFFFFFFFFu >> __clz(mS)) >> 1 : 0u;
-  // end bit e = lowest set bit of mE; kept lanes below e: kw & (2^e - 1)
-  const uint32_t belowE = (mE & (0u - mE)) - 1u;
-  const uint32_t ps = mS ? Pw + __popc(kw & belowS) : sp;
-  const uint32_t pe = mE ? Pw + __popc(kw & belowE) : ep;
-  return ps + pe + 1u;
+  uint32_t a, b;
+  word_group_pfx(T, sp, ep, kw, Pw, a, b);
+  return a + b + 1u;
 }
 template <class PfxF>
 __device__ __forceinline__ uint32_t tied_r2(uint32_t T, uint32_t lb, uint32_t nb, uint32_t n, uint32_t kw,

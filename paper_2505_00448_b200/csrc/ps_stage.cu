@@ -10,6 +10,7 @@
 #include <omp.h>
 #include <algorithm>
 #include <cstring>
+#include <cmath>
 
 namespace {
 
@@ -20,6 +21,7 @@ struct Ring {
   int device = -1;
   void* buf[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t done = nullptr;
 };
 Ring g_ring[64];
 
@@ -32,6 +34,7 @@ int ring_for_device(Ring** out) {
       PS_CUDA(cudaHostAlloc(&r.buf[b], kChunk, cudaHostAllocDefault));
       PS_CUDA(cudaEventCreateWithFlags(&r.ev[b], cudaEventDisableTiming));
     }
+    PS_CUDA(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
     r.device = dev;
   }
   *out = &r;
@@ -47,18 +50,47 @@ void par_copy(void* dst, const void* src, size_t bytes) {
   }
 }
 
+// One label row: the per-cell rules of prep_rows_kernel, branch-free so the
+// compiler vectorises the code loop (AVX2 clone picked at load time).
+__attribute__((target_clones("avx2", "default"))) void label_row(const double* row, int64_t S, int64_t W, double cf,
+                                                                 uint64_t sent_bits, int sent_nan, uint8_t* crow,
+                                                                 uint32_t* zrow) {
+  alignas(64) uint8_t zf[32];
+  int64_t q0 = 0;
+  for (int64_t w = 0; w < W; ++w, q0 += 32) {
+    const int64_t len = std::min<int64_t>(S - q0, 32);
+    for (int64_t q = 0; q < len; ++q) {
+      const double v = row[q0 + q];
+      uint64_t bits;
+      std::memcpy(&bits, &v, sizeof(bits));
+      const bool pres = sent_nan ? (v == v) : (bits != sent_bits);
+      const bool ok = (v > -1.0) & (v < cf);  // false for NaN
+      const int32_t lab = (int32_t)(ok ? v : 0.0);  // trunc toward zero (categorical.py:87)
+      crow[q0 + q] = pres ? (ok ? (uint8_t)lab : (uint8_t)0xFE) : (uint8_t)0xFF;
+      zf[q] = pres & (v == 0.0);
+    }
+    uint32_t zw = 0;
+    for (int64_t q = 0; q < len; ++q) zw |= (uint32_t)zf[q] << q;
+    zrow[w] = zw;
+  }
+}
+
 }  // namespace
 
 // rows x width bytes from host (pitch spitch) to device (pitch dpitch)
 int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
-                    cudaStream_t s) {
-  if (width * rows < kDirect || dpitch > kChunk) {
-    PS_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s));
-    return PS_OK;
-  }
+                    cudaStream_t s, const ps_rows_done_fn& on_rows) {
   Ring* r = nullptr;
   int rc = ring_for_device(&r);
   if (rc) return rc;
+  if (width * rows < kDirect || dpitch > kChunk) {
+    PS_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyHostToDevice, s));
+    if (on_rows) {
+      PS_CUDA(cudaEventRecord(r->done, s));
+      return on_rows(0, (int64_t)rows, r->done);
+    }
+    return PS_OK;
+  }
   const size_t rows_per = std::max<size_t>(1, kChunk / dpitch);
   int b = 0;
   for (size_t r0 = 0; r0 < rows; r0 += rows_per, b ^= 1) {
@@ -74,6 +106,45 @@ int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, si
       for (long long i = 0; i < (long long)nr; ++i) std::memcpy(pb + i * dpitch, sp + i * spitch, width);
     }
     PS_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + r0 * dpitch, pb, nr * dpitch, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaEventRecord(r->ev[b], s));
+    if (on_rows) {
+      rc = on_rows((int64_t)r0, (int64_t)nr, r->ev[b]);
+      if (rc) return rc;
+    }
+  }
+  return PS_OK;
+}
+
+// Label matrices from the host: every core converts its rows of fp64 labels
+// into the device layout while staging -- uint8 codes (trunc(label), 0xFE
+// present but outside [0, c_f) or NaN, 0xFF missing; padded with 0xFF to ldc)
+// and the "present && label == 0.0" bit words -- with the same rules as
+// prep_rows_kernel, so only ~1 B per cell crosses PCIe instead of 8.
+int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
+                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, uint32_t* d_zero, int64_t W,
+                        cudaStream_t s) {
+  Ring* r = nullptr;
+  int rc = ring_for_device(&r);
+  if (rc) return rc;
+  const size_t row_bytes = (size_t)ldc + (size_t)W * 4;
+  const int64_t rows_per = std::max<int64_t>(1, (int64_t)(kChunk / row_bytes));
+  if ((size_t)rows_per * row_bytes > kChunk) return ps_fail(PS_ERR_INVALID, "label row larger than the staging chunk");
+  int b = 0;
+  for (int64_t r0 = 0; r0 < F; r0 += rows_per, b ^= 1) {
+    const int64_t nr = std::min<int64_t>(rows_per, F - r0);
+    PS_CUDA(cudaEventSynchronize(r->ev[b]));
+    uint8_t* pc = static_cast<uint8_t*>(r->buf[b]);
+    uint32_t* pz = reinterpret_cast<uint32_t*>(pc + (size_t)nr * ldc);  // ldc % 16 == 0: aligned
+    const int nt = std::max(1, std::min(omp_get_max_threads(), (int)nr));
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int64_t i = 0; i < nr; ++i) {
+      const int64_t f = r0 + i;
+      label_row(src + (size_t)f * spitch, S, W, (double)cat[f], sent_bits, sent_nan, pc + (size_t)i * ldc,
+                pz + (size_t)i * W);
+      std::memset(pc + (size_t)i * ldc + S, 0xFF, (size_t)(ldc - S));
+    }
+    PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)r0 * ldc, pc, (size_t)nr * ldc, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(d_zero + (size_t)r0 * W, pz, (size_t)nr * W * 4, cudaMemcpyHostToDevice, s));
     PS_CUDA(cudaEventRecord(r->ev[b], s));
   }
   return PS_OK;

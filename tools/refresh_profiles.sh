@@ -28,7 +28,7 @@ done
 if [ "${2:-}" = "full" ]; then
   for spec in "2:spearman_walk" "3:onehot_gemm_sk" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm" "5 --scale 0.15:pearson_tile"; do
     c=${spec%%:*}; k=${spec##*:}
-    n=$(echo $c | sed 's/ --test /_/')
+    n=$(echo $c | sed 's/ --test /_/; s/ --scale /_s/')
     timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
       -o $OUT/ncu_${n}_$k python tools/profile_one.py --config $c > $OUT/ncu_${n}.log 2>&1
   done
