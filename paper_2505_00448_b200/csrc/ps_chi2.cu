@@ -275,20 +275,31 @@ __global__ void chi2_finish_kernel(const float* __restrict__ C, int64_t ldC,
 // partner inside the evaluated pairs (categorical.py:84-91): rows [lo, hi)
 // always meet themselves on the diagonal; rows >= hi only where some row of
 // [lo, hi) is present.
+// LabelOutOfRange (categorical.py:84-91): a bad present label of a feature f
+// that meets a computed pair -- every f in [lo, hi) (its diagonal pair), or
+// f >= hi where some row g in [lo, hi) is present at the same sample.
+// Grid: x over mask words, y over chunks of kCheckRows features; the OR of the
+// row masks is only formed when a chunk actually holds a bad label.
+constexpr int kCheckRows = 32;
 __global__ void label_check_kernel(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ mask,
                                    int64_t W, int64_t F, int64_t lo, int64_t hi, int* __restrict__ err) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t col = 0;
-    for (int64_t g = lo; g < hi; ++g) col |= mask[g * W + w];
-    for (int64_t f = lo; f < F; ++f) {
-      const uint32_t b = bad[f * W + w];
-      if (b && (f < hi || (b & col))) {
-        ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
-        return;
-      }
-    }
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  const int64_t f0 = lo + (int64_t)blockIdx.y * kCheckRows, f1 = min(F, f0 + kCheckRows);
+  uint32_t in_rows = 0, beyond = 0;
+  for (int64_t f = f0; f < f1; ++f) {
+    const uint32_t b = bad[f * W + w];
+    if (f < hi) in_rows |= b;
+    else beyond |= b;
   }
+  if (in_rows) {
+    ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
+    return;
+  }
+  if (!beyond) return;
+  uint32_t col = 0;
+  for (int64_t g = lo; g < hi && !(col & beyond); ++g) col |= mask[g * W + w];
+  if (col & beyond) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
 }
 
 }  // namespace
@@ -358,8 +369,8 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   }
   {
     const int64_t W = a->W;
-    label_check_kernel<<<(unsigned)std::min<int64_t>(ps_ceil_div(W, 128), 1024), 128, 0, s>>>(
-        a->d_bad, a->d_mask, W, F, lo, hi, ds->d_err);
+    const dim3 grid((unsigned)ps_ceil_div(W, 128), (unsigned)ps_ceil_div(F - lo, kCheckRows));
+    label_check_kernel<<<grid, 128, 0, s>>>(a->d_bad, a->d_mask, W, F, lo, hi, ds->d_err);
     PS_LAUNCHED();
   }
   onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);

@@ -81,8 +81,14 @@ __global__ void __launch_bounds__(NTH, 2)
 group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double* __restrict__ vals,
                   int64_t ld, const uint32_t* __restrict__ mask, const double* __restrict__ center,
                   int64_t W, int64_t Fq, int64_t row_tile0, int64_t col_tiles, int32_t* __restrict__ Mn,
-                  double* __restrict__ Ms, double* __restrict__ Mq) {
+                  double* __restrict__ Ms, double* __restrict__ Mq, int64_t kparts, int64_t part_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // split-K (grids too small to fill the SMs): part y covers mask words
+  // [W y / kparts, W (y + 1) / kparts) and writes its own partial moments
+  const int64_t kc0 = W * blockIdx.y / kparts, kc1 = W * (blockIdx.y + 1) / kparts;
+  Mn += blockIdx.y * part_stride;
+  Ms += blockIdx.y * part_stride;
+  Mq += blockIdx.y * part_stride;
   Stage* st = reinterpret_cast<Stage*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = warp >> 1, wj = warp & 1;
@@ -125,16 +131,16 @@ group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double*
     asm volatile("cp.async.commit_group;");
   };
   for (int q = 0; q < NSTAGE - 1; ++q) {
-    if (q < W) issue(q, st[q]);
+    if (kc0 + q < kc1) issue(kc0 + q, st[q]);
     else asm volatile("cp.async.commit_group;");
   }
-  for (int64_t c = 0; c < W; ++c) {
-    const int cur = (int)(c % NSTAGE);
+  for (int64_t c = kc0; c < kc1; ++c) {
+    const int cur = (int)((c - kc0) % NSTAGE);
     asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2));
     __syncthreads();
     {
       const int64_t cn = c + NSTAGE - 1;
-      if (cn < W) issue(cn, st[(int)(cn % NSTAGE)]);
+      if (cn < kc1) issue(cn, st[(int)((cn - kc0) % NSTAGE)]);
       else asm volatile("cp.async.commit_group;");
     }
     const Stage& s = st[cur];
@@ -184,6 +190,27 @@ group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double*
         Ms[r * Fq + h] = as[i][j][e];
         Mq[r * Fq + h] = aq[i][j][e];
       }
+}
+
+// Fixed-order sum of the split-K partial moments (deterministic).
+__global__ void group_parts_reduce_kernel(const int32_t* __restrict__ Pn, const double* __restrict__ Ps,
+                                          const double* __restrict__ Pq, int64_t kparts, int64_t stride,
+                                          int64_t r0, int64_t r1, int64_t Fq, int32_t* __restrict__ Mn,
+                                          double* __restrict__ Ms, double* __restrict__ Mq) {
+  const int64_t n = (r1 - r0) * Fq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = r0 * Fq + i;
+    int32_t cn = 0;
+    double cs = 0.0, cq = 0.0;
+    for (int64_t y = 0; y < kparts; ++y) {
+      cn += Pn[y * stride + idx];
+      cs += Ps[y * stride + idx];
+      cq += Pq[y * stride + idx];
+    }
+    Mn[idx] = cn;
+    Ms[idx] = cs;
+    Mq[idx] = cq;
+  }
 }
 
 struct Outs {
@@ -434,21 +461,19 @@ __global__ void group_replay_kernel(int test, const uint32_t* __restrict__ zero_
 
 // LabelOutOfRange (mixed.py:511-515): a bad present label of a label row in
 // [g0, g1) meeting a present value of any continuous feature in [h0, h1).
+// (grid: x over mask words, y over chunks of 32 label rows)
 __global__ void mixed_label_check_kernel(const uint32_t* __restrict__ bad, const uint32_t* __restrict__ vmask,
                                          int64_t W, int64_t g0, int64_t g1, int64_t h0, int64_t h1,
                                          int* __restrict__ err) {
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < W;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t anyb = 0;
-    for (int64_t g = g0; g < g1; ++g) anyb |= bad[g * W + w];
-    if (!anyb) continue;
-    uint32_t col = 0;
-    for (int64_t h = h0; h < h1 && !(col & anyb); ++h) col |= vmask[h * W + w];
-    if (col & anyb) {
-      ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
-      return;
-    }
-  }
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  const int64_t ga = g0 + (int64_t)blockIdx.y * 32, gb = min(g1, ga + 32);
+  uint32_t anyb = 0;
+  for (int64_t g = ga; g < gb; ++g) anyb |= bad[g * W + w];
+  if (!anyb) return;
+  uint32_t col = 0;
+  for (int64_t h = h0; h < h1 && !(col & anyb); ++h) col |= vmask[h * W + w];
+  if (col & anyb) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
 }
 
 }  // namespace
@@ -506,8 +531,8 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   if (test == PS_TEST_ANOVA) {
     const int64_t h0 = g1 - g0 > 1 ? 0 : lo - g0 * Fq;
     const int64_t h1 = g1 - g0 > 1 ? Fq : hi - g0 * Fq;
-    mixed_label_check_kernel<<<(unsigned)std::min<int64_t>(ps_ceil_div(W, 128), 1024), 128, 0, s>>>(
-        lab->d_bad, val->d_mask, W, g0, g1, h0, h1, ds->d_err);
+    const dim3 grid((unsigned)ps_ceil_div(W, 128), (unsigned)ps_ceil_div(g1 - g0, 32));
+    mixed_label_check_kernel<<<grid, 128, 0, s>>>(lab->d_bad, val->d_mask, W, g0, g1, h0, h1, ds->d_err);
     PS_LAUNCHED();
   }
   onehot_bits_kernel<<<(unsigned)Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, d_rf,
@@ -516,12 +541,33 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   const size_t smem = NSTAGE * sizeof(Stage);
   PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = (rtile1 - rtile0) * ctiles;
+  int32_t* Pn = nullptr;
+  double *Ps = nullptr, *Pq = nullptr;
   if (grid > 0) {
+    // split K when the tile grid cannot fill two CTAs per SM
+    const int64_t kparts = std::max<int64_t>(
+        1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
+    const int64_t stride = Rp * Fq;
+    if (kparts > 1) {
+      PS_CUDA(ps_alloc(&Pn, (size_t)(kparts * stride), s));
+      PS_CUDA(ps_alloc(&Ps, (size_t)(kparts * stride), s));
+      PS_CUDA(ps_alloc(&Pq, (size_t)(kparts * stride), s));
+    }
     ps_prof_begin("group_gemm", s);
-    group_gemm_kernel<<<(unsigned)grid, NTH, smem, s>>>(bits, Rp, val->d_vals, val->ld, val->d_mask,
-                                                         val->d_center, W, Fq, rtile0, ctiles, Mn, Ms, Mq);
+    group_gemm_kernel<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
+        bits, Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, ctiles, kparts > 1 ? Pn : Mn,
+        kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride);
     ps_prof_end(s);
     PS_LAUNCHED();
+    if (kparts > 1) {
+      const int64_t r0 = rtile0 * T, r1 = rtile1 * T;
+      const int blocks = (int)std::min<int64_t>(ps_ceil_div((r1 - r0) * Fq, 256), (int64_t)ds->num_sms * 8);
+      group_parts_reduce_kernel<<<blocks, 256, 0, s>>>(Pn, Ps, Pq, kparts, stride, r0, r1, Fq, Mn, Ms, Mq);
+      PS_LAUNCHED();
+      ps_free(Pn, s);
+      ps_free(Ps, s);
+      ps_free(Pq, s);
+    }
   }
   Outs o{stat, p, eff, rep, repc, cap, ds->d_err};
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(hi - lo, 128), (int64_t)ds->num_sms * 16);
