@@ -276,8 +276,8 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
                     int64_t ldt, uint8_t* __restrict__ tied, int32_t* __restrict__ lens, int64_t f0) {
   constexpr int NMAX = QT * ITEMS;
   extern __shared__ __align__(16) unsigned char qsm[];
-  uint64_t* skey = reinterpret_cast<uint64_t*>(qsm);  // full keys, once sorted
-  uint32_t* sk32 = reinterpret_cast<uint32_t*>(qsm);  // 32-bit pass keys (same bytes, earlier)
+  uint32_t* sk32 = reinterpret_cast<uint32_t*>(qsm);  // 32-bit pass keys (high halves once sorted)
+  uint16_t* sinv = reinterpret_cast<uint16_t*>(qsm);  // inverse permutation, staged at the end
   uint16_t* sidx = reinterpret_cast<uint16_t*>(qsm + (size_t)NMAX * 8);
   __shared__ uint16_t wcnt[QW][256];
   __shared__ int warp_buf[QW];
@@ -287,38 +287,47 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* row = vals + f * ld;
   const uint32_t* mrow = mask + f * W;
+  auto key_of = [&](uint32_t sid) -> uint64_t { return sort_key(row[sid]); };
 
-  // 1. stable compaction of present sample ids (sample order) into smem;
-  //    AND / OR over the keys for pass skipping
+  // 1. stable compaction of present sample ids: thread t owns the contiguous
+  //    samples [t*ITEMS, (t+1)*ITEMS); one block scan of the counts places them.
+  //    AND / OR over the present keys decide which radix bytes are constant.
   if (threadIdx.x == 0) {
     s_and = ~0ull;
     s_or = 0ull;
     s_any_tie = 0;
     s_long = 0;
   }
-  int n = 0;
-  unsigned long long a = ~0ull, o = 0ull;
-  for (int64_t base = 0; base < S; base += QT) {
-    const int64_t s = base + threadIdx.x;
-    const bool pres = s < S && ((mrow[s >> 5] >> (s & 31)) & 1u);
-    int tot;
-    const int pos = block_excl_scan<QW>(pres ? 1 : 0, warp_buf, tot);
-    if (pres) {
-      const uint64_t k = sort_key(row[s]);
-      a &= k;
-      o |= k;
-      sidx[n + pos] = (uint16_t)s;
-    }
-    n += tot;
-  }
+  int n;
+  {
+    const int64_t s0 = (int64_t)threadIdx.x * ITEMS;
+    uint32_t bits = 0;  // presence of this thread's ITEMS samples (ITEMS <= 32)
 #pragma unroll
-  for (int sft = 16; sft > 0; sft >>= 1) {
-    a &= __shfl_xor_sync(PS_FULL, a, sft);
-    o |= __shfl_xor_sync(PS_FULL, o, sft);
-  }
-  if (lane == 0) {
-    atomicAnd(&s_and, a);
-    atomicOr(&s_or, o);
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t sp = s0 + i;
+      if (sp < S && ((mrow[sp >> 5] >> (sp & 31)) & 1u)) bits |= 1u << i;
+    }
+    int tot;
+    int pos = block_excl_scan<QW>(__popc(bits), warp_buf, tot);
+    n = tot;
+    unsigned long long a = ~0ull, o = 0ull;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if ((bits >> i) & 1u) {
+        const uint64_t k = key_of((uint32_t)(s0 + i));
+        a &= k;
+        o |= k;
+        sidx[pos++] = (uint16_t)(s0 + i);
+      }
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+      a &= __shfl_xor_sync(PS_FULL, a, sft);
+      o |= __shfl_xor_sync(PS_FULL, o, sft);
+    }
+    if (lane == 0) {
+      atomicAnd(&s_and, a);
+      atomicOr(&s_or, o);
+    }
   }
   __syncthreads();
   const unsigned long long diff = s_and ^ s_or;
@@ -328,7 +337,7 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   //    so (i, lane) order IS sequence order).  Round 0 sorts on the HIGH half
   //    only (sign, exponent, top mantissa bits); the rare runs whose high
   //    halves collide but whose full keys differ are then repaired by an
-  //    insertion sort on the full key.  A feature with a long colliding run
+  //    insertion sort on the low halves.  A feature with a long colliding run
   //    is re-sorted on both halves (round 1: low half, then high half).  The
   //    32-bit pass keys are re-derived from the values through the sample id
   //    (one gather per stage), so only 6 B per element move per pass.
@@ -339,9 +348,8 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
       for (int i = 0; i < ITEMS; ++i) {
         const int p = warp * 32 * ITEMS + i * 32 + lane;
         idx[i] = p < n ? sidx[p] : 0xFFFFu;
-        const uint64_t k = p < n ? sort_key(row[idx[i]]) : ~0ull;  // padding sorts last
+        const uint64_t k = p < n ? key_of(idx[i]) : ~0ull;  // padding sorts last
         k32[i] = st ? (uint32_t)(k >> 32) : (uint32_t)k;
-        if ((i & 7) == 7) asm volatile("" ::: "memory");  // <= 8 gathers in flight (registers)
       }
       __syncthreads();
       for (int b = 0; b < 4; ++b) {
@@ -401,49 +409,52 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
         __syncthreads();
       }
     }
-    // full keys of the sorted order (overwrites the pass keys)
-    for (int p = threadIdx.x; p < n; p += QT) skey[p] = sort_key(row[sidx[p]]);
-    __syncthreads();
+    // sk32 must hold the HIGH halves in sorted order: the last high-half pass
+    // scattered them; if none ran, the high halves are all equal (s_and's)
+    if ((diff >> 32) == 0 || n <= 1) {
+      for (int p = threadIdx.x; p < n; p += QT) sk32[p] = (uint32_t)(s_and >> 32);
+      __syncthreads();
+    }
     if (round == 1 || (uint32_t)diff == 0u) break;  // low halves all equal: sorted
-    // repair runs of equal high halves with differing full keys
+    // repair runs of equal high halves whose full keys differ: sort the run by
+    // its low halves (stable), staged in sk32 and restored afterwards
     for (int p = threadIdx.x; p < n; p += QT) {
-      const uint64_t k = skey[p];
-      if (p > 0 && (skey[p - 1] >> 32) == (k >> 32)) continue;  // not a run start
+      const uint32_t h = sk32[p];
+      if (p > 0 && sk32[p - 1] == h) continue;  // not a run start
       int e = p + 1;
+      while (e < n && sk32[e] == h) ++e;
+      if (e - p == 1) continue;
+      const uint32_t l0 = (uint32_t)key_of(sidx[p]);
       bool mixed = false;
-      while (e < n && (skey[e] >> 32) == (k >> 32)) {
-        mixed |= skey[e] != k;
-        ++e;
-      }
+      for (int q = p + 1; q < e && !mixed; ++q) mixed = (uint32_t)key_of(sidx[q]) != l0;
       if (!mixed) continue;
       if (e - p > 64) {
         s_long = 1;
         continue;
       }
-      for (int i = p + 1; i < e; ++i) {  // stable insertion sort of [p, e) by the full key
-        const uint64_t ki = skey[i];
+      for (int q = p; q < e; ++q) sk32[q] = (uint32_t)key_of(sidx[q]);
+      for (int i = p + 1; i < e; ++i) {  // stable insertion sort of [p, e) by the low half
+        const uint32_t ki = sk32[i];
         const uint16_t xi = sidx[i];
         int j = i - 1;
-        while (j >= p && skey[j] > ki) {
-          skey[j + 1] = skey[j];
+        while (j >= p && sk32[j] > ki) {
+          sk32[j + 1] = sk32[j];
           sidx[j + 1] = sidx[j];
           --j;
         }
-        skey[j + 1] = ki;
+        sk32[j + 1] = ki;
         sidx[j + 1] = xi;
       }
+      for (int q = p; q < e; ++q) sk32[q] = h;
     }
     __syncthreads();
     if (!s_long) break;
   }
-  // sorted keys are in smem (written by the compaction or the last pass)
-  // 4. outputs
+
+  // 3. outputs: order, tie-group boundaries (full-key equality: high halves
+  //    from smem, low halves fetched only where the high halves agree)
   uint16_t* ord = order + f * ldo;
-  uint16_t* iv = inv + f * ldo;
-  for (int64_t s = threadIdx.x; s < ldo; s += QT) iv[s] = 0xFFFF;
-  __syncthreads();
   for (int p = threadIdx.x; p < (int)ldo; p += QT) ord[p] = p < n ? sidx[p] : (uint16_t)S;
-  for (int p = threadIdx.x; p < n; p += QT) iv[sidx[p]] = (uint16_t)p;
   uint32_t* tbr = tb + f * ldt;
   uint16_t* lbr = lastb + f * ldt;
   uint16_t* nbr = nextb + f * ldt;
@@ -452,8 +463,9 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
     const int p = w * 32 + lane;
     bool bnd;
     if (p < n) {
-      const uint64_t k = skey[p];
-      bnd = p == 0 || k != skey[p - 1] || key_is_nan(k);
+      const uint32_t h = sk32[p];
+      bnd = p == 0 || h != sk32[p - 1] || h == 0xFFF80000u;  // (canonical NaN: never ties)
+      if (!bnd) bnd = (uint32_t)key_of(sidx[p]) != (uint32_t)key_of(sidx[p - 1]);  // high halves agree
       if (!bnd) s_any_tie = 1;
     } else {
       bnd = p == n;
@@ -462,6 +474,14 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
     if (lane == 0) tbr[w] = word;
   }
   __syncthreads();
+  // inverse permutation staged in smem (over the no longer needed keys), then
+  // written out coalesced
+  for (int64_t s = threadIdx.x; s < ldo; s += QT) sinv[s] = 0xFFFF;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += QT) sinv[sidx[p]] = (uint16_t)p;
+  __syncthreads();
+  uint16_t* iv = inv + f * ldo;
+  for (int64_t s = threadIdx.x; s < ldo; s += QT) iv[s] = sinv[s];
   if (warp == 0) {
     int carry = 0;
     for (int w0 = 0; w0 < nw; w0 += 32) {
