@@ -117,6 +117,11 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
   uint8_t* cg_s[2];
   cg_s[0] = take(ldc);
   cg_s[1] = take(ldc);
+  // KM == 8: the tie-free sweep accumulates per (warp, level, lane) in shared
+  // memory (bank = lane: conflict-free) -- one LDS/IADD/STS per kept position
+  // instead of a KM-way select chain in registers
+  constexpr bool SMACC = KM == 8;
+  uint32_t* accs = reinterpret_cast<uint32_t*>(take(SMACC ? (size_t)RW * KM * 32 * 4 : 0));
   // byte offsets into the dynamic buffer: indexing `smem[...]` directly keeps
   // the gathers in the shared window (LDS), never generic loads
   const uint32_t cg_off[2] = {(uint32_t)(cg_s[0] - smem), (uint32_t)(cg_s[1] - smem)};
@@ -143,6 +148,8 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
     asm volatile("cp.async.commit_group;");
   };
 
+  if constexpr (SMACC)
+    for (int i = threadIdx.x; i < RW * KM * 32; i += RTH) accs[i] = 0u;
   const int64_t items = hi - lo;
   for (;;) {
     __syncthreads();
@@ -209,12 +216,22 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
               atomicAdd(&bsum[warp][c], local);
               atomicAdd(&bcnt[warp][c], 1u);
             }
+          } else if constexpr (SMACC) {
+            if (keep && c < (uint32_t)KM) accs[(warp * KM + (int)c) * 32 + lane] += (1u << 20) + local;
           } else {
             const uint32_t packed = (1u << 20) + local;
 #pragma unroll
             for (int j = 0; j < KM; ++j) acc[j] += c == (uint32_t)j ? packed : 0u;  // select, not a branch
           }
           run += __popc(B);
+        }
+        if constexpr (SMACC) {
+#pragma unroll
+          for (int j = 0; j < KM; ++j) {
+            uint32_t& slot = accs[(warp * KM + j) * 32 + lane];
+            acc[j] = slot;
+            slot = 0u;
+          }
         }
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
@@ -500,16 +517,17 @@ __global__ void binary_codes_kernel(const uint32_t* __restrict__ mask, const uin
   }
 }
 
-size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc) {
+size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc, int KM) {
   auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
-  return r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2) + 2 * r16(ldt * 4) + 2 * r16(ldc);
+  return r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2) + 2 * r16(ldt * 4) + 2 * r16(ldc) +
+         (KM == 8 ? (size_t)RW * KM * 32 * 4 : 0);
 }
 
 template <int KM>
 int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo, int64_t hi, int check,
                 int* queue, RankSums rs, cudaStream_t s) {
   ps_device_state* ds = ps_state();
-  const size_t smem = walk_smem(val->ldo, val->ldt, lab->ldc);
+  const size_t smem = walk_smem(val->ldo, val->ldt, lab->ldc, KM);
   auto kern = rank_mixed_walk_kernel<KM>;
   cudaFuncAttributes fa{};
   PS_CUDA(cudaFuncGetAttributes(&fa, kern));
