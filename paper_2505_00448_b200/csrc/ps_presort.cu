@@ -432,20 +432,28 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
         s_long = 1;
         continue;
       }
-      for (int q = p; q < e; ++q) sk32[q] = (uint32_t)key_of(sidx[q]);
-      for (int i = p + 1; i < e; ++i) {  // stable insertion sort of [p, e) by the low half
-        const uint32_t ki = sk32[i];
-        const uint16_t xi = sidx[i];
+      // stable insertion sort of [p, e) by the low half, in thread-local
+      // storage (sk32 stays intact: other threads read it to find run starts)
+      uint32_t lo[64];
+      uint16_t id[64];
+      const int m = e - p;
+      for (int q = 0; q < m; ++q) {
+        id[q] = sidx[p + q];
+        lo[q] = (uint32_t)key_of(id[q]);
+      }
+      for (int i = 1; i < m; ++i) {
+        const uint32_t ki = lo[i];
+        const uint16_t xi = id[i];
         int j = i - 1;
-        while (j >= p && sk32[j] > ki) {
-          sk32[j + 1] = sk32[j];
-          sidx[j + 1] = sidx[j];
+        while (j >= 0 && lo[j] > ki) {
+          lo[j + 1] = lo[j];
+          id[j + 1] = id[j];
           --j;
         }
-        sk32[j + 1] = ki;
-        sidx[j + 1] = xi;
+        lo[j + 1] = ki;
+        id[j + 1] = xi;
       }
-      for (int q = p; q < e; ++q) sk32[q] = h;
+      for (int q = 0; q < m; ++q) sidx[p + q] = id[q];
     }
     __syncthreads();
     if (!s_long) break;

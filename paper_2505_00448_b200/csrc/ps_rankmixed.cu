@@ -563,7 +563,10 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
   ps_device_state* ds = ps_state();
   const bool kw = test == PS_TEST_KRUSKAL;
   const int kmax = kw ? std::max(1, lab->cmax) : 2;
-  const int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 256;
+  int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 256;
+  // the KM = 8 variant keeps per-lane accumulators in shared memory; when they
+  // do not fit next to the walk's tables, use the register variant
+  if (KM == 8 && walk_smem(val->ldo, val->ldt, lab->ldc, 8) > 222 * 1024) KM = 16;
   const int64_t npairs = Fc * Fq;
   // per-pair level stride: the template width, or the real level count for k > 16
   RankSums rs{KM > 16 ? (kmax + 31) / 32 * 32 : KM, nullptr, nullptr, nullptr};
