@@ -11,6 +11,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <thread>
 
 namespace {
 
@@ -461,7 +462,6 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   const int64_t cells = rows * cols;
   bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
   double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
-  double* d_adj = nullptr;
   for (int k = 0; k < 4 && !rc; ++k) {
     const bool want = (outs && outs[k]) || (k == 1 && any_adj);
     if (!want) continue;
@@ -491,24 +491,50 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   }
   if (!rc) rc = drain_errors(s);
   tr.mark("compute");
+  // The p-value adjustments run on the auxiliary stream, driven by a helper
+  // thread (the adjust path reads sizes back to the host), while this thread
+  // stages the raw matrices to the host; the adjusted matrices follow.
+  double* d_adjk[3] = {nullptr, nullptr, nullptr};
+  int rc_adj = PS_OK;
+  std::thread adj_thread;
+  if (!rc && any_adj) {
+    for (int k = 0; k < 3 && !rc; ++k)
+      if (adj_outs[k] && ps_alloc(&d_adjk[k], (size_t)cells, s) != cudaSuccess)
+        rc = ps_fail(PS_ERR_CUDA, "out of device memory");
+    if (!rc) {
+      cudaError_t e = cudaEventRecord(st->aux_ev, s);  // p (and the buffers) are ready
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st->aux, st->aux_ev, 0);
+      if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust handoff");
+    }
+    if (!rc) {
+      const int dev = st->device;
+      adj_thread = std::thread([&, dev] {
+        cudaSetDevice(dev);
+        for (int k = 0; k < 3 && rc_adj == PS_OK; ++k)
+          if (adj_outs[k]) rc_adj = ps_adjust_run(d_out[1], rows, cols, k, homogeneous ? 1 : 0, d_adjk[k], st->aux);
+      });
+    }
+  }
   for (int k = 0; k < 4 && !rc; ++k)
     if (outs && outs[k] && d_out[k]) rc = ps_stage_d2h(outs[k], d_out[k], sizeof(double) * cells, s);
   tr.mark("d2h");
+  if (adj_thread.joinable()) adj_thread.join();
+  if (!rc) rc = rc_adj;
   if (!rc && any_adj) {
-    if (ps_alloc(&d_adj, (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
-    for (int k = 0; k < 3 && !rc; ++k) {
-      if (!adj_outs[k]) continue;
-      rc = ps_adjust_run(d_out[1], rows, cols, k, homogeneous ? 1 : 0, d_adj, s);
-      if (!rc) rc = ps_stage_d2h(adj_outs[k], d_adj, sizeof(double) * cells, s);
-    }
+    cudaError_t e = cudaEventRecord(st->aux_ev, st->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, st->aux_ev, 0);
+    if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust join");
+    for (int k = 0; k < 3 && !rc; ++k)
+      if (adj_outs[k]) rc = ps_stage_d2h(adj_outs[k], d_adjk[k], sizeof(double) * cells, s);
   }
   tr.mark("adjust");
   if (!rc) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = ps_cuda_check(e, "run");
   }
+  for (int k = 0; k < 3; ++k) ps_free(d_adjk[k], s);
   for (int k = 0; k < 4; ++k) ps_free(d_out[k], s);
-  ps_free(d_adj, s);
+
   ps_matrix_destroy(ma);
   ps_matrix_destroy(mb);
   if (rc) cudaStreamSynchronize(s);

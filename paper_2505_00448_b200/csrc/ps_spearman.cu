@@ -32,11 +32,15 @@
 #include "ps_specfun.cuh"
 #include "ps_ties.cuh"
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace {
 
-constexpr int SW = 16;            // warps per CTA
+#ifndef PS_SW
+#define PS_SW 16
+#endif
+constexpr int SW = PS_SW;          // warps per CTA
 constexpr int STH = SW * 32;
 
 struct PairSums {
@@ -222,7 +226,7 @@ __device__ unsigned long long g_walk_cycles[40];
 constexpr unsigned long long kClosed = ~0ull;  // "tie-free: use the closed form"
 
 template <bool OGS, bool R2>
-__global__ void __launch_bounds__(STH, 2)
+__global__ void __launch_bounds__(STH, 32 / SW)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
@@ -769,7 +773,8 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   {
   const bool r2 = a->S <= 32767;  // 2r fits 16 bits: no parity bits
   size_t smem = walk_smem(a->ldo, a->ldt, true, r2);
-  const bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
+  bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
+  if (const char* e = getenv("PS_SPEARMAN_OGS")) ogs = smem <= limit && e[0] == '1';  // tuning override
   if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2);
   if (smem > limit)
     return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
