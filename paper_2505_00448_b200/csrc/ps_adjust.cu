@@ -258,6 +258,207 @@ __global__ void bonferroni_kernel(const uint64_t* __restrict__ keys, const uint3
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small families (m <= kSmallMax): the whole BH / BY adjustment in one CTA --
+// stable LSD radix on the high 32 key bits in registers / shared memory (as
+// the presort), short runs of equal high halves repaired on the low halves
+// (long ones: full 8-byte sort), then the scaled values, a block-wide reverse
+// cumulative minimum and the scatter.  No host round trips, two launches in
+// all (compaction + this) instead of ~30.
+constexpr int kSmallThreads = 1024, kSmallItems = 24;
+constexpr int kSmallMax = kSmallThreads * kSmallItems;  // 24576
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+adjust_small_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ fidx,
+                    const unsigned long long* __restrict__ count, double by_factor, int64_t cols, int symmetric,
+                    double* __restrict__ out) {
+  constexpr int ITEMS = kSmallItems;
+  extern __shared__ __align__(16) unsigned char asm_raw[];
+  uint32_t* sk32 = reinterpret_cast<uint32_t*>(asm_raw);
+  uint16_t* spos = reinterpret_cast<uint16_t*>(asm_raw + (size_t)kSmallMax * 4);
+  __shared__ uint16_t wcnt[kSmallWarps][256];
+  __shared__ int warp_buf[kSmallWarps];
+  __shared__ unsigned long long s_and, s_or;
+  __shared__ int s_long;
+  __shared__ double s_tmin[kSmallWarps];
+  const int m = (int)*count;
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    s_and = ~0ull;
+    s_or = 0ull;
+    s_long = 0;
+  }
+  __syncthreads();
+  uint32_t k32[ITEMS], idx[ITEMS];  // idx: position in keys[] | in-warp offset << 16
+  {
+    unsigned long long a = ~0ull, o = 0ull;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int p = warp * 32 * ITEMS + i * 32 + lane;
+      if (p < m) {
+        const uint64_t k = keys[p];
+        a &= k;
+        o |= k;
+      }
+    }
+#pragma unroll
+    for (int sft = 16; sft > 0; sft >>= 1) {
+      a &= __shfl_xor_sync(PS_FULL, a, sft);
+      o |= __shfl_xor_sync(PS_FULL, o, sft);
+    }
+    if (lane == 0) {
+      atomicAnd(&s_and, a);
+      atomicOr(&s_or, o);
+    }
+  }
+  __syncthreads();
+  const unsigned long long diff = s_and ^ s_or;
+  for (int round = 0, st0 = 1; round < 2; ++round, st0 = 0) {
+    for (int st = st0; st < 2; ++st) {
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int p = warp * 32 * ITEMS + i * 32 + lane;
+        const int pos = round == 0 ? p : (p < m ? spos[p] : p);
+        idx[i] = p < m ? (uint32_t)pos : 0xFFFFu;
+        const uint64_t k = p < m ? keys[pos] : ~0ull;
+        k32[i] = st ? (uint32_t)(k >> 32) : (uint32_t)k;
+      }
+      __syncthreads();
+      for (int b = 0; b < 4; ++b) {
+        const int shift = 8 * b;
+        if (((diff >> (32 * st + shift)) & 0xffull) == 0 || m <= 1) continue;
+        for (int i = threadIdx.x; i < kSmallWarps * 256; i += kSmallThreads) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const uint32_t dg = (k32[i] >> shift) & 0xffu;
+          const uint32_t peers = __match_any_sync(PS_FULL, dg);
+          const uint32_t base = wcnt[warp][dg];
+          __syncwarp();
+          idx[i] = (idx[i] & 0xFFFFu) | ((base + __popc(peers & lanemask_lt())) << 16);
+          if ((peers >> lane) == 1u) wcnt[warp][dg] = (uint16_t)(base + __popc(peers));
+          __syncwarp();
+        }
+        __syncthreads();
+        if (threadIdx.x < 256) {
+          uint32_t tot = 0;
+          for (int w = 0; w < kSmallWarps; ++w) tot += wcnt[w][threadIdx.x];
+          uint32_t x = tot;
+#pragma unroll
+          for (int sft = 1; sft < 32; sft <<= 1) {
+            const uint32_t y = __shfl_up_sync(PS_FULL, x, sft);
+            if (lane >= sft) x += y;
+          }
+          if (lane == 31) warp_buf[warp] = (int)x;
+          asm volatile("bar.sync 1, 256;");
+          uint32_t before = 0;
+          for (int w = 0; w < warp; ++w) before += (uint32_t)warp_buf[w];
+          uint32_t run = before + x - tot;
+          for (int w = 0; w < kSmallWarps; ++w) {
+            const uint32_t c = wcnt[w][threadIdx.x];
+            wcnt[w][threadIdx.x] = (uint16_t)run;
+            run += c;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const uint32_t dg = (k32[i] >> shift) & 0xffu;
+          const uint32_t dst = (uint32_t)wcnt[warp][dg] + (idx[i] >> 16);
+          sk32[dst] = k32[i];
+          spos[dst] = (uint16_t)idx[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int p = warp * 32 * ITEMS + i * 32 + lane;
+          k32[i] = sk32[p];
+          idx[i] = spos[p];
+        }
+        __syncthreads();
+      }
+    }
+    // positions not permuted by any pass are still in load order
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int p = warp * 32 * ITEMS + i * 32 + lane;
+      if (p < m) {
+        spos[p] = (uint16_t)idx[i];
+        sk32[p] = (uint32_t)(keys[idx[i] & 0xFFFFu] >> 32);
+      }
+    }
+    __syncthreads();
+    if (round == 1 || (uint32_t)diff == 0u) break;
+    for (int p = threadIdx.x; p < m; p += kSmallThreads) {  // repair colliding high halves
+      const uint32_t h = sk32[p];
+      if (p > 0 && sk32[p - 1] == h) continue;
+      int e = p + 1;
+      while (e < m && sk32[e] == h) ++e;
+      if (e - p == 1) continue;
+      if (e - p > 64) {
+        s_long = 1;
+        continue;
+      }
+      uint32_t lo[64];
+      uint16_t id[64];
+      const int n = e - p;
+      for (int q = 0; q < n; ++q) {
+        id[q] = spos[p + q];
+        lo[q] = (uint32_t)keys[id[q]];
+      }
+      for (int i = 1; i < n; ++i) {
+        const uint32_t ki = lo[i];
+        const uint16_t xi = id[i];
+        int j = i - 1;
+        while (j >= 0 && lo[j] > ki) {
+          lo[j + 1] = lo[j];
+          id[j + 1] = id[j];
+          --j;
+        }
+        lo[j + 1] = ki;
+        id[j + 1] = xi;
+      }
+      for (int q = 0; q < n; ++q) spos[p + q] = id[q];
+    }
+    __syncthreads();
+    if (!s_long) break;
+  }
+  // scaled values v_i = p_(i) * (scale / i) and their reverse cumulative
+  // minimum: thread t owns sorted positions [t*ITEMS, (t+1)*ITEMS)
+  const double scale = (double)m * by_factor;
+  const int i0 = threadIdx.x * ITEMS;
+  auto scaled = [&](int p) { return val_of(keys[spos[p]]) * (scale / (double)(p + 1)); };
+  double tmin = CUDART_INF;
+  for (int i = 0; i < ITEMS; ++i)
+    if (i0 + i < m) tmin = fmin(tmin, scaled(i0 + i));
+  // exclusive suffix minimum over threads (later threads)
+  double wmin = tmin;
+#pragma unroll
+  for (int sft = 1; sft < 32; sft <<= 1) {
+    const double y = __shfl_down_sync(PS_FULL, wmin, sft);
+    if (lane + sft < 32) wmin = fmin(wmin, y);
+  }
+  if (lane == 0) s_tmin[warp] = wmin;  // min over this warp's threads
+  __syncthreads();
+  double run = __shfl_down_sync(PS_FULL, wmin, 1);
+  if (lane == 31) run = CUDART_INF;
+  for (int w = warp + 1; w < kSmallWarps; ++w) run = fmin(run, s_tmin[w]);
+  for (int i = ITEMS - 1; i >= 0; --i) {
+    const int p = i0 + i;
+    if (p >= m) continue;
+    run = fmin(run, scaled(p));
+    const double r = fmin(1.0, run);
+    const int64_t f = fidx[spos[p]];
+    out[f] = r;
+    if (symmetric) {
+      const int64_t rr = f / cols, cc = f - rr * cols;
+      out[cc * cols + rr] = r;
+    }
+  }
+}
+
 int scan_u32(uint32_t* a, int64_t n, cudaStream_t s) {
   const int64_t nb = ps_ceil_div(n, 1024);
   uint32_t* sums = nullptr;
@@ -305,8 +506,21 @@ double numpy_pairwise_harmonic(int64_t m) {
 }
 
 int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int64_t cols,
-                int symmetric, int method, double* out, cudaStream_t s) {
+                int symmetric, int method, double* out, cudaStream_t s, int64_t fam_max) {
   ps_device_state* ds = ps_state();
+  if (method == PS_ADJ_BONFERRONI) {  // m is read on the device: no host round trip
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(fam_max, 256), (int64_t)ds->num_sms * 8));
+    bonferroni_kernel<<<blocks, 256, 0, s>>>(keys, idx, d_count, cols, symmetric, out);
+    PS_LAUNCHED();
+    return PS_OK;
+  }
+  if (method == PS_ADJ_BH && fam_max <= kSmallMax) {
+    const size_t smem = (size_t)kSmallMax * 6;
+    PS_CUDA(cudaFuncSetAttribute(adjust_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    adjust_small_kernel<<<1, kSmallThreads, smem, s>>>(keys, idx, d_count, 1.0, cols, symmetric, out);
+    PS_LAUNCHED();
+    return PS_OK;
+  }
   unsigned long long m_host = 0;
   PS_CUDA(cudaMemcpyAsync(&m_host, d_count, sizeof(m_host), cudaMemcpyDeviceToHost, s));
   PS_CUDA(cudaStreamSynchronize(s));
@@ -406,7 +620,7 @@ int ps_adjust_run(const double* p, int64_t rows, int64_t cols, int method, int s
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(n, 256), (int64_t)ds->num_sms * 8);
   extract_kernel<<<blocks, 256, 0, s>>>(p, rows, cols, symmetric, keys, idx, d_count);
   PS_LAUNCHED();
-  rc = adjust_core(keys, idx, d_count, cols, symmetric, method, out, s);
+  rc = adjust_core(keys, idx, d_count, cols, symmetric, method, out, s, fam);
   ps_free(keys, s);
   ps_free(idx, s);
   ps_free(d_count, s);
@@ -429,7 +643,7 @@ int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cu
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(n, 256), (int64_t)ds->num_sms * 8);
   extract_vec_kernel<<<blocks, 256, 0, s>>>(p, n, keys, idx, d_count);
   PS_LAUNCHED();
-  rc = adjust_core(keys, idx, d_count, n, 0, method, out, s);
+  rc = adjust_core(keys, idx, d_count, n, 0, method, out, s, n);
   ps_free(keys, s);
   ps_free(idx, s);
   ps_free(d_count, s);

@@ -29,9 +29,23 @@ def test_adjust_vector_families(oracle, method):
 
 
 @pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
-def test_adjust_symmetric(oracle, method):
+def test_adjust_low_bit_collisions(oracle, method):
+    """p-values equal in their high 32 bits (the small-family sort orders the
+    high halves first, then repairs or fully re-sorts colliding runs)."""
+    rng = np.random.default_rng(3)
+    for size in [500, 20000]:
+        v = 0.5 + rng.integers(0, 40, size) * 2.0**-45     # long colliding runs
+        w = rng.random(size)
+        w[::5] = 0.25 + rng.integers(0, 3, w[::5].size) * 2.0**-50  # short runs
+        for x in (v, w):
+            got = ps.adjust(x.reshape(1, -1), method, symmetric=False).ravel()
+            assert bitwise_equal(got, oracle.adjust_family(x, method)), (method, size)
+
+
+@pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
+@pytest.mark.parametrize("n", [150, 301])
+def test_adjust_symmetric(oracle, method, n):
     rng = np.random.default_rng(7)
-    n = 301
     up = rng.random(n * (n - 1) // 2) ** 3
     up[rng.random(up.size) < 0.1] = np.nan
     m = np.zeros((n, n))
