@@ -17,6 +17,7 @@
 #include "ps_tc05.cuh"
 #include <cudaTypedefs.h>
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace {
@@ -90,7 +91,7 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 }
 
 __global__ void __launch_bounds__(TTH_WS, 1)
-onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, const int2* __restrict__ tiles,
+onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbase, const int2* __restrict__ tiles,
                       int64_t ntiles, float* __restrict__ C, int64_t ldC) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TSTAGES], empty[TSTAGES], accfull, accempty;
@@ -128,8 +129,8 @@ onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, const in
         if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
         const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
         tc05::mbar_arrive_expect_tx(&full[st], TSTAGE_BYTES);
-        tc05::tma_load_2d(sa, &tmap, kc * TKB, t.x * TM, &full[st]);
-        tc05::tma_load_2d(sb, &tmap, kc * TKB, t.y * TN, &full[st]);
+        tc05::tma_load_2d(sa, &tmap, (kbase + kc) * TKB, t.x * TM, &full[st]);
+        tc05::tma_load_2d(sb, &tmap, (kbase + kc) * TKB, t.y * TN, &full[st]);
       }
     }
   } else if (warp == 5) {
@@ -393,11 +394,23 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
     CUtensorMap map;
     int rc = make_onehot_map(&map, O, Rp, Sp, TM);
     if (rc) return rc;
-    const int nk = (int)(Sp / TKB);
-    const int64_t iters = (int64_t)tl.size() * nk;
-    const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
+    // K phases: the one-hot operand (Rp x Sp bytes) is streamed through L2 in
+    // slabs that fit it, all CTAs working inside the same slab (stream-K
+    // spreads CTAs over K, which thrashes L2 when O is larger than it)
+    const int nk_all = (int)(Sp / TKB);
+    const int64_t slab_budget = 96ll << 20;  // L2 is 126 MB
+    int phases = (int)std::max<int64_t>(1, ps_ceil_div(Rp * Sp, slab_budget));
+    if (const char* e = getenv("PS_CHI2_PHASES")) phases = std::max(1, atoi(e));  // tuning override
+    phases = std::min(phases, nk_all);
     ps_prof_begin("chi2_gemm", s);
-    onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, d_tiles, (int64_t)tl.size(), C, Rp);
+    for (int ph = 0; ph < phases; ++ph) {
+      const int kb0 = (int)((int64_t)nk_all * ph / phases), kb1 = (int)((int64_t)nk_all * (ph + 1) / phases);
+      const int nk = kb1 - kb0;
+      const int64_t iters = (int64_t)tl.size() * nk;
+      const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
+      onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_tiles, (int64_t)tl.size(),
+                                                                      C, Rp);
+    }
     ps_prof_end(s);
     PS_LAUNCHED();
   }
