@@ -146,7 +146,12 @@ def sharded_run(request, mat_a, mat_b=None,
             continue
         t = torch.from_numpy(np.where(own, raw[name], 0.0))
         if world > 1:
-            tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
+            if tdist.get_backend() == "nccl":  # NCCL reduces device tensors (NVLink)
+                t = t.cuda()
+                tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
+                t = t.cpu()
+            else:
+                tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
         full[name] = t.numpy()
     if adjust_fn is None:
         from .adjust import adjust as adjust_fn  # device adjustment
