@@ -289,9 +289,10 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   const uint32_t* mrow = mask + f * W;
   auto key_of = [&](uint32_t sid) -> uint64_t { return sort_key(row[sid]); };
 
-  // 1. stable compaction of present sample ids: thread t owns the contiguous
-  //    samples [t*ITEMS, (t+1)*ITEMS); one block scan of the counts places them.
-  //    AND / OR over the present keys decide which radix bytes are constant.
+  // 1. stable compaction of present sample ids: warp w owns samples
+  //    [w*32*ITEMS, (w+1)*32*ITEMS) in (item, lane) order (coalesced loads);
+  //    one block scan of the warp counts places them.  AND / OR over the
+  //    present keys decide which radix bytes are constant.
   if (threadIdx.x == 0) {
     s_and = ~0ull;
     s_or = 0ull;
@@ -300,25 +301,38 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   }
   int n;
   {
-    const int64_t s0 = (int64_t)threadIdx.x * ITEMS;
-    uint32_t bits = 0;  // presence of this thread's ITEMS samples (ITEMS <= 32)
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int64_t sp = s0 + i;
-      if (sp < S && ((mrow[sp >> 5] >> (sp & 31)) & 1u)) bits |= 1u << i;
-    }
-    int tot;
-    int pos = block_excl_scan<QW>(__popc(bits), warp_buf, tot);
-    n = tot;
+    const int64_t s0 = (int64_t)warp * 32 * ITEMS;
+    uint32_t bal[ITEMS];
+    int wcount = 0;
     unsigned long long a = ~0ull, o = 0ull;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      if ((bits >> i) & 1u) {
-        const uint64_t k = key_of((uint32_t)(s0 + i));
+    for (int i = 0; i < ITEMS; ++i) {
+      const int64_t sp = s0 + i * 32 + lane;
+      const bool pres = sp < S && ((mrow[sp >> 5] >> (sp & 31)) & 1u);
+      bal[i] = __ballot_sync(PS_FULL, pres);
+      wcount += __popc(bal[i]);
+      if (pres) {
+        const uint64_t k = key_of((uint32_t)sp);
         a &= k;
         o |= k;
-        sidx[pos++] = (uint16_t)(s0 + i);
       }
+    }
+    // exclusive scan of the warp counts (lane 0 of each warp holds one)
+    if (lane == 0) warp_buf[warp] = wcount;
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < QW; ++w) {
+      const int c = warp_buf[w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    n = tot;
+    int run = before;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      if ((bal[i] >> lane) & 1u) sidx[run + __popc(bal[i] & lanemask_lt())] = (uint16_t)(s0 + i * 32 + lane);
+      run += __popc(bal[i]);
+    }
 #pragma unroll
     for (int sft = 16; sft > 0; sft >>= 1) {
       a &= __shfl_xor_sync(PS_FULL, a, sft);
