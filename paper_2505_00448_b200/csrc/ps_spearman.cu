@@ -73,8 +73,8 @@ extern __shared__ __align__(16) uint32_t sm32[];
 // 32-bit shared-address accessors: one register holds the CTA window base,
 // so hot loops never re-derive it from a generic pointer.
 __device__ __forceinline__ uint32_t ld16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  uint32_t v;  // zero-extended straight into a 32-bit register (no PRMT)
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint32_t ld32(uint32_t a) {
