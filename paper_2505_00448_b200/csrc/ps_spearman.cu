@@ -226,7 +226,7 @@ __device__ unsigned long long g_walk_cycles[40];
 constexpr unsigned long long kClosed = ~0ull;  // "tie-free: use the closed form"
 
 template <bool OGS, bool R2>
-__global__ void __launch_bounds__(STH, 32 / SW)
+__global__ void __launch_bounds__(STH, OGS ? 32 / SW : 16 / SW)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
@@ -375,11 +375,14 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // rank within the warp's segment; the segment bases are folded in by
       // pass B, so no prefix phase is needed here.
       const bool encA = !tg && La * 32 <= 4095;
+      // 2r fits 16 bits for this pair (always when S <= 32767; for larger S
+      // whenever the joint count n <= 32767): no parity bits needed
+      bool r2fit = R2;
       uint32_t segpreA = 0, n = 0, abase = 0;
       unsigned long long sa2 = 0;
       if (encA) {
         uint32_t cnt = 0;
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
           const uint32_t p = (uint32_t)(word * 32 + lane);
           const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
@@ -398,7 +401,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         // q = inv_h[order_g[p]]; with g's order staged in shared memory the
         // gathered q overwrites it in place, so phase 2 reads it sequentially
         uint32_t cnt = 0;
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
           const uint32_t p = (uint32_t)(word * 32 + lane);
           const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
@@ -415,6 +418,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       {
         uint32_t segpre;
         segment_bases(wtot, segpre, n);
+        r2fit = R2 || (2u * n + 1u <= 0xFFFFu);
         abase = __shfl_sync(PS_FULL, segpre, warp);
         if (tg && R2) {
           if (OGS)
@@ -437,16 +441,16 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // ---------------- pass A, phase 2: ranks -> R[q] -------------------
       auto q_at = [&](uint32_t p) -> uint32_t { return OGS ? ld16(aOg + 2 * p) : ld16(aInv + 2 * (uint32_t)og_g[p]); };
       if (!tg) {
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
           const uint32_t kw = ld32(kA(word));
           const uint32_t r = abase + ldP(word) + __popc(kw & ltmask) + 1u;
           const uint32_t q = q_at((uint32_t)(word * 32 + lane));
-          if ((kw >> lane) & 1u) st16(aR + 2 * q, R2 ? 2u * r : r);
+          if ((kw >> lane) & 1u) st16(aR + 2 * q, r2fit ? 2u * r : r);
         }
       } else if (R2) {
         const uint32_t* tbgg = tb + g * ldt;
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
           const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
           const uint32_t kw = rec.x;
@@ -462,6 +466,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         const uint32_t* tbgg = tb + g * ldt;
         const uint16_t* lbgg = lastb + g * ldt;
         const uint16_t* nbgg = nextb + g * ldt;
+#pragma unroll 4
         for (int word = a0; word < a1; ++word) {
           const uint32_t kw = ld32(kA(word));
           const uint32_t p = (uint32_t)(word * 32 + lane);
@@ -479,7 +484,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           if ((kw >> lane) & 1u) {
             const uint32_t q = q_at(p);
             sa2 += (unsigned long long)r2 * r2;
-            if (R2) {
+            if (r2fit) {
               st16(aR + 2 * q, r2);
             } else {
               st16(aR + 2 * q, r2 >> 1);
@@ -494,7 +499,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // decode R -> 2 r_g (all lanes must execute: shuffles)
       auto r2g_of = [&](uint32_t v, int word) -> uint32_t {
         if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu));
-        if (R2) return v;
+        if (r2fit) return v;
         return 2u * v + (tg ? ((ld32(aPar + 4 * word) >> lane) & 1u) : 0u);
       };
       const bool sweepB = !th;
@@ -505,7 +510,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         // segment bases of h's order are folded in after the reduction.
         uint32_t cnt = 0, s0l = 0;  // s0l: per lane <= 2S * (words per warp) < 2^32
         auto sweep = [&](auto enc) {
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
           for (int word = b0; word < b1; ++word) {
             const uint32_t q = (uint32_t)(word * 32 + lane);
             const uint32_t v = ld16(aR + 2 * q);
@@ -520,7 +525,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
               st16(aR + 2 * q, 0u);
             }
             cnt += __popc(B);
-            if (!R2 && tg) {  // parity bits of this word were read above
+            if (!r2fit && tg) {  // parity bits of this word were read above
               __syncwarp();
               if (lane == 0) st32(aPar + 4 * word, 0u);
             }
@@ -534,7 +539,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // ---------------- pass B, phase 1: keep = R != 0 over h's order ------
       {
         uint32_t cnt = 0;
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = b0; word < b1; ++word) {
           const bool keep = ld16(aR + 2 * (uint32_t)(word * 32 + lane)) != 0u;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
@@ -564,7 +569,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       }
       // ---------------- pass B, phase 2: accumulate, clear R ---------------
       if (!th) {
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(kA(word));
           const uint32_t q = (uint32_t)(word * 32 + lane);
@@ -575,7 +580,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             sab += (unsigned long long)r2g * rh;
             st16(aR + 2 * q, 0u);
           }
-          if (!R2 && tg) {
+          if (!r2fit && tg) {
             __syncwarp();
             if (lane == 0) st32(aPar + 4 * word, 0u);
           }
@@ -583,7 +588,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
       } else if (R2) {
         auto walk2 = [&](auto enc) {
-#pragma unroll 4
+#pragma unroll(OGS ? 4 : 8)
           for (int word = b0; word < b1; ++word) {
             const uint4 rec = ld128(aK + 16 * word);  // {K, P, sp, ep}
             const uint32_t kw = rec.x;
@@ -602,6 +607,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         if (encA) walk2(std::true_type{});
         else walk2(std::false_type{});
       } else {
+#pragma unroll 4
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(kA(word));
           const uint32_t q = (uint32_t)(word * 32 + lane);
@@ -614,7 +620,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             sbb += (unsigned long long)r2h * r2h;
             st16(aR + 2 * q, 0u);
           }
-          if (!R2 && tg) {
+          if (!r2fit && tg) {
             __syncwarp();
             if (lane == 0) st32(aPar + 4 * word, 0u);
           }
