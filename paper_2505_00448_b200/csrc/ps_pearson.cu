@@ -26,8 +26,12 @@ namespace {
 constexpr int T = 64;            // features per tile edge
 constexpr int KC = 32;           // samples per k-chunk (one mask word)
 constexpr int XS = KC + 4;       // padded smem row stride (doubles): 2 wavefronts per fragment load
-constexpr int NWARP = 8;         // 4 x 2 warps, 16 x 32 pairs each
-constexpr int WM = 2, WN = 4;    // 8x8 accumulator blocks per warp (rows x cols)
+#ifndef PS_PEARSON_WN
+#define PS_PEARSON_WN 4
+#endif
+constexpr int WM = 2, WN = PS_PEARSON_WN;  // 8x8 accumulator blocks per warp (rows x cols)
+constexpr int WJ = T / (8 * WN);           // column groups of warps
+constexpr int NWARP = (T / (8 * WM)) * WJ;  // WN = 4: 4 x 2 warps of 16 x 32 pairs
 constexpr int NTHR = NWARP * 32;
 constexpr double kReplayTau = 1e-3;
 
@@ -101,7 +105,7 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage* st = reinterpret_cast<Stage*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wi = warp >> 1, wj = warp & 1;
+  const int wi = warp / WJ, wj = warp % WJ;
   const int64_t tile = tile0 + blockIdx.x / nsplit;
   const int split = blockIdx.x % nsplit;
   int64_t I, J;
