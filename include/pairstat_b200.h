@@ -56,6 +56,7 @@ extern "C" {
 #define PS_ERR_UNKNOWN_METHOD 8     /* UnknownMethod     adjust.py:66-70 */
 #define PS_ERR_NON_SQUARE 9         /* NonSquareSymmetric adjust.py:77-81 */
 #define PS_ERR_NO_DEVICE 10
+#define PS_ERR_IO 11                /* OSError of matio.write_matrix / read_matrix */
 
 /* Tests, in the reference's TESTS order (datamodel.py:47-57). */
 #define PS_TEST_PEARSON 0
@@ -172,6 +173,39 @@ void ps_reset_kernel_launches(void);
  * is bracketed by CUDA events on its launch stream.  collect() sums them. */
 void ps_profile_enable(int on);
 int ps_profile_collect(const char* name, double* total_ms, int64_t* count);
+
+/* ---- delimited matrix files (matio.py:40-125; host code, no device) ----
+ * ps_write_matrix: the reference's write_matrix byte for byte: header
+ * delim-joined ["", col ids...], rows [row id, f"{v:.17g}"...] ("nan" for any
+ * NaN), "\n" line ends.  row_ids / col_ids may be NULL (f0.., s0..). */
+int ps_write_matrix(const char* path, const double* values, int64_t rows, int64_t cols,
+                    const char* const* row_ids, const char* const* col_ids, char delim);
+
+/* ps_read_matrix: read_matrix's parse (str.splitlines boundaries, empty lines
+ * skipped, Python float() grammar).  On return `error` is 0 (ok), 1 (empty
+ * file), 2 (ragged: err_row, err_count values) or 3 (malformed: err_row,
+ * err_col, err_cell bytes); rows are 1-based file lines as in the reference's
+ * messages.  ids are '\0'-terminated strings laid end to end.  Cells holding
+ * non-ASCII bytes are listed in `fallback` (flat indices) for the caller to
+ * parse.  Release with ps_matrix_file_free. */
+typedef struct ps_matrix_file {
+  int error;
+  int os_errno;
+  int64_t n_rows, n_cols;
+  const double* values;
+  const char* row_ids;
+  int64_t row_ids_len;
+  const char* col_ids;
+  int64_t col_ids_len;
+  const int64_t* fallback;
+  int64_t n_fallback;
+  int64_t err_row, err_col, err_count;
+  const char* err_cell;
+  int64_t err_cell_len;
+  void* impl;
+} ps_matrix_file;
+int ps_read_matrix(const char* path, char delim, ps_matrix_file* out);
+void ps_matrix_file_free(ps_matrix_file* f);
 
 #ifdef __cplusplus
 }

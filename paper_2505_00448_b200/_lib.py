@@ -60,6 +60,9 @@ EXPORTED = (
     "ps_reset_kernel_launches",
     "ps_profile_enable",
     "ps_profile_collect",
+    "ps_write_matrix",
+    "ps_read_matrix",
+    "ps_matrix_file_free",
 )
 
 
@@ -72,6 +75,30 @@ class MatrixDesc(ctypes.Structure):
         ("na_sentinel", ctypes.c_double),
         ("kind", ctypes.c_int),
         ("category_counts", ctypes.c_void_p),
+    ]
+
+
+class MatrixFile(ctypes.Structure):
+    """ps_matrix_file (include/pairstat_b200.h)."""
+
+    _fields_ = [
+        ("error", ctypes.c_int),
+        ("os_errno", ctypes.c_int),
+        ("n_rows", ctypes.c_int64),
+        ("n_cols", ctypes.c_int64),
+        ("values", ctypes.c_void_p),
+        ("row_ids", ctypes.c_void_p),
+        ("row_ids_len", ctypes.c_int64),
+        ("col_ids", ctypes.c_void_p),
+        ("col_ids_len", ctypes.c_int64),
+        ("fallback", ctypes.c_void_p),
+        ("n_fallback", ctypes.c_int64),
+        ("err_row", ctypes.c_int64),
+        ("err_col", ctypes.c_int64),
+        ("err_count", ctypes.c_int64),
+        ("err_cell", ctypes.c_void_p),
+        ("err_cell_len", ctypes.c_int64),
+        ("impl", ctypes.c_void_p),
     ]
 
 
@@ -120,6 +147,10 @@ def _declare(lib: ctypes.CDLL) -> None:
         ctypes.POINTER(ctypes.c_void_p),
     ]
     lib.ps_kernel_launches.restype = ctypes.c_int64
+    lib.ps_write_matrix.argtypes = [ctypes.c_char_p, dp, i64, i64, vp, vp, ctypes.c_char]
+    lib.ps_read_matrix.argtypes = [ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(MatrixFile)]
+    lib.ps_matrix_file_free.argtypes = [ctypes.POINTER(MatrixFile)]
+    lib.ps_matrix_file_free.restype = None
     lib.ps_profile_enable.argtypes = [i32]
     lib.ps_profile_collect.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int64)]

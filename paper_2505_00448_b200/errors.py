@@ -88,6 +88,7 @@ PS_ERR_DOMAIN = 7
 PS_ERR_UNKNOWN_METHOD = 8
 PS_ERR_NON_SQUARE = 9
 PS_ERR_NO_DEVICE = 10
+PS_ERR_IO = 11
 
 STATUS_TO_ERROR: dict[int, type[Exception]] = {
     PS_ERR_INVALID: ValueError,
@@ -100,6 +101,7 @@ STATUS_TO_ERROR: dict[int, type[Exception]] = {
     PS_ERR_UNKNOWN_METHOD: UnknownMethod,
     PS_ERR_NON_SQUARE: NonSquareSymmetric,
     PS_ERR_NO_DEVICE: RuntimeError,
+    PS_ERR_IO: OSError,
 }
 
 # Messages the reference raises from inside its kernels; the regexes in the
