@@ -32,6 +32,7 @@ constexpr int NTH = NW * 32;
 constexpr int WM = 2, WN = 4;
 constexpr int NSTAGE = 3;
 constexpr double kReplayTau = 1e-6;
+constexpr double kCancelTau = 1e-5;  // mean differences below this fraction of the raw RMS are replayed
 
 struct Stage {
   double x[T][XS];
@@ -327,12 +328,15 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
         if (!empty && n > k) {
           const double grand = total / (double)n;
           double ssb = 0.0, ssw = 0.0, mlo = CUDART_INF, mhi = -CUDART_INF, scale = 0.0;
+          double maxdev = 0.0, rms = 0.0;
           for (int j = 0; j < k; ++j) {
             const int64_t cell = (base + j) * Fq + h;
             const double nj = (double)Mn[cell], sj = Ms[cell], qj = Mq[cell];
             const double mj = sj / nj;
             const double dev = mj - grand;
             ssb += nj * dev * dev;
+            maxdev = fmax(maxdev, fabs(dev));
+            rms = fmax(rms, sqrt(fmax(0.0, (qj + 2.0 * c * sj + nj * c * c) / nj)));  // raw-value RMS
             const double gs = qj - sj * mj;
             // the reference forms ssq - sum*mean in raw (uncentred) sums:
             // replay exactly whenever the sign of that could be in doubt
@@ -343,6 +347,10 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
             mhi = fmax(mhi, mr);
             scale = fmax(scale, fabs(mr));
           }
+          // group means that agree to ~1e-4 of the raw magnitudes: SSB is a
+          // difference of nearly equal raw means, where the reference's own
+          // one-pass rounding is ~1e-9 of it -- replay the reference exactly
+          if (!(maxdev > kCancelTau * rms)) replay = true;
           if (replay) {
             push_replay(o, g, h);
             continue;
@@ -360,7 +368,10 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
         const double s0 = Ms[c0], s1 = Ms[c1], q0 = Mq[c0], q1 = Mq[c1];
         const double m0 = s0 / (double)n0, m1 = s1 / (double)n1;
         const double w0 = q0 - s0 * m0, w1 = q1 - s1 * m1;
-        if (!(w0 > kReplayTau * (q0 + (double)n0 * c * c)) || !(w1 > kReplayTau * (q1 + (double)n1 * c * c))) {
+        const double rms0 = sqrt(fmax(0.0, (q0 + 2.0 * c * s0 + (double)n0 * c * c) / (double)n0));
+        const double rms1 = sqrt(fmax(0.0, (q1 + 2.0 * c * s1 + (double)n1 * c * c) / (double)n1));
+        if (!(w0 > kReplayTau * (q0 + (double)n0 * c * c)) || !(w1 > kReplayTau * (q1 + (double)n1 * c * c)) ||
+            !(fabs(m0 - m1) > kCancelTau * fmax(rms0, rms1))) {  // (see the ANOVA SSB criterion)
           push_replay(o, g, h);
           continue;
         }
@@ -392,65 +403,82 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
   }
 }
 
-// Exact replay of _anova_rows / _ttest_rows (mixed.py:182-202, :498-520):
-// one thread per cell, samples in order, raw fp64 one-pass sums.
-template <int KM>
-__global__ void group_replay_kernel(int test, const uint32_t* __restrict__ zero_bits,
-                                    const uint8_t* __restrict__ codes, int64_t ldc,
-                                    const uint32_t* __restrict__ lmask, const double* __restrict__ vals,
-                                    int64_t ld, const uint32_t* __restrict__ vmask, int64_t W, int64_t S,
-                                    const int32_t* __restrict__ cat, int64_t Fq, int student, Outs o) {
-  const int count = *o.replay_count;
-  if (count == 0) return;
-  const bool overflow = count > o.replay_cap;
-  (void)overflow;
-  const int n_items = min(count, o.replay_cap);
-  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
-    const int64_t g = o.replay[it].x, h = o.replay[it].y;
-    const double* xv = vals + h * ld;
-    const uint32_t* mg = lmask + g * W;
+// Exact replay of _anova_rows / _ttest_rows (mixed.py:182-202, :498-520) for
+// the ill-conditioned cells.  The reference sums every group sequentially in
+// sample order; those per-group sums are independent, so one thread owns one
+// (cell, group): it walks the jointly present samples of its group (one-hot
+// row bits & the continuous mask, bit by bit in order) with raw fp64 one-pass
+// sums in registers.  A second kernel applies the reference finish.
+struct GroupPart {
+  long long n;
+  double sum, ssq;
+};
+
+__global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, const int32_t* __restrict__ off,
+                                          const double* __restrict__ vals, int64_t ld,
+                                          const uint32_t* __restrict__ vmask, int64_t W, const int2* __restrict__ items,
+                                          int n_items, int kslots, GroupPart* __restrict__ parts) {
+  // one warp per (cell, group): the lanes load each 32-sample word's values
+  // (coalesced) and lane 0 accumulates the group's present samples in order
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)n_items * kslots;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += nwarps) {
+    const int it = (int)(t / kslots), j = (int)(t % kslots);
+    const int64_t g = items[it].x, h = items[it].y;
+    const int k = off[g + 1] - off[g];
+    if (j >= k) continue;  // warp-uniform
+    const uint32_t* oh = ohbits + (int64_t)(off[g] + j) * W;
     const uint32_t* mh = vmask + h * W;
+    const double* xv = vals + h * ld;
+    long long n = 0;
+    double sum = 0.0, ssq = 0.0;
+    for (int64_t w0 = 0; w0 < W; w0 += 32) {
+      const uint32_t mw = w0 + lane < W ? oh[w0 + lane] & mh[w0 + lane] : 0u;
+      // values of the next 4 words in flight while the current one is summed
+      double pre[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pre[u] = w0 + u < W ? xv[(w0 + u) * 32 + lane] : 0.0;
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) {
+        uint32_t m = __shfl_sync(PS_FULL, mw, q);
+        const double vl = pre[q & 3];
+        pre[q & 3] = (q + 4 < 32 && w0 + q + 4 < W) ? xv[(w0 + q + 4) * 32 + lane] : 0.0;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1u;
+          const double v = __shfl_sync(PS_FULL, vl, b);
+          ++n;
+          sum += v;
+          ssq += v * v;
+        }
+      }
+    }
+    if (lane == 0) parts[t] = GroupPart{n, sum, ssq};
+  }
+}
+
+template <int KM>
+__global__ void group_replay_finish_kernel(int test, const int2* __restrict__ items, int n_items, int kslots,
+                                           const GroupPart* __restrict__ parts, const int32_t* __restrict__ off,
+                                           int64_t Fq, int student, Outs o) {
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
+    const int64_t g = items[it].x, h = items[it].y;
+    const GroupPart* pp = parts + (int64_t)it * kslots;
     double r0, r1, r2;
     if (test == PS_TEST_ANOVA) {
-      const int k = cat[g];
+      const int k = off[g + 1] - off[g];
       long long counts[KM];
       double sums[KM], ssq[KM];
       for (int j = 0; j < k; ++j) {
-        counts[j] = 0;
-        sums[j] = 0.0;
-        ssq[j] = 0.0;
-      }
-      const uint8_t* cg = codes + g * ldc;
-      for (int64_t s = 0; s < S; ++s) {
-        if (((mg[s >> 5] & mh[s >> 5]) >> (s & 31)) & 1u) {
-          const int j = cg[s];
-          if (j >= k) continue;  // out-of-range labels are reported by the label check
-          const double v = xv[s];
-          counts[j] += 1;
-          sums[j] += v;
-          ssq[j] += v * v;
-        }
+        counts[j] = pp[j].n;
+        sums[j] = pp[j].sum;
+        ssq[j] = pp[j].ssq;
       }
       anova_finish_raw(counts, sums, ssq, k, &r0, &r1, &r2, o.err);
-    } else {
-      const uint32_t* zg = zero_bits + g * W;  // present && label == 0.0
-      long long n0 = 0, n1 = 0;
-      double s0 = 0, s1 = 0, q0 = 0, q1 = 0;
-      for (int64_t s = 0; s < S; ++s) {
-        if (((mg[s >> 5] & mh[s >> 5]) >> (s & 31)) & 1u) {
-          const double v = xv[s];
-          if ((zg[s >> 5] >> (s & 31)) & 1u) {
-            ++n0;
-            s0 += v;
-            q0 += v * v;
-          } else {
-            ++n1;
-            s1 += v;
-            q1 += v * v;
-          }
-        }
-      }
-      ttest_finish_raw(n0, n1, s0, s1, q0, q1, student, &r0, &r1, &r2, o.err);
+    } else {  // one-hot rows: "label == 0", "label != 0"
+      ttest_finish_raw(pp[0].n, pp[1].n, pp[0].sum, pp[1].sum, pp[0].ssq, pp[1].ssq, student, &r0, &r1, &r2,
+                       o.err);
     }
     const int64_t idx = g * Fq + h;
     if (o.stat) o.stat[idx] = r0;
@@ -579,19 +607,28 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
     group_finish_kernel<256><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq,
                                                     lo, hi, student, o);
   PS_LAUNCHED();
-  if (small)
-    group_replay_kernel<16><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_zero, lab->d_codes, lab->ldc,
-                                                           lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
-                                                           S, lab->d_cat, Fq, student, o);
-  else
-    group_replay_kernel<256><<<ds->num_sms * 2, 64, 0, s>>>(test, lab->d_zero, lab->d_codes, lab->ldc,
-                                                            lab->d_mask, val->d_vals, val->ld, val->d_mask, W,
-                                                            S, lab->d_cat, Fq, student, o);
-  PS_LAUNCHED();
   // a replay list overflow (pathological: > 4M ill-conditioned cells) is reported
   int count = 0;
   PS_CUDA(cudaMemcpyAsync(&count, repc, sizeof(int), cudaMemcpyDeviceToHost, s));
   PS_CUDA(cudaStreamSynchronize(s));
+  const int n_items = std::min(count, cap);
+  if (n_items > 0) {
+    const int kslots = test == PS_TEST_ANOVA ? std::max(2, lab->cmax) : 2;
+    GroupPart* parts = nullptr;
+    PS_CUDA(ps_alloc(&parts, (size_t)n_items * kslots, s));
+    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((int64_t)n_items * kslots, 4), (int64_t)ds->num_sms * 8);
+    group_replay_parts_kernel<<<pblocks, 128, 0, s>>>(bits, d_off, val->d_vals, val->ld, val->d_mask, W, rep,
+                                                      n_items, kslots, parts);
+    PS_LAUNCHED();
+    const int fblocks = (int)std::min<int64_t>(ps_ceil_div(n_items, 128), (int64_t)ds->num_sms * 4);
+    if (small)
+      group_replay_finish_kernel<16><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student, o);
+    else
+      group_replay_finish_kernel<256><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student,
+                                                             o);
+    PS_LAUNCHED();
+    ps_free(parts, s);
+  }
   ps_free(bits, s);
   ps_free(d_rf, s);
   ps_free(d_rl, s);
