@@ -85,3 +85,16 @@ def test_pearson_config1(oracle):
     m = ~np.isnan(rr)
     assert np.all(np.abs(r[m] - rr[m]) <= 1e-9 * np.maximum(np.abs(rr[m]), 1e-3))
     assert p_close(res["p"], ref["p"])
+
+
+def test_pearson_config5_recipe_full_sample_count(oracle):
+    """Config-5 generator and missingness at its FULL sample count (10^5):
+    300 features x 10^5 samples, every pair checked against the oracle (the
+    k-loop length is what stresses the fp64 contraction's summation order)."""
+    import workloads as wl
+
+    rng = np.random.default_rng([wl.SEED_BASE, 5, 1])
+    x = wl._mcar(rng, wl._latent(rng, 300, 100000), 0.30)
+    mat = ps.make_matrix(x, "continuous", na_sentinel=wl.SENTINEL)
+    req = ps.TestRequest("pearson", ("stat", "p", "r2"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
