@@ -506,6 +506,18 @@ __global__ void mixed_label_check_kernel(const uint32_t* __restrict__ bad, const
 
 }  // namespace
 
+// LabelOutOfRange check of label rows [g0, g1) against continuous features
+// [h0, h1) (also used by the Kruskal-Wallis walk, mixed.py:613-617).
+int ps_mixed_label_check(ps_matrix* lab, ps_matrix* val, int64_t g0, int64_t g1, int64_t h0, int64_t h1,
+                         cudaStream_t s) {
+  if (g1 <= g0 || h1 <= h0) return PS_OK;
+  const int64_t W = val->W;
+  const dim3 grid((unsigned)ps_ceil_div(W, 128), (unsigned)ps_ceil_div(g1 - g0, 32));
+  mixed_label_check_kernel<<<grid, 128, 0, s>>>(lab->d_bad, val->d_mask, W, g0, g1, h0, h1, ps_state()->d_err);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
 int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
                         double* stat, double* p, double* eff, cudaStream_t s) {
   const int64_t Fc = lab->F, Fq = val->F, S = val->S;

@@ -89,6 +89,8 @@ inline void ps_free(void* p, cudaStream_t s) {
 
 // Kernel-family entry points (implemented per translation unit).
 int ps_prepare_matrix(ps_matrix* m, cudaStream_t s);
+int ps_mixed_label_check(ps_matrix* lab, ps_matrix* val, int64_t g0, int64_t g1, int64_t h0, int64_t h1,
+                         cudaStream_t s);
 int ps_prepare_alloc(ps_matrix* m, cudaStream_t s);
 int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
 int ps_presort_matrix(ps_matrix* m, cudaStream_t s);

@@ -122,6 +122,7 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
   // instead of a KM-way select chain in registers
   constexpr bool SMACC = KM == 8;
   uint32_t* accs = reinterpret_cast<uint32_t*>(take(SMACC ? (size_t)RW * KM * 32 * 4 : 0));
+  const uint32_t aAcc = (uint32_t)__cvta_generic_to_shared(accs) + 4u * (uint32_t)(((threadIdx.x >> 5) * KM) * 32 + (threadIdx.x & 31));
   // byte offsets into the dynamic buffer: indexing `smem[...]` directly keeps
   // the gathers in the shared window (LDS), never generic loads
   const uint32_t cg_off[2] = {(uint32_t)(cg_s[0] - smem), (uint32_t)(cg_s[1] - smem)};
@@ -193,7 +194,6 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
         __syncwarp();
       }
       long long tie = 0;
-      bool bad = false;
       if (!th) {
         // Tie-free h: ONE sweep over a contiguous segment per warp.  Ranks are
         // segment-local (running kept count); per level we keep sum(local)
@@ -207,7 +207,6 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
 #pragma unroll 4
         for (int word = w0; word < w1; ++word) {
           const uint32_t c = smem[cgo + smem16[oh_off + word * 32 + lane]];  // sentinel padded: 0xFF
-          bad |= c == 0xFEu;
           const bool keep = c != 0xFFu;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
           const uint32_t local = run + __popc(B & lanemask_lt()) + 1u;
@@ -217,7 +216,12 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
               atomicAdd(&bcnt[warp][c], 1u);
             }
           } else if constexpr (SMACC) {
-            if (keep && c < (uint32_t)KM) accs[(warp * KM + (int)c) * 32 + lane] += (1u << 20) + local;
+            if (keep && c < (uint32_t)KM) {  // slot (warp, c, lane): bank = lane
+              const uint32_t a = aAcc + (c << 7);
+              uint32_t v;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v + (1u << 20) + local));
+            }
           } else {
             const uint32_t packed = (1u << 20) + local;
 #pragma unroll
@@ -245,7 +249,6 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       for (int word = warp; word < nw; word += RW) {
         const int p = word * 32 + lane;
         const uint32_t c = p < nh ? (uint32_t)smem[cgo + smem16[oh_off + p]] : 0xFFu;
-        bad |= c == 0xFEu;
         const uint32_t B = __ballot_sync(PS_FULL, c != 0xFFu);
         if (lane == 0) K[word] = B;
       }
@@ -287,7 +290,6 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
           }
         }
       }
-      if (check_labels && __any_sync(PS_FULL, bad) && lane == 0) ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
       // -------- reduce to the pair's exact sums --------
 #pragma unroll
       for (int j = 0; j < (BIG ? 0 : NR); ++j) {
@@ -592,7 +594,10 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
     PS_LAUNCHED();
     codes = bcodes;
   }
-  int rc = 0;
+  // LabelOutOfRange: a present out-of-range label meeting a present value
+  // (mixed.py:613-617) -- checked up front, so the walk never tracks it
+  int rc = kw ? ps_mixed_label_check(lab, val, 0, Fc, lo, hi, s) : PS_OK;
+  if (rc) return rc;
   if (KM == 2) rc = launch_walk<2>(lab, val, codes, lo, hi, kw, queue, rs, s);
   else if (KM == 8) rc = launch_walk<8>(lab, val, codes, lo, hi, kw, queue, rs, s);
   else if (KM == 16) rc = launch_walk<16>(lab, val, codes, lo, hi, kw, queue, rs, s);
