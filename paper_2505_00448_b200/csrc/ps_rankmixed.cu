@@ -293,6 +293,7 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       // -------- reduce to the pair's exact sums --------
 #pragma unroll
       for (int j = 0; j < (BIG ? 0 : NR); ++j) {
+        if (j >= k && j != 0) continue;  // (uniform) levels past this label row's count
         // per lane: sum of local ranks < 2^20 (tie-free sweep) or of 2r < 2^24
         // (tied walk), so the warp sums fit 32 bits: integer warp reduce
         const uint32_t a = __reduce_add_sync(PS_FULL, acc[j]);
