@@ -174,6 +174,18 @@ void ps_reset_kernel_launches(void);
 void ps_profile_enable(int on);
 int ps_profile_collect(const char* name, double* total_ms, int64_t* count);
 
+/* ---- presort tables in caller buffers (multi-GPU sharded presort) ----
+ * Rank r presorts its own rows into buffers of F rows (ps_presort_layout gives
+ * the row strides: order / inv uint16 x ldo, tb uint32 x ldt, lastb / nextb
+ * uint16 x ldt, tied uint8, len int32), the ranks all-gather the rows (NCCL),
+ * then ps_matrix_presort_done marks the tables complete.  Rows are
+ * independent, so the gathered tables equal a single-GPU presort bit for bit. */
+int ps_presort_layout(int64_t n_samples, int64_t* ldo, int64_t* ldt);
+int ps_matrix_attach_presort(ps_matrix* m, void* order, void* inv, void* tb, void* lastb, void* nextb, void* tied,
+                             void* len, void* stream);
+int ps_matrix_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, void* stream);
+int ps_matrix_presort_done(ps_matrix* m, void* stream);
+
 /* ---- delimited matrix files (matio.py:40-125; host code, no device) ----
  * ps_write_matrix: the reference's write_matrix byte for byte: header
  * delim-joined ["", col ids...], rows [row id, f"{v:.17g}"...] ("nan" for any

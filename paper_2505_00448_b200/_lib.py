@@ -60,6 +60,10 @@ EXPORTED = (
     "ps_reset_kernel_launches",
     "ps_profile_enable",
     "ps_profile_collect",
+    "ps_presort_layout",
+    "ps_matrix_attach_presort",
+    "ps_matrix_presort_rows",
+    "ps_matrix_presort_done",
     "ps_write_matrix",
     "ps_read_matrix",
     "ps_matrix_file_free",
@@ -147,6 +151,10 @@ def _declare(lib: ctypes.CDLL) -> None:
         ctypes.POINTER(ctypes.c_void_p),
     ]
     lib.ps_kernel_launches.restype = ctypes.c_int64
+    lib.ps_presort_layout.argtypes = [i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.ps_matrix_attach_presort.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.ps_matrix_presort_rows.argtypes = [vp, i64, i64, vp]
+    lib.ps_matrix_presort_done.argtypes = [vp, vp]
     lib.ps_write_matrix.argtypes = [ctypes.c_char_p, dp, i64, i64, vp, vp, ctypes.c_char]
     lib.ps_read_matrix.argtypes = [ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(MatrixFile)]
     lib.ps_matrix_file_free.argtypes = [ctypes.POINTER(MatrixFile)]

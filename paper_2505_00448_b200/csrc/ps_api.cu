@@ -1,6 +1,7 @@
 // ps_api.cu -- the C ABI (include/pairstat_b200.h): device state, prepared
 // matrices, block entry points and the host-buffer run() used by Python.
 #include "ps_internal.cuh"
+#include "ps_ties.cuh"
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -310,6 +311,36 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
   return PS_OK;
 }
 
+int ps_presort_layout(int64_t S, int64_t* ldo, int64_t* ldt) {
+  if (S <= 0 || S > 65535) return ps_fail(PS_ERR_INVALID, "rank tests need 1 <= samples <= 65535");
+  *ldo = ps_round_up(S + 1, 64);
+  *ldt = tie_words(S);
+  return PS_OK;
+}
+
+int ps_matrix_attach_presort(ps_matrix* m, void* order, void* inv, void* tb, void* lastb, void* nextb, void* tied,
+                             void* len, void* stream) {
+  Guard g;
+  if (!m || m->has_presort || m->d_order) return ps_fail(PS_ERR_INVALID, "matrix already has presort tables");
+  return ps_presort_attach(m, static_cast<uint16_t*>(order), static_cast<uint16_t*>(inv), static_cast<uint32_t*>(tb),
+                           static_cast<uint16_t*>(lastb), static_cast<uint16_t*>(nextb), static_cast<uint8_t*>(tied),
+                           static_cast<int32_t*>(len), as_stream(stream));
+}
+
+int ps_matrix_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, void* stream) {
+  Guard g;
+  if (!m || !m->d_order) return ps_fail(PS_ERR_INVALID, "matrix has no presort tables attached");
+  f0 = std::max<int64_t>(0, f0);
+  f1 = std::min<int64_t>(m->F, f1);
+  return ps_presort_rows(m, f0, f1, as_stream(stream));
+}
+
+int ps_matrix_presort_done(ps_matrix* m, void* stream) {
+  Guard g;
+  if (!m || !m->d_order) return ps_fail(PS_ERR_INVALID, "matrix has no presort tables attached");
+  return ps_presort_end(m, as_stream(stream));
+}
+
 int ps_matrix_destroy(ps_matrix* m) {
   if (!m) return PS_OK;
   Guard g;
@@ -322,13 +353,16 @@ int ps_matrix_destroy(ps_matrix* m) {
   ps_free(m->d_codes, s);
   ps_free(m->d_zero, s);
   ps_free(m->d_bad, s);
-  ps_free(m->d_order, s);
-  ps_free(m->d_inv, s);
-  ps_free(m->d_tb, s);
-  ps_free(m->d_lastb, s);
-  ps_free(m->d_nextb, s);
-  ps_free(m->d_tied, s);
-  ps_free(m->d_len, s);
+  if (m->owns_presort) {
+    ps_free(m->d_order, s);
+    ps_free(m->d_inv, s);
+    ps_free(m->d_tb, s);
+    ps_free(m->d_lastb, s);
+    ps_free(m->d_nextb, s);
+    ps_free(m->d_tied, s);
+    ps_free(m->d_len, s);
+  }
+  for (void* p : m->presort_scratch) ps_free(p, s);
   delete[] m->h_cat;
   delete m;
   return PS_OK;

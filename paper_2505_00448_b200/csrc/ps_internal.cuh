@@ -33,6 +33,7 @@ struct ps_matrix {
   uint32_t* d_bad = nullptr;      // F x W bits: present && label out of [0, c_f)
   // presort tables (rank tests)
   bool has_presort = false;
+  bool owns_presort = true;       // false: tables live in caller buffers (ps_matrix_attach_presort)
   int32_t* d_len = nullptr;       // F present counts (== d_count)
   int64_t ldo = 0;                // row stride of d_order / d_inv (uint16), multiple of 64
   int64_t ldt = 0;                // row stride of the tie tables (words), tie_words(S)
@@ -95,6 +96,8 @@ int ps_prepare_alloc(ps_matrix* m, cudaStream_t s);
 int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
 int ps_presort_matrix(ps_matrix* m, cudaStream_t s);
 int ps_presort_begin(ps_matrix* m, cudaStream_t s);
+int ps_presort_attach(ps_matrix* m, uint16_t* order, uint16_t* inv, uint32_t* tb, uint16_t* lastb, uint16_t* nextb,
+                      uint8_t* tied, int32_t* len, cudaStream_t s);
 int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
 int ps_presort_end(ps_matrix* m, cudaStream_t s);
 int ps_fill_nan(double* p, int64_t n, cudaStream_t s);

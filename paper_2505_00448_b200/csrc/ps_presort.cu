@@ -547,6 +547,8 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
 
 // Presort in three steps so the per-feature sorts can follow the input
 // upload chunk by chunk (ps_matrix_create overlaps them with the H2D copy).
+static int presort_scratch(ps_matrix* m, cudaStream_t s);
+
 int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
   if (m->S > 65535)
     return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
@@ -559,6 +561,29 @@ int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
+  return presort_scratch(m, s);
+}
+
+// Caller-owned tables (multi-GPU: every rank presorts its own rows into them,
+// then the ranks all-gather the rows; rows are independent).
+int ps_presort_attach(ps_matrix* m, uint16_t* order, uint16_t* inv, uint32_t* tb, uint16_t* lastb, uint16_t* nextb,
+                      uint8_t* tied, int32_t* len, cudaStream_t s) {
+  if (m->S > 65535)
+    return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
+  m->ldo = ps_round_up(m->S + 1, 64);
+  m->ldt = tie_words(m->S);
+  m->d_order = order;
+  m->d_inv = inv;
+  m->d_tb = tb;
+  m->d_lastb = lastb;
+  m->d_nextb = nextb;
+  m->d_tied = tied;
+  m->d_len = len;
+  m->owns_presort = false;
+  return presort_scratch(m, s);
+}
+
+static int presort_scratch(ps_matrix* m, cudaStream_t s) {
   if (ps_ceil_div(m->S, QT) > 20) {  // global-memory radix path: per-feature scratch
     const int64_t FS = m->F * m->S;
     uint64_t *kA = nullptr, *kB = nullptr;
