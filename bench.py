@@ -349,12 +349,20 @@ def main():
     del want
 
     def step():
-        da = blocks.DeviceMatrix(xa, ka, sentinel, cat_a, n_samples=S,
-                                 presort=test == "spearman", stream=stream)
+        if world > 1 and test == "spearman":
+            # each rank presorts 1/world of the features; NCCL all-gathers the tables
+            da = blocks.DeviceMatrix(xa, ka, sentinel, cat_a, n_samples=S, stream=stream)
+            da.presort_sharded(rank, world, stream=stream)
+        else:
+            da = blocks.DeviceMatrix(xa, ka, sentinel, cat_a, n_samples=S,
+                                     presort=test == "spearman", stream=stream)
         db = None
         if xb is not None:
+            rank_walk = test in ("mwu", "kruskal")
             db = blocks.DeviceMatrix(xb, kb, sentinel, None, n_samples=S,
-                                     presort=test in ("mwu", "kruskal"), stream=stream)
+                                     presort=rank_walk and world == 1, stream=stream)
+            if rank_walk and world > 1:  # the walk only touches this rank's features
+                db.presort_rows_only(lo, hi, stream=stream)
         blocks.block(test, da, db, lo, hi, outs, stream=stream)
         if adj_methods:
             dist.adjust_gathered(test, outs[1], shape, plan, adj_methods, adj_out, stream)

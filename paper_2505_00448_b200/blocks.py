@@ -86,7 +86,13 @@ class DeviceMatrix:
         self.n_samples = S
         self.kind = kind
 
-    def presort_sharded(self, rank: int, world: int, gather=None, stream=None) -> None:
+    def presort_rows_only(self, f0: int, f1: int, stream=None) -> None:
+        """Presort only features [f0, f1) -- enough for a rank-range of a
+        Mann-Whitney / Kruskal-Wallis block, whose walk touches only the
+        continuous features of its range."""
+        self.presort_sharded(0, 1, rows=(f0, f1), stream=stream)
+
+    def presort_sharded(self, rank: int, world: int, gather=None, stream=None, rows=None) -> None:
         """Presort this rank's share of the features and all-gather the rows.
 
         Multi-GPU: instead of every rank presorting all F
@@ -102,17 +108,17 @@ class DeviceMatrix:
         ldo, ldt = ctypes.c_int64(), ctypes.c_int64()
         _lib.check(lib.ps_presort_layout(self.n_samples, ctypes.byref(ldo), ctypes.byref(ldt)))
         c = -(-self.n_features // world)
-        rows = c * world
+        nrows = c * world
         dev = torch.device("cuda", torch.cuda.current_device())
         widths = {"order": (ldo.value, torch.int16), "inv": (ldo.value, torch.int16),
                   "tb": (ldt.value, torch.int32), "lastb": (ldt.value, torch.int16),
                   "nextb": (ldt.value, torch.int16), "tied": (1, torch.uint8), "len": (1, torch.int32)}
-        tabs = {k: torch.zeros((rows, w), dtype=dt, device=dev) for k, (w, dt) in widths.items()}
+        tabs = {k: torch.zeros((nrows, w), dtype=dt, device=dev) for k, (w, dt) in widths.items()}
         self._keep.append(tabs)
         self.presort_tables = tabs
         s = _stream_ptr(stream)
         _lib.check(lib.ps_matrix_attach_presort(self.handle, *[_ptr(tabs[k]) for k in widths], s))
-        f0, f1 = rank * c, min(self.n_features, (rank + 1) * c)
+        f0, f1 = (rank * c, min(self.n_features, (rank + 1) * c)) if rows is None else rows
         if f1 > f0:
             _lib.check(lib.ps_matrix_presort_rows(self.handle, f0, f1, s))
         if world > 1:
@@ -123,7 +129,7 @@ class DeviceMatrix:
                     tdist.all_gather_into_tensor(full, local)
             sync(stream)  # the rows are complete before the collective reads them
             for name, t in tabs.items():
-                b = t.view(torch.uint8).view(rows, -1)
+                b = t.view(torch.uint8).view(nrows, -1)
                 gather(name, b, b[rank * c:(rank + 1) * c])
             torch.cuda.synchronize()  # the collectives ran on another stream
         _lib.check(lib.ps_matrix_presort_done(self.handle, s))

@@ -173,10 +173,17 @@ def _device_compute(request):
 
         canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
         shape = (mat_a.n_features, mat_a.n_features if mat_b is None else mat_b.n_features)
-        da = blocks.DeviceMatrix.from_datamatrix(mat_a, presort=test == "spearman")
+        _, world, rank = _world()
+        sharded = world > 1
+        da = blocks.DeviceMatrix.from_datamatrix(mat_a, presort=test == "spearman" and not sharded)
+        if test == "spearman" and sharded:  # 1/world of the presort per rank + all-gather
+            da.presort_sharded(rank, world)
         db = None
         if mat_b is not None:
-            db = blocks.DeviceMatrix.from_datamatrix(mat_b, presort=test in ("mwu", "kruskal"))
+            walk = test in ("mwu", "kruskal")
+            db = blocks.DeviceMatrix.from_datamatrix(mat_b, presort=walk and not sharded)
+            if walk and sharded:  # the walk only touches features [lo, hi)
+                db.presort_rows_only(lo, hi)
         outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda")
                 if n in wanted else None for n in canonical]
         blocks.block(test, da, db, lo, hi, outs, t_variant=request.t_variant,

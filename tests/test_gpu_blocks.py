@@ -121,3 +121,25 @@ def test_sharded_presort_matches_single_device(oracle, test, S):
         assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
     for d in (ref_dm, r0, r1):
         d.close()
+
+
+@pytest.mark.parametrize("test", ["kruskal", "mwu"])
+def test_rank_walk_with_rows_only_presort(test):
+    """A rank of a mixed rank test presorts only its continuous features."""
+    S, Fq = 700, 30
+    kind = "categorical" if test == "kruskal" else "dichotomous"
+    lab = ps.make_matrix(workloads.simulate(5, S, kind, categories=4, na_ratio=0.1, seed=9), kind)
+    cont = workloads.simulate(Fq, S, "continuous", na_ratio=0.2, seed=11)
+    cont[12] = np.round(cont[12])
+    mat = ps.make_matrix(cont, "continuous")
+    dl = blocks.DeviceMatrix(lab.values, kind, lab.na_sentinel, lab.category_counts)
+    full = blocks.DeviceMatrix(mat.values, "continuous", mat.na_sentinel, presort=True)
+    part = blocks.DeviceMatrix(mat.values, "continuous", mat.na_sentinel)
+    part.presort_rows_only(10, 20)
+    shape = (5, Fq)
+    a = _device_outputs(test, dl, full, shape, 10, 20)
+    b = _device_outputs(test, dl, part, shape, 10, 20)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+    for d in (dl, full, part):
+        d.close()
