@@ -288,7 +288,7 @@ def main():
     ap.add_argument("--test", default=None, help="test within a multi-test config (config 4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
 
     cfg = workloads.config(args.config)
@@ -457,7 +457,8 @@ def main():
         mat_a = ps.make_matrix(a, ka, na_sentinel=sentinel)
         mat_b = ps.make_matrix(b, kb, na_sentinel=sentinel) if b is not None else None
         req = ps.TestRequest(test, outputs)
-        ps.run(req, mat_a, mat_b)
+        for _ in range(2):  # warm-up (pool growth, first-touch of the pinned ring)
+            ps.run(req, mat_a, mat_b)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 #include <vector>
 #include <thread>
@@ -41,8 +42,13 @@ int init_state(ps_device_state* st, int dev) {
   PS_CUDA(cudaMalloc(&st->d_err, sizeof(int)));
   PS_CUDA(cudaMemset(st->d_err, 0, sizeof(int)));
   PS_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
-  PS_CUDA(cudaStreamCreateWithFlags(&st->aux, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;
+  PS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // aux carries the per-chunk prep / presort that incremental walks wait on
+  PS_CUDA(cudaStreamCreateWithPriority(&st->aux, cudaStreamNonBlocking, prio_hi));
   PS_CUDA(cudaEventCreateWithFlags(&st->aux_ev, cudaEventDisableTiming));
+  for (int k = 0; k < 2; ++k) PS_CUDA(cudaStreamCreateWithFlags(&st->walk[k], cudaStreamNonBlocking));
+  for (int k = 0; k < 3; ++k) PS_CUDA(cudaEventCreateWithFlags(&st->walk_ev[k], cudaEventDisableTiming));
   // keep freed workspace cached in the stream-ordered pool between calls
   cudaMemPool_t pool;
   PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -129,6 +135,46 @@ struct Trace {
     t = now;
   }
 };
+// PS_TIMELINE=1: device timestamps (a one-thread kernel reads %globaltimer
+// when its stream reaches the mark) and host enqueue times of the staging /
+// presort / walk stages of ps_run, printed at the end of the run.
+__global__ void stamp_kernel(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+struct Timeline {
+  bool on = getenv("PS_TIMELINE") != nullptr;
+  std::vector<std::string> what;
+  std::vector<double> host_ms;
+  unsigned long long* d = nullptr;
+  std::chrono::steady_clock::time_point t0;
+  void mark(const std::string& w, cudaStream_t st) {
+    if (!on) return;
+    if (!d) {
+      cudaMalloc(&d, 256 * sizeof(unsigned long long));
+      t0 = std::chrono::steady_clock::now();
+    }
+    if (what.size() >= 256) return;
+    stamp_kernel<<<1, 1, 0, st>>>(d + what.size());
+    what.push_back(w);
+    host_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+  void dump() {
+    if (!on || what.empty()) return;
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> t(what.size());
+    cudaMemcpy(t.data(), d, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    for (size_t k = 0; k < t.size(); ++k)
+      fprintf(stderr, "[timeline] %-28s gpu %8.3f ms   host %8.3f ms\n", what[k].c_str(), (t[k] - t[0]) * 1e-6,
+              host_ms[k] - host_ms[0]);
+    what.clear();
+    host_ms.clear();
+    cudaFree(d);
+    d = nullptr;
+  }
+};
+Timeline g_tl;
 }  // namespace
 
 extern "C" {
@@ -187,15 +233,20 @@ int ps_set_device(int device) {
   return ensure_state();
 }
 
-int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_presort, void* stream,
-                     ps_matrix** out) {
-  Guard g;
+}  // extern "C"
+
+// Called on the auxiliary stream after each staged chunk of rows [0, r1) is
+// prepared (and presorted): lets ps_run start computing on the rows already
+// uploaded while the rest of the input is still in flight.
+using RowsHook = std::function<int(ps_matrix*, int64_t r1, cudaStream_t aux)>;
+
+static int matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_presort, cudaStream_t s,
+                         ps_matrix** out, const RowsHook* hook) {
   *out = nullptr;
   int rc = ensure_state();
   if (rc) return rc;
   if (!desc || desc->n_features <= 0 || desc->n_samples <= 0)
     return ps_fail(PS_ERR_INVALID, "expected a non-empty matrix");
-  cudaStream_t s = as_stream(stream);
   Trace tr;
   tr.s = s;
   ps_matrix* m = new ps_matrix();
@@ -276,8 +327,11 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
       if (!rc) {
         auto on_rows = [&](int64_t r0, int64_t nr, cudaEvent_t ev) -> int {
           PS_CUDA(cudaStreamWaitEvent(st->aux, ev, 0));
+          g_tl.mark("rows " + std::to_string(r0 + nr) + " copied", st->aux);
           int c = ps_prepare_rows(m, r0, r0 + nr, st->aux);
           if (!c && want_presort) c = ps_presort_rows(m, r0, r0 + nr, st->aux);
+          g_tl.mark("  presorted", st->aux);
+          if (!c && hook) c = (*hook)(m, r0 + nr, st->aux);
           return c;
         };
         rc = ps_stage_h2d_2d(m->d_vals, sizeof(double) * m->ld, desc->values, sizeof(double) * src_ld,
@@ -309,6 +363,14 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
   }
   *out = m;
   return PS_OK;
+}
+
+extern "C" {
+
+int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_presort, void* stream,
+                     ps_matrix** out) {
+  Guard g;
+  return matrix_create(desc, values_on_device, want_presort, as_stream(stream), out, nullptr);
 }
 
 int ps_presort_layout(int64_t S, int64_t* ldo, int64_t* ldt) {
@@ -485,16 +547,33 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   const bool presort_b = test == PS_TEST_MWU || test == PS_TEST_KRUSKAL;
   ps_matrix* ma = nullptr;
   ps_matrix* mb = nullptr;
-  rc = ps_matrix_create(a, 0, presort_a, s, &ma);
-  if (!rc && !homogeneous) rc = ps_matrix_create(b, 0, presort_b, s, &mb);
+  bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
+  const bool any_out = any_adj || (outs && (outs[0] || outs[1] || outs[2] || outs[3]));
+  // Spearman: the walk over columns h < r1 starts as soon as rows [0, r1) are
+  // uploaded and presorted, overlapping the rest of the upload
+  ps_spearman_job* sjob = nullptr;
+  RowsHook walk_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
+    if (!sjob) {
+      int c = ps_spearman_begin(m, 0, m->F, aux, &sjob);
+      if (c) return c;
+    }
+    int c = ps_spearman_walk_upto(sjob, r1, aux);
+    g_tl.mark("  walk launched " + std::to_string(r1), st->walk[0]);
+    g_tl.mark("  walk launched " + std::to_string(r1) + "'", st->walk[1]);
+    return c;
+  };
+  g_tl.mark("start", s);
+  const bool overlap = test == PS_TEST_SPEARMAN && any_out && !getenv("PS_NO_OVERLAP");
+  rc = matrix_create(a, 0, presort_a, s, &ma, overlap ? &walk_hook : nullptr);
+  if (!rc && !homogeneous) rc = matrix_create(b, 0, presort_b, s, &mb, nullptr);
   if (rc) {
+    ps_spearman_abort(sjob, s);
     ps_matrix_destroy(ma);
     return rc;
   }
   tr.mark("matrices");
   const int64_t rows = ma->F, cols = homogeneous ? ma->F : mb->F;
   const int64_t cells = rows * cols;
-  bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
   double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
   for (int k = 0; k < 4 && !rc; ++k) {
     const bool want = (outs && outs[k]) || (k == 1 && any_adj);
@@ -505,7 +584,14 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   if (!rc) {
     switch (test) {
       case PS_TEST_PEARSON: rc = ps_pearson_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s); break;
-      case PS_TEST_SPEARMAN: rc = ps_spearman_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s); break;
+      case PS_TEST_SPEARMAN:
+        if (sjob) {
+          rc = ps_spearman_end(sjob, d_out[0], d_out[1], d_out[2], s);
+          sjob = nullptr;
+        } else {
+          rc = ps_spearman_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s);
+        }
+        break;
       case PS_TEST_CHI2: rc = ps_chi2_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], d_out[3], s); break;
       case PS_TEST_TTEST:
         rc = ps_group_moment_run(PS_TEST_TTEST, ma, mb, 0, cells, t_variant == 0, d_out[0], d_out[1],
@@ -523,7 +609,9 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
       default: rc = ps_fail(PS_ERR_INVALID, "unknown test");
     }
   }
+  if (sjob) ps_spearman_abort(sjob, s);  // not consumed (an earlier failure)
   if (!rc) rc = drain_errors(s);
+  g_tl.mark("compute done", s);
   tr.mark("compute");
   // The p-value adjustments run on the auxiliary stream, driven by a helper
   // thread (the adjust path reads sizes back to the host), while this thread
@@ -566,6 +654,8 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) rc = ps_cuda_check(e, "run");
   }
+  g_tl.mark("end", s);
+  g_tl.dump();
   for (int k = 0; k < 3; ++k) ps_free(d_adjk[k], s);
   for (int k = 0; k < 4; ++k) ps_free(d_out[k], s);
 

@@ -54,6 +54,8 @@ struct ps_device_state {
   cudaStream_t stream = nullptr;  // library stream used by ps_run
   cudaStream_t aux = nullptr;     // second stream: per-chunk prep / presort during uploads
   cudaEvent_t aux_ev = nullptr;
+  cudaStream_t walk[2] = {nullptr, nullptr};  // incremental rank walks during uploads
+  cudaEvent_t walk_ev[3] = {nullptr, nullptr, nullptr};
 };
 
 ps_device_state* ps_state();                 // current device's state
@@ -103,6 +105,14 @@ int ps_presort_end(ps_matrix* m, cudaStream_t s);
 int ps_fill_nan(double* p, int64_t n, cudaStream_t s);
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s);
+struct ps_spearman_job;
+// Incremental Spearman walk (ps_run overlaps it with the input upload):
+// begin allocates, walk_upto walks the columns h < h1 whose rows are
+// presorted, end walks the rest, folds and finishes (and frees the job).
+int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, cudaStream_t s, ps_spearman_job** job);
+int ps_spearman_walk_upto(ps_spearman_job* job, int64_t h1, cudaStream_t s);
+int ps_spearman_end(ps_spearman_job* job, double* stat, double* p, double* rho, cudaStream_t s);
+void ps_spearman_abort(ps_spearman_job* job, cudaStream_t s);
 int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
                     cudaStream_t s);
 int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi,

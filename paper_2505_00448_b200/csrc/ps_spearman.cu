@@ -64,6 +64,48 @@ struct PairParts {
 };
 constexpr int kSlots = 3;
 
+// Work items of one walk launch: the pairs g <= h with h in [h0, h1) and g in
+// [lo, min(h, hi - 1)], cut into blocks of at most gb consecutive g.  Items
+// are numbered from the largest h down (most work first) and decoded in
+// closed form, so a launch needs no item table.
+struct WalkItems {
+  int64_t h0, h1, lo, hi, gb;
+  int sh;  // log2(gb) when gb is a power of two (shift instead of divide), else -1
+  __host__ __device__ int64_t div(int64_t n) const {  // n, gb < 2^31
+    return sh >= 0 ? n >> sh : (int64_t)((uint32_t)n / (uint32_t)gb);
+  }
+  // sum_{x=1..n} ceil(x / gb)
+  __host__ __device__ int64_t ramp(int64_t n) const {
+    if (n <= 0) return 0;
+    const int64_t q = div(n), r = n - q * gb;
+    return gb * q * (q + 1) / 2 + r * (q + 1);
+  }
+  // items with h' in [a, h1), a >= max(h0, lo)
+  __host__ __device__ int64_t from(int64_t a) const {
+    const int64_t m1 = h1 < hi - 1 ? h1 : hi - 1;  // ramp region h' < hi - 1
+    int64_t c = 0;
+    if (a < m1) c += ramp(m1 - lo) - ramp(a - lo);
+    const int64_t f0 = a > hi - 1 ? a : hi - 1;
+    if (f0 < h1) c += (h1 - f0) * div(hi - lo + gb - 1);
+    return c;
+  }
+  __host__ __device__ int64_t first() const { return h0 > lo ? h0 : lo; }
+  __host__ __device__ int64_t total() const { return first() < h1 && lo < hi ? from(first()) : 0; }
+};
+
+// The item table of one launch: column h writes its blocks at the closed-form
+// offset from(h + 1), so no scan is needed.  item = (h, g0, g1).
+__global__ void walk_items_kernel(WalkItems wi, int4* __restrict__ items) {
+  const int64_t h = wi.first() + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h >= wi.h1) return;
+  const int64_t base = wi.from(h + 1), nb = wi.from(h) - base;
+  const int64_t gend = (h < wi.hi - 1 ? h : wi.hi - 1) + 1;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t g0 = wi.lo + b * wi.gb;
+    items[base + b] = make_int4((int)h, (int)g0, (int)(g0 + wi.gb < gend ? g0 + wi.gb : gend), 0);
+  }
+}
+
 // All shared-memory regions are addressed as integer offsets into two views of
 // the one dynamic buffer, so every access compiles to LDS/STS (no generic
 // pointers, no per-access window conversion).
@@ -230,8 +272,8 @@ __global__ void __launch_bounds__(STH, OGS ? 32 / SW : 16 / SW)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
-                     const int32_t* __restrict__ lens, int64_t F, int64_t lo, int64_t hi,
-                     int* __restrict__ queue, PairParts out) {
+                     const int32_t* __restrict__ lens, int64_t F, const int4* __restrict__ items, int n_items,
+                     int once, int* __restrict__ queue, PairParts out) {
   const WalkLayout L(ldo, ldt, OGS, R2);
   __shared__ uint32_t wtot[SW], wtotA[SW];
   __shared__ int s_item;
@@ -311,14 +353,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
     asm volatile("cp.async.commit_group;");
   };
 
-  const int64_t nh_items = F - lo;
+  __shared__ int4 s_it;
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    if (threadIdx.x == 0) {
+      const int item = atomicAdd(queue, 1);
+      s_it = item < n_items ? items[item] : make_int4(-1, 0, 0, 0);
+    }
     __syncthreads();
-    const int item = s_item;
-    if (item >= nh_items) break;
-    const int64_t h = F - 1 - item;  // largest rows of work first
+    const int4 it = s_it;
+    if (it.x < 0) break;
+    const int64_t h = it.x;
+    const int64_t lo = it.y;  // g block [lo, gmax]
     const int nh = lens[h];
     const bool th = tied[h] != 0;
     {
@@ -333,7 +379,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
       }
     }
-    const int64_t gmax = std::min<int64_t>(h, hi - 1);
+    const int64_t gmax = it.z - 1;
     if (OGS && lo <= gmax) prefetch(lo, 0);
     __syncthreads();
     const int nwb = (nh + 31) >> 5;
@@ -647,6 +693,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       WT(6);
     }
     if (OGS) asm volatile("cp.async.wait_group 0;");
+    if (once) break;  // one item per CTA: retiring CTAs let higher-priority kernels in
   }
 }
 
@@ -756,74 +803,213 @@ size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs, bool r2) { return (size_t)W
 
 }  // namespace
 
-int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
-                    cudaStream_t s) {
+using WalkKernel = decltype(&spearman_walk_kernel<true, true>);
+
+struct ps_spearman_job {
+  ps_matrix* a = nullptr;
+  int64_t lo = 0, hi = 0;
+  WalkKernel kern = nullptr;
+  size_t smem = 0;
+  int grid_max = 1;
+  int64_t gb = 32;     // g rows per work item of incremental launches
+  int64_t rows = 0;    // g rows per partials chunk
+  bool single = false; // one chunk: columns may be walked incrementally
+  int64_t h_done = 0;  // columns [lo, h_done) walked (single chunk)
+  PairSums ps{};
+  PairParts pp{nullptr, nullptr, 0};
+  int4* items = nullptr;  // item tables, one region per launch
+  int64_t items_cap = 0, items_used = 0;
+  int* queues = nullptr;
+  int qn = 256, qi = 0;
+  cudaStream_t home = nullptr;  // allocation stream (frees are ordered on it)
+  int nws = 0;                  // incremental launches so far (alternate walk streams)
+};
+
+static void job_free(ps_spearman_job* j, cudaStream_t s) {
+  ps_free(j->ps.n, s);
+  ps_free(j->ps.sxx4, s);
+  ps_free(j->ps.syy4, s);
+  ps_free(j->ps.sxy4, s);
+  ps_free(j->pp.part, s);
+  ps_free(j->pp.meta, s);
+  ps_free(j->queues, s);
+  ps_free(j->items, s);
+  delete j;
+}
+
+// One walk launch over columns [h0, h1) and g rows [c0, c1) (partials chunk c0).
+static int walk_launch(ps_spearman_job* j, int64_t h0, int64_t h1, int64_t c0, int64_t c1, int64_t gb,
+                       cudaStream_t s, int grid_max, int once = 0) {
+  int sh = -1;
+  for (int b = 0; b < 40; ++b)
+    if (((int64_t)1 << b) == gb) sh = b;
+  const WalkItems wi{h0, h1, c0, c1, gb, sh};
+  const int64_t n = wi.total();
+  if (n <= 0) return PS_OK;
+  if (j->qi >= j->qn) {
+    PS_CUDA(cudaMemsetAsync(j->queues, 0, sizeof(int) * j->qn, s));
+    j->qi = 0;
+  }
+  int* q = j->queues + j->qi++;
+  if (j->items_used + n > j->items_cap) return ps_fail(PS_ERR_INVALID, "spearman: item table overflow");
+  int4* items = j->items + j->items_used;
+  j->items_used += n;
+  walk_items_kernel<<<(unsigned)ps_ceil_div(h1 - wi.first(), 128), 128, 0, s>>>(wi, items);
+  PS_LAUNCHED();
+  ps_matrix* a = j->a;
+  PairParts pp = j->pp;
+  pp.c0 = c0;
+  const int grid = once ? (int)n : (int)std::min<int64_t>(n, grid_max);
+  ps_prof_begin("spearman_walk", s);
+  j->kern<<<grid, STH, j->smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
+                                     a->d_tied, a->d_len, a->F, items, (int)n, once, q, pp);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+static int partials_launch(ps_spearman_job* j, int64_t c0, int64_t c1, cudaStream_t s) {
+  PairParts pp = j->pp;
+  pp.c0 = c0;
+  const int pblocks = (int)std::min<int64_t>(ps_ceil_div((c1 - c0) * j->a->F, 8), (int64_t)ps_state()->num_sms * 32);
+  spearman_partials_kernel<<<pblocks, 256, 0, s>>>(pp, j->a->F, c1, j->ps);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, cudaStream_t s, ps_spearman_job** out) {
+  *out = nullptr;
   const int64_t F = a->F;
   lo = std::max<int64_t>(0, lo);
   hi = std::min<int64_t>(F, hi);
-  if (hi <= lo || (!stat && !p && !rho)) return PS_OK;
-  if (!a->has_presort) {
-    int rc = ps_presort_matrix(a, s);
-    if (rc) return rc;
-  }
   ps_device_state* ds = ps_state();
   const size_t limit = 227 * 1024 - 1024;
-  PairSums ps{};
-  int* queue = nullptr;
-  PS_CUDA(ps_alloc(&ps.n, (size_t)(F * F), s));
-  PS_CUDA(ps_alloc(&ps.sxx4, (size_t)(F * F), s));
-  PS_CUDA(ps_alloc(&ps.syy4, (size_t)(F * F), s));
-  PS_CUDA(ps_alloc(&ps.sxy4, (size_t)(F * F), s));
-  PS_CUDA(ps_alloc(&queue, 1, s));
-  PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
-  {
   const bool r2 = a->S <= 32767;  // 2r fits 16 bits: no parity bits
   size_t smem = walk_smem(a->ldo, a->ldt, true, r2);
   bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
   if (const char* e = getenv("PS_SPEARMAN_OGS")) ogs = smem <= limit && e[0] == '1';  // tuning override
   if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2);
-  if (smem > limit)
-    return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
-  auto kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
-                  : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
-  PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > limit) return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
+  ps_spearman_job* j = new ps_spearman_job();
+  j->a = a;
+  j->lo = lo;
+  j->hi = hi;
+  j->h_done = lo;
+  j->smem = smem;
+  j->kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
+                : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
+  j->home = s;
+  if (const char* e = getenv("PS_SPEARMAN_GB")) j->gb = std::max<int64_t>(1, atoll(e));
+  int rc = PS_OK;
+  auto fail = [&](cudaError_t e) {
+    job_free(j, s);
+    return ps_cuda_check(e, "spearman setup");
+  };
+  cudaError_t e = cudaFuncSetAttribute(j->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, STH, smem));
-  per_sm = std::max(1, per_sm);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, j->kern, STH, smem);
+  if (e != cudaSuccess) return fail(e);
+  j->grid_max = ds->num_sms * std::max(1, per_sm);
   // g rows per chunk: the per-warp partials take kSlots * SW * 8 B per cell
   const int64_t per_row = F * (int64_t)(kSlots * SW + 1) * 8;
-  const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(hi - lo, ((int64_t)2 << 30) / per_row));
-  PairParts pp{nullptr, nullptr, lo};
-  PS_CUDA(ps_alloc(&pp.part, (size_t)(rows * F * kSlots * SW), s));
-  PS_CUDA(ps_alloc(&pp.meta, (size_t)(rows * F), s));
-  for (int64_t c0 = lo; c0 < hi; c0 += rows) {
-    const int64_t c1 = std::min<int64_t>(hi, c0 + rows);
-    pp.c0 = c0;
-    if (c0 > lo) PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
-    const int64_t items = F - c0;
-    const int grid = (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
-    ps_prof_begin("spearman_walk", s);
-    kern<<<grid, STH, smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
-                                 a->d_tied, a->d_len, F, c0, c1, queue, pp);
-    ps_prof_end(s);
-    PS_LAUNCHED();
-    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((c1 - c0) * F, 8), (int64_t)ds->num_sms * 32);
-    spearman_partials_kernel<<<pblocks, 256, 0, s>>>(pp, F, c1, ps);
-    PS_LAUNCHED();
-  }
-  ps_free(pp.part, s);
-  ps_free(pp.meta, s);
-  }
-  const int64_t total = (hi - lo) * F;
-  const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
-  spearman_finish_kernel<<<blocks, 128, 0, s>>>(ps, F, lo, hi, stat, p, rho, ds->d_err);
-  PS_LAUNCHED();
-  ps_free(ps.n, s);
-  ps_free(ps.sxx4, s);
-  ps_free(ps.syy4, s);
-  ps_free(ps.sxy4, s);
-  ps_free(queue, s);
+  j->rows = std::max<int64_t>(1, std::min<int64_t>(hi - lo, ((int64_t)2 << 30) / per_row));
+  j->single = j->rows >= hi - lo;
+  if ((e = ps_alloc(&j->ps.n, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.sxx4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.syy4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.sxy4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->queues, (size_t)j->qn, s)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemsetAsync(j->queues, 0, sizeof(int) * j->qn, s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->pp.part, (size_t)(j->rows * F * kSlots * SW), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->pp.meta, (size_t)(j->rows * F), s)) != cudaSuccess) return fail(e);
+  // item tables: launches over disjoint column ranges of one chunk hold at
+  // most pairs / gb + F items; one item per column per chunk otherwise
+  const int64_t npairs = (hi - lo) * F, nchunks = ps_ceil_div(hi - lo, j->rows);
+  j->items_cap = nchunks * F + 64;
+  if (j->single || getenv("PS_SPEARMAN_GB")) j->items_cap += ps_ceil_div(npairs, j->gb) + F;
+  if ((e = ps_alloc(&j->items, (size_t)j->items_cap, s)) != cudaSuccess) return fail(e);
+  (void)rc;
+  *out = j;
   return PS_OK;
+}
+
+// Incremental launches alternate between two walk streams, so a launch can
+// fill the SMs while the previous one drains its last items; their work items
+// are g blocks of j->gb rows (columns of one upload chunk are too few to fill
+// the GPU one column per item).
+int ps_spearman_walk_upto(ps_spearman_job* j, int64_t h1, cudaStream_t s) {
+  if (!j->single) return PS_OK;
+  h1 = std::min<int64_t>(h1, j->a->F);
+  if (h1 <= j->h_done) return PS_OK;
+  ps_device_state* ds = ps_state();
+  const int k = j->nws++ & 1;
+  // one item per CTA (not persistent) while rows are still arriving: the
+  // per-chunk prep and presort kernels run on a higher-priority stream and
+  // take SMs as walk CTAs retire; the last launch is persistent
+  PS_CUDA(cudaEventRecord(ds->walk_ev[2], s));
+  PS_CUDA(cudaStreamWaitEvent(ds->walk[k], ds->walk_ev[2], 0));
+  int rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, ds->walk[k], j->grid_max, h1 < j->a->F);
+  j->h_done = h1;
+  return rc;
+}
+
+int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cudaStream_t s) {
+  int rc = PS_OK;
+  const int64_t F = j->a->F, lo = j->lo, hi = j->hi;
+  ps_device_state* ds = ps_state();
+  for (int k = 0; k < 2 && j->nws > k; ++k) {
+    PS_CUDA(cudaEventRecord(ds->walk_ev[k], ds->walk[k]));
+    PS_CUDA(cudaStreamWaitEvent(s, ds->walk_ev[k], 0));
+  }
+  // one item per column h (largest first) unless overridden: no per-item
+  // reload of h's tables, and the smallest columns form the tail
+  int64_t gb_full = F;
+  if (getenv("PS_SPEARMAN_GB")) gb_full = j->gb;
+  if (j->single) {
+    rc = walk_launch(j, j->h_done, F, lo, hi, j->nws ? j->gb : gb_full, s, j->grid_max);
+    if (!rc) rc = partials_launch(j, lo, hi, s);
+  } else {
+    for (int64_t c0 = lo; c0 < hi && !rc; c0 += j->rows) {
+      const int64_t c1 = std::min<int64_t>(hi, c0 + j->rows);
+      rc = walk_launch(j, c0, F, c0, c1, gb_full, s, j->grid_max);
+      if (!rc) rc = partials_launch(j, c0, c1, s);
+    }
+  }
+  if (!rc && hi > lo) {
+    ps_device_state* ds = ps_state();
+    const int64_t total = (hi - lo) * F;
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
+    spearman_finish_kernel<<<blocks, 128, 0, s>>>(j->ps, F, lo, hi, stat, p, rho, ds->d_err);
+    PS_LAUNCHED();
+  }
+  if (j->home != s) {  // free in the allocation stream's order (pool reuse across runs)
+    PS_CUDA(cudaEventRecord(ds->walk_ev[2], s));
+    PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[2], 0));
+  }
+  job_free(j, j->home);
+  return rc;
+}
+
+void ps_spearman_abort(ps_spearman_job* j, cudaStream_t s) {
+  if (!j) return;
+  cudaStreamSynchronize(s);
+  cudaDeviceSynchronize();
+  job_free(j, j->home);
+}
+
+int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
+                    cudaStream_t s) {
+  lo = std::max<int64_t>(0, lo);
+  hi = std::min<int64_t>(a->F, hi);
+  if (hi <= lo || (!stat && !p && !rho)) return PS_OK;
+  if (!a->has_presort) {
+    int rc = ps_presort_matrix(a, s);
+    if (rc) return rc;
+  }
+  ps_spearman_job* j = nullptr;
+  int rc = ps_spearman_begin(a, lo, hi, s, &j);
+  if (rc) return rc;
+  return ps_spearman_end(j, stat, p, rho, s);
 }
 
 #ifdef PS_WALK_TIMING

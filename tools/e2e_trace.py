@@ -18,7 +18,13 @@ if cfg.get("config") == 4 or sys.argv[1] == "4":
 mat_a = ps.make_matrix(a, ka, na_sentinel=workloads.SENTINEL)
 mat_b = ps.make_matrix(b, kb, na_sentinel=workloads.SENTINEL) if b is not None else None
 req = ps.TestRequest(test, outputs)
-for i in range(3):
+reps = int(os.environ.get("REPS", "3"))
+times = []
+for i in range(reps):
     t0 = time.perf_counter()
     ps.run(req, mat_a, mat_b)
-    print("run total %.3f ms" % ((time.perf_counter() - t0) * 1e3), file=sys.stderr, flush=True)
+    times.append((time.perf_counter() - t0) * 1e3)
+    print("run total %.3f ms" % times[-1], file=sys.stderr, flush=True)
+if reps > 3:
+    w = sorted(times[1:])
+    print("summary min %.3f median %.3f ms" % (w[0], w[len(w) // 2]), file=sys.stderr, flush=True)
