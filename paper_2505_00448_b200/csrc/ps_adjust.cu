@@ -259,6 +259,283 @@ __global__ void bonferroni_kernel(const uint64_t* __restrict__ keys, const uint3
 }
 
 // ---------------------------------------------------------------------------
+// Large families, fast path: a stable LSD radix over the HIGH 32 key bits only
+// (four 8-bit passes moving 4-byte high halves and 4-byte positions into the
+// compacted arrays), then runs of equal high halves are put in full-key order
+// by one thread per run (runs of up to kShortRun); a mixed run longer than
+// that raises a flag and the caller re-sorts on all 64 bits (the original
+// compacted arrays are untouched).  One host round trip in all.
+constexpr int kShortRun = 64;
+static_assert(kSortThreads == kBuckets, "one thread per digit");
+
+__device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* wsum /* [8] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  uint32_t base = 0;
+  for (int w = 0; w < warp; ++w) base += wsum[w];
+  return base + x - v;
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kSortThreads)
+h32_hist_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ dk,
+                const unsigned long long* __restrict__ count, int shift, uint32_t* __restrict__ tile_hist,
+                int64_t ntiles) {
+  __shared__ uint32_t h[kBuckets];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t m = (int64_t)*count, t0 = blockIdx.x * (int64_t)kTile;
+  for (int q = 0; q < kSortItems; ++q) {
+    const int64_t i = t0 + (int64_t)q * kSortThreads + threadIdx.x;
+    const bool ok = i < m;
+    uint32_t d = 0xffffffffu;
+    if (ok) d = ((FIRST ? (uint32_t)(keys[i] >> 32) : dk[i]) >> shift) & 0xffu;
+    const uint32_t peers = __match_any_sync(PS_FULL, d);
+    if (ok && (peers & lanemask_lt()) == 0) atomicAdd(&h[d], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  tile_hist[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Row d of the digit-major tile histogram -> exclusive offsets within digit d;
+// totals[d] = the digit's count.  One block per digit.
+__global__ void __launch_bounds__(kSortThreads)
+digit_scan_kernel(uint32_t* __restrict__ tile_hist, int64_t ntiles, uint32_t* __restrict__ totals) {
+  __shared__ uint32_t wsum[kSortThreads / 32];
+  uint32_t* row = tile_hist + (int64_t)blockIdx.x * ntiles;
+  const int64_t per = (ntiles + kSortThreads - 1) / kSortThreads;
+  const int64_t b = threadIdx.x * per, e = b + per < ntiles ? b + per : ntiles;
+  uint32_t sum = 0;
+  for (int64_t i = b; i < e; ++i) sum += row[i];
+  uint32_t run = block_excl_scan256(sum, wsum);
+  if (threadIdx.x == kSortThreads - 1) totals[blockIdx.x] = run + sum;
+  for (int64_t i = b; i < e; ++i) {
+    const uint32_t c = row[i];
+    row[i] = run;
+    run += c;
+  }
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(kSortThreads)
+h32_scatter_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ dk_in,
+                   const uint32_t* __restrict__ pos_in, uint32_t* __restrict__ dk_out, uint32_t* __restrict__ pos_out,
+                   const unsigned long long* __restrict__ count, int shift, const uint32_t* __restrict__ tile_off,
+                   const uint32_t* __restrict__ totals, int64_t ntiles) {
+  constexpr int NW = kSortThreads / 32;
+  constexpr int PER_WARP = kTile / NW;
+  __shared__ uint32_t wcnt[NW][kBuckets];
+  __shared__ uint32_t wsum[NW];
+  const int64_t m = (int64_t)*count;
+  if (blockIdx.x * (int64_t)kTile >= m) return;  // block-uniform
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NW * kBuckets; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  // digit base = exclusive scan of the digit totals + this tile's offset
+  const uint32_t dbase = block_excl_scan256(totals[threadIdx.x], wsum) +
+                         tile_off[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+  __syncthreads();
+  const int64_t w0 = blockIdx.x * (int64_t)kTile + (int64_t)warp * PER_WARP;
+  auto load = [&](int64_t i, uint32_t& k, uint32_t& v) {
+    if (FIRST) {
+      k = (uint32_t)(keys[i] >> 32);
+      v = (uint32_t)i;
+    } else {
+      k = dk_in[i];
+      v = pos_in[i];
+    }
+  };
+  for (int r = 0; r < PER_WARP; r += 32) {
+    const int64_t i = w0 + r + lane;
+    const bool ok = i < m;
+    uint32_t d = 0xffffffffu;
+    if (ok) {
+      uint32_t k, v;
+      load(i, k, v);
+      d = (k >> shift) & 0xffu;
+    }
+    const uint32_t peers = __match_any_sync(PS_FULL, d);
+    if (ok && (peers & lanemask_lt()) == 0) wcnt[warp][d] += __popc(peers);
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    uint32_t run = dbase;
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = wcnt[w][d];
+      wcnt[w][d] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < PER_WARP; r += 32) {
+    const int64_t i = w0 + r + lane;
+    const bool ok = i < m;
+    uint32_t k = 0, v = 0, d = 0xffffffffu;
+    if (ok) {
+      load(i, k, v);
+      d = (k >> shift) & 0xffu;
+    }
+    const uint32_t peers = __match_any_sync(PS_FULL, d);
+    const uint32_t rank = __popc(peers & lanemask_lt());
+    uint32_t start = 0;
+    if (ok) start = wcnt[warp][d];
+    __syncwarp();
+    if (ok) {
+      const uint32_t p = start + rank;
+      dk_out[p] = k;
+      pos_out[p] = v;
+      if ((peers >> lane) == 1u) wcnt[warp][d] = start + __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+// Runs of equal high halves.  Runs of <= kShortRun: the run's first thread
+// insertion-sorts its positions by the full key.  Runs of <= kBlockRun: queued
+// for a CTA-wide sort (long_run_sort_kernel).  Longer runs whose keys differ
+// set *flag (the caller re-sorts on all 64 bits).
+constexpr int kBlockRun = 16384;
+
+__device__ __forceinline__ int64_t run_end(const uint32_t* dk, int64_t i, int64_t m, uint32_t h) {
+  int64_t a = i, b = m;  // first index in [i, m) with dk > h (dk ascending)
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (dk[mid] <= h) a = mid + 1;
+    else b = mid;
+  }
+  return a;
+}
+__device__ __forceinline__ int64_t run_begin(const uint32_t* dk, int64_t i, uint32_t h) {
+  int64_t a = 0, b = i;  // first index in [0, i] with dk == h
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (dk[mid] < h) a = mid + 1;
+    else b = mid;
+  }
+  return a;
+}
+
+__global__ void h32_fixup_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ dk,
+                                 uint32_t* __restrict__ pos, const unsigned long long* __restrict__ count,
+                                 int* __restrict__ flag /* [0] fallback, [1] queued runs */,
+                                 int2* __restrict__ runs) {
+  const int64_t m = (int64_t)*count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = dk[i];
+    if (i > 0 && dk[i - 1] == h) {
+      // inside a run: a differing neighbour in a run too long for the CTA
+      // sort means the fallback (the reads may race with a short run's
+      // insertion sort, which cannot change the run's length)
+      if (keys[pos[i - 1]] != keys[pos[i]]) {
+        const int64_t L = run_end(dk, i, m, h) - run_begin(dk, i, h);
+        if (L > kBlockRun) atomicExch(&flag[0], 1);
+      }
+      continue;
+    }
+    if (i + 1 >= m || dk[i + 1] != h) continue;  // singleton
+    const int64_t e = run_end(dk, i, m, h), L = e - i;
+    if (L > kBlockRun) continue;
+    if (L > kShortRun) {
+      const int q = atomicAdd(&flag[1], 1);
+      runs[q] = make_int2((int)i, (int)L);
+      continue;
+    }
+    for (int64_t a = i + 1; a < e; ++a) {
+      const uint32_t pa = pos[a];
+      const uint64_t ka = keys[pa];
+      int64_t b = a - 1;
+      while (b >= i && keys[pos[b]] > ka) {
+        pos[b + 1] = pos[b];
+        --b;
+      }
+      pos[b + 1] = pa;
+    }
+  }
+}
+
+// One CTA per queued run: bitonic sort of (low half << 32 | position) in
+// shared memory (equal low halves are equal keys: their order is free).
+constexpr int kRunSortThreads = 1024;
+__global__ void __launch_bounds__(kRunSortThreads)
+long_run_sort_kernel(const uint64_t* __restrict__ keys, uint32_t* __restrict__ pos, const int* __restrict__ flag,
+                     const int2* __restrict__ runs) {
+  extern __shared__ unsigned long long lr[];
+  const int nruns = flag[1];
+  for (int r = blockIdx.x; r < nruns; r += gridDim.x) {
+    const int2 run = runs[r];
+    int n = 1;
+    while (n < run.y) n <<= 1;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      unsigned long long v = ~0ull;
+      if (t < run.y) {
+        const uint32_t p = pos[run.x + t];
+        v = ((keys[p] & 0xffffffffull) << 32) | p;
+      }
+      lr[t] = v;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n; k <<= 1) {
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+          const int o = t ^ jj;
+          if (o > t) {
+            const unsigned long long a = lr[t], b = lr[o];
+            const bool up = (t & k) == 0;
+            if ((a > b) == up) {
+              lr[t] = b;
+              lr[o] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int t = threadIdx.x; t < run.y; t += blockDim.x) pos[run.x + t] = (uint32_t)lr[t];
+    __syncthreads();
+  }
+}
+
+// ranked[i] = val(keys[pos[i]]) * fl(scale / (i+1)), block suffix minima
+__global__ void rank_scale_pos_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pos, int64_t m,
+                                      double scale, double* __restrict__ ranked, double* __restrict__ block_min) {
+  __shared__ double s[1024];
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  double v = CUDART_INF;
+  if (i < m) v = val_of(keys[pos[i]]) * (scale / (double)(i + 1));
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    double t = threadIdx.x + o < 1024 ? s[threadIdx.x + o] : CUDART_INF;
+    __syncthreads();
+    s[threadIdx.x] = fmin(s[threadIdx.x], t);
+    __syncthreads();
+  }
+  if (i < m) ranked[i] = s[threadIdx.x];
+  if (threadIdx.x == 0) block_min[blockIdx.x] = s[0];
+}
+__global__ void bh_scatter_pos_kernel(const double* __restrict__ ranked, const double* __restrict__ bm,
+                                      const uint32_t* __restrict__ pos, const uint32_t* __restrict__ idx, int64_t m,
+                                      int64_t cols, int symmetric, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * 1024LL + threadIdx.x;
+  if (i >= m) return;
+  double v = fmin(ranked[i], bm[blockIdx.x]);
+  v = fmin(1.0, v);
+  const int64_t f = idx[pos[i]];
+  out[f] = v;
+  if (symmetric) {
+    const int64_t r = f / cols, c = f - r * cols;
+    out[c * cols + r] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Small families (m <= kSmallMax): the whole BH / BY adjustment in one CTA --
 // stable LSD radix on the high 32 key bits in registers / shared memory (as
 // the presort), short runs of equal high halves repaired on the low halves
@@ -505,6 +782,93 @@ double numpy_pairwise_harmonic(int64_t m) {
   return Rec::sum(0, m);
 }
 
+// Fast large-family BH / BY (see h32_* above).  Families above kFastMax keep
+// the 64-bit sort (the high halves of more p-values collide too often).
+constexpr int64_t kFastMax = (int64_t)1 << 26;
+constexpr int kNeedFullSort = -12345;
+
+int adjust_fast(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int64_t cols, int symmetric,
+                int method, double* out, cudaStream_t s, int64_t fam_max) {
+  ps_device_state* ds = ps_state();
+  const int64_t ntiles = std::max<int64_t>(1, ps_ceil_div(fam_max, kTile));
+  uint32_t *dk[2] = {nullptr, nullptr}, *pos[2] = {nullptr, nullptr}, *tile_hist = nullptr, *totals = nullptr;
+  unsigned long long* host_pair = nullptr;  // {count, flag}
+  int* d_flag = nullptr;  // {fallback, queued runs}
+  int2* runs = nullptr;
+  PS_CUDA(ps_alloc(&dk[0], (size_t)fam_max, s));
+  PS_CUDA(ps_alloc(&dk[1], (size_t)fam_max, s));
+  PS_CUDA(ps_alloc(&pos[0], (size_t)fam_max, s));
+  PS_CUDA(ps_alloc(&pos[1], (size_t)fam_max, s));
+  PS_CUDA(ps_alloc(&tile_hist, (size_t)(ntiles * kBuckets), s));
+  PS_CUDA(ps_alloc(&totals, (size_t)kBuckets, s));
+  PS_CUDA(ps_alloc(&d_flag, 2, s));
+  PS_CUDA(cudaMemsetAsync(d_flag, 0, 2 * sizeof(int), s));
+  PS_CUDA(ps_alloc(&runs, (size_t)(fam_max / (kShortRun + 1) + 1), s));
+  int cur = 0;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    if (pass == 0) h32_hist_kernel<true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, nullptr, d_count, shift, tile_hist, ntiles);
+    else h32_hist_kernel<false><<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, dk[cur], d_count, shift, tile_hist, ntiles);
+    PS_LAUNCHED();
+    digit_scan_kernel<<<kBuckets, kSortThreads, 0, s>>>(tile_hist, ntiles, totals);
+    PS_LAUNCHED();
+    if (pass == 0)
+      h32_scatter_kernel<true><<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, nullptr, nullptr, dk[cur ^ 1], pos[cur ^ 1],
+                                                                        d_count, shift, tile_hist, totals, ntiles);
+    else
+      h32_scatter_kernel<false><<<(unsigned)ntiles, kSortThreads, 0, s>>>(keys, dk[cur], pos[cur], dk[cur ^ 1],
+                                                                         pos[cur ^ 1], d_count, shift, tile_hist,
+                                                                         totals, ntiles);
+    PS_LAUNCHED();
+    cur ^= 1;
+  }
+  {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(fam_max, 256), (int64_t)ds->num_sms * 8));
+    h32_fixup_kernel<<<blocks, 256, 0, s>>>(keys, dk[cur], pos[cur], d_count, d_flag, runs);
+    PS_LAUNCHED();
+    const size_t smem = (size_t)kBlockRun * sizeof(unsigned long long);
+    PS_CUDA(cudaFuncSetAttribute(long_run_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    long_run_sort_kernel<<<ds->num_sms, kRunSortThreads, smem, s>>>(keys, pos[cur], d_flag, runs);
+    PS_LAUNCHED();
+  }
+  unsigned long long hp[2] = {0, 0};
+  PS_CUDA(cudaMemcpyAsync(&hp[0], d_count, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  int flag_h = 0;
+  PS_CUDA(cudaMemcpyAsync(&flag_h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  (void)host_pair;
+  const int64_t m = (int64_t)hp[0];
+  int rc = PS_OK;
+  if (flag_h) {
+    rc = kNeedFullSort;
+  } else if (m > 0) {
+    double scale = (double)m;
+    if (method == PS_ADJ_BY) scale *= numpy_pairwise_harmonic(m);
+    const int64_t nb = ps_ceil_div(m, 1024);
+    double* ranked = nullptr;
+    double* bm = nullptr;
+    PS_CUDA(ps_alloc(&ranked, (size_t)m, s));
+    PS_CUDA(ps_alloc(&bm, (size_t)nb, s));
+    rank_scale_pos_kernel<<<(unsigned)nb, 1024, 0, s>>>(keys, pos[cur], m, scale, ranked, bm);
+    PS_LAUNCHED();
+    block_suffix_min_kernel<<<1, 32, 0, s>>>(bm, nb);
+    PS_LAUNCHED();
+    bh_scatter_pos_kernel<<<(unsigned)nb, 1024, 0, s>>>(ranked, bm, pos[cur], idx, m, cols, symmetric, out);
+    PS_LAUNCHED();
+    ps_free(ranked, s);
+    ps_free(bm, s);
+  }
+  for (int k = 0; k < 2; ++k) {
+    ps_free(dk[k], s);
+    ps_free(pos[k], s);
+  }
+  ps_free(tile_hist, s);
+  ps_free(totals, s);
+  ps_free(d_flag, s);
+  ps_free(runs, s);
+  return rc;
+}
+
 int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int64_t cols,
                 int symmetric, int method, double* out, cudaStream_t s, int64_t fam_max) {
   ps_device_state* ds = ps_state();
@@ -520,6 +884,10 @@ int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     adjust_small_kernel<<<1, kSmallThreads, smem, s>>>(keys, idx, d_count, 1.0, cols, symmetric, out);
     PS_LAUNCHED();
     return PS_OK;
+  }
+  if (fam_max <= kFastMax && !getenv("PS_ADJUST_FULLSORT")) {
+    int rc = adjust_fast(keys, idx, d_count, cols, symmetric, method, out, s, fam_max);
+    if (rc != kNeedFullSort) return rc;
   }
   unsigned long long m_host = 0;
   PS_CUDA(cudaMemcpyAsync(&m_host, d_count, sizeof(m_host), cudaMemcpyDeviceToHost, s));

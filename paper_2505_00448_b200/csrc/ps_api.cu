@@ -610,6 +610,13 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     }
   }
   if (sjob) ps_spearman_abort(sjob, s);  // not consumed (an earlier failure)
+  // while the device computes: fault in the host output pages
+  if (!rc && !getenv("PS_NO_PREFAULT")) {
+    for (int k = 0; k < 4; ++k)
+      if (outs && outs[k]) ps_host_prefault(outs[k], sizeof(double) * cells);
+    for (int k = 0; k < 3; ++k)
+      if (adj_outs && adj_outs[k]) ps_host_prefault(adj_outs[k], sizeof(double) * cells);
+  }
   if (!rc) rc = drain_errors(s);
   g_tl.mark("compute done", s);
   tr.mark("compute");
@@ -637,8 +644,17 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
       });
     }
   }
-  for (int k = 0; k < 4 && !rc; ++k)
-    if (outs && outs[k] && d_out[k]) rc = ps_stage_d2h(outs[k], d_out[k], sizeof(double) * cells, s);
+  if (!rc && outs) {
+    void* hd[4];
+    const void* ds_[4];
+    size_t nb[4];
+    for (int k = 0; k < 4; ++k) {
+      hd[k] = outs[k];
+      ds_[k] = d_out[k];
+      nb[k] = outs[k] && d_out[k] ? sizeof(double) * cells : 0;
+    }
+    rc = ps_stage_d2h_many(4, hd, ds_, nb, s);
+  }
   tr.mark("d2h");
   if (adj_thread.joinable()) adj_thread.join();
   if (!rc) rc = rc_adj;
@@ -646,8 +662,17 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     cudaError_t e = cudaEventRecord(st->aux_ev, st->aux);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, st->aux_ev, 0);
     if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust join");
-    for (int k = 0; k < 3 && !rc; ++k)
-      if (adj_outs[k]) rc = ps_stage_d2h(adj_outs[k], d_adjk[k], sizeof(double) * cells, s);
+    if (!rc) {
+      void* hd[3];
+      const void* ds_[3];
+      size_t nb[3];
+      for (int k = 0; k < 3; ++k) {
+        hd[k] = adj_outs[k];
+        ds_[k] = d_adjk[k];
+        nb[k] = adj_outs[k] && d_adjk[k] ? sizeof(double) * cells : 0;
+      }
+      rc = ps_stage_d2h_many(3, hd, ds_, nb, s);
+    }
   }
   tr.mark("adjust");
   if (!rc) {

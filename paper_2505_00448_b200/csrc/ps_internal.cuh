@@ -133,4 +133,6 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
                         cudaStream_t s);
 int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld, cudaStream_t s);
 int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void ps_host_prefault(void* dst, size_t bytes);
+int ps_stage_d2h_many(int n, void* const* dst, const void* const* src, const size_t* bytes, cudaStream_t s);
 int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s);

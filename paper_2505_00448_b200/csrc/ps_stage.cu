@@ -12,6 +12,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <cmath>
+#include <vector>
 
 namespace {
 
@@ -49,7 +50,7 @@ int ring_for_device(Ring** out) {
 }
 
 void par_copy(void* dst, const void* src, size_t bytes) {
-  const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(bytes >> 20)));
+  const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(bytes >> 18)));
 #pragma omp parallel for num_threads(nt) schedule(static)
   for (int t = 0; t < nt; ++t) {
     const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
@@ -99,9 +100,16 @@ int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, si
     return PS_OK;
   }
   const size_t rows_per = std::max<size_t>(1, kChunk / dpitch);
-  int b = 0;
-  for (size_t r0 = 0; r0 < rows; r0 += rows_per, b ^= 1) {
-    const size_t nr = std::min(rows_per, rows - r0);
+  // with a per-chunk consumer, the first chunks are smaller so that device
+  // work on the first rows starts sooner (graduated 1/4, 1/4, 1/2, 1, 1 ...)
+  auto chunk_rows = [&](int k) -> size_t {
+    static const bool flat = getenv("PS_STAGE_FLAT") != nullptr;  // A/B switch
+    if (!on_rows || k >= 3 || flat) return rows_per;
+    return std::max<size_t>(1, rows_per / (k < 2 ? 4 : 2));
+  };
+  int b = 0, k = 0;
+  for (size_t r0 = 0, nr = 0; r0 < rows; r0 += nr, b ^= 1, ++k) {
+    nr = std::min(chunk_rows(k), rows - r0);
     PS_CUDA(cudaEventSynchronize(r->ev[b]));  // the DMA that last read this buffer is done
     char* pb = static_cast<char*>(r->buf[b]);
     const char* sp = static_cast<const char*>(src) + r0 * spitch;
@@ -158,30 +166,66 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
 }
 
 // contiguous device -> host copy; returns after dst is complete
+// Touch every page of a host output buffer (one write per 4 KiB page, all
+// cores) so that first-touch page faults are taken while the device computes,
+// not inside the device-to-host copy.  The buffer is about to be overwritten.
+void ps_host_prefault(void* dst, size_t bytes) {
+  if (!dst || bytes == 0) return;
+  char* p = static_cast<char*>(dst);
+  const size_t page = 4096;
+  const long long n = (long long)((bytes + page - 1) / page);
+  const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(n / 256)));
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (long long i = 0; i < n; ++i) static_cast<volatile char*>(p)[(size_t)i * page] = 0;
+}
+
 int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  if (bytes < kDirect) {
-    PS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  void* d[1] = {dst};
+  const void* sp[1] = {src};
+  size_t b[1] = {bytes};
+  return ps_stage_d2h_many(1, d, sp, b, s);
+}
+
+// Several device buffers to host memory as one pipeline of sub-chunks: the
+// DMA of chunk i + 1 overlaps the host copy of chunk i, across buffers.
+int ps_stage_d2h_many(int n, void* const* dst, const void* const* src, const size_t* bytes, cudaStream_t s) {
+  struct Piece {
+    char* d;
+    const char* s;
+    size_t len;
+  };
+  std::vector<Piece> pieces;
+  for (int k = 0; k < n; ++k) {
+    if (!dst[k] || !src[k] || !bytes[k]) continue;
+    if (bytes[k] < kDirect) {
+      PS_CUDA(cudaMemcpyAsync(dst[k], src[k], bytes[k], cudaMemcpyDeviceToHost, s));
+      continue;
+    }
+    const size_t piece = std::min(kChunk, std::max<size_t>(2u << 20, bytes[k] / 4));
+    for (size_t off = 0; off < bytes[k]; off += piece)
+      pieces.push_back({static_cast<char*>(dst[k]) + off, static_cast<const char*>(src[k]) + off,
+                        std::min(piece, bytes[k] - off)});
+  }
+  if (pieces.empty()) {
     PS_CUDA(cudaStreamSynchronize(s));
     return PS_OK;
   }
   Ring* r = nullptr;
   int rc = ring_for_device(&r);
   if (rc) return rc;
-  const size_t n = (bytes + kChunk - 1) / kChunk;
   auto issue = [&](size_t i) -> int {
-    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    PS_CUDA(cudaMemcpyAsync(r->buf[i & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaMemcpyAsync(r->buf[i & 1], pieces[i].s, pieces[i].len, cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaEventRecord(r->ev[i & 1], s));
     return PS_OK;
   };
   rc = issue(0);
-  for (size_t i = 0; i < n && !rc; ++i) {
-    if (i + 1 < n) rc = issue(i + 1);  // next chunk's DMA overlaps this chunk's host copy
+  for (size_t i = 0; i < pieces.size() && !rc; ++i) {
+    if (i + 1 < pieces.size()) rc = issue(i + 1);  // next piece's DMA overlaps this piece's host copy
     if (rc) break;
     PS_CUDA(cudaEventSynchronize(r->ev[i & 1]));
-    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    par_copy(static_cast<char*>(dst) + off, r->buf[i & 1], len);
-    // the buffer is reused by chunk i + 2, issued after this copy returns
+    par_copy(pieces[i].d, r->buf[i & 1], pieces[i].len);
+    // the buffer is reused by piece i + 2, issued after this copy returns
   }
+  if (!rc) PS_CUDA(cudaStreamSynchronize(s));  // the direct (small) copies
   return rc;
 }

@@ -18,7 +18,7 @@ import paper_2505_00448_b200 as ps
 @pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
 def test_adjust_vector_families(oracle, method):
     rng = np.random.default_rng(55)
-    for size in [1, 2, 3, 7, 100, 1000, 4097, 20000, 200001]:
+    for size in [1, 2, 3, 7, 100, 1000, 4097, 20000, 24577, 200001, 1000003]:
         v = rng.random(size)
         ties = rng.random(size) < 0.3
         v[ties] = np.round(v[ties], 1)
@@ -40,6 +40,39 @@ def test_adjust_low_bit_collisions(oracle, method):
         for x in (v, w):
             got = ps.adjust(x.reshape(1, -1), method, symmetric=False).ravel()
             assert bitwise_equal(got, oracle.adjust_family(x, method)), (method, size)
+
+
+@pytest.mark.parametrize("method", ["bh", "by"])
+def test_adjust_large_family_runs(oracle, method):
+    """Families above the single-CTA size take the high-half radix with
+    run repair: short colliding runs are repaired in place, long runs of
+    differing keys fall back to the 64-bit sort, long runs of one value need
+    neither."""
+    rng = np.random.default_rng(11)
+    size = 150001
+    cases = []
+    w = rng.random(size)
+    w[::3] = 0.25 + rng.integers(0, 5, w[::3].size) * 2.0**-50       # short runs
+    cases.append(w)
+    v = rng.random(size)
+    v[: size // 2] = 0.5 + rng.integers(0, 1000, size // 2) * 2.0**-45  # long mixed runs
+    cases.append(v)
+    u = rng.random(size)
+    u[rng.random(size) < 0.4] = 1.0                                    # one long run of 1.0
+    u[rng.random(size) < 0.05] = np.nan
+    cases.append(u)
+    t = rng.random(size) ** 8                                          # many binades
+    cases.append(t)
+    z = rng.random(size)
+    z[:9000] = rng.integers(0, 900, 9000) * 2.0**-1074                  # a long run of subnormals
+    z[9000:12000] = 0.0
+    cases.append(z)
+    y = rng.random(size)
+    y[:40000] = rng.integers(0, 300, 40000) * 2.0**-1074                # too long for the CTA sort
+    cases.append(y)
+    for x in cases:
+        got = ps.adjust(x.reshape(1, -1), method, symmetric=False).ravel()
+        assert bitwise_equal(got, oracle.adjust_family(x, method)), method
 
 
 @pytest.mark.parametrize("method", ["bonferroni", "bh", "by"])
