@@ -47,8 +47,8 @@ int init_state(ps_device_state* st, int dev) {
   // aux carries the per-chunk prep / presort that incremental walks wait on
   PS_CUDA(cudaStreamCreateWithPriority(&st->aux, cudaStreamNonBlocking, prio_hi));
   PS_CUDA(cudaEventCreateWithFlags(&st->aux_ev, cudaEventDisableTiming));
-  for (int k = 0; k < 2; ++k) PS_CUDA(cudaStreamCreateWithFlags(&st->walk[k], cudaStreamNonBlocking));
-  for (int k = 0; k < 3; ++k) PS_CUDA(cudaEventCreateWithFlags(&st->walk_ev[k], cudaEventDisableTiming));
+  for (auto& w : st->walk) PS_CUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
+  for (auto& e : st->walk_ev) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // keep freed workspace cached in the stream-ordered pool between calls
   cudaMemPool_t pool;
   PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -226,6 +226,30 @@ int ps_device_count(int* count) {
   *count = n;
   return PS_OK;
 }
+
+}  // extern "C"
+
+cudaStream_t ps_walk_stream(int k, cudaStream_t after) {
+  ps_device_state* st = ps_state();
+  constexpr int K = ps_device_state::kWalkStreams;
+  cudaStream_t w = st->walk[k % K];
+  cudaEventRecord(st->walk_ev[K], after);
+  cudaStreamWaitEvent(w, st->walk_ev[K], 0);
+  if (g_tl.on) g_tl.mark("  walk launch " + std::to_string(k), after);
+  return w;
+}
+
+int ps_walk_streams_join(int used, cudaStream_t s) {
+  ps_device_state* st = ps_state();
+  for (int k = 0; k < ps_device_state::kWalkStreams && k < used; ++k) {
+    PS_CUDA(cudaEventRecord(st->walk_ev[k], st->walk[k]));
+    PS_CUDA(cudaStreamWaitEvent(s, st->walk_ev[k], 0));
+    if (g_tl.on) g_tl.mark("  walk stream " + std::to_string(k) + " done", st->walk[k]);
+  }
+  return PS_OK;
+}
+
+extern "C" {
 
 int ps_set_device(int device) {
   Guard g;
@@ -557,18 +581,27 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
       int c = ps_spearman_begin(m, 0, m->F, aux, &sjob);
       if (c) return c;
     }
-    int c = ps_spearman_walk_upto(sjob, r1, aux);
-    g_tl.mark("  walk launched " + std::to_string(r1), st->walk[0]);
-    g_tl.mark("  walk launched " + std::to_string(r1) + "'", st->walk[1]);
-    return c;
+    return ps_spearman_walk_upto(sjob, r1, aux);
   };
   g_tl.mark("start", s);
   const bool overlap = test == PS_TEST_SPEARMAN && any_out && !getenv("PS_NO_OVERLAP");
   rc = matrix_create(a, 0, presort_a, s, &ma, overlap ? &walk_hook : nullptr);
-  if (!rc && !homogeneous) rc = matrix_create(b, 0, presort_b, s, &mb, nullptr);
+  // Mann-Whitney / Kruskal-Wallis: likewise, per uploaded chunk of features
+  ps_rank_job* rjob = nullptr;
+  RowsHook rank_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
+    if (!rjob) {
+      int c = ps_rank_mixed_begin(test, ma, m, 0, m->F, test == PS_TEST_MWU ? u_mode : 0, aux, &rjob);
+      if (c) return c;
+    }
+    return ps_rank_mixed_walk_upto(rjob, r1, aux);
+  };
+  const bool overlap_rank = (test == PS_TEST_MWU || test == PS_TEST_KRUSKAL) && any_out && !getenv("PS_NO_OVERLAP");
+  if (!rc && !homogeneous) rc = matrix_create(b, 0, presort_b, s, &mb, overlap_rank ? &rank_hook : nullptr);
   if (rc) {
     ps_spearman_abort(sjob, s);
+    ps_rank_mixed_abort(rjob, s);
     ps_matrix_destroy(ma);
+    ps_matrix_destroy(mb);
     return rc;
   }
   tr.mark("matrices");
@@ -601,15 +634,20 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
         rc = ps_group_moment_run(PS_TEST_ANOVA, ma, mb, 0, cells, 1, d_out[0], d_out[1], d_out[2], s);
         break;
       case PS_TEST_MWU:
-        rc = ps_rank_mixed_run(PS_TEST_MWU, ma, mb, 0, cols, u_mode, d_out[0], d_out[1], d_out[2], s);
-        break;
       case PS_TEST_KRUSKAL:
-        rc = ps_rank_mixed_run(PS_TEST_KRUSKAL, ma, mb, 0, cols, 0, d_out[0], d_out[1], d_out[2], s);
+        if (rjob) {
+          rc = ps_rank_mixed_end(rjob, d_out[0], d_out[1], d_out[2], s);
+          rjob = nullptr;
+        } else {
+          rc = ps_rank_mixed_run(test, ma, mb, 0, cols, test == PS_TEST_MWU ? u_mode : 0, d_out[0], d_out[1],
+                                 d_out[2], s);
+        }
         break;
       default: rc = ps_fail(PS_ERR_INVALID, "unknown test");
     }
   }
   if (sjob) ps_spearman_abort(sjob, s);  // not consumed (an earlier failure)
+  if (rjob) ps_rank_mixed_abort(rjob, s);
   // while the device computes: fault in the host output pages
   if (!rc && !getenv("PS_NO_PREFAULT")) {
     for (int k = 0; k < 4; ++k)

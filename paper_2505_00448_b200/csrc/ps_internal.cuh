@@ -54,8 +54,9 @@ struct ps_device_state {
   cudaStream_t stream = nullptr;  // library stream used by ps_run
   cudaStream_t aux = nullptr;     // second stream: per-chunk prep / presort during uploads
   cudaEvent_t aux_ev = nullptr;
-  cudaStream_t walk[2] = {nullptr, nullptr};  // incremental rank walks during uploads
-  cudaEvent_t walk_ev[3] = {nullptr, nullptr, nullptr};
+  static constexpr int kWalkStreams = 4;
+  cudaStream_t walk[kWalkStreams] = {};  // incremental rank walks during uploads
+  cudaEvent_t walk_ev[kWalkStreams + 1] = {};
 };
 
 ps_device_state* ps_state();                 // current device's state
@@ -105,6 +106,17 @@ int ps_presort_end(ps_matrix* m, cudaStream_t s);
 int ps_fill_nan(double* p, int64_t n, cudaStream_t s);
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s);
+// Walk streams for incremental launches: launch k goes to stream k mod
+// kWalkStreams after it waits on `after`; join makes `s` wait on every used one.
+cudaStream_t ps_walk_stream(int k, cudaStream_t after);
+int ps_walk_streams_join(int used, cudaStream_t s);
+struct ps_rank_job;
+// Incremental Mann-Whitney / Kruskal-Wallis walks (as the Spearman job).
+int ps_rank_mixed_begin(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode, cudaStream_t s,
+                        ps_rank_job** job);
+int ps_rank_mixed_walk_upto(ps_rank_job* job, int64_t h1, cudaStream_t s);
+int ps_rank_mixed_end(ps_rank_job* job, double* stat, double* p, double* eff, cudaStream_t s);
+void ps_rank_mixed_abort(ps_rank_job* job, cudaStream_t s);
 struct ps_spearman_job;
 // Incremental Spearman walk (ps_run overlaps it with the input upload):
 // begin allocates, walk_upto walks the columns h < h1 whose rows are

@@ -99,7 +99,7 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
                        const uint16_t* __restrict__ lastb, const uint16_t* __restrict__ nextb, int64_t ldt,
                        const uint8_t* __restrict__ tied, const int32_t* __restrict__ lens,
                        const uint8_t* __restrict__ codes, int64_t ldc, const int32_t* __restrict__ cat,
-                       int64_t Fc, int64_t Fq, int64_t lo, int64_t hi, int check_labels,
+                       int64_t Fc, int64_t Fq, int64_t lo, int64_t hi, int gb, int once, int check_labels,
                        int* __restrict__ queue, RankSums out, int* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* cur = smem;
@@ -151,14 +151,17 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
 
   if constexpr (SMACC)
     for (int i = threadIdx.x; i < RW * KM * 32; i += RTH) accs[i] = 0u;
-  const int64_t items = hi - lo;
+  // items: (feature h, block of gb label rows), h-major
+  const int64_t nblk = (Fc + gb - 1) / gb;
+  const int64_t items = (hi - lo) * nblk;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
     __syncthreads();
     const int item = s_item;
     if (item >= items) break;
-    const int64_t h = lo + item;
+    const int64_t h = lo + item / nblk;
+    const int64_t g0 = (item % nblk) * gb, g1 = g0 + gb < Fc ? g0 + gb : Fc;
     const int nh = lens[h];
     const bool th = tied[h] != 0;
     {
@@ -173,11 +176,11 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
         }
       }
     }
-    prefetch(0, 0);
+    prefetch(g0, 0);
     const int nw = (nh + 31) >> 5;
-    for (int64_t g = 0; g < Fc; ++g) {
-      const int buf = (int)(g & 1);
-      if (g + 1 < Fc) prefetch(g + 1, buf ^ 1);
+    for (int64_t g = g0; g < g1; ++g) {
+      const int buf = (int)((g - g0) & 1);
+      if (g + 1 < g1) prefetch(g + 1, buf ^ 1);
       else asm volatile("cp.async.commit_group;");
       asm volatile("cp.async.wait_group 1;");
       __syncthreads();
@@ -361,6 +364,7 @@ rank_mixed_walk_kernel(const uint16_t* __restrict__ order, int64_t ldo, const ui
       }
     }
     asm volatile("cp.async.wait_group 0;");
+    if (once) break;  // one item per CTA: retiring CTAs let higher-priority kernels in
   }
 }
 
@@ -527,8 +531,8 @@ size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc, int KM) {
 }
 
 template <int KM>
-int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo, int64_t hi, int check,
-                int* queue, RankSums rs, cudaStream_t s) {
+int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo, int64_t hi, int gb, int once,
+                int check, int* queue, RankSums rs, cudaStream_t s) {
   ps_device_state* ds = ps_state();
   const size_t smem = walk_smem(val->ldo, val->ldt, lab->ldc, KM);
   auto kern = rank_mixed_walk_kernel<KM>;
@@ -540,11 +544,12 @@ int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo
   int per_sm = 0;
   PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RTH, smem));
   per_sm = std::max(1, per_sm);
-  const int grid = (int)std::min<int64_t>(hi - lo, (int64_t)ds->num_sms * per_sm);
+  const int64_t items = (hi - lo) * ps_ceil_div(lab->F, gb);
+  const int grid = once ? (int)items : (int)std::min<int64_t>(items, (int64_t)ds->num_sms * per_sm);
   ps_prof_begin("rank_mixed_walk", s);
   kern<<<grid, RTH, smem, s>>>(val->d_order, val->ldo, val->d_tb, val->d_lastb, val->d_nextb, val->ldt,
                                val->d_tied, val->d_len, codes, lab->ldc, lab->d_cat, lab->F, val->F, lo, hi,
-                               check, queue, rs, ds->d_err);
+                               gb, once, check, queue, rs, ds->d_err);
   ps_prof_end(s);
   PS_LAUNCHED();
   return PS_OK;
@@ -552,73 +557,170 @@ int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo
 
 }  // namespace
 
-int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode,
-                      double* stat, double* p, double* eff, cudaStream_t s) {
+constexpr int kIncrementalRows = 32;
+
+struct ps_rank_job {
+  int test = 0, u_mode = 0, KM = 2;
+  bool kw = false;
+  ps_matrix* lab = nullptr;
+  ps_matrix* val = nullptr;
+  int64_t lo = 0, hi = 0, h_done = 0;
+  RankSums rs{2, nullptr, nullptr, nullptr};
+  uint8_t* bcodes = nullptr;
+  const uint8_t* codes = nullptr;
+  int* queues = nullptr;
+  int qn = 256, qi = 0, nws = 0;
+  int2* exl = nullptr;
+  int* exc = nullptr;
+  int excap = 0;
+  cudaStream_t home = nullptr;
+};
+
+static void rank_job_free(ps_rank_job* j, cudaStream_t s) {
+  ps_free(j->rs.cnt, s);
+  ps_free(j->rs.r2, s);
+  ps_free(j->rs.tie, s);
+  ps_free(j->queues, s);
+  ps_free(j->exl, s);
+  ps_free(j->exc, s);
+  ps_free(j->bcodes, s);
+  delete j;
+}
+
+// label check + walk of the continuous features [h0, h1); work items are
+// (feature, gb label rows)
+static int rank_walk_range(ps_rank_job* j, int64_t h0, int64_t h1, int gb, int once, cudaStream_t s) {
+  if (h1 <= h0) return PS_OK;
+  if (j->qi >= j->qn) {
+    PS_CUDA(cudaMemsetAsync(j->queues, 0, sizeof(int) * j->qn, s));
+    j->qi = 0;
+  }
+  int* q = j->queues + j->qi++;
+  // LabelOutOfRange: a present out-of-range label meeting a present value
+  // (mixed.py:613-617) -- checked up front, so the walk never tracks it
+  int rc = j->kw ? ps_mixed_label_check(j->lab, j->val, 0, j->lab->F, h0, h1, s) : PS_OK;
+  if (rc) return rc;
+  const int KM = j->KM;
+  if (KM == 2) return launch_walk<2>(j->lab, j->val, j->codes, h0, h1, gb, once, j->kw, q, j->rs, s);
+  if (KM == 8) return launch_walk<8>(j->lab, j->val, j->codes, h0, h1, gb, once, j->kw, q, j->rs, s);
+  if (KM == 16) return launch_walk<16>(j->lab, j->val, j->codes, h0, h1, gb, once, j->kw, q, j->rs, s);
+  return launch_walk<256>(j->lab, j->val, j->codes, h0, h1, gb, once, j->kw, q, j->rs, s);
+}
+
+int ps_rank_mixed_begin(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode, cudaStream_t s,
+                        ps_rank_job** out) {
+  *out = nullptr;
   const int64_t Fc = lab->F, Fq = val->F;
   if (lab->S != val->S) return ps_fail(PS_ERR_INVALID, "sample counts differ");
+  ps_rank_job* j = new ps_rank_job();
+  j->test = test;
+  j->u_mode = u_mode;
+  j->lab = lab;
+  j->val = val;
+  j->lo = std::max<int64_t>(0, lo);
+  j->hi = std::min<int64_t>(Fq, hi);
+  j->h_done = j->lo;
+  j->home = s;
+  j->kw = test == PS_TEST_KRUSKAL;
+  const int kmax = j->kw ? std::max(1, lab->cmax) : 2;
+  int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 256;
+  // the KM = 8 variant keeps per-lane accumulators in shared memory; when they
+  // do not fit next to the walk's tables, use the register variant
+  if (KM == 8 && walk_smem(val->ldo, val->ldt, lab->ldc, 8) > 222 * 1024) KM = 16;
+  j->KM = KM;
+  const int64_t npairs = Fc * Fq;
+  // per-pair level stride: the template width, or the real level count for k > 16
+  j->rs = RankSums{KM > 16 ? (kmax + 31) / 32 * 32 : KM, nullptr, nullptr, nullptr};
+  j->excap = (int)std::min<int64_t>(Fc * std::max<int64_t>(1, j->hi - j->lo), 1 << 20);
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) { e = x; return x == cudaSuccess; };
+  if (ok(ps_alloc(&j->rs.cnt, (size_t)(npairs * j->rs.KM), s)) && ok(ps_alloc(&j->rs.r2, (size_t)(npairs * j->rs.KM), s)) &&
+      ok(ps_alloc(&j->rs.tie, (size_t)npairs, s)) && ok(ps_alloc(&j->queues, (size_t)j->qn, s)) &&
+      ok(ps_alloc(&j->exl, (size_t)j->excap, s)) && ok(ps_alloc(&j->exc, 1, s)) &&
+      ok(cudaMemsetAsync(j->queues, 0, sizeof(int) * j->qn, s)) && ok(cudaMemsetAsync(j->exc, 0, sizeof(int), s)) &&
+      ok(cudaMemsetAsync(j->rs.cnt, 0, sizeof(int32_t) * npairs * j->rs.KM, s)) &&
+      ok(cudaMemsetAsync(j->rs.r2, 0, sizeof(unsigned long long) * npairs * j->rs.KM, s))) {
+    j->codes = lab->d_codes;
+    if (!j->kw && ok(ps_alloc(&j->bcodes, (size_t)(Fc * lab->ldc), s))) {
+      binary_codes_kernel<<<(unsigned)Fc, 256, 0, s>>>(lab->d_mask, lab->d_zero, lab->W, lab->S, lab->ldc, j->bcodes);
+      e = cudaGetLastError();
+      ps_count_launch();
+      j->codes = j->bcodes;
+    }
+  }
+  if (e != cudaSuccess) {
+    rank_job_free(j, s);
+    return ps_cuda_check(e, "rank test setup");
+  }
+  *out = j;
+  return PS_OK;
+}
+
+// Incremental walks (ps_run: features of each uploaded chunk), alternating
+// between the two walk streams; each item is one feature, so a launch's CTAs
+// retire one by one and the next chunk's presort (higher-priority stream)
+// and walk fill the SMs.
+int ps_rank_mixed_walk_upto(ps_rank_job* j, int64_t h1, cudaStream_t s) {
+  h1 = std::min<int64_t>(h1, j->hi);
+  if (h1 <= j->h_done) return PS_OK;
+  ps_device_state* ds = ps_state();
+  cudaStream_t w = ps_walk_stream(j->nws++, s);
+  // label-row blocks keep items short, so SMs free up often for the
+  // presort of the next chunk
+  int gb = kIncrementalRows;
+  if (const char* e = getenv("PS_RANK_GB")) gb = std::max(1, atoi(e));
+  int rc = rank_walk_range(j, j->h_done, h1, gb, h1 < j->hi, w);
+  j->h_done = h1;
+  return rc;
+}
+
+int ps_rank_mixed_end(ps_rank_job* j, double* stat, double* p, double* eff, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  int jr = ps_walk_streams_join(j->nws, s);
+  if (jr) return jr;
+  int rc = rank_walk_range(j, j->h_done, j->hi, (int)std::max<int64_t>(1, j->lab->F), 0, s);
+  j->h_done = j->hi;
+  const int64_t Fc = j->lab->F, Fq = j->val->F, lo = j->lo, hi = j->hi;
+  if (!rc && hi > lo && (stat || p || eff)) {
+    const int64_t total = Fc * (hi - lo);
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
+    rank_mixed_finish_kernel<<<blocks, 128, 0, s>>>(j->test, j->rs, j->lab->d_cat, Fc, Fq, lo, hi, j->u_mode, stat, p,
+                                                    eff, j->exl, j->exc, j->excap, ds->d_err);
+    ps_count_launch();
+    if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "rank finish launch");
+    if (!rc && !j->kw && j->u_mode != PS_U_ASYMPTOTIC && p) {
+      mwu_exact_kernel<<<ds->num_sms, 32, 0, s>>>(j->rs, Fq, j->exl, j->exc, j->excap, p);
+      ps_count_launch();
+      if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "mwu exact launch");
+    }
+  }
+  if (j->home != s) {  // free in the allocation stream's order
+    PS_CUDA(cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s));
+    PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0));
+  }
+  rank_job_free(j, j->home);
+  return rc;
+}
+
+void ps_rank_mixed_abort(ps_rank_job* j, cudaStream_t s) {
+  if (!j) return;
+  cudaStreamSynchronize(s);
+  cudaDeviceSynchronize();
+  rank_job_free(j, j->home);
+}
+
+int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode,
+                      double* stat, double* p, double* eff, cudaStream_t s) {
+  if (lab->S != val->S) return ps_fail(PS_ERR_INVALID, "sample counts differ");
   lo = std::max<int64_t>(0, lo);
-  hi = std::min<int64_t>(Fq, hi);
+  hi = std::min<int64_t>(val->F, hi);
   if (hi <= lo || (!stat && !p && !eff)) return PS_OK;
   if (!val->has_presort) {
     int rc = ps_presort_matrix(val, s);
     if (rc) return rc;
   }
-  ps_device_state* ds = ps_state();
-  const bool kw = test == PS_TEST_KRUSKAL;
-  const int kmax = kw ? std::max(1, lab->cmax) : 2;
-  int KM = kmax <= 2 ? 2 : kmax <= 8 ? 8 : kmax <= 16 ? 16 : 256;
-  // the KM = 8 variant keeps per-lane accumulators in shared memory; when they
-  // do not fit next to the walk's tables, use the register variant
-  if (KM == 8 && walk_smem(val->ldo, val->ldt, lab->ldc, 8) > 222 * 1024) KM = 16;
-  const int64_t npairs = Fc * Fq;
-  // per-pair level stride: the template width, or the real level count for k > 16
-  RankSums rs{KM > 16 ? (kmax + 31) / 32 * 32 : KM, nullptr, nullptr, nullptr};
-  uint8_t* bcodes = nullptr;
-  int* queue = nullptr;
-  int2* exl = nullptr;
-  int* exc = nullptr;
-  const int excap = (int)std::min<int64_t>(Fc * (hi - lo), 1 << 20);
-  PS_CUDA(ps_alloc(&rs.cnt, (size_t)(npairs * rs.KM), s));
-  PS_CUDA(ps_alloc(&rs.r2, (size_t)(npairs * rs.KM), s));
-  PS_CUDA(ps_alloc(&rs.tie, (size_t)npairs, s));
-  PS_CUDA(ps_alloc(&queue, 1, s));
-  PS_CUDA(ps_alloc(&exl, (size_t)excap, s));
-  PS_CUDA(ps_alloc(&exc, 1, s));
-  PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
-  PS_CUDA(cudaMemsetAsync(exc, 0, sizeof(int), s));
-  PS_CUDA(cudaMemsetAsync(rs.cnt, 0, sizeof(int32_t) * npairs * rs.KM, s));
-  PS_CUDA(cudaMemsetAsync(rs.r2, 0, sizeof(unsigned long long) * npairs * rs.KM, s));
-  const uint8_t* codes = lab->d_codes;
-  if (!kw) {
-    PS_CUDA(ps_alloc(&bcodes, (size_t)(Fc * lab->ldc), s));
-    binary_codes_kernel<<<(unsigned)Fc, 256, 0, s>>>(lab->d_mask, lab->d_zero, lab->W, lab->S, lab->ldc, bcodes);
-    PS_LAUNCHED();
-    codes = bcodes;
-  }
-  // LabelOutOfRange: a present out-of-range label meeting a present value
-  // (mixed.py:613-617) -- checked up front, so the walk never tracks it
-  int rc = kw ? ps_mixed_label_check(lab, val, 0, Fc, lo, hi, s) : PS_OK;
+  ps_rank_job* j = nullptr;
+  int rc = ps_rank_mixed_begin(test, lab, val, lo, hi, u_mode, s, &j);
   if (rc) return rc;
-  if (KM == 2) rc = launch_walk<2>(lab, val, codes, lo, hi, kw, queue, rs, s);
-  else if (KM == 8) rc = launch_walk<8>(lab, val, codes, lo, hi, kw, queue, rs, s);
-  else if (KM == 16) rc = launch_walk<16>(lab, val, codes, lo, hi, kw, queue, rs, s);
-  else rc = launch_walk<256>(lab, val, codes, lo, hi, kw, queue, rs, s);
-  if (rc) return rc;
-  const int64_t total = Fc * (hi - lo);
-  const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
-  rank_mixed_finish_kernel<<<blocks, 128, 0, s>>>(test, rs, lab->d_cat, Fc, Fq, lo, hi, u_mode, stat, p, eff,
-                                                  exl, exc, excap, ds->d_err);
-  PS_LAUNCHED();
-  if (!kw && u_mode != PS_U_ASYMPTOTIC && p) {
-    mwu_exact_kernel<<<ds->num_sms, 32, 0, s>>>(rs, Fq, exl, exc, excap, p);
-    PS_LAUNCHED();
-  }
-  ps_free(rs.cnt, s);
-  ps_free(rs.r2, s);
-  ps_free(rs.tie, s);
-  ps_free(queue, s);
-  ps_free(exl, s);
-  ps_free(exc, s);
-  ps_free(bcodes, s);
-  return PS_OK;
+  return ps_rank_mixed_end(j, stat, p, eff, s);
 }

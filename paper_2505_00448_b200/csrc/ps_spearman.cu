@@ -941,14 +941,11 @@ int ps_spearman_walk_upto(ps_spearman_job* j, int64_t h1, cudaStream_t s) {
   if (!j->single) return PS_OK;
   h1 = std::min<int64_t>(h1, j->a->F);
   if (h1 <= j->h_done) return PS_OK;
-  ps_device_state* ds = ps_state();
-  const int k = j->nws++ & 1;
   // one item per CTA (not persistent) while rows are still arriving: the
   // per-chunk prep and presort kernels run on a higher-priority stream and
   // take SMs as walk CTAs retire; the last launch is persistent
-  PS_CUDA(cudaEventRecord(ds->walk_ev[2], s));
-  PS_CUDA(cudaStreamWaitEvent(ds->walk[k], ds->walk_ev[2], 0));
-  int rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, ds->walk[k], j->grid_max, h1 < j->a->F);
+  cudaStream_t w = ps_walk_stream(j->nws++, s);
+  int rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, w, j->grid_max, h1 < j->a->F);
   j->h_done = h1;
   return rc;
 }
@@ -957,10 +954,8 @@ int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cu
   int rc = PS_OK;
   const int64_t F = j->a->F, lo = j->lo, hi = j->hi;
   ps_device_state* ds = ps_state();
-  for (int k = 0; k < 2 && j->nws > k; ++k) {
-    PS_CUDA(cudaEventRecord(ds->walk_ev[k], ds->walk[k]));
-    PS_CUDA(cudaStreamWaitEvent(s, ds->walk_ev[k], 0));
-  }
+  int jr = ps_walk_streams_join(j->nws, s);
+  if (jr) return jr;
   // one item per column h (largest first) unless overridden: no per-item
   // reload of h's tables, and the smallest columns form the tail
   int64_t gb_full = F;
@@ -983,8 +978,8 @@ int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cu
     PS_LAUNCHED();
   }
   if (j->home != s) {  // free in the allocation stream's order (pool reuse across runs)
-    PS_CUDA(cudaEventRecord(ds->walk_ev[2], s));
-    PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[2], 0));
+    PS_CUDA(cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s));
+    PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0));
   }
   job_free(j, j->home);
   return rc;
