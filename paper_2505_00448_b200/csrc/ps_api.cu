@@ -596,10 +596,22 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     return ps_rank_mixed_walk_upto(rjob, r1, aux);
   };
   const bool overlap_rank = (test == PS_TEST_MWU || test == PS_TEST_KRUSKAL) && any_out && !getenv("PS_NO_OVERLAP");
-  if (!rc && !homogeneous) rc = matrix_create(b, 0, presort_b, s, &mb, overlap_rank ? &rank_hook : nullptr);
+  // ANOVA / t-test: the moment contraction of each uploaded chunk's columns
+  ps_group_job* gjob = nullptr;
+  RowsHook group_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
+    if (!gjob) {
+      int c = ps_group_moment_begin(test, ma, m, test == PS_TEST_TTEST ? (t_variant == 0) : 1, aux, &gjob);
+      if (c) return c;
+    }
+    return ps_group_moment_upto(gjob, r1, aux);
+  };
+  const bool overlap_group = (test == PS_TEST_ANOVA || test == PS_TEST_TTEST) && any_out && !getenv("PS_NO_OVERLAP");
+  if (!rc && !homogeneous)
+    rc = matrix_create(b, 0, presort_b, s, &mb, overlap_rank ? &rank_hook : overlap_group ? &group_hook : nullptr);
   if (rc) {
     ps_spearman_abort(sjob, s);
     ps_rank_mixed_abort(rjob, s);
+    ps_group_moment_abort(gjob, s);
     ps_matrix_destroy(ma);
     ps_matrix_destroy(mb);
     return rc;
@@ -627,11 +639,14 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
         break;
       case PS_TEST_CHI2: rc = ps_chi2_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], d_out[3], s); break;
       case PS_TEST_TTEST:
-        rc = ps_group_moment_run(PS_TEST_TTEST, ma, mb, 0, cells, t_variant == 0, d_out[0], d_out[1],
-                                 d_out[2], s);
-        break;
       case PS_TEST_ANOVA:
-        rc = ps_group_moment_run(PS_TEST_ANOVA, ma, mb, 0, cells, 1, d_out[0], d_out[1], d_out[2], s);
+        if (gjob) {
+          rc = ps_group_moment_end(gjob, d_out[0], d_out[1], d_out[2], s);
+          gjob = nullptr;
+        } else {
+          rc = ps_group_moment_run(test, ma, mb, 0, cells, test == PS_TEST_TTEST ? (t_variant == 0) : 1, d_out[0],
+                                   d_out[1], d_out[2], s);
+        }
         break;
       case PS_TEST_MWU:
       case PS_TEST_KRUSKAL:
@@ -648,6 +663,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   }
   if (sjob) ps_spearman_abort(sjob, s);  // not consumed (an earlier failure)
   if (rjob) ps_rank_mixed_abort(rjob, s);
+  if (gjob) ps_group_moment_abort(gjob, s);
   // while the device computes: fault in the host output pages
   if (!rc && !getenv("PS_NO_PREFAULT")) {
     for (int k = 0; k < 4; ++k)

@@ -81,8 +81,10 @@ __global__ void onehot_bits_kernel(const uint8_t* __restrict__ codes, int64_t ld
 __global__ void __launch_bounds__(NTH, 2)
 group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double* __restrict__ vals,
                   int64_t ld, const uint32_t* __restrict__ mask, const double* __restrict__ center,
-                  int64_t W, int64_t Fq, int64_t row_tile0, int64_t col_tiles, int32_t* __restrict__ Mn,
-                  double* __restrict__ Ms, double* __restrict__ Mq, int64_t kparts, int64_t part_stride) {
+                  int64_t W, int64_t Fq, int64_t row_tile0, int64_t col_tile0, int64_t col_tiles,
+                  int32_t* __restrict__ Mn,
+                  double* __restrict__ Ms, double* __restrict__ Mq, int64_t kparts, int64_t part_stride,
+                  int64_t ldm, int64_t mcol0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // split-K (grids too small to fill the SMs): part y covers mask words
   // [W y / kparts, W (y + 1) / kparts) and writes its own partial moments
@@ -93,7 +95,7 @@ group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double*
   Stage* st = reinterpret_cast<Stage*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = warp >> 1, wj = warp & 1;
-  const int64_t rt = row_tile0 + blockIdx.x / col_tiles, ct = blockIdx.x % col_tiles;
+  const int64_t rt = row_tile0 + blockIdx.x / col_tiles, ct = col_tile0 + blockIdx.x % col_tiles;
   const int64_t row0 = rt * T, col0 = ct * T;
   const int fr = lane >> 2, fk = lane & 3;
   double cj[WN];
@@ -187,10 +189,36 @@ group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double*
         const int64_t r = row0 + wi * 8 * WM + i * 8 + fr;
         const int64_t h = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
         if (h >= Fq) continue;
-        Mn[r * Fq + h] = an[i][j][e];
-        Ms[r * Fq + h] = as[i][j][e];
-        Mq[r * Fq + h] = aq[i][j][e];
+        const int64_t o = r * ldm + (h - mcol0);  // M (ldm = Fq) or a column-window partial
+        Mn[o] = an[i][j][e];
+        Ms[o] = as[i][j][e];
+        Mq[o] = aq[i][j][e];
       }
+}
+
+// Fixed-order sum of split-K partials of a column window [c0, c0 + width)
+// (partials laid out rows x width) into M (rows x Fq).
+__global__ void group_parts_reduce_cols_kernel(const int32_t* __restrict__ Pn, const double* __restrict__ Ps,
+                                               const double* __restrict__ Pq, int64_t kparts, int64_t stride,
+                                               int64_t rows, int64_t width, int64_t c0, int64_t Fq,
+                                               int32_t* __restrict__ Mn, double* __restrict__ Ms,
+                                               double* __restrict__ Mq) {
+  const int64_t n = rows * width;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / width, c = i - r * width;
+    if (c0 + c >= Fq) continue;
+    int32_t cn = 0;
+    double cs = 0.0, cq = 0.0;
+    for (int64_t y = 0; y < kparts; ++y) {
+      cn += Pn[y * stride + i];
+      cs += Ps[y * stride + i];
+      cq += Pq[y * stride + i];
+    }
+    const int64_t o = r * Fq + c0 + c;
+    Mn[o] = cn;
+    Ms[o] = cs;
+    Mq[o] = cq;
+  }
 }
 
 // Fixed-order sum of the split-K partial moments (deterministic).
@@ -518,6 +546,51 @@ int ps_mixed_label_check(ps_matrix* lab, ps_matrix* val, int64_t g0, int64_t g1,
   return PS_OK;
 }
 
+// Per-cell statistics from the moments of cells [lo, hi), then the exact
+// in-order replay of the ill-conditioned cells (one host round trip for the
+// replay count).
+static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
+                               const int32_t* Mn, const double* Ms, const double* Mq, const int32_t* d_off,
+                               const uint32_t* bits, int2* rep, int* repc, int cap, double* stat, double* p,
+                               double* eff, int* count_out, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  const int64_t Fq = val->F, W = val->W;
+  Outs o{stat, p, eff, rep, repc, cap, ds->d_err};
+  const int blocks = (int)std::min<int64_t>(ps_ceil_div(hi - lo, 128), (int64_t)ds->num_sms * 16);
+  const bool small = lab->cmax <= 16;
+  if (small)
+    group_finish_kernel<16><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq, lo,
+                                                   hi, student, o);
+  else
+    group_finish_kernel<256><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq,
+                                                    lo, hi, student, o);
+  PS_LAUNCHED();
+  // a replay list overflow (pathological: > 4M ill-conditioned cells) is reported
+  int count = 0;
+  PS_CUDA(cudaMemcpyAsync(&count, repc, sizeof(int), cudaMemcpyDeviceToHost, s));
+  PS_CUDA(cudaStreamSynchronize(s));
+  const int n_items = std::min(count, cap);
+  if (n_items > 0) {
+    const int kslots = test == PS_TEST_ANOVA ? std::max(2, lab->cmax) : 2;
+    GroupPart* parts = nullptr;
+    PS_CUDA(ps_alloc(&parts, (size_t)n_items * kslots, s));
+    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((int64_t)n_items * kslots, 4), (int64_t)ds->num_sms * 8);
+    group_replay_parts_kernel<<<pblocks, 128, 0, s>>>(bits, d_off, val->d_vals, val->ld, val->d_mask, W, rep,
+                                                      n_items, kslots, parts);
+    PS_LAUNCHED();
+    const int fblocks = (int)std::min<int64_t>(ps_ceil_div(n_items, 128), (int64_t)ds->num_sms * 4);
+    if (small)
+      group_replay_finish_kernel<16><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student, o);
+    else
+      group_replay_finish_kernel<256><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student,
+                                                             o);
+    PS_LAUNCHED();
+    ps_free(parts, s);
+  }
+  *count_out = count;
+  return PS_OK;
+}
+
 int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
                         double* stat, double* p, double* eff, cudaStream_t s) {
   const int64_t Fc = lab->F, Fq = val->F, S = val->S;
@@ -595,8 +668,8 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
     }
     ps_prof_begin("group_gemm", s);
     group_gemm_kernel<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
-        bits, Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, ctiles, kparts > 1 ? Pn : Mn,
-        kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride);
+        bits, Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, 0, ctiles, kparts > 1 ? Pn : Mn,
+        kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride, Fq, 0);
     ps_prof_end(s);
     PS_LAUNCHED();
     if (kparts > 1) {
@@ -609,38 +682,10 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
       ps_free(Pq, s);
     }
   }
-  Outs o{stat, p, eff, rep, repc, cap, ds->d_err};
-  const int blocks = (int)std::min<int64_t>(ps_ceil_div(hi - lo, 128), (int64_t)ds->num_sms * 16);
-  const bool small = lab->cmax <= 16;
-  if (small)
-    group_finish_kernel<16><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq, lo,
-                                                   hi, student, o);
-  else
-    group_finish_kernel<256><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq,
-                                                    lo, hi, student, o);
-  PS_LAUNCHED();
-  // a replay list overflow (pathological: > 4M ill-conditioned cells) is reported
   int count = 0;
-  PS_CUDA(cudaMemcpyAsync(&count, repc, sizeof(int), cudaMemcpyDeviceToHost, s));
-  PS_CUDA(cudaStreamSynchronize(s));
-  const int n_items = std::min(count, cap);
-  if (n_items > 0) {
-    const int kslots = test == PS_TEST_ANOVA ? std::max(2, lab->cmax) : 2;
-    GroupPart* parts = nullptr;
-    PS_CUDA(ps_alloc(&parts, (size_t)n_items * kslots, s));
-    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((int64_t)n_items * kslots, 4), (int64_t)ds->num_sms * 8);
-    group_replay_parts_kernel<<<pblocks, 128, 0, s>>>(bits, d_off, val->d_vals, val->ld, val->d_mask, W, rep,
-                                                      n_items, kslots, parts);
-    PS_LAUNCHED();
-    const int fblocks = (int)std::min<int64_t>(ps_ceil_div(n_items, 128), (int64_t)ds->num_sms * 4);
-    if (small)
-      group_replay_finish_kernel<16><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student, o);
-    else
-      group_replay_finish_kernel<256><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student,
-                                                             o);
-    PS_LAUNCHED();
-    ps_free(parts, s);
-  }
+  int frc = group_finish_replay(test, lab, val, lo, hi, student, Mn, Ms, Mq, d_off, bits, rep, repc, cap, stat, p, eff,
+                                &count, s);
+  if (frc) return frc;
   ps_free(bits, s);
   ps_free(d_rf, s);
   ps_free(d_rl, s);
@@ -652,4 +697,163 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   ps_free(repc, s);
   if (count > cap) return ps_fail(PS_ERR_INVALID, "too many ill-conditioned cells for the exact replay list");
   return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Incremental ANOVA / t-test (ps_run overlaps the moment contraction with the
+// upload of the continuous matrix): every staged chunk of features whose
+// column tiles are complete is contracted on a walk stream; the statistics,
+// the label-range check and the replay run once all moments exist.
+struct ps_group_job {
+  int test = 0, student = 1;
+  ps_matrix* lab = nullptr;
+  ps_matrix* val = nullptr;
+  int64_t R = 0, Rp = 0, h_done = 0;
+  uint32_t* bits = nullptr;
+  int32_t *d_rf = nullptr, *d_rl = nullptr, *d_off = nullptr, *Mn = nullptr, *repc = nullptr;
+  double *Ms = nullptr, *Mq = nullptr;
+  int2* rep = nullptr;
+  int cap = 0, nws = 0;
+  cudaStream_t home = nullptr;
+};
+
+static void group_job_free(ps_group_job* j, cudaStream_t s) {
+  ps_free(j->bits, s);
+  ps_free(j->d_rf, s);
+  ps_free(j->d_rl, s);
+  ps_free(j->d_off, s);
+  ps_free(j->Mn, s);
+  ps_free(j->Ms, s);
+  ps_free(j->Mq, s);
+  ps_free(j->rep, s);
+  ps_free(j->repc, s);
+  delete j;
+}
+
+// moments of all level rows x the column tiles [ct0, ct1); split K (fixed
+// order) when the tile grid cannot fill two CTAs per SM, with partials laid
+// out over the column window only
+static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream_t s) {
+  if (ct1 <= ct0 || j->R == 0) return PS_OK;
+  ps_device_state* ds = ps_state();
+  ps_matrix* val = j->val;
+  const int64_t Fq = val->F, W = val->W, rtiles = ps_ceil_div(j->R, T), ctiles = ct1 - ct0;
+  const size_t smem = NSTAGE * sizeof(Stage);
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = rtiles * ctiles;
+  const int64_t kparts = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
+  const int64_t rows = rtiles * T, width = ctiles * T, c0 = ct0 * T, stride = rows * width;
+  int32_t* Pn = nullptr;
+  double *Ps = nullptr, *Pq = nullptr;
+  if (kparts > 1) {
+    PS_CUDA(ps_alloc(&Pn, (size_t)(kparts * stride), s));
+    PS_CUDA(ps_alloc(&Ps, (size_t)(kparts * stride), s));
+    PS_CUDA(ps_alloc(&Pq, (size_t)(kparts * stride), s));
+  }
+  ps_prof_begin("group_gemm", s);
+  group_gemm_kernel<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
+      j->bits, j->Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, 0, ct0, ctiles,
+      kparts > 1 ? Pn : j->Mn, kparts > 1 ? Ps : j->Ms, kparts > 1 ? Pq : j->Mq, kparts, stride,
+      kparts > 1 ? width : Fq, kparts > 1 ? c0 : 0);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  if (kparts > 1) {
+    const int blocks = (int)std::min<int64_t>(ps_ceil_div(stride, 256), (int64_t)ds->num_sms * 8);
+    group_parts_reduce_cols_kernel<<<blocks, 256, 0, s>>>(Pn, Ps, Pq, kparts, stride, rows, width, c0, Fq, j->Mn,
+                                                          j->Ms, j->Mq);
+    PS_LAUNCHED();
+    ps_free(Pn, s);
+    ps_free(Ps, s);
+    ps_free(Pq, s);
+  }
+  return PS_OK;
+}
+
+int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student, cudaStream_t s, ps_group_job** out) {
+  *out = nullptr;
+  const int64_t Fc = lab->F, Fq = val->F;
+  if (lab->S != val->S) return ps_fail(PS_ERR_INVALID, "sample counts differ");
+  ps_group_job* j = new ps_group_job();
+  j->test = test;
+  j->student = student;
+  j->lab = lab;
+  j->val = val;
+  j->home = s;
+  std::vector<int32_t> off(Fc + 1, 0), rf, rl;
+  for (int64_t g = 0; g < Fc; ++g) off[g + 1] = off[g] + (test == PS_TEST_ANOVA ? (int)lab->h_cat[g] : 2);
+  for (int64_t g = 0; g < Fc; ++g)
+    for (int q = 0; q < off[g + 1] - off[g]; ++q) {
+      rf.push_back((int32_t)g);
+      rl.push_back(test == PS_TEST_ANOVA ? q : -1 - q);
+    }
+  j->R = off[Fc];
+  j->Rp = std::max<int64_t>(T, ps_round_up(j->R, T));
+  j->cap = (int)std::min<int64_t>(Fc * Fq, 1 << 22);
+  const int64_t W = val->W;
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) { e = x; return x == cudaSuccess; };
+  if (ok(ps_alloc(&j->bits, (size_t)(j->Rp * W), s)) && ok(ps_alloc(&j->d_rf, (size_t)std::max<int64_t>(j->R, 1), s)) &&
+      ok(ps_alloc(&j->d_rl, (size_t)std::max<int64_t>(j->R, 1), s)) && ok(ps_alloc(&j->d_off, (size_t)(Fc + 1), s)) &&
+      ok(ps_alloc(&j->Mn, (size_t)(j->Rp * Fq), s)) && ok(ps_alloc(&j->Ms, (size_t)(j->Rp * Fq), s)) &&
+      ok(ps_alloc(&j->Mq, (size_t)(j->Rp * Fq), s)) && ok(ps_alloc(&j->rep, (size_t)j->cap, s)) &&
+      ok(ps_alloc(&j->repc, 1, s)) && ok(cudaMemsetAsync(j->repc, 0, sizeof(int), s)) &&
+      (j->R == 0 || (ok(cudaMemcpyAsync(j->d_rf, rf.data(), sizeof(int32_t) * j->R, cudaMemcpyHostToDevice, s)) &&
+                     ok(cudaMemcpyAsync(j->d_rl, rl.data(), sizeof(int32_t) * j->R, cudaMemcpyHostToDevice, s)))) &&
+      ok(cudaMemcpyAsync(j->d_off, off.data(), sizeof(int32_t) * (Fc + 1), cudaMemcpyHostToDevice, s))) {
+    onehot_bits_kernel<<<(unsigned)j->Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, j->d_rf,
+                                                       j->d_rl, j->R, lab->S, j->bits);
+    ps_count_launch();
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(s);
+    group_job_free(j, s);
+    return ps_cuda_check(e, "group test setup");
+  }
+  // the pageable copies above are staged by the driver: the vectors may go
+  *out = j;
+  return PS_OK;
+}
+
+int ps_group_moment_upto(ps_group_job* j, int64_t h1, cudaStream_t s) {
+  const int64_t Fq = j->val->F;
+  h1 = h1 >= Fq ? Fq : h1 / T * T;  // whole column tiles only (a partial tile waits for its rows)
+  if (h1 <= j->h_done) return PS_OK;
+  cudaStream_t w = ps_walk_stream(j->nws++, s);
+  int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w);
+  j->h_done = h1;
+  return rc;
+}
+
+int ps_group_moment_end(ps_group_job* j, double* stat, double* p, double* eff, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  int rc = ps_walk_streams_join(j->nws, s);
+  ps_matrix *lab = j->lab, *val = j->val;
+  const int64_t Fc = lab->F, Fq = val->F;
+  if (!rc) rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(Fq, T), s);
+  j->h_done = Fq;
+  if (!rc && j->test == PS_TEST_ANOVA) {
+    const dim3 grid((unsigned)ps_ceil_div(val->W, 128), (unsigned)ps_ceil_div(Fc, 32));
+    mixed_label_check_kernel<<<grid, 128, 0, s>>>(lab->d_bad, val->d_mask, val->W, 0, Fc, 0, Fq, ds->d_err);
+    ps_count_launch();
+  }
+  int count = 0;
+  if (!rc && (stat || p || eff))
+    rc = group_finish_replay(j->test, lab, val, 0, Fc * Fq, j->student, j->Mn, j->Ms, j->Mq, j->d_off, j->bits, j->rep,
+                             j->repc, j->cap, stat, p, eff, &count, s);
+  if (j->home != s) {
+    cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s);
+    cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0);
+  }
+  const int cap = j->cap;
+  group_job_free(j, j->home);
+  if (!rc && count > cap) return ps_fail(PS_ERR_INVALID, "too many ill-conditioned cells for the exact replay list");
+  return rc;
+}
+
+void ps_group_moment_abort(ps_group_job* j, cudaStream_t s) {
+  if (!j) return;
+  cudaStreamSynchronize(s);
+  cudaDeviceSynchronize();
+  group_job_free(j, j->home);
 }

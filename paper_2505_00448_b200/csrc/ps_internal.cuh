@@ -110,6 +110,12 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
 // kWalkStreams after it waits on `after`; join makes `s` wait on every used one.
 cudaStream_t ps_walk_stream(int k, cudaStream_t after);
 int ps_walk_streams_join(int used, cudaStream_t s);
+struct ps_group_job;
+// Incremental ANOVA / t-test moment contraction (as the Spearman job).
+int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student, cudaStream_t s, ps_group_job** job);
+int ps_group_moment_upto(ps_group_job* job, int64_t h1, cudaStream_t s);
+int ps_group_moment_end(ps_group_job* job, double* stat, double* p, double* eff, cudaStream_t s);
+void ps_group_moment_abort(ps_group_job* job, cudaStream_t s);
 struct ps_rank_job;
 // Incremental Mann-Whitney / Kruskal-Wallis walks (as the Spearman job).
 int ps_rank_mixed_begin(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int u_mode, cudaStream_t s,
