@@ -755,11 +755,19 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
 __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64_t hi,
                                        double* __restrict__ stat, double* __restrict__ pout,
                                        double* __restrict__ rho_out, int* __restrict__ err) {
-  const int64_t total = (hi - lo) * F;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = lo + it / F, h = it % F;
-    if (h < g) continue;
+  // one thread per triangle cell (g <= h, g in [lo, hi)): no idle lower half
+  auto before = [&](int64_t g) {  // cells of rows [lo, g)
+    return (g - lo) * F - (g * (g - 1) / 2 - lo * (lo - 1) / 2);
+  };
+  const int64_t total = before(hi);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = lo, b = hi - 1;  // last row g with before(g) <= t
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (before(mid) <= t) a = mid;
+      else b = mid - 1;
+    }
+    const int64_t g = a, h = g + (t - before(g));
     const int64_t cell = g * F + h;
     const long long n = in.n[cell];
     double rho = PS_NAN, p = PS_NAN;
@@ -972,8 +980,8 @@ int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cu
   }
   if (!rc && hi > lo) {
     ps_device_state* ds = ps_state();
-    const int64_t total = (hi - lo) * F;
-    const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
+    const int64_t tri = (hi - lo) * F - (hi * (hi - 1) / 2 - lo * (lo - 1) / 2);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(tri, 128), (int64_t)ds->num_sms * 16));
     spearman_finish_kernel<<<blocks, 128, 0, s>>>(j->ps, F, lo, hi, stat, p, rho, ds->d_err);
     PS_LAUNCHED();
   }
