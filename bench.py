@@ -289,6 +289,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-warmup", type=int, default=3)
     args = ap.parse_args()
 
     cfg = workloads.config(args.config)
@@ -457,12 +458,15 @@ def main():
         mat_a = ps.make_matrix(a, ka, na_sentinel=sentinel)
         mat_b = ps.make_matrix(b, kb, na_sentinel=sentinel) if b is not None else None
         req = ps.TestRequest(test, outputs)
-        for _ in range(2):  # warm-up (pool growth, first-touch of the pinned ring)
+        for _ in range(args.e2e_warmup):  # warm-up (pool growth, first-touch of the pinned ring)
             ps.run(req, mat_a, mat_b)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
             res = ps.run(req, mat_a, mat_b)
+            if os.environ.get("PS_BENCH_VERBOSE"):
+                print("e2e step ms %.3f" % ((time.perf_counter() - t1) * 1e3), file=sys.stderr)
         dt = (time.perf_counter() - t0) / args.e2e_steps
         h2d = a.nbytes + (b.nbytes if b is not None else 0)
         d2h = sum(res[n].nbytes for n in outputs)

@@ -49,6 +49,7 @@ int init_state(ps_device_state* st, int dev) {
   PS_CUDA(cudaEventCreateWithFlags(&st->aux_ev, cudaEventDisableTiming));
   for (auto& w : st->walk) PS_CUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
   for (auto& e : st->walk_ev) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  PS_CUDA(cudaEventCreateWithFlags(&st->alloc_ev, cudaEventDisableTiming));
   // keep freed workspace cached in the stream-ordered pool between calls
   cudaMemPool_t pool;
   PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -575,10 +576,19 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   const bool any_out = any_adj || (outs && (outs[0] || outs[1] || outs[2] || outs[3]));
   // Spearman: the walk over columns h < r1 starts as soon as rows [0, r1) are
   // uploaded and presorted, overlapping the rest of the upload
+  // jobs allocate on the main stream (one stream for every large allocation
+  // keeps the memory pool reusing its blocks from run to run); the auxiliary
+  // stream then waits for those allocations
+  auto after_alloc = [&](cudaStream_t aux) -> int {
+    PS_CUDA(cudaEventRecord(st->alloc_ev, s));
+    PS_CUDA(cudaStreamWaitEvent(aux, st->alloc_ev, 0));
+    return PS_OK;
+  };
   ps_spearman_job* sjob = nullptr;
   RowsHook walk_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
     if (!sjob) {
-      int c = ps_spearman_begin(m, 0, m->F, aux, &sjob);
+      int c = ps_spearman_begin(m, 0, m->F, s, &sjob);
+      if (!c) c = after_alloc(aux);
       if (c) return c;
     }
     return ps_spearman_walk_upto(sjob, r1, aux);
@@ -590,7 +600,8 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   ps_rank_job* rjob = nullptr;
   RowsHook rank_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
     if (!rjob) {
-      int c = ps_rank_mixed_begin(test, ma, m, 0, m->F, test == PS_TEST_MWU ? u_mode : 0, aux, &rjob);
+      int c = ps_rank_mixed_begin(test, ma, m, 0, m->F, test == PS_TEST_MWU ? u_mode : 0, s, &rjob);
+      if (!c) c = after_alloc(aux);
       if (c) return c;
     }
     return ps_rank_mixed_walk_upto(rjob, r1, aux);
@@ -600,7 +611,8 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   ps_group_job* gjob = nullptr;
   RowsHook group_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
     if (!gjob) {
-      int c = ps_group_moment_begin(test, ma, m, test == PS_TEST_TTEST ? (t_variant == 0) : 1, aux, &gjob);
+      int c = ps_group_moment_begin(test, ma, m, test == PS_TEST_TTEST ? (t_variant == 0) : 1, s, &gjob);
+      if (!c) c = after_alloc(aux);
       if (c) return c;
     }
     return ps_group_moment_upto(gjob, r1, aux);

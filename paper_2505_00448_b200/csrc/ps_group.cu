@@ -715,6 +715,11 @@ struct ps_group_job {
   int2* rep = nullptr;
   int cap = 0, nws = 0;
   cudaStream_t home = nullptr;
+  // split-K partials of the incremental launches, one set per walk stream
+  int32_t* pn[ps_device_state::kWalkStreams] = {};
+  double* psum[ps_device_state::kWalkStreams] = {};
+  double* pq[ps_device_state::kWalkStreams] = {};
+  int64_t pcap = 0;  // elements per partial array
 };
 
 static void group_job_free(ps_group_job* j, cudaStream_t s) {
@@ -727,13 +732,21 @@ static void group_job_free(ps_group_job* j, cudaStream_t s) {
   ps_free(j->Mq, s);
   ps_free(j->rep, s);
   ps_free(j->repc, s);
+  for (int k = 0; k < ps_device_state::kWalkStreams; ++k) {
+    ps_free(j->pn[k], s);
+    ps_free(j->psum[k], s);
+    ps_free(j->pq[k], s);
+  }
   delete j;
 }
 
 // moments of all level rows x the column tiles [ct0, ct1); split K (fixed
 // order) when the tile grid cannot fill two CTAs per SM, with partials laid
 // out over the column window only
-static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream_t s) {
+// `slot` >= 0: an incremental launch using the job's partial buffers of that
+// walk-stream slot (allocated once, on the job's home stream); -1: a one-off
+// launch on `s` with its own partial buffers.
+static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream_t s, int slot = -1) {
   if (ct1 <= ct0 || j->R == 0) return PS_OK;
   ps_device_state* ds = ps_state();
   ps_matrix* val = j->val;
@@ -741,11 +754,17 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
   const size_t smem = NSTAGE * sizeof(Stage);
   PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = rtiles * ctiles;
-  const int64_t kparts = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
+  int64_t kparts = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
   const int64_t rows = rtiles * T, width = ctiles * T, c0 = ct0 * T, stride = rows * width;
+  if (slot >= 0) kparts = std::max<int64_t>(1, std::min<int64_t>(kparts, j->pcap / std::max<int64_t>(1, stride)));
+  if (slot == -2) kparts = 1;  // incremental launch without partial buffers
   int32_t* Pn = nullptr;
   double *Ps = nullptr, *Pq = nullptr;
-  if (kparts > 1) {
+  if (kparts > 1 && slot >= 0) {
+    Pn = j->pn[slot];
+    Ps = j->psum[slot];
+    Pq = j->pq[slot];
+  } else if (kparts > 1) {
     PS_CUDA(ps_alloc(&Pn, (size_t)(kparts * stride), s));
     PS_CUDA(ps_alloc(&Ps, (size_t)(kparts * stride), s));
     PS_CUDA(ps_alloc(&Pq, (size_t)(kparts * stride), s));
@@ -762,9 +781,11 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
     group_parts_reduce_cols_kernel<<<blocks, 256, 0, s>>>(Pn, Ps, Pq, kparts, stride, rows, width, c0, Fq, j->Mn,
                                                           j->Ms, j->Mq);
     PS_LAUNCHED();
-    ps_free(Pn, s);
-    ps_free(Ps, s);
-    ps_free(Pq, s);
+    if (slot < 0) {
+      ps_free(Pn, s);
+      ps_free(Ps, s);
+      ps_free(Pq, s);
+    }
   }
   return PS_OK;
 }
@@ -810,6 +831,16 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
     group_job_free(j, s);
     return ps_cuda_check(e, "group test setup");
   }
+  {
+    // partial capacity per walk-stream slot: a staging chunk's columns (+ one
+    // tile), split as far as a one-tile-column grid would be
+    ps_device_state* ds = ps_state();
+    const int64_t rtiles = ps_ceil_div(std::max<int64_t>(j->R, 1), T);
+    const int64_t chunk_rows = (int64_t)std::max<size_t>(1, ps_stage_chunk_bytes() / (sizeof(double) * val->ld));
+    const int64_t width_cap = (ps_ceil_div(chunk_rows, T) + 1) * T;
+    const int64_t kp = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, rtiles), W / 16));
+    j->pcap = kp > 1 ? kp * rtiles * T * width_cap : 0;
+  }
   // the pageable copies above are staged by the driver: the vectors may go
   *out = j;
   return PS_OK;
@@ -819,8 +850,18 @@ int ps_group_moment_upto(ps_group_job* j, int64_t h1, cudaStream_t s) {
   const int64_t Fq = j->val->F;
   h1 = h1 >= Fq ? Fq : h1 / T * T;  // whole column tiles only (a partial tile waits for its rows)
   if (h1 <= j->h_done) return PS_OK;
+  const int slot = j->nws % ps_device_state::kWalkStreams;
+  if (!j->pn[slot] && j->pcap > 0) {
+    // first use of this slot: allocate on the home stream, order aux after it
+    ps_device_state* ds = ps_state();
+    PS_CUDA(ps_alloc(&j->pn[slot], (size_t)j->pcap, j->home));
+    PS_CUDA(ps_alloc(&j->psum[slot], (size_t)j->pcap, j->home));
+    PS_CUDA(ps_alloc(&j->pq[slot], (size_t)j->pcap, j->home));
+    PS_CUDA(cudaEventRecord(ds->alloc_ev, j->home));
+    PS_CUDA(cudaStreamWaitEvent(s, ds->alloc_ev, 0));
+  }
   cudaStream_t w = ps_walk_stream(j->nws++, s);
-  int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w);
+  int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w, j->pn[slot] ? slot : -2);
   j->h_done = h1;
   return rc;
 }

@@ -57,6 +57,7 @@ struct ps_device_state {
   static constexpr int kWalkStreams = 4;
   cudaStream_t walk[kWalkStreams] = {};  // incremental rank walks during uploads
   cudaEvent_t walk_ev[kWalkStreams + 1] = {};
+  cudaEvent_t alloc_ev = nullptr;  // orders allocations made on `stream` before work on `aux`
 };
 
 ps_device_state* ps_state();                 // current device's state
@@ -152,5 +153,6 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
 int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld, cudaStream_t s);
 int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void ps_host_prefault(void* dst, size_t bytes);
+size_t ps_stage_chunk_bytes();  // staging chunk size (bytes)
 int ps_stage_d2h_many(int n, void* const* dst, const void* const* src, const size_t* bytes, cudaStream_t s);
 int ps_adjust_family_run(const double* p, int64_t n, int method, double* out, cudaStream_t s);

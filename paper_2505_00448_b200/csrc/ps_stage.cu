@@ -166,6 +166,8 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
 }
 
 // contiguous device -> host copy; returns after dst is complete
+size_t ps_stage_chunk_bytes() { return kChunk; }
+
 // Touch every page of a host output buffer (one write per 4 KiB page, all
 // cores) so that first-touch page faults are taken while the device computes,
 // not inside the device-to-host copy.  The buffer is about to be overwritten.
