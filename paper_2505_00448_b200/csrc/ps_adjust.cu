@@ -460,44 +460,116 @@ __global__ void h32_fixup_kernel(const uint64_t* __restrict__ keys, const uint32
   }
 }
 
-// One CTA per queued run: bitonic sort of (low half << 32 | position) in
-// shared memory (equal low halves are equal keys: their order is free).
+// One CTA per queued run: stable LSD radix on the low key halves in
+// registers / shared memory (warp-striped items, per-warp digit counts,
+// constant bytes skipped), as the small-family kernel does for high halves.
 constexpr int kRunSortThreads = 1024;
+constexpr int kRunItems = kBlockRun / kRunSortThreads;  // 16
+constexpr int kRunWarps = kRunSortThreads / 32;
+constexpr size_t kRunSortSmem = (size_t)kBlockRun * (4 + 2 + 4);
 __global__ void __launch_bounds__(kRunSortThreads)
 long_run_sort_kernel(const uint64_t* __restrict__ keys, uint32_t* __restrict__ pos, const int* __restrict__ flag,
                      const int2* __restrict__ runs) {
-  extern __shared__ unsigned long long lr[];
+  extern __shared__ __align__(16) unsigned char lrs[];
+  uint32_t* sk = reinterpret_cast<uint32_t*>(lrs);                                // low halves
+  uint16_t* sx = reinterpret_cast<uint16_t*>(lrs + (size_t)kBlockRun * 4);        // run-local index
+  uint32_t* sp = reinterpret_cast<uint32_t*>(lrs + (size_t)kBlockRun * 6);        // original positions
+  __shared__ uint16_t wcnt[kRunWarps][256];
+  __shared__ int warp_buf[kRunWarps];
+  __shared__ uint32_t s_and, s_or;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nruns = flag[1];
   for (int r = blockIdx.x; r < nruns; r += gridDim.x) {
     const int2 run = runs[r];
-    int n = 1;
-    while (n < run.y) n <<= 1;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      unsigned long long v = ~0ull;
-      if (t < run.y) {
-        const uint32_t p = pos[run.x + t];
-        v = ((keys[p] & 0xffffffffull) << 32) | p;
+    const int L = run.y;
+    if (threadIdx.x == 0) {
+      s_and = 0xffffffffu;
+      s_or = 0u;
+    }
+    uint32_t k32[kRunItems], idx[kRunItems];  // idx: run-local index | in-warp offset << 16
+    __syncthreads();
+    {
+      uint32_t a = 0xffffffffu, o = 0u;
+#pragma unroll
+      for (int q = 0; q < kRunItems; ++q) {
+        const int t = warp * 32 * kRunItems + q * 32 + lane;
+        idx[q] = (uint32_t)t;
+        k32[q] = 0xffffffffu;  // padding sorts last
+        if (t < L) {
+          const uint32_t p = pos[run.x + t];
+          sp[t] = p;
+          k32[q] = (uint32_t)keys[p];
+          a &= k32[q];
+          o |= k32[q];
+        }
       }
-      lr[t] = v;
+      a = __reduce_and_sync(PS_FULL, a);
+      o = __reduce_or_sync(PS_FULL, o);
+      if (lane == 0) {
+        atomicAnd(&s_and, a);
+        atomicOr(&s_or, o);
+      }
     }
     __syncthreads();
-    for (int k = 2; k <= n; k <<= 1) {
-      for (int jj = k >> 1; jj > 0; jj >>= 1) {
-        for (int t = threadIdx.x; t < n; t += blockDim.x) {
-          const int o = t ^ jj;
-          if (o > t) {
-            const unsigned long long a = lr[t], b = lr[o];
-            const bool up = (t & k) == 0;
-            if ((a > b) == up) {
-              lr[t] = b;
-              lr[o] = a;
-            }
-          }
-        }
-        __syncthreads();
+    const uint32_t diff = s_and ^ s_or;
+    for (int b = 0; b < 4; ++b) {
+      const int shift = 8 * b;
+      if (((diff >> shift) & 0xffu) == 0) continue;
+      for (int q = threadIdx.x; q < kRunWarps * 256; q += kRunSortThreads) (&wcnt[0][0])[q] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kRunItems; ++q) {
+        const uint32_t dg = (k32[q] >> shift) & 0xffu;
+        const uint32_t peers = __match_any_sync(PS_FULL, dg);
+        const uint32_t base = wcnt[warp][dg];
+        __syncwarp();
+        idx[q] = (idx[q] & 0xFFFFu) | ((base + __popc(peers & lanemask_lt())) << 16);
+        if ((peers >> lane) == 1u) wcnt[warp][dg] = (uint16_t)(base + __popc(peers));
+        __syncwarp();
       }
+      __syncthreads();
+      if (threadIdx.x < 256) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kRunWarps; ++w) tot += wcnt[w][threadIdx.x];
+        uint32_t x = tot;
+#pragma unroll
+        for (int sft = 1; sft < 32; sft <<= 1) {
+          const uint32_t y = __shfl_up_sync(PS_FULL, x, sft);
+          if (lane >= sft) x += y;
+        }
+        if (lane == 31) warp_buf[warp] = (int)x;
+        asm volatile("bar.sync 1, 256;");
+        uint32_t before = 0;
+        for (int w = 0; w < warp; ++w) before += (uint32_t)warp_buf[w];
+        uint32_t run_ = before + x - tot;
+        for (int w = 0; w < kRunWarps; ++w) {
+          const uint32_t c = wcnt[w][threadIdx.x];
+          wcnt[w][threadIdx.x] = (uint16_t)run_;
+          run_ += c;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kRunItems; ++q) {
+        const uint32_t dg = (k32[q] >> shift) & 0xffu;
+        const uint32_t dst = (uint32_t)wcnt[warp][dg] + (idx[q] >> 16);
+        sk[dst] = k32[q];
+        sx[dst] = (uint16_t)idx[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kRunItems; ++q) {
+        const int t = warp * 32 * kRunItems + q * 32 + lane;
+        k32[q] = sk[t];
+        idx[q] = sx[t];
+      }
+      __syncthreads();
     }
-    for (int t = threadIdx.x; t < run.y; t += blockDim.x) pos[run.x + t] = (uint32_t)lr[t];
+#pragma unroll
+    for (int q = 0; q < kRunItems; ++q) {
+      const int t = warp * 32 * kRunItems + q * 32 + lane;
+      if (t < L) pos[run.x + t] = sp[idx[q] & 0xFFFFu];
+    }
     __syncthreads();
   }
 }
@@ -826,9 +898,9 @@ int adjust_fast(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(fam_max, 256), (int64_t)ds->num_sms * 8));
     h32_fixup_kernel<<<blocks, 256, 0, s>>>(keys, dk[cur], pos[cur], d_count, d_flag, runs);
     PS_LAUNCHED();
-    const size_t smem = (size_t)kBlockRun * sizeof(unsigned long long);
-    PS_CUDA(cudaFuncSetAttribute(long_run_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    long_run_sort_kernel<<<ds->num_sms, kRunSortThreads, smem, s>>>(keys, pos[cur], d_flag, runs);
+    PS_CUDA(cudaFuncSetAttribute(long_run_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kRunSortSmem));
+    long_run_sort_kernel<<<ds->num_sms, kRunSortThreads, kRunSortSmem, s>>>(keys, pos[cur], d_flag, runs);
     PS_LAUNCHED();
   }
   unsigned long long hp[2] = {0, 0};

@@ -70,6 +70,10 @@ def test_adjust_large_family_runs(oracle, method):
     y = rng.random(size)
     y[:40000] = rng.integers(0, 300, 40000) * 2.0**-1074                # too long for the CTA sort
     cases.append(y)
+    x = rng.random(size)
+    x[:5000] = 0.5 + rng.integers(0, 5000, 5000) * 2.0**-40             # CTA bitonic (wide low halves)
+    x[5000:7000] = 0.25 + rng.integers(0, 2000, 2000) * 2.0**-54        # CTA counting sort
+    cases.append(x)
     for x in cases:
         got = ps.adjust(x.reshape(1, -1), method, symmetric=False).ravel()
         assert bitwise_equal(got, oracle.adjust_family(x, method)), method
