@@ -217,11 +217,31 @@ __global__ void rank_scale_kernel(const uint64_t* __restrict__ keys, int64_t m, 
   if (i < m) ranked[i] = s[threadIdx.x];
   if (threadIdx.x == 0) block_min[blockIdx.x] = s[0];
 }
-// suffix-min over block minima (exclusive, i.e. min of later blocks), in place
-__global__ void block_suffix_min_kernel(double* __restrict__ bm, int64_t nb) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double run = CUDART_INF;
-  for (int64_t b = nb - 1; b >= 0; --b) {
+// suffix-min over block minima (exclusive, i.e. min of later blocks), in
+// place; one CTA: each thread a contiguous chunk, a reverse scan of the chunk
+// minima across the block
+constexpr int kSuffixThreads = 1024;
+__global__ void __launch_bounds__(kSuffixThreads) block_suffix_min_kernel(double* __restrict__ bm, int64_t nb) {
+  __shared__ double wmin[kSuffixThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (nb + kSuffixThreads - 1) / kSuffixThreads;
+  const int64_t c0 = min(nb, (int64_t)threadIdx.x * per), c1 = min(nb, c0 + per);
+  double m = CUDART_INF;
+  for (int64_t b = c0; b < c1; ++b) m = fmin(m, bm[b]);
+  // exclusive suffix min over threads (higher threads are later chunks)
+  double x = m;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_down_sync(PS_FULL, x, o);
+    if (lane + o < 32) x = fmin(x, y);
+  }
+  if (lane == 0) wmin[warp] = x;  // min over this warp's lanes
+  __syncthreads();
+  double after = CUDART_INF;       // min over later warps
+  for (int w = warp + 1; w < kSuffixThreads / 32; ++w) after = fmin(after, wmin[w]);
+  const double later_lanes = __shfl_down_sync(PS_FULL, x, 1);
+  double run = fmin(after, lane < 31 ? later_lanes : CUDART_INF);
+  for (int64_t b = c1 - 1; b >= c0; --b) {
     const double v = bm[b];
     bm[b] = run;
     run = fmin(run, v);
@@ -923,7 +943,7 @@ int adjust_fast(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     PS_CUDA(ps_alloc(&bm, (size_t)nb, s));
     rank_scale_pos_kernel<<<(unsigned)nb, 1024, 0, s>>>(keys, pos[cur], m, scale, ranked, bm);
     PS_LAUNCHED();
-    block_suffix_min_kernel<<<1, 32, 0, s>>>(bm, nb);
+    block_suffix_min_kernel<<<1, kSuffixThreads, 0, s>>>(bm, nb);
     PS_LAUNCHED();
     bh_scatter_pos_kernel<<<(unsigned)nb, 1024, 0, s>>>(ranked, bm, pos[cur], idx, m, cols, symmetric, out);
     PS_LAUNCHED();
@@ -1023,7 +1043,7 @@ int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
   PS_CUDA(ps_alloc(&bm, (size_t)nb, s));
   rank_scale_kernel<<<(unsigned)nb, 1024, 0, s>>>(kin, m, scale, ranked, bm);
   PS_LAUNCHED();
-  block_suffix_min_kernel<<<1, 32, 0, s>>>(bm, nb);
+  block_suffix_min_kernel<<<1, kSuffixThreads, 0, s>>>(bm, nb);
   PS_LAUNCHED();
   bh_scatter_kernel<<<(unsigned)nb, 1024, 0, s>>>(ranked, bm, vin, m, cols, symmetric, out);
   PS_LAUNCHED();
