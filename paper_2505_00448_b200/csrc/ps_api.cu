@@ -574,6 +574,25 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   ps_matrix* mb = nullptr;
   bool any_adj = adj_outs && (adj_outs[0] || adj_outs[1] || adj_outs[2]);
   const bool any_out = any_adj || (outs && (outs[0] || outs[1] || outs[2] || outs[3]));
+  if (!a || a->n_features <= 0 || (!homogeneous && b->n_features <= 0))
+    return ps_fail(PS_ERR_INVALID, "expected a non-empty matrix");
+  // device outputs first: incremental kernels may write them during the upload
+  const int64_t rows = a->n_features, cols = homogeneous ? a->n_features : b->n_features;
+  const int64_t cells = rows * cols;
+  double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
+  auto free_outs = [&]() {
+    for (int k = 0; k < 4; ++k) ps_free(d_out[k], s);
+  };
+  for (int k = 0; k < 4 && !rc; ++k) {
+    const bool want = (outs && outs[k]) || (k == 1 && any_adj);
+    if (!want) continue;
+    if (ps_alloc(&d_out[k], (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
+    if (!rc) rc = ps_fill_nan(d_out[k], cells, s);
+  }
+  if (rc) {
+    free_outs();
+    return rc;
+  }
   // Spearman: the walk over columns h < r1 starts as soon as rows [0, r1) are
   // uploaded and presorted, overlapping the rest of the upload
   // jobs allocate on the main stream (one stream for every large allocation
@@ -583,6 +602,16 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     PS_CUDA(cudaEventRecord(st->alloc_ev, s));
     PS_CUDA(cudaStreamWaitEvent(aux, st->alloc_ev, 0));
     return PS_OK;
+  };
+  // Pearson: the tile columns of the uploaded rows
+  ps_pearson_job* pjob = nullptr;
+  RowsHook pearson_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
+    if (!pjob) {
+      int c = ps_pearson_begin(m, d_out[0], d_out[1], d_out[2], s, &pjob);
+      if (!c) c = after_alloc(aux);
+      if (c) return c;
+    }
+    return ps_pearson_upto(pjob, r1, aux);
   };
   ps_spearman_job* sjob = nullptr;
   RowsHook walk_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
@@ -594,8 +623,14 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     return ps_spearman_walk_upto(sjob, r1, aux);
   };
   g_tl.mark("start", s);
-  const bool overlap = test == PS_TEST_SPEARMAN && any_out && !getenv("PS_NO_OVERLAP");
-  rc = matrix_create(a, 0, presort_a, s, &ma, overlap ? &walk_hook : nullptr);
+  const bool no_overlap = getenv("PS_NO_OVERLAP") != nullptr;
+  const bool overlap = test == PS_TEST_SPEARMAN && any_out && !no_overlap;
+  // (only when the tile triangle alone fills the GPU: small matrices keep the
+  // split-K whole-matrix launch)
+  const int64_t nt_p = (rows + 63) / 64;
+  const bool overlap_pearson =
+      test == PS_TEST_PEARSON && any_out && !no_overlap && nt_p * (nt_p + 1) / 2 >= 8LL * st->num_sms;
+  rc = matrix_create(a, 0, presort_a, s, &ma, overlap ? &walk_hook : overlap_pearson ? &pearson_hook : nullptr);
   // Mann-Whitney / Kruskal-Wallis: likewise, per uploaded chunk of features
   ps_rank_job* rjob = nullptr;
   RowsHook rank_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
@@ -621,26 +656,26 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   if (!rc && !homogeneous)
     rc = matrix_create(b, 0, presort_b, s, &mb, overlap_rank ? &rank_hook : overlap_group ? &group_hook : nullptr);
   if (rc) {
+    ps_pearson_abort(pjob, s);
     ps_spearman_abort(sjob, s);
     ps_rank_mixed_abort(rjob, s);
     ps_group_moment_abort(gjob, s);
     ps_matrix_destroy(ma);
     ps_matrix_destroy(mb);
+    free_outs();
     return rc;
   }
   tr.mark("matrices");
-  const int64_t rows = ma->F, cols = homogeneous ? ma->F : mb->F;
-  const int64_t cells = rows * cols;
-  double* d_out[4] = {nullptr, nullptr, nullptr, nullptr};
-  for (int k = 0; k < 4 && !rc; ++k) {
-    const bool want = (outs && outs[k]) || (k == 1 && any_adj);
-    if (!want) continue;
-    if (ps_alloc(&d_out[k], (size_t)cells, s) != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "out of device memory");
-    if (!rc) rc = ps_fill_nan(d_out[k], cells, s);
-  }
   if (!rc) {
     switch (test) {
-      case PS_TEST_PEARSON: rc = ps_pearson_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s); break;
+      case PS_TEST_PEARSON:
+        if (pjob) {
+          rc = ps_pearson_end(pjob, s);
+          pjob = nullptr;
+        } else {
+          rc = ps_pearson_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s);
+        }
+        break;
       case PS_TEST_SPEARMAN:
         if (sjob) {
           rc = ps_spearman_end(sjob, d_out[0], d_out[1], d_out[2], s);
@@ -673,7 +708,8 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
       default: rc = ps_fail(PS_ERR_INVALID, "unknown test");
     }
   }
-  if (sjob) ps_spearman_abort(sjob, s);  // not consumed (an earlier failure)
+  if (pjob) ps_pearson_abort(pjob, s);  // not consumed (an earlier failure)
+  if (sjob) ps_spearman_abort(sjob, s);
   if (rjob) ps_rank_mixed_abort(rjob, s);
   if (gjob) ps_group_moment_abort(gjob, s);
   // while the device computes: fault in the host output pages

@@ -43,6 +43,14 @@ __host__ __device__ __forceinline__ void ps_tri_tile(int64_t t, int64_t T, int64
   *I = i;
   *J = i + (t - (i * T - i * (i - 1) / 2));
 }
+// column-major upper triangle: tile t -> (I <= J), columns J in order
+__host__ __device__ __forceinline__ void ps_tri_tile_cm(int64_t t, int64_t* I, int64_t* J) {
+  int64_t j = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while (j > 0 && j * (j + 1) / 2 > t) --j;
+  while ((j + 1) * (j + 2) / 2 <= t) ++j;
+  *J = j;
+  *I = t - j * (j + 1) / 2;
+}
 __host__ __device__ __forceinline__ int64_t ps_tri_offset(int64_t I, int64_t T) {
   return I * T - I * (I - 1) / 2;
 }

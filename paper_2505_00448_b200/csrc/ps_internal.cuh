@@ -111,6 +111,12 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
 // kWalkStreams after it waits on `after`; join makes `s` wait on every used one.
 cudaStream_t ps_walk_stream(int k, cudaStream_t after);
 int ps_walk_streams_join(int used, cudaStream_t s);
+struct ps_pearson_job;
+// Incremental Pearson tiles (outputs must exist when the job begins).
+int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStream_t s, ps_pearson_job** job);
+int ps_pearson_upto(ps_pearson_job* job, int64_t h1, cudaStream_t s);
+int ps_pearson_end(ps_pearson_job* job, cudaStream_t s);
+void ps_pearson_abort(ps_pearson_job* job, cudaStream_t s);
 struct ps_group_job;
 // Incremental ANOVA / t-test moment contraction (as the Spearman job).
 int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student, cudaStream_t s, ps_group_job** job);

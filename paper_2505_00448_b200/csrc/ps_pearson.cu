@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
                     int64_t W, const double* __restrict__ center, int64_t F, int64_t NT,
                     int64_t tile0, int64_t lo, int64_t hi, int nsplit, int64_t chunks_per_split,
-                    Outs o, double* __restrict__ ws) {
+                    Outs o, double* __restrict__ ws, int colmajor) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage* st = reinterpret_cast<Stage*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -109,7 +109,8 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   const int64_t tile = tile0 + blockIdx.x / nsplit;
   const int split = blockIdx.x % nsplit;
   int64_t I, J;
-  ps_tri_tile(tile, NT, &I, &J);
+  if (colmajor) ps_tri_tile_cm(tile, &I, &J);  // incremental launches: columns of uploaded rows
+  else ps_tri_tile(tile, NT, &I, &J);
   const int64_t row0 = I * T, col0 = J * T;
   const int64_t c_begin = (int64_t)split * chunks_per_split;
   const int64_t c_end = min(W, c_begin + chunks_per_split);
@@ -390,7 +391,7 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   const int64_t grid = ntiles * nsplit;
   ps_prof_begin("pearson_tile", s);
   pearson_tile_kernel<<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
-      a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws);
+      a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
   ps_prof_end(s);
   PS_LAUNCHED();
   if (nsplit > 1) {
@@ -410,4 +411,91 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   ps_free(o.replay_count, s);
   ps_free(ws, s);
   return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Incremental Pearson (ps_run overlaps the tiles with the input upload): the
+// tile columns J whose rows [0, (J+1) T) are uploaded run on the walk
+// streams in column-major triangle order (no split-K: results are identical
+// to the whole-matrix launch tile by tile); the replay of ill-conditioned
+// pairs runs once all tiles are done.
+struct ps_pearson_job {
+  ps_matrix* a = nullptr;
+  Outs o{};
+  int64_t J_done = 0;  // tile columns launched
+  int nws = 0;
+  cudaStream_t home = nullptr;
+};
+
+int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStream_t s, ps_pearson_job** out) {
+  *out = nullptr;
+  ps_pearson_job* j = new ps_pearson_job();
+  j->a = a;
+  j->home = s;
+  const int64_t F = a->F;
+  const int cap = (int)std::min<int64_t>(F * F, 1 << 22);
+  j->o = Outs{stat, p, r2, nullptr, nullptr, cap, ps_state()->d_err};
+  cudaError_t e = ps_alloc(&j->o.replay, (size_t)cap, s);
+  if (e == cudaSuccess) e = ps_alloc(&j->o.replay_count, 1, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(j->o.replay_count, 0, sizeof(int), s);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kSmemBytes);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(s);
+    ps_free(j->o.replay, s);
+    ps_free(j->o.replay_count, s);
+    delete j;
+    return ps_cuda_check(e, "pearson setup");
+  }
+  *out = j;
+  return PS_OK;
+}
+
+static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream_t s) {
+  if (J1 <= J0) return PS_OK;
+  ps_matrix* a = j->a;
+  const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
+  const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
+  ps_prof_begin("pearson_tile", s);
+  pearson_tile_kernel<<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(a->d_vals, a->ld, a->d_mask, W, a->d_center, F,
+                                                                     NT, t0, 0, F, 1, W, j->o, nullptr, 1);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
+  const int64_t F = j->a->F;
+  const int64_t J1 = h1 >= F ? ps_ceil_div(F, T) : h1 / T;  // whole tile columns only
+  if (J1 <= j->J_done) return PS_OK;
+  cudaStream_t w = ps_walk_stream(j->nws++, s);
+  int rc = pearson_columns(j, j->J_done, J1, w);
+  j->J_done = J1;
+  return rc;
+}
+
+int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  int rc = ps_walk_streams_join(j->nws, s);
+  ps_matrix* a = j->a;
+  if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
+  if (!rc) {
+    pearson_replay_kernel<<<ds->num_sms * 4, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->S, a->F, j->o.replay,
+                                                         j->o.replay_count, j->o.replay_cap, 0, a->F, j->o);
+    ps_count_launch();
+    if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson replay launch");
+  }
+  ps_free(j->o.replay, j->home);
+  ps_free(j->o.replay_count, j->home);
+  delete j;
+  return rc;
+}
+
+void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
+  if (!j) return;
+  cudaStreamSynchronize(s);
+  cudaDeviceSynchronize();
+  ps_free(j->o.replay, j->home);
+  ps_free(j->o.replay_count, j->home);
+  delete j;
 }
