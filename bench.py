@@ -403,7 +403,9 @@ def main():
     launches = int(lib.ps_kernel_launches())
     clk = clocks.stop()
     lib.ps_profile_enable(0)
-    kern_ms, kern_n = _lib.profile_collect(ROOF[test][3])
+    # busy time of the dominant kernel (union over its launches: incremental
+    # launches of one step run concurrently on several streams)
+    kern_ms, kern_n = _lib.profile_collect_union(ROOF[test][3])
     total_ms = sum(times)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
@@ -416,7 +418,7 @@ def main():
     bound, unit, per_ps, _kname = ROOF[test]
     roof = None
     if kern_n:
-        launch_ms = kern_ms / kern_n
+        launch_ms = kern_ms / args.steps  # kernel busy ms per step (all of its launches)
         units_per_launch = work_units / world
         if test == "chi2":
             ks = cat_a
@@ -450,7 +452,8 @@ def main():
                 traffic = None
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                 "frac": achieved / peak, "traffic": traffic, "kernel": ROOF[test][3],
-                "launch_ms": launch_ms, "work_per_pair_sample": per_ps_desc}
+                "launch_ms": launch_ms, "launches_per_step": kern_n / args.steps,
+                "work_per_pair_sample": per_ps_desc}
 
     # ---------------- end to end through run()
     e2e = None

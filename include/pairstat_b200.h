@@ -173,6 +173,9 @@ void ps_reset_kernel_launches(void);
  * is bracketed by CUDA events on its launch stream.  collect() sums them. */
 void ps_profile_enable(int on);
 int ps_profile_collect(const char* name, double* total_ms, int64_t* count);
+/* The union of the launch intervals instead of their sum: the kernel's busy
+ * time when launches of it run concurrently on several streams. */
+int ps_profile_collect_union(const char* name, double* busy_ms, int64_t* count);
 
 /* ---- presort tables in caller buffers (multi-GPU sharded presort) ----
  * Rank r presorts its own rows into buffers of F rows (ps_presort_layout gives

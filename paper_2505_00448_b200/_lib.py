@@ -60,6 +60,7 @@ EXPORTED = (
     "ps_reset_kernel_launches",
     "ps_profile_enable",
     "ps_profile_collect",
+    "ps_profile_collect_union",
     "ps_presort_layout",
     "ps_matrix_attach_presort",
     "ps_matrix_presort_rows",
@@ -162,6 +163,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.ps_profile_enable.argtypes = [i32]
     lib.ps_profile_collect.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int64)]
+    lib.ps_profile_collect_union.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(ctypes.c_int64)]
 
 
 def profile_collect(name: str) -> tuple[float, int]:
@@ -250,3 +253,11 @@ def specfun(name: str, args) -> np.ndarray:
     out = np.empty(a.shape[0])
     check(load().ps_specfun_eval(which, a.ctypes.data, a.shape[0], nargs, out.ctypes.data))
     return out
+
+
+def profile_collect_union(name: str) -> tuple[float, int]:
+    """Busy time (union of launch intervals) and launch count of a kernel."""
+    ms = ctypes.c_double(0.0)
+    cnt = ctypes.c_int64(0)
+    load().ps_profile_collect_union(name.encode(), ctypes.byref(ms), ctypes.byref(cnt))
+    return ms.value, cnt.value

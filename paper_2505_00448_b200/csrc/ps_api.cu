@@ -217,6 +217,49 @@ int ps_profile_collect(const char* name, double* total_ms, int64_t* count) {
   return PS_OK;
 }
 
+// Union of the named kernel's launch intervals (concurrent launches on
+// several streams count once): the kernel's busy time on the device.
+int ps_profile_collect_union(const char* name, double* busy_ms, int64_t* count) {
+  Guard g;
+  std::vector<std::pair<double, double>> iv;
+  std::vector<ProfRec> keep;
+  cudaEvent_t base = nullptr;
+  for (auto& r : g_prof_recs) {
+    if (r.name != name) {
+      keep.push_back(r);
+      continue;
+    }
+    cudaEventSynchronize(r.b);
+    if (!base) base = r.a;
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, base, r.a);
+    cudaEventElapsedTime(&b, base, r.b);
+    iv.emplace_back(a, b);
+  }
+  std::sort(iv.begin(), iv.end());
+  double busy = 0.0, cs = 0.0, ce = -1e300;
+  for (const auto& x : iv) {
+    if (x.first > ce) {
+      if (ce > cs) busy += ce - cs;
+      cs = x.first;
+      ce = x.second;
+    } else if (x.second > ce) {
+      ce = x.second;
+    }
+  }
+  if (!iv.empty() && ce > cs) busy += ce - cs;
+  for (auto& r : g_prof_recs)
+    if (r.name == name) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+  g_prof_recs.swap(keep);
+  g_prof_open = nullptr;
+  *busy_ms = busy;
+  *count = (int64_t)iv.size();
+  return PS_OK;
+}
+
 int ps_device_count(int* count) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -259,6 +302,41 @@ int ps_set_device(int device) {
 }
 
 }  // extern "C"
+
+bool ps_presort_pending(const ps_matrix* m) {
+  for (const auto& mk : m->presort_marks)
+    if (cudaEventQuery(mk.second) == cudaErrorNotReady) return true;
+  cudaGetLastError();
+  return false;
+}
+
+// Device-resident presort in chunks of one CTA wave of features on the
+// auxiliary stream, each chunk marked by an event; the main stream waits for
+// the whole presort (every other consumer stays ordered), while the rank walks
+// of a following block call may start on the chunks already presorted.
+static int presort_in_chunks(ps_matrix* m, cudaStream_t s) {
+  ps_device_state* st = ps_state();
+  const int64_t step = st->num_sms;
+  if (m->F < 2 * step || getenv("PS_NO_OVERLAP")) return ps_presort_matrix(m, s);
+  int rc = ps_presort_begin(m, s);
+  if (rc) return rc;
+  PS_CUDA(cudaEventRecord(st->aux_ev, s));
+  PS_CUDA(cudaStreamWaitEvent(st->aux, st->aux_ev, 0));
+  for (int64_t r0 = 0; r0 < m->F && !rc; r0 += step) {
+    const int64_t r1 = std::min<int64_t>(m->F, r0 + step);
+    rc = ps_presort_rows(m, r0, r1, st->aux);
+    cudaEvent_t e = nullptr;
+    cudaError_t ce = cudaSuccess;
+    if (!rc) ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (!rc && ce == cudaSuccess) ce = cudaEventRecord(e, st->aux);
+    if (e) m->presort_marks.emplace_back(r1, e);
+    if (!rc && ce != cudaSuccess) rc = ps_cuda_check(ce, "presort mark");
+  }
+  if (rc) return rc;
+  PS_CUDA(cudaEventRecord(st->aux_ev, st->aux));
+  PS_CUDA(cudaStreamWaitEvent(s, st->aux_ev, 0));
+  return ps_presort_end(m, s);
+}
 
 // Called on the auxiliary stream after each staged chunk of rows [0, r1) is
 // prepared (and presorted): lets ps_run start computing on the rows already
@@ -380,7 +458,10 @@ static int matrix_create(const ps_matrix_desc* desc, int values_on_device, int w
   tr.mark("  upload");
   rc = ps_prepare_matrix(m, s);
   tr.mark("  prepare");
-  if (!rc && want_presort) rc = ps_presort_matrix(m, s);
+  // the prepared values / codes (before any presort wait on s)
+  if (!rc && cudaEventCreateWithFlags(&m->ready, cudaEventDisableTiming) == cudaSuccess)
+    cudaEventRecord(m->ready, s);
+  if (!rc && want_presort) rc = presort_in_chunks(m, s);
   tr.mark("  presort");
   if (rc) {
     ps_matrix_destroy(m);
@@ -450,6 +531,8 @@ int ps_matrix_destroy(ps_matrix* m) {
     ps_free(m->d_len, s);
   }
   for (void* p : m->presort_scratch) ps_free(p, s);
+  for (auto& mk : m->presort_marks) cudaEventDestroy(mk.second);
+  if (m->ready) cudaEventDestroy(m->ready);
   delete[] m->h_cat;
   delete m;
   return PS_OK;

@@ -2,6 +2,8 @@
 // shared between the per-test translation units and the C-ABI layer.
 #pragma once
 #include <functional>
+#include <utility>
+#include <vector>
 #include <cstdint>
 #include <string>
 #include <cuda_runtime.h>
@@ -44,7 +46,15 @@ struct ps_matrix {
   uint16_t* d_nextb = nullptr;    // F x ldt: suffix-min boundary position per word
   uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
   void* presort_scratch[4] = {nullptr, nullptr, nullptr, nullptr};  // global radix path (S > 20480)
+  // device-side presort in row chunks on the auxiliary stream: (rows [0, r1)
+  // presorted, event) -- rank walks start on the chunks already done
+  std::vector<std::pair<int64_t, cudaEvent_t>> presort_marks;
+  cudaEvent_t ready = nullptr;  // device-created matrices: values / codes prepared
 };
+
+// true when the matrix carries presort chunk marks some of which are still
+// pending on the device (the walks can then overlap the presort)
+bool ps_presort_pending(const ps_matrix* m);
 
 // Per-device library state.
 struct ps_device_state {

@@ -719,8 +719,36 @@ int ps_rank_mixed_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int6
     int rc = ps_presort_matrix(val, s);
     if (rc) return rc;
   }
+  // the continuous matrix still presorting in chunks on the auxiliary stream:
+  // walk each presorted chunk of features as it completes (the label matrix
+  // must be prepared first: its ready event)
+  // (Kruskal-Wallis only: the Mann-Whitney walk is short next to the presort
+  // and gains nothing from starting early)
+  const bool inc = test == PS_TEST_KRUSKAL && ps_presort_pending(val);
+  ps_device_state* ds = ps_state();
+  cudaStream_t home = inc ? ds->walk[0] : s;
+  if (inc && lab->ready) PS_CUDA(cudaStreamWaitEvent(home, lab->ready, 0));
+  if (inc && !lab->ready) {  // no marker: order after everything on s
+    PS_CUDA(cudaEventRecord(ds->alloc_ev, s));
+    PS_CUDA(cudaStreamWaitEvent(home, ds->alloc_ev, 0));
+  }
   ps_rank_job* j = nullptr;
-  int rc = ps_rank_mixed_begin(test, lab, val, lo, hi, u_mode, s, &j);
+  int rc = ps_rank_mixed_begin(test, lab, val, lo, hi, u_mode, home, &j);
   if (rc) return rc;
-  return ps_rank_mixed_end(j, stat, p, eff, s);
+  if (inc) {
+    PS_CUDA(cudaEventRecord(ds->alloc_ev, home));
+    int gb = kIncrementalRows;
+    if (const char* e = getenv("PS_RANK_GB")) gb = std::max(1, atoi(e));
+    for (const auto& mk : val->presort_marks) {
+      const int64_t h1 = std::min<int64_t>(mk.first, j->hi);
+      if (h1 <= j->h_done || rc) continue;
+      cudaStream_t w = ds->walk[j->nws++ % ps_device_state::kWalkStreams];
+      PS_CUDA(cudaStreamWaitEvent(w, mk.second, 0));
+      PS_CUDA(cudaStreamWaitEvent(w, ds->alloc_ev, 0));
+      rc = rank_walk_range(j, j->h_done, h1, gb, h1 < j->hi, w);
+      j->h_done = h1;
+    }
+  }
+  int rc2 = ps_rank_mixed_end(j, stat, p, eff, s);
+  return rc ? rc : rc2;
 }

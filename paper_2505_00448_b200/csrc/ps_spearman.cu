@@ -1009,10 +1009,28 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
     int rc = ps_presort_matrix(a, s);
     if (rc) return rc;
   }
+  // a presort still running in chunks on the auxiliary stream: walk each
+  // presorted chunk's columns on the walk streams as it completes
+  const bool inc = ps_presort_pending(a);
+  ps_device_state* ds = ps_state();
+  cudaStream_t home = inc ? ds->walk[0] : s;
   ps_spearman_job* j = nullptr;
-  int rc = ps_spearman_begin(a, lo, hi, s, &j);
+  int rc = ps_spearman_begin(a, lo, hi, home, &j);
   if (rc) return rc;
-  return ps_spearman_end(j, stat, p, rho, s);
+  if (inc && j->single) {
+    PS_CUDA(cudaEventRecord(ds->alloc_ev, home));
+    for (const auto& mk : a->presort_marks) {
+      const int64_t h1 = std::min<int64_t>(mk.first, a->F);
+      if (h1 <= j->h_done || rc) continue;
+      cudaStream_t w = ds->walk[j->nws++ % ps_device_state::kWalkStreams];
+      PS_CUDA(cudaStreamWaitEvent(w, mk.second, 0));
+      PS_CUDA(cudaStreamWaitEvent(w, ds->alloc_ev, 0));
+      rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, w, j->grid_max, h1 < a->F);
+      j->h_done = h1;
+    }
+  }
+  int rc2 = ps_spearman_end(j, stat, p, rho, s);
+  return rc ? rc : rc2;
 }
 
 #ifdef PS_WALK_TIMING
