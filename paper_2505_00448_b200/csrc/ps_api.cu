@@ -699,7 +699,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   ps_spearman_job* sjob = nullptr;
   RowsHook walk_hook = [&](ps_matrix* m, int64_t r1, cudaStream_t aux) -> int {
     if (!sjob) {
-      int c = ps_spearman_begin(m, 0, m->F, s, &sjob);
+      int c = ps_spearman_begin(m, 0, m->F, d_out[0], d_out[1], d_out[2], s, &sjob);
       if (!c) c = after_alloc(aux);
       if (c) return c;
     }
@@ -761,7 +761,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
         break;
       case PS_TEST_SPEARMAN:
         if (sjob) {
-          rc = ps_spearman_end(sjob, d_out[0], d_out[1], d_out[2], s);
+          rc = ps_spearman_end(sjob, s);
           sjob = nullptr;
         } else {
           rc = ps_spearman_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s);

@@ -144,9 +144,10 @@ struct ps_spearman_job;
 // Incremental Spearman walk (ps_run overlaps it with the input upload):
 // begin allocates, walk_upto walks the columns h < h1 whose rows are
 // presorted, end walks the rest, folds and finishes (and frees the job).
-int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, cudaStream_t s, ps_spearman_job** job);
+int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho, cudaStream_t s,
+                      ps_spearman_job** job);
 int ps_spearman_walk_upto(ps_spearman_job* job, int64_t h1, cudaStream_t s);
-int ps_spearman_end(ps_spearman_job* job, double* stat, double* p, double* rho, cudaStream_t s);
+int ps_spearman_end(ps_spearman_job* job, cudaStream_t s);
 void ps_spearman_abort(ps_spearman_job* job, cudaStream_t s);
 int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
                     cudaStream_t s);

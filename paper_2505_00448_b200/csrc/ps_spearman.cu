@@ -699,14 +699,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
 
 // One warp per (g, h) cell of chunk [c0, c1): fold the SW per-warp partials
 // into the exact 4x sums (tie-free walks: the closed-form sentinel).
-__global__ void spearman_partials_kernel(PairParts in, int64_t F, int64_t c1, PairSums out) {
+// (columns h in [h0, h1) only: incremental launches fold their own columns)
+__global__ void spearman_partials_kernel(PairParts in, int64_t F, int64_t c1, PairSums out, int64_t h0,
+                                         int64_t h1) {
   const int lane = threadIdx.x & 31;
-  const int64_t ncell = (c1 - in.c0) * F;
+  const int64_t nh = h1 - h0;
+  const int64_t ncell = (c1 - in.c0) * nh;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t cell = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); cell < ncell;
-       cell += nwarps) {
-    const int64_t g = in.c0 + cell / F, h = cell % F;
+  for (int64_t ci = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); ci < ncell;
+       ci += nwarps) {
+    const int64_t g = in.c0 + ci / nh, h = h0 + ci % nh;
     if (h < g) continue;  // warp-uniform
+    const int64_t cell = (g - in.c0) * F + h;
     const unsigned long long meta = in.meta[cell];
     const bool tg = (meta >> 40) & 1, th = (meta >> 41) & 1, sweep = (meta >> 42) & 1;
     const unsigned long long* pp = in.part + cell * (kSlots * SW);
@@ -752,22 +756,29 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
 }
 
 // rho / p from the exact sums (continuous.py:174-203), one thread per pair.
-__global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64_t hi,
+__host__ __device__ inline int64_t finish_before(int64_t g, int64_t lo, int64_t h0, int64_t h1) {
+  // cells (x, h), x in [lo, g), h in [max(x, h0), h1)
+  int64_t c = 0;
+  const int64_t e0 = g < h0 + 1 ? g : h0 + 1;  // rows x <= h0: h1 - h0 cells each
+  if (e0 > lo && h1 > h0) c += (e0 - lo) * (h1 - h0);
+  const int64_t a = lo > h0 + 1 ? lo : h0 + 1, b = g < h1 ? g : h1;  // rows h0 < x < h1: h1 - x
+  if (b > a) c += (b - a) * h1 - (a + b - 1) * (b - a) / 2;
+  return c;
+}
+
+__global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64_t hi, int64_t h0, int64_t h1,
                                        double* __restrict__ stat, double* __restrict__ pout,
                                        double* __restrict__ rho_out, int* __restrict__ err) {
-  // one thread per triangle cell (g <= h, g in [lo, hi)): no idle lower half
-  auto before = [&](int64_t g) {  // cells of rows [lo, g)
-    return (g - lo) * F - (g * (g - 1) / 2 - lo * (lo - 1) / 2);
-  };
-  const int64_t total = before(hi);
+  // one thread per cell (g <= h, g in [lo, hi), h in [h0, h1)): no idle lower half
+  const int64_t total = finish_before(hi, lo, h0, h1);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = lo, b = hi - 1;  // last row g with before(g) <= t
     while (a < b) {
       const int64_t mid = (a + b + 1) >> 1;
-      if (before(mid) <= t) a = mid;
+      if (finish_before(mid, lo, h0, h1) <= t) a = mid;
       else b = mid - 1;
     }
-    const int64_t g = a, h = g + (t - before(g));
+    const int64_t g = a, h = (g > h0 ? g : h0) + (t - finish_before(g, lo, h0, h1));
     const int64_t cell = g * F + h;
     const long long n = in.n[cell];
     double rho = PS_NAN, p = PS_NAN;
@@ -829,6 +840,8 @@ struct ps_spearman_job {
   int64_t items_cap = 0, items_used = 0;
   int* queues = nullptr;
   int qn = 256, qi = 0;
+  double *stat = nullptr, *p = nullptr, *rho = nullptr;  // device outputs
+  int64_t h_fin = 0;  // columns [lo, h_fin) folded and finished (incremental)
   cudaStream_t home = nullptr;  // allocation stream (frees are ordered on it)
   int nws = 0;                  // incremental launches so far (alternate walk streams)
 };
@@ -876,16 +889,43 @@ static int walk_launch(ps_spearman_job* j, int64_t h0, int64_t h1, int64_t c0, i
   return PS_OK;
 }
 
-static int partials_launch(ps_spearman_job* j, int64_t c0, int64_t c1, cudaStream_t s) {
+static int partials_launch(ps_spearman_job* j, int64_t c0, int64_t c1, cudaStream_t s, int64_t h0 = 0,
+                           int64_t h1 = -1) {
+  if (h1 < 0) h1 = j->a->F;
+  if (h1 <= h0) return PS_OK;
   PairParts pp = j->pp;
   pp.c0 = c0;
-  const int pblocks = (int)std::min<int64_t>(ps_ceil_div((c1 - c0) * j->a->F, 8), (int64_t)ps_state()->num_sms * 32);
-  spearman_partials_kernel<<<pblocks, 256, 0, s>>>(pp, j->a->F, c1, j->ps);
+  const int pblocks = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ps_ceil_div((c1 - c0) * (h1 - h0), 8), (int64_t)ps_state()->num_sms * 32));
+  spearman_partials_kernel<<<pblocks, 256, 0, s>>>(pp, j->a->F, c1, j->ps, h0, h1);
   PS_LAUNCHED();
   return PS_OK;
 }
 
-int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, cudaStream_t s, ps_spearman_job** out) {
+// rho / p of the cells of rows [lo, hi) x columns [h0, h1)
+static int finish_launch(ps_spearman_job* j, int64_t h0, int64_t h1, cudaStream_t s) {
+  const int64_t F = j->a->F, lo = j->lo, hi = j->hi;
+  if (h1 <= h0 || hi <= lo || (!j->stat && !j->p && !j->rho)) return PS_OK;
+  ps_device_state* ds = ps_state();
+  const int64_t cells = finish_before(hi, lo, h0, h1);
+  if (cells <= 0) return PS_OK;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(cells, 128), (int64_t)ds->num_sms * 16));
+  spearman_finish_kernel<<<blocks, 128, 0, s>>>(j->ps, F, lo, hi, h0, h1, j->stat, j->p, j->rho, ds->d_err);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
+// after an incremental walk launch of columns [h0, h1) on stream w: those
+// cells are complete -- fold and finish them on the same stream
+static int fold_finish_columns(ps_spearman_job* j, int64_t h0, int64_t h1, cudaStream_t w) {
+  int rc = partials_launch(j, j->lo, j->hi, w, h0, h1);
+  if (!rc) rc = finish_launch(j, h0, h1, w);
+  if (!rc) j->h_fin = h1;
+  return rc;
+}
+
+int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho, cudaStream_t s,
+                      ps_spearman_job** out) {
   *out = nullptr;
   const int64_t F = a->F;
   lo = std::max<int64_t>(0, lo);
@@ -903,6 +943,10 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, cudaStream_t s, ps_s
   j->lo = lo;
   j->hi = hi;
   j->h_done = lo;
+  j->h_fin = lo;
+  j->stat = stat;
+  j->p = p;
+  j->rho = rho;
   j->smem = smem;
   j->kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
                 : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
@@ -954,11 +998,12 @@ int ps_spearman_walk_upto(ps_spearman_job* j, int64_t h1, cudaStream_t s) {
   // take SMs as walk CTAs retire; the last launch is persistent
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, w, j->grid_max, h1 < j->a->F);
+  if (!rc) rc = fold_finish_columns(j, j->h_done, h1, w);
   j->h_done = h1;
   return rc;
 }
 
-int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cudaStream_t s) {
+int ps_spearman_end(ps_spearman_job* j, cudaStream_t s) {
   int rc = PS_OK;
   const int64_t F = j->a->F, lo = j->lo, hi = j->hi;
   ps_device_state* ds = ps_state();
@@ -970,7 +1015,7 @@ int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cu
   if (getenv("PS_SPEARMAN_GB")) gb_full = j->gb;
   if (j->single) {
     rc = walk_launch(j, j->h_done, F, lo, hi, j->nws ? j->gb : gb_full, s, j->grid_max);
-    if (!rc) rc = partials_launch(j, lo, hi, s);
+    if (!rc) rc = partials_launch(j, lo, hi, s, j->h_fin, F);
   } else {
     for (int64_t c0 = lo; c0 < hi && !rc; c0 += j->rows) {
       const int64_t c1 = std::min<int64_t>(hi, c0 + j->rows);
@@ -978,13 +1023,7 @@ int ps_spearman_end(ps_spearman_job* j, double* stat, double* p, double* rho, cu
       if (!rc) rc = partials_launch(j, c0, c1, s);
     }
   }
-  if (!rc && hi > lo) {
-    ps_device_state* ds = ps_state();
-    const int64_t tri = (hi - lo) * F - (hi * (hi - 1) / 2 - lo * (lo - 1) / 2);
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(tri, 128), (int64_t)ds->num_sms * 16));
-    spearman_finish_kernel<<<blocks, 128, 0, s>>>(j->ps, F, lo, hi, stat, p, rho, ds->d_err);
-    PS_LAUNCHED();
-  }
+  if (!rc) rc = finish_launch(j, j->single ? j->h_fin : 0, F, s);
   if (j->home != s) {  // free in the allocation stream's order (pool reuse across runs)
     PS_CUDA(cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s));
     PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0));
@@ -1015,7 +1054,7 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   ps_device_state* ds = ps_state();
   cudaStream_t home = inc ? ds->walk[0] : s;
   ps_spearman_job* j = nullptr;
-  int rc = ps_spearman_begin(a, lo, hi, home, &j);
+  int rc = ps_spearman_begin(a, lo, hi, stat, p, rho, home, &j);
   if (rc) return rc;
   if (inc && j->single) {
     PS_CUDA(cudaEventRecord(ds->alloc_ev, home));
@@ -1026,10 +1065,11 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
       PS_CUDA(cudaStreamWaitEvent(w, mk.second, 0));
       PS_CUDA(cudaStreamWaitEvent(w, ds->alloc_ev, 0));
       rc = walk_launch(j, j->h_done, h1, j->lo, j->hi, j->gb, w, j->grid_max, h1 < a->F);
+      if (!rc) rc = fold_finish_columns(j, j->h_done, h1, w);
       j->h_done = h1;
     }
   }
-  int rc2 = ps_spearman_end(j, stat, p, rho, s);
+  int rc2 = ps_spearman_end(j, s);
   return rc ? rc : rc2;
 }
 
