@@ -317,7 +317,10 @@ bool ps_presort_pending(const ps_matrix* m) {
 static int presort_in_chunks(ps_matrix* m, cudaStream_t s) {
   ps_device_state* st = ps_state();
   const int64_t step = st->num_sms;
-  if (m->F < 2 * step || getenv("PS_NO_OVERLAP")) return ps_presort_matrix(m, s);
+  // (S > 32767: the walks run one CTA per SM from global orders and their
+  // one-item-per-CTA launches cost more than the presort they hide: config
+  // 5s step 449 ms presorted up front vs 497-779 ms in chunks)
+  if (m->F < 2 * step || m->S > 32767 || getenv("PS_NO_OVERLAP")) return ps_presort_matrix(m, s);
   int rc = ps_presort_begin(m, s);
   if (rc) return rc;
   PS_CUDA(cudaEventRecord(st->aux_ev, s));

@@ -198,6 +198,145 @@ onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
   if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
+// Cluster-pair variant: the two CTAs of a cluster walk the same (unit, K step)
+// range, a unit being two tiles that share an operand -- both in one tile row
+// (same A rows) or both in the last tile column (same B rows).  Each CTA TMA-
+// loads half of the shared operand and multicasts it to both CTAs, plus its
+// own tile's other operand: 48 KB of L2 reads per CTA per K step instead of
+// 64 KB.  A stage is reused only after both CTAs' MMAs released it (the MMA
+// commit arrives on the `empty` barrier of both CTAs).  An unpaired tile runs
+// with a dummy partner that only contributes its half of the shared operand.
+//   unit = (I0, J0, I1, J1); I0 == I1: A shared; I1 < 0: dummy second tile.
+constexpr int THALF = TA_BYTES / 2;  // 128 rows x 128 B
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TTH_WS, 1)
+onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbase, const int4* __restrict__ units,
+                      int64_t nunits, float* __restrict__ C, int64_t ldC) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[TSTAGES], empty[TSTAGES], accfull, accempty;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)tc05::cluster_ctarank();
+  const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;
+  const int64_t total = nunits * nk;
+  const int64_t i0 = total * cl / ncl, i1 = total * (cl + 1) / ncl;
+  auto tile_of = [&](const int4& u, int& I, int& J) -> bool {  // false: dummy
+    I = rank ? u.z : u.x;
+    J = rank ? u.w : u.y;
+    return I >= 0;
+  };
+
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
+  if (tid == 32) {
+    for (int i = 0; i < TSTAGES; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], 2);  // both CTAs' MMA commits
+    }
+    tc05::mbar_init(&accfull, 1);
+    tc05::mbar_init(&accempty, 128);
+    tc05::fence_barrier_init();
+  }
+  if (tid == 4 * 32) tc05::prefetch_tmap(&tmap);
+  tc05::fence_before_sync();
+  tc05::cluster_sync();  // barriers initialised in both CTAs before any multicast
+  tc05::fence_after_sync();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t q = it - i0;
+        const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
+        const int4 u = units[it / nk];
+        const int kx = (kbase + (int)(it % nk)) * TKB;
+        int I, J;
+        const bool own = tile_of(u, I, J);
+        const bool shareA = u.z < 0 || u.x == u.z;
+        if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
+        const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
+        tc05::mbar_arrive_expect_tx(&full[st], own ? TSTAGE_BYTES : TA_BYTES);
+        const int shared_row = (shareA ? u.x : u.y) * TM + rank * 128;
+        tc05::tma_load_2d_mc((shareA ? sa : sb) + rank * THALF, &tmap, kx, shared_row, &full[st], (uint16_t)3);
+        if (own) {
+          const uint32_t od = shareA ? sb : sa;
+          const int orow = (shareA ? J : I) * TM;
+          tc05::tma_load_2d(od, &tmap, kx, orow, &full[st]);
+          tc05::tma_load_2d(od + THALF, &tmap, kx, orow + 128, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc05::idesc_i8(128, TN, true);
+      int seg = 0;
+      for (int64_t it = i0; it < i1; ++it) {
+        const int64_t q = it - i0;
+        const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
+        const int kc = (int)(it % nk);
+        int I, J;
+        const bool own = tile_of(units[it / nk], I, J);
+        const bool first = it == i0 || kc == 0;
+        const bool last = it + 1 == i1 || kc == nk - 1;
+        if (own && first && seg > 0) {  // the epilogue has drained the previous segment
+          tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
+        tc05::fence_after_sync();
+        if (own) {
+          const uint32_t sa = sbase + st * TSTAGE_BYTES, sb = sa + TA_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < TKB / 32; ++kk) {
+            const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+            const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+            tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+            tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * TKB + kk * 32), bd, idesc, acc);
+          }
+        }
+        tc05::commit_mc(&empty[st], (uint16_t)3);
+        if (own && last) {
+          tc05::commit(&accfull);
+          ++seg;
+        }
+      }
+    }
+  } else {
+    // epilogue warps 0-3: one pass per segment of an own tile, in the MMA issuer's order
+    int seg = 0;
+    for (int64_t it = i0; it < i1;) {
+      const int64_t unit = it / nk;
+      const int64_t seg_end = std::min<int64_t>(i1, (unit + 1) * nk);
+      it = seg_end;
+      int I, J;
+      if (!tile_of(units[unit], I, J)) continue;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int64_t r = (int64_t)I * TM + half * 128 + warp * 32 + lane;
+        float* crow = C + r * ldC + (int64_t)J * TN;
+#pragma unroll 1
+        for (int cc = 0; cc < TN / 32; ++cc) {
+          uint32_t v[32];
+          tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            red_add_v4(crow + cc * 32 + j, (float)(int)v[j], (float)(int)v[j + 1], (float)(int)v[j + 2],
+                       (float)(int)v[j + 3]);
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive(&accempty);
+      ++seg;
+    }
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::cluster_sync();  // no CTA leaves while its partner may still multicast / commit into it
+  if (warp == 0) tc05::tmem_dealloc(tmem, 512);
+}
+
 // ----------------------------------------------------------------- epilogue
 __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
   if (o) {
@@ -389,30 +528,88 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
   if (!tl.empty()) {
     PS_CUDA(ps_alloc(&d_tiles, tl.size(), s));
     PS_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, s));
-    PS_CUDA(cudaFuncSetAttribute(onehot_gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTc05Smem));
+    // cluster pairs (default; PS_CHI2_MC=0: one CTA per tile stream)
+    const char* mce = getenv("PS_CHI2_MC");
+    const bool mc = !(mce && mce[0] == '0') && ds->num_sms >= 2;
+    std::vector<int4> un;
+    if (mc) {  // tiles of one row in pairs (A shared); rows' last tiles paired by column (B shared)
+      std::vector<int2> left;
+      for (size_t i = 0; i < tl.size();) {
+        size_t e = i;
+        while (e < tl.size() && tl[e].x == tl[i].x) ++e;
+        size_t k = i;
+        for (; k + 1 < e; k += 2) un.push_back(make_int4(tl[k].x, tl[k].y, tl[k + 1].x, tl[k + 1].y));
+        if (k < e) left.push_back(tl[k]);
+        i = e;
+      }
+      size_t k = 0;
+      for (; k + 1 < left.size(); k += 2) {
+        if (left[k].y == left[k + 1].y)
+          un.push_back(make_int4(left[k].x, left[k].y, left[k + 1].x, left[k + 1].y));
+        else {
+          un.push_back(make_int4(left[k].x, left[k].y, -1, -1));
+          un.push_back(make_int4(left[k + 1].x, left[k + 1].y, -1, -1));
+        }
+      }
+      if (k < left.size()) un.push_back(make_int4(left[k].x, left[k].y, -1, -1));
+    }
+    int4* d_units = nullptr;
+    if (mc) {
+      PS_CUDA(ps_alloc(&d_units, un.size(), s));
+      PS_CUDA(cudaMemcpyAsync(d_units, un.data(), sizeof(int4) * un.size(), cudaMemcpyHostToDevice, s));
+    }
+    PS_CUDA(cudaFuncSetAttribute(mc ? (const void*)onehot_gemm_mc_kernel : (const void*)onehot_gemm_sk_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTc05Smem));
     CUtensorMap map;
-    int rc = make_onehot_map(&map, O, Rp, Sp, TM);
+    int rc = make_onehot_map(&map, O, Rp, Sp, mc ? 128 : TM);
     if (rc) return rc;
     // K phases: the one-hot operand (Rp x Sp bytes) is streamed through L2 in
     // slabs that fit it, all CTAs working inside the same slab (stream-K
     // spreads CTAs over K, which thrashes L2 when O is larger than it)
     const int nk_all = (int)(Sp / TKB);
     const int64_t slab_budget = 96ll << 20;  // L2 is 126 MB
-    int phases = (int)std::max<int64_t>(1, ps_ceil_div(Rp * Sp, slab_budget));
+    // (cluster pairs read 25% less through L2: one pass over K measured
+    // fastest there, 0.187 vs 0.212 ms in two phases at config 3)
+    int phases = (int)std::max<int64_t>(1, ps_ceil_div(Rp * Sp, mc ? 2 * slab_budget : slab_budget));
     if (const char* e = getenv("PS_CHI2_PHASES")) phases = std::max(1, atoi(e));  // tuning override
     phases = std::min(phases, nk_all);
     ps_prof_begin("chi2_gemm", s);
     for (int ph = 0; ph < phases; ++ph) {
       const int kb0 = (int)((int64_t)nk_all * ph / phases), kb1 = (int)((int64_t)nk_all * (ph + 1) / phases);
       const int nk = kb1 - kb0;
-      const int64_t iters = (int64_t)tl.size() * nk;
-      const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
-      onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_tiles, (int64_t)tl.size(),
-                                                                      C, Rp);
+      if (mc) {
+        static int max_clusters = 0;  // co-resident 2-CTA clusters (GPCs may hold an odd SM count)
+        if (!max_clusters) {
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = dim3((unsigned)(ds->num_sms & ~1));
+          lc.blockDim = dim3(TTH_WS);
+          lc.dynamicSmemBytes = kTc05Smem;
+          cudaLaunchAttribute at;
+          at.id = cudaLaunchAttributeClusterDimension;
+          at.val.clusterDim.x = 2;
+          at.val.clusterDim.y = 1;
+          at.val.clusterDim.z = 1;
+          lc.attrs = &at;
+          lc.numAttrs = 1;
+          if (cudaOccupancyMaxActiveClusters(&max_clusters, onehot_gemm_mc_kernel, &lc) != cudaSuccess ||
+              max_clusters <= 0)
+            max_clusters = ds->num_sms / 2;
+          cudaGetLastError();
+        }
+        const int64_t iters = (int64_t)un.size() * nk;
+        const int grid = 2 * (int)std::min<int64_t>(iters, max_clusters);
+        onehot_gemm_mc_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_units, (int64_t)un.size(),
+                                                                        C, Rp);
+      } else {
+        const int64_t iters = (int64_t)tl.size() * nk;
+        const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
+        onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_tiles, (int64_t)tl.size(),
+                                                                        C, Rp);
+      }
+      PS_LAUNCHED();
     }
     ps_prof_end(s);
-    PS_LAUNCHED();
+    ps_free(d_units, s);
   }
   int32_t* d_cat = a->d_cat;
   const int64_t total = (hi - lo) * F;

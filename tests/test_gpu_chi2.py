@@ -73,3 +73,20 @@ def test_chi2_config3_slice(oracle):
     mat = ps.make_matrix(c["a"], "categorical", na_sentinel=workloads.SENTINEL)
     req = ps.TestRequest("chi2", OUTS)
     _check(ps.run(req, mat), oracle.oracle_run(req, mat))
+
+
+@pytest.mark.parametrize("mc,phases", [("1", None), ("1", "3"), ("0", None)])
+@pytest.mark.parametrize("F", [150, 200])
+def test_chi2_cluster_pairs(oracle, monkeypatch, mc, phases, F):
+    """Contingency tables from the 2-CTA cluster GEMM (tile pairs sharing a
+    multicast operand, an unpaired tile with a dummy partner) equal the
+    single-CTA stream-K GEMM's and the oracle's, for any number of K phases.
+    10 levels per feature: F = 150 -> 6 tile rows (three leftover tiles: one
+    column pair, one dummy partner), F = 200 -> 8 tile rows (two column pairs)."""
+    monkeypatch.setenv("PS_CHI2_MC", mc)
+    if phases:
+        monkeypatch.setenv("PS_CHI2_PHASES", phases)
+    raw = workloads.simulate(F, 3000, "categorical", categories=10, na_ratio=0.15, seed=F + 1)
+    mat = ps.make_matrix(raw, "categorical")
+    req = ps.TestRequest("chi2", OUTS)
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
