@@ -38,9 +38,20 @@ __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, co
   const int f = row_feat[r];
   const uint8_t lev = (uint8_t)row_level[r];
   const uint8_t* c = codes + f * ldc;
-  for (int64_t s = threadIdx.x * 16; s < Sp; s += blockDim.x * 16) {
-    uint4 cv = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-    if (s < ldc) cv = *reinterpret_cast<const uint4*>(c + s);
+  constexpr int kU = 4;  // 16-byte loads in flight per thread
+  for (int64_t s0 = threadIdx.x * 16; s0 < Sp; s0 += blockDim.x * 16 * kU) {
+  uint4 cvu[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t s = s0 + (int64_t)u * blockDim.x * 16;
+    cvu[u] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    if (s < ldc) cvu[u] = *reinterpret_cast<const uint4*>(c + s);
+  }
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int64_t s = s0 + (int64_t)u * blockDim.x * 16;
+    if (s >= Sp) break;
+    const uint4 cv = cvu[u];
     const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
     uint32_t w[4];
 #pragma unroll
@@ -55,6 +66,7 @@ __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, co
       w[q] = v;
     }
     *reinterpret_cast<uint4*>(out + s) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
   }
 }
 
