@@ -182,13 +182,13 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
 }
 
-// Exact warp sum of 64-bit lane values: three 22-bit slices through the
-// integer warp-reduce unit (each slice sum < 2^27).
+// Exact warp sum of 64-bit lane values below 2^54 (every walk sum: at most
+// 2048 words x (2S)^2 < 2^45 per lane): two 27-bit slices through the integer
+// warp-reduce unit (each slice sum < 2^32).
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
-  const uint32_t s0 = __reduce_add_sync(PS_FULL, (uint32_t)(x & 0x3FFFFFu));
-  const uint32_t s1 = __reduce_add_sync(PS_FULL, (uint32_t)((x >> 22) & 0x3FFFFFu));
-  const uint32_t s2 = __reduce_add_sync(PS_FULL, (uint32_t)(x >> 44));
-  return (unsigned long long)s0 + ((unsigned long long)s1 << 22) + ((unsigned long long)s2 << 44);
+  const uint32_t s0 = __reduce_add_sync(PS_FULL, (uint32_t)(x & 0x7FFFFFFu));
+  const uint32_t s1 = __reduce_add_sync(PS_FULL, (uint32_t)(x >> 27));
+  return (unsigned long long)s0 + ((unsigned long long)s1 << 27);
 }
 
 // sum_{k=1..n} (2k)^2: the rank-square total of a tie-free walk
