@@ -129,6 +129,7 @@ class ClockSampler:
         self.rows = []
         self.proc = None
         self.thread = None
+        self.first = 0  # rows before mark() predate the timed region
 
     def start(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -150,6 +151,9 @@ class ClockSampler:
         self.thread = threading.Thread(target=reader, daemon=True)
         self.thread.start()
 
+    def mark(self):
+        self.first = len(self.rows)
+
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -161,6 +165,7 @@ class ClockSampler:
             self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
+        self.rows = self.rows[self.first:]
         sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -372,6 +377,12 @@ def main():
             db.close()
 
     lib = _lib.load()
+    # nvidia-smi is started before the warm-up: its start-up (NVML init) can
+    # stall this process's CUDA calls for ~15 ms; only rows sampled inside the
+    # timed region are kept (mark)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.5)
     for _ in range(args.warmup):
         step()
     blocks.sync(stream)
@@ -379,8 +390,7 @@ def main():
     lib.ps_profile_enable(1)
     _lib.profile_collect(ROOF[test][3])
     lib.ps_reset_kernel_launches()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
