@@ -54,14 +54,15 @@ __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, co
     const uint4 cv = cvu[u];
     const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
     uint32_t w[4];
+    const uint32_t lev4 = 0x01010101u * lev;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int64_t ss = s + q * 4 + b;
-        const uint8_t code = ss < S ? (uint8_t)(cw[q] >> (8 * b)) : 0xFF;
-        v |= (code == lev ? 1u : 0u) << (8 * b);
+      // byte-wise code == lev (SIMD compare: 0xFF per equal byte) -> 0/1 bytes
+      uint32_t v = __vcmpeq4(cw[q], lev4) & 0x01010101u;
+      const int64_t sq = s + q * 4;
+      if (sq + 4 > S) {  // samples past S are absent
+        const int64_t keep = S - sq;
+        v = keep <= 0 ? 0u : v & (0xFFFFFFFFu >> (8 * (4 - keep)));
       }
       w[q] = v;
     }

@@ -29,7 +29,7 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
   // kU rows of the loop's loads in flight per thread (one 8-B load per thread
   // at a time leaves HBM mostly idle); processed in the original order, so the
   // pivot sum is unchanged
-  constexpr int kU = 4;
+  constexpr int kU = 8;
   for (int64_t base0 = (int64_t)warp * 32; base0 < S; base0 += (int64_t)kPrepThreads * kU) {
   double vu[kU];
 #pragma unroll
