@@ -446,9 +446,14 @@ __global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, c
                                           const double* __restrict__ vals, int64_t ld,
                                           const uint32_t* __restrict__ vmask, int64_t W, const int2* __restrict__ items,
                                           int n_items, int kslots, GroupPart* __restrict__ parts) {
-  // one warp per (cell, group): the lanes load each 32-sample word's values
-  // (coalesced) and lane 0 accumulates the group's present samples in order
+  // one warp per (cell, group), 1024 samples per round: the lanes compact the
+  // group's jointly present values of the round into shared memory in sample
+  // order (coalesced loads), then lane 0 runs the reference's sequential
+  // one-pass sums over them -- a chain of dependent fp64 adds only
+  __shared__ double sbuf[4][1024];  // blockDim.x == 128
+  double* buf = sbuf[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
   const int64_t total = (int64_t)n_items * kslots;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += nwarps) {
@@ -463,24 +468,42 @@ __global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, c
     double sum = 0.0, ssq = 0.0;
     for (int64_t w0 = 0; w0 < W; w0 += 32) {
       const uint32_t mw = w0 + lane < W ? oh[w0 + lane] & mh[w0 + lane] : 0u;
-      // values of the next 4 words in flight while the current one is summed
-      double pre[4];
+      const uint32_t c = __popc(mw);
+      uint32_t x = c;  // inclusive scan of the words' counts
 #pragma unroll
-      for (int u = 0; u < 4; ++u) pre[u] = w0 + u < W ? xv[(w0 + u) * 32 + lane] : 0.0;
-#pragma unroll 4
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t excl = x - c, tot = __shfl_sync(PS_FULL, x, 31);
+#pragma unroll 8
       for (int q = 0; q < 32; ++q) {
-        uint32_t m = __shfl_sync(PS_FULL, mw, q);
-        const double vl = pre[q & 3];
-        pre[q & 3] = (q + 4 < 32 && w0 + q + 4 < W) ? xv[(w0 + q + 4) * 32 + lane] : 0.0;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1u;
-          const double v = __shfl_sync(PS_FULL, vl, b);
-          ++n;
+        const uint32_t m = __shfl_sync(PS_FULL, mw, q);
+        const uint32_t o = __shfl_sync(PS_FULL, excl, q);
+        if ((m >> lane) & 1u) buf[o + __popc(m & lt)] = xv[(w0 + q) * 32 + lane];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t i = 0;
+        for (; i + 4 <= tot; i += 4) {
+          const double v0 = buf[i], v1 = buf[i + 1], v2 = buf[i + 2], v3 = buf[i + 3];
+          sum += v0;
+          ssq += v0 * v0;
+          sum += v1;
+          ssq += v1 * v1;
+          sum += v2;
+          ssq += v2 * v2;
+          sum += v3;
+          ssq += v3 * v3;
+        }
+        for (; i < tot; ++i) {
+          const double v = buf[i];
           sum += v;
           ssq += v * v;
         }
+        n += tot;
       }
+      __syncwarp();
     }
     if (lane == 0) parts[t] = GroupPart{n, sum, ssq};
   }
