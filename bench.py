@@ -1,25 +1,37 @@
 #!/usr/bin/env python
 """Benchmark of the all-pairs test engine on B200 (driver contract: one JSON line).
 
-Metric (BASELINE.json): variable-pairs x samples per second for one test on one
-BASELINE config; homogeneous pairs P = F(F-1)/2, mixed pairs P = F_C * F_Q,
-samples = all samples S.  Default workload: configs[1] (config 2, Spearman
-1000 x 10^4), the config the metric is quoted on.
+Metric (BASELINE.json): variable-pairs x samples per second per test
+(Pearson, Spearman, chi-squared) at 1/2/4/8 B200.  Homogeneous pairs
+P = F(F-1)/2, mixed pairs P = F_C * F_Q, samples = all samples S.
 
-* value   -- device-resident: inputs already in HBM; one step = prepare
-             (validity bits, presort) + the test's block over the full range +
-             the config's adjustments, all on the device.  CUDA events on the
-             launching stream, L2 flushed (512 MiB write) between steps outside
-             the events; max over ranks.
-* e2e     -- the public API ``run(TestRequest, DataMatrix)`` from host numpy
-             inputs to host ResultSet (H2D + D2H inside the timed region).
+Default workload: config 5 -- the scale run the 1/2/4/8-GPU metric is defined
+on (Pearson 20,000 x 10^5 fp64, 30% MCAR, global BH; the largest config and
+it fits one B200).  Its Spearman (config 5s, 2000 x 5*10^4) and a chi-squared
+(config 3, 500 x 5*10^4) leg run in the same invocation and are reported under
+``legs``.  ``--config 1|2|3|4|5s`` measures another config alone.
+
+* value   -- device-resident: inputs already in HBM (N > 1: each rank holds
+             its 1/N row shard); one step = [N > 1: NCCL all-gather of the
+             input shards] + prepare (validity bits, presort) + the test's
+             block over the rank's range + [N > 1: all-gather of the packed
+             p cells] + the config's adjustments, all on the device.  CUDA
+             events on the launching stream, L2 flushed (512 MiB write)
+             between steps outside the events; max over ranks.
+* e2e     -- through the public API from host numpy: ``run()`` at N = 1,
+             ``dist.sharded_run(..., assemble="owned")`` at N > 1 (each rank
+             H2Ds its shard, gets its own rows back); H2D + D2H inside the
+             timed region, max over ranks.
 * roofline-- dominant kernel, algorithmic bytes/flops per launch / its
-             event-timed duration, against the measured peak.
-* cpu_baseline -- the C oracle port (oracle/, OpenMP, all host cores) on a
-             bounded slice of the same inputs.
+             event-timed busy time, against the measured peak.
+* cpu_baseline -- the C oracle port (oracle/, OpenMP, all host cores): the
+             reference's block kernel timed on a bounded slice of the same
+             inputs (triangle rows from row 0), extrapolated by pair count,
+             plus the one-off presort for rank tests.
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port; the
-reference itself is numba-in-Python and cannot travel) with all host threads.
+reference itself is numba-in-Python and cannot travel) with all host threads,
+on the same config dict; under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -63,6 +75,7 @@ OUTPUTS = {
     5: ("stat", "p", "p_bonferroni", "p_bh"),
     "5s": ("rho", "p", "p_bonferroni", "p_bh"),
 }
+LEGS = {5: [("5s", "spearman"), (3, "chi2")]}
 
 
 def parse_config(v: str):
@@ -90,17 +103,89 @@ def device_peaks(peaks: dict) -> dict:
     out["dmma_tflops"] = mb.get("dmma_tflops", 37.0)
     out["imma_tops"] = mb.get("imma_mma_sync_tops", 1127.0)
     out["tcgen05_i8_tops"] = mb.get("tcgen05_i8_tops", 4500.0)  # measured: tools/microbench/tc05_peak.cu
-    # SMEM crossbar: 148 SMs x 128 B/clk at the max SM clock
-    out["smem_gbs"] = 148 * 128 * out["sm_max_mhz"] * 1e6 / 1e9
+    # SMEM crossbar: 148 SMs x 128 B/clk at the max SM clock (measured copy
+    # throughput, when the microbenchmark ran: profiles/peaks_r0*.json)
+    out["smem_gbs"] = mb.get("smem_gbs", 148 * 128 * out["sm_max_mhz"] * 1e6 / 1e9)
+    out["smem_source"] = "measured" if "smem_gbs" in mb else "derived 148 x 128 B/clk x max clock"
     return out
 
 
-def pair_count(cfg: dict, test: str) -> int:
-    if test in ("pearson", "spearman", "chi2"):
-        F = cfg["F"]
-        return F * (F - 1) // 2
-    rows = cfg["two_level_rows"].size if test in ("ttest", "mwu") else cfg["F"]
-    return rows * cfg["Fq"]
+# ---------------------------------------------------------------- workloads
+
+class Workload:
+    """One (config, test) workload as THIS rank sees it: host row shards of
+    the inputs (rank r holds rows row_shards(F, world)[r]) plus the metadata
+    of the whole matrices.  Config 5 generates only the rank's rows."""
+
+    def __init__(self, cfg_key, test: str, rank: int, world: int):
+        from paper_2505_00448_b200 import dist
+
+        self.key, self.test = cfg_key, test
+        if cfg_key == 5:
+            F, S = 20000, 100000
+            _, sh = dist.row_shards(F, world)
+            r0, r1 = sh[rank]
+            self.a_rows = workloads.config5_rows(F, S, r0, r1)
+            self.desc = f"pearson scale {F}x{S} 30% MCAR"
+            self.Fa, self.Fb, self.S = F, None, S
+            self.kind_a, self.kind_b = "continuous", None
+            self.a_full = self.a_rows if world == 1 else None
+            self.b_full = None
+            self.cat_a = None
+        else:
+            cfg = workloads.config(cfg_key)
+            a, b = cfg["a"], cfg["b"]
+            ka, kb = cfg["kind_a"], cfg["kind_b"]
+            if test in ("ttest", "mwu"):
+                a = np.ascontiguousarray(a[cfg["two_level_rows"]])
+                ka = "dichotomous"
+            self.desc = cfg["desc"]
+            self.kind_a, self.kind_b = ka, kb
+            self.a_full, self.b_full = a, b
+            self.Fa, self.Fb, self.S = a.shape[0], (b.shape[0] if b is not None else None), a.shape[1]
+            self.cat_a = label_counts(a) if ka != "continuous" else None
+            _, sh = dist.row_shards(self.Fa, world)
+            self.a_rows = a[sh[rank][0]:sh[rank][1]]
+        self.b_rows = None
+        if self.b_full is not None:
+            _, sh = dist.row_shards(self.Fb, world)
+            self.b_rows = self.b_full[sh[rank][0]:sh[rank][1]]
+        self.r0_a = dist.row_shards(self.Fa, world)[1][rank][0]
+        self.r0_b = dist.row_shards(self.Fb, world)[1][rank][0] if self.Fb else 0
+        self.outputs = OUTPUTS[cfg_key] if cfg_key != 4 else ("stat", "p", "p_bh")
+
+    @property
+    def homogeneous(self) -> bool:
+        return self.test in ("pearson", "spearman", "chi2")
+
+    @property
+    def pairs(self) -> int:
+        if self.homogeneous:
+            return self.Fa * (self.Fa - 1) // 2
+        return self.Fa * self.Fb
+
+    @property
+    def shape(self):
+        return (self.Fa, self.Fa) if self.homogeneous else (self.Fa, self.Fb)
+
+    def sharded_inputs(self):
+        from paper_2505_00448_b200 import dist
+
+        sa = dist.ShardedInput(self.a_rows, self.r0_a, self.Fa, self.S, self.kind_a, workloads.SENTINEL, self.cat_a)
+        sb = None
+        if self.b_rows is not None:
+            sb = dist.ShardedInput(self.b_rows, self.r0_b, self.Fb, self.S, self.kind_b, workloads.SENTINEL, None)
+        return sa, sb
+
+    def datamatrices(self):
+        import paper_2505_00448_b200 as ps
+
+        if getattr(self, "_mats", None) is None:
+            ma = ps.make_matrix(self.a_full, self.kind_a, na_sentinel=workloads.SENTINEL)
+            mb = (ps.make_matrix(self.b_full, self.kind_b, na_sentinel=workloads.SENTINEL)
+                  if self.b_full is not None else None)
+            self._mats = (ma, mb)
+        return self._mats
 
 
 def label_counts(raw: np.ndarray) -> np.ndarray:
@@ -112,13 +197,11 @@ def label_counts(raw: np.ndarray) -> np.ndarray:
     return out
 
 
-def build_inputs(cfg: dict, test: str):
-    """Host raw matrices (a, b) for `test`, plus kinds and category counts."""
-    a, b = cfg["a"], cfg["b"]
-    if test in ("ttest", "mwu"):
-        a = np.ascontiguousarray(a[cfg["two_level_rows"]])
-        return a, b, "dichotomous", "continuous"
-    return a, b, cfg["kind_a"], cfg["kind_b"]
+def config_dict(wl: Workload, world: int) -> dict:
+    """The config object of the JSON line -- identical for both arms."""
+    return {"workload": wl.desc, "config": wl.key, "test": wl.test, "pairs": wl.pairs, "samples": wl.S,
+            "outputs": list(wl.outputs), "l2": "flushed (512 MiB write) between steps",
+            "parallelism": f"pair-shard x{world}"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -179,223 +262,231 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- CPU legs
 
-def cpu_baseline(cfg: dict, test: str, target_s: float, mat_a, mat_b, t_variant="student"):
-    """Oracle port (C + OpenMP, all host cores) on a bounded slice of rows."""
+def cpu_baseline(wl: Workload, target_s: float, mat_a, mat_b, t_variant="student"):
+    """The reference's block kernel (C oracle port, OpenMP on all host cores)
+    on a bounded slice of the workload, extrapolated by pair count.
+
+    Homogeneous tests run triangle rows [0, k) (the longest rows first); mixed
+    tests run whole work units (label rows x every feature for ttest / anova,
+    continuous features for mwu / kruskal).  The one-off presort of the rank
+    tests (engine.py:379-400) is timed separately and added once."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import pyoracle
 
     pyoracle.build()
     threads = os.cpu_count() or 1
-    S = mat_a.n_samples
-    if test in ("pearson", "spearman", "chi2"):
-        F = mat_a.n_features
-        total_pairs = F * (F - 1) // 2
+    test, S = wl.test, wl.S
+    prep, run = pyoracle.block_runner(test, mat_a, mat_b, wanted=("stat", "p"), t_variant=t_variant,
+                                      threads=threads)
+    if wl.homogeneous:
+        F = wl.Fa
+        units_total, unit_pairs = F, None
 
-        def slice_pairs(k):  # rows [0, k) of the triangle, off-diagonal pairs
+        def pairs_of(k):  # off-diagonal pairs of triangle rows [0, k)
             return k * F - k * (k + 1) // 2
 
-        def run_rows(k):
-            t0 = time.perf_counter()
-            pyoracle.compute(test, mat_a, None, wanted={"stat", "p"}, threads=threads, lo=0, hi=k)
-            return time.perf_counter() - t0
-
-        k = max(1, F // 100)
-        dt = run_rows(k)
-        while dt < 0.5 and k < F:
-            k = min(F, k * 4)
-            dt = run_rows(k)
-        rate = slice_pairs(k) * S / dt
-        k2 = k
-        want_pairs = rate * target_s / S
-        while k2 < F and slice_pairs(k2) < want_pairs:
-            k2 += max(1, F // 200)
-        k2 = min(k2, F)
-        dt = run_rows(k2)
-        pairs = slice_pairs(k2)
-        sample = f"triangle rows [0,{k2}) of {F}: {pairs} of {total_pairs} pairs x {S} samples"
+        def run_units(k):
+            return run(0, k)
     else:
-        Fq = mat_b.n_features
-        rows = mat_a.n_features
-        per_unit = rows  # pairs per continuous feature (mwu/kruskal) or per grid row
+        if test in ("mwu", "kruskal"):
+            units_total = wl.Fb
 
-        def run_units(u):
-            t0 = time.perf_counter()
-            if test in ("mwu", "kruskal"):
-                pyoracle.compute(test, mat_a, mat_b, wanted={"stat", "p"}, threads=threads, lo=0, hi=u)
-            else:
-                pyoracle.compute(test, mat_a, mat_b, wanted={"stat", "p"}, threads=threads, lo=0,
-                                 hi=u * Fq, t_variant=t_variant)
-            return time.perf_counter() - t0
+            def pairs_of(k):
+                return k * wl.Fa
 
-        units_total = Fq if test in ("mwu", "kruskal") else rows
-        u = max(1, units_total // 100)
-        dt = run_units(u)
-        while dt < 0.5 and u < units_total:
-            u = min(units_total, u * 4)
-            dt = run_units(u)
-        pairs_u = per_unit if test in ("mwu", "kruskal") else Fq
-        rate = u * pairs_u * S / dt
-        u2 = min(units_total, max(u, int(rate * target_s / (pairs_u * S))))
-        dt = run_units(u2)
-        pairs = u2 * pairs_u
-        sample = f"{u2} of {units_total} work units: {pairs} pairs x {S} samples"
-    value = pairs * S / dt
-    return {"value": value, "unit": "pair-samples/s", "cores": threads, "kind": "port",
-            "sample": sample + f" ({dt:.1f} s)"}
+            def run_units(k):
+                return run(0, k)
+        else:
+            units_total = wl.Fa
+
+            def pairs_of(k):
+                return k * wl.Fb
+
+            def run_units(k):
+                return run(0, k * wl.Fb)
+    # at least one unit per thread: the reference (and the port) parallelise
+    # over triangle rows / units, so fewer units would idle cores
+    k = min(units_total, threads)
+    dt = run_units(k)
+    while dt < 0.3 and k < units_total:
+        k = min(units_total, k * 2)
+        dt = run_units(k)
+    rate = pairs_of(k) / dt
+    k2 = k
+    while k2 < units_total and pairs_of(k2) < rate * target_s:
+        k2 = min(units_total, max(k2 + 1, int(k2 * 1.25)))
+    if k2 != k:
+        dt = run_units(k2)
+    total_s = prep + dt * wl.pairs / max(1, pairs_of(k2))
+    value = wl.pairs * S / total_s
+    what = "triangle rows" if wl.homogeneous else ("continuous features" if test in ("mwu", "kruskal")
+                                                   else "label rows")
+    sample = (f"{what} [0,{k2}) of {units_total}: {pairs_of(k2)} of {wl.pairs} pairs x {S} samples in {dt:.2f} s"
+              + (f" + presort {prep:.2f} s" if prep > 0 else "") + ", extrapolated by pair count")
+    return {"value": value, "unit": "pair-samples/s", "cores": threads, "kind": "port", "sample": sample,
+            "sample_seconds": dt}
 
 
-def run_reference_arm(args, cfg, test):
-    import paper_2505_00448_b200 as ps
+def run_reference_arm(args):
+    import paper_2505_00448_b200 as ps  # noqa: F401  (make_matrix, no device use)
 
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    a, b, ka, kb = build_inputs(cfg, test)
-    mat_a = ps.make_matrix(a, ka, na_sentinel=workloads.SENTINEL)
-    mat_b = ps.make_matrix(b, kb, na_sentinel=workloads.SENTINEL) if b is not None else None
+    cfg_key = args.config
+    test = args.test or ("pearson" if cfg_key in (1, 5) else workloads.config(cfg_key)["tests"][0]
+                         if cfg_key != "5s" else "spearman")
+    wl = Workload(cfg_key, test, 0, 1)
+    mat_a, mat_b = wl.datamatrices()
     per_step = float(os.environ.get("REF_STEP_SECONDS", "6"))
-    vals = []
-    base = None
+    vals, base = [], None
     for i in range(args.warmup + args.steps):
-        base = cpu_baseline(cfg, test, per_step, mat_a, mat_b)
+        base = cpu_baseline(wl, per_step, mat_a, mat_b)
         if i >= args.warmup:
             vals.append(base["value"])
     value = statistics.mean(vals)
     base["value"] = value
+    legs = {}
+    if not args.no_legs:
+        for key, t in LEGS.get(cfg_key, []):
+            lw = Workload(key, t, 0, 1)
+            la, lb = lw.datamatrices()
+            b = cpu_baseline(lw, 3.0, la, lb)
+            legs[f"{t} (config {key})"] = {"value": b["value"], "unit": "pair-samples/s", "cpu_baseline": b,
+                                           "config": config_dict(lw, world)}
     line = {
-        "metric": f"pair-samples/s ({test}, config {args.config})",
+        "metric": f"pair-samples/s ({test}, config {cfg_key})",
         "impl": "reference",
         "value": value,
         "unit": "pair-samples/s",
-        "n_gpus": args.gpus,
+        "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "higher_is_better": True,
         "dtype": "f64",
-        "data": "synthetic (seeded BASELINE recipe, SURVEY 8d)",
-        "config": {"workload": cfg["desc"], "config": args.config, "test": test},
+        "data": "synthetic (seeded BASELINE recipe, SURVEY 8d; CHRIS cohort unavailable)",
+        "config": config_dict(wl, world),
         "cpu_baseline": base,
-        "e2e": {"value": value, "unit": "pair-samples/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": "pair-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "legs": legs,
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- GPU arm
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=parse_config, default=2)
-    ap.add_argument("--test", default=None, help="test within a multi-test config (config 4)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-warmup", type=int, default=3)
-    args = ap.parse_args()
+def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):
+    if not kern_n:
+        return None
+    test, S = wl.test, wl.S
+    bound, unit, per_ps, kname = ROOF[test]
+    launch_ms = kern_ms / steps  # kernel busy ms per step (all of its launches)
+    units = wl.pairs * S / world
+    if test == "chi2":
+        ks = wl.cat_a.astype(np.float64)
+        per_launch = (ks.sum() ** 2 - (ks * ks).sum()) * S / world  # 2 k_g k_h over g < h
+        peak, achieved = peaks["tcgen05_i8_tops"], None
+        desc = "2 k_g k_h int8 ops (tcgen05 kind::i8)"
+        achieved = per_launch / (launch_ms / 1e3) / 1e12
+    elif test == "anova":
+        per_launch = 4.0 * float(wl.cat_a.sum()) * wl.Fb * S / world
+        peak = peaks["dmma_tflops"]
+        achieved = per_launch / (launch_ms / 1e3) / 1e12
+        desc = "4 k_g FP64 flops"
+    elif bound == "tensor":
+        per_launch = per_ps * units
+        peak = peaks["dmma_tflops"]
+        achieved = per_launch / (launch_ms / 1e3) / 1e12
+        desc = f"{per_ps:g} FP64 flops"
+    else:
+        per_launch = per_ps * units
+        peak = peaks["smem_gbs"]
+        achieved = per_launch / (launch_ms / 1e3) / 1e9
+        desc = f"{per_ps:g} B smem ({peaks['smem_source']})"
+    traffic = None
+    for tf in sorted(PROFILES.glob("traffic_r0*.json"), reverse=True):
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{wl.key}:{test}")
+        except Exception:
+            traffic = None
+        if traffic is not None:
+            break
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": traffic, "kernel": kname, "launch_ms": launch_ms, "launches_per_step": kern_n / steps,
+            "work_per_pair_sample": desc}
 
-    cfg = workloads.config(args.config)
-    test = args.test or cfg["tests"][0]
-    if args.impl == "reference":
-        run_reference_arm(args, cfg, test)
-        return
 
+def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int, local: int, peaks: dict,
+                   clocks=None):
+    """Device-resident steps; returns (ms_per_step, roofline, launches, clock summary)."""
     import torch
+
     import paper_2505_00448_b200 as ps
     from paper_2505_00448_b200 import _lib, blocks, dist
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    _lib.check(_lib.load().ps_set_device(local))
-    if world > 1:
-        import torch.distributed as tdist
-
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    a, b, ka, kb = build_inputs(cfg, test)
-    sentinel = workloads.SENTINEL
-    S = a.shape[1]
-    cat_a = label_counts(a) if ka != "continuous" else None
-    outputs = OUTPUTS[args.config]
-    if args.config == 4:
-        outputs = ("stat", "p", "p_bh")
-    P = pair_count(cfg, test)
-    work_units = P * S
-    peaks = device_peaks(load_peaks())
-
+    lib = _lib.load()
+    test, S = wl.test, wl.S
     stream = torch.cuda.current_stream()
+    dev = torch.device("cuda", local)
     Sp = ((S + 31) // 32) * 32
-
-    def to_dev(x):
-        t = torch.zeros((x.shape[0], Sp), dtype=torch.float64, device="cuda")
-        t[:, :S] = torch.from_numpy(x)
-        return t
-
-    xa = to_dev(a)
-    xb = to_dev(b) if b is not None else None
-    plan = dist.plan(test, a.shape[0], None if b is None else b.shape[0], world)
-    lo, hi = plan[rank]
-    homog = test in ("pearson", "spearman", "chi2")
-    shape = (a.shape[0], a.shape[0]) if homog else (a.shape[0], b.shape[0])
+    ca, _ = dist.row_shards(wl.Fa, world)
+    shard_a = dist.upload_rows(wl.a_rows, 0, wl.a_rows.shape[0], ca if world > 1 else wl.Fa, Sp, dev, stream)
+    shard_b = None
+    if wl.b_rows is not None:
+        cb, _ = dist.row_shards(wl.Fb, world)
+        shard_b = dist.upload_rows(wl.b_rows, 0, wl.b_rows.shape[0], cb if world > 1 else wl.Fb, Sp, dev, stream)
+    blocks.sync(stream)
+    ranges = dist.plan(test, wl.Fa, wl.Fb, world)
+    lo, hi = ranges[rank]
+    shape = wl.shape
     n_canon = 2 + len(ps.EFFECTS_BY_TEST[test])
-    want = {"stat"} | {"p"}
-    outs = [torch.empty(shape, dtype=torch.float64, device="cuda") if i < 2 else None
-            for i in range(n_canon)]
+    outs = [torch.empty(shape, dtype=torch.float64, device=dev) if i < 2 else None for i in range(n_canon)]
+    if test == "chi2" and "cramers_v" in wl.outputs:
+        outs[3] = torch.empty(shape, dtype=torch.float64, device=dev)
     adj_methods = [m for m, k in (("bonferroni", "p_bonferroni"), ("bh", "p_bh"), ("by", "p_by"))
-                   if k in outputs]
-    if test == "chi2":
-        outs[3] = torch.empty(shape, dtype=torch.float64, device="cuda")  # cramers_v
-    adj_out = torch.empty(shape, dtype=torch.float64, device="cuda") if adj_methods else None
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    del want
+                   if k in wl.outputs]
+    adj_outs = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in adj_methods]
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
+        xa = dist.gather_input(shard_a, wl.Fa)          # NCCL all-gather of the shards (N > 1)
+        xb = dist.gather_input(shard_b, wl.Fb) if shard_b is not None else None
         if world > 1 and test == "spearman":
             # each rank presorts 1/world of the features; NCCL all-gathers the tables
-            da = blocks.DeviceMatrix(xa, ka, sentinel, cat_a, n_samples=S, stream=stream)
+            da = blocks.DeviceMatrix(xa, wl.kind_a, workloads.SENTINEL, wl.cat_a, n_samples=S, stream=stream)
             da.presort_sharded(rank, world, stream=stream)
         else:
-            da = blocks.DeviceMatrix(xa, ka, sentinel, cat_a, n_samples=S,
+            da = blocks.DeviceMatrix(xa, wl.kind_a, workloads.SENTINEL, wl.cat_a, n_samples=S,
                                      presort=test == "spearman", stream=stream)
         db = None
         if xb is not None:
             rank_walk = test in ("mwu", "kruskal")
-            db = blocks.DeviceMatrix(xb, kb, sentinel, None, n_samples=S,
+            db = blocks.DeviceMatrix(xb, wl.kind_b, workloads.SENTINEL, None, n_samples=S,
                                      presort=rank_walk and world == 1, stream=stream)
             if rank_walk and world > 1:  # the walk only touches this rank's features
                 db.presort_rows_only(lo, hi, stream=stream)
         blocks.block(test, da, db, lo, hi, outs, stream=stream)
         if adj_methods:
-            dist.adjust_gathered(test, outs[1], shape, plan, adj_methods, adj_out, stream)
+            dist.exchange_adjust(test, outs[1], shape, ranges, adj_methods, adj_outs, stream)
         da.close()
         if db is not None:
             db.close()
 
-    lib = _lib.load()
-    # nvidia-smi is started before the warm-up: its start-up (NVML init) can
-    # stall this process's CUDA calls for ~15 ms; only rows sampled inside the
-    # timed region are kept (mark)
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.5)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     blocks.sync(stream)
     torch.cuda.synchronize()
     lib.ps_profile_enable(1)
     _lib.profile_collect(ROOF[test][3])
     lib.ps_reset_kernel_launches()
-    clocks.mark()
+    if clocks is not None:
+        clocks.mark()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -411,110 +502,153 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     launches = int(lib.ps_kernel_launches())
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks is not None else None
     lib.ps_profile_enable(0)
     # busy time of the dominant kernel (union over its launches: incremental
     # launches of one step run concurrently on several streams)
     kern_ms, kern_n = _lib.profile_collect_union(ROOF[test][3])
     total_ms = sum(times)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    value = work_units / (ms_per_step / 1e3)
+        total_ms, kern_ms = float(t[0].item()), float(t[1].item())
+    del outs, adj_outs, flush, shard_a, shard_b
+    torch.cuda.empty_cache()
+    return total_ms / steps, roofline(wl, kern_ms, kern_n, steps, world, peaks), launches, clk
 
-    # ---------------- roofline of the dominant kernel
-    bound, unit, per_ps, _kname = ROOF[test]
-    roof = None
-    if kern_n:
-        launch_ms = kern_ms / args.steps  # kernel busy ms per step (all of its launches)
-        units_per_launch = work_units / world
-        if test == "chi2":
-            ks = cat_a
-            ksum = float(ks.sum())
-            per_launch = 2.0 * (ksum * ksum - float((ks * ks).sum())) / 2.0 * S / world
-            peak = peaks["tcgen05_i8_tops"]
-            achieved = per_launch / (launch_ms / 1e3) / 1e12
-            per_ps_desc = "2 k_g k_h int8 ops (tcgen05 kind::i8)"
-        elif test == "anova":
-            ksum = float(cat_a.sum())
-            per_launch = 4.0 * ksum * b.shape[0] * S / world
-            peak = peaks["dmma_tflops"]
-            achieved = per_launch / (launch_ms / 1e3) / 1e12
-            per_ps_desc = "4 k_g FP64 flops"
-        elif bound == "tensor":
-            per_launch = per_ps * units_per_launch
-            peak = peaks["dmma_tflops"]
-            achieved = per_launch / (launch_ms / 1e3) / 1e12
-            per_ps_desc = f"{per_ps:g} FP64 flops"
-        else:
-            per_launch = per_ps * units_per_launch
-            peak = peaks["smem_gbs"]
-            achieved = per_launch / (launch_ms / 1e3) / 1e9
-            per_ps_desc = f"{per_ps:g} B smem"
-        traffic = None
-        tf = PROFILES / "traffic_r01.json"
-        if tf.exists():
-            try:
-                traffic = json.loads(tf.read_text()).get(f"{args.config}:{test}")
-            except Exception:
-                traffic = None
-        roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                "frac": achieved / peak, "traffic": traffic, "kernel": ROOF[test][3],
-                "launch_ms": launch_ms, "launches_per_step": kern_n / args.steps,
-                "work_per_pair_sample": per_ps_desc}
 
-    # ---------------- end to end through run()
-    e2e = None
-    if rank == 0 and world == 1 and args.e2e_steps > 0:
-        mat_a = ps.make_matrix(a, ka, na_sentinel=sentinel)
-        mat_b = ps.make_matrix(b, kb, na_sentinel=sentinel) if b is not None else None
-        req = ps.TestRequest(test, outputs)
-        for _ in range(args.e2e_warmup):  # warm-up (pool growth, first-touch of the pinned ring)
-            ps.run(req, mat_a, mat_b)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            t1 = time.perf_counter()
-            res = ps.run(req, mat_a, mat_b)
-            if os.environ.get("PS_BENCH_VERBOSE"):
-                print("e2e step ms %.3f" % ((time.perf_counter() - t1) * 1e3), file=sys.stderr)
-        dt = (time.perf_counter() - t0) / args.e2e_steps
-        h2d = a.nbytes + (b.nbytes if b is not None else 0)
-        d2h = sum(res[n].nbytes for n in outputs)
-        e2e = {"value": work_units / dt, "unit": "pair-samples/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3}
+def measure_e2e(wl: Workload, steps: int, warmup: int, world: int):
+    """The public API from host numpy: run() (N = 1) or dist.sharded_run with
+    each rank's shard (N > 1); max over ranks."""
+    import torch
+
+    import paper_2505_00448_b200 as ps
+    from paper_2505_00448_b200 import dist
+
+    req = ps.TestRequest(wl.test, wl.outputs)
+    if world == 1:
+        mat_a, mat_b = wl.datamatrices()
+
+        def call():
+            return ps.run(req, mat_a, mat_b)
+    else:
+        sa, sb = wl.sharded_inputs()
+
+        def call():
+            return dist.sharded_run(req, sa, sb, assemble="owned")
+    for _ in range(warmup):
+        call()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        t1 = time.perf_counter()
+        res = call()
+        if os.environ.get("PS_BENCH_VERBOSE"):
+            print("e2e step ms %.3f" % ((time.perf_counter() - t1) * 1e3), file=sys.stderr)
+    dt = (time.perf_counter() - t0) / steps
+    d2h = sum(np.asarray(res[n]).nbytes for n in wl.outputs)
+    h2d = wl.a_rows.nbytes + (wl.b_rows.nbytes if wl.b_rows is not None else 0)
+    if world > 1:
+        t = torch.tensor([dt, float(d2h), float(h2d)], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
+        dt, d2h, h2d = float(t[0]), float(t[1]), float(t[2])
+    return {"value": wl.pairs * wl.S / dt, "unit": "pair-samples/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
+            "api": "run()" if world == 1 else "dist.sharded_run(assemble='owned')"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=parse_config, default=5)
+    ap.add_argument("--test", default=None, help="test within a multi-test config (config 4)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-legs", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-warmup", type=int, default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+
+    from paper_2505_00448_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    _lib.check(_lib.load().ps_set_device(local))
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg_key = args.config
+    test = args.test or ("pearson" if cfg_key in (1, 5) else "spearman" if cfg_key in (2, "5s")
+                         else workloads.config(cfg_key)["tests"][0])
+    big = cfg_key == 5
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else (3 if big else 5)
+    e2e_warmup = args.e2e_warmup if args.e2e_warmup is not None else (1 if big else 3)
+    peaks = device_peaks(load_peaks())
+
+    wl = Workload(cfg_key, test, rank, world)
+    # nvidia-smi is started before the warm-up: its start-up (NVML init) can
+    # stall this process's CUDA calls for ~15 ms; only rows sampled inside the
+    # timed region are kept (mark)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.5)
+    ms, roof, launches, clk = measure_device(wl, args.steps, args.warmup, world, rank, local, peaks, clocks)
+    value = wl.pairs * wl.S / (ms / 1e3)
+
+    e2e = measure_e2e(wl, e2e_steps, e2e_warmup, world) if e2e_steps > 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mat_a = ps.make_matrix(a, ka, na_sentinel=sentinel)
-        mat_b = ps.make_matrix(b, kb, na_sentinel=sentinel) if b is not None else None
-        cpu = cpu_baseline(cfg, test, args.cpu_seconds, mat_a, mat_b)
+        mat_a, mat_b = wl.datamatrices()
+        cpu = cpu_baseline(wl, args.cpu_seconds, mat_a, mat_b)
+        del mat_a, mat_b
+    wl._mats = None
+
+    legs = {}
+    if not args.no_legs:
+        for key, t in LEGS.get(cfg_key, []):
+            lw = Workload(key, t, rank, world)
+            lms, lroof, _, _ = measure_device(lw, 3, 3, world, rank, local, peaks)
+            legs[f"{t} (config {key})"] = {
+                "value": lw.pairs * lw.S / (lms / 1e3), "unit": "pair-samples/s", "ms_per_step": lms,
+                "steps": 3, "warmup": 3, "roofline": lroof, "config": config_dict(lw, world)}
 
     if rank == 0:
         line = {
-            "metric": f"pair-samples/s ({test}, config {args.config})",
+            "metric": f"pair-samples/s ({test}, config {cfg_key})",
             "value": value,
             "unit": "pair-samples/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
+            "ms_per_step": ms,
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64" if test != "chi2" else "u8/i32",
             "data": "synthetic (seeded BASELINE recipe, SURVEY 8d; CHRIS cohort unavailable)",
-            "config": {"workload": cfg["desc"], "config": args.config, "test": test,
-                       "pairs": P, "samples": S, "outputs": list(outputs),
-                       "l2": "flushed (512 MiB write) between steps",
-                       "parallelism": f"pair-shard x{world}"},
+            "config": config_dict(wl, world),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,
+            "legs": legs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -189,6 +189,27 @@ int ps_matrix_attach_presort(ps_matrix* m, void* order, void* inv, void* tb, voi
 int ps_matrix_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, void* stream);
 int ps_matrix_presort_done(ps_matrix* m, void* stream);
 
+/* ---- multi-GPU result exchange (family = adjust.py:23-87) ----
+ * A rank owning the reference partition [lo, hi) of `test` (triangle rows for
+ * pearson / spearman / chi2, engine.py:93-125; flat cells for ttest / anova;
+ * continuous features for mwu / kruskal, engine.py:70-90) packs the cells of
+ * its range from a device rows x cols matrix into a dense device vector and,
+ * after the ranks all-gathered the vectors, unpacks any rank's segment back
+ * (mirrored for the symmetric layout).  Triangle rows hold the h > g cells
+ * (diag = 0: the adjustment family; unpack writes a NaN diagonal) or h >= g
+ * (diag = 1: raw outputs with their self-tests), row-major: one contiguous
+ * segment of the reference's family order. */
+/* Host rows -> device rows through the library's pinned, all-core staging
+ * ring (each rank uploads its shard of the input); device padding columns
+ * [width, dpitch) are zeroed.  Pitches and width in bytes. */
+int ps_copy_h2d_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t rows,
+                   void* stream);
+int ps_cells_count(int test, int diag, int64_t rows, int64_t cols, int64_t lo, int64_t hi, int64_t* n);
+int ps_cells_pack(int test, int diag, const double* mat, int64_t rows, int64_t cols, int64_t lo, int64_t hi,
+                  double* vec, void* stream);
+int ps_cells_unpack(int test, int diag, const double* vec, int64_t rows, int64_t cols, int64_t lo, int64_t hi,
+                    double* mat, void* stream);
+
 /* ---- delimited matrix files (matio.py:40-125; host code, no device) ----
  * ps_write_matrix: the reference's write_matrix byte for byte: header
  * delim-joined ["", col ids...], rows [row id, f"{v:.17g}"...] ("nan" for any

@@ -240,3 +240,73 @@ def oracle_run(request, mat_a, mat_b=None, threads: int | None = None) -> dict[s
         else:
             res[name] = raw[name]
     return res
+
+
+def block_runner(test: str, mat_a, mat_b=None, wanted=("stat", "p"), t_variant="student", u_mode="auto",
+                 threads: int | None = None):
+    """Timed CPU baseline of the reference's block kernels (bench.py only).
+
+    Inputs are converted once and, for the rank tests, presorted once (the
+    reference's engine.run presorts every feature once per run,
+    engine.py:379-400); outputs are allocated once.  Returns
+    ``(prep_seconds, run)`` where ``run(lo, hi)`` executes the block over
+    the reference's range [lo, hi) and returns its wall seconds.
+    """
+    import time
+
+    threads = threads or default_threads()
+    canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
+    homogeneous = mat_b is None
+    shape = (mat_a.n_features, mat_a.n_features) if homogeneous else (mat_a.n_features, mat_b.n_features)
+    outs = {n: (np.full(shape, np.nan) if n in wanted else None) for n in canonical}
+    o = [_dp(outs[n]) for n in canonical]
+    L = lib()
+    S = ctypes.c_int64(mat_a.n_samples)
+    th = ctypes.c_int(threads)
+    i64 = ctypes.c_int64
+    if homogeneous:
+        F = i64(mat_a.n_features)
+        va = np.ascontiguousarray(mat_a.values)
+        pa = _u8(mat_a.present)
+        t0 = time.perf_counter()
+        if test == "spearman":
+            orders, svals, lengths = presort(va, pa, threads)
+        prep = time.perf_counter() - t0
+        cat = np.ascontiguousarray(mat_a.category_counts, dtype=np.int64) if test == "chi2" else None
+    else:
+        Fc, Fq = i64(mat_a.n_features), i64(mat_b.n_features)
+        la = np.ascontiguousarray(mat_a.values)
+        lp = _u8(mat_a.present)
+        vb = np.ascontiguousarray(mat_b.values)
+        vp = _u8(mat_b.present)
+        cat = np.ascontiguousarray(mat_a.category_counts, dtype=np.int64) if test in ("anova", "kruskal") else None
+        t0 = time.perf_counter()
+        if test in ("mwu", "kruskal"):
+            orders, svals, lengths = presort(vb, vp, threads)
+        prep = time.perf_counter() - t0
+
+    def run(lo: int, hi: int) -> float:
+        c_lo, c_hi = i64(lo), i64(hi)
+        t = time.perf_counter()
+        if test == "pearson":
+            code = L.orc_pearson_block(_dp(va), _bp(pa), F, S, c_lo, c_hi, *o, th)
+        elif test == "spearman":
+            code = L.orc_spearman_block(_ip(orders), _dp(svals), _ip(lengths), _bp(pa), F, S, c_lo, c_hi, *o, th)
+        elif test == "chi2":
+            code = L.orc_chi2_block(_dp(va), _bp(pa), _ip(cat), F, S, c_lo, c_hi, *o, th)
+        elif test == "ttest":
+            code = L.orc_ttest_block(_dp(la), _bp(lp), _dp(vb), _bp(vp), Fc, Fq, S, c_lo, c_hi,
+                                     ctypes.c_int(1 if t_variant == "student" else 0), *o, th)
+        elif test == "anova":
+            code = L.orc_anova_block(_dp(la), _bp(lp), _ip(cat), _dp(vb), _bp(vp), Fc, Fq, S, c_lo, c_hi, *o, th)
+        elif test == "mwu":
+            code = L.orc_mwu_block(_ip(orders), _dp(svals), _ip(lengths), _dp(la), _bp(lp), Fc, Fq, S, c_lo, c_hi,
+                                   ctypes.c_int(U_MODE_CODES[u_mode]), *o, th)
+        else:
+            code = L.orc_kruskal_block(_ip(orders), _dp(svals), _ip(lengths), _dp(la), _bp(lp), _ip(cat), Fc, Fq,
+                                       S, c_lo, c_hi, *o, th)
+        dt = time.perf_counter() - t
+        _check(code)
+        return dt
+
+    return prep, run

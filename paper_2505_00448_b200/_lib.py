@@ -65,6 +65,10 @@ EXPORTED = (
     "ps_matrix_attach_presort",
     "ps_matrix_presort_rows",
     "ps_matrix_presort_done",
+    "ps_copy_h2d_2d",
+    "ps_cells_count",
+    "ps_cells_pack",
+    "ps_cells_unpack",
     "ps_write_matrix",
     "ps_read_matrix",
     "ps_matrix_file_free",
@@ -156,6 +160,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.ps_matrix_attach_presort.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.ps_matrix_presort_rows.argtypes = [vp, i64, i64, vp]
     lib.ps_matrix_presort_done.argtypes = [vp, vp]
+    lib.ps_copy_h2d_2d.argtypes = [vp, i64, vp, i64, i64, i64, vp]
+    lib.ps_cells_count.argtypes = [i32, i32, i64, i64, i64, i64, ctypes.POINTER(ctypes.c_int64)]
+    lib.ps_cells_pack.argtypes = [i32, i32, dp, i64, i64, i64, i64, dp, vp]
+    lib.ps_cells_unpack.argtypes = [i32, i32, dp, i64, i64, i64, i64, dp, vp]
     lib.ps_write_matrix.argtypes = [ctypes.c_char_p, dp, i64, i64, vp, vp, ctypes.c_char]
     lib.ps_read_matrix.argtypes = [ctypes.c_char_p, ctypes.c_char, ctypes.POINTER(MatrixFile)]
     lib.ps_matrix_file_free.argtypes = [ctypes.POINTER(MatrixFile)]

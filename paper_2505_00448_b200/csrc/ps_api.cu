@@ -813,6 +813,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   // stages the raw matrices to the host; the adjusted matrices follow.
   double* d_adjk[3] = {nullptr, nullptr, nullptr};
   int rc_adj = PS_OK;
+  std::string adj_error;
   std::thread adj_thread;
   if (!rc && any_adj) {
     for (int k = 0; k < 3 && !rc; ++k)
@@ -829,6 +830,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
         cudaSetDevice(dev);
         for (int k = 0; k < 3 && rc_adj == PS_OK; ++k)
           if (adj_outs[k]) rc_adj = ps_adjust_run(d_out[1], rows, cols, k, homogeneous ? 1 : 0, d_adjk[k], st->aux);
+        if (rc_adj) adj_error = g_last_error;  // thread_local: hand the message to the caller's thread
       });
     }
   }
@@ -844,13 +846,18 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     rc = ps_stage_d2h_many(4, hd, ds_, nb, s);
   }
   tr.mark("d2h");
-  if (adj_thread.joinable()) adj_thread.join();
-  if (!rc) rc = rc_adj;
-  if (!rc && any_adj) {
+  if (adj_thread.joinable()) {
+    adj_thread.join();
+    // whatever happened, the main stream (which frees p, the adjusted buffers
+    // and the adjust scratch) is ordered after everything issued on aux
     cudaError_t e = cudaEventRecord(st->aux_ev, st->aux);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, st->aux_ev, 0);
-    if (e != cudaSuccess) rc = ps_cuda_check(e, "adjust join");
-    if (!rc) {
+    if (e != cudaSuccess) cudaStreamSynchronize(st->aux);
+    if (!rc && e != cudaSuccess) rc = ps_cuda_check(e, "adjust join");
+  }
+  if (!rc && rc_adj) rc = ps_fail(rc_adj, adj_error);
+  if (!rc && any_adj) {
+    {
       void* hd[3];
       const void* ds_[3];
       size_t nb[3];
@@ -875,6 +882,25 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   ps_matrix_destroy(ma);
   ps_matrix_destroy(mb);
   if (rc) cudaStreamSynchronize(s);
+  return rc;
+}
+
+// Pageable host rows -> device rows through the pinned all-core staging ring
+// (multi-GPU: each rank uploads its own shard of the input); the device
+// padding columns [width, dpitch) are zeroed.  Returns once the host buffer
+// may be reused (the last DMA may still be in flight on `stream`).
+int ps_copy_h2d_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t rows,
+                   void* stream) {
+  Guard g;
+  int rc = ensure_state();
+  if (rc) return rc;
+  if (rows <= 0 || width <= 0) return PS_OK;
+  if (!dst || !src || dpitch < width || spitch < width) return ps_fail(PS_ERR_INVALID, "bad copy geometry");
+  cudaStream_t s = as_stream(stream);
+  rc = ps_stage_h2d_2d(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)rows, s);
+  if (!rc && dpitch > width)
+    PS_CUDA(cudaMemset2DAsync(static_cast<char*>(dst) + width, (size_t)dpitch, 0, (size_t)(dpitch - width),
+                              (size_t)rows, s));
   return rc;
 }
 

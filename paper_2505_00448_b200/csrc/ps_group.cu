@@ -614,6 +614,14 @@ static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t
   return PS_OK;
 }
 
+// Split-K factor of the moment contraction: enough K parts that the WHOLE
+// (label rows x features) tile grid gives two CTAs per SM, at least 16 mask
+// words per part.  A function of (R, Fq, W) only.
+static int64_t group_kparts(const ps_device_state* ds, int64_t R, int64_t Fq, int64_t W) {
+  const int64_t tiles = ps_ceil_div(std::max<int64_t>(R, 1), T) * ps_ceil_div(Fq, T);
+  return std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, tiles), W / 16));
+}
+
 int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
                         double* stat, double* p, double* eff, cudaStream_t s) {
   const int64_t Fc = lab->F, Fq = val->F, S = val->S;
@@ -680,9 +688,10 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   int32_t* Pn = nullptr;
   double *Ps = nullptr, *Pq = nullptr;
   if (grid > 0) {
-    // split K when the tile grid cannot fill two CTAs per SM
-    const int64_t kparts = std::max<int64_t>(
-        1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
+    // split K when the WHOLE tile grid cannot fill two CTAs per SM (the split
+    // is a function of the matrices, not of the range: every cell's k-order,
+    // hence every bit, is the same for any range / rank / incremental launch)
+    const int64_t kparts = group_kparts(ds, R, Fq, W);
     const int64_t stride = Rp * Fq;
     if (kparts > 1) {
       PS_CUDA(ps_alloc(&Pn, (size_t)(kparts * stride), s));
@@ -777,10 +786,11 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
   const size_t smem = NSTAGE * sizeof(Stage);
   PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = rtiles * ctiles;
-  int64_t kparts = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, grid), W / 16));
+  const int64_t kparts = group_kparts(ds, j->R, Fq, W);
   const int64_t rows = rtiles * T, width = ctiles * T, c0 = ct0 * T, stride = rows * width;
-  if (slot >= 0) kparts = std::max<int64_t>(1, std::min<int64_t>(kparts, j->pcap / std::max<int64_t>(1, stride)));
-  if (slot == -2) kparts = 1;  // incremental launch without partial buffers
+  // the slot's partial buffers hold a staging chunk's columns; a wider window
+  // gets its own (same split, so the same bits)
+  if (slot >= 0 && kparts * stride > j->pcap) slot = -1;
   int32_t* Pn = nullptr;
   double *Ps = nullptr, *Pq = nullptr;
   if (kparts > 1 && slot >= 0) {
@@ -861,7 +871,7 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
     const int64_t rtiles = ps_ceil_div(std::max<int64_t>(j->R, 1), T);
     const int64_t chunk_rows = (int64_t)std::max<size_t>(1, ps_stage_chunk_bytes() / (sizeof(double) * val->ld));
     const int64_t width_cap = (ps_ceil_div(chunk_rows, T) + 1) * T;
-    const int64_t kp = std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, rtiles), W / 16));
+    const int64_t kp = group_kparts(ds, j->R, Fq, W);
     j->pcap = kp > 1 ? kp * rtiles * T * width_cap : 0;
   }
   // the pageable copies above are staged by the driver: the vectors may go
@@ -884,7 +894,7 @@ int ps_group_moment_upto(ps_group_job* j, int64_t h1, cudaStream_t s) {
     PS_CUDA(cudaStreamWaitEvent(s, ds->alloc_ev, 0));
   }
   cudaStream_t w = ps_walk_stream(j->nws++, s);
-  int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w, j->pn[slot] ? slot : -2);
+  int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w, j->pn[slot] ? slot : -1);
   j->h_done = h1;
   return rc;
 }

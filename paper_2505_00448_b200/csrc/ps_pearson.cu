@@ -363,11 +363,15 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   const int64_t tile0 = ps_tri_offset(I0, NT);
   const int64_t ntiles = ps_tri_offset(I1 + 1, NT) - tile0;
   const int64_t W = a->W;
-  // split-K so that small problems still fill the machine (>= 2 CTAs per SM)
+  // split-K so that small problems still fill the machine (>= 2 CTAs per SM).
+  // The split count is a function of the WHOLE triangle (F, S), never of the
+  // range: a pair's k-order -- hence every bit of its result -- is the same
+  // whichever range (rank, thread block of the reference) computes it.
   int nsplit = 1;
   const int64_t want = 2LL * ds->num_sms;
-  if (ntiles < want) {
-    nsplit = (int)std::min<int64_t>(ps_ceil_div(want, ntiles), std::max<int64_t>(1, W / 4));
+  const int64_t ntiles_all = NT * (NT + 1) / 2;
+  if (ntiles_all < want) {
+    nsplit = (int)std::min<int64_t>(ps_ceil_div(want, ntiles_all), std::max<int64_t>(1, W / 4));
     nsplit = std::max(1, nsplit);
   }
   const int64_t cps = ps_ceil_div(W, nsplit);

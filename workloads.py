@@ -100,6 +100,50 @@ def config_spearman_like(rng: np.random.Generator, F: int, S: int) -> np.ndarray
     return x
 
 
+C5_BLOCK = 256  # rows per independently seeded block of the config-5 matrix
+
+
+def config5_rows(F: int, S: int, r0: int, r1: int, rng: np.random.Generator | None = None,
+                 threads: int | None = None) -> np.ndarray:
+    """Rows [r0, r1) of the config-5 Pearson matrix (latent factor, 30% MCAR).
+
+    The shared factors come from ``default_rng([SEED_BASE, 5])`` (L then Z);
+    each block of ``C5_BLOCK`` rows draws its noise and then its MCAR cells
+    from its own ``default_rng([SEED_BASE, 5, 1000 + block])``.  So any row
+    range -- one rank's shard of the 16 GB input -- is generated on its own,
+    block-parallel, and equals the same rows of the whole matrix.
+    """
+    import concurrent.futures as cf
+    import os
+
+    if rng is None:
+        rng = np.random.default_rng([SEED_BASE, 5])
+    L = rng.uniform(-0.8, 0.8, size=(F, 5))
+    Z = rng.standard_normal((5, S))
+    out = np.empty((r1 - r0, S))
+
+    def block(b):
+        lo, hi = max(r0, b * C5_BLOCK), min(r1, (b + 1) * C5_BLOCK)
+        rb = np.random.default_rng([SEED_BASE, 5, 1000 + b])
+        n = min(F, (b + 1) * C5_BLOCK) - b * C5_BLOCK  # the whole block is drawn
+        sel = slice(lo - b * C5_BLOCK, hi - b * C5_BLOCK)
+        noise = rb.standard_normal((n, S))[sel]
+        miss = (rb.random((n, S)) < 0.30)[sel]
+        x = out[lo - r0:hi - r0]
+        # L Z as five elementwise terms in a fixed order (a BLAS matmul's
+        # rounding can depend on how many rows it is handed)
+        np.multiply(L[lo:hi, 0:1], Z[0], out=x)
+        for q in range(1, 5):
+            x += L[lo:hi, q:q + 1] * Z[q]
+        x += noise
+        x[miss] = SENTINEL
+
+    blocks = range(r0 // C5_BLOCK, (r1 + C5_BLOCK - 1) // C5_BLOCK)
+    with cf.ThreadPoolExecutor(threads or min(32, os.cpu_count() or 1)) as ex:
+        list(ex.map(block, blocks))
+    return out
+
+
 def config(k: int, scale: float = 1.0) -> dict:
     """Inputs of BASELINE config k (1..5, '5s' for the config-5 Spearman leg).
 
@@ -152,7 +196,7 @@ def config(k: int, scale: float = 1.0) -> dict:
                     desc=f"mixed {Fc}x{Fq}x{S} k in 2..8, 25% shifted pairs, 10% MCAR")
     if k == 5:
         F, S = max(2, int(20000 * scale)), max(100, int(100000 * scale))
-        x = _mcar(rng, _latent(rng, F, S), 0.30)
+        x = config5_rows(F, S, 0, F, rng=rng)
         return dict(tests=["pearson"], a=x, b=None, kind_a="continuous", kind_b=None, F=F, S=S,
                     desc=f"pearson scale {F}x{S} 30% MCAR")
     if k == "5s":
