@@ -309,4 +309,5 @@ def block_runner(test: str, mat_a, mat_b=None, wanted=("stat", "p"), t_variant="
         _check(code)
         return dt
 
+    run.outs = outs  # the (shared, NaN-prefilled) output matrices
     return prep, run

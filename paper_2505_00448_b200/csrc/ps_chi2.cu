@@ -98,14 +98,28 @@ constexpr int TSTAGE_BYTES = TA_BYTES + TB_BYTES;
 constexpr size_t kTc05Smem = (size_t)TSTAGES * TSTAGE_BYTES + 1024;
 constexpr int TTH_WS = 192;
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+// Partial tables are added into C: fp32 (one vector red per 4 cells) while
+// every count is < 2^24 -- exact, and integer-valued adds commute -- or u32
+// (scalar reds) when the sample count could reach 2^24 (categorical.py:84-93
+// keeps int64 tables; no count ever exceeds S < 2^32).
+__device__ __forceinline__ void red_add4(float* addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"((float)(int)a), "f"((float)(int)b),
+               "f"((float)(int)c), "f"((float)(int)d)
                : "memory");
 }
+__device__ __forceinline__ void red_add4(uint32_t* addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr), "r"(a) : "memory");
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr + 1), "r"(b) : "memory");
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr + 2), "r"(c) : "memory");
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(addr + 3), "r"(d) : "memory");
+}
 
+// C holds the rows [crow0, crow0 + band) of the table matrix (a row band:
+// scratch stays bounded for wide matrices)
+template <typename Acc>
 __global__ void __launch_bounds__(TTH_WS, 1)
 onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbase, const int2* __restrict__ tiles,
-                      int64_t ntiles, float* __restrict__ C, int64_t ldC) {
+                      int64_t ntiles, Acc* __restrict__ C, int64_t ldC, int64_t crow0) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TSTAGES], empty[TSTAGES], accfull, accempty;
   __shared__ uint32_t tmem_base_s;
@@ -189,15 +203,13 @@ onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         const int64_t r = (int64_t)t.x * TM + half * 128 + warp * 32 + lane;
-        float* crow = C + r * ldC + (int64_t)t.y * TN;
+        Acc* crow = C + (r - crow0) * ldC + (int64_t)t.y * TN;
 #pragma unroll 1
         for (int cc = 0; cc < TN / 32; ++cc) {
           uint32_t v[32];
           tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            red_add_v4(crow + cc * 32 + j, (float)(int)v[j], (float)(int)v[j + 1], (float)(int)v[j + 2],
-                       (float)(int)v[j + 3]);
+          for (int j = 0; j < 32; j += 4) red_add4(crow + cc * 32 + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
       tc05::fence_before_sync();
@@ -221,9 +233,10 @@ onehot_gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
 // with a dummy partner that only contributes its half of the shared operand.
 //   unit = (I0, J0, I1, J1); I0 == I1: A shared; I1 < 0: dummy second tile.
 constexpr int THALF = TA_BYTES / 2;  // 128 rows x 128 B
+template <typename Acc>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TTH_WS, 1)
 onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbase, const int4* __restrict__ units,
-                      int64_t nunits, float* __restrict__ C, int64_t ldC) {
+                      int64_t nunits, Acc* __restrict__ C, int64_t ldC, int64_t crow0) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TSTAGES], empty[TSTAGES], accfull, accempty;
   __shared__ uint32_t tmem_base_s;
@@ -328,15 +341,13 @@ onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
 #pragma unroll 1
       for (int half = 0; half < 2; ++half) {
         const int64_t r = (int64_t)I * TM + half * 128 + warp * 32 + lane;
-        float* crow = C + r * ldC + (int64_t)J * TN;
+        Acc* crow = C + (r - crow0) * ldC + (int64_t)J * TN;
 #pragma unroll 1
         for (int cc = 0; cc < TN / 32; ++cc) {
           uint32_t v[32];
           tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            red_add_v4(crow + cc * 32 + j, (float)(int)v[j], (float)(int)v[j + 1], (float)(int)v[j + 2],
-                       (float)(int)v[j + 3]);
+          for (int j = 0; j < 32; j += 4) red_add4(crow + cc * 32 + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
       tc05::fence_before_sync();
@@ -360,8 +371,8 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
 
 // One thread per pair (g <= h): categorical.py:31-74 in the same op order.
 // Row/column sums are cached for up to CM levels; the table is read from C.
-template <int CM>
-__global__ void chi2_finish_kernel(const float* __restrict__ C, int64_t ldC,
+template <int CM, typename Acc>
+__global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64_t crow0,
                                    const int32_t* __restrict__ off, const int32_t* __restrict__ cat,
                                    int64_t F, int64_t lo, int64_t hi, double* __restrict__ stat,
                                    double* __restrict__ pout, double* __restrict__ phi_out,
@@ -373,7 +384,7 @@ __global__ void chi2_finish_kernel(const float* __restrict__ C, int64_t ldC,
     if (h < g) continue;
     const int cg = cat[g], ch = cat[h];
     const bool diag = g == h;
-    const float* T = C + (int64_t)off[g] * ldC + off[h];  // exact integer counts
+    const Acc* T = C + ((int64_t)off[g] - crow0) * ldC + off[h];  // exact integer counts
     // the diagonal pair's table is diagonal; its lower half lies outside the
     // computed upper-triangular tiles, so read only the diagonal
     auto tab = [&](int i, int j) -> long long {
@@ -484,60 +495,28 @@ static int make_onehot_map(CUtensorMap* map, const uint8_t* O, int64_t rows, int
   return PS_OK;
 }
 
-int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi, double* v,
-                cudaStream_t s) {
-  const int64_t F = a->F, S = a->S;
-  lo = std::max<int64_t>(0, lo);
-  hi = std::min<int64_t>(F, hi);
-  if (hi <= lo || (!stat && !p && !phi && !v)) return PS_OK;
+// One row band of the contingency tables: the features [ga, gb) of the range,
+// their table rows (C rows [crow0, crow0 + band)) against every column tile
+// right of the diagonal, then the per-pair finish.
+template <typename Acc>
+static int chi2_band(ps_matrix* a, const std::vector<int32_t>& off, int64_t ga, int64_t gb, int64_t Rp,
+                     const CUtensorMap& map, int nk_all, const int32_t* d_off, double* stat, double* p, double* phi,
+                     double* v, cudaStream_t s) {
   ps_device_state* ds = ps_state();
-  // one-hot row layout (host: category counts are host-resident)
-  std::vector<int32_t> off(F + 1, 0), cat32(F);
-  for (int64_t f = 0; f < F; ++f) {
-    cat32[f] = (int32_t)a->h_cat[f];
-    off[f + 1] = off[f] + cat32[f];
-  }
+  const int64_t F = a->F;
   const int64_t R = off[F];
-  const int64_t Rp = std::max<int64_t>(TN, ps_round_up(R, TN));
-  const int64_t Sp = ps_round_up(S, TKB);
-  std::vector<int32_t> row_feat(R), row_level(R);
-  for (int64_t f = 0; f < F; ++f)
-    for (int32_t l = 0; l < cat32[f]; ++l) {
-      row_feat[off[f] + l] = (int32_t)f;
-      row_level[off[f] + l] = l;
-    }
-  uint8_t* O = nullptr;
-  float* C = nullptr;  // exact integer counts (< 2^24), accumulated by the stream-K GEMM
-  int32_t *d_off = nullptr, *d_rf = nullptr, *d_rl = nullptr;
-  PS_CUDA(ps_alloc(&O, (size_t)(Rp * Sp), s));
-  PS_CUDA(ps_alloc(&C, (size_t)(Rp * Rp), s));
-  PS_CUDA(cudaMemsetAsync(C, 0, sizeof(float) * Rp * Rp, s));
-  PS_CUDA(ps_alloc(&d_off, (size_t)(F + 1), s));
-  PS_CUDA(ps_alloc(&d_rf, (size_t)std::max<int64_t>(R, 1), s));
-  PS_CUDA(ps_alloc(&d_rl, (size_t)std::max<int64_t>(R, 1), s));
-  PS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (F + 1), cudaMemcpyHostToDevice, s));
-  if (R > 0) {
-    PS_CUDA(cudaMemcpyAsync(d_rf, row_feat.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
-    PS_CUDA(cudaMemcpyAsync(d_rl, row_level.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
-  }
-  {
-    const int64_t W = a->W;
-    const dim3 grid((unsigned)ps_ceil_div(W, 128), (unsigned)ps_ceil_div(F - lo, kCheckRows));
-    label_check_kernel<<<grid, 128, 0, s>>>(a->d_bad, a->d_mask, W, F, lo, hi, ds->d_err);
-    PS_LAUNCHED();
-  }
-  onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
-  PS_LAUNCHED();
-  // 256 x 256 tiles of C needed by pairs with g in [lo, hi): row tiles covering
-  // off[lo] .. off[hi]-1, column tiles from the diagonal rightwards
+  const int64_t I0 = off[ga] / TM;
+  const int64_t I1 = std::max<int64_t>(I0, (off[gb] - 1) / TM);
+  const int64_t crow0 = I0 * TM, band = (I1 - I0 + 1) * TM;
+  Acc* C = nullptr;
+  PS_CUDA(ps_alloc(&C, (size_t)(band * Rp), s));
+  PS_CUDA(cudaMemsetAsync(C, 0, sizeof(Acc) * band * Rp, s));
   std::vector<int2> tl;
-  if (R > 0) {
-    const int64_t I0 = off[lo] / TM;
-    const int64_t I1 = std::max<int64_t>(I0, (off[hi] - 1) / TM);
+  if (R > 0)
     for (int64_t I = I0; I <= I1; ++I)
       for (int64_t J = (I * TM) / TN; J < Rp / TN; ++J) tl.push_back(make_int2((int)I, (int)J));
-  }
   int2* d_tiles = nullptr;
+  int4* d_units = nullptr;
   if (!tl.empty()) {
     PS_CUDA(ps_alloc(&d_tiles, tl.size(), s));
     PS_CUDA(cudaMemcpyAsync(d_tiles, tl.data(), sizeof(int2) * tl.size(), cudaMemcpyHostToDevice, s));
@@ -565,21 +544,15 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
         }
       }
       if (k < left.size()) un.push_back(make_int4(left[k].x, left[k].y, -1, -1));
-    }
-    int4* d_units = nullptr;
-    if (mc) {
       PS_CUDA(ps_alloc(&d_units, un.size(), s));
       PS_CUDA(cudaMemcpyAsync(d_units, un.data(), sizeof(int4) * un.size(), cudaMemcpyHostToDevice, s));
     }
-    PS_CUDA(cudaFuncSetAttribute(mc ? (const void*)onehot_gemm_mc_kernel : (const void*)onehot_gemm_sk_kernel,
+    PS_CUDA(cudaFuncSetAttribute(mc ? (const void*)onehot_gemm_mc_kernel<Acc> : (const void*)onehot_gemm_sk_kernel<Acc>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTc05Smem));
-    CUtensorMap map;
-    int rc = make_onehot_map(&map, O, Rp, Sp, mc ? 128 : TM);
-    if (rc) return rc;
     // K phases: the one-hot operand (Rp x Sp bytes) is streamed through L2 in
     // slabs that fit it, all CTAs working inside the same slab (stream-K
     // spreads CTAs over K, which thrashes L2 when O is larger than it)
-    const int nk_all = (int)(Sp / TKB);
+    const int64_t Sp = (int64_t)nk_all * TKB;
     const int64_t slab_budget = 96ll << 20;  // L2 is 126 MB
     // (cluster pairs read 25% less through L2: one pass over K measured
     // fastest there, 0.187 vs 0.212 ms in two phases at config 3)
@@ -604,39 +577,108 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
           at.val.clusterDim.z = 1;
           lc.attrs = &at;
           lc.numAttrs = 1;
-          if (cudaOccupancyMaxActiveClusters(&max_clusters, onehot_gemm_mc_kernel, &lc) != cudaSuccess ||
+          if (cudaOccupancyMaxActiveClusters(&max_clusters, onehot_gemm_mc_kernel<Acc>, &lc) != cudaSuccess ||
               max_clusters <= 0)
             max_clusters = ds->num_sms / 2;
           cudaGetLastError();
         }
         const int64_t iters = (int64_t)un.size() * nk;
         const int grid = 2 * (int)std::min<int64_t>(iters, max_clusters);
-        onehot_gemm_mc_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_units, (int64_t)un.size(),
-                                                                        C, Rp);
+        onehot_gemm_mc_kernel<Acc><<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_units,
+                                                                             (int64_t)un.size(), C, Rp, crow0);
       } else {
         const int64_t iters = (int64_t)tl.size() * nk;
         const int grid = (int)std::min<int64_t>(iters, ds->num_sms);
-        onehot_gemm_sk_kernel<<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_tiles, (int64_t)tl.size(),
-                                                                        C, Rp);
+        onehot_gemm_sk_kernel<Acc><<<(unsigned)grid, TTH_WS, kTc05Smem, s>>>(map, nk, kb0, d_tiles,
+                                                                             (int64_t)tl.size(), C, Rp, crow0);
       }
       PS_LAUNCHED();
     }
     ps_prof_end(s);
-    ps_free(d_units, s);
   }
-  int32_t* d_cat = a->d_cat;
-  const int64_t total = (hi - lo) * F;
+  const int64_t total = (gb - ga) * F;
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
   if (a->cmax <= 16)
-    chi2_finish_kernel<16><<<blocks, 128, 0, s>>>(C, Rp, d_off, d_cat, F, lo, hi, stat, p, phi, v, ds->d_err);
+    chi2_finish_kernel<16, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
+                                                       ds->d_err);
   else
-    chi2_finish_kernel<256><<<blocks, 128, 0, s>>>(C, Rp, d_off, d_cat, F, lo, hi, stat, p, phi, v, ds->d_err);
+    chi2_finish_kernel<256, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
+                                                        ds->d_err);
   PS_LAUNCHED();
-  ps_free(O, s);
   ps_free(C, s);
+  ps_free(d_tiles, s);
+  ps_free(d_units, s);
+  return PS_OK;
+}
+
+int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi, double* v,
+                cudaStream_t s) {
+  const int64_t F = a->F, S = a->S;
+  lo = std::max<int64_t>(0, lo);
+  hi = std::min<int64_t>(F, hi);
+  if (hi <= lo || (!stat && !p && !phi && !v)) return PS_OK;
+  ps_device_state* ds = ps_state();
+  // one-hot row layout (host: category counts are host-resident)
+  std::vector<int32_t> off(F + 1, 0), cat32(F);
+  for (int64_t f = 0; f < F; ++f) {
+    cat32[f] = (int32_t)a->h_cat[f];
+    off[f + 1] = off[f] + cat32[f];
+  }
+  const int64_t R = off[F];
+  const int64_t Rp = std::max<int64_t>(TN, ps_round_up(R, TN));
+  const int64_t Sp = ps_round_up(S, TKB);
+  std::vector<int32_t> row_feat(R), row_level(R);
+  for (int64_t f = 0; f < F; ++f)
+    for (int32_t l = 0; l < cat32[f]; ++l) {
+      row_feat[off[f] + l] = (int32_t)f;
+      row_level[off[f] + l] = l;
+    }
+  uint8_t* O = nullptr;
+  int32_t *d_off = nullptr, *d_rf = nullptr, *d_rl = nullptr;
+  PS_CUDA(ps_alloc(&O, (size_t)(Rp * Sp), s));
+  PS_CUDA(ps_alloc(&d_off, (size_t)(F + 1), s));
+  PS_CUDA(ps_alloc(&d_rf, (size_t)std::max<int64_t>(R, 1), s));
+  PS_CUDA(ps_alloc(&d_rl, (size_t)std::max<int64_t>(R, 1), s));
+  PS_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (F + 1), cudaMemcpyHostToDevice, s));
+  if (R > 0) {
+    PS_CUDA(cudaMemcpyAsync(d_rf, row_feat.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(d_rl, row_level.data(), sizeof(int32_t) * R, cudaMemcpyHostToDevice, s));
+  }
+  {
+    const int64_t W = a->W;
+    const dim3 grid((unsigned)ps_ceil_div(W, 128), (unsigned)ps_ceil_div(F - lo, kCheckRows));
+    label_check_kernel<<<grid, 128, 0, s>>>(a->d_bad, a->d_mask, W, F, lo, hi, ds->d_err);
+    PS_LAUNCHED();
+  }
+  onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
+  PS_LAUNCHED();
+  CUtensorMap map;
+  {
+    const char* mce = getenv("PS_CHI2_MC");
+    const bool mc = !(mce && mce[0] == '0') && ds->num_sms >= 2;
+    int rc = make_onehot_map(&map, O, Rp, Sp, mc ? 128 : TM);
+    if (rc) return rc;
+  }
+  // Row bands: the table scratch of a band (band rows x Rp counts) stays
+  // within PS_CHI2_BAND_MB (default 2 GiB) however wide the matrix is; a band
+  // is at least one feature.  Config 3 (Rp = 3072) is one band.
+  int64_t budget = 2048ll << 20;
+  if (const char* e = getenv("PS_CHI2_BAND_MB")) budget = std::max(1L, atol(e)) << 20;
+  const int64_t band_rows = std::max<int64_t>(TM, budget / (Rp * 4) / TM * TM);
+  // u32 tables when any count could reach 2^24 (fp32 is exact below it)
+  const bool wide_counts = S >= (1LL << 24) || getenv("PS_CHI2_U32");
+  int rc = PS_OK;
+  for (int64_t ga = lo; ga < hi && !rc;) {
+    int64_t gb = ga + 1;
+    // rows [off[ga], off[gb]) plus the tile-alignment slack of the first tile
+    while (gb < hi && (off[gb + 1] - (off[ga] / TM) * TM) <= band_rows) ++gb;
+    rc = wide_counts ? chi2_band<uint32_t>(a, off, ga, gb, Rp, map, (int)(Sp / TKB), d_off, stat, p, phi, v, s)
+                     : chi2_band<float>(a, off, ga, gb, Rp, map, (int)(Sp / TKB), d_off, stat, p, phi, v, s);
+    ga = gb;
+  }
+  ps_free(O, s);
   ps_free(d_off, s);
   ps_free(d_rf, s);
   ps_free(d_rl, s);
-  ps_free(d_tiles, s);
-  return PS_OK;
+  return rc;
 }

@@ -571,14 +571,18 @@ int ps_mixed_label_check(ps_matrix* lab, ps_matrix* val, int64_t g0, int64_t g1,
 
 // Per-cell statistics from the moments of cells [lo, hi), then the exact
 // in-order replay of the ill-conditioned cells (one host round trip for the
-// replay count).
-static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
-                               const int32_t* Mn, const double* Ms, const double* Mq, const int32_t* d_off,
-                               const uint32_t* bits, int2* rep, int* repc, int cap, double* stat, double* p,
-                               double* eff, int* count_out, cudaStream_t s) {
+// replay count).  The replay list holds `cap` cells; when more cells need the
+// replay (e.g. many constant continuous columns), the range is finished again
+// in chunks of `cap` cells, each of which cannot overflow its list -- the
+// reference answers every cell (mixed.py:453-495), so must we.
+static int group_finish_chunk(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
+                              const int32_t* Mn, const double* Ms, const double* Mq, const int32_t* d_off,
+                              const uint32_t* bits, int2* rep, int* repc, int cap, double* stat, double* p,
+                              double* eff, int* count_out, cudaStream_t s) {
   ps_device_state* ds = ps_state();
   const int64_t Fq = val->F, W = val->W;
   Outs o{stat, p, eff, rep, repc, cap, ds->d_err};
+  PS_CUDA(cudaMemsetAsync(repc, 0, sizeof(int), s));
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(hi - lo, 128), (int64_t)ds->num_sms * 16);
   const bool small = lab->cmax <= 16;
   if (small)
@@ -588,11 +592,12 @@ static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t
     group_finish_kernel<256><<<blocks, 128, 0, s>>>(test, Mn, Ms, Mq, d_off, lab->d_cat, val->d_center, Fq,
                                                     lo, hi, student, o);
   PS_LAUNCHED();
-  // a replay list overflow (pathological: > 4M ill-conditioned cells) is reported
   int count = 0;
   PS_CUDA(cudaMemcpyAsync(&count, repc, sizeof(int), cudaMemcpyDeviceToHost, s));
   PS_CUDA(cudaStreamSynchronize(s));
-  const int n_items = std::min(count, cap);
+  *count_out = count;
+  if (count > cap) return PS_OK;  // the caller re-finishes in chunks
+  const int n_items = count;
   if (n_items > 0) {
     const int kslots = test == PS_TEST_ANOVA ? std::max(2, lab->cmax) : 2;
     GroupPart* parts = nullptr;
@@ -610,8 +615,29 @@ static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t
     PS_LAUNCHED();
     ps_free(parts, s);
   }
-  *count_out = count;
   return PS_OK;
+}
+
+static int group_finish_replay(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
+                               const int32_t* Mn, const double* Ms, const double* Mq, const int32_t* d_off,
+                               const uint32_t* bits, int2* rep, int* repc, int cap, double* stat, double* p,
+                               double* eff, cudaStream_t s) {
+  int count = 0;
+  int rc = group_finish_chunk(test, lab, val, lo, hi, student, Mn, Ms, Mq, d_off, bits, rep, repc, cap, stat, p, eff,
+                              &count, s);
+  for (int64_t c0 = lo; !rc && count > cap && c0 < hi; c0 += cap) {
+    int cc = 0;
+    rc = group_finish_chunk(test, lab, val, c0, std::min<int64_t>(hi, c0 + cap), student, Mn, Ms, Mq, d_off, bits,
+                            rep, repc, cap, stat, p, eff, &cc, s);
+  }
+  return rc;
+}
+
+// replay list capacity (PS_REPLAY_CAP: tests shrink it to exercise the chunked re-finish)
+static int replay_cap(int64_t cells) {
+  int64_t lim = 1 << 22;
+  if (const char* e = getenv("PS_REPLAY_CAP")) lim = std::max(1L, atol(e));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cells, lim));
 }
 
 // Split-K factor of the moment contraction: enough K parts that the WHOLE
@@ -656,7 +682,7 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   int32_t *d_rf = nullptr, *d_rl = nullptr, *d_off = nullptr, *Mn = nullptr, *repc = nullptr;
   double *Ms = nullptr, *Mq = nullptr;
   int2* rep = nullptr;
-  const int cap = (int)std::min<int64_t>(hi - lo, 1 << 22);
+  const int cap = replay_cap(hi - lo);
   PS_CUDA(ps_alloc(&bits, (size_t)(Rp * W), s));
   PS_CUDA(ps_alloc(&d_rf, (size_t)std::max<int64_t>(R, 1), s));
   PS_CUDA(ps_alloc(&d_rl, (size_t)std::max<int64_t>(R, 1), s));
@@ -714,9 +740,8 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
       ps_free(Pq, s);
     }
   }
-  int count = 0;
   int frc = group_finish_replay(test, lab, val, lo, hi, student, Mn, Ms, Mq, d_off, bits, rep, repc, cap, stat, p, eff,
-                                &count, s);
+                                s);
   if (frc) return frc;
   ps_free(bits, s);
   ps_free(d_rf, s);
@@ -727,7 +752,6 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   ps_free(Mq, s);
   ps_free(rep, s);
   ps_free(repc, s);
-  if (count > cap) return ps_fail(PS_ERR_INVALID, "too many ill-conditioned cells for the exact replay list");
   return PS_OK;
 }
 
@@ -842,7 +866,7 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
     }
   j->R = off[Fc];
   j->Rp = std::max<int64_t>(T, ps_round_up(j->R, T));
-  j->cap = (int)std::min<int64_t>(Fc * Fq, 1 << 22);
+  j->cap = replay_cap(Fc * Fq);
   const int64_t W = val->W;
   cudaError_t e = cudaSuccess;
   auto ok = [&](cudaError_t x) { e = x; return x == cudaSuccess; };
@@ -911,17 +935,14 @@ int ps_group_moment_end(ps_group_job* j, double* stat, double* p, double* eff, c
     mixed_label_check_kernel<<<grid, 128, 0, s>>>(lab->d_bad, val->d_mask, val->W, 0, Fc, 0, Fq, ds->d_err);
     ps_count_launch();
   }
-  int count = 0;
   if (!rc && (stat || p || eff))
     rc = group_finish_replay(j->test, lab, val, 0, Fc * Fq, j->student, j->Mn, j->Ms, j->Mq, j->d_off, j->bits, j->rep,
-                             j->repc, j->cap, stat, p, eff, &count, s);
+                             j->repc, j->cap, stat, p, eff, s);
   if (j->home != s) {
     cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s);
     cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0);
   }
-  const int cap = j->cap;
   group_job_free(j, j->home);
-  if (!rc && count > cap) return ps_fail(PS_ERR_INVALID, "too many ill-conditioned cells for the exact replay list");
   return rc;
 }
 

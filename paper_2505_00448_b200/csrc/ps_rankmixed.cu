@@ -467,16 +467,35 @@ __global__ void rank_mixed_finish_kernel(int test, RankSums in, const int32_t* _
 // counts f(n0, n1, u) are the coefficients of the Gaussian binomial
 // [n0+n1 choose n0]_q, built by P <- P (1 - q^(n1+i)) / (1 - q^i); every step
 // is an exact int64 polynomial, identical to the reference's DP table row.
-__global__ void mwu_exact_kernel(RankSums in, int64_t Fq, const int2* __restrict__ list,
-                                 const int* __restrict__ count_ptr, int cap, double* __restrict__ pout) {
+//
+// The finish kernel lists the cells that need it; when the list overflowed
+// (more exact cells than its capacity -- e.g. u_mode='exact' on a wide matrix
+// with S <= 64) every cell of the range is re-decided here with the same
+// predicate, so no exact p is ever dropped.
+__global__ void mwu_exact_kernel(RankSums in, int64_t Fc, int64_t Fq, int64_t lo, int64_t hi, int mode,
+                                 const int2* __restrict__ list, const int* __restrict__ count_ptr, int cap,
+                                 double* __restrict__ pout) {
   __shared__ long long poly[1152];  // degree <= a (b + 1) <= 32 * 33 during the product
-  const int count = min(*count_ptr, cap);
-  for (int it = blockIdx.x; it < count; it += gridDim.x) {
-    const int64_t g = list[it].x, h = list[it].y;
+  const int count = *count_ptr;
+  const bool all_cells = count > cap;
+  const int64_t n_items = all_cells ? Fc * (hi - lo) : count;
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int64_t g, h;
+    if (all_cells) {
+      g = it / (hi - lo);
+      h = lo + it % (hi - lo);
+    } else {
+      g = list[it].x;
+      h = list[it].y;
+    }
     const int64_t pair = g * Fq + h;
     const long long n0 = in.cnt[pair * in.KM + 0];
     const long long n1 = in.cnt[pair * in.KM + 1];
     const double r0 = (double)in.r2[pair * in.KM + 0] * 0.5;
+    if (all_cells) {  // block-uniform decision (every thread reads the same cell)
+      double a_, b_, c_;
+      if (!mwu_finish(n0, n1, r0, (double)in.tie[pair], mode, &a_, &b_, &c_, nullptr)) continue;
+    }
     const int a = (int)(n0 < n1 ? n0 : n1), bb = (int)(n0 < n1 ? n1 : n0);
     const int umax = (int)(n0 * n1);
     if (threadIdx.x == 0) {
@@ -631,7 +650,11 @@ int ps_rank_mixed_begin(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   const int64_t npairs = Fc * Fq;
   // per-pair level stride: the template width, or the real level count for k > 16
   j->rs = RankSums{KM > 16 ? (kmax + 31) / 32 * 32 : KM, nullptr, nullptr, nullptr};
-  j->excap = (int)std::min<int64_t>(Fc * std::max<int64_t>(1, j->hi - j->lo), 1 << 20);
+  // exact-U cell list (cold path); PS_EXACT_CAP shrinks it so the tests can
+  // exercise the overflow re-scan of mwu_exact_kernel
+  int64_t cap_lim = 1 << 20;
+  if (const char* e = getenv("PS_EXACT_CAP")) cap_lim = std::max(1L, atol(e));
+  j->excap = (int)std::min<int64_t>(Fc * std::max<int64_t>(1, j->hi - j->lo), cap_lim);
   cudaError_t e = cudaSuccess;
   auto ok = [&](cudaError_t x) { e = x; return x == cudaSuccess; };
   if (ok(ps_alloc(&j->rs.cnt, (size_t)(npairs * j->rs.KM), s)) && ok(ps_alloc(&j->rs.r2, (size_t)(npairs * j->rs.KM), s)) &&
@@ -689,7 +712,8 @@ int ps_rank_mixed_end(ps_rank_job* j, double* stat, double* p, double* eff, cuda
     ps_count_launch();
     if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "rank finish launch");
     if (!rc && !j->kw && j->u_mode != PS_U_ASYMPTOTIC && p) {
-      mwu_exact_kernel<<<ds->num_sms, 32, 0, s>>>(j->rs, Fq, j->exl, j->exc, j->excap, p);
+      mwu_exact_kernel<<<ds->num_sms * 8, 32, 0, s>>>(j->rs, Fc, Fq, lo, hi, j->u_mode, j->exl, j->exc, j->excap,
+                                                      p);
       ps_count_launch();
       if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "mwu exact launch");
     }

@@ -124,12 +124,14 @@ def all_gather(out, inp) -> None:
     if world == 1:
         out.copy_(inp.reshape(out.shape))
         return
-    if tdist.get_backend() == "nccl" or not out.is_cuda:
+    if tdist.get_backend() == "nccl":
         tdist.all_gather_into_tensor(out, inp)
         return
-    o = out.cpu()
-    tdist.all_gather_into_tensor(o, inp.cpu())
-    out.copy_(o)
+    # gloo: flat host buffers (its all-gather wants matching 1-D chunks)
+    o = out.detach().cpu().reshape(-1) if out.is_cuda else out.reshape(-1)
+    tdist.all_gather_into_tensor(o, inp.detach().cpu().reshape(-1).contiguous())
+    if out.is_cuda or o.data_ptr() != out.data_ptr():
+        out.copy_(o.view(out.shape))
 
 
 # --------------------------------------------------------------------------

@@ -6,7 +6,10 @@ recomputes sampled row ranges of it (the oracle takes the reference's
 features cost seconds), and the full matrices are checked for the
 size-independent properties of the outputs: symmetry, value ranges, NaN
 diagonal of adjusted matrices, Bonferroni = min(1, m p) and BH monotone
-(p <= p_bh <= p_bonferroni).
+(p <= p_bh <= p_bonferroni).  The adjusted matrices are compared by VALUE:
+bit for bit with the oracle's adjustment of the device p, and (configs 1-4,
+where the whole oracle run takes seconds) within the p tolerance of the
+oracle's own end-to-end adjusted matrices.
 """
 
 from __future__ import annotations
@@ -98,6 +101,20 @@ def test_full_size_against_oracle_rows(oracle, cfg_key, test):
         exp_b = np.minimum(1.0, m * fam)
         assert bitwise_equal(pb[iu], exp_b)
         assert np.isnan(np.diag(pb)).all()
+    # adjusted matrices: bit for bit the oracle's adjust (adjust.py:46-87) of
+    # the device p, and -- where the whole oracle run takes seconds -- within
+    # the p-value tolerance of the oracle's end-to-end adjusted matrices
+    adj_names = [n for n in ("p_bonferroni", "p_bh") if n in req.outputs]
+    for n in adj_names:
+        method = {"p_bonferroni": "bonferroni", "p_bh": "bh"}[n]
+        assert bitwise_equal(res[n], oracle.adjust(p, method, homog)), (test, n)
+    if adj_names and cfg_key != "5s":
+        ref_p = oracle.compute(test, ma, mb, wanted={"p"})["p"]
+        for n in adj_names:
+            method = {"p_bonferroni": "bonferroni", "p_bh": "bh"}[n]
+            want = oracle.adjust(ref_p, method, homog)
+            assert same_nan(res[n], want), (test, n)
+            assert p_close(res[n], want, rtol=2e-6), (test, n)
     if "p_bh" in req.outputs:
         bh = res["p_bh"]
         if homog:

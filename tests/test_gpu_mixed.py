@@ -87,6 +87,8 @@ def test_anova_config4_slice(oracle):
     ref = oracle.oracle_run(req, a, b)
     _check_moment(res, ref, ("stat", "p", "partial_eta2"))
     assert same_nan(res["p_bh"], ref["p_bh"])
+    assert p_close(res["p_bh"], ref["p_bh"], rtol=2e-6)
+    assert bitwise_equal(res["p_bh"], oracle.adjust(res["p"], "bh", False))
 
 
 def test_anova_label_out_of_range():
@@ -208,6 +210,8 @@ def test_kruskal_config4_slice(oracle):
     res, ref = ps.run(req, a, b), oracle.oracle_run(req, a, b)
     assert bitwise_equal(res["stat"], ref["stat"])
     assert p_close(res["p"], ref["p"]) and same_nan(res["p_bh"], ref["p_bh"])
+    assert p_close(res["p_bh"], ref["p_bh"], rtol=2e-6)
+    assert bitwise_equal(res["p_bh"], oracle.adjust(res["p"], "bh", False))
 
 
 @pytest.mark.parametrize("test", ["kruskal", "mwu"])

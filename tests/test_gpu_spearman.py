@@ -87,6 +87,8 @@ def test_spearman_config2_slice(oracle):
     ref = oracle.oracle_run(req, mat)
     _check(res, ref)
     assert same_nan(res["p_bh"], ref["p_bh"])
+    assert p_close(res["p_bh"], ref["p_bh"], rtol=2e-6)
+    assert bitwise_equal(res["p_bh"], oracle.adjust(res["p"], "bh", True))
 
 
 @pytest.mark.parametrize("S", [500, 6000, 20000])
