@@ -452,7 +452,8 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
     def step():
         xa = dist.gather_input(shard_a, wl.Fa)          # NCCL all-gather of the shards (N > 1)
         xb = dist.gather_input(shard_b, wl.Fb) if shard_b is not None else None
-        if world > 1 and test == "spearman":
+        shard_presort = world > 1 and S <= 65535  # sharded tables are 16-bit
+        if shard_presort and test == "spearman":
             # each rank presorts 1/world of the features; NCCL all-gathers the tables
             da = blocks.DeviceMatrix(xa, wl.kind_a, workloads.SENTINEL, wl.cat_a, n_samples=S, stream=stream)
             da.presort_sharded(rank, world, stream=stream)
@@ -463,8 +464,8 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
         if xb is not None:
             rank_walk = test in ("mwu", "kruskal")
             db = blocks.DeviceMatrix(xb, wl.kind_b, workloads.SENTINEL, None, n_samples=S,
-                                     presort=rank_walk and world == 1, stream=stream)
-            if rank_walk and world > 1:  # the walk only touches this rank's features
+                                     presort=rank_walk and not shard_presort, stream=stream)
+            if rank_walk and shard_presort:  # the walk only touches this rank's features
                 db.presort_rows_only(lo, hi, stream=stream)
         blocks.block(test, da, db, lo, hi, outs, stream=stream)
         if adj_methods:

@@ -524,6 +524,9 @@ int ps_matrix_destroy(ps_matrix* m) {
   ps_free(m->d_codes, s);
   ps_free(m->d_zero, s);
   ps_free(m->d_bad, s);
+  ps_free(m->d_order32, s);
+  ps_free(m->d_lastb32, s);
+  ps_free(m->d_nextb32, s);
   if (m->owns_presort) {
     ps_free(m->d_order, s);
     ps_free(m->d_inv, s);
@@ -710,7 +713,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
   };
   g_tl.mark("start", s);
   const bool no_overlap = getenv("PS_NO_OVERLAP") != nullptr;
-  const bool overlap = test == PS_TEST_SPEARMAN && any_out && !no_overlap;
+  const bool overlap = test == PS_TEST_SPEARMAN && any_out && !no_overlap && !ps_spearman_wide(a->n_samples);
   // (only when the tile triangle alone fills the GPU: small matrices keep the
   // split-K whole-matrix launch)
   const int64_t nt_p = (rows + 63) / 64;

@@ -45,6 +45,12 @@ struct ps_matrix {
   uint16_t* d_lastb = nullptr;    // F x ldt: prefix-max boundary position per word
   uint16_t* d_nextb = nullptr;    // F x ldt: suffix-min boundary position per word
   uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
+  // S > 65535 ("wide"): 32-bit orders and tie prefix tables instead of the
+  // 16-bit ones (no inverse permutation); walked by the wide rank kernels
+  bool wide = false;
+  uint32_t* d_order32 = nullptr;  // F x ldo
+  uint32_t* d_lastb32 = nullptr;  // F x ldt
+  uint32_t* d_nextb32 = nullptr;  // F x ldt
   void* presort_scratch[4] = {nullptr, nullptr, nullptr, nullptr};  // global radix path (S > 20480)
   // device-side presort in row chunks on the auxiliary stream: (rows [0, r1)
   // presorted, event) -- rank walks start on the chunks already done
@@ -151,6 +157,7 @@ int ps_spearman_end(ps_spearman_job* job, cudaStream_t s);
 void ps_spearman_abort(ps_spearman_job* job, cudaStream_t s);
 int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho,
                     cudaStream_t s);
+bool ps_spearman_wide(int64_t S);  // S beyond the shared-memory walk (wide walk, no upload overlap)
 int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* phi,
                 double* v, cudaStream_t s);
 int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi,

@@ -66,12 +66,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_buf, int& total)
   return before + x - v;
 }
 
+// OT = uint16_t (S <= 65535: 16-bit tables + inverse permutation) or
+// uint32_t (wide: S > 65535, no inverse)
+template <typename OT>
 __global__ void __launch_bounds__(NT)
 presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
                int64_t W, int64_t S, uint64_t* __restrict__ keyA, uint32_t* __restrict__ idxA,
-               uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, uint16_t* __restrict__ order,
+               uint64_t* __restrict__ keyB, uint32_t* __restrict__ idxB, OT* __restrict__ order,
                uint16_t* __restrict__ inv, int64_t ldo, uint32_t* __restrict__ tb,
-               uint16_t* __restrict__ lastb, uint16_t* __restrict__ nextb, int64_t ldt,
+               OT* __restrict__ lastb, OT* __restrict__ nextb, int64_t ldt,
                uint8_t* __restrict__ tied, int32_t* __restrict__ lens, int64_t f0) {
   __shared__ int warp_buf[NW];
   __shared__ uint32_t hist[8][256];
@@ -185,24 +188,25 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
   }
 
   // 3. outputs: order, inverse permutation, tie-group boundary tables
-  uint16_t* ord = order + f * ldo;
-  uint16_t* iv = inv + f * ldo;
+  OT* ord = order + f * ldo;
+  uint16_t* iv = inv ? inv + f * ldo : nullptr;
   // positions past n hold the sentinel sample id S, whose inverse is 0xFFFF
   // (absent), so walks over whole 32-position words need no bounds checks
-  for (int64_t s = threadIdx.x; s < ldo; s += NT) iv[s] = 0xFFFF;
+  if (iv)
+    for (int64_t s = threadIdx.x; s < ldo; s += NT) iv[s] = 0xFFFF;
   __syncthreads();
   for (int64_t p = threadIdx.x; p < ldo; p += NT) {
     if (p < n) {
       const uint32_t s = iA[p];
-      ord[p] = (uint16_t)s;
-      iv[s] = (uint16_t)p;
+      ord[p] = (OT)s;
+      if (iv) iv[s] = (uint16_t)p;
     } else {
-      ord[p] = (uint16_t)S;
+      ord[p] = (OT)S;
     }
   }
   uint32_t* tbr = tb + f * ldt;
-  uint16_t* lbr = lastb + f * ldt;
-  uint16_t* nbr = nextb + f * ldt;
+  OT* lbr = lastb + f * ldt;
+  OT* nbr = nextb + f * ldt;
   const int nw = (int)ldt;
   for (int w = warp; w < nw; w += NW) {
     const int p = w * 32 + lane;
@@ -229,23 +233,24 @@ presort_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __re
         if (lane >= o) x = max(x, y);
       }
       x = max(x, carry);
-      if (w < nw) lbr[w] = (uint16_t)x;
+      if (w < nw) lbr[w] = (OT)x;
       carry = __shfl_sync(PS_FULL, x, 31);
     }
   } else if (warp == 1) {  // nextb: inclusive suffix min of the first boundary per word
-    int carry = 0xFFFF;
+    const int none = sizeof(OT) == 2 ? 0xFFFF : 0x7FFFFFFF;
+    int carry = none;
     const int last0 = ((nw - 1) / 32) * 32;
     for (int w0 = last0; w0 >= 0; w0 -= 32) {
       const int w = w0 + lane;
       const uint32_t word = w < nw ? tbr[w] : 0u;
-      int x = word ? w * 32 + __ffs(word) - 1 : 0xFFFF;
+      int x = word ? w * 32 + __ffs(word) - 1 : none;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_down_sync(PS_FULL, x, o);
         if (lane + o < 32) x = min(x, y);
       }
       x = min(x, carry);
-      if (w < nw) nbr[w] = (uint16_t)x;
+      if (w < nw) nbr[w] = (OT)x;
       carry = __shfl_sync(PS_FULL, x, 0);
     }
   }
@@ -550,10 +555,18 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
 static int presort_scratch(ps_matrix* m, cudaStream_t s);
 
 int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
-  if (m->S > 65535)
-    return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
   m->ldo = ps_round_up(m->S + 1, 64);  // room for the sentinel sample id S
   m->ldt = tie_words(m->S);
+  if (m->S > 65535) {  // wide: 32-bit orders and tie prefix tables
+    m->wide = true;
+    PS_CUDA(ps_alloc(&m->d_order32, (size_t)(m->F * m->ldo), s));
+    PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
+    PS_CUDA(ps_alloc(&m->d_lastb32, (size_t)(m->F * m->ldt), s));
+    PS_CUDA(ps_alloc(&m->d_nextb32, (size_t)(m->F * m->ldt), s));
+    PS_CUDA(ps_alloc(&m->d_tied, (size_t)m->F, s));
+    PS_CUDA(ps_alloc(&m->d_len, (size_t)m->F, s));
+    return presort_scratch(m, s);
+  }
   PS_CUDA(ps_alloc(&m->d_order, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_inv, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
@@ -569,7 +582,7 @@ int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
 int ps_presort_attach(ps_matrix* m, uint16_t* order, uint16_t* inv, uint32_t* tb, uint16_t* lastb, uint16_t* nextb,
                       uint8_t* tied, int32_t* len, cudaStream_t s) {
   if (m->S > 65535)
-    return ps_fail(PS_ERR_INVALID, "rank tests on more than 65535 samples are not supported yet");
+    return ps_fail(PS_ERR_INVALID, "caller-owned (sharded) presort tables hold 16-bit orders: samples <= 65535");
   m->ldo = ps_round_up(m->S + 1, 64);
   m->ldt = tie_words(m->S);
   m->d_order = order;
@@ -612,12 +625,21 @@ int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
     PS_LAUNCHED();
     return PS_OK;
   };
+  if (m->wide) {
+    presort_kernel<uint32_t><<<(unsigned)nf, NT, 0, s>>>(
+        m->d_vals, m->ld, m->d_mask, m->W, m->S, static_cast<uint64_t*>(m->presort_scratch[0]),
+        static_cast<uint32_t*>(m->presort_scratch[2]), static_cast<uint64_t*>(m->presort_scratch[1]),
+        static_cast<uint32_t*>(m->presort_scratch[3]), m->d_order32, nullptr, m->ldo, m->d_tb, m->d_lastb32,
+        m->d_nextb32, m->ldt, m->d_tied, m->d_len, f0);
+    PS_LAUNCHED();
+    return PS_OK;
+  }
   if (items <= 4) return smem_path(presort_smem_kernel<4>, 4);
   if (items <= 8) return smem_path(presort_smem_kernel<8>, 8);
   if (items <= 12) return smem_path(presort_smem_kernel<12>, 12);
   if (items <= 16) return smem_path(presort_smem_kernel<16>, 16);
   if (items <= 20) return smem_path(presort_smem_kernel<20>, 20);
-  presort_kernel<<<(unsigned)nf, NT, 0, s>>>(
+  presort_kernel<uint16_t><<<(unsigned)nf, NT, 0, s>>>(
       m->d_vals, m->ld, m->d_mask, m->W, m->S, static_cast<uint64_t*>(m->presort_scratch[0]),
       static_cast<uint32_t*>(m->presort_scratch[2]), static_cast<uint64_t*>(m->presort_scratch[1]),
       static_cast<uint32_t*>(m->presort_scratch[3]), m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,

@@ -26,6 +26,7 @@
 #include "ps_internal.cuh"
 #include "ps_specfun.cuh"
 #include "ps_ties.cuh"
+#include "ps_wide.cuh"
 #include <math_constants.h>
 #include <algorithm>
 
@@ -543,6 +544,105 @@ __global__ void binary_codes_kernel(const uint32_t* __restrict__ mask, const uin
   }
 }
 
+// Wide walk (S beyond the shared-memory walk; ps_wide.cuh): one CTA per
+// (label row g, continuous feature h) pair from an atomic queue, g fastest.
+// Walk h's order keeping the samples whose label is present, then add each
+// kept position's doubled rank 2r = Pfx(gs) + Pfx(ge) + 1 to its level
+// (per-warp shared accumulators) and sum(t^3 - t) over the tie groups of the
+// kept samples -- the same exact sums the shared-memory walk produces
+// (mixed.py:366-403, :581-623), finished by rank_mixed_finish_kernel.
+template <typename OT>
+__global__ void __launch_bounds__(wide::WT, 1)
+rank_mixed_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t* __restrict__ tb,
+                       const OT* __restrict__ lastb, const OT* __restrict__ nextb, int64_t ldt,
+                       const int32_t* __restrict__ len, const uint8_t* __restrict__ codes, int64_t ldc,
+                       const uint32_t* __restrict__ lmask, int64_t lW, int64_t Fc, int64_t Fq, int64_t lo, int64_t hi,
+                       uint32_t* __restrict__ scratch, int64_t scr, int* __restrict__ queue, RankSums rs,
+                       int* __restrict__ err) {
+  extern __shared__ unsigned long long wacc[];  // [WW][KM] r2 sums, then [WW][KM] counts (u32)
+  __shared__ uint32_t sbuf[wide::WW];
+  __shared__ unsigned long long ubuf[wide::WW];
+  __shared__ long long s_item;
+  const int KM = rs.KM;
+  unsigned int* wcnt = reinterpret_cast<unsigned int*>(wacc + wide::WW * KM);
+  const int warp = threadIdx.x >> 5;
+  const int64_t kw = ldo / 32 + 2;
+  uint32_t* K = scratch + blockIdx.x * scr;
+  uint32_t* P = K + kw;
+  const int64_t total = (hi - lo) * Fc;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    for (int i = threadIdx.x; i < wide::WW * KM; i += wide::WT) {
+      wacc[i] = 0ull;
+      wcnt[i] = 0u;
+    }
+    __syncthreads();
+    const int64_t t = s_item;
+    if (t >= total) break;
+    const int64_t h = lo + t / Fc, g = t % Fc;
+    const OT* oh = order + h * ldo;
+    const uint32_t* tbh = tb + h * ldt;
+    const uint8_t* cg = codes + g * ldc;
+    const uint32_t nh = (uint32_t)len[h];
+    wide::keep_scan(oh, nh, lmask + g * lW, K, P, sbuf);
+    long long tie = 0;
+    for (uint32_t q = threadIdx.x; q < nh; q += wide::WT) {
+      const uint32_t te = wide::tie_end(tbh, nextb + h * ldt, q);
+      if ((tbh[q >> 5] >> (q & 31u)) & 1u) {  // q starts a tie group: its kept count
+        const long long c = (long long)(wide::pfx(K, P, te) - wide::pfx(K, P, q));
+        tie += c * c * c - c;
+      }
+      if (!((K[q >> 5] >> (q & 31u)) & 1u)) continue;
+      const uint32_t r2 = wide::pfx(K, P, wide::tie_start(tbh, lastb + h * ldt, q)) + wide::pfx(K, P, te) + 1u;
+      const uint32_t lv = cg[(uint32_t)oh[q]];
+      if (lv >= (uint32_t)KM) {
+        ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
+        continue;
+      }
+      atomicAdd(&wacc[warp * KM + lv], (unsigned long long)r2);
+      atomicAdd(&wcnt[warp * KM + lv], 1u);
+    }
+    const unsigned long long tsum = wide::block_sum_u64((unsigned long long)tie, ubuf);  // ends with a barrier
+    const int64_t pair = g * Fq + h;
+    for (int j = threadIdx.x; j < KM; j += wide::WT) {
+      unsigned long long r = 0;
+      unsigned int c = 0;
+      for (int w = 0; w < wide::WW; ++w) {
+        r += wacc[w * KM + j];
+        c += wcnt[w * KM + j];
+      }
+      rs.r2[pair * KM + j] = r;
+      rs.cnt[pair * KM + j] = (int32_t)c;
+    }
+    if (threadIdx.x == 0) rs.tie[pair] = (long long)tsum;
+    __syncthreads();
+  }
+}
+
+template <typename OT>
+int launch_wide_walk(ps_matrix* lab, ps_matrix* val, const OT* order, const OT* lastb, const OT* nextb,
+                     const uint8_t* codes, int64_t lo, int64_t hi, RankSums rs, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  const int grid = ds->num_sms;
+  const int64_t scr = 2 * (val->ldo / 32 + 2);
+  const size_t smem = (size_t)wide::WW * rs.KM * (8 + 4);
+  uint32_t* scratch = nullptr;
+  int* queue = nullptr;
+  PS_CUDA(ps_alloc(&scratch, (size_t)(grid * scr), s));
+  PS_CUDA(ps_alloc(&queue, 1, s));
+  PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+  PS_CUDA(cudaFuncSetAttribute(rank_mixed_wide_kernel<OT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ps_prof_begin("rank_mixed_walk", s);
+  rank_mixed_wide_kernel<OT><<<grid, wide::WT, smem, s>>>(order, val->ldo, val->d_tb, lastb, nextb, val->ldt,
+                                                          val->d_len, codes, lab->ldc, lab->d_mask, lab->W, lab->F,
+                                                          val->F, lo, hi, scratch, scr, queue, rs, ds->d_err);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  ps_free(scratch, s);
+  ps_free(queue, s);
+  return PS_OK;
+}
+
 size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc, int KM) {
   auto r16 = [](size_t b) { return (b + 15) & ~size_t(15); };
   return r16(ldo * 2) + r16(ldt * 4) + 2 * r16(ldt * 2) + 2 * r16(ldt * 4) + 2 * r16(ldc) +
@@ -557,8 +657,10 @@ int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo
   auto kern = rank_mixed_walk_kernel<KM>;
   cudaFuncAttributes fa{};
   PS_CUDA(cudaFuncGetAttributes(&fa, kern));
-  if (smem + fa.sharedSizeBytes > 227 * 1024)
-    return ps_fail(PS_ERR_INVALID, "rank walk: sample count too large for shared memory");
+  if (val->wide) return launch_wide_walk<uint32_t>(lab, val, val->d_order32, val->d_lastb32, val->d_nextb32, codes, lo,
+                                                   hi, rs, s);
+  if (smem + fa.sharedSizeBytes > 227 * 1024)  // tables beyond shared memory: the wide walk
+    return launch_wide_walk<uint16_t>(lab, val, val->d_order, val->d_lastb, val->d_nextb, codes, lo, hi, rs, s);
   PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   PS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RTH, smem));

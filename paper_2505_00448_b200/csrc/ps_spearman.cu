@@ -31,6 +31,7 @@
 #include "ps_internal.cuh"
 #include "ps_specfun.cuh"
 #include "ps_ties.cuh"
+#include "ps_wide.cuh"
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
@@ -755,6 +756,43 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
   }
 }
 
+// rho / p of one pair from its exact sums: n, raw sums of (2r_g)^2 (ra) and
+// (2r_h)^2 (rc) -- kClosed: tie-free, closed form -- and of (2r_g)(2r_h) (rb).
+__device__ __forceinline__ void spearman_from_sums(long long n, unsigned long long ra, unsigned long long rc,
+                                                   long long rb, double* rho_out, double* p_out, int* err) {
+  double rho = PS_NAN, p = PS_NAN;
+  if (n > 1) {
+    // raw sums of (2r)(2r) -> exact 4 x centred sums (rank totals are
+    // preserved by tie averaging); tie-free walks use the closed form
+    const unsigned long long un = (unsigned long long)n;
+    const long long base = n * (n + 1) * (n + 1);
+    const long long a4 = (long long)(ra == kClosed ? sq_closed(un) : ra) - base;
+    const long long c4 = (long long)(rc == kClosed ? sq_closed(un) : rc) - base;
+    const long long b4 = rb - base;
+    // exact quarter-integers, identical to the reference's fp64 sums
+    const double sxx = (double)a4 * 0.25;
+    const double syy = (double)c4 * 0.25;
+    const double sxy = (double)b4 * 0.25;
+    if (sxx > 0.0 && syy > 0.0) {
+      rho = sxy / sqrt(sxx * syy);
+      if (rho > 1.0) rho = 1.0;
+      else if (rho < -1.0) rho = -1.0;
+      if (n != 2) {
+        if (rho == 1.0 || rho == -1.0) {
+          p = 0.0;
+        } else {
+          const double fn = (double)n;
+          const double t = rho * sqrt((fn - 2.0) / (1.0 - rho * rho));
+          p = 2.0 * psf::t_sf(fabs(t), fn - 2.0, err);
+          if (p > 1.0) p = 1.0;
+        }
+      }
+    }
+  }
+  *rho_out = rho;
+  *p_out = p;
+}
+
 // rho / p from the exact sums (continuous.py:174-203), one thread per pair.
 __host__ __device__ inline int64_t finish_before(int64_t g, int64_t lo, int64_t h0, int64_t h1) {
   // cells (x, h), x in [lo, g), h in [max(x, h0), h1)
@@ -780,38 +818,9 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
     }
     const int64_t g = a, h = (g > h0 ? g : h0) + (t - finish_before(g, lo, h0, h1));
     const int64_t cell = g * F + h;
-    const long long n = in.n[cell];
-    double rho = PS_NAN, p = PS_NAN;
-    if (n > 1) {
-      // raw sums of (2r)(2r) -> exact 4 x centred sums (rank totals are
-      // preserved by tie averaging); tie-free walks use the closed form
-      const unsigned long long un = (unsigned long long)n;
-      const long long base = n * (n + 1) * (n + 1);
-      const unsigned long long ra = (unsigned long long)in.sxx4[cell];
-      const unsigned long long rc = (unsigned long long)in.syy4[cell];
-      const long long a4 = (long long)(ra == kClosed ? sq_closed(un) : ra) - base;
-      const long long c4 = (long long)(rc == kClosed ? sq_closed(un) : rc) - base;
-      const long long b4 = in.sxy4[cell] - base;
-      // exact quarter-integers, identical to the reference's fp64 sums
-      const double sxx = (double)a4 * 0.25;
-      const double syy = (double)c4 * 0.25;
-      const double sxy = (double)b4 * 0.25;
-      if (sxx > 0.0 && syy > 0.0) {
-        rho = sxy / sqrt(sxx * syy);
-        if (rho > 1.0) rho = 1.0;
-        else if (rho < -1.0) rho = -1.0;
-        if (n != 2) {
-          if (rho == 1.0 || rho == -1.0) {
-            p = 0.0;
-          } else {
-            const double fn = (double)n;
-            const double t = rho * sqrt((fn - 2.0) / (1.0 - rho * rho));
-            p = 2.0 * psf::t_sf(fabs(t), fn - 2.0, err);
-            if (p > 1.0) p = 1.0;
-          }
-        }
-      }
-    }
+    double rho, p;
+    spearman_from_sums(in.n[cell], (unsigned long long)in.sxx4[cell], (unsigned long long)in.syy4[cell],
+                       in.sxy4[cell], &rho, &p, err);
     put(stat, F, g, h, rho);
     put(pout, F, g, h, p);
     put(rho_out, F, g, h, rho);
@@ -819,6 +828,104 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
 }
 
 size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs, bool r2) { return (size_t)WalkLayout(ldo, ldt, ogs, r2).words * 4; }
+
+// ---------------------------------------------------------------------------
+// Wide walk (sample counts beyond the shared-memory walk: S > ~50k with the
+// 16-bit tables, S > 65535 with the 32-bit ones; ps_wide.cuh).  One CTA per
+// pair, pairs taken from an atomic queue over the cells (g, h >= g) of rows
+// [lo, hi).  Pass A walks g's order keeping h's samples and scatters g's
+// doubled rank into R[sample] (per-CTA global scratch); pass B walks h's
+// order keeping g's samples and accumulates (2r_g)(2r_h).  Exact integer
+// sums, finished like the shared-memory walk (spearman_from_sums).
+template <typename OT>
+__global__ void __launch_bounds__(wide::WT, 1)
+spearman_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t* __restrict__ tb,
+                     const OT* __restrict__ lastb, const OT* __restrict__ nextb, int64_t ldt,
+                     const int32_t* __restrict__ len, const uint32_t* __restrict__ mask, int64_t W, int64_t F,
+                     int64_t lo, int64_t hi, uint32_t* __restrict__ scratch, int64_t scr, int* __restrict__ queue,
+                     double* __restrict__ stat, double* __restrict__ pout, double* __restrict__ rho_out,
+                     int* __restrict__ err) {
+  __shared__ uint32_t sbuf[wide::WW];
+  __shared__ unsigned long long ubuf[wide::WW];
+  __shared__ long long s_item;
+  const int64_t kw = ldo / 32 + 2;
+  uint32_t* K = scratch + blockIdx.x * scr;
+  uint32_t* P = K + kw;
+  uint32_t* R = P + kw;
+  const int64_t total = finish_before(hi, lo, 0, F);
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
+    __syncthreads();
+    const int64_t t = s_item;
+    if (t >= total) break;
+    int64_t a = lo, b = hi - 1;  // last row g with before(g) <= t
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (finish_before(mid, lo, 0, F) <= t) a = mid;
+      else b = mid - 1;
+    }
+    const int64_t g = a, h = g + (t - finish_before(g, lo, 0, F));
+    const OT* og = order + g * ldo;
+    const OT* oh = order + h * ldo;
+    const uint32_t* tbg = tb + g * ldt;
+    const uint32_t* tbh = tb + h * ldt;
+    // pass A: g's order, kept where h is present; R[s] = 2 r_g(s)
+    const uint32_t n = wide::keep_scan(og, (uint32_t)len[g], mask + h * W, K, P, sbuf);
+    unsigned long long sa = 0, sb = 0, sc = 0;
+    if (n > 1) {
+      for (uint32_t q = threadIdx.x; q < (uint32_t)len[g]; q += wide::WT) {
+        if (!((K[q >> 5] >> (q & 31u)) & 1u)) continue;
+        const uint32_t r2 = wide::pfx(K, P, wide::tie_start(tbg, lastb + g * ldt, q)) +
+                            wide::pfx(K, P, wide::tie_end(tbg, nextb + g * ldt, q)) + 1u;
+        R[(uint32_t)og[q]] = r2;
+        sa += (unsigned long long)r2 * r2;
+      }
+      __syncthreads();
+      // pass B: h's order, kept where g is present
+      wide::keep_scan(oh, (uint32_t)len[h], mask + g * W, K, P, sbuf);
+      for (uint32_t q = threadIdx.x; q < (uint32_t)len[h]; q += wide::WT) {
+        if (!((K[q >> 5] >> (q & 31u)) & 1u)) continue;
+        const uint32_t r2 = wide::pfx(K, P, wide::tie_start(tbh, lastb + h * ldt, q)) +
+                            wide::pfx(K, P, wide::tie_end(tbh, nextb + h * ldt, q)) + 1u;
+        sc += (unsigned long long)r2 * r2;
+        sb += (unsigned long long)r2 * R[(uint32_t)oh[q]];
+      }
+      sa = wide::block_sum_u64(sa, ubuf);
+      sb = wide::block_sum_u64(sb, ubuf);
+      sc = wide::block_sum_u64(sc, ubuf);
+    }
+    if (threadIdx.x == 0) {
+      double rho, p;
+      spearman_from_sums((long long)n, sa, sc, (long long)sb, &rho, &p, err);
+      put(stat, F, g, h, rho);
+      put(pout, F, g, h, p);
+      put(rho_out, F, g, h, rho);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename OT>
+int spearman_wide_launch(ps_matrix* a, const OT* order, const OT* lastb, const OT* nextb, int64_t lo, int64_t hi,
+                         double* stat, double* p, double* rho, cudaStream_t s) {
+  ps_device_state* ds = ps_state();
+  const int grid = ds->num_sms;
+  const int64_t scr = 2 * (a->ldo / 32 + 2) + ps_round_up(a->S, 32);
+  uint32_t* scratch = nullptr;
+  int* queue = nullptr;
+  PS_CUDA(ps_alloc(&scratch, (size_t)(grid * scr), s));
+  PS_CUDA(ps_alloc(&queue, 1, s));
+  PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
+  ps_prof_begin("spearman_walk", s);
+  spearman_wide_kernel<OT><<<grid, wide::WT, 0, s>>>(order, a->ldo, a->d_tb, lastb, nextb, a->ldt, a->d_len, a->d_mask,
+                                                     a->W, a->F, lo, hi, scratch, scr, queue, stat, p, rho,
+                                                     ps_state()->d_err);
+  ps_prof_end(s);
+  PS_LAUNCHED();
+  ps_free(scratch, s);
+  ps_free(queue, s);
+  return PS_OK;
+}
 
 }  // namespace
 
@@ -922,6 +1029,16 @@ static int fold_finish_columns(ps_spearman_job* j, int64_t h0, int64_t h1, cudaS
   if (!rc) rc = finish_launch(j, h0, h1, w);
   if (!rc) j->h_fin = h1;
   return rc;
+}
+
+// true when the shared-memory walk's tables do not fit for S samples (or the
+// presort is 32-bit): such matrices take the wide walk
+bool ps_spearman_wide(int64_t S) {
+  if (S > 65535) return true;
+  const int64_t ldo = ps_round_up(S + 1, 64), ldt = tie_words(S);
+  const size_t limit = 227 * 1024 - 1024;
+  const bool r2 = S <= 32767;
+  return walk_smem(ldo, ldt, false, r2) > limit && walk_smem(ldo, ldt, true, r2) > limit;
 }
 
 int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho, cudaStream_t s,
@@ -1047,6 +1164,11 @@ int ps_spearman_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* 
   if (!a->has_presort) {
     int rc = ps_presort_matrix(a, s);
     if (rc) return rc;
+  }
+  if (ps_spearman_wide(a->S)) {  // beyond the shared-memory walk: one CTA per pair
+    if (a->wide)
+      return spearman_wide_launch<uint32_t>(a, a->d_order32, a->d_lastb32, a->d_nextb32, lo, hi, stat, p, rho, s);
+    return spearman_wide_launch<uint16_t>(a, a->d_order, a->d_lastb, a->d_nextb, lo, hi, stat, p, rho, s);
   }
   // a presort still running in chunks on the auxiliary stream: walk each
   // presorted chunk's columns on the walk streams as it completes

@@ -142,9 +142,37 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
   int rc = ring_for_device(&r);
   if (rc) return rc;
   const size_t row_bytes = (size_t)ldc + (size_t)W * 4;
-  const int64_t rows_per = std::max<int64_t>(1, (int64_t)(kChunk / row_bytes));
-  if ((size_t)rows_per * row_bytes > kChunk) return ps_fail(PS_ERR_INVALID, "label row larger than the staging chunk");
   int b = 0;
+  if (row_bytes > kChunk) {
+    // rows longer than a staging chunk (S of several million): each row in
+    // segments of whole 32-sample words, all host cores per segment
+    const int64_t seg_words = (int64_t)((kChunk - 128) / (32 + 4));  // + room for the padding past S
+    for (int64_t f = 0; f < F; ++f) {
+      const double* row = src + (size_t)f * spitch;
+      for (int64_t w0 = 0; w0 < W; w0 += seg_words, b ^= 1) {
+        const int64_t nw = std::min<int64_t>(seg_words, W - w0);
+        const int64_t q0 = w0 * 32, nq = std::min<int64_t>(S - q0, nw * 32);
+        PS_CUDA(cudaEventSynchronize(r->ev[b]));
+        uint8_t* pc = static_cast<uint8_t*>(r->buf[b]);
+        uint32_t* pz = reinterpret_cast<uint32_t*>(pc + (size_t)seg_words * 32 + 64);
+        const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(nw / 1024) + 1));
+#pragma omp parallel for num_threads(nt) schedule(static)
+        for (int t = 0; t < nt; ++t) {
+          const int64_t a = nw * t / nt, e = nw * (t + 1) / nt;
+          const int64_t qa = a * 32, qe = std::min<int64_t>(nq, e * 32);
+          if (qe > qa) label_row(row + q0 + qa, qe - qa, e - a, (double)cat[f], sent_bits, sent_nan, pc + qa, pz + a);
+        }
+        // codes of the row's last word past S, and the padding to ldc
+        const int64_t cbytes = (w0 + nw == W) ? ldc - q0 : nw * 32;
+        if (cbytes > nq) std::memset(pc + nq, 0xFF, (size_t)(cbytes - nq));
+        PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)f * ldc + q0, pc, (size_t)cbytes, cudaMemcpyHostToDevice, s));
+        PS_CUDA(cudaMemcpyAsync(d_zero + (size_t)f * W + w0, pz, (size_t)nw * 4, cudaMemcpyHostToDevice, s));
+        PS_CUDA(cudaEventRecord(r->ev[b], s));
+      }
+    }
+    return PS_OK;
+  }
+  const int64_t rows_per = std::max<int64_t>(1, (int64_t)(kChunk / row_bytes));
   for (int64_t r0 = 0; r0 < F; r0 += rows_per, b ^= 1) {
     const int64_t nr = std::min<int64_t>(rows_per, F - r0);
     PS_CUDA(cudaEventSynchronize(r->ev[b]));

@@ -310,7 +310,8 @@ def device_compute(request, a_dev, b_dev, a_meta, b_meta, ranges, wanted, stream
     canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
     shape = (a_meta.n_features, a_meta.n_features if b_meta is None else b_meta.n_features)
     S = a_meta.n_samples
-    sharded = world > 1
+    # sharded presort tables are 16-bit (S <= 65535); wider inputs presort whole
+    sharded = world > 1 and S <= 65535
     da = blocks.DeviceMatrix(a_dev, a_meta.kind, a_meta.na_sentinel, a_meta.category_counts, n_samples=S,
                              presort=test == "spearman" and not sharded, stream=stream)
     if test == "spearman" and sharded:  # 1/world of the presort per rank + all-gather

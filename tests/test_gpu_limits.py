@@ -108,3 +108,37 @@ def test_group_replay_chunked_equals_single_list(monkeypatch, test):
     want = ps.run(req, ma, mb)
     monkeypatch.setenv("PS_REPLAY_CAP", "7")
     _same(ps.run(req, ma, mb), want, req.outputs)
+
+
+@pytest.mark.parametrize("S", [55000, 70000])
+def test_spearman_wide_sample_counts(oracle, S):
+    """Beyond the shared-memory walk: S = 55,000 (16-bit tables, wide walk)
+    and S = 70,000 (32-bit presort + wide walk).  rho bit-exact."""
+    rng = np.random.default_rng(S)
+    x = workloads.config_spearman_like(rng, 7, S)
+    x[2, ::5] = np.nan   # NaN data under the numeric sentinel: present, sorts last
+    x[3] = np.round(x[3])  # heavy ties
+    mat = ps.make_matrix(x, "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("spearman", ("stat", "p", "rho", "p_bh"))
+    res, ref = ps.run(req, mat), oracle.oracle_run(req, mat)
+    for n in req.outputs:
+        assert same_nan(res[n], ref[n]), n
+    assert bitwise_equal(res["stat"], ref["stat"]) and bitwise_equal(res["rho"], ref["rho"])
+    assert p_close(res["p"], ref["p"]) and p_close(res["p_bh"], ref["p_bh"], rtol=2e-6)
+
+
+@pytest.mark.parametrize("test", ["kruskal", "mwu"])
+@pytest.mark.parametrize("S", [70000])
+def test_rank_mixed_wide_sample_counts(oracle, test, S):
+    kind = "categorical" if test == "kruskal" else "dichotomous"
+    lab = workloads.simulate(4, S, kind, categories=5, na_ratio=0.1, seed=S + 1)
+    val = workloads.simulate(6, S, "continuous", na_ratio=0.2, seed=S + 2)
+    val[1] = np.round(val[1], 2)  # ties
+    ma, mb = ps.make_matrix(lab, kind), ps.make_matrix(val, "continuous")
+    eff = ps.EFFECTS_BY_TEST[test]
+    req = ps.TestRequest(test, ("stat", "p") + eff)
+    res, ref = ps.run(req, ma, mb), oracle.oracle_run(req, ma, mb)
+    for n in req.outputs:
+        assert same_nan(res[n], ref[n]), n
+    assert bitwise_equal(res["stat"], ref["stat"]) and bitwise_equal(res[eff[0]], ref[eff[0]])
+    assert p_close(res["p"], ref["p"])
