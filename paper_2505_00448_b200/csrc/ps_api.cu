@@ -17,20 +17,24 @@
 
 namespace {
 
-std::recursive_mutex g_lock;
+// One lock per device: callers on the same device are serialised (its
+// streams, pool and error word are shared), callers driving different
+// devices -- a single-process multi-GPU run, one host thread per device --
+// run concurrently.
+std::recursive_mutex g_locks[64];
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
 ps_device_state g_states[64];
-
-struct Guard {
-  std::lock_guard<std::recursive_mutex> lk{g_lock};
-};
 
 int current_device() {
   int d = 0;
   cudaGetDevice(&d);
   return d;
 }
+
+struct Guard {
+  std::lock_guard<std::recursive_mutex> lk{g_locks[current_device() & 63]};
+};
 
 int init_state(ps_device_state* st, int dev) {
   if (st->device == dev) return PS_OK;
@@ -89,9 +93,10 @@ struct ProfRec {
   std::string name;
   cudaEvent_t a, b;
 };
-bool g_prof = false;
+std::atomic<bool> g_prof{false};
+std::mutex g_prof_lock;  // guards g_prof_recs (any device's thread may record)
 std::vector<ProfRec> g_prof_recs;
-ProfRec* g_prof_open = nullptr;
+thread_local int64_t g_prof_open = -1;  // index of this thread's open record
 
 }  // namespace
 
@@ -102,13 +107,15 @@ void ps_prof_begin(const char* name, cudaStream_t s) {
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
   cudaEventRecord(r.a, s);
+  std::lock_guard<std::mutex> lk(g_prof_lock);
   g_prof_recs.push_back(r);
-  g_prof_open = &g_prof_recs.back();
+  g_prof_open = (int64_t)g_prof_recs.size() - 1;
 }
 void ps_prof_end(cudaStream_t s) {
-  if (!g_prof || !g_prof_open) return;
-  cudaEventRecord(g_prof_open->b, s);
-  g_prof_open = nullptr;
+  if (!g_prof || g_prof_open < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_lock);
+  if (g_prof_open < (int64_t)g_prof_recs.size()) cudaEventRecord(g_prof_recs[g_prof_open].b, s);
+  g_prof_open = -1;
 }
 
 ps_device_state* ps_state() { return &g_states[current_device()]; }
@@ -185,15 +192,12 @@ const char* ps_last_error(void) { return g_last_error.c_str(); }
 int64_t ps_kernel_launches(void) { return g_launches.load(); }
 void ps_reset_kernel_launches(void) { g_launches = 0; }
 
-void ps_profile_enable(int on) {
-  Guard g;
-  g_prof = on != 0;
-}
+void ps_profile_enable(int on) { g_prof = on != 0; }
 
 // Sum of event-timed milliseconds and launch count of kernel `name` since the
 // last collect (synchronises on the recorded events); clears the records.
 int ps_profile_collect(const char* name, double* total_ms, int64_t* count) {
-  Guard g;
+  std::lock_guard<std::mutex> lk(g_prof_lock);
   double t = 0.0;
   int64_t c = 0;
   std::vector<ProfRec> keep;
@@ -211,7 +215,7 @@ int ps_profile_collect(const char* name, double* total_ms, int64_t* count) {
     }
   }
   g_prof_recs.swap(keep);
-  g_prof_open = nullptr;
+  g_prof_open = -1;
   *total_ms = t;
   *count = c;
   return PS_OK;
@@ -220,7 +224,7 @@ int ps_profile_collect(const char* name, double* total_ms, int64_t* count) {
 // Union of the named kernel's launch intervals (concurrent launches on
 // several streams count once): the kernel's busy time on the device.
 int ps_profile_collect_union(const char* name, double* busy_ms, int64_t* count) {
-  Guard g;
+  std::lock_guard<std::mutex> lk(g_prof_lock);
   std::vector<std::pair<double, double>> iv;
   std::vector<ProfRec> keep;
   cudaEvent_t base = nullptr;
@@ -254,7 +258,7 @@ int ps_profile_collect_union(const char* name, double* busy_ms, int64_t* count) 
       cudaEventDestroy(r.b);
     }
   g_prof_recs.swap(keep);
-  g_prof_open = nullptr;
+  g_prof_open = -1;
   *busy_ms = busy;
   *count = (int64_t)iv.size();
   return PS_OK;

@@ -333,7 +333,9 @@ __global__ void pearson_replay_kernel(const double* __restrict__ vals, int64_t l
           sxy += dx * dy;
         }
       }
-      if (sxx > 0.0 && syy > 0.0) {
+      // the reference's test (continuous.py:34): NaN sums (NaN data under a
+      // numeric sentinel) pass it and reach beta_sym_sf, which raises
+      if (!(sxx <= 0.0 || syy <= 0.0)) {
         r = sxy / sqrt(sxx * syy);
         if (r > 1.0) r = 1.0;
         else if (r < -1.0) r = -1.0;
@@ -386,12 +388,8 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   PS_CUDA(cudaMemsetAsync(o.replay_count, 0, sizeof(int), s));
   if (nsplit > 1) PS_CUDA(ps_alloc(&ws, (size_t)(ntiles * nsplit * 6 * T * T), s));
 
-  static bool attr_set = false;
-  if (!attr_set) {
-    PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmemBytes));
-    attr_set = true;
-  }
+  // (a function attribute is per device: set it on every call)
+  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
   const int64_t grid = ntiles * nsplit;
   ps_prof_begin("pearson_tile", s);
   pearson_tile_kernel<<<(unsigned)grid, NTHR, kSmemBytes, s>>>(

@@ -179,8 +179,10 @@ class TestRequest:
     """One run's configuration (reference ``datamodel.py:293-338``).
 
     ``threads`` is accepted for API compatibility; the device path ignores it.
-    ``devices`` (an extension) selects how many local GPUs a single-process
-    run may use; results never depend on it.
+    ``devices`` (an extension, SURVEY §8(b) "a device-count knob without
+    changing signatures") shards one run over local GPUs from one process:
+    an int N uses devices 0..N-1, a tuple names them (repeats allowed: logical
+    shards on one GPU, for testing).  Results never depend on it.
     """
 
     __test__ = False  # not a pytest class
@@ -191,8 +193,14 @@ class TestRequest:
     u_mode: str = "auto"
     threads: int = 1
     features_on_rows: bool = True
+    devices: int | tuple[int, ...] = 1
 
     def __post_init__(self) -> None:
+        if isinstance(self.devices, int):
+            if self.devices < 1:
+                raise ValueError(f"devices must be >= 1, got {self.devices}")
+        elif not self.devices or any((not isinstance(d, int)) or d < 0 for d in self.devices):
+            raise ValueError(f"devices must be a count or a tuple of device ids, got {self.devices!r}")
         if self.test not in TESTS:
             raise ValueError(f"unknown test {self.test!r}; expected one of {TESTS}")
         if self.t_variant not in T_VARIANTS:

@@ -296,22 +296,28 @@ def device_inputs(inputs, stream=None):
     return out
 
 
-def device_compute(request, a_dev, b_dev, a_meta, b_meta, ranges, wanted, stream=None):
+def device_compute(request, a_dev, b_dev, a_meta, b_meta, ranges, wanted, stream=None, rank=None, world=None):
     """This rank's block on the full device inputs: {name: device matrix}
-    holding the rank's cells (NaN elsewhere)."""
+    holding the rank's cells (NaN elsewhere).  ``rank``/``world`` default to
+    the process group's; a single-process run passes its shard index and
+    presorts whole (no collective)."""
     import torch
 
     from . import blocks
     from .datamodel import EFFECTS_BY_TEST
 
-    tdist, world, rank = _world()
+    if rank is None:
+        tdist, world, rank = _world()
+        group = True
+    else:
+        group = False
     test = request.test
     lo, hi = ranges[rank]
     canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
     shape = (a_meta.n_features, a_meta.n_features if b_meta is None else b_meta.n_features)
     S = a_meta.n_samples
     # sharded presort tables are 16-bit (S <= 65535); wider inputs presort whole
-    sharded = world > 1 and S <= 65535
+    sharded = group and world > 1 and S <= 65535
     da = blocks.DeviceMatrix(a_dev, a_meta.kind, a_meta.na_sentinel, a_meta.category_counts, n_samples=S,
                              presort=test == "spearman" and not sharded, stream=stream)
     if test == "spearman" and sharded:  # 1/world of the presort per rank + all-gather
@@ -429,3 +435,129 @@ def _host_sharded(request, mat_a, mat_b, compute, adjust_fn, shape, ranges, need
         else:
             out[name] = full[name]
     return out
+
+
+# --------------------------------------------------------------------------
+# one process, several local GPUs (TestRequest.devices)
+
+def local_run(request, mat_a, mat_b, devices):
+    """``run()`` sharded over local GPUs from one process: one host thread per
+    device (the library locks per device, so the devices run concurrently).
+
+    Shard r uploads its 1/N rows of each input, the full device inputs are
+    assembled from the shards by peer copies (NVLink), shard r computes the
+    reference partition ranges[r] of the pairs, packs its p family cells and
+    raw outputs (``ps_cells_pack``), and the first device gathers the packed
+    vectors (peer copies), adjusts the whole family once and unpacks every
+    segment into the full result matrices, which it copies to the host.
+    Bitwise identical to the one-device run (partition-independent k-order,
+    order-insensitive adjustment).
+    """
+    import threading
+
+    import torch
+
+    from . import _lib, blocks
+    from .datamodel import EFFECTS_BY_TEST, ResultSet
+    from .engine import ADJUSTED_OUTPUTS, validate
+
+    shape = validate(request, mat_a, mat_b)
+    test = request.test
+    n = len(devices)
+    ranges = plan(test, mat_a.n_features, None if mat_b is None else mat_b.n_features, n)
+    canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
+    adj_names = [x for x in request.outputs if x in ADJUSTED_OUTPUTS]
+    needed = {x for x in request.outputs if x not in ADJUSTED_OUTPUTS}
+    if adj_names:
+        needed.add("p")
+    raw_names = [x for x in canonical if x in needed]
+    S = mat_a.n_samples
+    ld = -(-S // 32) * 32
+    mats = [mat_a] + ([mat_b] if mat_b is not None else [])
+    shards = [[None] * len(mats) for _ in range(n)]
+    packs = [None] * n
+    errors = [None] * n
+    barrier = threading.Barrier(n)
+    lib = _lib.load()
+
+    def worker(r):
+        try:
+            dev = devices[r]
+            torch.cuda.set_device(dev)
+            _lib.check(lib.ps_set_device(dev))
+            stream = torch.cuda.current_stream(dev)
+            for i, m in enumerate(mats):  # 1. this shard's rows
+                c, sh = row_shards(m.n_features, n)
+                r0, r1 = sh[r]
+                shards[r][i] = upload_rows(m.values, r0, r1, c, ld, torch.device("cuda", dev), stream)
+            blocks.sync(stream)
+            barrier.wait()
+            full = []
+            for i, m in enumerate(mats):  # 2. the full inputs from every shard (peer copies)
+                c, _ = row_shards(m.n_features, n)
+                t = torch.empty((c * n, ld), dtype=torch.float64, device=dev)
+                for q in range(n):
+                    t[q * c:(q + 1) * c].copy_(shards[q][i], non_blocking=True)
+                full.append(t[:m.n_features])
+            torch.cuda.synchronize(dev)
+            raw = device_compute(request, full[0], full[1] if len(full) > 1 else None, mat_a, mat_b, ranges,
+                                 needed, stream, rank=r, world=n)
+            del full
+            lo, hi = ranges[r]
+            pk = {}
+            for name in raw_names:  # 3. this shard's cells, packed
+                cnt = cells_count(test, True, shape, lo, hi)
+                v = torch.empty(max(1, cnt), dtype=torch.float64, device=dev)
+                _pack(test, True, raw[name], shape, lo, hi, v, stream)
+                pk[name] = (v, cnt)
+            if adj_names:
+                cnt = cells_count(test, False, shape, lo, hi)
+                v = torch.empty(max(1, cnt), dtype=torch.float64, device=dev)
+                _pack(test, False, raw["p"], shape, lo, hi, v, stream)
+                pk["__family"] = (v, cnt)
+            blocks.sync(stream)
+            packs[r] = pk
+            barrier.wait()
+        except Exception as e:  # noqa: BLE001 -- re-raised in the caller
+            errors[r] = e
+            barrier.abort()
+
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(1, n)]
+    for t in threads:
+        t.start()
+    worker(0)
+    for t in threads:
+        t.join()
+    for e in errors:
+        if e is not None and not isinstance(e, threading.BrokenBarrierError):
+            raise e
+    for e in errors:
+        if e is not None:
+            raise e
+    # 4. assembly on the first device
+    dev0 = devices[0]
+    torch.cuda.set_device(dev0)
+    _lib.check(lib.ps_set_device(dev0))
+    stream = torch.cuda.current_stream(dev0)
+    result = {}
+    for name in raw_names:
+        full = torch.full(shape, math.nan, dtype=torch.float64, device=dev0)
+        for q, (lo, hi) in enumerate(ranges):
+            v, cnt = packs[q][name]
+            if cnt:
+                _unpack(test, True, v.to(dev0, non_blocking=True), shape, lo, hi, full, stream)
+        if name in request.outputs:
+            result[name] = full
+    if adj_names:
+        fam = torch.cat([packs[q]["__family"][0][:packs[q]["__family"][1]].to(dev0) for q in range(n)])
+        adj = torch.empty_like(fam)
+        offs = np.cumsum([0] + [packs[q]["__family"][1] for q in range(n)])
+        for name in adj_names:
+            out = torch.full(shape, math.nan, dtype=torch.float64, device=dev0)
+            if fam.numel():
+                blocks.adjust_family_device(fam, fam.numel(), ADJUSTED_OUTPUTS[name], adj, stream)
+            for q, (lo, hi) in enumerate(ranges):
+                _unpack(test, False, adj[int(offs[q]):] if fam.numel() else adj, shape, lo, hi, out, stream)
+            result[name] = out
+    blocks.sync(stream)
+    return ResultSet(matrices={k: v.cpu().numpy() for k, v in result.items()}, shape=shape)

@@ -58,11 +58,29 @@ def validate(request: TestRequest, mat_a: DataMatrix, mat_b: DataMatrix | None) 
     return (mat_a.n_features, mat_b.n_features)
 
 
+def device_list(devices) -> tuple[int, ...]:
+    """TestRequest.devices as a tuple of device ids (validated against the
+    visible devices)."""
+    ids = tuple(range(devices)) if isinstance(devices, int) else tuple(devices)
+    n = _lib.device_count()
+    bad = [d for d in ids if d >= n]
+    if bad:
+        raise ValueError(f"devices {bad} not visible ({n} CUDA device(s))")
+    return ids
+
+
 def run(request: TestRequest, mat_a: DataMatrix, mat_b: DataMatrix | None = None) -> ResultSet:
     """Run one pairwise test on the B200 and return the requested matrices."""
     shape = validate(request, mat_a, mat_b)
     lib = _lib.load()
     _lib.require_device()
+    devices = device_list(request.devices)
+    if len(devices) > 1:  # one process, several local GPUs (dist.local_run)
+        from .dist import local_run
+
+        return local_run(request, mat_a, mat_b, devices)
+    if devices[0] != 0:
+        _lib.check(lib.ps_set_device(devices[0]))
     test = request.test
     canonical = ("stat", "p") + EFFECTS_BY_TEST[test]
     raw = {n: np.empty(shape) for n in request.outputs if n not in ADJUSTED_OUTPUTS}

@@ -88,8 +88,31 @@ def test_nan_data_under_numeric_sentinel_pearson_raises(oracle):
     with pytest.raises(oracle.OracleError):
         oracle.oracle_run(ps.TestRequest("pearson", ("stat", "p")), m)
     # the library recovers: the next call runs normally
+    x = x.copy()  # make_matrix froze the array (datamodel.py:181-188)
     x[2, 7] = 0.5
     m2 = ps.make_matrix(x, "continuous", na_sentinel=-99.0)
     req = ps.TestRequest("pearson", ("stat", "p"))
     ref = oracle.oracle_run(req, m2)
     _compare("pearson", ps.run(req, m2), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("test", ["ttest", "anova"])
+def test_nan_data_under_numeric_sentinel_group_tests_raise(oracle, test):
+    """The reference's t-test / ANOVA also reach t_sf / f_sf with a NaN
+    statistic and raise NonConvergence (checked with pairstat.run)."""
+    import workloads
+
+    kind_a, _ = ps.KINDS_BY_TEST[test]
+    rng = np.random.default_rng(3)
+    lab = workloads.simulate(3, 60, kind_a, categories=3, na_ratio=0.1, seed=4)
+    lab[np.isnan(lab)] = -99.0
+    val = rng.normal(size=(4, 60))
+    val[1, 5] = np.nan
+    ma = ps.make_matrix(lab, kind_a, na_sentinel=-99.0)
+    mb = ps.make_matrix(val, "continuous", na_sentinel=-99.0)
+    req = ps.TestRequest(test, ("stat", "p"))
+    with pytest.raises(oracle.OracleError):
+        oracle.oracle_run(req, ma, mb)
+    with pytest.raises(ps.NonConvergence):
+        ps.run(req, ma, mb)
