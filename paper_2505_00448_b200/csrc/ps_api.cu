@@ -378,12 +378,13 @@ static int matrix_create(const ps_matrix_desc* desc, int values_on_device, int w
     std::memcpy(m->h_cat, desc->category_counts, sizeof(int64_t) * m->F);
     int64_t cmax = 0;
     for (int64_t f = 0; f < m->F; ++f) cmax = std::max(cmax, m->h_cat[f]);
-    if (cmax > 254) {
+    if (cmax > 65534) {
       delete[] m->h_cat;
       delete m;
-      return ps_fail(PS_ERR_INVALID, "category counts above 254 are not supported by the device path");
+      return ps_fail(PS_ERR_INVALID, "category counts above 65534 are not supported by the device path");
     }
     m->cmax = (int)cmax;
+    m->code_bytes = cmax > 254 ? 2 : 1;  // 16-bit label codes beyond 254 levels
     std::vector<int32_t> c32(m->h_cat, m->h_cat + m->F);
     rc = ps_alloc(&m->d_cat, (size_t)m->F, s) == cudaSuccess ? 0 : PS_ERR_CUDA;
     if (!rc) rc = cudaMemcpyAsync(m->d_cat, c32.data(), sizeof(int32_t) * m->F, cudaMemcpyHostToDevice, s)

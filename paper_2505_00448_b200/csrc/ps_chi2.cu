@@ -24,6 +24,29 @@ namespace {
 
 
 // ----------------------------------------------------------------- one-hot
+// 16-bit codes (category counts above 254): 8 samples per thread per step
+__global__ void onehot16_kernel(const uint16_t* __restrict__ codes, int64_t ldc, const int32_t* __restrict__ row_feat,
+                                const int32_t* __restrict__ row_level, int64_t R, int64_t Sp, int64_t S,
+                                uint8_t* __restrict__ O) {
+  const int64_t r = blockIdx.x;
+  uint8_t* out = O + r * Sp;
+  if (r >= R) {
+    for (int64_t s = threadIdx.x * 16; s < Sp; s += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(out + s) = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const uint16_t lev = (uint16_t)row_level[r];
+  const uint16_t* c = codes + row_feat[r] * ldc;
+  for (int64_t s = threadIdx.x * 8; s < Sp; s += blockDim.x * 8) {
+    uint32_t w[2] = {0u, 0u};
+    for (int q = 0; q < 8; ++q) {
+      const int64_t sq = s + q;
+      if (sq < S && c[sq] == lev) w[q >> 2] |= 1u << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint2*>(out + s) = make_uint2(w[0], w[1]);
+  }
+}
+
 __global__ void onehot_kernel(const uint8_t* __restrict__ codes, int64_t ldc, const int32_t* __restrict__ row_feat,
                               const int32_t* __restrict__ row_level, int64_t R, int64_t Sp, int64_t S,
                               uint8_t* __restrict__ O) {
@@ -376,7 +399,8 @@ __global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64
                                    const int32_t* __restrict__ off, const int32_t* __restrict__ cat,
                                    int64_t F, int64_t lo, int64_t hi, double* __restrict__ stat,
                                    double* __restrict__ pout, double* __restrict__ phi_out,
-                                   double* __restrict__ v_out, int* __restrict__ err) {
+                                   double* __restrict__ v_out, int* __restrict__ err, long long* big = nullptr,
+                                   int cmax_big = 0) {
   const int64_t total = (hi - lo) * F;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
        it += (int64_t)gridDim.x * blockDim.x) {
@@ -391,7 +415,11 @@ __global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64
       if (diag && i != j) return 0;
       return (long long)T[(int64_t)i * ldC + j];
     };
-    long long rs[CM], cs[CM];
+    // CM == 0 (category counts above 256): the row / column sums live in
+    // per-thread global scratch slices instead of registers / local memory
+    long long rs_l[CM > 0 ? CM : 1], cs_l[CM > 0 ? CM : 1];
+    long long* rs = CM > 0 ? rs_l : big + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 2 * cmax_big;
+    long long* cs = CM > 0 ? cs_l : rs + cmax_big;
     for (int j = 0; j < ch; ++j) cs[j] = 0;
     long long n = 0;
     for (int i = 0; i < cg; ++i) {
@@ -598,13 +626,21 @@ static int chi2_band(ps_matrix* a, const std::vector<int32_t>& off, int64_t ga, 
   }
   const int64_t total = (gb - ga) * F;
   const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
-  if (a->cmax <= 16)
+  long long* big = nullptr;
+  if (a->cmax <= 16) {
     chi2_finish_kernel<16, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
                                                        ds->d_err);
-  else
+  } else if (a->cmax <= 256) {
     chi2_finish_kernel<256, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
                                                         ds->d_err);
+  } else {
+    const int bb = ds->num_sms * 2;
+    PS_CUDA(ps_alloc(&big, (size_t)bb * 128 * 2 * a->cmax, s));
+    chi2_finish_kernel<0, Acc><<<bb, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v, ds->d_err,
+                                                  big, a->cmax);
+  }
   PS_LAUNCHED();
+  ps_free(big, s);
   ps_free(C, s);
   ps_free(d_tiles, s);
   ps_free(d_units, s);
@@ -650,7 +686,11 @@ int ps_chi2_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, d
     label_check_kernel<<<grid, 128, 0, s>>>(a->d_bad, a->d_mask, W, F, lo, hi, ds->d_err);
     PS_LAUNCHED();
   }
-  onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
+  if (a->code_bytes == 2)
+    onehot16_kernel<<<(unsigned)Rp, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(a->d_codes), a->ldc, d_rf, d_rl, R,
+                                                 Sp, S, O);
+  else
+    onehot_kernel<<<(unsigned)Rp, 256, 0, s>>>(a->d_codes, a->ldc, d_rf, d_rl, R, Sp, S, O);
   PS_LAUNCHED();
   CUtensorMap map;
   {

@@ -48,7 +48,8 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 // one-hot bit rows: row r = (feature row_feat[r], level row_level[r]); level
 // -1 / -2 select the t-test rows (present && v == 0.0 / present && v != 0.0).
-__global__ void onehot_bits_kernel(const uint8_t* __restrict__ codes, int64_t ldc,
+template <typename CT>
+__global__ void onehot_bits_kernel(const CT* __restrict__ codes, int64_t ldc,
                                    const uint32_t* __restrict__ mask, const uint32_t* __restrict__ zero,
                                    int64_t W, const int32_t* __restrict__ row_feat,
                                    const int32_t* __restrict__ row_level, int64_t R, int64_t S,
@@ -68,10 +69,10 @@ __global__ void onehot_bits_kernel(const uint8_t* __restrict__ codes, int64_t ld
     }
     return;
   }
-  const uint8_t* c = codes + f * ldc;
+  const CT* c = codes + f * ldc;
   for (int64_t w = warp; w < W; w += blockDim.x / 32) {
     const int64_t s = w * 32 + lane;
-    const bool hit = s < S && c[s] == (uint8_t)lev;
+    const bool hit = s < S && c[s] == (CT)lev;
     const uint32_t b = __ballot_sync(PS_FULL, hit);
     if (lane == 0) out[w] = b;
   }
@@ -257,9 +258,17 @@ __device__ __forceinline__ void push_replay(const Outs& o, int64_t g, int64_t h)
   if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
 }
 
+// element j of an array of GroupPart fields (stride = sizeof(GroupPart))
+template <typename T>
+struct Strided {
+  const T* p;
+  __device__ T operator[](int j) const;
+};
+
 // mixed.py:453-495 from raw (counts, sums, ssq) -- the exact reference form
-__device__ void anova_finish_raw(const long long* counts, const double* sums, const double* ssq, int k,
-                                 double* f_out, double* p_out, double* eta_out, int* err) {
+template <typename CA, typename SA, typename QA>
+__device__ void anova_finish_raw(CA counts, SA sums, QA ssq, int k, double* f_out, double* p_out, double* eta_out,
+                                 int* err) {
   *f_out = *p_out = *eta_out = PS_NAN;
   if (k < 2) return;
   long long n = 0;
@@ -441,6 +450,10 @@ struct GroupPart {
   long long n;
   double sum, ssq;
 };
+template <typename T>
+__device__ __forceinline__ T Strided<T>::operator[](int j) const {
+  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(p) + (size_t)j * sizeof(GroupPart));
+}
 
 __global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, const int32_t* __restrict__ off,
                                           const double* __restrict__ vals, int64_t ld,
@@ -519,14 +532,9 @@ __global__ void group_replay_finish_kernel(int test, const int2* __restrict__ it
     double r0, r1, r2;
     if (test == PS_TEST_ANOVA) {
       const int k = off[g + 1] - off[g];
-      long long counts[KM];
-      double sums[KM], ssq[KM];
-      for (int j = 0; j < k; ++j) {
-        counts[j] = pp[j].n;
-        sums[j] = pp[j].sum;
-        ssq[j] = pp[j].ssq;
-      }
-      anova_finish_raw(counts, sums, ssq, k, &r0, &r1, &r2, o.err);
+      // the per-group sums stay in the parts array (any level count)
+      anova_finish_raw(Strided<long long>{&pp[0].n}, Strided<double>{&pp[0].sum}, Strided<double>{&pp[0].ssq}, k,
+                       &r0, &r1, &r2, o.err);
     } else {  // one-hot rows: "label == 0", "label != 0"
       ttest_finish_raw(pp[0].n, pp[1].n, pp[0].sum, pp[1].sum, pp[0].ssq, pp[1].ssq, student, &r0, &r1, &r2,
                        o.err);
@@ -556,6 +564,16 @@ __global__ void mixed_label_check_kernel(const uint32_t* __restrict__ bad, const
 }
 
 }  // namespace
+
+static void launch_onehot_bits(ps_matrix* lab, int64_t W, const int32_t* rf, const int32_t* rl, int64_t R, int64_t Rp,
+                               uint32_t* bits, cudaStream_t s) {
+  if (lab->code_bytes == 2)
+    onehot_bits_kernel<uint16_t><<<(unsigned)Rp, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(lab->d_codes), lab->ldc,
+                                                             lab->d_mask, lab->d_zero, W, rf, rl, R, lab->S, bits);
+  else
+    onehot_bits_kernel<uint8_t><<<(unsigned)Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, rf,
+                                                            rl, R, lab->S, bits);
+}
 
 // LabelOutOfRange check of label rows [g0, g1) against continuous features
 // [h0, h1) (also used by the Kruskal-Wallis walk, mixed.py:613-617).
@@ -705,8 +723,7 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
     mixed_label_check_kernel<<<grid, 128, 0, s>>>(lab->d_bad, val->d_mask, W, g0, g1, h0, h1, ds->d_err);
     PS_LAUNCHED();
   }
-  onehot_bits_kernel<<<(unsigned)Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, d_rf,
-                                                  d_rl, R, lab->S, bits);
+  launch_onehot_bits(lab, W, d_rf, d_rl, R, Rp, bits, s);
   PS_LAUNCHED();
   const size_t smem = NSTAGE * sizeof(Stage);
   PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -878,8 +895,7 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
       (j->R == 0 || (ok(cudaMemcpyAsync(j->d_rf, rf.data(), sizeof(int32_t) * j->R, cudaMemcpyHostToDevice, s)) &&
                      ok(cudaMemcpyAsync(j->d_rl, rl.data(), sizeof(int32_t) * j->R, cudaMemcpyHostToDevice, s)))) &&
       ok(cudaMemcpyAsync(j->d_off, off.data(), sizeof(int32_t) * (Fc + 1), cudaMemcpyHostToDevice, s))) {
-    onehot_bits_kernel<<<(unsigned)j->Rp, 256, 0, s>>>(lab->d_codes, lab->ldc, lab->d_mask, lab->d_zero, W, j->d_rf,
-                                                       j->d_rl, j->R, lab->S, j->bits);
+    launch_onehot_bits(lab, W, j->d_rf, j->d_rl, j->R, j->Rp, j->bits, s);
     ps_count_launch();
     e = cudaGetLastError();
   }

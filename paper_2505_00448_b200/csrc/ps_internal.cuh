@@ -31,6 +31,7 @@ struct ps_matrix {
   int32_t* d_cat = nullptr;       // F category counts (device)
   int cmax = 0;
   uint8_t* d_codes = nullptr;     // F x ldc: trunc(label) or 0xFE (present, out of range) / 0xFF (missing)
+  int code_bytes = 1;             // 2 when some category count exceeds 254: uint16 codes, 0xFFFE / 0xFFFF
   uint32_t* d_zero = nullptr;     // F x W bits: present && value == 0.0 (ttest / mwu grouping)
   uint32_t* d_bad = nullptr;      // F x W bits: present && label out of [0, c_f)
   // presort tables (rank tests)
@@ -172,8 +173,8 @@ typedef std::function<int(int64_t, int64_t, cudaEvent_t)> ps_rows_done_fn;
 int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
                     cudaStream_t s, const ps_rows_done_fn& on_rows = nullptr);
 int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
-                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, uint32_t* d_zero, int64_t W,
-                        cudaStream_t s);
+                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, int code_bytes, uint32_t* d_zero,
+                        int64_t W, cudaStream_t s);
 int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld, cudaStream_t s);
 int ps_stage_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void ps_host_prefault(void* dst, size_t bytes);

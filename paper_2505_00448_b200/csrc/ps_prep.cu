@@ -13,12 +13,15 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 
+// CT: uint8_t codes (0xFE out of range, 0xFF missing), or uint16_t when a
+// category count exceeds 254 (0xFFFE / 0xFFFF)
+template <typename CT>
 __global__ void __launch_bounds__(kPrepThreads)
 prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t W,
                  uint64_t sent_bits, int sent_nan, uint32_t* __restrict__ mask,
                  double* __restrict__ center, int32_t* __restrict__ count,
                  // label outputs (nullptr for continuous)
-                 const int32_t* __restrict__ cat, uint8_t* __restrict__ codes, int64_t ldc,
+                 const int32_t* __restrict__ cat, CT* __restrict__ codes, int64_t ldc,
                  uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits, int64_t f0) {
   const int64_t f = f0 + blockIdx.x;
   const double* row = vals + f * ld;
@@ -52,16 +55,16 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
     if (pres) { sum += v; }
     cnt += pres ? 1 : 0;
     if (codes) {
-      uint8_t code = 0xFF;
+      CT code = (CT)~(CT)0;
       bool bad = false;
       if (pres) {
         // int(label) in the reference truncates toward zero (categorical.py:87).
         if (v != v || v <= -1.0 || v >= (double)cf) {
           bad = true;
         } else {
-          code = (uint8_t)(int)trunc(v);
+          code = (CT)(int)trunc(v);
         }
-        if (bad) code = 0xFE;
+        if (bad) code = (CT)~(CT)1;
       }
       if (s < S) codes[f * ldc + s] = code;
       const uint32_t zw = __ballot_sync(PS_FULL, pres && v == 0.0);
@@ -75,7 +78,7 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
   }
   }
   if (codes)
-    for (int64_t s = S + threadIdx.x; s < ldc; s += kPrepThreads) codes[f * ldc + s] = 0xFF;
+    for (int64_t s = S + threadIdx.x; s < ldc; s += kPrepThreads) codes[f * ldc + s] = (CT)~(CT)0;
   // block reduction of (sum, cnt); order is fixed, so the pivot is reproducible.
   __shared__ double ssum[kPrepThreads / 32];
   __shared__ int scnt[kPrepThreads / 32];
@@ -99,19 +102,20 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
 
 // Label matrices staged from the host as codes: presence / out-of-range bit
 // words and present counts from the codes (pivot unused for labels: 0).
+template <typename CT>
 __global__ void __launch_bounds__(kPrepThreads)
-label_bits_kernel(const uint8_t* __restrict__ codes, int64_t ldc, int64_t S, int64_t W,
+label_bits_kernel(const CT* __restrict__ codes, int64_t ldc, int64_t S, int64_t W,
                   uint32_t* __restrict__ mask, uint32_t* __restrict__ bad_bits, int32_t* __restrict__ count,
                   double* __restrict__ center) {
   const int64_t f = blockIdx.x;
-  const uint8_t* c = codes + f * ldc;
+  const CT* c = codes + f * ldc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int cnt = 0;
   for (int64_t base = (int64_t)warp * 32; base < S; base += (int64_t)kPrepThreads) {
     const int64_t s = base + lane;
-    const uint8_t code = s < S ? c[s] : (uint8_t)0xFF;
-    const uint32_t word = __ballot_sync(PS_FULL, code != 0xFF);
-    const uint32_t bw = __ballot_sync(PS_FULL, code == 0xFE);
+    const CT code = s < S ? c[s] : (CT)~(CT)0;
+    const uint32_t word = __ballot_sync(PS_FULL, code != (CT)~(CT)0);
+    const uint32_t bw = __ballot_sync(PS_FULL, code == (CT)~(CT)1);
     if (lane == 0) {
       mask[f * W + (base >> 5)] = word;
       bad_bits[f * W + (base >> 5)] = bw;
@@ -151,14 +155,19 @@ int ps_prepare_labels_from_host(ps_matrix* m, const double* src, int64_t src_ld,
   PS_CUDA(ps_alloc(&m->d_center, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
   m->ldc = ps_round_up(m->S + 1, 16);
-  PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
+  PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc * m->code_bytes), s));
   PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
   PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));
   int rc = ps_stage_labels_h2d(src, (size_t)src_ld, m->F, m->S, m->sentinel_bits, m->sentinel_is_nan, m->h_cat,
-                               m->d_codes, m->ldc, m->d_zero, m->W, s);
+                               m->d_codes, m->ldc, m->code_bytes, m->d_zero, m->W, s);
   if (rc) return rc;
-  label_bits_kernel<<<(unsigned)m->F, kPrepThreads, 0, s>>>(m->d_codes, m->ldc, m->S, m->W, m->d_mask, m->d_bad,
-                                                            m->d_count, m->d_center);
+  if (m->code_bytes == 2)
+    label_bits_kernel<uint16_t><<<(unsigned)m->F, kPrepThreads, 0, s>>>(
+        reinterpret_cast<const uint16_t*>(m->d_codes), m->ldc, m->S, m->W, m->d_mask, m->d_bad, m->d_count,
+        m->d_center);
+  else
+    label_bits_kernel<uint8_t><<<(unsigned)m->F, kPrepThreads, 0, s>>>(m->d_codes, m->ldc, m->S, m->W, m->d_mask,
+                                                                       m->d_bad, m->d_count, m->d_center);
   PS_LAUNCHED();
   return PS_OK;
 }
@@ -169,7 +178,7 @@ int ps_prepare_alloc(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_count, (size_t)m->F, s));
   if (m->kind != PS_KIND_CONTINUOUS) {
     m->ldc = ps_round_up(m->S + 1, 16);  // code[S] = 0xFF: sentinel for padded walks
-    PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc), s));
+    PS_CUDA(ps_alloc(&m->d_codes, (size_t)(m->F * m->ldc * m->code_bytes), s));
     PS_CUDA(ps_alloc(&m->d_zero, (size_t)(m->F * m->W), s));
     PS_CUDA(ps_alloc(&m->d_bad, (size_t)(m->F * m->W), s));
   }
@@ -179,9 +188,14 @@ int ps_prepare_alloc(ps_matrix* m, cudaStream_t s) {
 int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
   if (f1 <= f0) return PS_OK;
   const bool labels = m->kind != PS_KIND_CONTINUOUS;
-  prep_rows_kernel<<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
-      m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
-      labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero, m->d_bad, f0);
+  if (labels && m->code_bytes == 2)
+    prep_rows_kernel<uint16_t><<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
+        m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
+        m->d_cat, reinterpret_cast<uint16_t*>(m->d_codes), m->ldc, m->d_zero, m->d_bad, f0);
+  else
+    prep_rows_kernel<uint8_t><<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
+        m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
+        labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero, m->d_bad, f0);
   PS_LAUNCHED();
   return PS_OK;
 }

@@ -551,11 +551,14 @@ __global__ void binary_codes_kernel(const uint32_t* __restrict__ mask, const uin
 // (per-warp shared accumulators) and sum(t^3 - t) over the tie groups of the
 // kept samples -- the same exact sums the shared-memory walk produces
 // (mixed.py:366-403, :581-623), finished by rank_mixed_finish_kernel.
-template <typename OT>
+// CT: uint8_t codes, or uint16_t (category counts above 254).  GACC: the
+// level accumulators are the pair's global RankSums entries (global atomics;
+// level counts too large for per-warp shared accumulators).
+template <typename OT, typename CT, bool GACC>
 __global__ void __launch_bounds__(wide::WT, 1)
 rank_mixed_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t* __restrict__ tb,
                        const OT* __restrict__ lastb, const OT* __restrict__ nextb, int64_t ldt,
-                       const int32_t* __restrict__ len, const uint8_t* __restrict__ codes, int64_t ldc,
+                       const int32_t* __restrict__ len, const CT* __restrict__ codes, int64_t ldc,
                        const uint32_t* __restrict__ lmask, int64_t lW, int64_t Fc, int64_t Fq, int64_t lo, int64_t hi,
                        uint32_t* __restrict__ scratch, int64_t scr, int* __restrict__ queue, RankSums rs,
                        int* __restrict__ err) {
@@ -572,17 +575,19 @@ rank_mixed_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t
   const int64_t total = (hi - lo) * Fc;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(queue, 1);
-    for (int i = threadIdx.x; i < wide::WW * KM; i += wide::WT) {
-      wacc[i] = 0ull;
-      wcnt[i] = 0u;
-    }
+    if (!GACC)
+      for (int i = threadIdx.x; i < wide::WW * KM; i += wide::WT) {
+        wacc[i] = 0ull;
+        wcnt[i] = 0u;
+      }
     __syncthreads();
     const int64_t t = s_item;
     if (t >= total) break;
     const int64_t h = lo + t / Fc, g = t % Fc;
     const OT* oh = order + h * ldo;
     const uint32_t* tbh = tb + h * ldt;
-    const uint8_t* cg = codes + g * ldc;
+    const CT* cg = codes + g * ldc;
+    const int64_t pair = g * Fq + h;
     const uint32_t nh = (uint32_t)len[h];
     wide::keep_scan(oh, nh, lmask + g * lW, K, P, sbuf);
     long long tie = 0;
@@ -599,12 +604,16 @@ rank_mixed_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t
         ps_raise(err, PS_ERR_LABEL_OUT_OF_RANGE);
         continue;
       }
-      atomicAdd(&wacc[warp * KM + lv], (unsigned long long)r2);
-      atomicAdd(&wcnt[warp * KM + lv], 1u);
+      if (GACC) {
+        atomicAdd(&rs.r2[pair * KM + lv], (unsigned long long)r2);
+        atomicAdd(&rs.cnt[pair * KM + lv], 1);
+      } else {
+        atomicAdd(&wacc[warp * KM + lv], (unsigned long long)r2);
+        atomicAdd(&wcnt[warp * KM + lv], 1u);
+      }
     }
     const unsigned long long tsum = wide::block_sum_u64((unsigned long long)tie, ubuf);  // ends with a barrier
-    const int64_t pair = g * Fq + h;
-    for (int j = threadIdx.x; j < KM; j += wide::WT) {
+    for (int j = threadIdx.x; !GACC && j < KM; j += wide::WT) {
       unsigned long long r = 0;
       unsigned int c = 0;
       for (int w = 0; w < wide::WW; ++w) {
@@ -619,28 +628,42 @@ rank_mixed_wide_kernel(const OT* __restrict__ order, int64_t ldo, const uint32_t
   }
 }
 
-template <typename OT>
-int launch_wide_walk(ps_matrix* lab, ps_matrix* val, const OT* order, const OT* lastb, const OT* nextb,
-                     const uint8_t* codes, int64_t lo, int64_t hi, RankSums rs, cudaStream_t s) {
+template <typename OT, typename CT, bool GACC>
+int launch_wide_walk_t(ps_matrix* lab, ps_matrix* val, const OT* order, const OT* lastb, const OT* nextb,
+                       const CT* codes, int64_t lo, int64_t hi, RankSums rs, cudaStream_t s) {
   ps_device_state* ds = ps_state();
   const int grid = ds->num_sms;
   const int64_t scr = 2 * (val->ldo / 32 + 2);
-  const size_t smem = (size_t)wide::WW * rs.KM * (8 + 4);
+  const size_t smem = GACC ? 0 : (size_t)wide::WW * rs.KM * (8 + 4);
   uint32_t* scratch = nullptr;
   int* queue = nullptr;
   PS_CUDA(ps_alloc(&scratch, (size_t)(grid * scr), s));
   PS_CUDA(ps_alloc(&queue, 1, s));
   PS_CUDA(cudaMemsetAsync(queue, 0, sizeof(int), s));
-  PS_CUDA(cudaFuncSetAttribute(rank_mixed_wide_kernel<OT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = rank_mixed_wide_kernel<OT, CT, GACC>;
+  PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ps_prof_begin("rank_mixed_walk", s);
-  rank_mixed_wide_kernel<OT><<<grid, wide::WT, smem, s>>>(order, val->ldo, val->d_tb, lastb, nextb, val->ldt,
-                                                          val->d_len, codes, lab->ldc, lab->d_mask, lab->W, lab->F,
-                                                          val->F, lo, hi, scratch, scr, queue, rs, ds->d_err);
+  kern<<<grid, wide::WT, smem, s>>>(order, val->ldo, val->d_tb, lastb, nextb, val->ldt, val->d_len, codes, lab->ldc,
+                                    lab->d_mask, lab->W, lab->F, val->F, lo, hi, scratch, scr, queue, rs, ds->d_err);
   ps_prof_end(s);
   PS_LAUNCHED();
   ps_free(scratch, s);
   ps_free(queue, s);
   return PS_OK;
+}
+
+// the wide walk for any presort width / code width / level count
+template <typename OT>
+int launch_wide_walk(ps_matrix* lab, ps_matrix* val, const OT* order, const OT* lastb, const OT* nextb,
+                     const uint8_t* codes, int64_t lo, int64_t hi, RankSums rs, cudaStream_t s) {
+  const bool gacc = rs.KM > 256;  // per-warp shared accumulators: 32 warps x KM x 12 B
+  if (lab->code_bytes == 2 && codes == lab->d_codes) {
+    const uint16_t* c16 = reinterpret_cast<const uint16_t*>(codes);
+    return gacc ? launch_wide_walk_t<OT, uint16_t, true>(lab, val, order, lastb, nextb, c16, lo, hi, rs, s)
+                : launch_wide_walk_t<OT, uint16_t, false>(lab, val, order, lastb, nextb, c16, lo, hi, rs, s);
+  }
+  return gacc ? launch_wide_walk_t<OT, uint8_t, true>(lab, val, order, lastb, nextb, codes, lo, hi, rs, s)
+              : launch_wide_walk_t<OT, uint8_t, false>(lab, val, order, lastb, nextb, codes, lo, hi, rs, s);
 }
 
 size_t walk_smem(int64_t ldo, int64_t ldt, int64_t ldc, int KM) {
@@ -659,6 +682,8 @@ int launch_walk(ps_matrix* lab, ps_matrix* val, const uint8_t* codes, int64_t lo
   PS_CUDA(cudaFuncGetAttributes(&fa, kern));
   if (val->wide) return launch_wide_walk<uint32_t>(lab, val, val->d_order32, val->d_lastb32, val->d_nextb32, codes, lo,
                                                    hi, rs, s);
+  if ((lab->code_bytes == 2 && codes == lab->d_codes) || rs.KM > 256)  // more than 254 levels: the wide walk
+    return launch_wide_walk<uint16_t>(lab, val, val->d_order, val->d_lastb, val->d_nextb, codes, lo, hi, rs, s);
   if (smem + fa.sharedSizeBytes > 227 * 1024)  // tables beyond shared memory: the wide walk
     return launch_wide_walk<uint16_t>(lab, val, val->d_order, val->d_lastb, val->d_nextb, codes, lo, hi, rs, s);
   PS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

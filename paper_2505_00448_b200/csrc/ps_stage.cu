@@ -60,8 +60,9 @@ void par_copy(void* dst, const void* src, size_t bytes) {
 
 // One label row: the per-cell rules of prep_rows_kernel, branch-free so the
 // compiler vectorises the code loop (AVX2 clone picked at load time).
+template <typename CT>
 __attribute__((target_clones("avx2", "default"))) void label_row(const double* row, int64_t S, int64_t W, double cf,
-                                                                 uint64_t sent_bits, int sent_nan, uint8_t* crow,
+                                                                 uint64_t sent_bits, int sent_nan, CT* crow,
                                                                  uint32_t* zrow) {
   alignas(64) uint8_t zf[32];
   int64_t q0 = 0;
@@ -74,7 +75,7 @@ __attribute__((target_clones("avx2", "default"))) void label_row(const double* r
       const bool pres = sent_nan ? (v == v) : (bits != sent_bits);
       const bool ok = (v > -1.0) & (v < cf);  // false for NaN
       const int32_t lab = (int32_t)(ok ? v : 0.0);  // trunc toward zero (categorical.py:87)
-      crow[q0 + q] = pres ? (ok ? (uint8_t)lab : (uint8_t)0xFE) : (uint8_t)0xFF;
+      crow[q0 + q] = pres ? (ok ? (CT)lab : (CT)~(CT)1) : (CT)~(CT)0;
       zf[q] = pres & (v == 0.0);
     }
     uint32_t zw = 0;
@@ -135,37 +136,39 @@ int ps_stage_h2d_2d(void* dst, size_t dpitch, const void* src, size_t spitch, si
 // present but outside [0, c_f) or NaN, 0xFF missing; padded with 0xFF to ldc)
 // and the "present && label == 0.0" bit words -- with the same rules as
 // prep_rows_kernel, so only ~1 B per cell crosses PCIe instead of 8.
-int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
-                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, uint32_t* d_zero, int64_t W,
-                        cudaStream_t s) {
+template <typename CT>
+static int stage_labels(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
+                        const int64_t* cat, CT* d_codes, int64_t ldc, uint32_t* d_zero, int64_t W, cudaStream_t s) {
   Ring* r = nullptr;
   int rc = ring_for_device(&r);
   if (rc) return rc;
-  const size_t row_bytes = (size_t)ldc + (size_t)W * 4;
+  const size_t cb = sizeof(CT);
+  const size_t row_bytes = (size_t)ldc * cb + (size_t)W * 4;
   int b = 0;
   if (row_bytes > kChunk) {
     // rows longer than a staging chunk (S of several million): each row in
     // segments of whole 32-sample words, all host cores per segment
-    const int64_t seg_words = (int64_t)((kChunk - 128) / (32 + 4));  // + room for the padding past S
+    const int64_t seg_words = (int64_t)((kChunk - 256) / (32 * cb + 4));  // + room for the padding past S
     for (int64_t f = 0; f < F; ++f) {
       const double* row = src + (size_t)f * spitch;
       for (int64_t w0 = 0; w0 < W; w0 += seg_words, b ^= 1) {
         const int64_t nw = std::min<int64_t>(seg_words, W - w0);
         const int64_t q0 = w0 * 32, nq = std::min<int64_t>(S - q0, nw * 32);
         PS_CUDA(cudaEventSynchronize(r->ev[b]));
-        uint8_t* pc = static_cast<uint8_t*>(r->buf[b]);
-        uint32_t* pz = reinterpret_cast<uint32_t*>(pc + (size_t)seg_words * 32 + 64);
+        CT* pc = static_cast<CT*>(r->buf[b]);
+        uint32_t* pz = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(pc) + (size_t)seg_words * 32 * cb + 128);
         const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(nw / 1024) + 1));
 #pragma omp parallel for num_threads(nt) schedule(static)
         for (int t = 0; t < nt; ++t) {
-          const int64_t a = nw * t / nt, e = nw * (t + 1) / nt;
-          const int64_t qa = a * 32, qe = std::min<int64_t>(nq, e * 32);
-          if (qe > qa) label_row(row + q0 + qa, qe - qa, e - a, (double)cat[f], sent_bits, sent_nan, pc + qa, pz + a);
+          const int64_t a0 = nw * t / nt, e = nw * (t + 1) / nt;
+          const int64_t qa = a0 * 32, qe = std::min<int64_t>(nq, e * 32);
+          if (qe > qa)
+            label_row<CT>(row + q0 + qa, qe - qa, e - a0, (double)cat[f], sent_bits, sent_nan, pc + qa, pz + a0);
         }
         // codes of the row's last word past S, and the padding to ldc
-        const int64_t cbytes = (w0 + nw == W) ? ldc - q0 : nw * 32;
-        if (cbytes > nq) std::memset(pc + nq, 0xFF, (size_t)(cbytes - nq));
-        PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)f * ldc + q0, pc, (size_t)cbytes, cudaMemcpyHostToDevice, s));
+        const int64_t ccount = (w0 + nw == W) ? ldc - q0 : nw * 32;
+        for (int64_t i = nq; i < ccount; ++i) pc[i] = (CT)~(CT)0;
+        PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)f * ldc + q0, pc, (size_t)ccount * cb, cudaMemcpyHostToDevice, s));
         PS_CUDA(cudaMemcpyAsync(d_zero + (size_t)f * W + w0, pz, (size_t)nw * 4, cudaMemcpyHostToDevice, s));
         PS_CUDA(cudaEventRecord(r->ev[b], s));
       }
@@ -176,21 +179,30 @@ int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, 
   for (int64_t r0 = 0; r0 < F; r0 += rows_per, b ^= 1) {
     const int64_t nr = std::min<int64_t>(rows_per, F - r0);
     PS_CUDA(cudaEventSynchronize(r->ev[b]));
-    uint8_t* pc = static_cast<uint8_t*>(r->buf[b]);
+    CT* pc = static_cast<CT*>(r->buf[b]);
     uint32_t* pz = reinterpret_cast<uint32_t*>(pc + (size_t)nr * ldc);  // ldc % 16 == 0: aligned
     const int nt = std::max(1, std::min(omp_get_max_threads(), (int)nr));
 #pragma omp parallel for num_threads(nt) schedule(static)
     for (int64_t i = 0; i < nr; ++i) {
       const int64_t f = r0 + i;
-      label_row(src + (size_t)f * spitch, S, W, (double)cat[f], sent_bits, sent_nan, pc + (size_t)i * ldc,
-                pz + (size_t)i * W);
-      std::memset(pc + (size_t)i * ldc + S, 0xFF, (size_t)(ldc - S));
+      label_row<CT>(src + (size_t)f * spitch, S, W, (double)cat[f], sent_bits, sent_nan, pc + (size_t)i * ldc,
+                    pz + (size_t)i * W);
+      for (int64_t q = S; q < ldc; ++q) pc[(size_t)i * ldc + q] = (CT)~(CT)0;
     }
-    PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)r0 * ldc, pc, (size_t)nr * ldc, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(d_codes + (size_t)r0 * ldc, pc, (size_t)nr * ldc * cb, cudaMemcpyHostToDevice, s));
     PS_CUDA(cudaMemcpyAsync(d_zero + (size_t)r0 * W, pz, (size_t)nr * W * 4, cudaMemcpyHostToDevice, s));
     PS_CUDA(cudaEventRecord(r->ev[b], s));
   }
   return PS_OK;
+}
+
+int ps_stage_labels_h2d(const double* src, size_t spitch, int64_t F, int64_t S, uint64_t sent_bits, int sent_nan,
+                        const int64_t* cat, uint8_t* d_codes, int64_t ldc, int code_bytes, uint32_t* d_zero,
+                        int64_t W, cudaStream_t s) {
+  if (code_bytes == 2)
+    return stage_labels<uint16_t>(src, spitch, F, S, sent_bits, sent_nan, cat, reinterpret_cast<uint16_t*>(d_codes),
+                                  ldc, d_zero, W, s);
+  return stage_labels<uint8_t>(src, spitch, F, S, sent_bits, sent_nan, cat, d_codes, ldc, d_zero, W, s);
 }
 
 // contiguous device -> host copy; returns after dst is complete

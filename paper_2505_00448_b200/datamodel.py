@@ -151,30 +151,6 @@ def make_matrix(
 
 
 @dataclass(frozen=True)
-class PairView:
-    """Jointly present entries of two feature vectors, in sample order."""
-
-    xs: np.ndarray
-    ys: np.ndarray
-    n: int
-
-
-def pair_view(
-    g: np.ndarray,
-    h: np.ndarray,
-    sentinel_g: float = math.nan,
-    sentinel_h: float = math.nan,
-) -> PairView:
-    """Pairwise deletion of two equal-length vectors (reference ``:243-290``)."""
-    g = np.asarray(g, dtype=np.float64)
-    h = np.asarray(h, dtype=np.float64)
-    if g.shape != h.shape:
-        raise ValueError(f"feature vectors differ in length: {g.shape} vs {h.shape}")
-    keep = present_mask(g, sentinel_g) & present_mask(h, sentinel_h)
-    return PairView(xs=g[keep], ys=h[keep], n=int(keep.sum()))
-
-
-@dataclass(frozen=True)
 class TestRequest:
     """One run's configuration (reference ``datamodel.py:293-338``).
 

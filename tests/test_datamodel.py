@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import paper_2505_00448_b200 as ps
-from paper_2505_00448_b200.datamodel import pair_view, present_mask
+from paper_2505_00448_b200.datamodel import present_mask
 
 
 def test_exports_match_reference_surface():
@@ -81,13 +81,6 @@ def test_request_validation():
 def test_resultset_shape_check():
     with pytest.raises(ValueError, match="shape"):
         ps.ResultSet(matrices={"stat": np.zeros((2, 2))}, shape=(3, 3))
-
-
-def test_pair_view():
-    v = pair_view(np.array([1.0, np.nan, 3.0]), np.array([4.0, 5.0, np.nan]))
-    assert v.n == 1 and v.xs.tolist() == [1.0] and v.ys.tolist() == [4.0]
-    with pytest.raises(ValueError, match="differ in length"):
-        pair_view(np.zeros(2), np.zeros(3))
 
 
 def test_run_validation_before_device():

@@ -142,3 +142,51 @@ def test_rank_mixed_wide_sample_counts(oracle, test, S):
         assert same_nan(res[n], ref[n]), n
     assert bitwise_equal(res["stat"], ref["stat"]) and bitwise_equal(res[eff[0]], ref[eff[0]])
     assert p_close(res["p"], ref["p"])
+
+
+@pytest.mark.parametrize("host_labels", [True, False])
+@pytest.mark.parametrize("test", ["chi2", "anova", "kruskal"])
+def test_more_than_254_levels(oracle, test, host_labels):
+    """c = 300 levels (16-bit label codes; the reference's c_f = max label + 1
+    has no bound, datamodel.py:199-235).  Host labels are staged as codes by
+    the host threads; device-resident labels are coded by prep_rows."""
+    from paper_2505_00448_b200 import blocks
+    import torch
+
+    S = 4000
+    lab = workloads.simulate(5, S, "categorical", categories=300, na_ratio=0.1, seed=300)
+    lab[1] = np.where(np.isnan(lab[1]), np.nan, lab[1] % 7)  # a small-level row next to the wide ones
+    ma = ps.make_matrix(lab, "categorical")
+    assert int(ma.category_counts.max()) == 300
+    mb = None
+    if test != "chi2":
+        val = workloads.simulate(9, S, "continuous", na_ratio=0.1, seed=301)
+        val[2] = np.round(val[2], 2)
+        mb = ps.make_matrix(val, "continuous")
+    eff = ps.EFFECTS_BY_TEST[test]
+    names = ("stat", "p") + eff
+    req = ps.TestRequest(test, names)
+    ref = oracle.oracle_run(req, ma, mb)
+    if host_labels:
+        res = ps.run(req, ma, mb)
+    else:  # device-resident labels through the block API
+        shape = ref["stat"].shape
+        xa = torch.zeros((lab.shape[0], 4000), dtype=torch.float64, device="cuda")
+        xa[:, :S] = torch.from_numpy(np.ascontiguousarray(ma.values))
+        da = blocks.DeviceMatrix(xa, "categorical", ma.na_sentinel, ma.category_counts, n_samples=S)
+        db = blocks.DeviceMatrix(mb.values, "continuous", mb.na_sentinel, presort=test == "kruskal") if mb else None
+        outs = [torch.full(shape, float("nan"), dtype=torch.float64, device="cuda") for _ in names]
+        lo, hi = blocks.full_range(test, da, db)
+        blocks.block(test, da, db, lo, hi, outs)
+        blocks.sync()
+        res = {n: o.cpu().numpy() for n, o in zip(names, outs)}
+    exact = {"chi2": ("stat", "phi", "cramers_v"), "kruskal": ("stat", "eta2")}.get(test, ())
+    for n in names:
+        assert same_nan(res[n], ref[n]), n
+        if n in exact:
+            assert bitwise_equal(res[n], ref[n]), n
+        elif n == "p":
+            assert p_close(res[n], ref[n]), n
+        else:
+            m = ~np.isnan(ref[n])
+            np.testing.assert_allclose(res[n][m], ref[n][m], rtol=1e-9, atol=0)
