@@ -188,6 +188,11 @@ class Workload:
         return self._mats
 
 
+def default_test(cfg_key) -> str:
+    """The (first) test of a config (workloads.config(k)["tests"][0])."""
+    return {1: "pearson", 2: "spearman", 3: "chi2", 4: "anova", 5: "pearson", "5s": "spearman"}[cfg_key]
+
+
 def label_counts(raw: np.ndarray) -> np.ndarray:
     pres = raw != workloads.SENTINEL
     out = np.zeros(raw.shape[0], dtype=np.int64)
@@ -335,8 +340,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cfg_key = args.config
-    test = args.test or ("pearson" if cfg_key in (1, 5) else workloads.config(cfg_key)["tests"][0]
-                         if cfg_key != "5s" else "spearman")
+    test = args.test or default_test(cfg_key)
     wl = Workload(cfg_key, test, 0, 1)
     mat_a, mat_b = wl.datamatrices()
     per_step = float(os.environ.get("REF_STEP_SECONDS", "6"))
@@ -594,8 +598,7 @@ def main():
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg_key = args.config
-    test = args.test or ("pearson" if cfg_key in (1, 5) else "spearman" if cfg_key in (2, "5s")
-                         else workloads.config(cfg_key)["tests"][0])
+    test = args.test or default_test(cfg_key)
     big = cfg_key == 5
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else (3 if big else 5)
     e2e_warmup = args.e2e_warmup if args.e2e_warmup is not None else (1 if big else 3)

@@ -24,9 +24,12 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--reps", type=int, default=1)
     args = ap.parse_args()
-    cfg = workloads.config(args.config, scale=args.scale)
-    test = args.test or cfg["tests"][0]
-    a, b, ka, kb = bench.build_inputs(cfg, test)
+    if args.config == 5 and args.scale != 1.0:
+        cfg = workloads.config(5, scale=args.scale)
+        a, b, ka, kb, test = cfg["a"], None, "continuous", None, "pearson"
+    else:
+        wl = bench.Workload(args.config, args.test or bench.default_test(args.config), 0, 1)
+        a, b, ka, kb, test = wl.a_full, wl.b_full, wl.kind_a, wl.kind_b, wl.test
     cat = bench.label_counts(a) if ka != "continuous" else None
     homog = b is None
     shape = (a.shape[0], a.shape[0]) if homog else (a.shape[0], b.shape[0])

@@ -1,32 +1,36 @@
 #!/bin/bash
 # Re-measure every BASELINE config on one B200 and refresh profiles/:
-#   bench lines, ncu launch lists (time + DRAM bytes per launch), and
+#   the default bench line (config 5 + legs + CPU baseline + e2e), one bench
+#   line per config, ncu launch lists (time + DRAM bytes per launch) and
 #   ncu --set full reports of the dominant kernels.
-# usage (on the GPU box): bash tools/refresh_profiles.sh <round tag, e.g. r01> [full]
+# usage (on the GPU box): bash tools/refresh_profiles.sh <round tag, e.g. r02> [full]
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 OUT=gpurun_out/prof_$TAG
 mkdir -p $OUT
-CFGS=("1" "2" "3" "4 --test anova" "4 --test ttest" "4 --test kruskal" "4 --test mwu" "5" "5s")
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $OUT/gpu.txt 2>&1
+timeout 1200 python bench.py > $OUT/bench_default.jsonl 2> $OUT/bench_default.err
+tail -1 $OUT/bench_default.jsonl | cut -c1-300
+CFGS=("1" "2" "3" "4 --test anova" "4 --test ttest" "4 --test kruskal" "4 --test mwu" "5s")
 for c in "${CFGS[@]}"; do
   n=$(echo $c | sed 's/ --test /_/')
-  extra="--no-cpu-baseline"
-  [ "$n" = "2" ] && extra=""
-  steps=5; [ "$n" = "5" ] && steps=3; [ "$n" = "5s" ] && steps=3
-  timeout 900 python bench.py --config $c --steps $steps --warmup 3 $extra > $OUT/bench_$n.jsonl 2> $OUT/bench_$n.err
+  extra="--no-cpu-baseline --no-legs"
+  case "$n" in 2|3|4_anova|4_kruskal) extra="--no-legs" ;; esac
+  timeout 900 python bench.py --config $c --steps 5 --warmup 3 $extra > $OUT/bench_$n.jsonl 2> $OUT/bench_$n.err
   tail -1 $OUT/bench_$n.jsonl | cut -c1-200
 done
-# launch lists (1 timed step; cold-cache, serialised: shares, not absolutes)
-for c in "${CFGS[@]}"; do
+# launch lists (cold-cache, serialised: shares, not absolutes)
+CFGL=("5" "1" "2" "3" "4 --test anova" "4 --test ttest" "4 --test kruskal" "4 --test mwu" "5s")
+for c in "${CFGL[@]}"; do
   n=$(echo $c | sed 's/ --test /_/')
-  [ "$n" = "5" ] && continue
+  w=3; [ "$n" = "5" ] && w=1
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file $OUT/launches_$n.csv \
-    python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+    python bench.py --config $c --steps 1 --warmup $w --no-cpu-baseline --no-legs --e2e-steps 0 > /dev/null 2>&1
   python tools/summarize_launches.py $OUT/launches_$n.csv $OUT/launches_$n.json > $OUT/launches_$n.txt 2>/dev/null
 done
 if [ "${2:-}" = "full" ]; then
-  for spec in "2:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm" "5 --scale 0.15:pearson_tile"; do
+  for spec in "5 --scale 0.15:pearson_tile" "2:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm"; do
     c=${spec%%:*}; k=${spec##*:}
     n=$(echo $c | sed 's/ --test /_/; s/ --scale /_s/')
     timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
