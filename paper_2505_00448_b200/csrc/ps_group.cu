@@ -658,12 +658,19 @@ static int replay_cap(int64_t cells) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(cells, lim));
 }
 
-// Split-K factor of the moment contraction: enough K parts that the WHOLE
-// (label rows x features) tile grid gives two CTAs per SM, at least 16 mask
-// words per part.  A function of (R, Fq, W) only.
-static int64_t group_kparts(const ps_device_state* ds, int64_t R, int64_t Fq, int64_t W) {
-  const int64_t tiles = ps_ceil_div(std::max<int64_t>(R, 1), T) * ps_ceil_div(Fq, T);
-  return std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(2 * (int64_t)ds->num_sms, tiles), W / 16));
+// Split-K factor of the moment contraction: enough K parts that two CTAs per
+// SM are busy both for the whole (label rows x features) tile grid and for
+// the column tiles of one upload chunk (run() contracts each staged chunk as
+// it lands), at least 16 mask words per part.  A function of the matrices
+// (R, Fq, S) only -- never of the launch -- so every cell's k-order, hence
+// every bit, is the same for any range, rank or incremental launch.
+static int64_t group_kparts(const ps_device_state* ds, int64_t R, int64_t Fq, int64_t W, int64_t ld) {
+  const int64_t rtiles = ps_ceil_div(std::max<int64_t>(R, 1), T), ctiles = ps_ceil_div(Fq, T);
+  const int64_t chunk_rows = (int64_t)std::max<size_t>(1, ps_stage_chunk_bytes() / (sizeof(double) * ld));
+  const int64_t ct_chunk = std::min<int64_t>(ctiles, ps_ceil_div(chunk_rows, T));
+  const int64_t want = 2 * (int64_t)ds->num_sms;
+  const int64_t k = std::max(ps_ceil_div(want, rtiles * ctiles), ps_ceil_div(want, rtiles * ct_chunk));
+  return std::max<int64_t>(1, std::min<int64_t>(k, W / 16));
 }
 
 int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, int64_t hi, int student,
@@ -734,7 +741,7 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
     // split K when the WHOLE tile grid cannot fill two CTAs per SM (the split
     // is a function of the matrices, not of the range: every cell's k-order,
     // hence every bit, is the same for any range / rank / incremental launch)
-    const int64_t kparts = group_kparts(ds, R, Fq, W);
+    const int64_t kparts = group_kparts(ds, R, Fq, W, ps_round_up(val->S, 32));
     const int64_t stride = Rp * Fq;
     if (kparts > 1) {
       PS_CUDA(ps_alloc(&Pn, (size_t)(kparts * stride), s));
@@ -827,7 +834,7 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
   const size_t smem = NSTAGE * sizeof(Stage);
   PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = rtiles * ctiles;
-  const int64_t kparts = group_kparts(ds, j->R, Fq, W);
+  const int64_t kparts = group_kparts(ds, j->R, Fq, W, ps_round_up(val->S, 32));
   const int64_t rows = rtiles * T, width = ctiles * T, c0 = ct0 * T, stride = rows * width;
   // the slot's partial buffers hold a staging chunk's columns; a wider window
   // gets its own (same split, so the same bits)
@@ -911,7 +918,7 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
     const int64_t rtiles = ps_ceil_div(std::max<int64_t>(j->R, 1), T);
     const int64_t chunk_rows = (int64_t)std::max<size_t>(1, ps_stage_chunk_bytes() / (sizeof(double) * val->ld));
     const int64_t width_cap = (ps_ceil_div(chunk_rows, T) + 1) * T;
-    const int64_t kp = group_kparts(ds, j->R, Fq, W);
+    const int64_t kp = group_kparts(ds, j->R, Fq, W, ps_round_up(val->S, 32));
     j->pcap = kp > 1 ? kp * rtiles * T * width_cap : 0;
   }
   // the pageable copies above are staged by the driver: the vectors may go

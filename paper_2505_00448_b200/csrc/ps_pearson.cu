@@ -95,8 +95,31 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
   put(o.r2, F, g, h, r * r);
 }
 
+// x' = x - c_f on present cells, 0 elsewhere, for rows [f0, f0 + grid): the
+// tile kernel's operands pre-centred once per element (the same fp64
+// subtraction the tile kernel would do per use, so every bit is unchanged);
+// the tile loop then feeds x' and x'^2 to the DMMAs without per-use
+// subtract / select instructions on the FP64 pipe the DMMAs share.
+__global__ void center_rows_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
+                                   int64_t W, const double* __restrict__ center, double* __restrict__ out, int64_t f0) {
+  const int64_t f = f0 + blockIdx.x;
+  const double c = center[f];
+  const double* x = vals + f * ld;
+  double* y = out + f * ld;
+  const uint32_t* m = mask + f * W;
+  for (int64_t s = threadIdx.x * 2; s < ld; s += blockDim.x * 2) {
+    const uint32_t w = m[s >> 5];
+    const double2 v = *reinterpret_cast<const double2*>(x + s);
+    double2 r;
+    r.x = ((w >> (s & 31)) & 1u) ? v.x - c : 0.0;
+    r.y = ((w >> ((s + 1) & 31)) & 1u) ? v.y - c : 0.0;
+    *reinterpret_cast<double2*>(y + s) = r;
+  }
+}
+
 // grid.x = tiles in range x nsplit.  Each CTA accumulates one 64x64 tile over
-// its share of the k-chunks.
+// its share of the k-chunks.  PC: vals holds pre-centred x' (center_rows_kernel).
+template <bool PC>
 __global__ void __launch_bounds__(NTHR, 1)
 pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
                     int64_t W, const double* __restrict__ center, int64_t F, int64_t NT,
@@ -192,7 +215,7 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
       for (int q = 0; q < WM; ++q) {
         const bool pa = (mrow[q] >> k) & 1u;
         const double va = s.xi[wi * 8 * WM + q * 8 + fr][k];
-        xa[q] = pa ? va - ci[q] : 0.0;
+        xa[q] = PC ? va : (pa ? va - ci[q] : 0.0);
         ma[q] = pa ? 1.0 : 0.0;
         xa2[q] = xa[q] * xa[q];
       }
@@ -200,7 +223,7 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
       for (int q = 0; q < WN; ++q) {
         const bool pb = (mcol[q] >> k) & 1u;
         const double vb = s.xj[wj * 8 * WN + q * 8 + fr][k];
-        xb[q] = pb ? vb - cj[q] : 0.0;
+        xb[q] = PC ? vb : (pb ? vb - cj[q] : 0.0);
         mb[q] = pb ? 1.0 : 0.0;
         xb2[q] = xb[q] * xb[q];
       }
@@ -388,14 +411,30 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   PS_CUDA(cudaMemsetAsync(o.replay_count, 0, sizeof(int), s));
   if (nsplit > 1) PS_CUDA(ps_alloc(&ws, (size_t)(ntiles * nsplit * 6 * T * T), s));
 
+  // pre-centred operands (PS_PEARSON_RAW=1: centre inside the tile loop, A/B)
+  const bool pc = !getenv("PS_PEARSON_RAW");
+  double* xc = nullptr;
+  if (pc) {
+    PS_CUDA(ps_alloc(&xc, (size_t)(F * a->ld), s));
+    center_rows_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, W, a->d_center, xc, 0);
+    PS_LAUNCHED();
+  }
   // (a function attribute is per device: set it on every call)
-  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes));
+  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kSmemBytes));
+  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kSmemBytes));
   const int64_t grid = ntiles * nsplit;
   ps_prof_begin("pearson_tile", s);
-  pearson_tile_kernel<<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
-      a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
+  if (pc)
+    pearson_tile_kernel<true><<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
+        xc, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
+  else
+    pearson_tile_kernel<false><<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
+        a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
   ps_prof_end(s);
   PS_LAUNCHED();
+  ps_free(xc, s);
   if (nsplit > 1) {
     const int64_t total = ntiles * T * T;
     const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 256), (int64_t)ds->num_sms * 8);
@@ -424,6 +463,8 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
 struct ps_pearson_job {
   ps_matrix* a = nullptr;
   Outs o{};
+  double* xc = nullptr;    // pre-centred operands (nullptr: centre in the tile loop)
+  int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
   int nws = 0;
   cudaStream_t home = nullptr;
@@ -440,16 +481,33 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
   cudaError_t e = ps_alloc(&j->o.replay, (size_t)cap, s);
   if (e == cudaSuccess) e = ps_alloc(&j->o.replay_count, 1, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(j->o.replay_count, 0, sizeof(int), s);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kSmemBytes);
+  if (e == cudaSuccess && !getenv("PS_PEARSON_RAW")) e = ps_alloc(&j->xc, (size_t)(F * a->ld), s);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s);
     ps_free(j->o.replay, s);
     ps_free(j->o.replay_count, s);
+    ps_free(j->xc, s);
     delete j;
     return ps_cuda_check(e, "pearson setup");
   }
   *out = j;
+  return PS_OK;
+}
+
+// centre the rows [c_done, r1) on `s` -- the stream every later tile launch
+// is ordered after (the incremental launches' walk streams wait on it)
+static int pearson_center_upto(ps_pearson_job* j, int64_t r1, cudaStream_t s) {
+  ps_matrix* a = j->a;
+  r1 = std::min<int64_t>(a->F, r1);
+  if (!j->xc || r1 <= j->c_done) return PS_OK;
+  center_rows_kernel<<<(unsigned)(r1 - j->c_done), 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->d_center, j->xc,
+                                                                j->c_done);
+  PS_LAUNCHED();
+  j->c_done = r1;
   return PS_OK;
 }
 
@@ -459,8 +517,12 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
-  pearson_tile_kernel<<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(a->d_vals, a->ld, a->d_mask, W, a->d_center, F,
-                                                                     NT, t0, 0, F, 1, W, j->o, nullptr, 1);
+  if (j->xc)
+    pearson_tile_kernel<true><<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(j->xc, a->ld, a->d_mask, W, a->d_center,
+                                                                            F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
+  else
+    pearson_tile_kernel<false><<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(
+        a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
   ps_prof_end(s);
   PS_LAUNCHED();
   return PS_OK;
@@ -470,6 +532,8 @@ int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
   const int64_t F = j->a->F;
   const int64_t J1 = h1 >= F ? ps_ceil_div(F, T) : h1 / T;  // whole tile columns only
   if (J1 <= j->J_done) return PS_OK;
+  int rc0 = pearson_center_upto(j, J1 * T, s);
+  if (rc0) return rc0;
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = pearson_columns(j, j->J_done, J1, w);
   j->J_done = J1;
@@ -480,6 +544,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_device_state* ds = ps_state();
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
+  if (!rc) rc = pearson_center_upto(j, a->F, s);
   if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
   if (!rc) {
     pearson_replay_kernel<<<ds->num_sms * 4, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->S, a->F, j->o.replay,
@@ -489,6 +554,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   }
   ps_free(j->o.replay, j->home);
   ps_free(j->o.replay_count, j->home);
+  ps_free(j->xc, j->home);
   delete j;
   return rc;
 }
@@ -499,5 +565,6 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   cudaDeviceSynchronize();
   ps_free(j->o.replay, j->home);
   ps_free(j->o.replay_count, j->home);
+  ps_free(j->xc, j->home);
   delete j;
 }

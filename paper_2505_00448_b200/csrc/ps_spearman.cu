@@ -44,11 +44,14 @@ namespace {
 constexpr int SW = PS_SW;          // warps per CTA
 constexpr int STH = SW * 32;
 
+// Exact per-pair sums of the rows [row0, row0 + rows) of the current chunk
+// (rows x F, only g <= h written): scratch bounded by the chunk, not F^2.
 struct PairSums {
-  long long* n;    // F x F (only g <= h written)
+  long long* n;
   long long* sxx4;
   long long* syy4;
   long long* sxy4;
+  int64_t row0;
 };
 
 // Per-warp partial sums of one chunk of g rows [c0, c1): the walk writes them
@@ -740,7 +743,7 @@ __global__ void spearman_partials_kernel(PairParts in, int64_t F, int64_t c1, Pa
       c += __shfl_xor_sync(PS_FULL, c, o);
     }
     if (lane == 0) {
-      const int64_t o = g * F + h;
+      const int64_t o = (g - out.row0) * F + h;
       out.n[o] = (long long)(meta & ((1ull << 40) - 1));
       out.sxx4[o] = (long long)(tg ? a : kClosed);
       out.sxy4[o] = (long long)b;
@@ -817,7 +820,7 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
       else b = mid - 1;
     }
     const int64_t g = a, h = (g > h0 ? g : h0) + (t - finish_before(g, lo, h0, h1));
-    const int64_t cell = g * F + h;
+    const int64_t cell = (g - in.row0) * F + h;
     double rho, p;
     spearman_from_sums(in.n[cell], (unsigned long long)in.sxx4[cell], (unsigned long long)in.syy4[cell],
                        in.sxy4[cell], &rho, &p, err);
@@ -1009,9 +1012,12 @@ static int partials_launch(ps_spearman_job* j, int64_t c0, int64_t c1, cudaStrea
   return PS_OK;
 }
 
-// rho / p of the cells of rows [lo, hi) x columns [h0, h1)
-static int finish_launch(ps_spearman_job* j, int64_t h0, int64_t h1, cudaStream_t s) {
-  const int64_t F = j->a->F, lo = j->lo, hi = j->hi;
+// rho / p of the cells of rows [lo, hi) x columns [h0, h1) (rows default: the job's)
+static int finish_launch(ps_spearman_job* j, int64_t h0, int64_t h1, cudaStream_t s, int64_t lo = -1,
+                         int64_t hi = -1) {
+  const int64_t F = j->a->F;
+  if (lo < 0) lo = j->lo;
+  if (hi < 0) hi = j->hi;
   if (h1 <= h0 || hi <= lo || (!j->stat && !j->p && !j->rho)) return PS_OK;
   ps_device_state* ds = ps_state();
   const int64_t cells = finish_before(hi, lo, h0, h1);
@@ -1082,11 +1088,15 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double
   // g rows per chunk: the per-warp partials take kSlots * SW * 8 B per cell
   const int64_t per_row = F * (int64_t)(kSlots * SW + 1) * 8;
   j->rows = std::max<int64_t>(1, std::min<int64_t>(hi - lo, ((int64_t)2 << 30) / per_row));
+  if (const char* e = getenv("PS_SPEARMAN_ROWS")) j->rows = std::max<int64_t>(1, std::min<int64_t>(hi - lo, atoll(e)));
   j->single = j->rows >= hi - lo;
-  if ((e = ps_alloc(&j->ps.n, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
-  if ((e = ps_alloc(&j->ps.sxx4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
-  if ((e = ps_alloc(&j->ps.syy4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
-  if ((e = ps_alloc(&j->ps.sxy4, (size_t)(F * F), s)) != cudaSuccess) return fail(e);
+  // pair sums of one chunk of rows (the whole range when it is one chunk)
+  const int64_t ps_rows = std::max<int64_t>(1, j->single ? hi - lo : j->rows);
+  j->ps.row0 = lo;
+  if ((e = ps_alloc(&j->ps.n, (size_t)(ps_rows * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.sxx4, (size_t)(ps_rows * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.syy4, (size_t)(ps_rows * F), s)) != cudaSuccess) return fail(e);
+  if ((e = ps_alloc(&j->ps.sxy4, (size_t)(ps_rows * F), s)) != cudaSuccess) return fail(e);
   if ((e = ps_alloc(&j->queues, (size_t)j->qn, s)) != cudaSuccess) return fail(e);
   if ((e = cudaMemsetAsync(j->queues, 0, sizeof(int) * j->qn, s)) != cudaSuccess) return fail(e);
   if ((e = ps_alloc(&j->pp.part, (size_t)(j->rows * F * kSlots * SW), s)) != cudaSuccess) return fail(e);
@@ -1136,11 +1146,13 @@ int ps_spearman_end(ps_spearman_job* j, cudaStream_t s) {
   } else {
     for (int64_t c0 = lo; c0 < hi && !rc; c0 += j->rows) {
       const int64_t c1 = std::min<int64_t>(hi, c0 + j->rows);
+      j->ps.row0 = c0;  // the chunk's pair sums reuse one rows x F scratch
       rc = walk_launch(j, c0, F, c0, c1, gb_full, s, j->grid_max);
       if (!rc) rc = partials_launch(j, c0, c1, s);
+      if (!rc) rc = finish_launch(j, 0, F, s, c0, c1);
     }
   }
-  if (!rc) rc = finish_launch(j, j->single ? j->h_fin : 0, F, s);
+  if (!rc && j->single) rc = finish_launch(j, j->h_fin, F, s);
   if (j->home != s) {  // free in the allocation stream's order (pool reuse across runs)
     PS_CUDA(cudaEventRecord(ds->walk_ev[ps_device_state::kWalkStreams], s));
     PS_CUDA(cudaStreamWaitEvent(j->home, ds->walk_ev[ps_device_state::kWalkStreams], 0));

@@ -203,3 +203,15 @@ def test_more_than_254_levels(oracle, test, host_labels):
         else:
             m = ~np.isnan(ref[n])
             np.testing.assert_allclose(res[n][m], ref[n][m], rtol=1e-9, atol=0)
+
+
+def test_spearman_row_chunks_bound_scratch(monkeypatch):
+    """Pair sums live in a chunk of rows x F (not F x F): forcing 7-row
+    chunks (PS_SPEARMAN_ROWS) gives the one-chunk result bit for bit."""
+    x = workloads.config_spearman_like(np.random.default_rng(8), 90, 3000)
+    mat = ps.make_matrix(x, "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("spearman", ("stat", "p", "p_bh"))
+    want = ps.run(req, mat)
+    monkeypatch.setenv("PS_SPEARMAN_ROWS", "7")
+    monkeypatch.setenv("PS_NO_OVERLAP", "1")
+    _same(ps.run(req, mat), want, req.outputs)
