@@ -35,14 +35,21 @@ constexpr int NWARP = (T / (8 * WM)) * WJ;  // WN = 4: 4 x 2 warps of 16 x 32 pa
 constexpr int NTHR = NWARP * 32;
 constexpr double kReplayTau = 1e-3;
 
+// MODE 0: raw values, centred and squared per use; 1: pre-centred x'
+// (squared per use); 2: pre-centred x' and x'^2 (no FP64 ALU work in the
+// DMMA loop; 222 KB of stages)
+template <int MODE>
 struct Stage {
   double xi[T][XS];
   double xj[T][XS];
+  double qi[MODE == 2 ? T : 1][XS];
+  double qj[MODE == 2 ? T : 1][XS];
   uint32_t mi[T];
   uint32_t mj[T];
 };
 constexpr int NSTAGE = 3;
-constexpr size_t kSmemBytes = NSTAGE * sizeof(Stage);
+template <int MODE>
+constexpr size_t smem_bytes() { return NSTAGE * sizeof(Stage<MODE>); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -101,7 +108,8 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
 // the tile loop then feeds x' and x'^2 to the DMMAs without per-use
 // subtract / select instructions on the FP64 pipe the DMMAs share.
 __global__ void center_rows_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
-                                   int64_t W, const double* __restrict__ center, double* __restrict__ out, int64_t f0) {
+                                   int64_t W, const double* __restrict__ center, double* __restrict__ out,
+                                   double* __restrict__ out2, int64_t f0) {
   const int64_t f = f0 + blockIdx.x;
   const double c = center[f];
   const double* x = vals + f * ld;
@@ -114,18 +122,22 @@ __global__ void center_rows_kernel(const double* __restrict__ vals, int64_t ld, 
     r.x = ((w >> (s & 31)) & 1u) ? v.x - c : 0.0;
     r.y = ((w >> ((s + 1) & 31)) & 1u) ? v.y - c : 0.0;
     *reinterpret_cast<double2*>(y + s) = r;
+    if (out2) *reinterpret_cast<double2*>(out2 + f * ld + s) = make_double2(r.x * r.x, r.y * r.y);
   }
 }
 
 // grid.x = tiles in range x nsplit.  Each CTA accumulates one 64x64 tile over
-// its share of the k-chunks.  PC: vals holds pre-centred x' (center_rows_kernel).
-template <bool PC>
+// its share of the k-chunks.  MODE >= 1: vals holds pre-centred x'
+// (center_rows_kernel); MODE 2: sq holds x'^2.
+template <int MODE>
 __global__ void __launch_bounds__(NTHR, 1)
-pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ mask,
-                    int64_t W, const double* __restrict__ center, int64_t F, int64_t NT,
-                    int64_t tile0, int64_t lo, int64_t hi, int nsplit, int64_t chunks_per_split,
+pearson_tile_kernel(const double* __restrict__ vals, const double* __restrict__ sq, int64_t ld,
+                    const uint32_t* __restrict__ mask, int64_t W, const double* __restrict__ center, int64_t F,
+                    int64_t NT, int64_t tile0, int64_t lo, int64_t hi, int nsplit, int64_t chunks_per_split,
                     Outs o, double* __restrict__ ws, int colmajor) {
+  constexpr bool PC = MODE >= 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Stage = ::Stage<MODE>;
   Stage* st = reinterpret_cast<Stage*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wi = warp / WJ, wj = warp % WJ;
@@ -177,6 +189,12 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
       const unsigned sj = (unsigned)__cvta_generic_to_shared(&sd.xj[r][c2 * 2]);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(si), "l"(vals + gi * ld + off));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sj), "l"(vals + gj * ld + off));
+      if constexpr (MODE == 2) {
+        const unsigned qi = (unsigned)__cvta_generic_to_shared(&sd.qi[r][c2 * 2]);
+        const unsigned qj = (unsigned)__cvta_generic_to_shared(&sd.qj[r][c2 * 2]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(qi), "l"(sq + gi * ld + off));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(qj), "l"(sq + gj * ld + off));
+      }
     }
     if (tid < 2 * T) {
       const int64_t gr = (tid < T ? row0 : col0) + (tid & (T - 1));
@@ -217,7 +235,8 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
         const double va = s.xi[wi * 8 * WM + q * 8 + fr][k];
         xa[q] = PC ? va : (pa ? va - ci[q] : 0.0);
         ma[q] = pa ? 1.0 : 0.0;
-        xa2[q] = xa[q] * xa[q];
+        if constexpr (MODE == 2) xa2[q] = s.qi[wi * 8 * WM + q * 8 + fr][k];
+        else xa2[q] = xa[q] * xa[q];
       }
 #pragma unroll
       for (int q = 0; q < WN; ++q) {
@@ -225,7 +244,8 @@ pearson_tile_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
         const double vb = s.xj[wj * 8 * WN + q * 8 + fr][k];
         xb[q] = PC ? vb : (pb ? vb - cj[q] : 0.0);
         mb[q] = pb ? 1.0 : 0.0;
-        xb2[q] = xb[q] * xb[q];
+        if constexpr (MODE == 2) xb2[q] = s.qj[wj * 8 * WN + q * 8 + fr][k];
+        else xb2[q] = xb[q] * xb[q];
       }
 #pragma unroll
       for (int i = 0; i < WM; ++i)
@@ -376,6 +396,42 @@ __global__ void pearson_replay_kernel(const double* __restrict__ vals, int64_t l
 
 }  // namespace
 
+// default 1: x' once per element took the config-5 step 7209 -> 6627 ms
+// (bitwise identical); precomputed squares (mode 2) measured no faster
+// (613.6 vs 613.9 ms at 6000 x 10^5) and cost another F x ld buffer
+static int pearson_mode() {
+  const char* e = getenv("PS_PEARSON_MODE");
+  const int m = e ? atoi(e) : 1;
+  return m < 0 ? 0 : m > 2 ? 2 : m;
+}
+
+// (a function attribute is per device: set on every call)
+static cudaError_t set_tile_attrs() {
+  cudaError_t e = cudaFuncSetAttribute(pearson_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem_bytes<0>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pearson_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_bytes<1>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pearson_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_bytes<2>());
+  return e;
+}
+
+static void launch_tiles(int mode, unsigned grid, cudaStream_t s, const double* vals, const double* sq, int64_t ld,
+                         const uint32_t* mask, int64_t W, const double* center, int64_t F, int64_t NT, int64_t tile0,
+                         int64_t lo, int64_t hi, int nsplit, int64_t cps, const Outs& o, double* ws, int colmajor) {
+  if (mode == 2)
+    pearson_tile_kernel<2><<<grid, NTHR, smem_bytes<2>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
+                                                               nsplit, cps, o, ws, colmajor);
+  else if (mode == 1)
+    pearson_tile_kernel<1><<<grid, NTHR, smem_bytes<1>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
+                                                               nsplit, cps, o, ws, colmajor);
+  else
+    pearson_tile_kernel<0><<<grid, NTHR, smem_bytes<0>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
+                                                               nsplit, cps, o, ws, colmajor);
+}
+
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s) {
   const int64_t F = a->F;
@@ -411,30 +467,24 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   PS_CUDA(cudaMemsetAsync(o.replay_count, 0, sizeof(int), s));
   if (nsplit > 1) PS_CUDA(ps_alloc(&ws, (size_t)(ntiles * nsplit * 6 * T * T), s));
 
-  // pre-centred operands (PS_PEARSON_RAW=1: centre inside the tile loop, A/B)
-  const bool pc = !getenv("PS_PEARSON_RAW");
-  double* xc = nullptr;
-  if (pc) {
+  // operand mode (PS_PEARSON_MODE: 0 raw, 1 pre-centred x', 2 x' and x'^2)
+  const int mode = pearson_mode();
+  double *xc = nullptr, *xq = nullptr;
+  if (mode >= 1) {
     PS_CUDA(ps_alloc(&xc, (size_t)(F * a->ld), s));
-    center_rows_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, W, a->d_center, xc, 0);
+    if (mode == 2) PS_CUDA(ps_alloc(&xq, (size_t)(F * a->ld), s));
+    center_rows_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, W, a->d_center, xc, xq, 0);
     PS_LAUNCHED();
   }
-  // (a function attribute is per device: set it on every call)
-  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kSmemBytes));
-  PS_CUDA(cudaFuncSetAttribute(pearson_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kSmemBytes));
+  PS_CUDA(set_tile_attrs());
   const int64_t grid = ntiles * nsplit;
   ps_prof_begin("pearson_tile", s);
-  if (pc)
-    pearson_tile_kernel<true><<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
-        xc, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
-  else
-    pearson_tile_kernel<false><<<(unsigned)grid, NTHR, kSmemBytes, s>>>(
-        a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, tile0, lo, hi, nsplit, cps, o, ws, 0);
+  launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT, tile0,
+               lo, hi, nsplit, cps, o, ws, 0);
   ps_prof_end(s);
   PS_LAUNCHED();
   ps_free(xc, s);
+  ps_free(xq, s);
   if (nsplit > 1) {
     const int64_t total = ntiles * T * T;
     const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 256), (int64_t)ds->num_sms * 8);
@@ -463,7 +513,9 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
 struct ps_pearson_job {
   ps_matrix* a = nullptr;
   Outs o{};
-  double* xc = nullptr;    // pre-centred operands (nullptr: centre in the tile loop)
+  int mode = 0;            // operand mode (pearson_mode)
+  double* xc = nullptr;    // pre-centred x' (mode >= 1)
+  double* xq = nullptr;    // x'^2 (mode 2)
   int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
   int nws = 0;
@@ -481,16 +533,16 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
   cudaError_t e = ps_alloc(&j->o.replay, (size_t)cap, s);
   if (e == cudaSuccess) e = ps_alloc(&j->o.replay_count, 1, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(j->o.replay_count, 0, sizeof(int), s);
-  if (e == cudaSuccess && !getenv("PS_PEARSON_RAW")) e = ps_alloc(&j->xc, (size_t)(F * a->ld), s);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(pearson_tile_kernel<false>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  j->mode = pearson_mode();
+  if (e == cudaSuccess && j->mode >= 1) e = ps_alloc(&j->xc, (size_t)(F * a->ld), s);
+  if (e == cudaSuccess && j->mode == 2) e = ps_alloc(&j->xq, (size_t)(F * a->ld), s);
+  if (e == cudaSuccess) e = set_tile_attrs();
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s);
     ps_free(j->o.replay, s);
     ps_free(j->o.replay_count, s);
     ps_free(j->xc, s);
+    ps_free(j->xq, s);
     delete j;
     return ps_cuda_check(e, "pearson setup");
   }
@@ -505,7 +557,7 @@ static int pearson_center_upto(ps_pearson_job* j, int64_t r1, cudaStream_t s) {
   r1 = std::min<int64_t>(a->F, r1);
   if (!j->xc || r1 <= j->c_done) return PS_OK;
   center_rows_kernel<<<(unsigned)(r1 - j->c_done), 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->d_center, j->xc,
-                                                                j->c_done);
+                                                                j->xq, j->c_done);
   PS_LAUNCHED();
   j->c_done = r1;
   return PS_OK;
@@ -517,12 +569,8 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
-  if (j->xc)
-    pearson_tile_kernel<true><<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(j->xc, a->ld, a->d_mask, W, a->d_center,
-                                                                            F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
-  else
-    pearson_tile_kernel<false><<<(unsigned)(t1 - t0), NTHR, kSmemBytes, s>>>(
-        a->d_vals, a->ld, a->d_mask, W, a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
+  launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
+               a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
   ps_prof_end(s);
   PS_LAUNCHED();
   return PS_OK;
@@ -555,6 +603,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->o.replay, j->home);
   ps_free(j->o.replay_count, j->home);
   ps_free(j->xc, j->home);
+  ps_free(j->xq, j->home);
   delete j;
   return rc;
 }
@@ -566,5 +615,6 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->o.replay, j->home);
   ps_free(j->o.replay_count, j->home);
   ps_free(j->xc, j->home);
+  ps_free(j->xq, j->home);
   delete j;
 }

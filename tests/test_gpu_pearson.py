@@ -98,3 +98,19 @@ def test_pearson_config5_recipe_full_sample_count(oracle):
     mat = ps.make_matrix(x, "continuous", na_sentinel=wl.SENTINEL)
     req = ps.TestRequest("pearson", ("stat", "p", "r2"))
     _check(ps.run(req, mat), oracle.oracle_run(req, mat))
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_operand_modes_bit_identical(monkeypatch, mode):
+    """Pre-centred operands (default: x' computed once per element) are the
+    tile loop's own fp64 subtraction done ahead: every output bit equals the
+    other variants (PS_PEARSON_MODE=0 raw values, 2 x' and x'^2 precomputed)."""
+    x = workloads.simulate(300, 2000, "continuous", na_ratio=0.2, seed=123)
+    x[5] = 7.25  # constant row: replay path
+    mat = ps.make_matrix(x, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p", "r2", "p_bh"))
+    want = ps.run(req, mat)
+    monkeypatch.setenv("PS_PEARSON_MODE", mode)
+    got = ps.run(req, mat)
+    for n in req.outputs:
+        assert np.array_equal(got[n].view(np.uint64), want[n].view(np.uint64)), n
