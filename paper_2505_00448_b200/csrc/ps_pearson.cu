@@ -47,9 +47,12 @@ struct Stage {
   uint32_t mi[T];
   uint32_t mj[T];
 };
-constexpr int NSTAGE = 3;
-template <int MODE>
-constexpr size_t smem_bytes() { return NSTAGE * sizeof(Stage<MODE>); }
+// CPB chunks are computed per block barrier: CPB = 1 -> a 3-stage ring
+// (prefetch distance 2 chunks), CPB = 2 -> a 4-stage ring filled in pairs
+template <int CPB>
+constexpr int nstage() { return CPB == 1 ? 3 : 2 * CPB; }
+template <int MODE, int CPB = 1>
+constexpr size_t smem_bytes() { return nstage<CPB>() * sizeof(Stage<MODE>); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -129,7 +132,7 @@ __global__ void center_rows_kernel(const double* __restrict__ vals, int64_t ld, 
 // grid.x = tiles in range x nsplit.  Each CTA accumulates one 64x64 tile over
 // its share of the k-chunks.  MODE >= 1: vals holds pre-centred x'
 // (center_rows_kernel); MODE 2: sq holds x'^2.
-template <int MODE>
+template <int MODE, int CPB>
 __global__ void __launch_bounds__(NTHR, 1)
 pearson_tile_kernel(const double* __restrict__ vals, const double* __restrict__ sq, int64_t ld,
                     const uint32_t* __restrict__ mask, int64_t W, const double* __restrict__ center, int64_t F,
@@ -206,19 +209,27 @@ pearson_tile_kernel(const double* __restrict__ vals, const double* __restrict__ 
     asm volatile("cp.async.commit_group;");
   };
 
-  for (int q = 0; q < NSTAGE - 1; ++q) {
+  constexpr int NSTAGE = nstage<CPB>();
+  constexpr int AHEAD = CPB == 1 ? NSTAGE - 1 : CPB;  // chunks loaded before the loop
+  for (int q = 0; q < AHEAD; ++q) {
     if (c_begin + q < c_end) issue(c_begin + q, st[q]);
     else asm volatile("cp.async.commit_group;");
   }
-  for (int64_t c = c_begin; c < c_end; ++c) {
-    const int cur = (int)((c - c_begin) % NSTAGE);
-    asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2));
+  for (int64_t cb = c_begin; cb < c_end; cb += CPB) {
+    // the chunks [cb, cb + CPB) have landed (CPB = 1: one newer group may
+    // still be in flight)
+    if (CPB == 1) asm volatile("cp.async.wait_group %0;" ::"n"(NSTAGE - 2));
+    else asm volatile("cp.async.wait_group 0;");
     __syncthreads();
-    {
-      const int64_t cn = c + NSTAGE - 1;
+#pragma unroll
+    for (int q = 0; q < CPB; ++q) {
+      const int64_t cn = cb + (CPB == 1 ? NSTAGE - 1 : CPB) + q;
       if (cn < c_end) issue(cn, st[(int)((cn - c_begin) % NSTAGE)]);
       else asm volatile("cp.async.commit_group;");
     }
+#pragma unroll 1
+    for (int64_t c = cb; c < cb + CPB && c < c_end; ++c) {
+    const int cur = (int)((c - c_begin) % NSTAGE);
     const Stage& s = st[cur];
     uint32_t mrow[WM], mcol[WN];
 #pragma unroll
@@ -267,6 +278,7 @@ pearson_tile_kernel(const double* __restrict__ vals, const double* __restrict__ 
 #pragma unroll
         for (int e = 0; e < 2; ++e) an[i][j][e] += __popc(a & s.mj[wj * 8 * WN + j * 8 + 2 * fk + e]);
     }
+    }  // chunks of this barrier
   }
   asm volatile("cp.async.wait_group 0;");
 
@@ -399,6 +411,15 @@ __global__ void pearson_replay_kernel(const double* __restrict__ vals, int64_t l
 // default 1: x' once per element took the config-5 step 7209 -> 6627 ms
 // (bitwise identical); precomputed squares (mode 2) measured no faster
 // (613.6 vs 613.9 ms at 6000 x 10^5) and cost another F x ld buffer
+// chunks per block barrier (PS_PEARSON_CPB: 1, 2 or 3; default 3: config-5
+// recipe at 6000 x 10^5 614.4 (1) -> 603.0 (2) -> 600.0 ms (3, six stages,
+// 224 KB), bitwise identical)
+static int pearson_cpb() {
+  const char* e = getenv("PS_PEARSON_CPB");
+  const int v = e ? atoi(e) : 3;
+  return v <= 1 ? 1 : v >= 3 ? 3 : 2;
+}
+
 static int pearson_mode() {
   const char* e = getenv("PS_PEARSON_MODE");
   const int m = e ? atoi(e) : 1;
@@ -406,30 +427,39 @@ static int pearson_mode() {
 }
 
 // (a function attribute is per device: set on every call)
+template <int MODE, int CPB>
+static cudaError_t set_attr() {
+  return cudaFuncSetAttribute(pearson_tile_kernel<MODE, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem_bytes<MODE, CPB>());
+}
 static cudaError_t set_tile_attrs() {
-  cudaError_t e = cudaFuncSetAttribute(pearson_tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem_bytes<0>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(pearson_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_bytes<1>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(pearson_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_bytes<2>());
+  cudaError_t e = set_attr<0, 1>();
+  if (e == cudaSuccess) e = set_attr<1, 1>();
+  if (e == cudaSuccess) e = set_attr<2, 1>();
+  if (e == cudaSuccess) e = set_attr<1, 2>();
+  if (e == cudaSuccess) e = set_attr<1, 3>();
   return e;
 }
 
 static void launch_tiles(int mode, unsigned grid, cudaStream_t s, const double* vals, const double* sq, int64_t ld,
                          const uint32_t* mask, int64_t W, const double* center, int64_t F, int64_t NT, int64_t tile0,
                          int64_t lo, int64_t hi, int nsplit, int64_t cps, const Outs& o, double* ws, int colmajor) {
-  if (mode == 2)
-    pearson_tile_kernel<2><<<grid, NTHR, smem_bytes<2>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
-                                                               nsplit, cps, o, ws, colmajor);
+  const int cpb = pearson_cpb();
+  if (mode == 1 && cpb == 3)
+    pearson_tile_kernel<1, 3><<<grid, NTHR, smem_bytes<1, 3>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo,
+                                                                     hi, nsplit, cps, o, ws, colmajor);
+  else if (mode == 1 && cpb == 2)
+    pearson_tile_kernel<1, 2><<<grid, NTHR, smem_bytes<1, 2>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo,
+                                                                     hi, nsplit, cps, o, ws, colmajor);
+  else if (mode == 2)
+    pearson_tile_kernel<2, 1><<<grid, NTHR, smem_bytes<2, 1>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo,
+                                                                     hi, nsplit, cps, o, ws, colmajor);
   else if (mode == 1)
-    pearson_tile_kernel<1><<<grid, NTHR, smem_bytes<1>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
-                                                               nsplit, cps, o, ws, colmajor);
+    pearson_tile_kernel<1, 1><<<grid, NTHR, smem_bytes<1, 1>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo,
+                                                                     hi, nsplit, cps, o, ws, colmajor);
   else
-    pearson_tile_kernel<0><<<grid, NTHR, smem_bytes<0>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo, hi,
-                                                               nsplit, cps, o, ws, colmajor);
+    pearson_tile_kernel<0, 1><<<grid, NTHR, smem_bytes<0, 1>(), s>>>(vals, sq, ld, mask, W, center, F, NT, tile0, lo,
+                                                                     hi, nsplit, cps, o, ws, colmajor);
 }
 
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
