@@ -421,6 +421,28 @@ def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, 
             "work_per_pair_sample": desc}
 
 
+def _reduce(vals, op):
+    import torch
+    import torch.distributed as tdist
+
+    dev = "cuda" if tdist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=op)
+    return [float(x) for x in t.cpu()]
+
+
+def reduce_max(vals):
+    import torch.distributed as tdist
+
+    return _reduce(vals, tdist.ReduceOp.MAX)
+
+
+def reduce_sum(vals):
+    import torch.distributed as tdist
+
+    return _reduce(vals, tdist.ReduceOp.SUM)
+
+
 def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int, local: int, peaks: dict,
                    clocks=None):
     """Device-resident steps; returns (ms_per_step, roofline, launches, clock summary)."""
@@ -460,7 +482,8 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
         if shard_presort and test == "spearman":
             # each rank presorts 1/world of the features; NCCL all-gathers the tables
             da = blocks.DeviceMatrix(xa, wl.kind_a, workloads.SENTINEL, wl.cat_a, n_samples=S, stream=stream)
-            da.presort_sharded(rank, world, stream=stream)
+            da.presort_sharded(rank, world, stream=stream,
+                               gather=lambda name, full, local_: dist.all_gather(full, local_))
         else:
             da = blocks.DeviceMatrix(xa, wl.kind_a, workloads.SENTINEL, wl.cat_a, n_samples=S,
                                      presort=test == "spearman", stream=stream)
@@ -514,9 +537,7 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
     kern_ms, kern_n = _lib.profile_collect_union(ROOF[test][3])
     total_ms = sum(times)
     if world > 1:
-        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, kern_ms = float(t[0].item()), float(t[1].item())
+        total_ms, kern_ms = reduce_max([total_ms, kern_ms])
     del outs, adj_outs, flush, shard_a, shard_b
     torch.cuda.empty_cache()
     return total_ms / steps, roofline(wl, kern_ms, kern_n, steps, world, peaks), launches, clk
@@ -556,10 +577,8 @@ def measure_e2e(wl: Workload, steps: int, warmup: int, world: int):
     d2h = sum(np.asarray(res[n]).nbytes for n in wl.outputs)
     h2d = wl.a_rows.nbytes + (wl.b_rows.nbytes if wl.b_rows is not None else 0)
     if world > 1:
-        t = torch.tensor([dt, float(d2h), float(h2d)], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t[:1], op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t[1:], op=torch.distributed.ReduceOp.SUM)
-        dt, d2h, h2d = float(t[0]), float(t[1]), float(t[2])
+        (dt,) = reduce_max([dt])
+        d2h, h2d = reduce_sum([float(d2h), float(h2d)])
     return {"value": wl.pairs * wl.S / dt, "unit": "pair-samples/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
             "api": "run()" if world == 1 else "dist.sharded_run(assemble='owned')"}
@@ -589,13 +608,20 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU over NCCL; PS_BENCH_BACKEND=gloo + PS_BENCH_DEVICE=0
+    # run the N > 1 code path with every rank on one device (a functional
+    # check on a one-GPU box -- its timings mean nothing)
+    local = int(os.environ.get("PS_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    backend = os.environ.get("PS_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     _lib.check(_lib.load().ps_set_device(local))
     if world > 1:
         import torch.distributed as tdist
 
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
 
     cfg_key = args.config
     test = args.test or default_test(cfg_key)

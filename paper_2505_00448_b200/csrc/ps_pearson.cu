@@ -68,6 +68,7 @@ struct Outs {
   int* replay_count;
   int replay_cap;
   int* err;
+  int defer_p;  // 1: the tile epilogue parks n in p; pearson_p_kernel evaluates the tail
 };
 
 __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
@@ -89,6 +90,7 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
     if (!(sxx > kReplayTau * qx) || !(syy > kReplayTau * (diag ? qx : qy))) {
       int slot = atomicAdd(o.replay_count, 1);
       if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
+      if (o.defer_p) put(o.p, F, g, h, PS_NAN);  // not a parked n: pearson_p_kernel skips it
       return;  // the replay kernel writes this pair
     }
     const double sxy = diag ? sxx : xy - sx * sy / fn;
@@ -96,13 +98,39 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
     if (r > 1.0) r = 1.0;
     else if (r < -1.0) r = -1.0;
     if (n != 2) {
-      p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, o.err);
-      if (p > 1.0) p = 1.0;
+      if (o.defer_p) {
+        p = fn;  // pearson_p_kernel: p from (r, n) at full occupancy
+      } else {
+        p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, o.err);
+        if (p > 1.0) p = 1.0;
+      }
     }
   }
   put(o.stat, F, g, h, r);
   put(o.p, F, g, h, p);
   put(o.r2, F, g, h, r * r);
+}
+
+// The p-values of the tiles' pairs (continuous.py:47): the tile epilogue
+// parked n in p (NaN where p is NaN by rule, or the pair awaits the exact
+// replay); here one thread per upper-triangle cell of rows [lo, hi) runs the
+// beta continued fraction with the whole SM's warps in flight instead of
+// inside the one-CTA-per-SM tile kernel, where the DMMA pipe idled meanwhile.
+__global__ void pearson_p_kernel(const double* __restrict__ stat, double* __restrict__ pout, int64_t F, int64_t lo,
+                                 int64_t hi, int* __restrict__ err) {
+  const int64_t rows = hi - lo;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < rows * F;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = lo + it / F, h = it % F;
+    if (h < g) continue;
+    const double fn = pout[g * F + h];
+    if (fn != fn) continue;
+    const double r = stat[g * F + h];
+    double p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, err);
+    if (p > 1.0) p = 1.0;
+    pout[g * F + h] = p;
+    pout[h * F + g] = p;
+  }
 }
 
 // x' = x - c_f on present cells, 0 elsewhere, for rows [f0, f0 + grid): the
@@ -490,7 +518,8 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
 
   const int64_t npairs = (hi - lo) * F;  // upper bound on pairs touched
   const int cap = (int)std::min<int64_t>(npairs, 1 << 22);
-  Outs o{stat, p, r2, nullptr, nullptr, cap, ds->d_err};
+  // (the deferred tail needs r: only when stat is an output; PS_PEARSON_INLINE_P=1 keeps it in the tiles)
+  Outs o{stat, p, r2, nullptr, nullptr, cap, ds->d_err, (p && stat && !getenv("PS_PEARSON_INLINE_P")) ? 1 : 0};
   double* ws = nullptr;
   PS_CUDA(ps_alloc(&o.replay, (size_t)cap, s));
   PS_CUDA(ps_alloc(&o.replay_count, 1, s));
@@ -520,6 +549,10 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 256), (int64_t)ds->num_sms * 8);
     pearson_splitk_finish_kernel<<<blocks, 256, 0, s>>>(ws, F, NT, tile0, ntiles, nsplit, lo, hi,
                                                         o);
+    PS_LAUNCHED();
+  }
+  if (o.defer_p) {
+    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(stat, p, F, lo, hi, ds->d_err);
     PS_LAUNCHED();
   }
   {
@@ -559,7 +592,8 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
   j->home = s;
   const int64_t F = a->F;
   const int cap = (int)std::min<int64_t>(F * F, 1 << 22);
-  j->o = Outs{stat, p, r2, nullptr, nullptr, cap, ps_state()->d_err};
+  j->o = Outs{stat, p, r2, nullptr, nullptr, cap, ps_state()->d_err,
+              (p && stat && !getenv("PS_PEARSON_INLINE_P")) ? 1 : 0};
   cudaError_t e = ps_alloc(&j->o.replay, (size_t)cap, s);
   if (e == cudaSuccess) e = ps_alloc(&j->o.replay_count, 1, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(j->o.replay_count, 0, sizeof(int), s);
@@ -624,6 +658,11 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_matrix* a = j->a;
   if (!rc) rc = pearson_center_upto(j, a->F, s);
   if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
+  if (!rc && j->o.defer_p) {
+    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
+    ps_count_launch();
+    if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson p launch");
+  }
   if (!rc) {
     pearson_replay_kernel<<<ds->num_sms * 4, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->S, a->F, j->o.replay,
                                                          j->o.replay_count, j->o.replay_cap, 0, a->F, j->o);
