@@ -628,6 +628,83 @@ __global__ void bh_scatter_pos_kernel(const double* __restrict__ ranked, const d
 }
 
 // ---------------------------------------------------------------------------
+// Small families spread over the whole GPU (BH, m <= kSmallMax): the stable
+// sorted position of p_i is a count -- #{j : k_j < k_i} + #{j < i : k_j == k_i}
+// -- over (i-block x j-block) tiles of the family, the j keys staged in
+// shared memory and read as broadcasts; then one CTA forms the scaled values
+// in sorted order, their reverse cumulative minimum and the scatter.  ~40 us
+// at m = 2e4 instead of the single-CTA radix sort's ~170 us, with the count
+// read on the device (no host round trip).
+constexpr int kRankI = 256, kRankJ = 2048;
+__global__ void __launch_bounds__(kRankI)
+rank_count_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ count,
+                  uint32_t* __restrict__ rank) {
+  __shared__ uint64_t sk[kRankJ];
+  const int m = (int)*count;
+  const int i = blockIdx.x * kRankI + threadIdx.x;
+  const int j0 = blockIdx.y * kRankJ;
+  if (blockIdx.x * kRankI >= m || j0 >= m) return;  // block-uniform
+  const int jn = min(kRankJ, m - j0);
+  for (int t = threadIdx.x; t < jn; t += kRankI) sk[t] = keys[j0 + t];
+  __syncthreads();
+  if (i >= m) return;
+  const uint64_t ki = keys[i];
+  uint32_t c = 0;
+  // j < i ties count as smaller: stable order (the reference's argsort is stable)
+  const int split = min(max(i - j0, 0), jn);
+#pragma unroll 8
+  for (int t = 0; t < split; ++t) c += sk[t] <= ki ? 1u : 0u;
+#pragma unroll 8
+  for (int t = split; t < jn; ++t) c += sk[t] < ki ? 1u : 0u;
+  atomicAdd(&rank[i], c);
+}
+
+__global__ void rank_place_kernel(const uint32_t* __restrict__ rank, const unsigned long long* __restrict__ count,
+                                  uint32_t* __restrict__ pos) {
+  const int m = (int)*count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) pos[rank[i]] = (uint32_t)i;
+}
+
+// one CTA: v_r = p_(r) * (m / (r + 1)), reverse cumulative minimum, scatter
+constexpr int kStepThreads = 1024;
+__global__ void __launch_bounds__(kStepThreads)
+bh_stepup_small_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ fidx,
+                       const uint32_t* __restrict__ pos, const unsigned long long* __restrict__ count, int64_t cols,
+                       int symmetric, double* __restrict__ out) {
+  __shared__ double s_tmin[kStepThreads / 32];
+  const int m = (int)*count;
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (m + kStepThreads - 1) / kStepThreads;
+  const int i0 = threadIdx.x * per, i1 = min(m, i0 + per);
+  const double scale = (double)m;
+  auto scaled = [&](int r) { return val_of(keys[pos[r]]) * (scale / (double)(r + 1)); };
+  double tmin = CUDART_INF;
+  for (int r = i0; r < i1; ++r) tmin = fmin(tmin, scaled(r));
+  double wmin = tmin;  // suffix minimum over this warp's later threads (inclusive)
+#pragma unroll
+  for (int sft = 1; sft < 32; sft <<= 1) {
+    const double y = __shfl_down_sync(PS_FULL, wmin, sft);
+    if (lane + sft < 32) wmin = fmin(wmin, y);
+  }
+  if (lane == 0) s_tmin[warp] = wmin;
+  __syncthreads();
+  double run = __shfl_down_sync(PS_FULL, wmin, 1);
+  if (lane == 31) run = CUDART_INF;
+  for (int w = warp + 1; w < kStepThreads / 32; ++w) run = fmin(run, s_tmin[w]);
+  for (int r = i1 - 1; r >= i0; --r) {
+    run = fmin(run, scaled(r));
+    const double v = fmin(1.0, run);
+    const int64_t f = fidx[pos[r]];
+    out[f] = v;
+    if (symmetric) {
+      const int64_t rr = f / cols, cc = f - rr * cols;
+      out[cc * cols + rr] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Small families (m <= kSmallMax): the whole BH / BY adjustment in one CTA --
 // stable LSD radix on the high 32 key bits in registers / shared memory (as
 // the presort), short runs of equal high halves repaired on the low halves
@@ -970,7 +1047,23 @@ int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     PS_LAUNCHED();
     return PS_OK;
   }
-  if (method == PS_ADJ_BH && fam_max <= kSmallMax) {
+  if (method == PS_ADJ_BH && fam_max <= kSmallMax && !getenv("PS_ADJUST_SMALL_CTA")) {
+    uint32_t *rank = nullptr, *pos = nullptr;
+    PS_CUDA(ps_alloc(&rank, (size_t)std::max<int64_t>(fam_max, 1), s));
+    PS_CUDA(ps_alloc(&pos, (size_t)std::max<int64_t>(fam_max, 1), s));
+    PS_CUDA(cudaMemsetAsync(rank, 0, sizeof(uint32_t) * std::max<int64_t>(fam_max, 1), s));
+    const dim3 grid((unsigned)ps_ceil_div(fam_max, kRankI), (unsigned)ps_ceil_div(fam_max, kRankJ));
+    rank_count_kernel<<<grid, kRankI, 0, s>>>(keys, d_count, rank);
+    PS_LAUNCHED();
+    rank_place_kernel<<<(unsigned)std::max<int64_t>(1, ps_ceil_div(fam_max, 256)), 256, 0, s>>>(rank, d_count, pos);
+    PS_LAUNCHED();
+    bh_stepup_small_kernel<<<1, kStepThreads, 0, s>>>(keys, idx, pos, d_count, cols, symmetric, out);
+    PS_LAUNCHED();
+    ps_free(rank, s);
+    ps_free(pos, s);
+    return PS_OK;
+  }
+  if (method == PS_ADJ_BH && fam_max <= kSmallMax) {  // PS_ADJUST_SMALL_CTA: the single-CTA radix sort (A/B)
     const size_t smem = (size_t)kSmallMax * 6;
     PS_CUDA(cudaFuncSetAttribute(adjust_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     adjust_small_kernel<<<1, kSmallThreads, smem, s>>>(keys, idx, d_count, 1.0, cols, symmetric, out);

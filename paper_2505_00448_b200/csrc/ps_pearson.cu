@@ -519,7 +519,10 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   const int64_t npairs = (hi - lo) * F;  // upper bound on pairs touched
   const int cap = (int)std::min<int64_t>(npairs, 1 << 22);
   // (the deferred tail needs r: only when stat is an output; PS_PEARSON_INLINE_P=1 keeps it in the tiles)
-  Outs o{stat, p, r2, nullptr, nullptr, cap, ds->d_err, (p && stat && !getenv("PS_PEARSON_INLINE_P")) ? 1 : 0};
+  // (deferred only when the tiles fill the GPU: config 5 6000 x 10^5 600.1 ->
+  // 588.7 ms; at 200 x 1000 the extra launch costs more than it saves)
+  const bool defer = p && stat && !getenv("PS_PEARSON_INLINE_P") && ntiles_all >= ds->num_sms;
+  Outs o{stat, p, r2, nullptr, nullptr, cap, ds->d_err, defer ? 1 : 0};
   double* ws = nullptr;
   PS_CUDA(ps_alloc(&o.replay, (size_t)cap, s));
   PS_CUDA(ps_alloc(&o.replay_count, 1, s));
@@ -592,8 +595,9 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
   j->home = s;
   const int64_t F = a->F;
   const int cap = (int)std::min<int64_t>(F * F, 1 << 22);
+  const int64_t nt = ps_ceil_div(F, T);
   j->o = Outs{stat, p, r2, nullptr, nullptr, cap, ps_state()->d_err,
-              (p && stat && !getenv("PS_PEARSON_INLINE_P")) ? 1 : 0};
+              (p && stat && !getenv("PS_PEARSON_INLINE_P") && nt * (nt + 1) / 2 >= ps_state()->num_sms) ? 1 : 0};
   cudaError_t e = ps_alloc(&j->o.replay, (size_t)cap, s);
   if (e == cudaSuccess) e = ps_alloc(&j->o.replay_count, 1, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(j->o.replay_count, 0, sizeof(int), s);
