@@ -93,3 +93,38 @@ def test_two_rank_gloo_matches_single_process(tmp_path, test):
             g = got[name]
             same = (g.view(np.int64) == w.view(np.int64)) | (np.isnan(g) & np.isnan(w))
             assert same.all(), (rank, name)
+
+
+def _gather_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2505_00448_b200 import dist as d
+
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    out = torch.empty((world, 3), dtype=torch.float64)
+    d.all_gather(out, torch.full((3,), float(rank), dtype=torch.float64))
+    torch.save(out, os.path.join(out_dir, f"g{rank}.pt"))
+    tdist.destroy_process_group()
+
+
+def test_all_gather_helper_and_cell_counts(tmp_path):
+    """dist.all_gather (the device exchanges' collective) over gloo with 2-D
+    outputs, and the packed-cell counts of every partition summing to the
+    family (C ABI ps_cells_count, host-only)."""
+    import torch
+
+    mp.spawn(_gather_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        g = torch.load(tmp_path / f"g{r}.pt")
+        assert g.tolist() == [[0.0] * 3, [1.0] * 3]
+    for test, shape in (("pearson", (37, 37)), ("anova", (5, 11)), ("kruskal", (5, 11))):
+        units = 37 if test == "pearson" else (55 if test == "anova" else 11)
+        fam = 37 * 36 // 2 if test == "pearson" else 55
+        for world in (1, 2, 3, 8):
+            ranges = dist.plan(test, shape[0], None if test == "pearson" else shape[1], world)
+            assert sum(dist.cells_count(test, False, shape, lo, hi) for lo, hi in ranges) == fam
+            if test == "pearson":
+                assert sum(dist.cells_count(test, True, shape, lo, hi) for lo, hi in ranges) == fam + 37
+        assert ranges[-1][1] == units
