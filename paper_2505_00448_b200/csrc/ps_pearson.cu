@@ -19,6 +19,8 @@
 // Algorithmic work: 10 FP64 flops per pair-sample (5 masked MACs).
 #include "ps_internal.cuh"
 #include "ps_specfun.cuh"
+#include "ps_tc05.cuh"
+#include <cudaTypedefs.h>
 #include <algorithm>
 
 namespace {
@@ -344,6 +346,168 @@ pearson_tile_kernel(const double* __restrict__ vals, const double* __restrict__ 
       }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (no split-K): the pre-centred x' tiles arrive by
+// cp.async.bulk.tensor in 128-byte-swizzled 64-row x 16-sample boxes and the
+// presence words by a second tensor map, completion counted on per-stage
+// `full` mbarriers; each warp releases a stage on its `empty` mbarrier and
+// thread 0 -- the only producer -- refills a stage once all eight warps have
+// released it, one stage behind, so no block-wide barrier sits in the loop.
+// Same per-lane k order as pearson_tile_kernel: identical bits.
+constexpr int TG = 64;                        // samples per stage (2 mask words)
+constexpr int TBOX = 16;                      // doubles per box row (128 B, SW128)
+constexpr int TNB = TG / TBOX;                // boxes per operand per stage
+constexpr int TBOX_BYTES = T * TBOX * 8;      // 8 KB
+constexpr int TMASK_WORDS = 4;                // mask box: 4 words (16 B) x 64 rows
+constexpr int TSTAGE_BYTES = 2 * TNB * TBOX_BYTES + 2 * T * TMASK_WORDS * 4;
+constexpr int TNS = 3;
+constexpr size_t kTmaSmem = (size_t)TNS * TSTAGE_BYTES + 1024;
+
+__device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
+  // element (row r, sample k within the box) of a SWIZZLE_128B 64 x 16 double box
+  const uint32_t a = box_base + tc05::sw128_offset((uint32_t)r, (uint32_t)(k >> 1)) + (uint32_t)(k & 1) * 8u;
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
+__global__ void __launch_bounds__(NTHR, 1)
+pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap mmap, int64_t W,
+                   int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[TNS], empty[TNS];
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = warp / WJ, wj = warp % WJ;
+  int64_t I, J;
+  if (colmajor) ps_tri_tile_cm(tile0 + blockIdx.x, &I, &J);
+  else ps_tri_tile(tile0 + blockIdx.x, NT, &I, &J);
+  const int row0 = (int)(I * T), col0 = (int)(J * T);
+  const int64_t ngroups = ps_ceil_div(W, TG / 32);
+  if (tid == 0) {
+    for (int i = 0; i < TNS; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], NWARP);
+    }
+    tc05::fence_barrier_init();
+    tc05::prefetch_tmap(&xmap);
+    tc05::prefetch_tmap(&mmap);
+  }
+  __syncthreads();
+  auto stage_addr = [&](int st) { return sbase + (uint32_t)st * TSTAGE_BYTES; };
+  auto issue = [&](int64_t g) {  // thread 0
+    const int st = (int)(g % TNS);
+    const uint32_t a = stage_addr(st);
+    tc05::mbar_arrive_expect_tx(&full[st], TSTAGE_BYTES);
+    const int x0 = (int)(g * TG);
+    for (int b = 0; b < TNB; ++b) {
+      tc05::tma_load_2d(a + b * TBOX_BYTES, &xmap, x0 + b * TBOX, row0, &full[st]);
+      tc05::tma_load_2d(a + (TNB + b) * TBOX_BYTES, &xmap, x0 + b * TBOX, col0, &full[st]);
+    }
+    const uint32_t am = a + 2 * TNB * TBOX_BYTES;
+    tc05::tma_load_2d(am, &mmap, (int)(g * (TG / 32)), row0, &full[st]);
+    tc05::tma_load_2d(am + T * TMASK_WORDS * 4, &mmap, (int)(g * (TG / 32)), col0, &full[st]);
+  };
+  if (tid == 0)
+    for (int64_t g = 0; g < TNS - 1 && g < ngroups; ++g) issue(g);
+
+  const int fr = lane >> 2, fk = lane & 3;
+  double axy[WM][WN][2], asx[WM][WN][2], asxx[WM][WN][2], asy[WM][WN][2], asyy[WM][WN][2];
+  int an[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        axy[i][j][e] = asx[i][j][e] = asxx[i][j][e] = asy[i][j][e] = asyy[i][j][e] = 0.0;
+        an[i][j][e] = 0;
+      }
+  for (int64_t g = 0; g < ngroups; ++g) {
+    if (tid == 0) {  // refill the stage the slowest warp released one group ago
+      const int64_t gn = g + TNS - 1;
+      if (gn < ngroups) {
+        if (gn >= TNS) tc05::mbar_wait(&empty[gn % TNS], (uint32_t)(((gn / TNS) - 1) & 1));
+        issue(gn);
+      }
+    }
+    const int st = (int)(g % TNS);
+    tc05::mbar_wait(&full[st], (uint32_t)((g / TNS) & 1));
+    const uint32_t a = stage_addr(st);
+    const uint32_t* smi = reinterpret_cast<const uint32_t*>(tsm + (size_t)st * TSTAGE_BYTES + 2 * TNB * TBOX_BYTES);
+    const uint32_t* smj = smi + T * TMASK_WORDS;
+#pragma unroll
+    for (int h = 0; h < TG / 32; ++h) {
+      uint32_t mrow[WM], mcol[WN];
+#pragma unroll
+      for (int q = 0; q < WM; ++q) mrow[q] = smi[(wi * 8 * WM + q * 8 + fr) * TMASK_WORDS + h];
+#pragma unroll
+      for (int q = 0; q < WN; ++q) mcol[q] = smj[(wj * 8 * WN + q * 8 + fr) * TMASK_WORDS + h];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = kk * 4 + fk;     // bit within the mask word
+        const int ks = h * 32 + k;     // sample within the stage
+        const uint32_t bi = a + (uint32_t)(ks / TBOX) * TBOX_BYTES;
+        const uint32_t bj = a + (uint32_t)(TNB + ks / TBOX) * TBOX_BYTES;
+        double xa[WM], ma[WM], xa2[WM], xb[WN], mb[WN], xb2[WN];
+#pragma unroll
+        for (int q = 0; q < WM; ++q) {
+          xa[q] = ld_sw(bi, wi * 8 * WM + q * 8 + fr, ks % TBOX);
+          ma[q] = ((mrow[q] >> k) & 1u) ? 1.0 : 0.0;
+          xa2[q] = xa[q] * xa[q];
+        }
+#pragma unroll
+        for (int q = 0; q < WN; ++q) {
+          xb[q] = ld_sw(bj, wj * 8 * WN + q * 8 + fr, ks % TBOX);
+          mb[q] = ((mcol[q] >> k) & 1u) ? 1.0 : 0.0;
+          xb2[q] = xb[q] * xb[q];
+        }
+#pragma unroll
+        for (int i = 0; i < WM; ++i)
+#pragma unroll
+          for (int j = 0; j < WN; ++j) {
+            dmma(axy[i][j][0], axy[i][j][1], xa[i], xb[j]);
+            dmma(asx[i][j][0], asx[i][j][1], xa[i], mb[j]);
+            dmma(asxx[i][j][0], asxx[i][j][1], xa2[i], mb[j]);
+            dmma(asy[i][j][0], asy[i][j][1], ma[i], xb[j]);
+            dmma(asyy[i][j][0], asyy[i][j][1], ma[i], xb2[j]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < WM; ++i) {
+        const uint32_t av = mrow[i];
+#pragma unroll
+        for (int j = 0; j < WN; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            an[i][j][e] += __popc(av & smj[(wj * 8 * WN + j * 8 + 2 * fk + e) * TMASK_WORDS + h]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc05::mbar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t gg = row0 + wi * 8 * WM + i * 8 + fr;
+        const int64_t hh = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
+        if (gg < lo || gg >= hi || hh < gg || hh >= F) continue;
+        pearson_finish(gg, hh, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e], asyy[i][j][e],
+                       axy[i][j][e], o);
+      }
+}
+
+// presence words with a 16-byte-aligned row stride (the mask tensor map's
+// global stride must be a multiple of 16 bytes)
+__global__ void pad_mask_kernel(const uint32_t* __restrict__ mask, int64_t W, int64_t Wp, uint32_t* __restrict__ out) {
+  const int64_t f = blockIdx.x;
+  for (int64_t w = threadIdx.x; w < Wp; w += blockDim.x) out[f * Wp + w] = w < W ? mask[f * W + w] : 0u;
+}
+
 // Split-K reduction (fixed split order => deterministic) + epilogue.
 __global__ void pearson_splitk_finish_kernel(const double* __restrict__ ws, int64_t F, int64_t NT,
                                              int64_t tile0, int64_t ntiles, int nsplit, int64_t lo,
@@ -490,6 +654,54 @@ static void launch_tiles(int mode, unsigned grid, cudaStream_t s, const double* 
                                                                      hi, nsplit, cps, o, ws, colmajor);
 }
 
+// TMA tensor maps of the pre-centred operands and the padded presence words
+static PFN_cuTensorMapEncodeTiled_v12000 pearson_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_pearson_maps(CUtensorMap* xmap, CUtensorMap* mmap, const double* xc, int64_t ld, const uint32_t* mpad,
+                             int64_t Wp, int64_t F) {
+  auto enc = pearson_map_encoder();
+  if (!enc) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)F};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+    cuuint32_t box[2] = {(cuuint32_t)TBOX, (cuuint32_t)T};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(xc), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return ps_fail(PS_ERR_CUDA, "pearson operand tensor map");
+  }
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)Wp, (cuuint64_t)F};
+    cuuint64_t strides[1] = {(cuuint64_t)(Wp * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)TMASK_WORDS, (cuuint32_t)T};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(mmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(mpad), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return ps_fail(PS_ERR_CUDA, "pearson mask tensor map");
+  }
+  return PS_OK;
+}
+
+// the TMA-fed tiles (PS_PEARSON_TMA=0: cp.async tiles) -- pre-centred
+// operands, no split-K; the operand rows must be 16-byte multiples
+static bool pearson_tma_on(int mode, int nsplit, int64_t ld) {
+  const char* e = getenv("PS_PEARSON_TMA");
+  const bool on = !(e && e[0] == '0');
+  return on && mode == 1 && nsplit == 1 && (ld * 8) % 16 == 0;
+}
+
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s) {
   const int64_t F = a->F;
@@ -540,11 +752,28 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
   }
   PS_CUDA(set_tile_attrs());
   const int64_t grid = ntiles * nsplit;
-  ps_prof_begin("pearson_tile", s);
-  launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT, tile0,
-               lo, hi, nsplit, cps, o, ws, 0);
-  ps_prof_end(s);
-  PS_LAUNCHED();
+  uint32_t* mpad = nullptr;
+  if (pearson_tma_on(mode, nsplit, a->ld)) {
+    const int64_t Wp = ps_round_up(W, 4);
+    PS_CUDA(ps_alloc(&mpad, (size_t)(F * Wp), s));
+    pad_mask_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, W, Wp, mpad);
+    PS_LAUNCHED();
+    CUtensorMap xmap, mmap;
+    int rc = make_pearson_maps(&xmap, &mmap, xc, a->ld, mpad, Wp, F);
+    if (rc) return rc;
+    PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    ps_prof_begin("pearson_tile", s);
+    pearson_tma_kernel<<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mmap, W, F, NT, tile0, lo, hi, o, 0);
+    ps_prof_end(s);
+    PS_LAUNCHED();
+  } else {
+    ps_prof_begin("pearson_tile", s);
+    launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT,
+                 tile0, lo, hi, nsplit, cps, o, ws, 0);
+    ps_prof_end(s);
+    PS_LAUNCHED();
+  }
+  ps_free(mpad, s);
   ps_free(xc, s);
   ps_free(xq, s);
   if (nsplit > 1) {
@@ -580,6 +809,10 @@ struct ps_pearson_job {
   ps_matrix* a = nullptr;
   Outs o{};
   int mode = 0;            // operand mode (pearson_mode)
+  bool tma = false;        // TMA-fed tiles (padded presence words + tensor maps)
+  uint32_t* mpad = nullptr;
+  int64_t Wp = 0;
+  CUtensorMap xmap{}, mmap{};
   double* xc = nullptr;    // pre-centred x' (mode >= 1)
   double* xq = nullptr;    // x'^2 (mode 2)
   int64_t c_done = 0;      // rows centred
@@ -605,12 +838,22 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
   if (e == cudaSuccess && j->mode >= 1) e = ps_alloc(&j->xc, (size_t)(F * a->ld), s);
   if (e == cudaSuccess && j->mode == 2) e = ps_alloc(&j->xq, (size_t)(F * a->ld), s);
   if (e == cudaSuccess) e = set_tile_attrs();
+  j->tma = pearson_tma_on(j->mode, 1, a->ld);
+  if (e == cudaSuccess && j->tma) {
+    j->Wp = ps_round_up(a->W, 4);
+    e = ps_alloc(&j->mpad, (size_t)(F * j->Wp), s);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    if (e == cudaSuccess && make_pearson_maps(&j->xmap, &j->mmap, j->xc, a->ld, j->mpad, j->Wp, F) != PS_OK)
+      e = cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) {
     cudaStreamSynchronize(s);
     ps_free(j->o.replay, s);
     ps_free(j->o.replay_count, s);
     ps_free(j->xc, s);
     ps_free(j->xq, s);
+    ps_free(j->mpad, s);
     delete j;
     return ps_cuda_check(e, "pearson setup");
   }
@@ -627,6 +870,11 @@ static int pearson_center_upto(ps_pearson_job* j, int64_t r1, cudaStream_t s) {
   center_rows_kernel<<<(unsigned)(r1 - j->c_done), 256, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->d_center, j->xc,
                                                                 j->xq, j->c_done);
   PS_LAUNCHED();
+  if (j->tma) {
+    pad_mask_kernel<<<(unsigned)(r1 - j->c_done), 256, 0, s>>>(a->d_mask + j->c_done * a->W, a->W, j->Wp,
+                                                              j->mpad + j->c_done * j->Wp);
+    PS_LAUNCHED();
+  }
   j->c_done = r1;
   return PS_OK;
 }
@@ -637,8 +885,11 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
-  launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
-               a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
+  if (j->tma)
+    pearson_tma_kernel<<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mmap, W, F, NT, t0, 0, F, j->o, 1);
+  else
+    launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
+                 a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
   ps_prof_end(s);
   PS_LAUNCHED();
   return PS_OK;
@@ -677,6 +928,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->o.replay_count, j->home);
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
+  ps_free(j->mpad, j->home);
   delete j;
   return rc;
 }
@@ -689,5 +941,6 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->o.replay_count, j->home);
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
+  ps_free(j->mpad, j->home);
   delete j;
 }
