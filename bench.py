@@ -94,19 +94,23 @@ def device_peaks(peaks: dict) -> dict:
     own microbenchmarks (profiles/peaks_r01.json), else nominal."""
     out = {"hbm_gbs": peaks.get("hbm_gbs", 6650.0), "sm_max_mhz": peaks.get("sm_max_mhz", 1965.0)}
     mb = {}
-    f = PROFILES / "peaks_r01.json"
-    if f.exists():
-        try:
-            mb = json.loads(f.read_text())
-        except Exception:
-            mb = {}
+    for name in ("peaks_r01.json", "peaks_r02.json"):  # later rounds add / override
+        f = PROFILES / name
+        if f.exists():
+            try:
+                mb.update(json.loads(f.read_text()))
+            except Exception:
+                pass
     out["dmma_tflops"] = mb.get("dmma_tflops", 37.0)
     out["imma_tops"] = mb.get("imma_mma_sync_tops", 1127.0)
     out["tcgen05_i8_tops"] = mb.get("tcgen05_i8_tops", 4500.0)  # measured: tools/microbench/tc05_peak.cu
-    # SMEM crossbar: 148 SMs x 128 B/clk at the max SM clock (measured copy
-    # throughput, when the microbenchmark ran: profiles/peaks_r0*.json)
-    out["smem_gbs"] = mb.get("smem_gbs", 148 * 128 * out["sm_max_mhz"] * 1e6 / 1e9)
-    out["smem_source"] = "measured" if "smem_gbs" in mb else "derived 148 x 128 B/clk x max clock"
+    # SMEM: the measured conflict-free load bandwidth (tools/microbench/
+    # smem_peak.cu, profiles/peaks_r02.json), else 148 SMs x 128 B/clk x clock
+    if "smem_gbs" in mb:
+        out["smem_gbs"], out["smem_source"] = mb["smem_gbs"], "measured (tools/microbench/smem_peak.cu)"
+    else:
+        out["smem_gbs"] = 148 * 128 * out["sm_max_mhz"] * 1e6 / 1e9
+        out["smem_source"] = "derived 148 x 128 B/clk x max clock"
     return out
 
 

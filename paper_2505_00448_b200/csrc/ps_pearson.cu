@@ -358,10 +358,26 @@ constexpr int TG = 64;                        // samples per stage (2 mask words
 constexpr int TBOX = 16;                      // doubles per box row (128 B, SW128)
 constexpr int TNB = TG / TBOX;                // boxes per operand per stage
 constexpr int TBOX_BYTES = T * TBOX * 8;      // 8 KB
-constexpr int TMASK_WORDS = 4;                // mask box: 4 words (16 B) x 64 rows
+constexpr int TMASK_WORDS = 2;                // presence words per row per stage (cp.async, 8 B)
 constexpr int TSTAGE_BYTES = 2 * TNB * TBOX_BYTES + 2 * T * TMASK_WORDS * 4;
 constexpr int TNS = 3;
 constexpr size_t kTmaSmem = (size_t)TNS * TSTAGE_BYTES + 1024;
+
+// Whole-warp wait on an mbarrier phase: the try_wait loop is C++ (the
+// compiler sees the branch) and the warp reconverges before the
+// warp-synchronous DMMAs that follow -- an asm-internal spin loop would let
+// lanes leave it at different times and reach mma.sync diverged.
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* mbar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(tc05::smem_u32(mbar)), "r"(parity)
+        : "memory");
+  } while (!done);
+  __syncwarp();
+}
 
 __device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
   // element (row r, sample k within the box) of a SWIZZLE_128B 64 x 16 double box
@@ -372,8 +388,8 @@ __device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
 }
 
 __global__ void __launch_bounds__(NTHR, 1)
-pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap mmap, int64_t W,
-                   int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
+pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ mpad, int64_t Wp,
+                   int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TNS], empty[TNS];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -387,29 +403,42 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
   const int64_t ngroups = ps_ceil_div(W, TG / 32);
   if (tid == 0) {
     for (int i = 0; i < TNS; ++i) {
-      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&full[i], 1 + 32);  // lane 0's expect_tx + warp 0's cp.async arrivals
       tc05::mbar_init(&empty[i], NWARP);
     }
     tc05::fence_barrier_init();
     tc05::prefetch_tmap(&xmap);
-    tc05::prefetch_tmap(&mmap);
   }
   __syncthreads();
   auto stage_addr = [&](int st) { return sbase + (uint32_t)st * TSTAGE_BYTES; };
-  auto issue = [&](int64_t g) {  // thread 0
+  // warp 0, converged: lane 0 arms the stage's `full` barrier with the x'
+  // bytes and issues the TMA boxes; every lane copies presence words of two
+  // row-block and two column-block rows (8-byte cp.async, zero-filled past F)
+  // and arrives on `full` when its copies land (noinc: counted in the init)
+  auto issue = [&](int64_t g) {
     const int st = (int)(g % TNS);
     const uint32_t a = stage_addr(st);
-    tc05::mbar_arrive_expect_tx(&full[st], TSTAGE_BYTES);
-    const int x0 = (int)(g * TG);
-    for (int b = 0; b < TNB; ++b) {
-      tc05::tma_load_2d(a + b * TBOX_BYTES, &xmap, x0 + b * TBOX, row0, &full[st]);
-      tc05::tma_load_2d(a + (TNB + b) * TBOX_BYTES, &xmap, x0 + b * TBOX, col0, &full[st]);
+    if (lane == 0) {
+      tc05::mbar_arrive_expect_tx(&full[st], 2 * TNB * TBOX_BYTES);
+      const int x0 = (int)(g * TG);
+      for (int b = 0; b < TNB; ++b) {
+        tc05::tma_load_2d(a + b * TBOX_BYTES, &xmap, x0 + b * TBOX, row0, &full[st]);
+        tc05::tma_load_2d(a + (TNB + b) * TBOX_BYTES, &xmap, x0 + b * TBOX, col0, &full[st]);
+      }
     }
     const uint32_t am = a + 2 * TNB * TBOX_BYTES;
-    tc05::tma_load_2d(am, &mmap, (int)(g * (TG / 32)), row0, &full[st]);
-    tc05::tma_load_2d(am + T * TMASK_WORDS * 4, &mmap, (int)(g * (TG / 32)), col0, &full[st]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = lane + 32 * (q & 1);               // row within the block
+      const int64_t gr = (q < 2 ? row0 : col0) + r;  // feature row
+      const uint32_t dst = am + (uint32_t)((q < 2 ? 0 : T * TMASK_WORDS * 4) + r * TMASK_WORDS * 4);
+      const uint32_t* src = mpad + (gr < F ? gr : 0) * Wp + 2 * g;
+      const uint32_t nbytes = gr < F ? 8u : 0u;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc05::smem_u32(&full[st])) : "memory");
   };
-  if (tid == 0)
+  if (warp == 0)
     for (int64_t g = 0; g < TNS - 1 && g < ngroups; ++g) issue(g);
 
   const int fr = lane >> 2, fk = lane & 3;
@@ -425,15 +454,16 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_consta
         an[i][j][e] = 0;
       }
   for (int64_t g = 0; g < ngroups; ++g) {
-    if (tid == 0) {  // refill the stage the slowest warp released one group ago
+    if (warp == 0) {  // refill the stage the slowest warp released one group ago
       const int64_t gn = g + TNS - 1;
       if (gn < ngroups) {
-        if (gn >= TNS) tc05::mbar_wait(&empty[gn % TNS], (uint32_t)(((gn / TNS) - 1) & 1));
+        if (gn >= TNS && lane == 0) tc05::mbar_wait(&empty[gn % TNS], (uint32_t)(((gn / TNS) - 1) & 1));
+        __syncwarp();
         issue(gn);
       }
     }
     const int st = (int)(g % TNS);
-    tc05::mbar_wait(&full[st], (uint32_t)((g / TNS) & 1));
+    mbar_wait_warp(&full[st], (uint32_t)((g / TNS) & 1));
     const uint32_t a = stage_addr(st);
     const uint32_t* smi = reinterpret_cast<const uint32_t*>(tsm + (size_t)st * TSTAGE_BYTES + 2 * TNB * TBOX_BYTES);
     const uint32_t* smj = smi + T * TMASK_WORDS;
@@ -667,30 +697,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 pearson_map_encoder() {
   return fn;
 }
 
-static int make_pearson_maps(CUtensorMap* xmap, CUtensorMap* mmap, const double* xc, int64_t ld, const uint32_t* mpad,
-                             int64_t Wp, int64_t F) {
+static int make_pearson_map(CUtensorMap* xmap, const double* xc, int64_t ld, int64_t F) {
   auto enc = pearson_map_encoder();
   if (!enc) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)F};
-    cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
-    cuuint32_t box[2] = {(cuuint32_t)TBOX, (cuuint32_t)T};
-    cuuint32_t es[2] = {1, 1};
-    if (enc(xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(xc), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return ps_fail(PS_ERR_CUDA, "pearson operand tensor map");
-  }
-  {
-    cuuint64_t dims[2] = {(cuuint64_t)Wp, (cuuint64_t)F};
-    cuuint64_t strides[1] = {(cuuint64_t)(Wp * 4)};
-    cuuint32_t box[2] = {(cuuint32_t)TMASK_WORDS, (cuuint32_t)T};
-    cuuint32_t es[2] = {1, 1};
-    if (enc(mmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(mpad), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return ps_fail(PS_ERR_CUDA, "pearson mask tensor map");
-  }
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)F};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)TBOX, (cuuint32_t)T};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(xc), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return ps_fail(PS_ERR_CUDA, "pearson operand tensor map");
   return PS_OK;
 }
 
@@ -758,12 +775,12 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     PS_CUDA(ps_alloc(&mpad, (size_t)(F * Wp), s));
     pad_mask_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, W, Wp, mpad);
     PS_LAUNCHED();
-    CUtensorMap xmap, mmap;
-    int rc = make_pearson_maps(&xmap, &mmap, xc, a->ld, mpad, Wp, F);
+    CUtensorMap xmap;
+    int rc = make_pearson_map(&xmap, xc, a->ld, F);
     if (rc) return rc;
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     ps_prof_begin("pearson_tile", s);
-    pearson_tma_kernel<<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mmap, W, F, NT, tile0, lo, hi, o, 0);
+    pearson_tma_kernel<<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
     ps_prof_end(s);
     PS_LAUNCHED();
   } else {
@@ -812,7 +829,7 @@ struct ps_pearson_job {
   bool tma = false;        // TMA-fed tiles (padded presence words + tensor maps)
   uint32_t* mpad = nullptr;
   int64_t Wp = 0;
-  CUtensorMap xmap{}, mmap{};
+  CUtensorMap xmap{};
   double* xc = nullptr;    // pre-centred x' (mode >= 1)
   double* xq = nullptr;    // x'^2 (mode 2)
   int64_t c_done = 0;      // rows centred
@@ -844,7 +861,7 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
     e = ps_alloc(&j->mpad, (size_t)(F * j->Wp), s);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    if (e == cudaSuccess && make_pearson_maps(&j->xmap, &j->mmap, j->xc, a->ld, j->mpad, j->Wp, F) != PS_OK)
+    if (e == cudaSuccess && make_pearson_map(&j->xmap, j->xc, a->ld, F) != PS_OK)
       e = cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) {
@@ -886,7 +903,8 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
   if (j->tma)
-    pearson_tma_kernel<<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mmap, W, F, NT, t0, 0, F, j->o, 1);
+    pearson_tma_kernel<<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F, j->o,
+                                                                   1);
   else
     launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
                  a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
