@@ -79,6 +79,9 @@ __global__ void onehot_bits_kernel(const CT* __restrict__ codes, int64_t ldc,
 }
 
 // M[r][h] moments over upper-left-aligned 64 x 64 tiles of (label rows x features)
+// PC: vals holds the pre-centred x' (ps_center_rows; 0 where missing), so the
+// DMMA loop skips the per-use subtract / select (bitwise the same operands)
+template <bool PC>
 __global__ void __launch_bounds__(NTH, 2)
 group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double* __restrict__ vals,
                   int64_t ld, const uint32_t* __restrict__ mask, const double* __restrict__ center,
@@ -162,7 +165,7 @@ group_gemm_kernel(const uint32_t* __restrict__ ohbits, int64_t Rp, const double*
 #pragma unroll
       for (int q = 0; q < WN; ++q) {
         const bool pb = (mcol[q] >> k) & 1u;
-        xb[q] = pb ? s.x[wj * 8 * WN + q * 8 + fr][k] - cj[q] : 0.0;
+        xb[q] = PC ? s.x[wj * 8 * WN + q * 8 + fr][k] : (pb ? s.x[wj * 8 * WN + q * 8 + fr][k] - cj[q] : 0.0);
         xb2[q] = xb[q] * xb[q];
       }
 #pragma unroll
@@ -733,8 +736,17 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
   launch_onehot_bits(lab, W, d_rf, d_rl, R, Rp, bits, s);
   PS_LAUNCHED();
   const size_t smem = NSTAGE * sizeof(Stage);
-  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = (rtile1 - rtile0) * ctiles;
+  // pre-centred operands (PS_GROUP_RAW=1: centre inside the DMMA loop, A/B)
+  double* xc = nullptr;
+  const bool pc = !getenv("PS_GROUP_RAW");
+  if (pc && grid > 0) {
+    PS_CUDA(ps_alloc(&xc, (size_t)(Fq * val->ld), s));
+    int crc = ps_center_rows(val, xc, 0, Fq, s);
+    if (crc) return crc;
+  }
   int32_t* Pn = nullptr;
   double *Ps = nullptr, *Pq = nullptr;
   if (grid > 0) {
@@ -749,11 +761,17 @@ int ps_group_moment_run(int test, ps_matrix* lab, ps_matrix* val, int64_t lo, in
       PS_CUDA(ps_alloc(&Pq, (size_t)(kparts * stride), s));
     }
     ps_prof_begin("group_gemm", s);
-    group_gemm_kernel<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
-        bits, Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, 0, ctiles, kparts > 1 ? Pn : Mn,
-        kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride, Fq, 0);
+    if (pc)
+      group_gemm_kernel<true><<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
+          bits, Rp, xc, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, 0, ctiles, kparts > 1 ? Pn : Mn,
+          kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride, Fq, 0);
+    else
+      group_gemm_kernel<false><<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
+          bits, Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, rtile0, 0, ctiles, kparts > 1 ? Pn : Mn,
+          kparts > 1 ? Ps : Ms, kparts > 1 ? Pq : Mq, kparts, stride, Fq, 0);
     ps_prof_end(s);
     PS_LAUNCHED();
+    ps_free(xc, s);
     if (kparts > 1) {
       const int64_t r0 = rtile0 * T, r1 = rtile1 * T;
       const int blocks = (int)std::min<int64_t>(ps_ceil_div((r1 - r0) * Fq, 256), (int64_t)ds->num_sms * 8);
@@ -789,6 +807,8 @@ struct ps_group_job {
   ps_matrix* lab = nullptr;
   ps_matrix* val = nullptr;
   int64_t R = 0, Rp = 0, h_done = 0;
+  double* xc = nullptr;  // pre-centred x' (rows [0, c_done) ready)
+  int64_t c_done = 0;
   uint32_t* bits = nullptr;
   int32_t *d_rf = nullptr, *d_rl = nullptr, *d_off = nullptr, *Mn = nullptr, *repc = nullptr;
   double *Ms = nullptr, *Mq = nullptr;
@@ -803,6 +823,7 @@ struct ps_group_job {
 };
 
 static void group_job_free(ps_group_job* j, cudaStream_t s) {
+  ps_free(j->xc, s);
   ps_free(j->bits, s);
   ps_free(j->d_rf, s);
   ps_free(j->d_rl, s);
@@ -832,7 +853,8 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
   ps_matrix* val = j->val;
   const int64_t Fq = val->F, W = val->W, rtiles = ps_ceil_div(j->R, T), ctiles = ct1 - ct0;
   const size_t smem = NSTAGE * sizeof(Stage);
-  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PS_CUDA(cudaFuncSetAttribute(group_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = rtiles * ctiles;
   const int64_t kparts = group_kparts(ds, j->R, Fq, W, ps_round_up(val->S, 32));
   const int64_t rows = rtiles * T, width = ctiles * T, c0 = ct0 * T, stride = rows * width;
@@ -851,8 +873,9 @@ static int group_gemm_cols(ps_group_job* j, int64_t ct0, int64_t ct1, cudaStream
     PS_CUDA(ps_alloc(&Pq, (size_t)(kparts * stride), s));
   }
   ps_prof_begin("group_gemm", s);
-  group_gemm_kernel<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
-      j->bits, j->Rp, val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, 0, ct0, ctiles,
+  auto kern = j->xc ? group_gemm_kernel<true> : group_gemm_kernel<false>;
+  kern<<<dim3((unsigned)grid, (unsigned)kparts), NTH, smem, s>>>(
+      j->bits, j->Rp, j->xc ? j->xc : val->d_vals, val->ld, val->d_mask, val->d_center, W, Fq, 0, ct0, ctiles,
       kparts > 1 ? Pn : j->Mn, kparts > 1 ? Ps : j->Ms, kparts > 1 ? Pq : j->Mq, kparts, stride,
       kparts > 1 ? width : Fq, kparts > 1 ? c0 : 0);
   ps_prof_end(s);
@@ -921,6 +944,14 @@ int ps_group_moment_begin(int test, ps_matrix* lab, ps_matrix* val, int student,
     const int64_t kp = group_kparts(ds, j->R, Fq, W, ps_round_up(val->S, 32));
     j->pcap = kp > 1 ? kp * rtiles * T * width_cap : 0;
   }
+  if (!getenv("PS_GROUP_RAW") && j->R > 0) {
+    e = ps_alloc(&j->xc, (size_t)(Fq * val->ld), s);
+    if (e != cudaSuccess) {
+      cudaStreamSynchronize(s);
+      group_job_free(j, s);
+      return ps_cuda_check(e, "group test setup");
+    }
+  }
   // the pageable copies above are staged by the driver: the vectors may go
   *out = j;
   return PS_OK;
@@ -940,6 +971,11 @@ int ps_group_moment_upto(ps_group_job* j, int64_t h1, cudaStream_t s) {
     PS_CUDA(cudaEventRecord(ds->alloc_ev, j->home));
     PS_CUDA(cudaStreamWaitEvent(s, ds->alloc_ev, 0));
   }
+  if (j->xc && h1 > j->c_done) {  // centre the new rows on s: every later launch is ordered after it
+    int crc = ps_center_rows(j->val, j->xc, j->c_done, h1, s);
+    if (crc) return crc;
+    j->c_done = h1;
+  }
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(h1, T), w, j->pn[slot] ? slot : -1);
   j->h_done = h1;
@@ -951,6 +987,10 @@ int ps_group_moment_end(ps_group_job* j, double* stat, double* p, double* eff, c
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix *lab = j->lab, *val = j->val;
   const int64_t Fc = lab->F, Fq = val->F;
+  if (!rc && j->xc && Fq > j->c_done) {
+    rc = ps_center_rows(val, j->xc, j->c_done, Fq, s);
+    j->c_done = Fq;
+  }
   if (!rc) rc = group_gemm_cols(j, j->h_done / T, ps_ceil_div(Fq, T), s);
   j->h_done = Fq;
   if (!rc && j->test == PS_TEST_ANOVA) {

@@ -124,6 +124,8 @@ int ps_presort_end(ps_matrix* m, cudaStream_t s);
 int ps_fill_nan(double* p, int64_t n, cudaStream_t s);
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s);
+// pre-centred operands x' = x - c_f (0 where missing), rows [f0, f1) into out (F x ld)
+int ps_center_rows(const ps_matrix* m, double* out, int64_t f0, int64_t f1, cudaStream_t s);
 // Walk streams for incremental launches: launch k goes to stream k mod
 // kWalkStreams after it waits on `after`; join makes `s` wait on every used one.
 cudaStream_t ps_walk_stream(int k, cudaStream_t after);

@@ -719,6 +719,16 @@ static bool pearson_tma_on(int mode, int nsplit, int64_t ld) {
   return on && mode == 1 && nsplit == 1 && (ld * 8) % 16 == 0;
 }
 
+// x' = x - c_f (0 where missing) for rows [f0, f1) of m into out (F x ld);
+// shared with the ANOVA / t-test moment contraction (ps_group.cu)
+int ps_center_rows(const ps_matrix* m, double* out, int64_t f0, int64_t f1, cudaStream_t s) {
+  if (f1 <= f0) return PS_OK;
+  center_rows_kernel<<<(unsigned)(f1 - f0), 256, 0, s>>>(m->d_vals, m->ld, m->d_mask, m->W, m->d_center, out, nullptr,
+                                                         f0);
+  PS_LAUNCHED();
+  return PS_OK;
+}
+
 int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* r2,
                    cudaStream_t s) {
   const int64_t F = a->F;
