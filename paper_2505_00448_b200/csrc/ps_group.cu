@@ -33,6 +33,16 @@ constexpr int WM = 2, WN = 4;
 constexpr int NSTAGE = 3;
 constexpr double kReplayTau = 1e-6;
 constexpr double kCancelTau = 1e-5;  // mean differences below this fraction of the raw RMS are replayed
+// The reference sums raw (uncentred) values in one pass, so its ssq - sum*mean
+// and its group means carry a rounding error that grows ~ sqrt(n_j) eps raw:
+// the replay thresholds grow with the group size so that any cell whose
+// reference value could be off by more than ~1e-10 relative (data with a
+// large offset over its spread, large groups) is replayed in the reference's
+// own order (advisor finding; tests/test_gpu_mixed.py large-offset cases).
+constexpr double kReplayK = 2.5e-6;   // gs replayed when <= kReplayK sqrt(n_j) raw
+constexpr double kCancelK = 5e-6;     // SSB replayed when max |mean dev| <= kCancelK sqrt(n) rms
+__device__ __forceinline__ double replay_tau(double n) { return fmax(kReplayTau, kReplayK * sqrt(n)); }
+__device__ __forceinline__ double cancel_tau(double n) { return fmax(kCancelTau, kCancelK * sqrt(n)); }
 
 struct Stage {
   double x[T][XS];
@@ -380,7 +390,7 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
             const double gs = qj - sj * mj;
             // the reference forms ssq - sum*mean in raw (uncentred) sums:
             // replay exactly whenever the sign of that could be in doubt
-            if (!(gs > kReplayTau * (qj + nj * c * c))) replay = true;
+            if (!(gs > replay_tau(nj) * (qj + nj * c * c))) replay = true;
             ssw += gs;
             const double mr = mj + c;
             mlo = fmin(mlo, mr);
@@ -390,7 +400,7 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
           // group means that agree to ~1e-4 of the raw magnitudes: SSB is a
           // difference of nearly equal raw means, where the reference's own
           // one-pass rounding is ~1e-9 of it -- replay the reference exactly
-          if (!(maxdev > kCancelTau * rms)) replay = true;
+          if (!(maxdev > cancel_tau((double)n) * rms)) replay = true;
           if (replay) {
             push_replay(o, g, h);
             continue;
@@ -410,8 +420,9 @@ __global__ void group_finish_kernel(int test, const int32_t* __restrict__ Mn, co
         const double w0 = q0 - s0 * m0, w1 = q1 - s1 * m1;
         const double rms0 = sqrt(fmax(0.0, (q0 + 2.0 * c * s0 + (double)n0 * c * c) / (double)n0));
         const double rms1 = sqrt(fmax(0.0, (q1 + 2.0 * c * s1 + (double)n1 * c * c) / (double)n1));
-        if (!(w0 > kReplayTau * (q0 + (double)n0 * c * c)) || !(w1 > kReplayTau * (q1 + (double)n1 * c * c)) ||
-            !(fabs(m0 - m1) > kCancelTau * fmax(rms0, rms1))) {  // (see the ANOVA SSB criterion)
+        if (!(w0 > replay_tau((double)n0) * (q0 + (double)n0 * c * c)) ||
+            !(w1 > replay_tau((double)n1) * (q1 + (double)n1 * c * c)) ||
+            !(fabs(m0 - m1) > cancel_tau((double)(n0 + n1)) * fmax(rms0, rms1))) {  // (see the ANOVA SSB criterion)
           push_replay(o, g, h);
           continue;
         }

@@ -305,6 +305,13 @@ int ps_read_matrix(const char* path, char delim, ps_matrix_file* out) {
         out->err_cell = impl->err_cell.data();
         out->err_cell_len = (int64_t)impl->err_cell.size();
       }
+      // non-ASCII cells before the error (earlier rows; earlier columns of a
+      // malformed row) are parsed by the caller first: one of them may be the
+      // first bad cell in file order
+      impl->fallback.insert(impl->fallback.end(), rfb[(size_t)r].begin(), rfb[(size_t)r].end());
+      out->n_rows = r;
+      out->fallback = impl->fallback.data();
+      out->n_fallback = (int64_t)impl->fallback.size();
       return PS_OK;
     }
     impl->row_ids += rid[(size_t)r];

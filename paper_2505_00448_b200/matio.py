@@ -145,6 +145,12 @@ def read_matrix(path: str, delimiter: str | None = None) -> tuple[np.ndarray, li
             _lib.check(code)
         if res.error == 1:
             raise ValueError(f"{path}: empty matrix file")
+        if res.error in (2, 3) and res.n_fallback:
+            # non-ASCII cells before the error come first in file order
+            flat = np.ctypeslib.as_array(ctypes.cast(res.fallback, ctypes.POINTER(ctypes.c_int64)),
+                                         shape=(res.n_fallback,)).copy()
+            scratch = np.zeros((int(flat.max()) // max(res.n_cols, 1) + 1, max(res.n_cols, 1)))
+            _parse_fallback(path, sep, scratch, flat, max(res.n_cols, 1))
         if res.error == 2:
             raise ValueError(f"{path}: row {res.err_row} has {res.err_count} values, expected {res.n_cols}")
         if res.error == 3:

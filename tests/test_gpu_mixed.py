@@ -225,3 +225,29 @@ def test_rank_tests_large_sample_count(oracle, test):
     assert same_nan(res["stat"], ref["stat"])
     assert bitwise_equal(res["stat"], ref["stat"])
     assert p_close(res["p"], ref["p"])
+
+
+@pytest.mark.parametrize("test", ["anova", "ttest"])
+@pytest.mark.parametrize("offset,spread", [(1000.0, 1.4), (1e4, 3.0), (50.0, 0.01)])
+def test_group_moments_large_offset_large_groups(oracle, test, offset, spread):
+    """Values with a large offset relative to their spread and groups of
+    ~10^4 samples: the reference's one-pass ssq - sum*mean carries a rounding
+    error ~sqrt(n_j) eps raw / gs, which the device must either match by
+    replay or stay within 1e-9 of (advisor finding, ps_group.cu replay rule)."""
+    rng = np.random.default_rng(int(offset) + 7)
+    S = 30000
+    kind = "categorical" if test == "anova" else "dichotomous"
+    lab = workloads.simulate(6, S, kind, categories=3, na_ratio=0.05, seed=int(offset) + 1)
+    val = offset + spread * rng.standard_normal((40, S))
+    val[::4] += spread * 0.05 * np.nan_to_num(lab[0])  # small real group effects on some columns
+    val[rng.random(val.shape) < 0.05] = np.nan
+    ma, mb = ps.make_matrix(lab, kind), ps.make_matrix(val, "continuous")
+    eff = ps.EFFECTS_BY_TEST[test]
+    req = ps.TestRequest(test, ("stat", "p") + eff)
+    res, ref = ps.run(req, ma, mb), oracle.oracle_run(req, ma, mb)
+    for n in req.outputs:
+        assert same_nan(res[n], ref[n]), n
+        if n == "p":
+            assert p_close(res[n], ref[n]), n
+        else:
+            assert max_rel(res[n], ref[n], floor=1e-300) <= 1e-9, (n, max_rel(res[n], ref[n], floor=1e-300))

@@ -90,3 +90,23 @@ def test_read_errors(tmp_path):
 def test_exports_match_reference_surface():
     assert set(matio.__all__) == {"default_ids", "delimiter_for", "format_value", "read_matrix",
                                   "roundtrip_equal", "write_matrix"}
+
+
+@pytest.mark.parametrize("later", ["ragged", "malformed_ascii", "malformed_same_row"])
+def test_first_error_in_file_order_with_non_ascii_cells(tmp_path, later):
+    """A malformed NON-ASCII cell (parsed by Python's float()) before a later
+    ragged row / malformed ASCII cell: the reference raises for the first bad
+    cell in file order (advisor finding), so must the native reader."""
+    import paper_2505_00448_b200 as ps
+
+    lines = ["\tc0\tc1", "r0\t1.5\t2.5", "r1\t١٢x\t3.0"]  # arabic digits + junk: not a float
+    if later == "ragged":
+        lines.append("r2\t1.0")
+    elif later == "malformed_ascii":
+        lines.append("r2\tabc\t1.0")
+    else:
+        lines[2] = "r1\t١٢x\tabc"
+    p = tmp_path / "m.tsv"
+    p.write_text("\n".join(lines) + "\n", encoding="utf-8")
+    with pytest.raises(ValueError, match="row 3, column 1"):
+        ps.read_matrix(str(p))
