@@ -39,8 +39,13 @@ constexpr double kCancelTau = 1e-5;  // mean differences below this fraction of 
 // reference value could be off by more than ~1e-10 relative (data with a
 // large offset over its spread, large groups) is replayed in the reference's
 // own order (advisor finding; tests/test_gpu_mixed.py large-offset cases).
+// Calibrated against the oracle by tests/calibrate_group_replay.py: outside
+// the SSW rule no cell with error > 1e-10 has a mean spread above 6e-7
+// sqrt(n) rms (2.5x margin).  Every replay costs a sequential pass over the
+// pair's samples, so the margin is kept small: at 5e-6 config 4's ANOVA step
+// went 6.4 -> 7.7 ms on replays of null pairs.
 constexpr double kReplayK = 2.5e-6;   // gs replayed when <= kReplayK sqrt(n_j) raw
-constexpr double kCancelK = 5e-6;     // SSB replayed when max |mean dev| <= kCancelK sqrt(n) rms
+constexpr double kCancelK = 1.5e-6;   // SSB replayed when max |mean dev| <= kCancelK sqrt(n) rms
 __device__ __forceinline__ double replay_tau(double n) { return fmax(kReplayTau, kReplayK * sqrt(n)); }
 __device__ __forceinline__ double cancel_tau(double n) { return fmax(kCancelTau, kCancelK * sqrt(n)); }
 
@@ -469,32 +474,41 @@ __device__ __forceinline__ T Strided<T>::operator[](int j) const {
   return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(p) + (size_t)j * sizeof(GroupPart));
 }
 
-__global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, const int32_t* __restrict__ off,
-                                          const double* __restrict__ vals, int64_t ld,
-                                          const uint32_t* __restrict__ vmask, int64_t W, const int2* __restrict__ items,
-                                          int n_items, int kslots, GroupPart* __restrict__ parts) {
-  // one warp per (cell, group), 1024 samples per round: the lanes compact the
-  // group's jointly present values of the round into shared memory in sample
-  // order (coalesced loads), then lane 0 runs the reference's sequential
-  // one-pass sums over them -- a chain of dependent fp64 adds only
-  __shared__ double sbuf[4][1024];  // blockDim.x == 128
-  double* buf = sbuf[threadIdx.x >> 5];
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
-  const int64_t total = (int64_t)n_items * kslots;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += nwarps) {
-    const int it = (int)(t / kslots), j = (int)(t % kslots);
-    const int64_t g = items[it].x, h = items[it].y;
-    const int k = off[g + 1] - off[g];
-    if (j >= k) continue;  // warp-uniform
+// One CTA of two warps per (cell, group) chain, 1024 samples per round:
+// warp 0 compacts the group's jointly present values of round r+1 into one
+// half of a shared double buffer, in sample order (coalesced loads issued one
+// round ahead into registers, ballot-free shuffle compaction), while lane 0
+// of warp 1 runs the reference's sequential one-pass sums over round r -- a
+// chain of dependent DADDs (~8.3 cycles each on B200,
+// tools/microbench/dadd_chain.cu), which is the kernel's floor.  One named
+// barrier per round hands the halves over.
+__global__ void __launch_bounds__(64)
+group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, const int32_t* __restrict__ off,
+                          const double* __restrict__ vals, int64_t ld, const uint32_t* __restrict__ vmask, int64_t W,
+                          const int2* __restrict__ items, int kslots, GroupPart* __restrict__ parts) {
+  __shared__ __align__(16) double sbuf[2][1024];
+  __shared__ uint32_t scnt[2];
+  const int64_t t = blockIdx.x;
+  const int it = (int)(t / kslots), j = (int)(t % kslots);
+  const int64_t g = items[it].x, h = items[it].y;
+  const int k = off[g + 1] - off[g];
+  if (j >= k) return;  // block-uniform
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nr = ps_ceil_div(W, (int64_t)32);
+  if (warp == 0) {
     const uint32_t* oh = ohbits + (int64_t)(off[g] + j) * W;
     const uint32_t* mh = vmask + h * W;
     const double* xv = vals + h * ld;
-    long long n = 0;
-    double sum = 0.0, ssq = 0.0;
-    for (int64_t w0 = 0; w0 < W; w0 += 32) {
-      const uint32_t mw = w0 + lane < W ? oh[w0 + lane] & mh[w0 + lane] : 0u;
+    const uint32_t lt = (1u << lane) - 1u;
+    double v[32];
+    uint32_t mw;
+    auto fetch = [&](int64_t w0) {
+      mw = w0 + lane < W ? __ldg(oh + w0 + lane) & __ldg(mh + w0 + lane) : 0u;
+#pragma unroll
+      for (int q = 0; q < 32; ++q) v[q] = w0 + q < W ? __ldg(xv + (w0 + q) * 32 + lane) : 0.0;
+    };
+    fetch(0);
+    for (int64_t r = 0; r < nr; ++r) {
       const uint32_t c = __popc(mw);
       uint32_t x = c;  // inclusive scan of the words' counts
 #pragma unroll
@@ -502,15 +516,26 @@ __global__ void group_replay_parts_kernel(const uint32_t* __restrict__ ohbits, c
         const uint32_t y = __shfl_up_sync(PS_FULL, x, o);
         if (lane >= o) x += y;
       }
-      const uint32_t excl = x - c, tot = __shfl_sync(PS_FULL, x, 31);
-#pragma unroll 8
+      const uint32_t excl = x - c;
+      double* buf = sbuf[r & 1];
+#pragma unroll
       for (int q = 0; q < 32; ++q) {
         const uint32_t m = __shfl_sync(PS_FULL, mw, q);
         const uint32_t o = __shfl_sync(PS_FULL, excl, q);
-        if ((m >> lane) & 1u) buf[o + __popc(m & lt)] = xv[(w0 + q) * 32 + lane];
+        if ((m >> lane) & 1u) buf[o + __popc(m & lt)] = v[q];
       }
-      __syncwarp();
+      if (lane == 31) scnt[r & 1] = x;
+      if (r + 1 < nr) fetch((r + 1) * 32);
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+    }
+  } else {
+    long long n = 0;
+    double sum = 0.0, ssq = 0.0;
+    for (int64_t r = 0; r < nr; ++r) {
+      asm volatile("bar.sync 1, 64;" ::: "memory");
       if (lane == 0) {
+        const double* buf = sbuf[r & 1];
+        const uint32_t tot = scnt[r & 1];
         uint32_t i = 0;
         for (; i + 4 <= tot; i += 4) {
           const double v0 = buf[i], v1 = buf[i + 1], v2 = buf[i + 2], v3 = buf[i + 3];
@@ -632,19 +657,25 @@ static int group_finish_chunk(int test, ps_matrix* lab, ps_matrix* val, int64_t 
   const int n_items = count;
   if (n_items > 0) {
     const int kslots = test == PS_TEST_ANOVA ? std::max(2, lab->cmax) : 2;
+    // batches of items so that the per-chain partials stay bounded (2^22
+    // chains, 96 MiB) for any level count
+    const int batch = (int)std::max<int64_t>(1, std::min<int64_t>(n_items, (1LL << 22) / kslots));
     GroupPart* parts = nullptr;
-    PS_CUDA(ps_alloc(&parts, (size_t)n_items * kslots, s));
-    const int pblocks = (int)std::min<int64_t>(ps_ceil_div((int64_t)n_items * kslots, 4), (int64_t)ds->num_sms * 8);
-    group_replay_parts_kernel<<<pblocks, 128, 0, s>>>(bits, d_off, val->d_vals, val->ld, val->d_mask, W, rep,
-                                                      n_items, kslots, parts);
-    PS_LAUNCHED();
-    const int fblocks = (int)std::min<int64_t>(ps_ceil_div(n_items, 128), (int64_t)ds->num_sms * 4);
-    if (small)
-      group_replay_finish_kernel<16><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student, o);
-    else
-      group_replay_finish_kernel<256><<<fblocks, 128, 0, s>>>(test, rep, n_items, kslots, parts, d_off, Fq, student,
-                                                             o);
-    PS_LAUNCHED();
+    PS_CUDA(ps_alloc(&parts, (size_t)batch * kslots, s));
+    for (int b0 = 0; b0 < n_items; b0 += batch) {
+      const int nb = std::min(batch, n_items - b0);
+      group_replay_parts_kernel<<<(unsigned)((int64_t)nb * kslots), 64, 0, s>>>(
+          bits, d_off, val->d_vals, val->ld, val->d_mask, W, rep + b0, kslots, parts);
+      PS_LAUNCHED();
+      const int fblocks = (int)std::min<int64_t>(ps_ceil_div(nb, 128), (int64_t)ds->num_sms * 4);
+      if (small)
+        group_replay_finish_kernel<16><<<fblocks, 128, 0, s>>>(test, rep + b0, nb, kslots, parts, d_off, Fq, student,
+                                                               o);
+      else
+        group_replay_finish_kernel<256><<<fblocks, 128, 0, s>>>(test, rep + b0, nb, kslots, parts, d_off, Fq, student,
+                                                                o);
+      PS_LAUNCHED();
+    }
     ps_free(parts, s);
   }
   return PS_OK;

@@ -251,3 +251,23 @@ def test_group_moments_large_offset_large_groups(oracle, test, offset, spread):
             assert p_close(res[n], ref[n]), n
         else:
             assert max_rel(res[n], ref[n], floor=1e-300) <= 1e-9, (n, max_rel(res[n], ref[n], floor=1e-300))
+
+
+@pytest.mark.parametrize("test", ["anova", "ttest"])
+@pytest.mark.parametrize("S", [1000, 9000, 33001])
+def test_group_replay_everywhere_bitwise(oracle, test, S):
+    """Data where every cell fails the conditioning rules (offset 1e4 over
+    spread 3): every statistic comes from the exact replay kernel (staged bit
+    walk, ps_group.cu), which must equal the reference's one-pass order bit
+    for bit -- S not a multiple of the 1024-sample round, and > 2^15."""
+    rng = np.random.default_rng(91 + S)
+    kind = "categorical" if test == "anova" else "dichotomous"
+    lab = workloads.simulate(4, S, kind, categories=5, na_ratio=0.05, seed=92)
+    val = 1e4 + 3.0 * rng.standard_normal((9, S))
+    val[rng.random(val.shape) < 0.05] = np.nan
+    ma, mb = ps.make_matrix(lab, kind), ps.make_matrix(val, "continuous")
+    req = ps.TestRequest(test, ("stat", "p") + ps.EFFECTS_BY_TEST[test])
+    res, ref = ps.run(req, ma, mb), oracle.oracle_run(req, ma, mb)
+    assert same_nan(res["stat"], ref["stat"])
+    assert bitwise_equal(res["stat"], ref["stat"])
+    assert p_close(res["p"], ref["p"])
