@@ -271,6 +271,17 @@ __device__ unsigned long long g_walk_cycles[40];
 
 constexpr unsigned long long kClosed = ~0ull;  // "tie-free: use the closed form"
 
+// Register word records of the S > 32767 walks: a warp walks at most
+// ceil(2048 / SW) words (S <= 65535), one record per lane per slot.
+constexpr int kRecSlots = (2048 / SW + 31) / 32;
+__device__ __forceinline__ uint32_t pick_slot(const uint32_t (&r)[kRecSlots], int i) {
+  uint32_t v = r[0];
+#pragma unroll
+  for (int t = 1; t < kRecSlots; ++t)
+    if (i == t) v = r[t];
+  return v;
+}
+
 template <bool OGS, bool R2>
 __global__ void __launch_bounds__(STH, OGS ? 32 / SW : 16 / SW)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
@@ -513,34 +524,74 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           }
         }
       } else {
+        // S > 32767 (no room for 16-byte word records): the records of the
+        // warp's own words live in registers instead -- lane j of slot i holds
+        // word a0 + 32 i + j's {K, Pfx, T, group-entry / exit prefixes} -- and
+        // reach the walking warp by shuffle; g's order is prefetched one
+        // 8-word group ahead, so neither the tie tables' global loads nor the
+        // prefix lookups sit on the per-word chain.
         const uint32_t* tbgg = tb + g * ldt;
         const uint16_t* lbgg = lastb + g * ldt;
         const uint16_t* nbgg = nextb + g * ldt;
-#pragma unroll 4
-        for (int word = a0; word < a1; ++word) {
-          const uint32_t kw = ld32(kA(word));
-          const uint32_t p = (uint32_t)(word * 32 + lane);
-          uint32_t T, lb, nb;
-          if (OGS) {
-            T = ld32(aTbg + 4 * word);
-            lb = ld16(aLbg + 2 * (word ? word - 1 : 0));
-            nb = ld16(aNbg + 2 * (word + 1));
-          } else {
-            T = tbgg[word];
-            lb = lbgg[word ? word - 1 : 0];
-            nb = nbgg[word + 1];
-          }
-          const uint32_t r2 = tied_r2(T, lb, nb, (uint32_t)ng, kw, ldP(word), pfx);
-          if ((kw >> lane) & 1u) {
-            const uint32_t q = q_at(p);
-            sa2 += (unsigned long long)r2 * r2;
-            if (r2fit) {
-              st16(aR + 2 * q, r2);
+        uint32_t rK[kRecSlots], rP[kRecSlots], rT[kRecSlots], rS[kRecSlots], rE[kRecSlots];
+#pragma unroll
+        for (int i = 0; i < kRecSlots; ++i) {
+          const int w = a0 + 32 * i + lane;
+          rK[i] = rP[i] = rT[i] = rS[i] = rE[i] = 0u;
+          if (w < a1) {
+            uint32_t lb, nb;
+            if (OGS) {
+              rT[i] = ld32(aTbg + 4 * w);
+              lb = ld16(aLbg + 2 * (w ? w - 1 : 0));
+              nb = ld16(aNbg + 2 * (w + 1));
             } else {
-              st16(aR + 2 * q, r2 >> 1);
-              if (r2 & 1u) atomicOr(&sm32[L.par + (q >> 5)], 1u << (q & 31u));
+              rT[i] = tbgg[w];
+              lb = lbgg[w ? w - 1 : 0];
+              nb = nbgg[w + 1];
+            }
+            rK[i] = ld32(kA(w));
+            rP[i] = ldP(w);
+            rS[i] = (rT[i] & 1u) ? rP[i] : pfx(lb);
+            rE[i] = pfx(min(nb, (uint32_t)ng));
+          }
+        }
+        auto og_at = [&](int word) -> uint32_t {
+          if (word >= a1) return 0u;
+          const uint32_t p = (uint32_t)(word * 32 + lane);
+          return OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
+        };
+        uint32_t sc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sc[u] = og_at(a0 + u);
+        for (int w8 = a0; w8 < a1; w8 += 8) {
+          uint32_t sn[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sn[u] = og_at(w8 + 8 + u);
+          const int i = (w8 - a0) >> 5;
+          const uint32_t RK = pick_slot(rK, i), RP = pick_slot(rP, i), RT = pick_slot(rT, i);
+          const uint32_t RS = pick_slot(rS, i), RE = pick_slot(rE, i);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int word = w8 + u;
+            if (word < a1) {  // warp-uniform
+              const int jl = (word - a0) & 31;
+              const uint32_t kw = __shfl_sync(PS_FULL, RK, jl);
+              const uint32_t r2 = word_r2(__shfl_sync(PS_FULL, RT, jl), __shfl_sync(PS_FULL, RS, jl),
+                                          __shfl_sync(PS_FULL, RE, jl), kw, __shfl_sync(PS_FULL, RP, jl));
+              if ((kw >> lane) & 1u) {
+                const uint32_t q = OGS ? sc[u] : ld16(aInv + 2 * sc[u]);
+                sa2 += (unsigned long long)r2 * r2;
+                if (r2fit) {
+                  st16(aR + 2 * q, r2);
+                } else {
+                  st16(aR + 2 * q, r2 >> 1);
+                  if (r2 & 1u) atomicOr(&sm32[L.par + (q >> 5)], 1u << (q & 31u));
+                }
+              }
             }
           }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sc[u] = sn[u];
         }
       }
       __syncthreads();
@@ -657,22 +708,42 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         if (encA) walk2(std::true_type{});
         else walk2(std::false_type{});
       } else {
-#pragma unroll 4
-        for (int word = b0; word < b1; ++word) {
-          const uint32_t kw = ld32(kA(word));
-          const uint32_t q = (uint32_t)(word * 32 + lane);
-          const uint32_t v = ld16(aR + 2 * q);
-          const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
-          const uint32_t r2h = tied_r2(ld32(aTbh + 4 * word), ld16(aLbh + 2 * (word ? word - 1 : 0)),
-                                       ld16(aNbh + 2 * (word + 1)), (uint32_t)nh, kw, ldP(word), pfx);
-          if ((kw >> lane) & 1u) {
-            sab += (unsigned long long)r2g * r2h;
-            sbb += (unsigned long long)r2h * r2h;
-            st16(aR + 2 * q, 0u);
+        // S > 32767: register word records of h's walked words (see pass A)
+        uint32_t rK[kRecSlots], rP[kRecSlots], rT[kRecSlots], rS[kRecSlots], rE[kRecSlots];
+#pragma unroll
+        for (int i = 0; i < kRecSlots; ++i) {
+          const int w = b0 + 32 * i + lane;
+          rK[i] = rP[i] = rT[i] = rS[i] = rE[i] = 0u;
+          if (w < b1) {
+            rT[i] = ld32(aTbh + 4 * w);
+            rK[i] = ld32(kA(w));
+            rP[i] = ldP(w);
+            rS[i] = (rT[i] & 1u) ? rP[i] : pfx(ld16(aLbh + 2 * (w ? w - 1 : 0)));
+            rE[i] = pfx(min(ld16(aNbh + 2 * (w + 1)), (uint32_t)nh));
           }
-          if (!r2fit && tg) {
-            __syncwarp();
-            if (lane == 0) st32(aPar + 4 * word, 0u);
+        }
+#pragma unroll
+        for (int i = 0; i < kRecSlots; ++i) {
+          const int wb = b0 + 32 * i;
+          const int we = min(b1, wb + 32);
+#pragma unroll 4
+          for (int word = wb; word < we; ++word) {
+            const int jl = word - wb;
+            const uint32_t kw = __shfl_sync(PS_FULL, rK[i], jl);
+            const uint32_t q = (uint32_t)(word * 32 + lane);
+            const uint32_t v = ld16(aR + 2 * q);
+            const uint32_t r2g = r2g_of(v, word);  // all lanes (shuffle inside)
+            const uint32_t r2h = word_r2(__shfl_sync(PS_FULL, rT[i], jl), __shfl_sync(PS_FULL, rS[i], jl),
+                                         __shfl_sync(PS_FULL, rE[i], jl), kw, __shfl_sync(PS_FULL, rP[i], jl));
+            if ((kw >> lane) & 1u) {
+              sab += (unsigned long long)r2g * r2h;
+              sbb += (unsigned long long)r2h * r2h;
+              st16(aR + 2 * q, 0u);
+            }
+            if (!r2fit && tg) {
+              __syncwarp();
+              if (lane == 0) st32(aPar + 4 * word, 0u);
+            }
           }
         }
       }
