@@ -282,6 +282,59 @@ __device__ __forceinline__ uint32_t pick_slot(const uint32_t (&r)[kRecSlots], in
   return v;
 }
 
+// Walk of a warp's words [w0, w1) of g's order in groups of G words: the
+// group's order entries (staged in shared memory, or streamed from global
+// memory two groups ahead) are first mapped by pre() -- the gathers of the
+// whole group issue back to back -- and then handed to body(word, value) in
+// word order.  The shared accesses are volatile asm, so without the grouping
+// each word's gather would wait for the previous word's store; the global
+// loads are volatile too, so that ptxas cannot sink them to their use.
+__device__ __forceinline__ uint32_t ldg16_early(const uint16_t* a) {
+  unsigned short v;
+  asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(a));
+  return v;
+}
+template <bool OGS, class Pre, class Body>
+__device__ __forceinline__ void walk_order(const uint16_t* __restrict__ og, uint32_t aOg, int w0, int w1, Pre&& pre,
+                                           Body&& body) {
+  const int lane = threadIdx.x & 31;
+  constexpr int G = 8;
+  uint32_t s0[G], s1[G];
+  auto load = [&](uint32_t (&d)[G], int wb) {
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      const uint32_t p = (uint32_t)((wb + u) * 32 + lane);
+      d[u] = wb + u < w1 ? (OGS ? ld16(aOg + 2 * p) : ldg16_early(og + p)) : 0u;
+    }
+  };
+  load(s0, w0);
+  if (!OGS) load(s1, w0 + G);
+  for (int wb = w0; wb < w1; wb += G) {
+    uint32_t s2[G];
+    if (!OGS) load(s2, wb + 2 * G);
+    uint32_t q[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) q[u] = pre(s0[u]);
+    if (wb + G <= w1) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) body(wb + u, q[u]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        if (wb + u < w1) body(wb + u, q[u]);
+    }
+    if (OGS) {
+      load(s0, wb + G);
+    } else {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        s0[u] = s1[u];
+        s1[u] = s2[u];
+      }
+    }
+  }
+}
+
 template <bool OGS, bool R2>
 __global__ void __launch_bounds__(STH, OGS ? 32 / SW : 16 / SW)
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
@@ -293,7 +346,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
   __shared__ uint32_t wtot[SW], wtotA[SW];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sm32);
+  // the window base comes from a volatile asm so that it stays in a register:
+  // ptxas otherwise re-derives it (S2R SR_CgaCtaId + LEA) inside hot loops
+  uint32_t sb;
+  asm volatile("{\n\t.reg .u64 t;\n\tcvta.to.shared.u64 t, %1;\n\tcvt.u32.u64 %0, t;\n\t}" : "=r"(sb) : "l"(sm32));
   const uint32_t aInv = sb + 2 * L.inv16, aR = sb + 2 * L.R16, aK = sb + 4 * L.K, aP = sb + 2 * L.Pl;
   const uint32_t aPar = sb + 4 * L.par;
   auto kA = [&](uint32_t w) -> uint32_t { return R2 ? aK + 16 * w : aK + 4 * w; };
@@ -443,15 +499,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       unsigned long long sa2 = 0;
       if (encA) {
         uint32_t cnt = 0;
-#pragma unroll(OGS ? 4 : 8)
-        for (int word = a0; word < a1; ++word) {
-          const uint32_t p = (uint32_t)(word * 32 + lane);
-          const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
-          const uint32_t q = ld16(aInv + 2 * s);
+        auto body = [&](int, uint32_t q) {
           const bool keep = q != 0xFFFFu;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
           if (keep) st16(aR + 2 * q, ((uint32_t)warp << 12) | (cnt + __popc(B & ltmask) + 1u));
           cnt += __popc(B);
+        };
+        if (OGS) {  // (64-register kernels: the grouped walk costs more than it saves)
+#pragma unroll 4
+          for (int word = a0; word < a1; ++word)
+            body(word, ld16(aInv + 2 * ld16(aOg + 2 * (uint32_t)(word * 32 + lane))));
+        } else {
+          walk_order<false>(og_g, aOg, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); }, body);
         }
         if (lane == 0) wtotA[warp] = cnt;
         __syncthreads();
@@ -462,15 +521,18 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         // q = inv_h[order_g[p]]; with g's order staged in shared memory the
         // gathered q overwrites it in place, so phase 2 reads it sequentially
         uint32_t cnt = 0;
-#pragma unroll(OGS ? 4 : 8)
-        for (int word = a0; word < a1; ++word) {
-          const uint32_t p = (uint32_t)(word * 32 + lane);
-          const uint32_t s = OGS ? ld16(aOg + 2 * p) : (uint32_t)og_g[p];
-          const uint32_t q = ld16(aInv + 2 * s);
-          if (OGS) st16(aOg + 2 * p, q);
+        auto body = [&](int word, uint32_t q) {
+          if (OGS) st16(aOg + 2 * (uint32_t)(word * 32 + lane), q);
           const uint32_t B = __ballot_sync(PS_FULL, q != 0xFFFFu);
           if (lane == 0) stKP(word, B, cnt);
           cnt += __popc(B);
+        };
+        if (OGS) {
+#pragma unroll 4
+          for (int word = a0; word < a1; ++word)
+            body(word, ld16(aInv + 2 * ld16(aOg + 2 * (uint32_t)(word * 32 + lane))));
+        } else {
+          walk_order<false>(og_g, aOg, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); }, body);
         }
         if (lane == 0) wtot[warp] = cnt;
       }
