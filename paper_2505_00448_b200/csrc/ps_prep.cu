@@ -12,6 +12,11 @@
 namespace {
 
 constexpr int kPrepThreads = 256;
+// samples per CTA: a row is split into fixed segments so that a launch over a
+// few rows (one upload chunk) still puts several CTAs -- several loads in
+// flight -- on every SM.  The segment is a constant, so the pivot's summation
+// order (segment partials added in order) never depends on the launch.
+constexpr int64_t kPrepSeg = 8192;
 
 // CT: uint8_t codes (0xFE out of range, 0xFF missing), or uint16_t when a
 // category count exceeds 254 (0xFFFE / 0xFFFF)
@@ -22,18 +27,21 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
                  double* __restrict__ center, int32_t* __restrict__ count,
                  // label outputs (nullptr for continuous)
                  const int32_t* __restrict__ cat, CT* __restrict__ codes, int64_t ldc,
-                 uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits, int64_t f0) {
+                 uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits, int64_t f0,
+                 double* __restrict__ psum, int32_t* __restrict__ pcnt) {
   const int64_t f = f0 + blockIdx.x;
   const double* row = vals + f * ld;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cf = cat ? cat[f] : 0;
+  const int64_t s_lo = (int64_t)blockIdx.y * kPrepSeg;
+  const int64_t s_hi = min(S, s_lo + kPrepSeg);
   double sum = 0.0;
   int cnt = 0;
   // kU rows of the loop's loads in flight per thread (one 8-B load per thread
-  // at a time leaves HBM mostly idle); processed in the original order, so the
-  // pivot sum is unchanged
+  // at a time leaves HBM mostly idle); processed in the original order
   constexpr int kU = 8;
-  for (int64_t base0 = (int64_t)warp * 32; base0 < S; base0 += (int64_t)kPrepThreads * kU) {
+  static_assert(kPrepSeg % (kPrepThreads * kU) == 0, "segments hold whole load rounds");
+  for (int64_t base0 = s_lo + (int64_t)warp * 32; base0 < s_hi; base0 += (int64_t)kPrepThreads * kU) {
   double vu[kU];
 #pragma unroll
   for (int u = 0; u < kU; ++u) {
@@ -77,7 +85,7 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
     if (lane == 0) mask[f * W + (base >> 5)] = word;
   }
   }
-  if (codes)
+  if (codes && blockIdx.y + 1 == gridDim.y)
     for (int64_t s = S + threadIdx.x; s < ldc; s += kPrepThreads) codes[f * ldc + s] = (CT)~(CT)0;
   // block reduction of (sum, cnt); order is fixed, so the pivot is reproducible.
   __shared__ double ssum[kPrepThreads / 32];
@@ -92,12 +100,34 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
     double t = 0.0;
     int c = 0;
     for (int w = 0; w < kPrepThreads / 32; ++w) { t += ssum[w]; c += scnt[w]; }
-    count[f] = c;
-    // pivot: any finite value works for centring; use the mean when finite.
-    double piv = c > 0 ? t / (double)c : 0.0;
-    if (!isfinite(piv)) piv = 0.0;
-    center[f] = piv;
+    if (psum) {  // several segments: partials, folded in order by prep_finish_kernel
+      psum[blockIdx.x * gridDim.y + blockIdx.y] = t;
+      pcnt[blockIdx.x * gridDim.y + blockIdx.y] = c;
+    } else {
+      count[f] = c;
+      // pivot: any finite value works for centring; use the mean when finite.
+      double piv = c > 0 ? t / (double)c : 0.0;
+      if (!isfinite(piv)) piv = 0.0;
+      center[f] = piv;
+    }
   }
+}
+
+__global__ void prep_finish_kernel(const double* __restrict__ psum, const int32_t* __restrict__ pcnt, int nseg,
+                                   int64_t nrows, int64_t f0, int32_t* __restrict__ count,
+                                   double* __restrict__ center) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  double t = 0.0;
+  int c = 0;
+  for (int y = 0; y < nseg; ++y) {
+    t += psum[r * nseg + y];
+    c += pcnt[r * nseg + y];
+  }
+  count[f0 + r] = c;
+  double piv = c > 0 ? t / (double)c : 0.0;
+  if (!isfinite(piv)) piv = 0.0;
+  center[f0 + r] = piv;
 }
 
 // Label matrices staged from the host as codes: presence / out-of-range bit
@@ -188,15 +218,31 @@ int ps_prepare_alloc(ps_matrix* m, cudaStream_t s) {
 int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
   if (f1 <= f0) return PS_OK;
   const bool labels = m->kind != PS_KIND_CONTINUOUS;
+  const int64_t nrows = f1 - f0;
+  const int nseg = (int)std::max<int64_t>(1, ps_ceil_div(m->S, kPrepSeg));
+  double* psum = nullptr;
+  int32_t* pcnt = nullptr;
+  if (nseg > 1) {
+    PS_CUDA(ps_alloc(&psum, (size_t)(nrows * nseg), s));
+    PS_CUDA(ps_alloc(&pcnt, (size_t)(nrows * nseg), s));
+  }
+  const dim3 grid((unsigned)nrows, (unsigned)nseg);
   if (labels && m->code_bytes == 2)
-    prep_rows_kernel<uint16_t><<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
+    prep_rows_kernel<uint16_t><<<grid, kPrepThreads, 0, s>>>(
         m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
-        m->d_cat, reinterpret_cast<uint16_t*>(m->d_codes), m->ldc, m->d_zero, m->d_bad, f0);
+        m->d_cat, reinterpret_cast<uint16_t*>(m->d_codes), m->ldc, m->d_zero, m->d_bad, f0, psum, pcnt);
   else
-    prep_rows_kernel<uint8_t><<<(unsigned)(f1 - f0), kPrepThreads, 0, s>>>(
+    prep_rows_kernel<uint8_t><<<grid, kPrepThreads, 0, s>>>(
         m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
-        labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero, m->d_bad, f0);
+        labels ? m->d_cat : nullptr, m->d_codes, m->ldc, m->d_zero, m->d_bad, f0, psum, pcnt);
   PS_LAUNCHED();
+  if (nseg > 1) {
+    prep_finish_kernel<<<(unsigned)ps_ceil_div(nrows, 128), 128, 0, s>>>(psum, pcnt, nseg, nrows, f0, m->d_count,
+                                                                         m->d_center);
+    PS_LAUNCHED();
+    ps_free(psum, s);
+    ps_free(pcnt, s);
+  }
   return PS_OK;
 }
 
