@@ -644,7 +644,7 @@ __global__ void bh_scatter_pos_kernel(const double* __restrict__ ranked, const d
 constexpr int kChunk = 2048, kChunkThreads = 1024;
 __global__ void __launch_bounds__(kChunkThreads)
 bh_chunk_sort_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ count,
-                     uint64_t* __restrict__ skeys, uint32_t* __restrict__ crank) {
+                     uint64_t* __restrict__ skeys, uint32_t* __restrict__ crank, uint32_t* __restrict__ spos) {
   __shared__ uint64_t sk[kChunk];
   __shared__ uint16_t si[kChunk];
   const int m = (int)*count;
@@ -676,7 +676,142 @@ bh_chunk_sort_kernel(const uint64_t* __restrict__ keys, const unsigned long long
   }
   for (int t = threadIdx.x; t < kChunk; t += kChunkThreads) {
     skeys[c0 + t] = sk[t];
-    if (c0 + si[t] < m) crank[c0 + si[t]] = (uint32_t)t;
+    if (spos) spos[c0 + t] = (uint32_t)(c0 + si[t]);  // (padding: positions >= m, never read)
+    else if (c0 + si[t] < m) crank[c0 + si[t]] = (uint32_t)t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Medium families (BH, kSmallMax < m <= kMergeMax): the 2048-key sorted
+// chunks are merged pairwise, level by level -- each member's place in the
+// merged run is its place in its own run plus a binary search of the partner
+// run (keys < k in the later run, <= k in the earlier one: stable) -- then a
+// blocked suffix minimum over the sorted family.  Every launch reads m on the
+// device (no host round trip), against the 4-pass radix's ~16 launches and a
+// host synchronisation.
+constexpr int64_t kMergeMax = (int64_t)1 << 20;
+__global__ void bh_merge_level_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ pin,
+                                      uint64_t* __restrict__ kout, uint32_t* __restrict__ pout,
+                                      const unsigned long long* __restrict__ count, int64_t L) {
+  const int64_t m = (int64_t)*count;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t run = i / L, p = i - run * L;
+  const int64_t pb = (run ^ 1) * L;
+  const uint64_t k = kin[i];
+  int64_t c = 0;
+  if (pb < m) {
+    const uint64_t* b = kin + pb;
+    int64_t lo = 0, hi = min(L, m - pb);
+    if (run & 1) {  // partner run is earlier: its keys <= k come first
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (b[mid] <= k) lo = mid + 1;
+        else hi = mid;
+      }
+    } else {  // partner run is later: its keys < k come first
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (b[mid] < k) lo = mid + 1;
+        else hi = mid;
+      }
+    }
+    c = lo;
+  }
+  const int64_t o = (run & ~(int64_t)1) * L + p + c;
+  kout[o] = k;
+  pout[o] = pin[i];
+}
+
+// v_r = p_(r) m / (r + 1) over 1024-rank blocks: in-block inclusive suffix
+// minimum, and the block minimum
+__global__ void __launch_bounds__(1024)
+bh_sorted_scale_kernel(const uint64_t* __restrict__ sk, const unsigned long long* __restrict__ count,
+                       double* __restrict__ ranked, double* __restrict__ bmin) {
+  __shared__ double s_w[32];
+  __shared__ double s_after[32];
+  const int64_t m = (int64_t)*count;
+  const int64_t r = blockIdx.x * 1024LL + threadIdx.x;
+  if (blockIdx.x * 1024LL >= m) return;  // block-uniform
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v = r < m ? val_of(sk[r]) * ((double)m / (double)(r + 1)) : CUDART_INF;
+#pragma unroll
+  for (int sft = 1; sft < 32; sft <<= 1) {
+    const double y = __shfl_down_sync(PS_FULL, v, sft);
+    if (lane + sft < 32) v = fmin(v, y);
+  }
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double w = s_w[lane];
+#pragma unroll
+    for (int sft = 1; sft < 32; sft <<= 1) {
+      const double y = __shfl_down_sync(PS_FULL, w, sft);
+      if (lane + sft < 32) w = fmin(w, y);
+    }
+    const double after = __shfl_down_sync(PS_FULL, w, 1);
+    s_after[lane] = lane == 31 ? CUDART_INF : after;
+    if (lane == 0) bmin[blockIdx.x] = w;
+  }
+  __syncthreads();
+  if (r < m) ranked[r] = fmin(v, s_after[warp]);
+}
+
+// exclusive suffix minimum of the block minima (one CTA), in place: bmin[b]
+// becomes the minimum over the blocks after b
+__global__ void __launch_bounds__(1024)
+bh_block_suffix_kernel(double* __restrict__ bmin, const unsigned long long* __restrict__ count) {
+  __shared__ double s_w[32];
+  __shared__ double s_after[32];
+  const int64_t nb = ((int64_t)*count + 1023) / 1024;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (nb + 1023) / 1024;
+  const int64_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+  double tmin = CUDART_INF;
+  for (int64_t b = b0; b < b1; ++b) tmin = fmin(tmin, bmin[b]);
+  double incl = tmin;
+#pragma unroll
+  for (int sft = 1; sft < 32; sft <<= 1) {
+    const double y = __shfl_down_sync(PS_FULL, incl, sft);
+    if (lane + sft < 32) incl = fmin(incl, y);
+  }
+  if (lane == 0) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    double w = s_w[lane];
+#pragma unroll
+    for (int sft = 1; sft < 32; sft <<= 1) {
+      const double y = __shfl_down_sync(PS_FULL, w, sft);
+      if (lane + sft < 32) w = fmin(w, y);
+    }
+    const double after = __shfl_down_sync(PS_FULL, w, 1);
+    s_after[lane] = lane == 31 ? CUDART_INF : after;
+  }
+  __syncthreads();
+  double run = __shfl_down_sync(PS_FULL, incl, 1);
+  if (lane == 31) run = CUDART_INF;
+  run = fmin(run, s_after[warp]);
+  __syncthreads();  // every thread has read its inputs before the in-place writes
+  for (int64_t b = b1 - 1; b >= b0; --b) {
+    const double v = bmin[b];
+    bmin[b] = run;
+    run = fmin(run, v);
+  }
+}
+
+__global__ void bh_sorted_scatter_kernel(const double* __restrict__ ranked, const double* __restrict__ after,
+                                         const uint32_t* __restrict__ spos, const uint32_t* __restrict__ fidx,
+                                         const unsigned long long* __restrict__ count, int64_t cols, int symmetric,
+                                         double* __restrict__ out) {
+  const int64_t m = (int64_t)*count;
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const double v = fmin(1.0, fmin(ranked[r], after[r / 1024]));
+  const int64_t f = fidx[spos[r]];
+  out[f] = v;
+  if (symmetric) {
+    const int64_t rr = f / cols, cc = f - rr * cols;
+    out[cc * cols + rr] = v;
   }
 }
 
@@ -1134,7 +1269,7 @@ int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     PS_CUDA(ps_alloc(&crank, (size_t)(nch * kChunk), s));
     PS_CUDA(ps_alloc(&sidx, (size_t)(nch * kChunk), s));
     PS_CUDA(ps_alloc(&sval, (size_t)(nch * kChunk), s));
-    bh_chunk_sort_kernel<<<(unsigned)nch, kChunkThreads, 0, s>>>(keys, d_count, skeys, crank);
+    bh_chunk_sort_kernel<<<(unsigned)nch, kChunkThreads, 0, s>>>(keys, d_count, skeys, crank, nullptr);
     PS_LAUNCHED();
     const size_t smem = (size_t)nch * kChunk * sizeof(uint64_t);
     PS_CUDA(cudaFuncSetAttribute(bh_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1147,6 +1282,41 @@ int adjust_core(uint64_t* keys, uint32_t* idx, unsigned long long* d_count, int6
     ps_free(crank, s);
     ps_free(sidx, s);
     ps_free(sval, s);
+    return PS_OK;
+  }
+  if (method == PS_ADJ_BH && fam_max > kSmallMax && fam_max <= kMergeMax && !getenv("PS_ADJUST_RADIX")) {
+    const int64_t nch = ps_ceil_div(fam_max, kChunk);
+    const int64_t npad = nch * kChunk;
+    uint64_t *kb[2] = {nullptr, nullptr};
+    uint32_t *pb[2] = {nullptr, nullptr};
+    double *ranked = nullptr, *bmin = nullptr;
+    for (int b = 0; b < 2; ++b) {
+      PS_CUDA(ps_alloc(&kb[b], (size_t)npad, s));
+      PS_CUDA(ps_alloc(&pb[b], (size_t)npad, s));
+    }
+    PS_CUDA(ps_alloc(&ranked, (size_t)npad, s));
+    PS_CUDA(ps_alloc(&bmin, (size_t)ps_ceil_div(npad, 1024), s));
+    bh_chunk_sort_kernel<<<(unsigned)nch, kChunkThreads, 0, s>>>(keys, d_count, kb[0], nullptr, pb[0]);
+    PS_LAUNCHED();
+    int cur = 0;
+    const unsigned g256 = (unsigned)ps_ceil_div(fam_max, 256);
+    for (int64_t L = kChunk; L < fam_max; L <<= 1) {
+      bh_merge_level_kernel<<<g256, 256, 0, s>>>(kb[cur], pb[cur], kb[cur ^ 1], pb[cur ^ 1], d_count, L);
+      PS_LAUNCHED();
+      cur ^= 1;
+    }
+    bh_sorted_scale_kernel<<<(unsigned)ps_ceil_div(fam_max, 1024), 1024, 0, s>>>(kb[cur], d_count, ranked, bmin);
+    PS_LAUNCHED();
+    bh_block_suffix_kernel<<<1, 1024, 0, s>>>(bmin, d_count);
+    PS_LAUNCHED();
+    bh_sorted_scatter_kernel<<<g256, 256, 0, s>>>(ranked, bmin, pb[cur], idx, d_count, cols, symmetric, out);
+    PS_LAUNCHED();
+    for (int b = 0; b < 2; ++b) {
+      ps_free(kb[b], s);
+      ps_free(pb[b], s);
+    }
+    ps_free(ranked, s);
+    ps_free(bmin, s);
     return PS_OK;
   }
   if (method == PS_ADJ_BH && fam_max <= kSmallMax) {  // PS_ADJUST_SMALL_CTA: the single-CTA radix sort (A/B)

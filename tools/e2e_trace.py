@@ -9,14 +9,11 @@ import bench  # noqa: E402
 import workloads  # noqa: E402
 import paper_2505_00448_b200 as ps  # noqa: E402
 
-cfg = workloads.config(bench.parse_config(sys.argv[1]))
-test = sys.argv[2] if len(sys.argv) > 2 else cfg["tests"][0]
-a, b, ka, kb = bench.build_inputs(cfg, test)
-outputs = bench.OUTPUTS[bench.parse_config(sys.argv[1])]
-if cfg.get("config") == 4 or sys.argv[1] == "4":
-    outputs = ("stat", "p", "p_bh")
-mat_a = ps.make_matrix(a, ka, na_sentinel=workloads.SENTINEL)
-mat_b = ps.make_matrix(b, kb, na_sentinel=workloads.SENTINEL) if b is not None else None
+key = bench.parse_config(sys.argv[1])
+test = sys.argv[2] if len(sys.argv) > 2 else bench.default_test(key)
+wl = bench.Workload(key, test, 0, 1)
+mat_a, mat_b = wl.datamatrices()
+outputs = wl.outputs
 req = ps.TestRequest(test, outputs)
 reps = int(os.environ.get("REPS", "3"))
 times = []
