@@ -532,6 +532,9 @@ int ps_matrix_destroy(ps_matrix* m) {
   ps_free(m->d_order32, s);
   ps_free(m->d_lastb32, s);
   ps_free(m->d_nextb32, s);
+  ps_free(m->d_gp, s);
+  ps_free(m->d_bpos, s);
+  ps_free(m->d_ngrp, s);
   if (m->owns_presort) {
     ps_free(m->d_order, s);
     ps_free(m->d_inv, s);

@@ -46,6 +46,12 @@ struct ps_matrix {
   uint16_t* d_lastb = nullptr;    // F x ldt: prefix-max boundary position per word
   uint16_t* d_nextb = nullptr;    // F x ldt: suffix-min boundary position per word
   uint8_t* d_tied = nullptr;      // F: 1 if the feature has a tie group of size > 1
+  // tie-group index of the 16-bit tables (always library-owned): per word the
+  // number of group starts before it, the start position of every group
+  // (group D = the end sentinel n) and the group count D
+  uint16_t* d_gp = nullptr;       // F x ldt
+  uint16_t* d_bpos = nullptr;     // F x ldo
+  int32_t* d_ngrp = nullptr;      // F
   // S > 65535 ("wide"): 32-bit orders and tie prefix tables instead of the
   // 16-bit ones (no inverse permutation); walked by the wide rank kernels
   bool wide = false;
@@ -61,6 +67,9 @@ struct ps_matrix {
 
 // true when the matrix carries presort chunk marks some of which are still
 // pending on the device (the walks can then overlap the presort)
+// tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits
+int ps_tie_index(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
+
 bool ps_presort_pending(const ps_matrix* m);
 
 // Per-device library state.

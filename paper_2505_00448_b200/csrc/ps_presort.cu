@@ -548,6 +548,61 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
   }
 }
 
+// Tie-group index of one feature (16-bit tables): gp[w] = number of group
+// starts at positions < 32 w, bpos[k] = start of group k (k < D), bpos[D] = n,
+// ngrp = D.  Derived from the boundary bits alone (bit n is the end sentinel),
+// so it is identical for owned and caller-owned (gathered) tables.
+__global__ void tie_index_kernel(const uint32_t* __restrict__ tb, int64_t ldt, const int32_t* __restrict__ lens,
+                                 uint16_t* __restrict__ gp, uint16_t* __restrict__ bpos, int64_t ldo,
+                                 int32_t* __restrict__ ngrp, int64_t f0) {
+  const int64_t f = f0 + blockIdx.x;
+  const int n = lens[f];
+  const int nw = (n + 31) >> 5;  // words holding positions < n
+  const uint32_t* t = tb + f * ldt;
+  uint16_t* g = gp + f * ldt;
+  uint16_t* bp = bpos + f * ldo;
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int w0 = 0; w0 < nw; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    uint32_t T = 0u;
+    if (w < nw) {
+      T = t[w];
+      const int rem = n - 32 * w;  // positions of this word below n
+      if (rem < 32) T &= (1u << rem) - 1u;
+    }
+    const int c = __popc(T);
+    int x = c;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(PS_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    int before = carry;
+    for (int i = 0; i < warp; ++i) before += wsum[i];
+    int tot = carry;
+    for (int i = 0; i < nwarp; ++i) tot += wsum[i];
+    const int ex = before + x - c;
+    if (w < nw) {
+      g[w] = (uint16_t)ex;
+      int k = ex;
+      for (uint32_t m = T; m; m &= m - 1u) bp[k++] = (uint16_t)(32 * w + __ffs(m) - 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry = tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bp[carry] = (uint16_t)n;
+    ngrp[f] = carry;
+  }
+}
+
 }  // namespace
 
 // Presort in three steps so the per-feature sorts can follow the input
@@ -569,6 +624,9 @@ int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
   }
   PS_CUDA(ps_alloc(&m->d_order, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_inv, (size_t)(m->F * m->ldo), s));
+  PS_CUDA(ps_alloc(&m->d_gp, (size_t)(m->F * m->ldt), s));
+  PS_CUDA(ps_alloc(&m->d_bpos, (size_t)(m->F * m->ldo), s));
+  PS_CUDA(ps_alloc(&m->d_ngrp, (size_t)m->F, s));
   PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_lastb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
@@ -593,6 +651,9 @@ int ps_presort_attach(ps_matrix* m, uint16_t* order, uint16_t* inv, uint32_t* tb
   m->d_tied = tied;
   m->d_len = len;
   m->owns_presort = false;
+  PS_CUDA(ps_alloc(&m->d_gp, (size_t)(m->F * m->ldt), s));
+  PS_CUDA(ps_alloc(&m->d_bpos, (size_t)(m->F * m->ldo), s));
+  PS_CUDA(ps_alloc(&m->d_ngrp, (size_t)m->F, s));
   return presort_scratch(m, s);
 }
 
@@ -634,21 +695,40 @@ int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
     PS_LAUNCHED();
     return PS_OK;
   }
-  if (items <= 4) return smem_path(presort_smem_kernel<4>, 4);
-  if (items <= 8) return smem_path(presort_smem_kernel<8>, 8);
-  if (items <= 12) return smem_path(presort_smem_kernel<12>, 12);
-  if (items <= 16) return smem_path(presort_smem_kernel<16>, 16);
-  if (items <= 20) return smem_path(presort_smem_kernel<20>, 20);
-  presort_kernel<uint16_t><<<(unsigned)nf, NT, 0, s>>>(
-      m->d_vals, m->ld, m->d_mask, m->W, m->S, static_cast<uint64_t*>(m->presort_scratch[0]),
-      static_cast<uint32_t*>(m->presort_scratch[2]), static_cast<uint64_t*>(m->presort_scratch[1]),
-      static_cast<uint32_t*>(m->presort_scratch[3]), m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
-      m->d_nextb, m->ldt, m->d_tied, m->d_len, f0);
+  int rc;
+  if (items <= 4) rc = smem_path(presort_smem_kernel<4>, 4);
+  else if (items <= 8) rc = smem_path(presort_smem_kernel<8>, 8);
+  else if (items <= 12) rc = smem_path(presort_smem_kernel<12>, 12);
+  else if (items <= 16) rc = smem_path(presort_smem_kernel<16>, 16);
+  else if (items <= 20) rc = smem_path(presort_smem_kernel<20>, 20);
+  else {
+    presort_kernel<uint16_t><<<(unsigned)nf, NT, 0, s>>>(
+        m->d_vals, m->ld, m->d_mask, m->W, m->S, static_cast<uint64_t*>(m->presort_scratch[0]),
+        static_cast<uint32_t*>(m->presort_scratch[2]), static_cast<uint64_t*>(m->presort_scratch[1]),
+        static_cast<uint32_t*>(m->presort_scratch[3]), m->d_order, m->d_inv, m->ldo, m->d_tb, m->d_lastb,
+        m->d_nextb, m->ldt, m->d_tied, m->d_len, f0);
+    PS_LAUNCHED();
+    rc = PS_OK;
+  }
+  // caller-owned tables hold other ranks' rows only after the gather: their
+  // index is built by ps_presort_end over all rows
+  if (!rc && m->owns_presort) rc = ps_tie_index(m, f0, f1, s);
+  return rc;
+}
+
+int ps_tie_index(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
+  if (f1 <= f0 || !m->d_gp) return PS_OK;
+  tie_index_kernel<<<(unsigned)(f1 - f0), 256, 0, s>>>(m->d_tb, m->ldt, m->d_len, m->d_gp, m->d_bpos, m->ldo,
+                                                      m->d_ngrp, f0);
   PS_LAUNCHED();
   return PS_OK;
 }
 
 int ps_presort_end(ps_matrix* m, cudaStream_t s) {
+  if (!m->owns_presort && !m->wide) {
+    const int rc = ps_tie_index(m, 0, m->F, s);
+    if (rc) return rc;
+  }
   for (void*& p : m->presort_scratch) {
     ps_free(p, s);
     p = nullptr;

@@ -43,6 +43,10 @@ namespace {
 #endif
 constexpr int SW = PS_SW;          // warps per CTA
 constexpr int STH = SW * 32;
+// tie-free g, one-sweep pass A: R[q] = warp << kEncShift | local rank (>= 1)
+constexpr int kEncShift = SW <= 16 ? 12 : 11;
+constexpr uint32_t kEncMask = (1u << kEncShift) - 1u;
+static_assert(SW <= (1 << (16 - kEncShift)), "warp index must fit the R encoding");
 
 // Exact per-pair sums of the rows [row0, row0 + rows) of the current chunk
 // (rows x F, only g <= h written): scratch bounded by the chunk, not F^2.
@@ -201,22 +205,44 @@ __device__ __forceinline__ unsigned long long sq_closed(unsigned long long n) {
 }
 
 // Shared-memory layout, in 32-bit words (all regions 16-byte aligned).
+//
+// Group-table mode (a tied feature with at most `cap` tie groups): instead of
+// resolving each position's tie group per pair (word records + word_r2), the
+// pair's kept prefix is evaluated once per GROUP START (tab[k] = Pfx(bpos[k]),
+// k <= D) and a kept position p of group k = gid(p) gets 2r = tab[k] +
+// tab[k + 1] + 1, gid(p) = gp[p / 32] + popc(boundary bits <= p) - 1.  The
+// h-side regions hold either the fallback tables (lastb | nextb) or
+// (gp | group starts | tab [| g's group starts when g is streamed]); g's
+// double-buffered regions hold (lastb | nextb) or (gp | group starts).
 struct WalkLayout {
   uint32_t inv16, R16, tbh, lbh16, nbh16, par, K, Pl, SE;
+  uint32_t gph16, bposh16, tab16, bposg16s;  // h side (aliases lbh16 / nbh16) + streamed g's group starts
   uint32_t og16[2], tbg[2], lbg16[2], nbg16[2];
+  uint32_t gpg16[2], bposg16[2];              // alias lbg16 / nbg16
   uint32_t words;
-  __host__ __device__ WalkLayout(int64_t ldo, int64_t ldt, bool ogs, bool r2) {
+  __host__ __device__ static int64_t capr(int cap) { return ((int64_t)cap + 2 + 7) & ~int64_t(7); }  // entries
+  __host__ __device__ WalkLayout(int64_t ldo, int64_t ldt, bool ogs, bool r2, int cap) {
     uint32_t w = 0;
     auto take = [&](int64_t bytes) {
       const uint32_t o = w;
       w += (uint32_t)(((bytes + 15) / 16) * 4);
       return o;
     };
+    const int64_t ldt2 = ((ldt * 2 + 15) / 16) * 16;  // bytes of one 16-bit per-word table
+    const int64_t cr = capr(cap);
     inv16 = take(ldo * 2) * 2;
     R16 = take(ldo * 2) * 2;
     tbh = take(ldt * 4);
-    lbh16 = take(ldt * 2) * 2;
-    nbh16 = take(ldt * 2) * 2;
+    {
+      const int64_t tab_bytes = cap > 0 ? ldt2 + 2 * cr * (ogs ? 2 : 3) : 0;
+      const uint32_t u = take(std::max<int64_t>(2 * ldt2, tab_bytes));
+      lbh16 = u * 2;
+      nbh16 = lbh16 + (uint32_t)(ldt2 / 2);
+      gph16 = lbh16;
+      bposh16 = nbh16;
+      tab16 = bposh16 + (uint32_t)cr;
+      bposg16s = tab16 + (uint32_t)cr;
+    }
     par = r2 ? 0 : take(ldt * 4);
     // per word of the walked order: kept bits K, segment-relative prefix P and
     // (R2 tied passes) the prefixes of the tie groups entering / leaving it;
@@ -228,8 +254,12 @@ struct WalkLayout {
     for (int b = 0; b < 2; ++b) {
       og16[b] = ogs ? take(ldo * 2) * 2 : 0;
       tbg[b] = ogs ? take(ldt * 4) : 0;
-      lbg16[b] = ogs ? take(ldt * 2) * 2 : 0;
-      nbg16[b] = ogs ? take(ldt * 2) * 2 : 0;
+      const int64_t tb = cap > 0 ? ldt2 + 2 * cr : 0;
+      const uint32_t v = ogs ? take(std::max<int64_t>(2 * ldt2, tb)) * 2 : 0;
+      lbg16[b] = v;
+      nbg16[b] = v + (uint32_t)(ldt2 / 2);
+      gpg16[b] = lbg16[b];
+      bposg16[b] = nbg16[b];
     }
     words = w;
   }
@@ -336,13 +366,14 @@ __device__ __forceinline__ void walk_order(const uint16_t* __restrict__ og, uint
 }
 
 template <bool OGS, bool R2>
-__global__ void __launch_bounds__(STH, OGS ? 32 / SW : 16 / SW)
+__global__ void __launch_bounds__(STH, OGS ? (SW <= 16 ? 32 / SW : 1) : (SW <= 16 ? 16 / SW : 1))
 spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restrict__ inv, int64_t ldo,
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
-                     const int32_t* __restrict__ lens, int64_t F, const int4* __restrict__ items, int n_items,
-                     int once, int* __restrict__ queue, PairParts out) {
-  const WalkLayout L(ldo, ldt, OGS, R2);
+                     const int32_t* __restrict__ lens, const uint16_t* __restrict__ gpt,
+                     const uint16_t* __restrict__ bpos, const int32_t* __restrict__ ngrp, int cap, int64_t F,
+                     const int4* __restrict__ items, int n_items, int once, int* __restrict__ queue, PairParts out) {
+  const WalkLayout L(ldo, ldt, OGS, R2, cap);
   __shared__ uint32_t wtot[SW], wtotA[SW];
   __shared__ int s_item;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -404,6 +435,10 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
   if (!R2)
     for (int64_t i = threadIdx.x; i < ldt; i += STH) sm32[L.par + i] = 0u;
 
+  // group-table mode of g: tied, few enough groups, and the h-side regions
+  // not holding h's fallback tables (gtab_ok, per item)
+  bool gtab_ok = false;
+  auto gtab_of = [&](int64_t g) -> bool { return gtab_ok && tied[g] && ngrp[g] <= cap; };
   auto prefetch = [&](int64_t g, int b) {
     const int ng = lens[g];
     const int nch = ((ng + 31) >> 5) * 4;  // whole 32-position words (sentinel padded)
@@ -413,15 +448,55 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
     if (tied[g]) {
       const int tch4 = (int)(ldt * 4 / 16), tch2 = (int)(ldt * 2 / 16);
       const unsigned char* t4 = reinterpret_cast<const unsigned char*>(tb + g * ldt);
-      const unsigned char* l2 = reinterpret_cast<const unsigned char*>(lastb + g * ldt);
-      const unsigned char* n2 = reinterpret_cast<const unsigned char*>(nextb + g * ldt);
       for (int c = threadIdx.x; c < tch4; c += STH) cp16(sb + L.tbg[b] * 4 + c * 16, t4 + c * 16);
-      for (int c = threadIdx.x; c < tch2; c += STH) {
-        cp16(sb + L.lbg16[b] * 2 + c * 16, l2 + c * 16);
-        cp16(sb + L.nbg16[b] * 2 + c * 16, n2 + c * 16);
+      if (gtab_of(g)) {
+        const unsigned char* g2 = reinterpret_cast<const unsigned char*>(gpt + g * ldt);
+        const unsigned char* b2 = reinterpret_cast<const unsigned char*>(bpos + g * ldo);
+        const int bch = (ngrp[g] + 1 + 7) >> 3;
+        for (int c = threadIdx.x; c < tch2; c += STH) cp16(sb + L.gpg16[b] * 2 + c * 16, g2 + c * 16);
+        for (int c = threadIdx.x; c < bch; c += STH) cp16(sb + L.bposg16[b] * 2 + c * 16, b2 + c * 16);
+      } else {
+        const unsigned char* l2 = reinterpret_cast<const unsigned char*>(lastb + g * ldt);
+        const unsigned char* n2 = reinterpret_cast<const unsigned char*>(nextb + g * ldt);
+        for (int c = threadIdx.x; c < tch2; c += STH) {
+          cp16(sb + L.lbg16[b] * 2 + c * 16, l2 + c * 16);
+          cp16(sb + L.nbg16[b] * 2 + c * 16, n2 + c * 16);
+        }
       }
     }
     asm volatile("cp.async.commit_group;");
+  };
+
+  // Group table of the walked feature (D groups, starts at shared byte address
+  // aB, length nf): tab[k] = Pfx(start of group k), k <= D, from the pair's
+  // segment-relative word prefixes (segment of word w: w / Lseg, base: lane
+  // of segpre).  Returns this thread's share of sum_k c_k (2 r_k)^2.
+  const uint32_t aTab = sb + 2 * L.tab16;
+  auto build_tab = [&](int D, uint32_t aB, int Lseg, uint32_t segpre, uint32_t tot,
+                       uint32_t nf) -> unsigned long long {
+    // ceil(2^32 / Lseg): floor(w / Lseg) = umulhi(w, magic) exactly for w < 2^16 (Lseg = 1 overflows: direct)
+    const uint32_t magic = (uint32_t)((0x100000000ull + (uint32_t)Lseg - 1u) / (uint32_t)Lseg);
+    for (int kb = warp * 32; kb <= D; kb += STH) {  // warp-uniform
+      const int k = kb + lane;
+      const uint32_t x = k <= D ? ld16(aB + 2 * (uint32_t)k) : nf;
+      const uint32_t wx = min(x, nf - 1u) >> 5;
+      const uint32_t base = __shfl_sync(PS_FULL, segpre, Lseg == 1 ? (int)wx : (int)__umulhi(wx, magic));
+      const uint32_t v = ldP(wx) + base + __popc(ld32(kA(wx)) & ((1u << (x & 31u)) - 1u));
+      if (k <= D) st16(aTab + 2 * (uint32_t)k, x >= nf ? tot : v);
+    }
+    __syncthreads();
+    unsigned long long acc = 0;
+    for (int k = threadIdx.x; k < D; k += STH) {
+      const uint32_t a = ld16(aTab + 2 * (uint32_t)k), b = ld16(aTab + 2 * (uint32_t)k + 2u);
+      const unsigned long long r2 = a + b + 1u;
+      acc += (unsigned long long)(b - a) * r2 * r2;
+    }
+    return acc;
+  };
+  // doubled rank of every lane of a word of a group-table feature
+  auto tab_r2 = [&](uint32_t T, uint32_t gw) -> uint32_t {
+    const uint32_t gid = gw + __popc(T & (0xFFFFFFFFu >> (31 - lane))) - 1u;
+    return ld16(aTab + 2 * gid) + ld16(aTab + 2 * gid + 2u) + 1u;
   };
 
   __shared__ int4 s_it;
@@ -438,11 +513,20 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
     const int64_t lo = it.y;  // g block [lo, gmax]
     const int nh = lens[h];
     const bool th = tied[h] != 0;
+    const int Dh = th ? ngrp[h] : 0;
+    const bool htab = th && Dh <= cap;
+    gtab_ok = !th || htab;
     {
       const uint4* src = reinterpret_cast<const uint4*>(inv + h * ldo);
       uint4* dst = reinterpret_cast<uint4*>(&SM16[L.inv16]);
       for (int64_t i = threadIdx.x; i < ldo / 8; i += STH) dst[i] = src[i];
-      if (th) {
+      if (htab) {
+        for (int64_t i = threadIdx.x; i < ldt; i += STH) {
+          sm32[L.tbh + i] = tb[h * ldt + i];
+          SM16[L.gph16 + i] = gpt[h * ldt + i];
+        }
+        for (int i = threadIdx.x; i <= Dh; i += STH) SM16[L.bposh16 + i] = bpos[h * ldo + i];
+      } else if (th) {
         for (int64_t i = threadIdx.x; i < ldt; i += STH) {
           sm32[L.tbh + i] = tb[h * ldt + i];
           SM16[L.lbh16 + i] = lastb[h * ldt + i];
@@ -461,13 +545,16 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
 #endif
     int ng_next = lo <= gmax ? lens[lo] : 0;
     bool tg_next = lo <= gmax ? tied[lo] != 0 : false;
+    int dg_next = lo <= gmax ? ngrp[lo] : 0;
     for (int64_t g = lo; g <= gmax; ++g) {
       const int buf = (int)((g - lo) & 1);
       const int ng = ng_next;
       const bool tg = tg_next;
+      const int Dg = dg_next;
       if (g + 1 <= gmax) {
         ng_next = lens[g + 1];
         tg_next = tied[g + 1] != 0;
+        dg_next = ngrp[g + 1];
       }
       if (OGS) {
         if (g + 1 <= gmax) prefetch(g + 1, buf ^ 1);
@@ -484,6 +571,13 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       const uint32_t aOg = sb + 2 * L.og16[buf];
       const uint32_t aTbg = sb + 4 * L.tbg[buf], aLbg = sb + 2 * L.lbg16[buf], aNbg = sb + 2 * L.nbg16[buf];
       const uint16_t* og_g = order + g * ldo;
+      const bool gtab = tg && gtab_ok && Dg <= cap;
+      const uint32_t aBg = OGS ? sb + 2 * L.bposg16[buf] : sb + 2 * L.bposg16s;
+      if (!OGS && gtab) {  // streamed g: its group starts by cp.async, waited for after phase 1
+        const unsigned char* b2 = reinterpret_cast<const unsigned char*>(bpos + g * ldo);
+        for (int c = threadIdx.x; c < ((Dg + 1 + 7) >> 3); c += STH) cp16(aBg + c * 16, b2 + c * 16);
+        asm volatile("cp.async.commit_group;");
+      }
       // ---------------- pass A, phase 1: keep bits over g's order ----------
       const int nwa = (ng + 31) >> 5;
       const int La = (nwa + SW - 1) / SW;
@@ -491,7 +585,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // Tie-free g: one sweep.  R[q] = (warp << 12) | local
       // rank within the warp's segment; the segment bases are folded in by
       // pass B, so no prefix phase is needed here.
-      const bool encA = !tg && La * 32 <= 4095;
+      const bool encA = !tg && La * 32 <= (int)kEncMask;
       // 2r fits 16 bits for this pair (always when S <= 32767; for larger S
       // whenever the joint count n <= 32767): no parity bits needed
       bool r2fit = R2;
@@ -502,7 +596,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         auto body = [&](int, uint32_t q) {
           const bool keep = q != 0xFFFFu;
           const uint32_t B = __ballot_sync(PS_FULL, keep);
-          if (keep) st16(aR + 2 * q, ((uint32_t)warp << 12) | (cnt + __popc(B & ltmask) + 1u));
+          if (keep) st16(aR + 2 * q, ((uint32_t)warp << kEncShift) | (cnt + __popc(B & ltmask) + 1u));
           cnt += __popc(B);
         };
         if (OGS) {  // (64-register kernels: the grouped walk costs more than it saves)
@@ -536,6 +630,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
         if (lane == 0) wtot[warp] = cnt;
       }
+      if (!OGS && gtab) asm volatile("cp.async.wait_group 0;");
       __syncthreads();
       WT(1);
       {
@@ -543,7 +638,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         segment_bases(wtot, segpre, n);
         r2fit = R2 || (2u * n + 1u <= 0xFFFFu);
         abase = __shfl_sync(PS_FULL, segpre, warp);
-        if (tg && R2) {
+        if (gtab) {
+          sa2 = build_tab(Dg, aBg, La, segpre, n, (uint32_t)ng);
+        } else if (tg && R2) {
           if (OGS)
             fill_spep(a0, a1, La, segpre, n, (uint32_t)ng, [&](int w) { return ld32(aTbg + 4 * w); },
                       [&](int w) { return ld16(aLbg + 2 * w); }, [&](int w) { return ld16(aNbg + 2 * w); });
@@ -563,7 +660,64 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       WT(2);
       // ---------------- pass A, phase 2: ranks -> R[q] -------------------
       auto q_at = [&](uint32_t p) -> uint32_t { return OGS ? ld16(aOg + 2 * p) : ld16(aInv + 2 * (uint32_t)og_g[p]); };
-      if (!tg) {
+      auto st_r2 = [&](uint32_t q, uint32_t r2) {
+        if (r2fit) {
+          st16(aR + 2 * q, r2);
+        } else {
+          st16(aR + 2 * q, r2 >> 1);
+          if (r2 & 1u) atomicOr(&sm32[L.par + (q >> 5)], 1u << (q & 31u));
+        }
+      };
+      if (gtab && OGS) {
+        const uint32_t aGpg = sb + 2 * L.gpg16[buf];
+#pragma unroll 4
+        for (int word = a0; word < a1; ++word) {
+          const uint32_t kw = ld32(kA(word));
+          const uint32_t r2 = tab_r2(ld32(aTbg + 4 * word), ld16(aGpg + 2 * word));
+          if ((kw >> lane) & 1u) st_r2(ld16(aOg + 2 * (uint32_t)(word * 32 + lane)), r2);
+        }
+      } else if (gtab) {
+        // streamed g: boundary bits and group counts of the warp's words in
+        // registers (lane j of slot i: word a0 + 32 i + j), g's order two
+        // 8-word groups ahead
+        const uint32_t* tbgg = tb + g * ldt;
+        const uint16_t* gpgg = gpt + g * ldt;
+        uint32_t rT[kRecSlots], rG[kRecSlots];
+#pragma unroll
+        for (int i = 0; i < kRecSlots; ++i) {
+          const int w = a0 + 32 * i + lane;
+          rT[i] = w < a1 ? tbgg[w] : 0u;
+          rG[i] = w < a1 ? (uint32_t)gpgg[w] : 0u;
+        }
+        auto og_at = [&](int word) -> uint32_t {
+          return word < a1 ? (uint32_t)og_g[(uint32_t)(word * 32 + lane)] : 0u;
+        };
+        uint32_t sc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sc[u] = og_at(a0 + u);
+        for (int w8 = a0; w8 < a1; w8 += 8) {
+          uint32_t sn[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sn[u] = og_at(w8 + 8 + u);
+          const int i = (w8 - a0) >> 5;
+          const uint32_t RT = pick_slot(rT, i), RG = pick_slot(rG, i);
+          uint32_t q[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[u] = ld16(aInv + 2 * sc[u]);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int word = w8 + u;
+            if (word < a1) {  // warp-uniform
+              const int jl = (word - a0) & 31;
+              const uint32_t kw = ld32(kA(word));
+              const uint32_t r2 = tab_r2(__shfl_sync(PS_FULL, RT, jl), __shfl_sync(PS_FULL, RG, jl));
+              if ((kw >> lane) & 1u) st_r2(q[u], r2);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sc[u] = sn[u];
+        }
+      } else if (!tg) {
 #pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
           const uint32_t kw = ld32(kA(word));
@@ -661,7 +815,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       WT(3);
       // decode R -> 2 r_g (all lanes must execute: shuffles)
       auto r2g_of = [&](uint32_t v, int word) -> uint32_t {
-        if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu));
+        if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask));
         if (r2fit) return v;
         return 2u * v + (tg ? ((ld32(aPar + 4 * word) >> lane) & 1u) : 0u);
       };
@@ -680,7 +834,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             const bool keep = v != 0u;
             const uint32_t B = __ballot_sync(PS_FULL, keep);
             uint32_t r2g;
-            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu)) << 1;
+            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask)) << 1;
             else r2g = r2g_of(v, word);
             if (keep) {
               sab += (unsigned long long)r2g * (cnt + __popc(B & ltmask) + 1u);
@@ -718,7 +872,9 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         uint32_t segpre, tot;
         segment_bases(wtot, segpre, tot);
         bbase = __shfl_sync(PS_FULL, segpre, warp);
-        if (th && R2) {
+        if (htab) {
+          sbb = build_tab(Dh, sb + 2 * L.bposh16, Lb, segpre, tot, (uint32_t)nh);
+        } else if (th && R2) {
           fill_spep(b0, b1, Lb, segpre, tot, (uint32_t)nh, [&](int w) { return ld32(aTbh + 4 * w); },
                     [&](int w) { return ld16(aLbh + 2 * w); }, [&](int w) { return ld16(aNbh + 2 * w); });
         } else if (th) {
@@ -731,7 +887,33 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         }
       }
       // ---------------- pass B, phase 2: accumulate, clear R ---------------
-      if (!th) {
+      if (htab) {
+        const uint32_t aGph = sb + 2 * L.gph16;
+        auto walkt = [&](auto enc) {
+#pragma unroll 4
+          for (int word = b0; word < b1; ++word) {
+            const uint32_t kw = ld32(kA(word));
+            const uint32_t q = (uint32_t)(word * 32 + lane);
+            const uint32_t v = ld16(aR + 2 * q);
+            uint32_t r2g;  // all lanes (shuffle)
+            if constexpr (decltype(enc)::value)
+              r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask)) << 1;
+            else
+              r2g = r2g_of(v, word);
+            const uint32_t r2h = tab_r2(ld32(aTbh + 4 * word), ld16(aGph + 2 * word));
+            if ((kw >> lane) & 1u) {
+              sab += (unsigned long long)r2g * r2h;
+              st16(aR + 2 * q, 0u);
+            }
+            if (!r2fit && tg) {
+              __syncwarp();
+              if (lane == 0) st32(aPar + 4 * word, 0u);
+            }
+          }
+        };
+        if (encA) walkt(std::true_type{});
+        else walkt(std::false_type{});
+      } else if (!th) {
 #pragma unroll(OGS ? 4 : 8)
         for (int word = b0; word < b1; ++word) {
           const uint32_t kw = ld32(kA(word));
@@ -758,7 +940,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             const uint32_t q = (uint32_t)(word * 32 + lane);
             const uint32_t v = ld16(aR + 2 * q);
             uint32_t r2g;  // all lanes (shuffle)
-            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> 12)) + (v & 0xFFFu)) << 1;
+            if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask)) << 1;
             else r2g = v;
             const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
             const uint32_t r2hk = (kw >> lane) & 1u ? r2h : 0u;
@@ -963,7 +1145,9 @@ __global__ void spearman_finish_kernel(PairSums in, int64_t F, int64_t lo, int64
   }
 }
 
-size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs, bool r2) { return (size_t)WalkLayout(ldo, ldt, ogs, r2).words * 4; }
+size_t walk_smem(int64_t ldo, int64_t ldt, bool ogs, bool r2, int cap) {
+  return (size_t)WalkLayout(ldo, ldt, ogs, r2, cap).words * 4;
+}
 
 // ---------------------------------------------------------------------------
 // Wide walk (sample counts beyond the shared-memory walk: S > ~50k with the
@@ -1072,6 +1256,7 @@ struct ps_spearman_job {
   int64_t lo = 0, hi = 0;
   WalkKernel kern = nullptr;
   size_t smem = 0;
+  int cap = 0;         // group-table capacity (0: tie-group records only)
   int grid_max = 1;
   int64_t gb = 32;     // g rows per work item of incremental launches
   int64_t rows = 0;    // g rows per partials chunk
@@ -1126,7 +1311,8 @@ static int walk_launch(ps_spearman_job* j, int64_t h0, int64_t h1, int64_t c0, i
   const int grid = once ? (int)n : (int)std::min<int64_t>(n, grid_max);
   ps_prof_begin("spearman_walk", s);
   j->kern<<<grid, STH, j->smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
-                                     a->d_tied, a->d_len, a->F, items, (int)n, once, q, pp);
+                                     a->d_tied, a->d_len, a->d_gp, a->d_bpos, a->d_ngrp, j->cap, a->F, items,
+                                     (int)n, once, q, pp);
   ps_prof_end(s);
   PS_LAUNCHED();
   return PS_OK;
@@ -1177,7 +1363,7 @@ bool ps_spearman_wide(int64_t S) {
   const int64_t ldo = ps_round_up(S + 1, 64), ldt = tie_words(S);
   const size_t limit = 227 * 1024 - 1024;
   const bool r2 = S <= 32767;
-  return walk_smem(ldo, ldt, false, r2) > limit && walk_smem(ldo, ldt, true, r2) > limit;
+  return walk_smem(ldo, ldt, false, r2, 0) > limit && walk_smem(ldo, ldt, true, r2, 0) > limit;
 }
 
 int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p, double* rho, cudaStream_t s,
@@ -1189,11 +1375,23 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double
   ps_device_state* ds = ps_state();
   const size_t limit = 227 * 1024 - 1024;
   const bool r2 = a->S <= 32767;  // 2r fits 16 bits: no parity bits
-  size_t smem = walk_smem(a->ldo, a->ldt, true, r2);
+  size_t smem = walk_smem(a->ldo, a->ldt, true, r2, 0);
   bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
   if (const char* e = getenv("PS_SPEARMAN_OGS")) ogs = smem <= limit && e[0] == '1';  // tuning override
-  if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2);
+  if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2, 0);
   if (smem > limit) return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
+  // group-table capacity: the largest that keeps the CTAs per SM of the
+  // table-less layout (two per SM when that fits in half the budget)
+  int cap = 0;
+  if (a->d_gp && !getenv("PS_SPEARMAN_NOTAB")) {
+    const size_t budget = smem <= limit / 2 ? limit / 2 : limit;
+    for (int c = 2040; c >= 64; c -= 8)
+      if (walk_smem(a->ldo, a->ldt, ogs, r2, c) <= budget) {
+        cap = c;
+        break;
+      }
+    if (cap) smem = walk_smem(a->ldo, a->ldt, ogs, r2, cap);
+  }
   ps_spearman_job* j = new ps_spearman_job();
   j->a = a;
   j->lo = lo;
@@ -1204,6 +1402,7 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double
   j->p = p;
   j->rho = rho;
   j->smem = smem;
+  j->cap = cap;
   j->kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
                 : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
   j->home = s;
