@@ -535,6 +535,7 @@ int ps_matrix_destroy(ps_matrix* m) {
   ps_free(m->d_gp, s);
   ps_free(m->d_bpos, s);
   ps_free(m->d_ngrp, s);
+  ps_free(m->d_ordgid, s);
   if (m->owns_presort) {
     ps_free(m->d_order, s);
     ps_free(m->d_inv, s);

@@ -52,6 +52,7 @@ struct ps_matrix {
   uint16_t* d_gp = nullptr;       // F x ldt
   uint16_t* d_bpos = nullptr;     // F x ldo
   int32_t* d_ngrp = nullptr;      // F
+  uint32_t* d_ordgid = nullptr;   // F x ldo: order | group id << 16 (only when the Spearman walk streams g)
   // S > 65535 ("wide"): 32-bit orders and tie prefix tables instead of the
   // 16-bit ones (no inverse permutation); walked by the wide rank kernels
   bool wide = false;
@@ -67,6 +68,8 @@ struct ps_matrix {
 
 // true when the matrix carries presort chunk marks some of which are still
 // pending on the device (the walks can then overlap the presort)
+// true when the Spearman walk streams g's order (large S): d_ordgid is built
+bool ps_spearman_streams_g(int64_t S);
 // tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits
 int ps_tie_index(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s);
 

@@ -554,7 +554,8 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
 // so it is identical for owned and caller-owned (gathered) tables.
 __global__ void tie_index_kernel(const uint32_t* __restrict__ tb, int64_t ldt, const int32_t* __restrict__ lens,
                                  uint16_t* __restrict__ gp, uint16_t* __restrict__ bpos, int64_t ldo,
-                                 int32_t* __restrict__ ngrp, int64_t f0) {
+                                 int32_t* __restrict__ ngrp, const uint16_t* __restrict__ order,
+                                 uint32_t* __restrict__ ordgid, int64_t f0) {
   const int64_t f = f0 + blockIdx.x;
   const int n = lens[f];
   const int nw = (n + 31) >> 5;  // words holding positions < n
@@ -601,6 +602,17 @@ __global__ void tie_index_kernel(const uint32_t* __restrict__ tb, int64_t ldt, c
     bp[carry] = (uint16_t)n;
     ngrp[f] = carry;
   }
+  if (ordgid) {  // whole words: positions past n keep their sentinel id (group id unused)
+    __syncthreads();
+    const uint16_t* o = order + f * ldo;
+    uint32_t* og = ordgid + f * ldo;
+    for (int p = threadIdx.x; p < nw * 32; p += blockDim.x) {
+      const int w = p >> 5;
+      const uint32_t T = t[w] & (0xFFFFFFFFu >> (31 - (p & 31)));
+      const uint32_t gid = (uint32_t)g[w] + __popc(T) - 1u;
+      og[p] = (uint32_t)o[p] | (gid << 16);
+    }
+  }
 }
 
 }  // namespace
@@ -627,6 +639,7 @@ int ps_presort_begin(ps_matrix* m, cudaStream_t s) {
   PS_CUDA(ps_alloc(&m->d_gp, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_bpos, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_ngrp, (size_t)m->F, s));
+  if (ps_spearman_streams_g(m->S)) PS_CUDA(ps_alloc(&m->d_ordgid, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_tb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_lastb, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_nextb, (size_t)(m->F * m->ldt), s));
@@ -654,6 +667,7 @@ int ps_presort_attach(ps_matrix* m, uint16_t* order, uint16_t* inv, uint32_t* tb
   PS_CUDA(ps_alloc(&m->d_gp, (size_t)(m->F * m->ldt), s));
   PS_CUDA(ps_alloc(&m->d_bpos, (size_t)(m->F * m->ldo), s));
   PS_CUDA(ps_alloc(&m->d_ngrp, (size_t)m->F, s));
+  if (ps_spearman_streams_g(m->S)) PS_CUDA(ps_alloc(&m->d_ordgid, (size_t)(m->F * m->ldo), s));
   return presort_scratch(m, s);
 }
 
@@ -719,7 +733,7 @@ int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
 int ps_tie_index(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
   if (f1 <= f0 || !m->d_gp) return PS_OK;
   tie_index_kernel<<<(unsigned)(f1 - f0), 256, 0, s>>>(m->d_tb, m->ldt, m->d_len, m->d_gp, m->d_bpos, m->ldo,
-                                                      m->d_ngrp, f0);
+                                                      m->d_ngrp, m->d_order, m->d_ordgid, f0);
   PS_LAUNCHED();
   return PS_OK;
 }

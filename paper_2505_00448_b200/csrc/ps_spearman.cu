@@ -217,6 +217,7 @@ __device__ __forceinline__ unsigned long long sq_closed(unsigned long long n) {
 struct WalkLayout {
   uint32_t inv16, R16, tbh, lbh16, nbh16, par, K, Pl, SE;
   uint32_t gph16, bposh16, tab16, bposg16s;  // h side (aliases lbh16 / nbh16) + streamed g's group starts
+  uint32_t tabg32;                            // g's packed group table (R2: own region; else aliases par)
   uint32_t og16[2], tbg[2], lbg16[2], nbg16[2];
   uint32_t gpg16[2], bposg16[2];              // alias lbg16 / nbg16
   uint32_t words;
@@ -243,7 +244,8 @@ struct WalkLayout {
       tab16 = bposh16 + (uint32_t)cr;
       bposg16s = tab16 + (uint32_t)cr;
     }
-    par = r2 ? 0 : take(ldt * 4);
+    par = r2 ? 0 : take(std::max<int64_t>(ldt * 4, cap > 0 ? 4 * cr : 0));
+    tabg32 = r2 ? (cap > 0 ? take(4 * cr) : 0) : par;
     // per word of the walked order: kept bits K, segment-relative prefix P and
     // (R2 tied passes) the prefixes of the tie groups entering / leaving it;
     // for R2 one 16-byte record {K, P, sp, ep} per word (one LDS.128), else
@@ -324,44 +326,82 @@ __device__ __forceinline__ uint32_t ldg16_early(const uint16_t* a) {
   asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(a));
   return v;
 }
-template <bool OGS, class Pre, class Body>
-__device__ __forceinline__ void walk_order(const uint16_t* __restrict__ og, uint32_t aOg, int w0, int w1, Pre&& pre,
-                                           Body&& body) {
+// eight loads of one lane at a fixed 32-position stride (eight consecutive
+// words of a streamed order): immediate offsets, one address per group
+__device__ __forceinline__ void ldg_x8(const uint16_t* p, uint32_t (&d)[8]) {
+  unsigned short v0, v1, v2, v3, v4, v5, v6, v7;
+  asm volatile(
+      "ld.global.nc.u16 %0, [%8];\n\tld.global.nc.u16 %1, [%8+64];\n\t"
+      "ld.global.nc.u16 %2, [%8+128];\n\tld.global.nc.u16 %3, [%8+192];\n\t"
+      "ld.global.nc.u16 %4, [%8+256];\n\tld.global.nc.u16 %5, [%8+320];\n\t"
+      "ld.global.nc.u16 %6, [%8+384];\n\tld.global.nc.u16 %7, [%8+448];"
+      : "=h"(v0), "=h"(v1), "=h"(v2), "=h"(v3), "=h"(v4), "=h"(v5), "=h"(v6), "=h"(v7)
+      : "l"(p));
+  d[0] = v0; d[1] = v1; d[2] = v2; d[3] = v3; d[4] = v4; d[5] = v5; d[6] = v6; d[7] = v7;
+}
+__device__ __forceinline__ void ldg_x8(const uint32_t* p, uint32_t (&d)[8]) {
+  asm volatile(
+      "ld.global.nc.u32 %0, [%8];\n\tld.global.nc.u32 %1, [%8+128];\n\t"
+      "ld.global.nc.u32 %2, [%8+256];\n\tld.global.nc.u32 %3, [%8+384];\n\t"
+      "ld.global.nc.u32 %4, [%8+512];\n\tld.global.nc.u32 %5, [%8+640];\n\t"
+      "ld.global.nc.u32 %6, [%8+768];\n\tld.global.nc.u32 %7, [%8+896];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+      : "l"(p));
+}
+__device__ __forceinline__ uint32_t ldg_early(const uint16_t* a) { return ldg16_early(a); }
+__device__ __forceinline__ uint32_t ldg_early(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(a));
+  return v;
+}
+
+// Walk of a warp's words [w0, w1) of a streamed g order (global memory;
+// 16-bit sample ids, or 32-bit id | group id << 16) in groups of G = 8 words,
+// loaded two groups ahead: the group's entries are first mapped by pre() --
+// the gathers of the whole group issue back to back -- and then handed to
+// body(word, pre(x), x) in word order.  The shared accesses are volatile asm,
+// so without the grouping each word's gather would wait for the previous
+// word's store; the global loads are volatile too, so that ptxas cannot sink
+// them to their use.  Three register groups rotate by unrolling (no moves);
+// full groups load with immediate offsets.
+template <class E, class Pre, class Body>
+__device__ __forceinline__ void walk_order(const E* __restrict__ og, int w0, int w1, Pre&& pre, Body&& body) {
   const int lane = threadIdx.x & 31;
   constexpr int G = 8;
-  uint32_t s0[G], s1[G];
+  const E* pl = og + lane;
   auto load = [&](uint32_t (&d)[G], int wb) {
+    if (wb + G <= w1) {
+      ldg_x8(pl + (size_t)wb * 32, d);
+    } else {
 #pragma unroll
-    for (int u = 0; u < G; ++u) {
-      const uint32_t p = (uint32_t)((wb + u) * 32 + lane);
-      d[u] = wb + u < w1 ? (OGS ? ld16(aOg + 2 * p) : ldg16_early(og + p)) : 0u;
+      for (int u = 0; u < G; ++u) d[u] = wb + u < w1 ? ldg_early(pl + (size_t)(wb + u) * 32) : 0u;
     }
   };
-  load(s0, w0);
-  if (!OGS) load(s1, w0 + G);
-  for (int wb = w0; wb < w1; wb += G) {
-    uint32_t s2[G];
-    if (!OGS) load(s2, wb + 2 * G);
+  auto run = [&](const uint32_t (&d)[G], int wb) {
     uint32_t q[G];
 #pragma unroll
-    for (int u = 0; u < G; ++u) q[u] = pre(s0[u]);
+    for (int u = 0; u < G; ++u) q[u] = pre(d[u]);
     if (wb + G <= w1) {
 #pragma unroll
-      for (int u = 0; u < G; ++u) body(wb + u, q[u]);
+      for (int u = 0; u < G; ++u) body(wb + u, q[u], d[u]);
     } else {
 #pragma unroll
       for (int u = 0; u < G; ++u)
-        if (wb + u < w1) body(wb + u, q[u]);
+        if (wb + u < w1) body(wb + u, q[u], d[u]);
     }
-    if (OGS) {
-      load(s0, wb + G);
-    } else {
-#pragma unroll
-      for (int u = 0; u < G; ++u) {
-        s0[u] = s1[u];
-        s1[u] = s2[u];
-      }
-    }
+  };
+  uint32_t A[G], B[G], C[G];
+  load(A, w0);
+  load(B, w0 + G);
+  for (int wb = w0; wb < w1; wb += 3 * G) {
+    load(C, wb + 2 * G);
+    run(A, wb);
+    if (wb + G >= w1) break;
+    load(A, wb + 3 * G);
+    run(B, wb + G);
+    if (wb + 2 * G >= w1) break;
+    load(B, wb + 4 * G);
+    run(C, wb + 2 * G);
   }
 }
 
@@ -371,7 +411,8 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
                      const uint32_t* __restrict__ tb, const uint16_t* __restrict__ lastb,
                      const uint16_t* __restrict__ nextb, int64_t ldt, const uint8_t* __restrict__ tied,
                      const int32_t* __restrict__ lens, const uint16_t* __restrict__ gpt,
-                     const uint16_t* __restrict__ bpos, const int32_t* __restrict__ ngrp, int cap, int64_t F,
+                     const uint16_t* __restrict__ bpos, const int32_t* __restrict__ ngrp,
+                     const uint32_t* __restrict__ ordgid, int cap, int64_t F,
                      const int4* __restrict__ items, int n_items, int once, int* __restrict__ queue, PairParts out) {
   const WalkLayout L(ldo, ldt, OGS, R2, cap);
   __shared__ uint32_t wtot[SW], wtotA[SW];
@@ -493,6 +534,31 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
     }
     return acc;
   };
+  // g's packed table: tabg[k] = Pfx(start of group k) | Pfx(its end) << 16
+  // (k < D); the caller's next block barrier publishes it
+  const uint32_t aTabG = sb + 4 * L.tabg32;
+  auto build_tabg = [&](int D, uint32_t aB, int Lseg, uint32_t segpre, uint32_t tot,
+                        uint32_t nf) -> unsigned long long {
+    const uint32_t magic = (uint32_t)((0x100000000ull + (uint32_t)Lseg - 1u) / (uint32_t)Lseg);
+    auto pabs = [&](uint32_t x) -> uint32_t {  // all lanes (shuffle inside)
+      const uint32_t wx = min(x, nf - 1u) >> 5;
+      const uint32_t base = __shfl_sync(PS_FULL, segpre, Lseg == 1 ? (int)wx : (int)__umulhi(wx, magic));
+      const uint32_t v = ldP(wx) + base + __popc(ld32(kA(wx)) & ((1u << (x & 31u)) - 1u));
+      return x >= nf ? tot : v;
+    };
+    unsigned long long acc = 0;
+    for (int kb = warp * 32; kb < D; kb += STH) {  // warp-uniform
+      const int k = kb + lane;
+      const uint32_t a = pabs(k < D ? ld16(aB + 2 * (uint32_t)k) : nf);
+      const uint32_t b = pabs(k < D ? ld16(aB + 2 * (uint32_t)k + 2u) : nf);
+      if (k < D) {
+        st32(aTabG + 4 * (uint32_t)k, a | (b << 16));
+        const unsigned long long r2 = a + b + 1u;
+        acc += (unsigned long long)(b - a) * r2 * r2;
+      }
+    }
+    return acc;
+  };
   // doubled rank of every lane of a word of a group-table feature
   auto tab_r2 = [&](uint32_t T, uint32_t gw) -> uint32_t {
     const uint32_t gid = gw + __popc(T & (0xFFFFFFFFu >> (31 - lane))) - 1u;
@@ -500,6 +566,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
   };
 
   __shared__ int4 s_it;
+  bool par_dirty = false;  // (!R2) g's packed table, which aliases the parity words, was used
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -571,12 +638,16 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       const uint32_t aOg = sb + 2 * L.og16[buf];
       const uint32_t aTbg = sb + 4 * L.tbg[buf], aLbg = sb + 2 * L.lbg16[buf], aNbg = sb + 2 * L.nbg16[buf];
       const uint16_t* og_g = order + g * ldo;
-      const bool gtab = tg && gtab_ok && Dg <= cap;
+      const bool gtab = tg && gtab_ok && Dg <= cap && (OGS || ordgid != nullptr);
       const uint32_t aBg = OGS ? sb + 2 * L.bposg16[buf] : sb + 2 * L.bposg16s;
       if (!OGS && gtab) {  // streamed g: its group starts by cp.async, waited for after phase 1
         const unsigned char* b2 = reinterpret_cast<const unsigned char*>(bpos + g * ldo);
         for (int c = threadIdx.x; c < ((Dg + 1 + 7) >> 3); c += STH) cp16(aBg + c * 16, b2 + c * 16);
         asm volatile("cp.async.commit_group;");
+      }
+      if (!R2 && par_dirty && tg && !gtab) {  // this pair may set parity bits: clear the table's entries
+        for (int i = threadIdx.x; i < (int)ldt; i += STH) sm32[L.par + i] = 0u;
+        par_dirty = false;
       }
       // ---------------- pass A, phase 1: keep bits over g's order ----------
       const int nwa = (ng + 31) >> 5;
@@ -604,14 +675,44 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           for (int word = a0; word < a1; ++word)
             body(word, ld16(aInv + 2 * ld16(aOg + 2 * (uint32_t)(word * 32 + lane))));
         } else {
-          walk_order<false>(og_g, aOg, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); }, body);
+          walk_order(og_g, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); },
+                     [&](int word, uint32_t q, uint32_t) { body(word, q); });
         }
         if (lane == 0) wtotA[warp] = cnt;
         __syncthreads();
         segment_bases(wtotA, segpreA, n);
         WT(1);
       } else {
-      {
+      if (gtab) {
+        // group-table g, one phase: every kept position scatters its group
+        // id + 1 to R[q]; pass B reads 2 r_g from g's packed group table
+        uint32_t cnt = 0;
+        const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
+        if (OGS) {
+          const uint32_t aGpg = sb + 2 * L.gpg16[buf];
+#pragma unroll 4
+          for (int word = a0; word < a1; ++word) {
+            const uint32_t q = ld16(aInv + 2 * ld16(aOg + 2 * (uint32_t)(word * 32 + lane)));
+            const uint32_t gid1 = ld16(aGpg + 2 * word) + __popc(ld32(aTbg + 4 * word) & le);
+            const bool keep = q != 0xFFFFu;
+            const uint32_t B = __ballot_sync(PS_FULL, keep);
+            if (lane == 0) stKP(word, B, cnt);
+            if (keep) st16(aR + 2 * q, gid1);
+            cnt += __popc(B);
+          }
+        } else {
+          // streamed g: sample id | group id << 16 per position (ordgid)
+          walk_order(ordgid + g * ldo, a0, a1, [&](uint32_t x) { return ld16(aInv + 2 * (x & 0xFFFFu)); },
+                     [&](int word, uint32_t q, uint32_t x) {
+                       const bool keep = q != 0xFFFFu;
+                       const uint32_t B = __ballot_sync(PS_FULL, keep);
+                       if (lane == 0) stKP(word, B, cnt);
+                       if (keep) st16(aR + 2 * q, (x >> 16) + 1u);
+                       cnt += __popc(B);
+                     });
+        }
+        if (lane == 0) wtot[warp] = cnt;
+      } else {
         // q = inv_h[order_g[p]]; with g's order staged in shared memory the
         // gathered q overwrites it in place, so phase 2 reads it sequentially
         uint32_t cnt = 0;
@@ -626,7 +727,8 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           for (int word = a0; word < a1; ++word)
             body(word, ld16(aInv + 2 * ld16(aOg + 2 * (uint32_t)(word * 32 + lane))));
         } else {
-          walk_order<false>(og_g, aOg, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); }, body);
+          walk_order(og_g, a0, a1, [&](uint32_t s) { return ld16(aInv + 2 * s); },
+                     [&](int word, uint32_t q, uint32_t) { body(word, q); });
         }
         if (lane == 0) wtot[warp] = cnt;
       }
@@ -639,7 +741,8 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
         r2fit = R2 || (2u * n + 1u <= 0xFFFFu);
         abase = __shfl_sync(PS_FULL, segpre, warp);
         if (gtab) {
-          sa2 = build_tab(Dg, aBg, La, segpre, n, (uint32_t)ng);
+          sa2 = build_tabg(Dg, aBg, La, segpre, n, (uint32_t)ng);
+          if (!R2) par_dirty = true;
         } else if (tg && R2) {
           if (OGS)
             fill_spep(a0, a1, La, segpre, n, (uint32_t)ng, [&](int w) { return ld32(aTbg + 4 * w); },
@@ -668,55 +771,8 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
           if (r2 & 1u) atomicOr(&sm32[L.par + (q >> 5)], 1u << (q & 31u));
         }
       };
-      if (gtab && OGS) {
-        const uint32_t aGpg = sb + 2 * L.gpg16[buf];
-#pragma unroll 4
-        for (int word = a0; word < a1; ++word) {
-          const uint32_t kw = ld32(kA(word));
-          const uint32_t r2 = tab_r2(ld32(aTbg + 4 * word), ld16(aGpg + 2 * word));
-          if ((kw >> lane) & 1u) st_r2(ld16(aOg + 2 * (uint32_t)(word * 32 + lane)), r2);
-        }
-      } else if (gtab) {
-        // streamed g: boundary bits and group counts of the warp's words in
-        // registers (lane j of slot i: word a0 + 32 i + j), g's order two
-        // 8-word groups ahead
-        const uint32_t* tbgg = tb + g * ldt;
-        const uint16_t* gpgg = gpt + g * ldt;
-        uint32_t rT[kRecSlots], rG[kRecSlots];
-#pragma unroll
-        for (int i = 0; i < kRecSlots; ++i) {
-          const int w = a0 + 32 * i + lane;
-          rT[i] = w < a1 ? tbgg[w] : 0u;
-          rG[i] = w < a1 ? (uint32_t)gpgg[w] : 0u;
-        }
-        auto og_at = [&](int word) -> uint32_t {
-          return word < a1 ? (uint32_t)og_g[(uint32_t)(word * 32 + lane)] : 0u;
-        };
-        uint32_t sc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) sc[u] = og_at(a0 + u);
-        for (int w8 = a0; w8 < a1; w8 += 8) {
-          uint32_t sn[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) sn[u] = og_at(w8 + 8 + u);
-          const int i = (w8 - a0) >> 5;
-          const uint32_t RT = pick_slot(rT, i), RG = pick_slot(rG, i);
-          uint32_t q[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) q[u] = ld16(aInv + 2 * sc[u]);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int word = w8 + u;
-            if (word < a1) {  // warp-uniform
-              const int jl = (word - a0) & 31;
-              const uint32_t kw = ld32(kA(word));
-              const uint32_t r2 = tab_r2(__shfl_sync(PS_FULL, RT, jl), __shfl_sync(PS_FULL, RG, jl));
-              if ((kw >> lane) & 1u) st_r2(q[u], r2);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) sc[u] = sn[u];
-        }
+      if (gtab) {
+        // (no second phase: ranks are resolved through g's table in pass B)
       } else if (!tg) {
 #pragma unroll(OGS ? 4 : 8)
         for (int word = a0; word < a1; ++word) {
@@ -816,9 +872,15 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
       // decode R -> 2 r_g (all lanes must execute: shuffles)
       auto r2g_of = [&](uint32_t v, int word) -> uint32_t {
         if (encA) return 2u * (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask));
+        if (gtab) {  // v = group id + 1 (0: not kept -- any in-range entry)
+          const uint32_t e = ld32(aTabG + 4 * (v ? v - 1u : 0u));
+          return (e & 0xFFFFu) + (e >> 16) + 1u;
+        }
         if (r2fit) return v;
         return 2u * v + (tg ? ((ld32(aPar + 4 * word) >> lane) & 1u) : 0u);
       };
+      // parity words of g's doubled ranks are in use (cleared on the way)
+      const bool parA = !r2fit && tg && !gtab;
       const bool sweepB = !th;
       unsigned long long sab = 0, sbb = 0, s0 = 0;
       uint32_t wtotB = 0;
@@ -842,10 +904,6 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
               st16(aR + 2 * q, 0u);
             }
             cnt += __popc(B);
-            if (!r2fit && tg) {  // parity bits of this word were read above
-              __syncwarp();
-              if (lane == 0) st32(aPar + 4 * word, 0u);
-            }
           }
         };
         if (encA) sweep(std::true_type{});
@@ -905,10 +963,6 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
               sab += (unsigned long long)r2g * r2h;
               st16(aR + 2 * q, 0u);
             }
-            if (!r2fit && tg) {
-              __syncwarp();
-              if (lane == 0) st32(aPar + 4 * word, 0u);
-            }
           }
         };
         if (encA) walkt(std::true_type{});
@@ -925,10 +979,6 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             sab += (unsigned long long)r2g * rh;
             st16(aR + 2 * q, 0u);
           }
-          if (!r2fit && tg) {
-            __syncwarp();
-            if (lane == 0) st32(aPar + 4 * word, 0u);
-          }
         }
         sab *= 2ull;  // r2g * r_h = (2 r_g)(2 r_h) / 2
       } else if (R2) {
@@ -941,7 +991,7 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
             const uint32_t v = ld16(aR + 2 * q);
             uint32_t r2g;  // all lanes (shuffle)
             if constexpr (decltype(enc)::value) r2g = (__shfl_sync(PS_FULL, segpreA, (int)(v >> kEncShift)) + (v & kEncMask)) << 1;
-            else r2g = v;
+            else r2g = r2g_of(v, word);
             const uint32_t r2h = word_r2(ld32(aTbh + 4 * word), rec.z, rec.w, kw, rec.y + bbase);
             const uint32_t r2hk = (kw >> lane) & 1u ? r2h : 0u;
             sab += (unsigned long long)r2g * r2hk;  // r2g is meaningless where not kept: r2hk = 0
@@ -984,14 +1034,14 @@ spearman_walk_kernel(const uint16_t* __restrict__ order, const uint16_t* __restr
               sbb += (unsigned long long)r2h * r2h;
               st16(aR + 2 * q, 0u);
             }
-            if (!r2fit && tg) {
-              __syncwarp();
-              if (lane == 0) st32(aPar + 4 * word, 0u);
-            }
           }
         }
       }
       }  // two-phase pass B
+      if (parA) {  // the parity words of this warp's h words were read: clear them
+        __syncwarp();
+        for (int w = b0 + lane; w < b1; w += 32) st32(aPar + 4 * w, 0u);
+      }
       WT(5);
       // ---------------- per-warp partial sums -> global ---------------------
       // (no block barrier: the next pair's top barrier orders R / record reuse)
@@ -1311,7 +1361,8 @@ static int walk_launch(ps_spearman_job* j, int64_t h0, int64_t h1, int64_t c0, i
   const int grid = once ? (int)n : (int)std::min<int64_t>(n, grid_max);
   ps_prof_begin("spearman_walk", s);
   j->kern<<<grid, STH, j->smem, s>>>(a->d_order, a->d_inv, a->ldo, a->d_tb, a->d_lastb, a->d_nextb, a->ldt,
-                                     a->d_tied, a->d_len, a->d_gp, a->d_bpos, a->d_ngrp, j->cap, a->F, items,
+                                     a->d_tied, a->d_len, a->d_gp, a->d_bpos, a->d_ngrp, a->d_ordgid, j->cap, a->F,
+                                     items,
                                      (int)n, once, q, pp);
   ps_prof_end(s);
   PS_LAUNCHED();
@@ -1356,6 +1407,16 @@ static int fold_finish_columns(ps_spearman_job* j, int64_t h0, int64_t h1, cudaS
   return rc;
 }
 
+// true when the shared-memory walk streams g's order from global memory
+// (does not stage it): such walks read the packed ordgid table
+bool ps_spearman_streams_g(int64_t S) {
+  if (S > 65535) return false;
+  const int64_t ldo = ps_round_up(S + 1, 64), ldt = tie_words(S);
+  const size_t limit = 227 * 1024 - 1024;
+  const size_t smem = walk_smem(ldo, ldt, true, S <= 32767, 0);
+  return !(smem <= limit / 2 || (smem <= limit && S > 12000));
+}
+
 // true when the shared-memory walk's tables do not fit for S samples (or the
 // presort is 32-bit): such matrices take the wide walk
 bool ps_spearman_wide(int64_t S) {
@@ -1376,21 +1437,32 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double
   const size_t limit = 227 * 1024 - 1024;
   const bool r2 = a->S <= 32767;  // 2r fits 16 bits: no parity bits
   size_t smem = walk_smem(a->ldo, a->ldt, true, r2, 0);
-  bool ogs = smem <= limit / 2 || (smem <= limit && a->S > 12000);
+  bool ogs = !ps_spearman_streams_g(a->S);
   if (const char* e = getenv("PS_SPEARMAN_OGS")) ogs = smem <= limit && e[0] == '1';  // tuning override
   if (!ogs) smem = walk_smem(a->ldo, a->ldt, false, r2, 0);
   if (smem > limit) return ps_fail(PS_ERR_INVALID, "spearman: sample count too large for the shared-memory walk");
   // group-table capacity: the largest that keeps the CTAs per SM of the
-  // table-less layout (two per SM when that fits in half the budget)
+  // table-less layout (occupancy queried for the kernel this layout runs)
+  WalkKernel kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
+                        : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
   int cap = 0;
   if (a->d_gp && !getenv("PS_SPEARMAN_NOTAB")) {
-    const size_t budget = smem <= limit / 2 ? limit / 2 : limit;
-    for (int c = 2040; c >= 64; c -= 8)
-      if (walk_smem(a->ldo, a->ldt, ogs, r2, c) <= budget) {
+    auto occ = [&](size_t sm) {
+      int n = 0;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, STH, sm) != cudaSuccess)
+        return 0;
+      return n;
+    };
+    const int want = occ(smem);
+    for (int c = 2040; c >= 64 && want > 0; c -= 8) {
+      const size_t sm = walk_smem(a->ldo, a->ldt, ogs, r2, c);
+      if (sm <= limit && occ(sm) >= want) {
         cap = c;
+        smem = sm;
         break;
       }
-    if (cap) smem = walk_smem(a->ldo, a->ldt, ogs, r2, cap);
+    }
   }
   ps_spearman_job* j = new ps_spearman_job();
   j->a = a;
@@ -1403,8 +1475,7 @@ int ps_spearman_begin(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double
   j->rho = rho;
   j->smem = smem;
   j->cap = cap;
-  j->kern = ogs ? (r2 ? spearman_walk_kernel<true, true> : spearman_walk_kernel<true, false>)
-                : (r2 ? spearman_walk_kernel<false, true> : spearman_walk_kernel<false, false>);
+  j->kern = kern;
   j->home = s;
   if (const char* e = getenv("PS_SPEARMAN_GB")) j->gb = std::max<int64_t>(1, atoll(e));
   int rc = PS_OK;
