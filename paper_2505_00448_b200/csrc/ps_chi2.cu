@@ -270,6 +270,14 @@ onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
   const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;
   const int64_t total = nunits * nk;
   const int64_t i0 = total * cl / ncl, i1 = total * (cl + 1) / ncl;
+  // A cluster's range [i0, i1) of the (unit, k) iterations splits into
+  // segments at unit boundaries; they are walked LAST FIRST.  Ranges are
+  // equal (L = i1 - i0), so cluster c's last segment starts at k = 0 at time 0
+  // and its first one, entered when the last ends, is exactly L mod nk steps
+  // behind: at any time every cluster is within L mod nk k-steps of the same
+  // k, and the one-hot slab in flight stays L2-resident (walked first to last,
+  // the ranges start at scattered k and the whole operand cycles through L2).
+  auto seg_start = [&](int64_t se) -> int64_t { return std::max<int64_t>(i0, ((se - 1) / nk) * nk); };
   auto tile_of = [&](const int4& u, int& I, int& J) -> bool {  // false: dummy
     I = rank ? u.z : u.x;
     J = rank ? u.w : u.y;
@@ -294,8 +302,10 @@ onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
 
   if (warp == 4) {
     if (lane == 0) {  // TMA producer
-      for (int64_t it = i0; it < i1; ++it) {
-        const int64_t q = it - i0;
+      int64_t q = 0;
+      for (int64_t se = i1; se > i0;) {  // segments last to first (see seg_start)
+        const int64_t ss = seg_start(se);
+        for (int64_t it = ss; it < se; ++it, ++q) {
         const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
         const int4 u = units[it / nk];
         const int kx = (kbase + (int)(it % nk)) * TKB;
@@ -313,20 +323,23 @@ onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
           tc05::tma_load_2d(od, &tmap, kx, orow, &full[st]);
           tc05::tma_load_2d(od + THALF, &tmap, kx, orow + 128, &full[st]);
         }
+        }
+        se = ss;
       }
     }
   } else if (warp == 5) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = tc05::idesc_i8(128, TN, true);
       int seg = 0;
-      for (int64_t it = i0; it < i1; ++it) {
-        const int64_t q = it - i0;
+      int64_t q = 0;
+      for (int64_t se = i1; se > i0;) {
+        const int64_t ss = seg_start(se);
+        for (int64_t it = ss; it < se; ++it, ++q) {
         const int st = (int)(q % TSTAGES), n = (int)(q / TSTAGES);
-        const int kc = (int)(it % nk);
         int I, J;
         const bool own = tile_of(units[it / nk], I, J);
-        const bool first = it == i0 || kc == 0;
-        const bool last = it + 1 == i1 || kc == nk - 1;
+        const bool first = it == ss;
+        const bool last = it + 1 == se;
         if (own && first && seg > 0) {  // the epilogue has drained the previous segment
           tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
           tc05::fence_after_sync();
@@ -348,15 +361,17 @@ onehot_gemm_mc_kernel(const __grid_constant__ CUtensorMap tmap, int nk, int kbas
           tc05::commit(&accfull);
           ++seg;
         }
+        }
+        se = ss;
       }
     }
   } else {
     // epilogue warps 0-3: one pass per segment of an own tile, in the MMA issuer's order
     int seg = 0;
-    for (int64_t it = i0; it < i1;) {
-      const int64_t unit = it / nk;
-      const int64_t seg_end = std::min<int64_t>(i1, (unit + 1) * nk);
-      it = seg_end;
+    for (int64_t se = i1; se > i0;) {
+      const int64_t ss = seg_start(se);
+      const int64_t unit = ss / nk;
+      se = ss;
       int I, J;
       if (!tile_of(units[unit], I, J)) continue;
       tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
@@ -392,8 +407,15 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
   }
 }
 
-// One thread per pair (g <= h): categorical.py:31-74 in the same op order.
-// Row/column sums are cached for up to CM levels; the table is read from C.
+// pairs (x, y >= x) with x in [lo, g): rows of the upper triangle before row g
+__device__ __forceinline__ int64_t upper_before(int64_t g, int64_t lo, int64_t F) {
+  return (g - lo) * F - (g * (g - 1) - lo * (lo - 1)) / 2;
+}
+
+// One thread per pair (g <= h, enumerated over the upper triangle of rows
+// [lo, hi): no idle threads): categorical.py:31-74 in the same op order.
+// Row / column sums are cached for up to CM levels (CM == 0, category counts
+// above 256: per-thread global scratch slices).  The table is read from C.
 template <int CM, typename Acc>
 __global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64_t crow0,
                                    const int32_t* __restrict__ off, const int32_t* __restrict__ cat,
@@ -401,11 +423,16 @@ __global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64
                                    double* __restrict__ pout, double* __restrict__ phi_out,
                                    double* __restrict__ v_out, int* __restrict__ err, long long* big = nullptr,
                                    int cmax_big = 0) {
-  const int64_t total = (hi - lo) * F;
+  const int64_t total = upper_before(hi, lo, F);
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
        it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = lo + it / F, h = it % F;
-    if (h < g) continue;
+    int64_t a = lo, b = hi - 1;  // last row g with upper_before(g) <= it
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (upper_before(mid, lo, F) <= it) a = mid;
+      else b = mid - 1;
+    }
+    const int64_t g = a, h = g + (it - upper_before(g, lo, F));
     const int cg = cat[g], ch = cat[h];
     const bool diag = g == h;
     const Acc* T = C + ((int64_t)off[g] - crow0) * ldC + off[h];  // exact integer counts
@@ -415,38 +442,43 @@ __global__ void chi2_finish_kernel(const Acc* __restrict__ C, int64_t ldC, int64
       if (diag && i != j) return 0;
       return (long long)T[(int64_t)i * ldC + j];
     };
-    // CM == 0 (category counts above 256): the row / column sums live in
-    // per-thread global scratch slices instead of registers / local memory
-    long long rs_l[CM > 0 ? CM : 1], cs_l[CM > 0 ? CM : 1];
-    long long* rs = CM > 0 ? rs_l : big + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 2 * cmax_big;
-    long long* cs = CM > 0 ? cs_l : rs + cmax_big;
-    for (int j = 0; j < ch; ++j) cs[j] = 0;
-    long long n = 0;
-    for (int i = 0; i < cg; ++i) {
-      long long r = 0;
-      for (int j = 0; j < ch; ++j) {
-        const long long t = tab(i, j);
-        r += t;
-        cs[j] += t;
-      }
-      rs[i] = r;
-      n += r;
-    }
     double chi2 = PS_NAN, p = PS_NAN, phi = PS_NAN, v = PS_NAN;
-    bool empty = n == 0;
-    for (int i = 0; i < cg; ++i) empty |= rs[i] == 0;
-    for (int j = 0; j < ch; ++j) empty |= cs[j] == 0;
-    if (!empty) {
-      double acc = 0.0;
-      const double dn = (double)n;
-      for (int i = 0; i < cg; ++i)
+    long long n = 0;
+    bool empty;
+    double acc = 0.0;
+    {
+      // row / column sums: per-thread arrays (CM > 0) or global scratch slices
+      long long rs_l[CM > 0 ? CM : 1], cs_l[CM > 0 ? CM : 1];
+      long long* rs = CM > 0 ? rs_l : big + (int64_t)(blockIdx.x * blockDim.x + threadIdx.x) * 2 * cmax_big;
+      long long* cs = CM > 0 ? cs_l : rs + cmax_big;
+      for (int j = 0; j < ch; ++j) cs[j] = 0;
+      for (int i = 0; i < cg; ++i) {
+        long long r = 0;
         for (int j = 0; j < ch; ++j) {
-          const double expected = (double)(rs[i] * cs[j]) / dn;
-          if (expected > 0.0) {
-            const double diff = (double)tab(i, j) - expected;
-            acc += diff * diff / expected;
-          }
+          const long long t = tab(i, j);
+          r += t;
+          cs[j] += t;
         }
+        rs[i] = r;
+        n += r;
+      }
+      empty = n == 0;
+      for (int i = 0; i < cg; ++i) empty |= rs[i] == 0;
+      for (int j = 0; j < ch; ++j) empty |= cs[j] == 0;
+      if (!empty) {
+        const double dn = (double)n;
+        for (int i = 0; i < cg; ++i)
+          for (int j = 0; j < ch; ++j) {
+            const double expected = (double)(rs[i] * cs[j]) / dn;
+            if (expected > 0.0) {
+              const double diff = (double)tab(i, j) - expected;
+              acc += diff * diff / expected;
+            }
+          }
+      }
+    }
+    if (!empty) {
+      const double dn = (double)n;
       chi2 = acc;
       phi = sqrt(acc / dn);
       const int cmin = cg < ch ? cg : ch;
@@ -624,15 +656,14 @@ static int chi2_band(ps_matrix* a, const std::vector<int32_t>& off, int64_t ga, 
     }
     ps_prof_end(s);
   }
-  const int64_t total = (gb - ga) * F;
-  const int blocks = (int)std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16);
+  const int64_t total = (gb - ga) * F - ((gb * (gb - 1)) - (ga * (ga - 1))) / 2;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ps_ceil_div(total, 128), (int64_t)ds->num_sms * 16));
   long long* big = nullptr;
+  auto fin = [&](auto kern) {
+    kern<<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v, ds->d_err, nullptr, 0);
+  };
   if (a->cmax <= 16) {
-    chi2_finish_kernel<16, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
-                                                       ds->d_err);
-  } else if (a->cmax <= 256) {
-    chi2_finish_kernel<256, Acc><<<blocks, 128, 0, s>>>(C, Rp, crow0, d_off, a->d_cat, F, ga, gb, stat, p, phi, v,
-                                                        ds->d_err);
+    fin(chi2_finish_kernel<16, Acc>);
   } else {
     const int bb = ds->num_sms * 2;
     PS_CUDA(ps_alloc(&big, (size_t)bb * 128 * 2 * a->cmax, s));

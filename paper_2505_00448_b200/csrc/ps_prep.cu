@@ -113,6 +113,63 @@ prep_rows_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t
   }
 }
 
+// Label matrices prepared from fp64 values on the device: presence / zero /
+// out-of-range bit words and label codes only (the pivot is unused for
+// labels: 0, as for host-staged codes).  Present counts are integer atomics
+// (order-free); the caller zeroes count / center of the rows first.
+template <typename CT>
+__global__ void __launch_bounds__(kPrepThreads, 4)
+prep_labels_kernel(const double* __restrict__ vals, int64_t ld, int64_t S, int64_t W, uint64_t sent_bits,
+                   int sent_nan, uint32_t* __restrict__ mask, int32_t* __restrict__ count,
+                   const int32_t* __restrict__ cat, CT* __restrict__ codes, int64_t ldc,
+                   uint32_t* __restrict__ zero_bits, uint32_t* __restrict__ bad_bits, int64_t f0) {
+  const int64_t f = f0 + blockIdx.x;
+  const double* row = vals + f * ld;
+  CT* crow = codes + f * ldc;
+  uint32_t* mrow = mask + f * W;
+  uint32_t* zrow = zero_bits + f * W;
+  uint32_t* brow = bad_bits + f * W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double dcf = (double)cat[f];
+  const int64_t s_lo = (int64_t)blockIdx.y * kPrepSeg;
+  const int64_t s_hi = min(S, s_lo + kPrepSeg);
+  constexpr CT kMiss = (CT)~(CT)0, kBad = (CT)~(CT)1;
+  int cnt = 0;  // lane 0: present count of the warp's words
+  constexpr int kU = 8;
+  for (int64_t base0 = s_lo + (int64_t)warp * 32; base0 < s_hi; base0 += (int64_t)kPrepThreads * kU) {
+    double vu[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t s = base0 + (int64_t)u * kPrepThreads + lane;
+      vu[u] = s < S ? row[s] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t base = base0 + (int64_t)u * kPrepThreads;
+      if (base >= S) break;
+      const int64_t s = base + lane;
+      const double v = vu[u];
+      const bool pres = s < S && ps_is_present(v, sent_bits, sent_nan);
+      // int(label) truncates toward zero (categorical.py:87); NaN fails both compares
+      const bool ok = pres && v > -1.0 && v < dcf;
+      if (s < S) crow[s] = ok ? (CT)(int)v : (pres ? kBad : kMiss);
+      const uint32_t word = __ballot_sync(PS_FULL, pres);
+      const uint32_t zw = __ballot_sync(PS_FULL, pres && v == 0.0);
+      const uint32_t bw = __ballot_sync(PS_FULL, pres && !ok);
+      if (lane == 0) {
+        const int64_t w = base >> 5;
+        mrow[w] = word;
+        zrow[w] = zw;
+        brow[w] = bw;
+        cnt += __popc(word);
+      }
+    }
+  }
+  if (blockIdx.y + 1 == gridDim.y)
+    for (int64_t s = S + threadIdx.x; s < ldc; s += kPrepThreads) crow[s] = kMiss;
+  if (lane == 0 && cnt) atomicAdd(&count[f], cnt);
+}
+
 __global__ void prep_finish_kernel(const double* __restrict__ psum, const int32_t* __restrict__ pcnt, int nseg,
                                    int64_t nrows, int64_t f0, int32_t* __restrict__ count,
                                    double* __restrict__ center) {
@@ -222,11 +279,25 @@ int ps_prepare_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
   const int nseg = (int)std::max<int64_t>(1, ps_ceil_div(m->S, kPrepSeg));
   double* psum = nullptr;
   int32_t* pcnt = nullptr;
+  const dim3 grid((unsigned)nrows, (unsigned)nseg);
+  if (labels) {
+    PS_CUDA(cudaMemsetAsync(m->d_count + f0, 0, sizeof(int32_t) * nrows, s));
+    PS_CUDA(cudaMemsetAsync(m->d_center + f0, 0, sizeof(double) * nrows, s));
+    if (m->code_bytes == 2)
+      prep_labels_kernel<uint16_t><<<grid, kPrepThreads, 0, s>>>(
+          m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_count, m->d_cat,
+          reinterpret_cast<uint16_t*>(m->d_codes), m->ldc, m->d_zero, m->d_bad, f0);
+    else
+      prep_labels_kernel<uint8_t><<<grid, kPrepThreads, 0, s>>>(
+          m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_count, m->d_cat,
+          m->d_codes, m->ldc, m->d_zero, m->d_bad, f0);
+    PS_LAUNCHED();
+    return PS_OK;
+  }
   if (nseg > 1) {
     PS_CUDA(ps_alloc(&psum, (size_t)(nrows * nseg), s));
     PS_CUDA(ps_alloc(&pcnt, (size_t)(nrows * nseg), s));
   }
-  const dim3 grid((unsigned)nrows, (unsigned)nseg);
   if (labels && m->code_bytes == 2)
     prep_rows_kernel<uint16_t><<<grid, kPrepThreads, 0, s>>>(
         m->d_vals, m->ld, m->S, m->W, m->sentinel_bits, m->sentinel_is_nan, m->d_mask, m->d_center, m->d_count,
