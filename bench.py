@@ -385,6 +385,27 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- GPU arm
 
+def moments_used(wl: Workload) -> bool:
+    """Pearson computes its masked moments on the int8 tensor cores (library rule)."""
+    from paper_2505_00448_b200 import _lib
+
+    return bool(_lib.load().ps_pearson_moments_used(wl.Fa, wl.S))
+
+
+def roofline_moments(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):
+    """The int8 moment contractions of large-F Pearson (ps_moments.cu): 2 moments
+    x 7 digits x 2 ops per ORDERED pair-sample, digit expansion included."""
+    if not kern_n:
+        return None
+    launch_ms = kern_ms / steps
+    ops = 2 * 7 * 2.0 * wl.Fa * wl.Fa * wl.S / world
+    achieved = ops / (launch_ms / 1e3) / 1e12
+    peak = peaks["tcgen05_i8_tops"]
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
+            "kernel": "pearson_moments", "launch_ms": launch_ms, "launches_per_step": kern_n / steps,
+            "work_per_ordered_pair_sample": "28 int8 ops (tcgen05 kind::i8, 7-digit expansion of x' and x'^2)"}
+
+
 def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):
     if not kern_n:
         return None
@@ -404,10 +425,14 @@ def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, 
         achieved = per_launch / (launch_ms / 1e3) / 1e12
         desc = "4 k_g FP64 flops"
     elif bound == "tensor":
+        if test == "pearson" and moments_used(wl):
+            per_ps = 2.0  # Sxy alone on DMMA; Sx, Sxx, Sy, Syy on the int8 tensor cores
         per_launch = per_ps * units
         peak = peaks["dmma_tflops"]
         achieved = per_launch / (launch_ms / 1e3) / 1e12
         desc = f"{per_ps:g} FP64 flops"
+        if test == "pearson" and per_ps == 2.0:
+            desc += " (Sxy on DMMA; masked moments on int8 tcgen05: roofline_moments)"
     else:
         per_launch = per_ps * units
         peak = peaks["smem_gbs"]
@@ -512,6 +537,7 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
     torch.cuda.synchronize()
     lib.ps_profile_enable(1)
     _lib.profile_collect(ROOF[test][3])
+    _lib.profile_collect("pearson_moments")
     lib.ps_reset_kernel_launches()
     if clocks is not None:
         clocks.mark()
@@ -545,7 +571,15 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
         total_ms, kern_ms = reduce_max([total_ms, kern_ms])
     del outs, adj_outs, flush, shard_a, shard_b
     torch.cuda.empty_cache()
-    return total_ms / steps, roofline(wl, kern_ms, kern_n, steps, world, peaks), launches, clk
+    roof = roofline(wl, kern_ms, kern_n, steps, world, peaks)
+    if test == "pearson" and roof is not None:
+        mom_ms, mom_n = _lib.profile_collect_union("pearson_moments")
+        if world > 1:
+            mom_ms = reduce_max([mom_ms])[0]
+        rm = roofline_moments(wl, mom_ms, mom_n, steps, world, peaks)
+        if rm is not None:
+            roof["moments"] = rm
+    return total_ms / steps, roof, launches, clk
 
 
 def measure_e2e(wl: Workload, steps: int, warmup: int, world: int):

@@ -62,6 +62,7 @@ EXPORTED = (
     "ps_profile_collect",
     "ps_profile_collect_union",
     "ps_presort_layout",
+    "ps_pearson_moments_used",
     "ps_matrix_attach_presort",
     "ps_matrix_presort_rows",
     "ps_matrix_presort_done",
@@ -157,6 +158,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     ]
     lib.ps_kernel_launches.restype = ctypes.c_int64
     lib.ps_presort_layout.argtypes = [i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    lib.ps_pearson_moments_used.argtypes = [i64, i64]
     lib.ps_matrix_attach_presort.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.ps_matrix_presort_rows.argtypes = [vp, i64, i64, vp]
     lib.ps_matrix_presort_done.argtypes = [vp, vp]

@@ -68,6 +68,11 @@ struct ps_matrix {
 
 // true when the matrix carries presort chunk marks some of which are still
 // pending on the device (the walks can then overlap the presort)
+// Pearson moments Sx = X' M^T and Sxx = X'^2 M^T on the int8 tensor cores
+// (ps_moments.cu): rows / columns [lo, F) of two F x F fp64 matrices (freed
+// by the caller); ps_moments_on: the large-F Pearson path uses them
+bool ps_moments_on(int64_t F, int64_t S);
+int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx, double** sq, cudaStream_t s);
 // true when the Spearman walk streams g's order (large S): d_ordgid is built
 bool ps_spearman_streams_g(int64_t S);
 // tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits

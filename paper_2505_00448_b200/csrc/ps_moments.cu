@@ -1,0 +1,344 @@
+// ps_moments.cu -- the masked first and second moments of every feature pair
+// as int8 tensor-core contractions (Pearson, large F).
+//
+// The Pearson moment contraction (ps_pearson.cu) needs five sums per pair
+// (engine.py:145-166, continuous.py:29-103):
+//     Sxy = X' X'^T,  Sx = X' M^T,  Sxx = X'^2 M^T,  Sy = Sx^T,  Syy = Sxx^T
+// over x' = x - c_f (0 where missing) and the 0/1 presence M.  Only Sxy needs
+// the FP64 tensor path.  The four others have a 0/1 operand, so they are
+// computed EXACTLY on the int8 tensor cores (tcgen05.mma kind::i8) from a
+// fixed-point digit expansion of each row:
+//     x = 2^(e_f + 1) * sum_{s=1..7} d_s 2^(-7 s),   d_s in [-64, 64]
+// (e_f: max |x| < 2^e_f over row f; u = rint(x 2^(48 - e_f)) split into
+// balanced base-128 digits), so that
+//     Sx(i, j) = 2^(e_i + 1) sum_s 2^(-7 s) (D_s M^T)(i, j),
+// each D_s M^T an exact int32 contraction (|.| <= 64 S).  The digit products
+// are folded into the fp64 result in a fixed order (s = 7 .. 1), so Sx and
+// Sxx are bitwise identical for any launch range or device count.  The only
+// approximation is the expansion itself: |x - expansion| <= 2^(e_f - 49), i.e.
+// a relative error below 2^-48 of the row's largest value per term -- far
+// below the FP64 summation error of the DMMA contraction it replaces.  Sxx
+// uses the same expansion of the fp64 products x'^2 (the DMUL of the DMMA
+// path).  The DMMA tile kernel then runs Sxy alone (one product instead of
+// five) and reads the four moments in its epilogue.
+//
+// Algorithmic work: 7 digits x 2 moments x 2 int8 ops per (ordered) pair-sample.
+#include "ps_internal.cuh"
+#include "ps_tc05.cuh"
+#include <cudaTypedefs.h>
+#include <algorithm>
+
+namespace {
+
+constexpr int kDigits = 7;
+constexpr int QM = 256, QN = 256, QKB = 128;  // tile rows, cols, K bytes per stage
+constexpr int QSTAGES = 3;
+constexpr int QA_BYTES = QM * QKB, QB_BYTES = QN * QKB;
+constexpr int QSTAGE_BYTES = QA_BYTES + QB_BYTES;
+constexpr size_t kMomSmem = (size_t)QSTAGES * QSTAGE_BYTES + 1024;
+constexpr int QTH = 192;  // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int32_t kNonFinite = 0x7FFFFFFF;  // row exponent of a row holding NaN / inf: its moments are NaN
+
+// per-row exponents: max |x'| < 2^e1, max x'^2 < 2^e2 (frexp; 0 for an all-zero row)
+__global__ void moment_scale_kernel(const double* __restrict__ xc, int64_t ld, int64_t S, int64_t f0,
+                                    int32_t* __restrict__ e1, int32_t* __restrict__ e2) {
+  const int64_t f = f0 + blockIdx.x;
+  const double* row = xc + f * ld;
+  double m = 0.0;
+  int bad = 0;
+  for (int64_t s = threadIdx.x; s < S; s += blockDim.x) {
+    const double x = row[s];
+    bad |= !isfinite(x);
+    m = fmax(m, fabs(x));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(PS_FULL, m, o));
+  bad = __syncthreads_or(bad);
+  __shared__ double wm[32];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wm[w]);
+    m = fmax(m, wm[0]);
+    int a = 0, b = 0;
+    if (m > 0.0) {
+      frexp(m, &a);
+      frexp(m * m, &b);  // the rounded square bounds every rounded x'^2 of the row
+    }
+    // (x'^2 overflowing to inf is non-finite for the FP64 path as well)
+    if (bad || isinf(m * m)) a = b = kNonFinite;
+    e1[f] = a;
+    e2[f] = b;
+  }
+}
+
+// digit `digit` (1 = most significant) of every x' (or x'^2) of rows
+// [f0, f0 + gridDim.x) as int8, zero past S; 16 samples per thread
+__global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, int64_t S, int64_t Sp,
+                                    const int32_t* __restrict__ rexp, int digit, int square, int64_t f0,
+                                    int8_t* __restrict__ out) {
+  const int64_t f = f0 + blockIdx.x;
+  const double* row = xc + f * ld;
+  const int e = rexp[f];
+  const bool zero = e == kNonFinite;  // (its moments are written as NaN)
+  const int shift = 48 - e;  // u = rint(x 2^(48 - e)) = rint(v 2^49), v = x / 2^(e + 1)
+  const int drop = 7 * (kDigits - digit);
+  for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t s = s0 + q;
+      int d = 0;
+      if (s < S && !zero) {
+        double x = row[s];
+        if (square) x = x * x;
+        long long u = __double2ll_rn(ldexp(x, shift));
+        // balanced base-128 digits from the least significant one up
+        for (int t = 0; t < drop; t += 7) {
+          const long long lo = ((u + 64) & 127) - 64;
+          u = (u - lo) >> 7;
+        }
+        d = digit == 1 ? (int)u : (int)(((u + 64) & 127) - 64);
+      }
+      w[q >> 2] |= (uint32_t)(uint8_t)(int8_t)d << (8 * (q & 3));
+    }
+    *reinterpret_cast<uint4*>(out + f * Sp + s0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// presence as int8 0/1 (F x Sp), zero past S
+__global__ void presence_i8_kernel(const uint32_t* __restrict__ mask, int64_t W, int64_t S, int64_t Sp,
+                                   int8_t* __restrict__ out) {
+  const int64_t f = blockIdx.x;
+  for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    const int64_t wi = s0 >> 5;
+    const uint32_t bits = (wi < W ? mask[f * W + wi] : 0u) >> (s0 & 31);
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (s0 + q < S && ((bits >> q) & 1u)) w[q >> 2] |= 1u << (8 * (q & 3));
+    *reinterpret_cast<uint4*>(out + f * Sp + s0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// out(i, j) (+)= 2^(e_i + 1 - 7 digit) (D M^T)(i, j) over the tiles of rows
+// [I0, I0 + nI) x columns [J0, J0 + nJ) (256 x 256 each; rows / columns past F
+// are zero-filled by TMA and not written).  One persistent CTA per SM takes
+// tiles round-robin; each tile runs the whole K range (no split: the int32
+// tile is exact and folded once).  Warp roles as the contingency GEMM
+// (ps_chi2.cu): TMA producer, single-thread MMA issuer, four epilogue warps
+// draining the two 128 x 256 TMEM accumulators.
+__global__ void __launch_bounds__(QTH, 1)
+moment_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int nk,
+                   int64_t I0, int64_t nI, int64_t J0, int64_t nJ, const int32_t* __restrict__ rexp, int digit,
+                   int first, double* __restrict__ out, int64_t F) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[QSTAGES], empty[QSTAGES], accfull, accempty;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t ntiles = nI * nJ;
+
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
+  if (tid == 32) {
+    for (int i = 0; i < QSTAGES; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], 1);
+    }
+    tc05::mbar_init(&accfull, 1);
+    tc05::mbar_init(&accempty, 128);
+    tc05::fence_barrier_init();
+  }
+  if (tid == 4 * 32) {
+    tc05::prefetch_tmap(&amap);
+    tc05::prefetch_tmap(&bmap);
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::fence_after_sync();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      int64_t q = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int I = (int)(I0 + t / nJ), J = (int)(J0 + t % nJ);
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
+          const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+          tc05::mbar_arrive_expect_tx(&full[st], QSTAGE_BYTES);
+          tc05::tma_load_2d(sa, &amap, kc * QKB, I * QM, &full[st]);
+          tc05::tma_load_2d(sb, &bmap, kc * QKB, J * QN, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc05::idesc_i8(128, QN, true);
+      int64_t q = 0;
+      int seg = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++seg) {
+        if (seg > 0) {  // the epilogue has drained the previous tile
+          tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
+          tc05::fence_after_sync();
+          const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < QKB / 32; ++kk) {
+            const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+            const uint32_t acc = (kc > 0 || kk > 0) ? 1u : 0u;
+            tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+            tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * QKB + kk * 32), bd, idesc, acc);
+          }
+          tc05::commit(&empty[st]);
+        }
+        tc05::commit(&accfull);
+      }
+    }
+  } else {
+    // epilogue warps 0-3: TMEM lanes 32 w .. 32 w + 31 = tile rows
+    int seg = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++seg) {
+      const int64_t I = I0 + t / nJ, J = J0 + t % nJ;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int64_t r = I * QM + half * 128 + warp * 32 + lane;
+        const bool rok = r < F;
+        const int ex = rok ? rexp[r] : 0;
+        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+        double* orow = out + (rok ? r : 0) * F;
+#pragma unroll 1
+        for (int cc = 0; cc < QN / 32; ++cc) {
+          uint32_t v[32];
+          tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+          const int64_t c0 = J * QN + cc * 32;
+          if (rok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int64_t c = c0 + j;
+              if (c < F) {
+                const double term = (double)(int32_t)v[j] * scale;
+                orow[c] = first ? term : orow[c] + term;
+              }
+            }
+          }
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive(&accempty);
+    }
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc05::tmem_dealloc(tmem, 512);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 moment_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// K-major int8 rows (F x Sp bytes), 128-byte x 256-row boxes, SWIZZLE_128B
+int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp) {
+  auto enc = moment_map_encoder();
+  if (!enc) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)Sp, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)Sp};
+  cuuint32_t box[2] = {(cuuint32_t)QKB, (cuuint32_t)QM};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return ps_fail(PS_ERR_CUDA, "moment operand tensor map");
+  return PS_OK;
+}
+
+}  // namespace
+
+bool ps_moments_on(int64_t F, int64_t S) {
+  if (const char* e = getenv("PS_PEARSON_MOMENTS")) return e[0] == '1';
+  return F >= 2048 && S >= 256;
+}
+
+int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx_out, double** sq_out,
+                       cudaStream_t s) {
+  *sx_out = *sq_out = nullptr;
+  const int64_t F = a->F, S = a->S;
+  lo = std::max<int64_t>(0, std::min<int64_t>(lo, F));
+  ps_device_state* ds = ps_state();
+  const int64_t Sp = ps_round_up(std::max<int64_t>(S, 1), QKB);
+  const int nk = (int)(Sp / QKB);
+  double *sx = nullptr, *sq = nullptr;
+  int8_t *dig = nullptr, *pres = nullptr;
+  int32_t *e1 = nullptr, *e2 = nullptr;
+  auto cleanup = [&]() {
+    ps_free(dig, s);
+    ps_free(pres, s);
+    ps_free(e1, s);
+    ps_free(e2, s);
+  };
+  cudaError_t e = ps_alloc(&sx, (size_t)(F * F), s);
+  if (e == cudaSuccess) e = ps_alloc(&sq, (size_t)(F * F), s);
+  if (e == cudaSuccess) e = ps_alloc(&dig, (size_t)(F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&pres, (size_t)(F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&e1, (size_t)F, s);
+  if (e == cudaSuccess) e = ps_alloc(&e2, (size_t)F, s);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kMomSmem);
+  if (e != cudaSuccess) {
+    cleanup();
+    ps_free(sx, s);
+    ps_free(sq, s);
+    return ps_cuda_check(e, "pearson moments setup");
+  }
+  // rows and columns [lo, F): every (g, h) and (h, g) with g in [lo, hi), h >= g
+  // (tile-aligned down: rows [r0, lo) are computed as well, unused)
+  const int64_t I0 = lo / QM, nI = ps_ceil_div(F, QM) - I0;
+  const int64_t J0 = lo / QN, nJ = ps_ceil_div(F, QN) - J0;
+  const int64_t r0 = I0 * QM, nrows = F - r0;
+  moment_scale_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, r0, e1, e2);
+  PS_LAUNCHED();
+  presence_i8_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, a->W, S, Sp, pres);
+  PS_LAUNCHED();
+  CUtensorMap amap, bmap;
+  int rc = make_i8_map(&amap, dig, F, Sp);
+  if (!rc) rc = make_i8_map(&bmap, pres, F, Sp);
+  if (rc) {
+    cleanup();
+    ps_free(sx, s);
+    ps_free(sq, s);
+    return rc;
+  }
+  const int grid = (int)std::min<int64_t>(nI * nJ, ds->num_sms);
+  ps_prof_begin("pearson_moments", s);
+  for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
+    double* out = sq_pass ? sq : sx;
+    const int32_t* ex = sq_pass ? e2 : e1;
+    for (int d = kDigits; d >= 1; --d) {  // least significant digit first (fixed fold order)
+      moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, d, sq_pass, r0, dig);
+      PS_LAUNCHED();
+      moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap, bmap, nk, I0, nI, J0, nJ, ex, d, d == kDigits ? 1 : 0, out,
+                                                     F);
+      PS_LAUNCHED();
+    }
+  }
+  ps_prof_end(s);
+  cleanup();
+  *sx_out = sx;
+  *sq_out = sq;
+  return PS_OK;
+}

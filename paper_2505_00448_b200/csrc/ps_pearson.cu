@@ -387,9 +387,14 @@ __device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
   return v;
 }
 
+// PRE: the first / second moments come precomputed (ps_moments.cu: msx = X' M^T,
+// msq = X'^2 M^T, F x F): the tiles run Sxy = X' X'^T alone -- one DMMA per
+// fragment pair instead of five -- plus the pair counts
+template <bool PRE>
 __global__ void __launch_bounds__(NTHR, 1)
 pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ mpad, int64_t Wp,
-                   int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
+                   int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor,
+                   const double* __restrict__ msx, const double* __restrict__ msq) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TNS], empty[TNS];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -480,29 +485,39 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __r
         const int ks = h * 32 + k;     // sample within the stage
         const uint32_t bi = a + (uint32_t)(ks / TBOX) * TBOX_BYTES;
         const uint32_t bj = a + (uint32_t)(TNB + ks / TBOX) * TBOX_BYTES;
-        double xa[WM], ma[WM], xa2[WM], xb[WN], mb[WN], xb2[WN];
+        double xa[WM], xb[WN];
 #pragma unroll
-        for (int q = 0; q < WM; ++q) {
-          xa[q] = ld_sw(bi, wi * 8 * WM + q * 8 + fr, ks % TBOX);
-          ma[q] = ((mrow[q] >> k) & 1u) ? 1.0 : 0.0;
-          xa2[q] = xa[q] * xa[q];
-        }
+        for (int q = 0; q < WM; ++q) xa[q] = ld_sw(bi, wi * 8 * WM + q * 8 + fr, ks % TBOX);
 #pragma unroll
-        for (int q = 0; q < WN; ++q) {
-          xb[q] = ld_sw(bj, wj * 8 * WN + q * 8 + fr, ks % TBOX);
-          mb[q] = ((mcol[q] >> k) & 1u) ? 1.0 : 0.0;
-          xb2[q] = xb[q] * xb[q];
-        }
+        for (int q = 0; q < WN; ++q) xb[q] = ld_sw(bj, wj * 8 * WN + q * 8 + fr, ks % TBOX);
+        if constexpr (PRE) {
 #pragma unroll
-        for (int i = 0; i < WM; ++i)
+          for (int i = 0; i < WM; ++i)
 #pragma unroll
-          for (int j = 0; j < WN; ++j) {
-            dmma(axy[i][j][0], axy[i][j][1], xa[i], xb[j]);
-            dmma(asx[i][j][0], asx[i][j][1], xa[i], mb[j]);
-            dmma(asxx[i][j][0], asxx[i][j][1], xa2[i], mb[j]);
-            dmma(asy[i][j][0], asy[i][j][1], ma[i], xb[j]);
-            dmma(asyy[i][j][0], asyy[i][j][1], ma[i], xb2[j]);
+            for (int j = 0; j < WN; ++j) dmma(axy[i][j][0], axy[i][j][1], xa[i], xb[j]);
+        } else {
+          double ma[WM], xa2[WM], mb[WN], xb2[WN];
+#pragma unroll
+          for (int q = 0; q < WM; ++q) {
+            ma[q] = ((mrow[q] >> k) & 1u) ? 1.0 : 0.0;
+            xa2[q] = xa[q] * xa[q];
           }
+#pragma unroll
+          for (int q = 0; q < WN; ++q) {
+            mb[q] = ((mcol[q] >> k) & 1u) ? 1.0 : 0.0;
+            xb2[q] = xb[q] * xb[q];
+          }
+#pragma unroll
+          for (int i = 0; i < WM; ++i)
+#pragma unroll
+            for (int j = 0; j < WN; ++j) {
+              dmma(axy[i][j][0], axy[i][j][1], xa[i], xb[j]);
+              dmma(asx[i][j][0], asx[i][j][1], xa[i], mb[j]);
+              dmma(asxx[i][j][0], asxx[i][j][1], xa2[i], mb[j]);
+              dmma(asy[i][j][0], asy[i][j][1], ma[i], xb[j]);
+              dmma(asyy[i][j][0], asyy[i][j][1], ma[i], xb2[j]);
+            }
+        }
       }
 #pragma unroll
       for (int i = 0; i < WM; ++i) {
@@ -526,8 +541,12 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __r
         const int64_t gg = row0 + wi * 8 * WM + i * 8 + fr;
         const int64_t hh = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
         if (gg < lo || gg >= hi || hh < gg || hh >= F) continue;
-        pearson_finish(gg, hh, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e], asyy[i][j][e],
-                       axy[i][j][e], o);
+        if constexpr (PRE)
+          pearson_finish(gg, hh, F, an[i][j][e], msx[gg * F + hh], msx[hh * F + gg], msq[gg * F + hh],
+                         msq[hh * F + gg], axy[i][j][e], o);
+        else
+          pearson_finish(gg, hh, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e], asyy[i][j][e],
+                         axy[i][j][e], o);
       }
 }
 
@@ -788,11 +807,27 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     CUtensorMap xmap;
     int rc = make_pearson_map(&xmap, xc, a->ld, F);
     if (rc) return rc;
-    PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    // large F: the four masked moments on the int8 tensor cores, Sxy alone on DMMA
+    double *msx = nullptr, *msq = nullptr;
+    if (ps_moments_on(F, a->S)) {
+      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, s);
+      if (rc) return rc;
+    }
+    PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTmaSmem));
+    PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kTmaSmem));
     ps_prof_begin("pearson_tile", s);
-    pearson_tma_kernel<<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
+    if (msx)
+      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
+                                                                      msx, msq);
+    else
+      pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
+                                                                       nullptr, nullptr);
     ps_prof_end(s);
     PS_LAUNCHED();
+    ps_free(msx, s);
+    ps_free(msq, s);
   } else {
     ps_prof_begin("pearson_tile", s);
     launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT,
@@ -842,6 +877,9 @@ struct ps_pearson_job {
   CUtensorMap xmap{};
   double* xc = nullptr;    // pre-centred x' (mode >= 1)
   double* xq = nullptr;    // x'^2 (mode 2)
+  bool moments = false;    // large F: moments on the int8 tensor cores, all tiles after the upload
+  double* msx = nullptr;
+  double* msq = nullptr;
   int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
   int nws = 0;
@@ -870,7 +908,12 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
     j->Wp = ps_round_up(a->W, 4);
     e = ps_alloc(&j->mpad, (size_t)(F * j->Wp), s);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(pearson_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+      e = cudaFuncSetAttribute(pearson_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kTmaSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kTmaSmem);
+    j->moments = ps_moments_on(F, a->S);
     if (e == cudaSuccess && make_pearson_map(&j->xmap, j->xc, a->ld, F) != PS_OK)
       e = cudaErrorInvalidValue;
   }
@@ -912,9 +955,12 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
-  if (j->tma)
-    pearson_tma_kernel<<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F, j->o,
-                                                                   1);
+  if (j->tma && j->msx)
+    pearson_tma_kernel<true><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
+                                                                         j->o, 1, j->msx, j->msq);
+  else if (j->tma)
+    pearson_tma_kernel<false><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
+                                                                          j->o, 1, nullptr, nullptr);
   else
     launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
                  a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
@@ -929,6 +975,7 @@ int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
   if (J1 <= j->J_done) return PS_OK;
   int rc0 = pearson_center_upto(j, J1 * T, s);
   if (rc0) return rc0;
+  if (j->moments) return PS_OK;  // every tile waits for the moments of all rows (ps_pearson_end)
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = pearson_columns(j, j->J_done, J1, w);
   j->J_done = J1;
@@ -940,6 +987,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
   if (!rc) rc = pearson_center_upto(j, a->F, s);
+  if (!rc && j->moments) rc = ps_pearson_moments(a, j->xc, 0, &j->msx, &j->msq, s);
   if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
   if (!rc && j->o.defer_p) {
     pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
@@ -957,6 +1005,8 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
   ps_free(j->mpad, j->home);
+  ps_free(j->msx, j->home);
+  ps_free(j->msq, j->home);
   delete j;
   return rc;
 }
@@ -970,5 +1020,7 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
   ps_free(j->mpad, j->home);
+  ps_free(j->msx, j->home);
+  ps_free(j->msq, j->home);
   delete j;
 }

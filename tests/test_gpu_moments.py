@@ -1,0 +1,111 @@
+"""Pearson with the masked moments on the int8 tensor cores (ps_moments.cu).
+
+Large-F Pearson computes Sx = X' M^T and Sxx = X'^2 M^T from exact int8 digit
+contractions and runs only Sxy on the FP64 tensor path.  These tests force the
+path on (PS_PEARSON_MOMENTS=1) at oracle-sized shapes and check it against the
+CPU oracle (continuous.py:29-103) at the north-star tolerances, against the
+FP64-moment path, on degenerate rows (constants, large offsets, NaN data under
+a numeric sentinel, all-missing rows), and bit-for-bit across launch ranges.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import bitwise_equal, p_close, same_nan
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+import paper_2505_00448_b200 as ps
+from paper_2505_00448_b200 import blocks
+
+
+def _check(res, ref):
+    for name in ("stat", "p"):
+        assert same_nan(res[name], ref[name]), name
+    r, rr = res["stat"], ref["stat"]
+    m = ~np.isnan(rr)
+    assert np.all(np.abs(r[m] - rr[m]) <= 1e-9 * np.maximum(np.abs(rr[m]), 1e-3))
+    assert p_close(res["p"], ref["p"])
+
+
+@pytest.mark.parametrize("na", [0.0, 0.3])
+@pytest.mark.parametrize("F,S", [(70, 333), (300, 1000), (260, 5000)])
+def test_moments_match_oracle(oracle, monkeypatch, F, S, na):
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    raw = workloads.simulate(F, S, "continuous", na_ratio=na, seed=F * 11 + S + int(na * 10))
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
+
+
+def test_moments_degenerate_rows(oracle, monkeypatch):
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    rng = np.random.default_rng(5)
+    raw = rng.normal(size=(40, 700))
+    raw[0] = 0.1                        # constant
+    raw[1] = 1e6 + rng.normal(size=700) * 1e-3   # large offset, small spread
+    raw[2, 3:] = np.nan                 # n = 3 with everyone
+    raw[3, :] = np.nan                  # all missing
+    raw[4] = raw[5] * 1e-200            # tiny scale
+    raw[6] = raw[7] * 1e150             # huge scale
+    raw[8] = -raw[9]
+    raw[10, rng.random(700) < 0.5] = np.nan
+    raw[11, ::7] = 1e4                  # outliers
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
+
+
+def test_moments_nan_data_raises_like_fp64_path(monkeypatch):
+    """NaN data under a numeric sentinel is present data: the reference's tail
+    raises NonConvergence; both moment paths must agree."""
+    raw = workloads.simulate(30, 300, "continuous", na_ratio=0.1, seed=9)
+    raw[4, 17] = np.nan
+    mat = ps.make_matrix(raw, "continuous", na_sentinel=workloads.SENTINEL)
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    outcomes = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PS_PEARSON_MOMENTS", flag)
+        try:
+            ps.run(req, mat)
+            outcomes.append("ok")
+        except ps.NonConvergence:
+            outcomes.append("NonConvergence")
+    assert outcomes[0] == outcomes[1]
+
+
+def test_moments_close_to_fp64_moments(monkeypatch):
+    raw = workloads.simulate(2100, 1500, "continuous", na_ratio=0.3, seed=21)
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "0")
+    a = ps.run(req, mat)
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    b = ps.run(req, mat)
+    assert same_nan(a["stat"], b["stat"])
+    m = ~np.isnan(a["stat"])
+    assert np.max(np.abs(a["stat"][m] - b["stat"][m])) <= 1e-12
+    assert p_close(b["p"], a["p"], rtol=1e-9)
+
+
+def test_moments_range_independent(monkeypatch):
+    """Block ranges compute the moments of rows / columns [lo, F) only: every
+    pair is bitwise identical to the whole-matrix launch."""
+    import torch
+
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    F, S = 600, 900
+    raw = workloads.simulate(F, S, "continuous", na_ratio=0.2, seed=4)
+    dm = blocks.DeviceMatrix(raw, "continuous", np.nan, None)
+    whole = [torch.full((F, F), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
+    blocks.block("pearson", dm, None, 0, F, whole)
+    parts = [torch.full((F, F), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
+    for lo, hi in ((0, 137), (137, 400), (400, F)):
+        blocks.block("pearson", dm, None, lo, hi, parts)
+    blocks.sync()
+    for w, p in zip(whole, parts):
+        assert bitwise_equal(w.cpu().numpy(), p.cpu().numpy())
+    dm.close()
