@@ -71,37 +71,42 @@ __global__ void moment_scale_kernel(const double* __restrict__ xc, int64_t ld, i
   }
 }
 
-// digit `digit` (1 = most significant) of every x' (or x'^2) of rows
-// [f0, f0 + gridDim.x) as int8, zero past S; 16 samples per thread
+// all kDigits digits of every x' (or x'^2) of rows [f0, f0 + gridDim.x) as
+// int8 planes out + (digit - 1) * plane (F x Sp each), zero past S; one pass
+// over the operand, 16 samples per thread
 __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, int64_t S, int64_t Sp,
-                                    const int32_t* __restrict__ rexp, int digit, int square, int64_t f0,
+                                    const int32_t* __restrict__ rexp, int square, int64_t f0, int64_t plane,
                                     int8_t* __restrict__ out) {
   const int64_t f = f0 + blockIdx.x;
   const double* row = xc + f * ld;
   const int e = rexp[f];
   const bool zero = e == kNonFinite;  // (its moments are written as NaN)
   const int shift = 48 - e;  // u = rint(x 2^(48 - e)) = rint(v 2^49), v = x / 2^(e + 1)
-  const int drop = 7 * (kDigits - digit);
   for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    uint32_t w[kDigits][4];
+#pragma unroll
+    for (int d = 0; d < kDigits; ++d) w[d][0] = w[d][1] = w[d][2] = w[d][3] = 0u;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int64_t s = s0 + q;
-      int d = 0;
       if (s < S && !zero) {
         double x = row[s];
         if (square) x = x * x;
         long long u = __double2ll_rn(ldexp(x, shift));
-        // balanced base-128 digits from the least significant one up
-        for (int t = 0; t < drop; t += 7) {
+        // balanced base-128 digits from the least significant one up; the
+        // most significant is what remains (|.| <= 64)
+#pragma unroll
+        for (int d = kDigits - 1; d >= 1; --d) {
           const long long lo = ((u + 64) & 127) - 64;
           u = (u - lo) >> 7;
+          w[d][q >> 2] |= (uint32_t)(uint8_t)(int8_t)lo << (8 * (q & 3));
         }
-        d = digit == 1 ? (int)u : (int)(((u + 64) & 127) - 64);
+        w[0][q >> 2] |= (uint32_t)(uint8_t)(int8_t)u << (8 * (q & 3));
       }
-      w[q >> 2] |= (uint32_t)(uint8_t)(int8_t)d << (8 * (q & 3));
     }
-    *reinterpret_cast<uint4*>(out + f * Sp + s0) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int d = 0; d < kDigits; ++d)
+      *reinterpret_cast<uint4*>(out + d * plane + f * Sp + s0) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
   }
 }
 
@@ -293,7 +298,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   };
   cudaError_t e = ps_alloc(&sx, (size_t)(F * F), s);
   if (e == cudaSuccess) e = ps_alloc(&sq, (size_t)(F * F), s);
-  if (e == cudaSuccess) e = ps_alloc(&dig, (size_t)(F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&dig, (size_t)(kDigits * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&pres, (size_t)(F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&e1, (size_t)F, s);
   if (e == cudaSuccess) e = ps_alloc(&e2, (size_t)F, s);
@@ -314,9 +319,9 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   PS_LAUNCHED();
   presence_i8_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, a->W, S, Sp, pres);
   PS_LAUNCHED();
-  CUtensorMap amap, bmap;
-  int rc = make_i8_map(&amap, dig, F, Sp);
-  if (!rc) rc = make_i8_map(&bmap, pres, F, Sp);
+  CUtensorMap amap[kDigits], bmap;
+  int rc = make_i8_map(&bmap, pres, F, Sp);
+  for (int d = 0; d < kDigits && !rc; ++d) rc = make_i8_map(&amap[d], dig + d * F * Sp, F, Sp);
   if (rc) {
     cleanup();
     ps_free(sx, s);
@@ -328,11 +333,11 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
     double* out = sq_pass ? sq : sx;
     const int32_t* ex = sq_pass ? e2 : e1;
+    moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, sq_pass, r0, F * Sp, dig);
+    PS_LAUNCHED();
     for (int d = kDigits; d >= 1; --d) {  // least significant digit first (fixed fold order)
-      moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, d, sq_pass, r0, dig);
-      PS_LAUNCHED();
-      moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap, bmap, nk, I0, nI, J0, nJ, ex, d, d == kDigits ? 1 : 0, out,
-                                                     F);
+      moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, I0, nI, J0, nJ, ex, d,
+                                                     d == kDigits ? 1 : 0, out, F);
       PS_LAUNCHED();
     }
   }

@@ -120,11 +120,19 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
 // inside the one-CTA-per-SM tile kernel, where the DMMA pipe idled meanwhile.
 __global__ void pearson_p_kernel(const double* __restrict__ stat, double* __restrict__ pout, int64_t F, int64_t lo,
                                  int64_t hi, int* __restrict__ err) {
-  const int64_t rows = hi - lo;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < rows * F;
+  // cells enumerated over the upper triangle only (no idle threads):
+  // before(g) = cells of rows [lo, g)
+  auto before = [&](int64_t g) { return (g - lo) * F - (g * (g - 1) - lo * (lo - 1)) / 2; };
+  const int64_t total = before(hi);
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
        it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = lo + it / F, h = it % F;
-    if (h < g) continue;
+    int64_t a = lo, b = hi - 1;  // last row g with before(g) <= it
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (before(mid) <= it) a = mid;
+      else b = mid - 1;
+    }
+    const int64_t g = a, h = g + (it - before(g));
     const double fn = pout[g * F + h];
     if (fn != fn) continue;
     const double r = stat[g * F + h];
