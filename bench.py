@@ -394,16 +394,16 @@ def moments_used(wl: Workload) -> bool:
 
 def roofline_moments(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):
     """The int8 moment contractions of large-F Pearson (ps_moments.cu): 2 moments
-    x 7 digits x 2 ops per ORDERED pair-sample, digit expansion included."""
+    x 8 digits x 2 ops per ORDERED pair-sample, digit expansion included."""
     if not kern_n:
         return None
     launch_ms = kern_ms / steps
-    ops = 2 * 7 * 2.0 * wl.Fa * wl.Fa * wl.S / world
+    ops = 2 * 8 * 2.0 * wl.Fa * wl.Fa * wl.S / world
     achieved = ops / (launch_ms / 1e3) / 1e12
     peak = peaks["tcgen05_i8_tops"]
     return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS", "frac": achieved / peak,
             "kernel": "pearson_moments", "launch_ms": launch_ms, "launches_per_step": kern_n / steps,
-            "work_per_ordered_pair_sample": "28 int8 ops (tcgen05 kind::i8, 7-digit expansion of x' and x'^2)"}
+            "work_per_ordered_pair_sample": "32 int8 ops (tcgen05 kind::i8, 8-digit expansion of x' and x'^2)"}
 
 
 def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):

@@ -72,7 +72,10 @@ struct ps_matrix {
 // (ps_moments.cu): rows / columns [lo, F) of two F x F fp64 matrices (freed
 // by the caller); ps_moments_on: the large-F Pearson path uses them
 bool ps_moments_on(int64_t F, int64_t S);
-int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx, double** sq, cudaStream_t s);
+// digits of the expansion: each expanded term is within 2^(e - 7 kMomentDigits) of x'
+constexpr int kMomentDigits = 8;
+int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx, double** sq, int32_t** e1,
+                       int32_t** e2, cudaStream_t s);
 // true when the Spearman walk streams g's order (large S): d_ordgid is built
 bool ps_spearman_streams_g(int64_t S);
 // tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits

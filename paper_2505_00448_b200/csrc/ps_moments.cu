@@ -8,21 +8,21 @@
 // the FP64 tensor path.  The four others have a 0/1 operand, so they are
 // computed EXACTLY on the int8 tensor cores (tcgen05.mma kind::i8) from a
 // fixed-point digit expansion of each row:
-//     x = 2^(e_f + 1) * sum_{s=1..7} d_s 2^(-7 s),   d_s in [-64, 64]
-// (e_f: max |x| < 2^e_f over row f; u = rint(x 2^(48 - e_f)) split into
+//     x = 2^(e_f + 1) * sum_{s=1..8} d_s 2^(-7 s),   d_s in [-64, 64]
+// (e_f: max |x| < 2^e_f over row f; u = rint(x 2^(55 - e_f)) split into
 // balanced base-128 digits), so that
 //     Sx(i, j) = 2^(e_i + 1) sum_s 2^(-7 s) (D_s M^T)(i, j),
 // each D_s M^T an exact int32 contraction (|.| <= 64 S).  The digit products
-// are folded into the fp64 result in a fixed order (s = 7 .. 1), so Sx and
+// are folded into the fp64 result in a fixed order (s = 8 .. 1), so Sx and
 // Sxx are bitwise identical for any launch range or device count.  The only
-// approximation is the expansion itself: |x - expansion| <= 2^(e_f - 49), i.e.
-// a relative error below 2^-48 of the row's largest value per term -- far
+// approximation is the expansion itself: |x - expansion| <= 2^(e_f - 56), i.e.
+// a relative error below 2^-55 of the row's largest value per term -- far
 // below the FP64 summation error of the DMMA contraction it replaces.  Sxx
 // uses the same expansion of the fp64 products x'^2 (the DMUL of the DMMA
 // path).  The DMMA tile kernel then runs Sxy alone (one product instead of
 // five) and reads the four moments in its epilogue.
 //
-// Algorithmic work: 7 digits x 2 moments x 2 int8 ops per (ordered) pair-sample.
+// Algorithmic work: 8 digits x 2 moments x 2 int8 ops per (ordered) pair-sample.
 #include "ps_internal.cuh"
 #include "ps_tc05.cuh"
 #include <cudaTypedefs.h>
@@ -30,7 +30,7 @@
 
 namespace {
 
-constexpr int kDigits = 7;
+constexpr int kDigits = kMomentDigits;
 constexpr int QM = 256, QN = 256, QKB = 128;  // tile rows, cols, K bytes per stage
 constexpr int QSTAGES = 3;
 constexpr int QA_BYTES = QM * QKB, QB_BYTES = QN * QKB;
@@ -81,7 +81,7 @@ __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, i
   const double* row = xc + f * ld;
   const int e = rexp[f];
   const bool zero = e == kNonFinite;  // (its moments are written as NaN)
-  const int shift = 48 - e;  // u = rint(x 2^(48 - e)) = rint(v 2^49), v = x / 2^(e + 1)
+  const int shift = 7 * kDigits - 1 - e;  // u = rint(v 2^(7 kDigits)), v = x / 2^(e + 1): |u| < 2^(7 kDigits - 1)
   for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
     uint32_t w[kDigits][4];
 #pragma unroll
@@ -280,8 +280,9 @@ bool ps_moments_on(int64_t F, int64_t S) {
 }
 
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx_out, double** sq_out,
-                       cudaStream_t s) {
+                       int32_t** e1_out, int32_t** e2_out, cudaStream_t s) {
   *sx_out = *sq_out = nullptr;
+  *e1_out = *e2_out = nullptr;
   const int64_t F = a->F, S = a->S;
   lo = std::max<int64_t>(0, std::min<int64_t>(lo, F));
   ps_device_state* ds = ps_state();
@@ -293,8 +294,6 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   auto cleanup = [&]() {
     ps_free(dig, s);
     ps_free(pres, s);
-    ps_free(e1, s);
-    ps_free(e2, s);
   };
   cudaError_t e = ps_alloc(&sx, (size_t)(F * F), s);
   if (e == cudaSuccess) e = ps_alloc(&sq, (size_t)(F * F), s);
@@ -308,6 +307,8 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     cleanup();
     ps_free(sx, s);
     ps_free(sq, s);
+    ps_free(e1, s);
+    ps_free(e2, s);
     return ps_cuda_check(e, "pearson moments setup");
   }
   // rows and columns [lo, F): every (g, h) and (h, g) with g in [lo, hi), h >= g
@@ -326,6 +327,8 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     cleanup();
     ps_free(sx, s);
     ps_free(sq, s);
+    ps_free(e1, s);
+    ps_free(e2, s);
     return rc;
   }
   const int grid = (int)std::min<int64_t>(nI * nJ, ds->num_sms);
@@ -345,5 +348,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   cleanup();
   *sx_out = sx;
   *sq_out = sq;
+  *e1_out = e1;
+  *e2_out = e2;
   return PS_OK;
 }

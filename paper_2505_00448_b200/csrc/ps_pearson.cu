@@ -80,6 +80,34 @@ __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, 
   }
 }
 
+// Exact replay of the pair (g, h): the replay kernel writes it.
+__device__ __forceinline__ void replay_pair(int64_t g, int64_t h, int64_t F, const Outs& o) {
+  int slot = atomicAdd(o.replay_count, 1);
+  if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
+  if (o.defer_p) put(o.p, F, g, h, PS_NAN);  // not a parked n: pearson_p_kernel skips it
+}
+
+// Digit-expansion moments (ps_moments.cu) carry a rigorous error bound: each
+// expanded term is within 2^(e - 7 D) of x' (D = kMomentDigits; e: the row
+// exponent of x', resp. x'^2), so |dSx| <= n 2^(e1 - 7 D), |dSxx| <= n 2^(e2 - 7 D) (+ the fp64 fold,
+// 8 ulp).  A pair whose centred sums could move by more than 1e-12 of
+// themselves (an outlier-dominated row exponent, a subset far smaller than the
+// row's scale) is replayed exactly instead -- data-independent parity.
+__device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, double qx, double qy, int e1g,
+                                                  int e2g, int e1h, int e2h) {
+  if (n <= 1) return false;
+  const double fn = (double)n;
+  constexpr int kB = 7 * kMomentDigits - 2;  // 4x the bound
+  const double d1g = ldexp(1.0, e1g - kB), d2g = ldexp(1.0, e2g - kB);
+  const double d1h = ldexp(1.0, e1h - kB), d2h = ldexp(1.0, e2h - kB);
+  const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
+  if (!(sxx > 0.0) || !(syy > 0.0)) return false;  // the degenerate-variance rule replays it anyway
+  const double exx = fn * d2g + 2.0 * fabs(sx) * d1g + 1e-15 * qx;
+  const double eyy = fn * d2h + 2.0 * fabs(sy) * d1h + 1e-15 * qy;
+  const double exy = fabs(sy) * d1g + fabs(sx) * d1h;
+  return exx > 1e-12 * sxx || eyy > 1e-12 * syy || exy > 1e-12 * sqrt(sxx * syy);
+}
+
 // Moments -> outputs for one upper-triangular pair (g <= h).
 __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx, double sy,
                                double qx, double qy, double xy, const Outs& o) {
@@ -90,10 +118,8 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
     const double sxx = qx - sx * sx / fn;
     const double syy = diag ? sxx : qy - sy * sy / fn;
     if (!(sxx > kReplayTau * qx) || !(syy > kReplayTau * (diag ? qx : qy))) {
-      int slot = atomicAdd(o.replay_count, 1);
-      if (slot < o.replay_cap) o.replay[slot] = make_int2((int)g, (int)h);
-      if (o.defer_p) put(o.p, F, g, h, PS_NAN);  // not a parked n: pearson_p_kernel skips it
-      return;  // the replay kernel writes this pair
+      replay_pair(g, h, F, o);
+      return;
     }
     const double sxy = diag ? sxx : xy - sx * sy / fn;
     r = sxy / sqrt(sxx * syy);
@@ -402,7 +428,8 @@ template <bool PRE>
 __global__ void __launch_bounds__(NTHR, 1)
 pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ mpad, int64_t Wp,
                    int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor,
-                   const double* __restrict__ msx, const double* __restrict__ msq) {
+                   const double* __restrict__ msx, const double* __restrict__ msq, const int32_t* __restrict__ me1,
+                   const int32_t* __restrict__ me2) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TNS], empty[TNS];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -549,12 +576,16 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __r
         const int64_t gg = row0 + wi * 8 * WM + i * 8 + fr;
         const int64_t hh = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
         if (gg < lo || gg >= hi || hh < gg || hh >= F) continue;
-        if constexpr (PRE)
-          pearson_finish(gg, hh, F, an[i][j][e], msx[gg * F + hh], msx[hh * F + gg], msq[gg * F + hh],
-                         msq[hh * F + gg], axy[i][j][e], o);
-        else
+        if constexpr (PRE) {
+          const double sx = msx[gg * F + hh], sy = msx[hh * F + gg], qx = msq[gg * F + hh], qy = msq[hh * F + gg];
+          if (gg != hh && moments_imprecise(an[i][j][e], sx, sy, qx, qy, me1[gg], me2[gg], me1[hh], me2[hh]))
+            replay_pair(gg, hh, F, o);
+          else
+            pearson_finish(gg, hh, F, an[i][j][e], sx, sy, qx, qy, axy[i][j][e], o);
+        } else {
           pearson_finish(gg, hh, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e], asyy[i][j][e],
                          axy[i][j][e], o);
+        }
       }
 }
 
@@ -817,8 +848,9 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     if (rc) return rc;
     // large F: the four masked moments on the int8 tensor cores, Sxy alone on DMMA
     double *msx = nullptr, *msq = nullptr;
+    int32_t *me1 = nullptr, *me2 = nullptr;
     if (ps_moments_on(F, a->S)) {
-      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, s);
+      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, &me1, &me2, s);
       if (rc) return rc;
     }
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -828,14 +860,16 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     ps_prof_begin("pearson_tile", s);
     if (msx)
       pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
-                                                                      msx, msq);
+                                                                      msx, msq, me1, me2);
     else
       pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
-                                                                       nullptr, nullptr);
+                                                                       nullptr, nullptr, nullptr, nullptr);
     ps_prof_end(s);
     PS_LAUNCHED();
     ps_free(msx, s);
     ps_free(msq, s);
+    ps_free(me1, s);
+    ps_free(me2, s);
   } else {
     ps_prof_begin("pearson_tile", s);
     launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT,
@@ -888,6 +922,8 @@ struct ps_pearson_job {
   bool moments = false;    // large F: moments on the int8 tensor cores, all tiles after the upload
   double* msx = nullptr;
   double* msq = nullptr;
+  int32_t* me1 = nullptr;
+  int32_t* me2 = nullptr;
   int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
   int nws = 0;
@@ -965,10 +1001,10 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   ps_prof_begin("pearson_tile", s);
   if (j->tma && j->msx)
     pearson_tma_kernel<true><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
-                                                                         j->o, 1, j->msx, j->msq);
+                                                                         j->o, 1, j->msx, j->msq, j->me1, j->me2);
   else if (j->tma)
     pearson_tma_kernel<false><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
-                                                                          j->o, 1, nullptr, nullptr);
+                                                                          j->o, 1, nullptr, nullptr, nullptr, nullptr);
   else
     launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
                  a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
@@ -995,7 +1031,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
   if (!rc) rc = pearson_center_upto(j, a->F, s);
-  if (!rc && j->moments) rc = ps_pearson_moments(a, j->xc, 0, &j->msx, &j->msq, s);
+  if (!rc && j->moments) rc = ps_pearson_moments(a, j->xc, 0, &j->msx, &j->msq, &j->me1, &j->me2, s);
   if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
   if (!rc && j->o.defer_p) {
     pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
@@ -1015,6 +1051,8 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->mpad, j->home);
   ps_free(j->msx, j->home);
   ps_free(j->msq, j->home);
+  ps_free(j->me1, j->home);
+  ps_free(j->me2, j->home);
   delete j;
   return rc;
 }
@@ -1030,5 +1068,7 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->mpad, j->home);
   ps_free(j->msx, j->home);
   ps_free(j->msq, j->home);
+  ps_free(j->me1, j->home);
+  ps_free(j->me2, j->home);
   delete j;
 }

@@ -109,3 +109,22 @@ def test_moments_range_independent(monkeypatch):
     for w, p in zip(whole, parts):
         assert bitwise_equal(w.cpu().numpy(), p.cpu().numpy())
     dm.close()
+
+
+def test_moments_outlier_exponent_replayed(oracle, monkeypatch):
+    """A row whose digit scale is set by one outlier: for partners missing at
+    the outlier the expansion's error bound exceeds 1e-12 of the centred sums,
+    so those pairs are replayed exactly (without the check r would be off by
+    ~1e-5 here)."""
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    rng = np.random.default_rng(8)
+    F, S = 48, 20000
+    raw = rng.normal(size=(F, S))
+    raw[3, 0] = 1e5                     # mean shift ~5: mild cancellation, huge row exponent
+    raw[7, 1] = -3e4
+    raw[rng.random(F) < 0.5, 0] = np.nan
+    raw[rng.random((F, S)) < 0.1] = np.nan
+    raw[3, 0] = 1e5
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
