@@ -71,6 +71,10 @@ struct Outs {
   int replay_cap;
   int* err;
   int defer_p;  // 1: the tile epilogue parks n in p; pearson_p_kernel evaluates the tail
+  // moments path: the tiles store Sxy and n (F x F, upper pairs) for
+  // pearson_pairs_kernel, which joins them with the int8 moments
+  double* sxy = nullptr;
+  int32_t* nn = nullptr;
 };
 
 __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
@@ -166,6 +170,33 @@ __global__ void pearson_p_kernel(const double* __restrict__ stat, double* __rest
     if (p > 1.0) p = 1.0;
     pout[g * F + h] = p;
     pout[h * F + g] = p;
+  }
+}
+
+// The moments path's pair epilogue: Sxy and n from the DMMA tiles, Sx / Sxx
+// (and their transposes Sy / Syy) from the int8 contractions; one thread per
+// upper-triangle cell of rows [lo, hi).  Pairs whose digit moments could move
+// the centred sums by more than 1e-12 are replayed exactly.
+__global__ void pearson_pairs_kernel(int64_t F, int64_t lo, int64_t hi, Outs o, const double* __restrict__ msx,
+                                     const double* __restrict__ msq, const int32_t* __restrict__ me1,
+                                     const int32_t* __restrict__ me2) {
+  auto before = [&](int64_t g) { return (g - lo) * F - (g * (g - 1) - lo * (lo - 1)) / 2; };
+  const int64_t total = before(hi);
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = lo, b = hi - 1;  // last row g with before(g) <= it
+    while (a < b) {
+      const int64_t mid = (a + b + 1) >> 1;
+      if (before(mid) <= it) a = mid;
+      else b = mid - 1;
+    }
+    const int64_t g = a, h = g + (it - before(g));
+    const int n = o.nn[g * F + h];
+    const double sx = msx[g * F + h], sy = msx[h * F + g], qx = msq[g * F + h], qy = msq[h * F + g];
+    if (g != h && moments_imprecise(n, sx, sy, qx, qy, me1[g], me2[g], me1[h], me2[h]))
+      replay_pair(g, h, F, o);
+    else
+      pearson_finish(g, h, F, n, sx, sy, qx, qy, o.sxy[g * F + h], o);
   }
 }
 
@@ -421,15 +452,14 @@ __device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
   return v;
 }
 
-// PRE: the first / second moments come precomputed (ps_moments.cu: msx = X' M^T,
-// msq = X'^2 M^T, F x F): the tiles run Sxy = X' X'^T alone -- one DMMA per
-// fragment pair instead of five -- plus the pair counts
+// PRE: the first / second moments come from the int8 contractions
+// (ps_moments.cu): the tiles run Sxy = X' X'^T alone -- one DMMA per fragment
+// pair instead of five -- plus the pair counts, and store both for
+// pearson_pairs_kernel (so they need no moments and overlap the upload)
 template <bool PRE>
 __global__ void __launch_bounds__(NTHR, 1)
 pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ mpad, int64_t Wp,
-                   int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor,
-                   const double* __restrict__ msx, const double* __restrict__ msq, const int32_t* __restrict__ me1,
-                   const int32_t* __restrict__ me2) {
+                   int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TNS], empty[TNS];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -577,11 +607,8 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __r
         const int64_t hh = col0 + wj * 8 * WN + j * 8 + 2 * fk + e;
         if (gg < lo || gg >= hi || hh < gg || hh >= F) continue;
         if constexpr (PRE) {
-          const double sx = msx[gg * F + hh], sy = msx[hh * F + gg], qx = msq[gg * F + hh], qy = msq[hh * F + gg];
-          if (gg != hh && moments_imprecise(an[i][j][e], sx, sy, qx, qy, me1[gg], me2[gg], me1[hh], me2[hh]))
-            replay_pair(gg, hh, F, o);
-          else
-            pearson_finish(gg, hh, F, an[i][j][e], sx, sy, qx, qy, axy[i][j][e], o);
+          o.sxy[gg * F + hh] = axy[i][j][e];
+          o.nn[gg * F + hh] = an[i][j][e];
         } else {
           pearson_finish(gg, hh, F, an[i][j][e], asx[i][j][e], asy[i][j][e], asxx[i][j][e], asyy[i][j][e],
                          axy[i][j][e], o);
@@ -847,29 +874,36 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     int rc = make_pearson_map(&xmap, xc, a->ld, F);
     if (rc) return rc;
     // large F: the four masked moments on the int8 tensor cores, Sxy alone on DMMA
-    double *msx = nullptr, *msq = nullptr;
-    int32_t *me1 = nullptr, *me2 = nullptr;
-    if (ps_moments_on(F, a->S)) {
-      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, &me1, &me2, s);
-      if (rc) return rc;
+    const bool mom = ps_moments_on(F, a->S);
+    if (mom) {
+      PS_CUDA(ps_alloc(&o.sxy, (size_t)(F * F), s));
+      PS_CUDA(ps_alloc(&o.nn, (size_t)(F * F), s));
     }
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kTmaSmem));
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kTmaSmem));
     ps_prof_begin("pearson_tile", s);
-    if (msx)
-      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
-                                                                      msx, msq, me1, me2);
+    if (mom)
+      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
     else
-      pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0,
-                                                                       nullptr, nullptr, nullptr, nullptr);
+      pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
     ps_prof_end(s);
     PS_LAUNCHED();
-    ps_free(msx, s);
-    ps_free(msq, s);
-    ps_free(me1, s);
-    ps_free(me2, s);
+    if (mom) {
+      double *msx = nullptr, *msq = nullptr;
+      int32_t *me1 = nullptr, *me2 = nullptr;
+      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, &me1, &me2, s);
+      if (rc) return rc;
+      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(F, lo, hi, o, msx, msq, me1, me2);
+      PS_LAUNCHED();
+      ps_free(msx, s);
+      ps_free(msq, s);
+      ps_free(me1, s);
+      ps_free(me2, s);
+      ps_free(o.sxy, s);
+      ps_free(o.nn, s);
+    }
   } else {
     ps_prof_begin("pearson_tile", s);
     launch_tiles(mode, (unsigned)grid, s, mode >= 1 ? xc : a->d_vals, xq, a->ld, a->d_mask, W, a->d_center, F, NT,
@@ -920,10 +954,7 @@ struct ps_pearson_job {
   double* xc = nullptr;    // pre-centred x' (mode >= 1)
   double* xq = nullptr;    // x'^2 (mode 2)
   bool moments = false;    // large F: moments on the int8 tensor cores, all tiles after the upload
-  double* msx = nullptr;
-  double* msq = nullptr;
-  int32_t* me1 = nullptr;
-  int32_t* me2 = nullptr;
+
   int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
   int nws = 0;
@@ -958,6 +989,8 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
       e = cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kTmaSmem);
     j->moments = ps_moments_on(F, a->S);
+    if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.sxy, (size_t)(F * F), s);
+    if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.nn, (size_t)(F * F), s);
     if (e == cudaSuccess && make_pearson_map(&j->xmap, j->xc, a->ld, F) != PS_OK)
       e = cudaErrorInvalidValue;
   }
@@ -968,6 +1001,8 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
     ps_free(j->xc, s);
     ps_free(j->xq, s);
     ps_free(j->mpad, s);
+    ps_free(j->o.sxy, s);
+    ps_free(j->o.nn, s);
     delete j;
     return ps_cuda_check(e, "pearson setup");
   }
@@ -999,12 +1034,12 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t F = a->F, NT = ps_ceil_div(F, T), W = a->W;
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
-  if (j->tma && j->msx)
+  if (j->tma && j->moments)
     pearson_tma_kernel<true><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
-                                                                         j->o, 1, j->msx, j->msq, j->me1, j->me2);
+                                                                         j->o, 1);
   else if (j->tma)
     pearson_tma_kernel<false><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
-                                                                          j->o, 1, nullptr, nullptr, nullptr, nullptr);
+                                                                          j->o, 1);
   else
     launch_tiles(j->mode, (unsigned)(t1 - t0), s, j->mode >= 1 ? j->xc : a->d_vals, j->xq, a->ld, a->d_mask, W,
                  a->d_center, F, NT, t0, 0, F, 1, W, j->o, nullptr, 1);
@@ -1019,7 +1054,6 @@ int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
   if (J1 <= j->J_done) return PS_OK;
   int rc0 = pearson_center_upto(j, J1 * T, s);
   if (rc0) return rc0;
-  if (j->moments) return PS_OK;  // every tile waits for the moments of all rows (ps_pearson_end)
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = pearson_columns(j, j->J_done, J1, w);
   j->J_done = J1;
@@ -1031,8 +1065,21 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
   if (!rc) rc = pearson_center_upto(j, a->F, s);
-  if (!rc && j->moments) rc = ps_pearson_moments(a, j->xc, 0, &j->msx, &j->msq, &j->me1, &j->me2, s);
   if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
+  if (!rc && j->moments) {
+    double *msx = nullptr, *msq = nullptr;
+    int32_t *me1 = nullptr, *me2 = nullptr;
+    rc = ps_pearson_moments(a, j->xc, 0, &msx, &msq, &me1, &me2, s);
+    if (!rc) {
+      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(a->F, 0, a->F, j->o, msx, msq, me1, me2);
+      ps_count_launch();
+      if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson pairs launch");
+    }
+    ps_free(msx, s);
+    ps_free(msq, s);
+    ps_free(me1, s);
+    ps_free(me2, s);
+  }
   if (!rc && j->o.defer_p) {
     pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
     ps_count_launch();
@@ -1049,10 +1096,8 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
   ps_free(j->mpad, j->home);
-  ps_free(j->msx, j->home);
-  ps_free(j->msq, j->home);
-  ps_free(j->me1, j->home);
-  ps_free(j->me2, j->home);
+  ps_free(j->o.sxy, j->home);
+  ps_free(j->o.nn, j->home);
   delete j;
   return rc;
 }
@@ -1066,9 +1111,7 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->xc, j->home);
   ps_free(j->xq, j->home);
   ps_free(j->mpad, j->home);
-  ps_free(j->msx, j->home);
-  ps_free(j->msq, j->home);
-  ps_free(j->me1, j->home);
-  ps_free(j->me2, j->home);
+  ps_free(j->o.sxy, j->home);
+  ps_free(j->o.nn, j->home);
   delete j;
 }
