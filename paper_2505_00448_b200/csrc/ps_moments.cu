@@ -245,6 +245,141 @@ moment_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
   if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
+// Cluster-pair variant: the two CTAs of a cluster take the row tiles
+// (I0 + 2p, J) and (I0 + 2p + 1, J) -- the same presence tile J -- and each
+// TMA-loads half of it, multicast into both CTAs: 48 KB of L2 reads per CTA
+// per K step instead of 64 KB.  A stage is refilled only after both CTAs'
+// MMAs released it (the MMA commit arrives on the `empty` barrier of both);
+// an odd last row tile runs with a dummy partner that only loads its half of
+// the shared tile.
+constexpr int QHALF = QB_BYTES / 2;  // 128 rows x 128 B
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTH, 1)
+moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int nk,
+                      int64_t I0, int64_t nI, int64_t J0, int64_t nJ, const int32_t* __restrict__ rexp, int digit,
+                      int first, double* __restrict__ out, int64_t F) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[QSTAGES], empty[QSTAGES], accfull, accempty;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)tc05::cluster_ctarank();
+  const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;
+  const int64_t np = (nI + 1) / 2, nunits = np * nJ;
+
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
+  if (tid == 32) {
+    for (int i = 0; i < QSTAGES; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], 2);  // both CTAs' MMA commits
+    }
+    tc05::mbar_init(&accfull, 1);
+    tc05::mbar_init(&accempty, 128);
+    tc05::fence_barrier_init();
+  }
+  if (tid == 4 * 32) {
+    tc05::prefetch_tmap(&amap);
+    tc05::prefetch_tmap(&bmap);
+  }
+  tc05::fence_before_sync();
+  tc05::cluster_sync();  // barriers initialised in both CTAs before any multicast
+  tc05::fence_after_sync();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      int64_t q = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        const int64_t ip = 2 * (u / nJ) + rank;
+        const bool own = ip < nI;
+        const int I = (int)(I0 + ip), J = (int)(J0 + u % nJ);
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
+          const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+          tc05::mbar_arrive_expect_tx(&full[st], own ? QSTAGE_BYTES : QB_BYTES);
+          tc05::tma_load_2d_mc(sb + rank * QHALF, &bmap, kc * QKB, J * QN + rank * 128, &full[st], (uint16_t)3);
+          if (own) tc05::tma_load_2d(sa, &amap, kc * QKB, I * QM, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc05::idesc_i8(128, QN, true);
+      int64_t q = 0;
+      int seg = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        const bool own = 2 * (u / nJ) + rank < nI;
+        if (own && seg > 0) {  // the epilogue has drained the previous tile
+          tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
+          tc05::fence_after_sync();
+          if (own) {
+            const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < QKB / 32; ++kk) {
+              const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+              const uint32_t acc = (kc > 0 || kk > 0) ? 1u : 0u;
+              tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+              tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * QKB + kk * 32), bd, idesc, acc);
+            }
+          }
+          tc05::commit_mc(&empty[st], (uint16_t)3);
+        }
+        if (own) {
+          tc05::commit(&accfull);
+          ++seg;
+        }
+      }
+    }
+  } else {
+    // epilogue warps 0-3: TMEM lanes 32 w .. 32 w + 31 = tile rows
+    int seg = 0;
+    for (int64_t u = cl; u < nunits; u += ncl) {
+      const int64_t ip = 2 * (u / nJ) + rank;
+      if (ip >= nI) continue;  // dummy partner
+      const int64_t I = I0 + ip, J = J0 + u % nJ;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int64_t r = I * QM + half * 128 + warp * 32 + lane;
+        const bool rok = r < F;
+        const int ex = rok ? rexp[r] : 0;
+        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+        double* orow = out + (rok ? r : 0) * F;
+#pragma unroll 1
+        for (int cc = 0; cc < QN / 32; ++cc) {
+          uint32_t v[32];
+          tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+          const int64_t c0 = J * QN + cc * 32;
+          if (rok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int64_t c = c0 + j;
+              if (c < F) {
+                const double term = (double)(int32_t)v[j] * scale;
+                orow[c] = first ? term : orow[c] + term;
+              }
+            }
+          }
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive(&accempty);
+      ++seg;
+    }
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::cluster_sync();  // no CTA leaves while its partner may still multicast / commit into it
+  if (warp == 0) tc05::tmem_dealloc(tmem, 512);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 moment_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -257,13 +392,13 @@ PFN_cuTensorMapEncodeTiled_v12000 moment_map_encoder() {
   return fn;
 }
 
-// K-major int8 rows (F x Sp bytes), 128-byte x 256-row boxes, SWIZZLE_128B
-int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp) {
+// K-major int8 rows (F x Sp bytes), 128-byte x box_rows boxes, SWIZZLE_128B
+int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp, int box_rows = QM) {
   auto enc = moment_map_encoder();
   if (!enc) return ps_fail(PS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)Sp, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)Sp};
-  cuuint32_t box[2] = {(cuuint32_t)QKB, (cuuint32_t)QM};
+  cuuint32_t box[2] = {(cuuint32_t)QKB, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   if (enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -303,6 +438,8 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   if (e == cudaSuccess) e = ps_alloc(&e2, (size_t)F, s);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kMomSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kMomSmem);
   if (e != cudaSuccess) {
     cleanup();
     ps_free(sx, s);
@@ -320,8 +457,9 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
   PS_LAUNCHED();
   presence_i8_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, a->W, S, Sp, pres);
   PS_LAUNCHED();
-  CUtensorMap amap[kDigits], bmap;
+  CUtensorMap amap[kDigits], bmap, bmap_half;
   int rc = make_i8_map(&bmap, pres, F, Sp);
+  if (!rc) rc = make_i8_map(&bmap_half, pres, F, Sp, QN / 2);  // multicast halves
   for (int d = 0; d < kDigits && !rc; ++d) rc = make_i8_map(&amap[d], dig + d * F * Sp, F, Sp);
   if (rc) {
     cleanup();
@@ -332,6 +470,28 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     return rc;
   }
   const int grid = (int)std::min<int64_t>(nI * nJ, ds->num_sms);
+  // cluster pairs (PS_MOMENTS_MC=0: one CTA per tile)
+  const char* mce = getenv("PS_MOMENTS_MC");
+  const bool mc = !(mce && mce[0] == '0') && ds->num_sms >= 2;
+  static int max_clusters = 0;  // co-resident 2-CTA clusters (GPCs may hold an odd SM count)
+  if (mc && !max_clusters) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)(ds->num_sms & ~1));
+    lc.blockDim = dim3(QTH);
+    lc.dynamicSmemBytes = kMomSmem;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = 2;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    lc.attrs = &at;
+    lc.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, moment_gemm_mc_kernel, &lc) != cudaSuccess || max_clusters <= 0)
+      max_clusters = ds->num_sms / 2;
+    cudaGetLastError();
+  }
+  const int64_t nunits = ((nI + 1) / 2) * nJ;
+  const int grid_mc = 2 * (int)std::min<int64_t>(nunits, max_clusters > 0 ? max_clusters : 1);
   ps_prof_begin("pearson_moments", s);
   for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
     double* out = sq_pass ? sq : sx;
@@ -339,8 +499,12 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, sq_pass, r0, F * Sp, dig);
     PS_LAUNCHED();
     for (int d = kDigits; d >= 1; --d) {  // least significant digit first (fixed fold order)
-      moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, I0, nI, J0, nJ, ex, d,
-                                                     d == kDigits ? 1 : 0, out, F);
+      if (mc)
+        moment_gemm_mc_kernel<<<grid_mc, QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, I0, nI, J0, nJ, ex, d,
+                                                             d == kDigits ? 1 : 0, out, F);
+      else
+        moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, I0, nI, J0, nJ, ex, d,
+                                                       d == kDigits ? 1 : 0, out, F);
       PS_LAUNCHED();
     }
   }
