@@ -553,11 +553,15 @@ presort_smem_kernel(const double* __restrict__ vals, int64_t ld, const uint32_t*
 // ngrp = D.  Derived from the boundary bits alone (bit n is the end sentinel),
 // so it is identical for owned and caller-owned (gathered) tables.
 __global__ void tie_index_kernel(const uint32_t* __restrict__ tb, int64_t ldt, const int32_t* __restrict__ lens,
-                                 uint16_t* __restrict__ gp, uint16_t* __restrict__ bpos, int64_t ldo,
-                                 int32_t* __restrict__ ngrp, const uint16_t* __restrict__ order,
-                                 uint32_t* __restrict__ ordgid, int64_t f0) {
+                                 const uint8_t* __restrict__ tied, uint16_t* __restrict__ gp,
+                                 uint16_t* __restrict__ bpos, int64_t ldo, int32_t* __restrict__ ngrp,
+                                 const uint16_t* __restrict__ order, uint32_t* __restrict__ ordgid, int64_t f0) {
   const int64_t f = f0 + blockIdx.x;
   const int n = lens[f];
+  if (!tied[f]) {  // every position its own group: the walks never read the index of a tie-free feature
+    if (threadIdx.x == 0) ngrp[f] = n;
+    return;
+  }
   const int nw = (n + 31) >> 5;  // words holding positions < n
   const uint32_t* t = tb + f * ldt;
   uint16_t* g = gp + f * ldt;
@@ -732,8 +736,8 @@ int ps_presort_rows(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
 
 int ps_tie_index(ps_matrix* m, int64_t f0, int64_t f1, cudaStream_t s) {
   if (f1 <= f0 || !m->d_gp) return PS_OK;
-  tie_index_kernel<<<(unsigned)(f1 - f0), 256, 0, s>>>(m->d_tb, m->ldt, m->d_len, m->d_gp, m->d_bpos, m->ldo,
-                                                      m->d_ngrp, m->d_order, m->d_ordgid, f0);
+  tie_index_kernel<<<(unsigned)(f1 - f0), 256, 0, s>>>(m->d_tb, m->ldt, m->d_len, m->d_tied, m->d_gp, m->d_bpos,
+                                                      m->ldo, m->d_ngrp, m->d_order, m->d_ordgid, f0);
   PS_LAUNCHED();
   return PS_OK;
 }
