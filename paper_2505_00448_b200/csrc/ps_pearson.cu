@@ -427,6 +427,10 @@ constexpr int TMASK_WORDS = 2;                // presence words per row per stag
 constexpr int TSTAGE_BYTES = 2 * TNB * TBOX_BYTES + 2 * T * TMASK_WORDS * 4;
 constexpr int TNS = 3;
 constexpr size_t kTmaSmem = (size_t)TNS * TSTAGE_BYTES + 1024;
+// PRE variant: 32-sample stages (one mask word), two CTAs per SM
+constexpr size_t kTmaSmemPre = (size_t)TNS * (2 * (32 / TBOX) * TBOX_BYTES + 2 * T * 1 * 4) + 1024;
+template <bool PRE>
+constexpr size_t tma_smem() { return PRE ? kTmaSmemPre : kTmaSmem; }
 
 // Whole-warp wait on an mbarrier phase: the try_wait loop is C++ (the
 // compiler sees the branch) and the warp reconverges before the
@@ -457,9 +461,15 @@ __device__ __forceinline__ double ld_sw(uint32_t box_base, int r, int k) {
 // pair instead of five -- plus the pair counts, and store both for
 // pearson_pairs_kernel (so they need no moments and overlap the upload)
 template <bool PRE>
-__global__ void __launch_bounds__(NTHR, 1)
+__global__ void __launch_bounds__(NTHR, PRE ? 2 : 1)
 pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __restrict__ mpad, int64_t Wp,
                    int64_t W, int64_t F, int64_t NT, int64_t tile0, int64_t lo, int64_t hi, Outs o, int colmajor) {
+  // PRE (one DMMA product): half-size stages (32 samples, one mask word) so
+  // that two CTAs share an SM -- twice the warps to hide the DMMA latency
+  constexpr int TG = PRE ? 32 : ::TG;
+  constexpr int TNB = TG / TBOX;
+  constexpr int TMASK_WORDS = TG / 32;
+  constexpr int TSTAGE_BYTES = 2 * TNB * TBOX_BYTES + 2 * T * TMASK_WORDS * 4;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   __shared__ uint64_t full[TNS], empty[TNS];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
@@ -502,9 +512,12 @@ pearson_tma_kernel(const __grid_constant__ CUtensorMap xmap, const uint32_t* __r
       const int r = lane + 32 * (q & 1);               // row within the block
       const int64_t gr = (q < 2 ? row0 : col0) + r;  // feature row
       const uint32_t dst = am + (uint32_t)((q < 2 ? 0 : T * TMASK_WORDS * 4) + r * TMASK_WORDS * 4);
-      const uint32_t* src = mpad + (gr < F ? gr : 0) * Wp + 2 * g;
-      const uint32_t nbytes = gr < F ? 8u : 0u;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
+      const uint32_t* src = mpad + (gr < F ? gr : 0) * Wp + TMASK_WORDS * g;
+      const uint32_t nbytes = gr < F ? 4u * TMASK_WORDS : 0u;
+      if constexpr (TMASK_WORDS == 2)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(nbytes) : "memory");
     }
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc05::smem_u32(&full[st])) : "memory");
   };
@@ -882,10 +895,11 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kTmaSmem));
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kTmaSmem));
+                                 (int)kTmaSmemPre));
     ps_prof_begin("pearson_tile", s);
     if (mom)
-      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
+      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmemPre, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o,
+                                                                         0);
     else
       pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
     ps_prof_end(s);
@@ -987,7 +1001,7 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
                                (int)kTmaSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kTmaSmem);
+                               (int)kTmaSmemPre);
     j->moments = ps_moments_on(F, a->S);
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.sxy, (size_t)(F * F), s);
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.nn, (size_t)(F * F), s);
@@ -1035,7 +1049,7 @@ static int pearson_columns(ps_pearson_job* j, int64_t J0, int64_t J1, cudaStream
   const int64_t t0 = J0 * (J0 + 1) / 2, t1 = J1 * (J1 + 1) / 2;
   ps_prof_begin("pearson_tile", s);
   if (j->tma && j->moments)
-    pearson_tma_kernel<true><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
+    pearson_tma_kernel<true><<<(unsigned)(t1 - t0), NTHR, kTmaSmemPre, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
                                                                          j->o, 1);
   else if (j->tma)
     pearson_tma_kernel<false><<<(unsigned)(t1 - t0), NTHR, kTmaSmem, s>>>(j->xmap, j->mpad, j->Wp, W, F, NT, t0, 0, F,
