@@ -74,8 +74,8 @@ struct ps_matrix {
 bool ps_moments_on(int64_t F, int64_t S);
 // digits of the expansion: each expanded term is within 2^(e - 7 kMomentDigits) of x'
 constexpr int kMomentDigits = 8;
-int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx, double** sq, int32_t** e1,
-                       int32_t** e2, cudaStream_t s);
+int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx, double** sq,
+                       int32_t** e1, int32_t** e2, cudaStream_t s);
 // true when the Spearman walk streams g's order (large S): d_ordgid is built
 bool ps_spearman_streams_g(int64_t S);
 // tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits

@@ -443,12 +443,13 @@ bool ps_moments_on(int64_t F, int64_t S) {
   return F >= 2048 && S >= 256;
 }
 
-int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double** sx_out, double** sq_out,
-                       int32_t** e1_out, int32_t** e2_out, cudaStream_t s) {
+int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx_out,
+                       double** sq_out, int32_t** e1_out, int32_t** e2_out, cudaStream_t s) {
   *sx_out = *sq_out = nullptr;
   *e1_out = *e2_out = nullptr;
   const int64_t F = a->F, S = a->S;
   lo = std::max<int64_t>(0, std::min<int64_t>(lo, F));
+  hi = std::max<int64_t>(lo + 1, std::min<int64_t>(hi, F));
   ps_device_state* ds = ps_state();
   const int64_t Sp = ps_round_up(std::max<int64_t>(S, 1), QKB);
   const int nk = (int)(Sp / QKB);
@@ -477,10 +478,17 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     ps_free(e2, s);
     return ps_cuda_check(e, "pearson moments setup");
   }
-  // rows and columns [lo, F): every (g, h) and (h, g) with g in [lo, hi), h >= g
-  // (tile-aligned down: rows [r0, lo) are computed as well, unused)
-  const int64_t I0 = lo / QM, nI = ps_ceil_div(F, QM) - I0;
-  const int64_t J0 = lo / QN, nJ = ps_ceil_div(F, QN) - J0;
+  // The pairs (g, h >= g), g in [lo, hi), read Sx(g, h) and Sx(h, g): an L of
+  // tiles -- rows [lo, hi) x columns [lo, F) (R1) plus rows past hi x columns
+  // [lo, hi) (R2) -- so a rank's share of the int8 work follows its share of
+  // the pairs (a single range [0, F) is the whole square).  Tile-aligned
+  // (rows / columns before lo are computed as well, unused); R2 starts at the
+  // tile row after R1's last, so no tile is folded twice.
+  const int64_t NTt = ps_ceil_div(F, QM);
+  const int64_t I0 = lo / QM, I1 = (hi - 1) / QM;
+  const int64_t J0 = lo / QN, Jh = (hi - 1) / QN;
+  const int64_t nI = I1 - I0 + 1, nJ = NTt - J0;            // R1
+  const int64_t I2 = I1 + 1, nI2 = NTt - I2, nJ2 = Jh - J0 + 1;  // R2
   const int64_t r0 = I0 * QM, nrows = F - r0;
   moment_scale_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, r0, e1, e2);
   PS_LAUNCHED();
@@ -498,7 +506,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     ps_free(e2, s);
     return rc;
   }
-  const int grid = (int)std::min<int64_t>(nI * nJ, ds->num_sms);
+  auto grid_of = [&](int64_t nr, int64_t nc) { return (int)std::min<int64_t>(nr * nc, ds->num_sms); };
   // cluster pairs (PS_MOMENTS_MC=0: one CTA per tile)
   const char* mce = getenv("PS_MOMENTS_MC");
   const bool mc = !(mce && mce[0] == '0') && ds->num_sms >= 2;
@@ -519,8 +527,9 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
       max_clusters = ds->num_sms / 2;
     cudaGetLastError();
   }
-  const int64_t nunits = ((nI + 1) / 2) * nJ;
-  const int grid_mc = 2 * (int)std::min<int64_t>(nunits, max_clusters > 0 ? max_clusters : 1);
+  auto grid_mc_of = [&](int64_t nr, int64_t nc) {
+    return 2 * (int)std::min<int64_t>(((nr + 1) / 2) * nc, max_clusters > 0 ? max_clusters : 1);
+  };
   ps_prof_begin("pearson_moments", s);
   for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
     double* out = sq_pass ? sq : sx;
@@ -528,13 +537,17 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, double*
     moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, sq_pass, r0, F * Sp, dig);
     PS_LAUNCHED();
     for (int d = kDigits; d >= 1; --d) {  // least significant digit first (fixed fold order)
-      if (mc)
-        moment_gemm_mc_kernel<<<grid_mc, QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, I0, nI, J0, nJ, ex, d,
-                                                             d == kDigits ? 1 : 0, out, F);
-      else
-        moment_gemm_kernel<<<grid, QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, I0, nI, J0, nJ, ex, d,
-                                                       d == kDigits ? 1 : 0, out, F);
-      PS_LAUNCHED();
+      for (int rect = 0; rect < 2; ++rect) {
+        const int64_t ri = rect ? I2 : I0, rn = rect ? nI2 : nI, cn = rect ? nJ2 : nJ;
+        if (rn <= 0 || cn <= 0) continue;
+        if (mc)
+          moment_gemm_mc_kernel<<<grid_mc_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, ri, rn, J0, cn,
+                                                                          ex, d, d == kDigits ? 1 : 0, out, F);
+        else
+          moment_gemm_kernel<<<grid_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, ri, rn, J0, cn, ex, d,
+                                                                    d == kDigits ? 1 : 0, out, F);
+        PS_LAUNCHED();
+      }
     }
   }
   ps_prof_end(s);

@@ -907,7 +907,7 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     if (mom) {
       double *msx = nullptr, *msq = nullptr;
       int32_t *me1 = nullptr, *me2 = nullptr;
-      rc = ps_pearson_moments(a, xc, lo, &msx, &msq, &me1, &me2, s);
+      rc = ps_pearson_moments(a, xc, lo, hi, &msx, &msq, &me1, &me2, s);
       if (rc) return rc;
       pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(F, lo, hi, o, msx, msq, me1, me2);
       PS_LAUNCHED();
@@ -1083,7 +1083,7 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   if (!rc && j->moments) {
     double *msx = nullptr, *msq = nullptr;
     int32_t *me1 = nullptr, *me2 = nullptr;
-    rc = ps_pearson_moments(a, j->xc, 0, &msx, &msq, &me1, &me2, s);
+    rc = ps_pearson_moments(a, j->xc, 0, a->F, &msx, &msq, &me1, &me2, s);
     if (!rc) {
       pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(a->F, 0, a->F, j->o, msx, msq, me1, me2);
       ps_count_launch();
