@@ -385,11 +385,12 @@ def run_reference_arm(args):
 
 # ---------------------------------------------------------------- GPU arm
 
-def moments_used(wl: Workload) -> bool:
-    """Pearson computes its masked moments on the int8 tensor cores (library rule)."""
+def moments_path(wl: Workload) -> int:
+    """Pearson contraction path (library rule, ps_pearson_moments_used): 0 FP64
+    DMMA, 1 int8 moments + DMMA Sxy, 2 everything on the int8 tensor cores."""
     from paper_2505_00448_b200 import _lib
 
-    return bool(_lib.load().ps_pearson_moments_used(wl.Fa, wl.S))
+    return int(_lib.load().ps_pearson_moments_used(wl.Fa, wl.S))
 
 
 def roofline_moments(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, peaks: dict):
@@ -424,14 +425,25 @@ def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, 
         peak = peaks["dmma_tflops"]
         achieved = per_launch / (launch_ms / 1e3) / 1e12
         desc = "4 k_g FP64 flops"
+    elif test == "pearson" and moments_path(wl) == 2:
+        # every contraction on the int8 tensor cores (prof region pearson_moments):
+        # Sx, Sxx over ordered pairs (8 digits x 2 moments x 2 ops), Sxy over the
+        # triangle (43 digit products x 2 ops), pair counts (2 ops)
+        F = wl.Fa
+        ops = (2 * 8 * 2.0 * F * F + (43 * 2.0 + 2.0) * F * (F + 1) / 2) * S / world
+        peak = peaks["tcgen05_i8_tops"]
+        achieved = ops / (launch_ms / 1e3) / 1e12
+        bound, unit = "tensor", "TOPS"
+        desc = ("152 int8 ops per pair-sample (tcgen05 kind::i8 exact digit contractions: Sx, Sxx, Sy, Syy "
+                "8 digits each, Sxy 43 digit products, n)")
     elif bound == "tensor":
-        if test == "pearson" and moments_used(wl):
+        if test == "pearson" and moments_path(wl) == 1:
             per_ps = 2.0  # Sxy alone on DMMA; Sx, Sxx, Sy, Syy on the int8 tensor cores
         per_launch = per_ps * units
         peak = peaks["dmma_tflops"]
         achieved = per_launch / (launch_ms / 1e3) / 1e12
         desc = f"{per_ps:g} FP64 flops"
-        if test == "pearson" and per_ps == 2.0:
+        if test == "pearson" and moments_path(wl) == 1:
             desc += " (Sxy on DMMA; masked moments on int8 tcgen05: roofline_moments)"
     else:
         per_launch = per_ps * units
@@ -565,14 +577,18 @@ def measure_device(wl: Workload, steps: int, warmup: int, world: int, rank: int,
     lib.ps_profile_enable(0)
     # busy time of the dominant kernel (union over its launches: incremental
     # launches of one step run concurrently on several streams)
-    kern_ms, kern_n = _lib.profile_collect_union(ROOF[test][3])
+    pearson_path = moments_path(wl) if test == "pearson" else 0
+    kname = "pearson_moments" if pearson_path == 2 else ROOF[test][3]
+    kern_ms, kern_n = _lib.profile_collect_union(kname)
     total_ms = sum(times)
     if world > 1:
         total_ms, kern_ms = reduce_max([total_ms, kern_ms])
     del outs, adj_outs, flush, shard_a, shard_b
     torch.cuda.empty_cache()
     roof = roofline(wl, kern_ms, kern_n, steps, world, peaks)
-    if test == "pearson" and roof is not None:
+    if roof is not None and pearson_path == 2:
+        roof["kernel"] = "pearson_moments (moment_gemm_mc, cross_gemm_mc)"
+    if pearson_path == 1 and roof is not None:
         mom_ms, mom_n = _lib.profile_collect_union("pearson_moments")
         if world > 1:
             mom_ms = reduce_max([mom_ms])[0]
@@ -709,7 +725,9 @@ def main():
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "f64" if test != "chi2" else "u8/i32",
+            "dtype": ("u8/i32" if test == "chi2" else
+                      "i8/i32 -> f64 (exact digit contractions)" if test == "pearson" and moments_path(wl) == 2
+                      else "f64"),
             "data": "synthetic (seeded BASELINE recipe, SURVEY 8d; CHRIS cohort unavailable)",
             "config": config_dict(wl, world),
             "roofline": roof,

@@ -117,11 +117,12 @@ int ps_matrix_destroy(ps_matrix* m);
 /* Block kernels (device outputs; see file header for range semantics). */
 int ps_pearson_block(ps_matrix* a, int64_t lo, int64_t hi, double* out_stat, double* out_p,
                      double* out_r2, void* stream);
-/* 1 when Pearson on an n_features x n_samples matrix computes its masked
- * first / second moments on the int8 tensor cores (exact digit contractions,
- * ps_moments.cu) and only Sxy on the FP64 tensor path; a function of the
- * shape alone (PS_PEARSON_MOMENTS=0/1 overrides), so every launch range and
- * device count of one matrix takes the same path. */
+/* The Pearson contraction path for an n_features x n_samples matrix, a
+ * function of the shape alone (PS_PEARSON_MOMENTS=0/1 and PS_PEARSON_SXY=dmma
+ * override), so every launch range and device count of one matrix takes the
+ * same path: 0 = five-product FP64 DMMA tiles; 1 = masked moments as exact
+ * int8 digit contractions + Sxy on DMMA tiles; 2 = moments, Sxy and pair
+ * counts all as int8 digit contractions (ps_moments.cu). */
 int ps_pearson_moments_used(int64_t n_features, int64_t n_samples);
 int ps_spearman_block(ps_matrix* a, int64_t lo, int64_t hi, double* out_stat, double* out_p,
                       double* out_rho, void* stream);

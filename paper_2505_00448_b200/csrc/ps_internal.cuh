@@ -75,7 +75,19 @@ bool ps_moments_on(int64_t F, int64_t S);
 // digits of the expansion: each expanded term is within 2^(e - 7 kMomentDigits) of x'
 constexpr int kMomentDigits = 8;
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx, double** sq,
-                       int32_t** e1, int32_t** e2, cudaStream_t s);
+                       int32_t** e1, int32_t** e2, double* sxy, int32_t* nn, cudaStream_t s);
+// the large-F Pearson path also takes Sxy and n from int8 digit products (no
+// FP64 tensor tiles); PS_PEARSON_SXY=dmma keeps the DMMA Sxy tiles
+bool ps_sxy_int8();
+// incremental form (ps_run follows the upload): rows, then tile columns of 256
+struct ps_moments_job;
+int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int32_t* nn, cudaStream_t s,
+                         ps_moments_job** out);
+int ps_moments_job_rows(ps_moments_job* j, int64_t r1, cudaStream_t s);
+int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s);
+int ps_moments_job_end(ps_moments_job* j, double** sx, double** sq, int32_t** e1, int32_t** e2, cudaStream_t s);
+void ps_moments_job_abort(ps_moments_job* j, cudaStream_t s);
+constexpr int kMomentTile = 256;
 // true when the Spearman walk streams g's order (large S): d_ordgid is built
 bool ps_spearman_streams_g(int64_t S);
 // tie-group index (d_gp / d_bpos / d_ngrp) of rows [f0, f1) from the boundary bits

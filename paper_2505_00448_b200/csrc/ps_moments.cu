@@ -31,6 +31,7 @@
 namespace {
 
 constexpr int kDigits = kMomentDigits;
+constexpr int kSxyMaxOrder = 10;  // digit products with s + t <= 10 enter Sxy
 constexpr int QM = 256, QN = 256, QKB = 128;  // tile rows, cols, K bytes per stage
 constexpr int QSTAGES = 3;
 constexpr int QA_BYTES = QM * QKB, QB_BYTES = QN * QKB;
@@ -131,8 +132,8 @@ __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, i
 
 // presence as int8 0/1 (F x Sp), zero past S
 __global__ void presence_i8_kernel(const uint32_t* __restrict__ mask, int64_t W, int64_t S, int64_t Sp,
-                                   int8_t* __restrict__ out) {
-  const int64_t f = blockIdx.x;
+                                   int8_t* __restrict__ out, int64_t f0 = 0) {
+  const int64_t f = f0 + blockIdx.x;
   for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
     uint32_t w[4] = {0u, 0u, 0u, 0u};
     const int64_t wi = s0 >> 5;
@@ -409,6 +410,186 @@ moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_con
   if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
+// Cross products over the upper triangle of tiles: out(i, j) (+)= w rs_i cs_j
+// (A B^T)(i, j) for the tile rows [I0, I0 + nI) and columns J >= I (Sxy from
+// digit planes s of rows i and t of rows j, w = 2^-7(s+t), rs = cs = 2^(e1+1));
+// or, with nout, the raw int32 products (pair counts from the presence).
+// Cluster pairs share the column tile as the contingency / moment GEMMs do:
+// the pair (I0 + 2p, I0 + 2p + 1) walks columns J >= I0 + 2p (one lower tile
+// per pair is computed and never read).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTH, 1)
+cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int nk,
+                     int64_t I0, int64_t nI, int64_t NT, const double* __restrict__ rs, const double* __restrict__ cs,
+                     double w, int first, double* __restrict__ out, int32_t* __restrict__ nout, int64_t F,
+                     int64_t Jlo) {
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  __shared__ uint64_t full[QSTAGES], empty[QSTAGES], accfull, accempty;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = tc05::smem_u32(tsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (int)tc05::cluster_ctarank();
+  const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;
+  // Jlo < 0: row-major over the range's row pairs, columns J >= the pair's
+  // first row, up to NT.  Jlo >= 0 (incremental upload): column-major over the
+  // column block [Jlo, NT), row pairs p with I0 + 2p <= J.
+  const int64_t np = (nI + 1) / 2, W0 = NT - I0;
+  auto cum = [&](int64_t p) { return p * W0 - p * (p - 1); };  // units of row pairs [0, p)
+  auto half_sum = [](int64_t x) -> int64_t { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); };  // sum_{m<x} m/2
+  auto ccum = [&](int64_t J) { return (J - Jlo) + half_sum(J - I0) - half_sum(Jlo - I0); };  // columns [Jlo, J)
+  const int64_t nunits = Jlo < 0 ? cum(np) : ccum(NT);
+  auto unit = [&](int64_t u, int64_t& pr, int64_t& J) {
+    if (Jlo < 0) {
+      int64_t a = 0, b = np - 1;
+      while (a < b) {
+        const int64_t m = (a + b + 1) >> 1;
+        if (cum(m) <= u) a = m;
+        else b = m - 1;
+      }
+      pr = a;
+      J = I0 + 2 * a + (u - cum(a));
+    } else {
+      int64_t a = Jlo, b = NT - 1;
+      while (a < b) {
+        const int64_t m = (a + b + 1) >> 1;
+        if (ccum(m) <= u) a = m;
+        else b = m - 1;
+      }
+      J = a;
+      pr = u - ccum(a);
+    }
+  };
+
+  if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
+  if (tid == 32) {
+    for (int i = 0; i < QSTAGES; ++i) {
+      tc05::mbar_init(&full[i], 1);
+      tc05::mbar_init(&empty[i], 2);
+    }
+    tc05::mbar_init(&accfull, 1);
+    tc05::mbar_init(&accempty, 128);
+    tc05::fence_barrier_init();
+  }
+  if (tid == 4 * 32) {
+    tc05::prefetch_tmap(&amap);
+    tc05::prefetch_tmap(&bmap);
+  }
+  tc05::fence_before_sync();
+  tc05::cluster_sync();
+  tc05::fence_after_sync();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer
+      int64_t q = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        int64_t pr, J;
+        unit(u, pr, J);
+        const int64_t ip = 2 * pr + rank;
+        const bool own = ip < nI;
+        const int I = (int)(I0 + ip);
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
+          const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+          tc05::mbar_arrive_expect_tx(&full[st], own ? QSTAGE_BYTES : QB_BYTES);
+          tc05::tma_load_2d_mc(sb + rank * QHALF, &bmap, kc * QKB, (int)J * QN + rank * 128, &full[st], (uint16_t)3);
+          if (own) tc05::tma_load_2d(sa, &amap, kc * QKB, I * QM, &full[st]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = tc05::idesc_i8(128, QN, true);
+      int64_t q = 0;
+      int seg = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        int64_t pr, J;
+        unit(u, pr, J);
+        const bool own = 2 * pr + rank < nI;
+        if (own && seg > 0) {
+          tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        for (int kc = 0; kc < nk; ++kc, ++q) {
+          const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
+          tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
+          tc05::fence_after_sync();
+          if (own) {
+            const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < QKB / 32; ++kk) {
+              const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+              const uint32_t acc = (kc > 0 || kk > 0) ? 1u : 0u;
+              tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+              tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * QKB + kk * 32), bd, idesc, acc);
+            }
+          }
+          tc05::commit_mc(&empty[st], (uint16_t)3);
+        }
+        if (own) {
+          tc05::commit(&accfull);
+          ++seg;
+        }
+      }
+    }
+  } else {
+    int seg = 0;
+    for (int64_t u = cl; u < nunits; u += ncl) {
+      int64_t pr, J;
+      unit(u, pr, J);
+      const int64_t ip = 2 * pr + rank;
+      if (ip >= nI) continue;  // dummy partner
+      const int64_t I = I0 + ip;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int64_t r = I * QM + half * 128 + warp * 32 + lane;
+        const bool rok = r < F;
+        const double rsw = rok && rs ? rs[r] * w : 0.0;
+#pragma unroll 1
+        for (int cc = 0; cc < QN / 32; ++cc) {
+          uint32_t v[32];
+          tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+          const int64_t c0 = J * QN + cc * 32;
+          if (!rok) continue;
+          if (nout) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c0 + j < F) nout[r * F + c0 + j] = (int32_t)v[j];
+          } else {
+            double* orow = out + r * F;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int64_t c = c0 + j;
+              if (c < F) {
+                const double term = (double)(int32_t)v[j] * rsw * cs[c];
+                orow[c] = first ? term : orow[c] + term;
+              }
+            }
+          }
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive(&accempty);
+      ++seg;
+    }
+  }
+  tc05::fence_before_sync();
+  __syncthreads();
+  tc05::cluster_sync();
+  if (warp == 0) tc05::tmem_dealloc(tmem, 512);
+}
+
+// 2^(e1 + 1) per row (NaN for rows holding NaN / inf): the Sxy fold scales
+__global__ void row_scale_kernel(const int32_t* __restrict__ e1, int64_t f0, int64_t n, double* __restrict__ sc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int e = e1[f0 + i];
+  sc[f0 + i] = e == kNonFinite ? PS_NAN : ldexp(1.0, e + 1);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 moment_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -438,13 +619,19 @@ int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp, 
 
 }  // namespace
 
+bool ps_sxy_int8() {
+  const char* e = getenv("PS_PEARSON_SXY");
+  return !(e && e[0] == 'd');
+}
+
 bool ps_moments_on(int64_t F, int64_t S) {
   if (const char* e = getenv("PS_PEARSON_MOMENTS")) return e[0] == '1';
   return F >= 2048 && S >= 256;
 }
 
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx_out,
-                       double** sq_out, int32_t** e1_out, int32_t** e2_out, cudaStream_t s) {
+                       double** sq_out, int32_t** e1_out, int32_t** e2_out, double* sxy, int32_t* nn,
+                       cudaStream_t s) {
   *sx_out = *sq_out = nullptr;
   *e1_out = *e2_out = nullptr;
   const int64_t F = a->F, S = a->S;
@@ -456,9 +643,11 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   double *sx = nullptr, *sq = nullptr;
   int8_t *dig = nullptr, *pres = nullptr;
   int32_t *e1 = nullptr, *e2 = nullptr;
+  double* rsc = nullptr;  // 2^(e1 + 1) per row (Sxy)
   auto cleanup = [&]() {
     ps_free(dig, s);
     ps_free(pres, s);
+    ps_free(rsc, s);
   };
   cudaError_t e = ps_alloc(&sx, (size_t)(F * F), s);
   if (e == cudaSuccess) e = ps_alloc(&sq, (size_t)(F * F), s);
@@ -466,6 +655,9 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   if (e == cudaSuccess) e = ps_alloc(&pres, (size_t)(F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&e1, (size_t)F, s);
   if (e == cudaSuccess) e = ps_alloc(&e2, (size_t)F, s);
+  if (e == cudaSuccess && sxy) e = ps_alloc(&rsc, (size_t)F, s);
+  if (e == cudaSuccess && sxy)
+    e = cudaFuncSetAttribute(cross_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kMomSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -494,10 +686,11 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   PS_LAUNCHED();
   presence_i8_kernel<<<(unsigned)F, 256, 0, s>>>(a->d_mask, a->W, S, Sp, pres);
   PS_LAUNCHED();
-  CUtensorMap amap[kDigits], bmap, bmap_half;
+  CUtensorMap amap[kDigits], ahalf[kDigits], bmap, bmap_half;
   int rc = make_i8_map(&bmap, pres, F, Sp);
   if (!rc) rc = make_i8_map(&bmap_half, pres, F, Sp, QN / 2);  // multicast halves
   for (int d = 0; d < kDigits && !rc; ++d) rc = make_i8_map(&amap[d], dig + d * F * Sp, F, Sp);
+  for (int d = 0; d < kDigits && !rc && sxy; ++d) rc = make_i8_map(&ahalf[d], dig + d * F * Sp, F, Sp, QN / 2);
   if (rc) {
     cleanup();
     ps_free(sx, s);
@@ -511,7 +704,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   const char* mce = getenv("PS_MOMENTS_MC");
   const bool mc = !(mce && mce[0] == '0') && ds->num_sms >= 2;
   static int max_clusters = 0;  // co-resident 2-CTA clusters (GPCs may hold an odd SM count)
-  if (mc && !max_clusters) {
+  if (!max_clusters) {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(ds->num_sms & ~1));
     lc.blockDim = dim3(QTH);
@@ -530,7 +723,21 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   auto grid_mc_of = [&](int64_t nr, int64_t nc) {
     return 2 * (int)std::min<int64_t>(((nr + 1) / 2) * nc, max_clusters > 0 ? max_clusters : 1);
   };
+  // Sxy and n over the upper triangle of the range's tile rows (int8 path)
+  const int64_t It0 = lo / QM, nIt = (hi - 1) / QM - It0 + 1;
+  auto cross = [&](const CUtensorMap& am, const CUtensorMap& bm, double w, int first, double* o, int32_t* no) {
+    const int64_t np = (nIt + 1) / 2, W0 = NTt - It0;
+    const int64_t units = np * W0 - np * (np - 1);
+    const int g = 2 * (int)std::min<int64_t>(units, max_clusters > 0 ? max_clusters : 1);
+    cross_gemm_mc_kernel<<<g, QTH, kMomSmem, s>>>(am, bm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1);
+    PS_LAUNCHED();
+  };
   ps_prof_begin("pearson_moments", s);
+  if (sxy) {
+    cross(bmap, bmap_half, 1.0, 1, nullptr, nn);  // pair counts n = M M^T
+    row_scale_kernel<<<(unsigned)ps_ceil_div(nrows, 256), 256, 0, s>>>(e1, r0, nrows, rsc);
+    PS_LAUNCHED();
+  }
   for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
     double* out = sq_pass ? sq : sx;
     const int32_t* ex = sq_pass ? e2 : e1;
@@ -549,6 +756,19 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
         PS_LAUNCHED();
       }
     }
+    if (sq_pass == 0 && sxy) {
+      // Sxy = 2^(e_i + e_j + 2) sum_{s + t <= 10} 2^-7(s+t) D_s D_t^T, folded in a
+      // fixed order (smallest weights first); terms with s + t > 10 are below
+      // 2^-60 of the row scales (the pair kernel's bound accounts for them)
+      int first = 1;
+      for (int k = 2 * kDigits; k >= 2; --k) {
+        if (k > kSxyMaxOrder) continue;
+        for (int sd = std::max(1, k - kDigits); sd <= std::min(kDigits, k - 1); ++sd) {
+          cross(amap[sd - 1], ahalf[k - sd - 1], ldexp(1.0, -7 * k), first, sxy, nullptr);
+          first = 0;
+        }
+      }
+    }
   }
   ps_prof_end(s);
   cleanup();
@@ -557,4 +777,181 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   *e1_out = e1;
   *e2_out = e2;
   return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Incremental form for ps_run (the contractions follow the input upload): the
+// rows of each uploaded chunk get their exponents, both digit-plane sets and
+// presence; every tile column block whose rows are complete then runs its
+// moment tiles (the new L of the square) and its Sxy / n triangle tiles.  Each
+// output tile is produced by exactly one block, in the same digit / product
+// order as ps_pearson_moments: bitwise identical results.
+struct ps_moments_job {
+  const ps_matrix* a = nullptr;
+  const double* xc = nullptr;
+  int64_t F = 0, S = 0, Sp = 0, NT = 0;
+  int nk = 0;
+  int8_t *dig = nullptr, *dig2 = nullptr, *pres = nullptr;
+  int32_t *e1 = nullptr, *e2 = nullptr;
+  double *rsc = nullptr, *sx = nullptr, *sq = nullptr, *sxy = nullptr;
+  int32_t* nn = nullptr;
+  CUtensorMap a1[kDigits], a1h[kDigits], a2[kDigits], bmap, bmap_half;
+  int64_t rows_done = 0, cols_done = 0;
+  int grid_cap = 1;
+};
+
+static void job_release(ps_moments_job* j, cudaStream_t s, bool outputs) {
+  ps_free(j->dig, s);
+  ps_free(j->dig2, s);
+  ps_free(j->pres, s);
+  ps_free(j->rsc, s);
+  if (outputs) {
+    ps_free(j->sx, s);
+    ps_free(j->sq, s);
+    ps_free(j->e1, s);
+    ps_free(j->e2, s);
+  }
+  delete j;
+}
+
+int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int32_t* nn, cudaStream_t s,
+                         ps_moments_job** out) {
+  *out = nullptr;
+  ps_moments_job* j = new ps_moments_job();
+  j->a = a;
+  j->xc = xc;
+  j->F = a->F;
+  j->S = a->S;
+  j->Sp = ps_round_up(std::max<int64_t>(a->S, 1), QKB);
+  j->NT = ps_ceil_div(a->F, QM);
+  j->nk = (int)(j->Sp / QKB);
+  j->sxy = sxy;
+  j->nn = nn;
+  const int64_t F = j->F, Sp = j->Sp;
+  cudaError_t e = ps_alloc(&j->sx, (size_t)(F * F), s);
+  if (e == cudaSuccess) e = ps_alloc(&j->sq, (size_t)(F * F), s);
+  if (e == cudaSuccess) e = ps_alloc(&j->dig, (size_t)(kDigits * F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&j->dig2, (size_t)(kDigits * F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&j->pres, (size_t)(F * Sp), s);
+  if (e == cudaSuccess) e = ps_alloc(&j->e1, (size_t)F, s);
+  if (e == cudaSuccess) e = ps_alloc(&j->e2, (size_t)F, s);
+  if (e == cudaSuccess) e = ps_alloc(&j->rsc, (size_t)F, s);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(moment_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(cross_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
+  if (e != cudaSuccess) {
+    job_release(j, s, true);
+    return ps_cuda_check(e, "pearson moments setup");
+  }
+  int rc = make_i8_map(&j->bmap, j->pres, F, Sp);
+  if (!rc) rc = make_i8_map(&j->bmap_half, j->pres, F, Sp, QN / 2);
+  for (int d = 0; d < kDigits && !rc; ++d) {
+    rc = make_i8_map(&j->a1[d], j->dig + d * F * Sp, F, Sp);
+    if (!rc) rc = make_i8_map(&j->a1h[d], j->dig + d * F * Sp, F, Sp, QN / 2);
+    if (!rc) rc = make_i8_map(&j->a2[d], j->dig2 + d * F * Sp, F, Sp);
+  }
+  if (rc) {
+    job_release(j, s, true);
+    return rc;
+  }
+  ps_device_state* ds = ps_state();
+  int mcl = 0;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(ds->num_sms & ~1));
+  lc.blockDim = dim3(QTH);
+  lc.dynamicSmemBytes = kMomSmem;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeClusterDimension;
+  at.val.clusterDim.x = 2;
+  at.val.clusterDim.y = 1;
+  at.val.clusterDim.z = 1;
+  lc.attrs = &at;
+  lc.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&mcl, moment_gemm_mc_kernel, &lc) != cudaSuccess || mcl <= 0)
+    mcl = ds->num_sms / 2;
+  cudaGetLastError();
+  j->grid_cap = mcl;
+  *out = j;
+  return PS_OK;
+}
+
+// rows [rows_done, r1): exponents, both digit-plane sets, presence, Sxy row scales
+int ps_moments_job_rows(ps_moments_job* j, int64_t r1, cudaStream_t s) {
+  r1 = std::min<int64_t>(r1, j->F);
+  const int64_t r0 = j->rows_done, n = r1 - r0;
+  if (n <= 0) return PS_OK;
+  const ps_matrix* a = j->a;
+  moment_scale_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, r0, j->e1, j->e2);
+  PS_LAUNCHED();
+  presence_i8_kernel<<<(unsigned)n, 256, 0, s>>>(a->d_mask, a->W, j->S, j->Sp, j->pres, r0);
+  PS_LAUNCHED();
+  moment_digit_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e1, 0, r0, j->F * j->Sp, j->dig);
+  PS_LAUNCHED();
+  moment_digit_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e2, 1, r0, j->F * j->Sp, j->dig2);
+  PS_LAUNCHED();
+  row_scale_kernel<<<(unsigned)ps_ceil_div(n, 256), 256, 0, s>>>(j->e1, r0, n, j->rsc);
+  PS_LAUNCHED();
+  j->rows_done = r1;
+  return PS_OK;
+}
+
+// tile columns [cols_done, J1) (their rows prepared): the new L of the moment
+// square and the column block of the Sxy / n triangle
+int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
+  J1 = std::min<int64_t>(J1, j->NT);
+  const int64_t J0 = j->cols_done;
+  if (J1 <= J0) return PS_OK;
+  auto gmc = [&](int64_t units) { return 2 * (int)std::min<int64_t>(std::max<int64_t>(units, 1), j->grid_cap); };
+  ps_prof_begin("pearson_moments", s);
+  for (int pass = 0; pass < 2; ++pass) {
+    double* out = pass ? j->sq : j->sx;
+    const int32_t* ex = pass ? j->e2 : j->e1;
+    for (int d = kDigits; d >= 1; --d) {
+      const CUtensorMap& am = pass ? j->a2[d - 1] : j->a1[d - 1];
+      // rows [0, J1) x columns [J0, J1), then rows [J0, J1) x columns [0, J0)
+      for (int rect = 0; rect < 2; ++rect) {
+        const int64_t ri = rect ? J0 : 0, rn = rect ? J1 - J0 : J1;
+        const int64_t ci = rect ? 0 : J0, cn = rect ? J0 : J1 - J0;
+        if (rn <= 0 || cn <= 0) continue;
+        moment_gemm_mc_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMomSmem, s>>>(am, j->bmap_half, j->nk, ri, rn, ci, cn,
+                                                                              ex, d, d == kDigits ? 1 : 0, out, j->F);
+        PS_LAUNCHED();
+      }
+    }
+  }
+  if (j->sxy) {
+    auto half_sum = [](int64_t x) -> int64_t { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); };
+    const int64_t units = (J1 - J0) + half_sum(J1) - half_sum(J0);
+    auto cross = [&](const CUtensorMap& am, const CUtensorMap& bm, double w, int first, double* o, int32_t* no) {
+      cross_gemm_mc_kernel<<<gmc(units), QTH, kMomSmem, s>>>(am, bm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o,
+                                                             no, j->F, J0);
+      PS_LAUNCHED();
+    };
+    cross(j->bmap, j->bmap_half, 1.0, 1, nullptr, j->nn);
+    int first = 1;
+    for (int k = 2 * kDigits; k >= 2; --k) {
+      if (k > kSxyMaxOrder) continue;
+      for (int sd = std::max(1, k - kDigits); sd <= std::min(kDigits, k - 1); ++sd) {
+        cross(j->a1[sd - 1], j->a1h[k - sd - 1], ldexp(1.0, -7 * k), first, j->sxy, nullptr);
+        first = 0;
+      }
+    }
+  }
+  ps_prof_end(s);
+  j->cols_done = J1;
+  return PS_OK;
+}
+
+int ps_moments_job_end(ps_moments_job* j, double** sx, double** sq, int32_t** e1, int32_t** e2, cudaStream_t s) {
+  *sx = j->sx;
+  *sq = j->sq;
+  *e1 = j->e1;
+  *e2 = j->e2;
+  job_release(j, s, false);
+  return PS_OK;
+}
+
+void ps_moments_job_abort(ps_moments_job* j, cudaStream_t s) {
+  if (j) job_release(j, s, true);
 }

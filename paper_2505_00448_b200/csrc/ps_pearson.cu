@@ -36,6 +36,7 @@ constexpr int WJ = T / (8 * WN);           // column groups of warps
 constexpr int NWARP = (T / (8 * WM)) * WJ;  // WN = 4: 4 x 2 warps of 16 x 32 pairs
 constexpr int NTHR = NWARP * 32;
 constexpr double kReplayTau = 1e-3;
+constexpr int64_t kMomBlock = 12;  // tile columns per incremental int8 launch set
 
 // MODE 0: raw values, centred and squared per use; 1: pre-centred x'
 // (squared per use); 2: pre-centred x' and x'^2 (no FP64 ALU work in the
@@ -112,6 +113,25 @@ __device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, d
   return exx > 1e-12 * sxx || eyy > 1e-12 * syy || exy > 1e-12 * sqrt(sxx * syy);
 }
 
+// Sxy from int8 digit products (ps_moments.cu, s + t <= 10): per element the
+// expansion errors give |x eps_y| + |y eps_x| <= 2^(e_g + e_h - 55) and the
+// dropped products < 2^(e_g + e_h - 60); the fp64 fold of 43 scaled exact
+// products errs by <= 43 * 2^-53 of the sum of their magnitudes, bounded (Cauchy-
+// Schwarz over the joint samples, digit excess delta = 2^-7 of the row scale) by
+// sqrt(qx qy) + delta 2^(e+1) sqrt(n q) terms.  4x margin; replay when the bound
+// exceeds 1e-12 sqrt(sxx syy).
+__device__ __forceinline__ bool sxy_imprecise(int n, double sx, double sy, double qx, double qy, int e1g, int e1h) {
+  if (n <= 1) return false;
+  const double fn = (double)n;
+  const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
+  if (!(sxx > 0.0) || !(syy > 0.0)) return false;  // replayed by the degenerate-variance rule anyway
+  const double ag = ldexp(1.0, e1g + 1), ah = ldexp(1.0, e1h + 1), dl = 0.0078125;
+  const double trunc = fn * ag * ah * ldexp(1.0, -55);
+  const double mag = sqrt(qx * qy) + dl * ag * sqrt(fn * qy) + dl * ah * sqrt(fn * qx) + fn * dl * dl * ag * ah;
+  const double bound = 4.0 * (trunc + 43.0 * ldexp(mag, -53));
+  return bound > 1e-12 * sqrt(sxx * syy);
+}
+
 // Moments -> outputs for one upper-triangular pair (g <= h).
 __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx, double sy,
                                double qx, double qy, double xy, const Outs& o) {
@@ -179,7 +199,7 @@ __global__ void pearson_p_kernel(const double* __restrict__ stat, double* __rest
 // the centred sums by more than 1e-12 are replayed exactly.
 __global__ void pearson_pairs_kernel(int64_t F, int64_t lo, int64_t hi, Outs o, const double* __restrict__ msx,
                                      const double* __restrict__ msq, const int32_t* __restrict__ me1,
-                                     const int32_t* __restrict__ me2) {
+                                     const int32_t* __restrict__ me2, int i8) {
   auto before = [&](int64_t g) { return (g - lo) * F - (g * (g - 1) - lo * (lo - 1)) / 2; };
   const int64_t total = before(hi);
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < total;
@@ -193,10 +213,12 @@ __global__ void pearson_pairs_kernel(int64_t F, int64_t lo, int64_t hi, Outs o, 
     const int64_t g = a, h = g + (it - before(g));
     const int n = o.nn[g * F + h];
     const double sx = msx[g * F + h], sy = msx[h * F + g], qx = msq[g * F + h], qy = msq[h * F + g];
-    if (g != h && moments_imprecise(n, sx, sy, qx, qy, me1[g], me2[g], me1[h], me2[h]))
+    const double xy = o.sxy[g * F + h];
+    if (g != h && (moments_imprecise(n, sx, sy, qx, qy, me1[g], me2[g], me1[h], me2[h]) ||
+                   (i8 && sxy_imprecise(n, sx, sy, qx, qy, me1[g], me1[h]))))
       replay_pair(g, h, F, o);
     else
-      pearson_finish(g, h, F, n, sx, sy, qx, qy, o.sxy[g * F + h], o);
+      pearson_finish(g, h, F, n, sx, sy, qx, qy, xy, o);
   }
 }
 
@@ -888,6 +910,7 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     if (rc) return rc;
     // large F: the four masked moments on the int8 tensor cores, Sxy alone on DMMA
     const bool mom = ps_moments_on(F, a->S);
+    const bool i8 = mom && ps_sxy_int8();  // Sxy and n from int8 digit products too: no DMMA tiles
     if (mom) {
       PS_CUDA(ps_alloc(&o.sxy, (size_t)(F * F), s));
       PS_CUDA(ps_alloc(&o.nn, (size_t)(F * F), s));
@@ -896,20 +919,23 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
                                  (int)kTmaSmem));
     PS_CUDA(cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kTmaSmemPre));
-    ps_prof_begin("pearson_tile", s);
-    if (mom)
-      pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmemPre, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o,
+    if (!i8) {
+      ps_prof_begin("pearson_tile", s);
+      if (mom)
+        pearson_tma_kernel<true><<<(unsigned)grid, NTHR, kTmaSmemPre, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o,
+                                                                           0);
+      else
+        pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o,
                                                                          0);
-    else
-      pearson_tma_kernel<false><<<(unsigned)grid, NTHR, kTmaSmem, s>>>(xmap, mpad, Wp, W, F, NT, tile0, lo, hi, o, 0);
-    ps_prof_end(s);
-    PS_LAUNCHED();
+      ps_prof_end(s);
+      PS_LAUNCHED();
+    }
     if (mom) {
       double *msx = nullptr, *msq = nullptr;
       int32_t *me1 = nullptr, *me2 = nullptr;
-      rc = ps_pearson_moments(a, xc, lo, hi, &msx, &msq, &me1, &me2, s);
+      rc = ps_pearson_moments(a, xc, lo, hi, &msx, &msq, &me1, &me2, i8 ? o.sxy : nullptr, i8 ? o.nn : nullptr, s);
       if (rc) return rc;
-      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(F, lo, hi, o, msx, msq, me1, me2);
+      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(F, lo, hi, o, msx, msq, me1, me2, i8 ? 1 : 0);
       PS_LAUNCHED();
       ps_free(msx, s);
       ps_free(msq, s);
@@ -967,7 +993,10 @@ struct ps_pearson_job {
   CUtensorMap xmap{};
   double* xc = nullptr;    // pre-centred x' (mode >= 1)
   double* xq = nullptr;    // x'^2 (mode 2)
-  bool moments = false;    // large F: moments on the int8 tensor cores, all tiles after the upload
+  bool moments = false;    // large F: moments on the int8 tensor cores
+  bool i8 = false;         // ... and Sxy / n too (no DMMA tiles): the int8 job follows the upload
+  ps_moments_job* mj = nullptr;
+  int64_t mcols = 0;       // 256-tile columns handed to the int8 job
 
   int64_t c_done = 0;      // rows centred
   int64_t J_done = 0;  // tile columns launched
@@ -1003,8 +1032,12 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
       e = cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kTmaSmemPre);
     j->moments = ps_moments_on(F, a->S);
+    j->i8 = j->moments && ps_sxy_int8();
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.sxy, (size_t)(F * F), s);
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.nn, (size_t)(F * F), s);
+    // (after Sxy / n exist: the job writes them)
+    if (e == cudaSuccess && j->i8 && ps_moments_job_begin(a, j->xc, j->o.sxy, j->o.nn, s, &j->mj) != PS_OK)
+      e = cudaErrorMemoryAllocation;
     if (e == cudaSuccess && make_pearson_map(&j->xmap, j->xc, a->ld, F) != PS_OK)
       e = cudaErrorInvalidValue;
   }
@@ -1017,6 +1050,7 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
     ps_free(j->mpad, s);
     ps_free(j->o.sxy, s);
     ps_free(j->o.nn, s);
+    ps_moments_job_abort(j->mj, s);
     delete j;
     return ps_cuda_check(e, "pearson setup");
   }
@@ -1068,6 +1102,22 @@ int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
   if (J1 <= j->J_done) return PS_OK;
   int rc0 = pearson_center_upto(j, J1 * T, s);
   if (rc0) return rc0;
+  if (j->i8) {  // rows of the chunk, then the complete 256-tile columns on a walk stream
+    const int64_t F = j->a->F, rows = j->c_done;  // centred rows only
+    const int64_t NTm = ps_ceil_div(F, kMomentTile);
+    const int64_t JM = rows >= F ? NTm : rows / kMomentTile;
+    // the whole int8 job on ONE walk stream (in order: a column block reads
+    // the digit planes of every earlier chunk), after the centring on `s`;
+    // the high-priority upload stream only centres
+    cudaStream_t w = ps_walk_stream(0, s);
+    j->nws = std::max(j->nws, 1);
+    int rc = ps_moments_job_rows(j->mj, rows, w);
+    // column blocks of at least a few tiles: single tile columns are too small
+    // launches (dozens of products each) to fill the GPU
+    if (rc || JM - j->mcols < std::min<int64_t>(kMomBlock, NTm - j->mcols)) return rc;
+    j->mcols = JM;
+    return ps_moments_job_cols(j->mj, JM, w);
+  }
   cudaStream_t w = ps_walk_stream(j->nws++, s);
   int rc = pearson_columns(j, j->J_done, J1, w);
   j->J_done = J1;
@@ -1079,13 +1129,20 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
   if (!rc) rc = pearson_center_upto(j, a->F, s);
-  if (!rc) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
+  if (!rc && !j->i8) rc = pearson_columns(j, j->J_done, ps_ceil_div(a->F, T), s);
   if (!rc && j->moments) {
     double *msx = nullptr, *msq = nullptr;
     int32_t *me1 = nullptr, *me2 = nullptr;
-    rc = ps_pearson_moments(a, j->xc, 0, a->F, &msx, &msq, &me1, &me2, s);
+    if (j->i8) {
+      rc = ps_moments_job_rows(j->mj, a->F, s);
+      if (!rc) rc = ps_moments_job_cols(j->mj, ps_ceil_div(a->F, kMomentTile), s);
+      if (!rc) rc = ps_moments_job_end(j->mj, &msx, &msq, &me1, &me2, j->home);
+      j->mj = nullptr;
+    } else {
+      rc = ps_pearson_moments(a, j->xc, 0, a->F, &msx, &msq, &me1, &me2, nullptr, nullptr, s);
+    }
     if (!rc) {
-      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(a->F, 0, a->F, j->o, msx, msq, me1, me2);
+      pearson_pairs_kernel<<<ds->num_sms * 16, 128, 0, s>>>(a->F, 0, a->F, j->o, msx, msq, me1, me2, j->i8 ? 1 : 0);
       ps_count_launch();
       if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson pairs launch");
     }
@@ -1127,5 +1184,6 @@ void ps_pearson_abort(ps_pearson_job* j, cudaStream_t s) {
   ps_free(j->mpad, j->home);
   ps_free(j->o.sxy, j->home);
   ps_free(j->o.nn, j->home);
+  ps_moments_job_abort(j->mj, j->home);
   delete j;
 }

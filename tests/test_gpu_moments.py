@@ -1,7 +1,8 @@
 """Pearson with the masked moments on the int8 tensor cores (ps_moments.cu).
 
-Large-F Pearson computes Sx = X' M^T and Sxx = X'^2 M^T from exact int8 digit
-contractions and runs only Sxy on the FP64 tensor path.  These tests force the
+Large-F Pearson computes Sx = X' M^T and Sxx = X'^2 M^T (and, by default, Sxy
+and the pair counts) from exact int8 digit contractions (PS_PEARSON_SXY=dmma:
+Sxy on the FP64 tensor tiles).  These tests force the
 path on (PS_PEARSON_MOMENTS=1) at oracle-sized shapes and check it against the
 CPU oracle (continuous.py:29-103) at the north-star tolerances, against the
 FP64-moment path, on degenerate rows (constants, large offsets, NaN data under
@@ -31,18 +32,22 @@ def _check(res, ref):
     assert p_close(res["p"], ref["p"])
 
 
+@pytest.mark.parametrize("sxy", ["int8", "dmma"])
 @pytest.mark.parametrize("na", [0.0, 0.3])
 @pytest.mark.parametrize("F,S", [(70, 333), (300, 1000), (260, 5000)])
-def test_moments_match_oracle(oracle, monkeypatch, F, S, na):
+def test_moments_match_oracle(oracle, monkeypatch, F, S, na, sxy):
     monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    monkeypatch.setenv("PS_PEARSON_SXY", sxy)
     raw = workloads.simulate(F, S, "continuous", na_ratio=na, seed=F * 11 + S + int(na * 10))
     mat = ps.make_matrix(raw, "continuous")
     req = ps.TestRequest("pearson", ("stat", "p"))
     _check(ps.run(req, mat), oracle.oracle_run(req, mat))
 
 
-def test_moments_degenerate_rows(oracle, monkeypatch):
+@pytest.mark.parametrize("sxy", ["int8", "dmma"])
+def test_moments_degenerate_rows(oracle, monkeypatch, sxy):
     monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    monkeypatch.setenv("PS_PEARSON_SXY", sxy)
     rng = np.random.default_rng(5)
     raw = rng.normal(size=(40, 700))
     raw[0] = 0.1                        # constant
