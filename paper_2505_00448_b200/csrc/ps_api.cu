@@ -487,7 +487,7 @@ int ps_matrix_create(const ps_matrix_desc* desc, int values_on_device, int want_
   return matrix_create(desc, values_on_device, want_presort, as_stream(stream), out, nullptr);
 }
 
-int ps_pearson_moments_used(int64_t F, int64_t S) { return ps_moments_on(F, S) ? (ps_sxy_int8() ? 2 : 1) : 0; }
+int ps_pearson_moments_used(int64_t F, int64_t S) { return ps_moments_on(F, S) ? (ps_sxy_int8(S) ? 2 : 1) : 0; }
 
 int ps_presort_layout(int64_t S, int64_t* ldo, int64_t* ldt) {
   if (S <= 0 || S > 65535) return ps_fail(PS_ERR_INVALID, "rank tests need 1 <= samples <= 65535");

@@ -78,7 +78,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
                        int32_t** e1, int32_t** e2, double* sxy, int32_t* nn, cudaStream_t s);
 // the large-F Pearson path also takes Sxy and n from int8 digit products (no
 // FP64 tensor tiles); PS_PEARSON_SXY=dmma keeps the DMMA Sxy tiles
-bool ps_sxy_int8();
+bool ps_sxy_int8(int64_t S);
 // incremental form (ps_run follows the upload): rows, then tile columns of 256
 struct ps_moments_job;
 int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int32_t* nn, cudaStream_t s,

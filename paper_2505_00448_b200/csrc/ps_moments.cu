@@ -619,12 +619,16 @@ int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp, 
 
 }  // namespace
 
-bool ps_sxy_int8() {
+// int8 Sxy: each digit product accumulates |d_s d_t| <= 4096 per sample in
+// int32, so the samples are capped at 2^31 / 4096 (the moments' 0/1 operand
+// allows 64x more)
+bool ps_sxy_int8(int64_t S) {
   const char* e = getenv("PS_PEARSON_SXY");
-  return !(e && e[0] == 'd');
+  return !(e && e[0] == 'd') && S <= (int64_t)(INT32_MAX / 4096);
 }
 
 bool ps_moments_on(int64_t F, int64_t S) {
+  if (S > (int64_t)(INT32_MAX / 64)) return false;  // int32 digit x presence sums
   if (const char* e = getenv("PS_PEARSON_MOMENTS")) return e[0] == '1';
   return F >= 2048 && S >= 256;
 }

@@ -910,7 +910,7 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
     if (rc) return rc;
     // large F: the four masked moments on the int8 tensor cores, Sxy alone on DMMA
     const bool mom = ps_moments_on(F, a->S);
-    const bool i8 = mom && ps_sxy_int8();  // Sxy and n from int8 digit products too: no DMMA tiles
+    const bool i8 = mom && ps_sxy_int8(a->S);  // Sxy and n from int8 digit products too: no DMMA tiles
     if (mom) {
       PS_CUDA(ps_alloc(&o.sxy, (size_t)(F * F), s));
       PS_CUDA(ps_alloc(&o.nn, (size_t)(F * F), s));
@@ -1032,7 +1032,7 @@ int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStre
       e = cudaFuncSetAttribute(pearson_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)kTmaSmemPre);
     j->moments = ps_moments_on(F, a->S);
-    j->i8 = j->moments && ps_sxy_int8();
+    j->i8 = j->moments && ps_sxy_int8(a->S);
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.sxy, (size_t)(F * F), s);
     if (e == cudaSuccess && j->moments) e = ps_alloc(&j->o.nn, (size_t)(F * F), s);
     // (after Sxy / n exist: the job writes them)

@@ -30,7 +30,7 @@ for c in "${CFGL[@]}"; do
   python tools/summarize_launches.py $OUT/launches_$n.csv $OUT/launches_$n.json > $OUT/launches_$n.txt 2>/dev/null
 done
 if [ "${2:-}" = "full" ]; then
-  for spec in "5 --scale 0.15:pearson_tma" "5 --scale 0.15:moment_gemm" "2:spearman_walk" "5s:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm"; do
+  for spec in "5 --scale 0.15:cross_gemm" "5 --scale 0.15:moment_gemm" "2:spearman_walk" "5s:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm"; do
     c=${spec%%:*}; k=${spec##*:}
     n=$(echo $c | sed 's/ --test /_/; s/ --scale /_s/')
     timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
