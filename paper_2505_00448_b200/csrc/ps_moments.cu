@@ -410,6 +410,15 @@ moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_con
   if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
+// Up to kCrossGroup digit products of one weight concatenated along K: one
+// exact int32 accumulation per tile (|sum| <= g 4096 S < 2^31), one fold.
+constexpr int kCrossGroup = 4;
+struct CrossMaps {
+  CUtensorMap a[kCrossGroup];  // 256-row boxes (own rows)
+  CUtensorMap b[kCrossGroup];  // 128-row boxes (multicast halves of the column tile)
+  int g;                       // products in the group
+};
+
 // Cross products over the upper triangle of tiles: out(i, j) (+)= w rs_i cs_j
 // (A B^T)(i, j) for the tile rows [I0, I0 + nI) and columns J >= I (Sxy from
 // digit planes s of rows i and t of rows j, w = 2^-7(s+t), rs = cs = 2^(e1+1));
@@ -418,7 +427,7 @@ moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_con
 // the pair (I0 + 2p, I0 + 2p + 1) walks columns J >= I0 + 2p (one lower tile
 // per pair is computed and never read).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTH, 1)
-cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int nk,
+cross_gemm_mc_kernel(const __grid_constant__ CrossMaps maps, int nk,
                      int64_t I0, int64_t nI, int64_t NT, const double* __restrict__ rs, const double* __restrict__ cs,
                      double w, int first, double* __restrict__ out, int32_t* __restrict__ nout, int64_t F,
                      int64_t Jlo) {
@@ -470,10 +479,12 @@ cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
     tc05::mbar_init(&accempty, 128);
     tc05::fence_barrier_init();
   }
-  if (tid == 4 * 32) {
-    tc05::prefetch_tmap(&amap);
-    tc05::prefetch_tmap(&bmap);
-  }
+  if (tid == 4 * 32)
+    for (int m = 0; m < maps.g; ++m) {
+      tc05::prefetch_tmap(&maps.a[m]);
+      tc05::prefetch_tmap(&maps.b[m]);
+    }
+  const int nkt = nk * maps.g;  // concatenated K steps
   tc05::fence_before_sync();
   tc05::cluster_sync();
   tc05::fence_after_sync();
@@ -488,13 +499,15 @@ cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
         const int64_t ip = 2 * pr + rank;
         const bool own = ip < nI;
         const int I = (int)(I0 + ip);
-        for (int kc = 0; kc < nk; ++kc, ++q) {
+        for (int kt = 0; kt < nkt; ++kt, ++q) {
+          const int m = kt / nk, kc = kt - m * nk;
           const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
           if (n > 0) tc05::mbar_wait(&empty[st], (uint32_t)((n - 1) & 1));
           const uint32_t sa = sbase + st * QSTAGE_BYTES, sb = sa + QA_BYTES;
           tc05::mbar_arrive_expect_tx(&full[st], own ? QSTAGE_BYTES : QB_BYTES);
-          tc05::tma_load_2d_mc(sb + rank * QHALF, &bmap, kc * QKB, (int)J * QN + rank * 128, &full[st], (uint16_t)3);
-          if (own) tc05::tma_load_2d(sa, &amap, kc * QKB, I * QM, &full[st]);
+          tc05::tma_load_2d_mc(sb + rank * QHALF, &maps.b[m], kc * QKB, (int)J * QN + rank * 128, &full[st],
+                               (uint16_t)3);
+          if (own) tc05::tma_load_2d(sa, &maps.a[m], kc * QKB, I * QM, &full[st]);
         }
       }
     }
@@ -511,7 +524,7 @@ cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
           tc05::mbar_wait(&accempty, (uint32_t)((seg - 1) & 1));
           tc05::fence_after_sync();
         }
-        for (int kc = 0; kc < nk; ++kc, ++q) {
+        for (int kt = 0; kt < nkt; ++kt, ++q) {
           const int st = (int)(q % QSTAGES), n = (int)(q / QSTAGES);
           tc05::mbar_wait(&full[st], (uint32_t)(n & 1));
           tc05::fence_after_sync();
@@ -520,7 +533,7 @@ cross_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
 #pragma unroll
             for (int kk = 0; kk < QKB / 32; ++kk) {
               const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
-              const uint32_t acc = (kc > 0 || kk > 0) ? 1u : 0u;
+              const uint32_t acc = (kt > 0 || kk > 0) ? 1u : 0u;
               tc05::mma_i8(tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
               tc05::mma_i8(tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * QKB + kk * 32), bd, idesc, acc);
             }
@@ -618,6 +631,27 @@ int make_i8_map(CUtensorMap* map, const int8_t* base, int64_t rows, int64_t Sp, 
 }
 
 }  // namespace
+
+// The Sxy digit products in fold order (smallest weights first, s ascending),
+// same-weight products grouped by up to kCrossGroup (as many as int32 allows
+// for S samples) into one K-concatenated contraction: emit(group maps, weight)
+template <class A, class B, class Emit>
+static void sxy_groups(int64_t S, const A& amaps, const B& bmaps, Emit&& emit) {
+  const int gmax = (int)std::max<int64_t>(1, std::min<int64_t>(kCrossGroup, (int64_t)INT32_MAX / (4096 * S)));
+  for (int k = kSxyMaxOrder; k >= 2; --k) {
+    CrossMaps cm;
+    cm.g = 0;
+    for (int sd = std::max(1, k - kDigits); sd <= std::min(kDigits, k - 1); ++sd) {
+      cm.a[cm.g] = amaps[sd - 1];
+      cm.b[cm.g] = bmaps[k - sd - 1];
+      if (++cm.g == gmax) {
+        emit(cm, ldexp(1.0, -7 * k));
+        cm.g = 0;
+      }
+    }
+    if (cm.g) emit(cm, ldexp(1.0, -7 * k));
+  }
+}
 
 // int8 Sxy: each digit product accumulates |d_s d_t| <= 4096 per sample in
 // int32, so the samples are capped at 2^31 / 4096 (the moments' 0/1 operand
@@ -729,16 +763,20 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   };
   // Sxy and n over the upper triangle of the range's tile rows (int8 path)
   const int64_t It0 = lo / QM, nIt = (hi - 1) / QM - It0 + 1;
-  auto cross = [&](const CUtensorMap& am, const CUtensorMap& bm, double w, int first, double* o, int32_t* no) {
+  auto cross = [&](const CrossMaps& cm, double w, int first, double* o, int32_t* no) {
     const int64_t np = (nIt + 1) / 2, W0 = NTt - It0;
     const int64_t units = np * W0 - np * (np - 1);
     const int g = 2 * (int)std::min<int64_t>(units, max_clusters > 0 ? max_clusters : 1);
-    cross_gemm_mc_kernel<<<g, QTH, kMomSmem, s>>>(am, bm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1);
+    cross_gemm_mc_kernel<<<g, QTH, kMomSmem, s>>>(cm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1);
     PS_LAUNCHED();
   };
   ps_prof_begin("pearson_moments", s);
   if (sxy) {
-    cross(bmap, bmap_half, 1.0, 1, nullptr, nn);  // pair counts n = M M^T
+    CrossMaps cn1;
+    cn1.g = 1;
+    cn1.a[0] = bmap;
+    cn1.b[0] = bmap_half;
+    cross(cn1, 1.0, 1, nullptr, nn);  // pair counts n = M M^T
     row_scale_kernel<<<(unsigned)ps_ceil_div(nrows, 256), 256, 0, s>>>(e1, r0, nrows, rsc);
     PS_LAUNCHED();
   }
@@ -765,13 +803,10 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
       // fixed order (smallest weights first); terms with s + t > 10 are below
       // 2^-60 of the row scales (the pair kernel's bound accounts for them)
       int first = 1;
-      for (int k = 2 * kDigits; k >= 2; --k) {
-        if (k > kSxyMaxOrder) continue;
-        for (int sd = std::max(1, k - kDigits); sd <= std::min(kDigits, k - 1); ++sd) {
-          cross(amap[sd - 1], ahalf[k - sd - 1], ldexp(1.0, -7 * k), first, sxy, nullptr);
-          first = 0;
-        }
-      }
+      sxy_groups(S, amap, ahalf, [&](const CrossMaps& cm, double w) {
+        cross(cm, w, first, sxy, nullptr);
+        first = 0;
+      });
     }
   }
   ps_prof_end(s);
@@ -927,20 +962,21 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
   if (j->sxy) {
     auto half_sum = [](int64_t x) -> int64_t { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); };
     const int64_t units = (J1 - J0) + half_sum(J1) - half_sum(J0);
-    auto cross = [&](const CUtensorMap& am, const CUtensorMap& bm, double w, int first, double* o, int32_t* no) {
-      cross_gemm_mc_kernel<<<gmc(units), QTH, kMomSmem, s>>>(am, bm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o,
-                                                             no, j->F, J0);
+    auto cross = [&](const CrossMaps& cm, double w, int first, double* o, int32_t* no) {
+      cross_gemm_mc_kernel<<<gmc(units), QTH, kMomSmem, s>>>(cm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o, no,
+                                                             j->F, J0);
       PS_LAUNCHED();
     };
-    cross(j->bmap, j->bmap_half, 1.0, 1, nullptr, j->nn);
+    CrossMaps cn1;
+    cn1.g = 1;
+    cn1.a[0] = j->bmap;
+    cn1.b[0] = j->bmap_half;
+    cross(cn1, 1.0, 1, nullptr, j->nn);
     int first = 1;
-    for (int k = 2 * kDigits; k >= 2; --k) {
-      if (k > kSxyMaxOrder) continue;
-      for (int sd = std::max(1, k - kDigits); sd <= std::min(kDigits, k - 1); ++sd) {
-        cross(j->a1[sd - 1], j->a1h[k - sd - 1], ldexp(1.0, -7 * k), first, j->sxy, nullptr);
-        first = 0;
-      }
-    }
+    sxy_groups(j->S, j->a1, j->a1h, [&](const CrossMaps& cm, double w) {
+      cross(cm, w, first, j->sxy, nullptr);
+      first = 0;
+    });
   }
   ps_prof_end(s);
   j->cols_done = J1;

@@ -24,9 +24,10 @@ def main():
     out = {"note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel: from the "
                    "full-size `ncu --set full` capture where one exists (ncu_summary.json, configs 2, 3, 4:anova, "
                    "4:kruskal, 5s), else averaged over the ncu launch-list pass (launches_<config>.json; "
-                   "config 5's pearson_tma is the Sxy tile kernel of the int8-moments path)."}
+                   "config 5: cross_gemm_mc, the int8 Sxy digit-product GEMM of the all-int8 Pearson path)."}
     for name, (key, test) in CONFIGS.items():
-        kern = "pearson_tile" if name == "1" else KERNEL[test]  # config 1: split-K cp.async tiles
+        # config 1: split-K cp.async tiles; config 5: the int8 Sxy cross GEMM (all-int8 path)
+        kern = "pearson_tile" if name == "1" else "cross_gemm" if name == "5" else KERNEL[test]
         val = None
         rep = f"ncu_{name}_{kern}.ncu-rep"
         if rep in full:
