@@ -74,6 +74,9 @@ struct ps_matrix {
 bool ps_moments_on(int64_t F, int64_t S);
 // digits of the expansion: each expanded term is within 2^(e - 7 kMomentDigits) of x'
 constexpr int kMomentDigits = 8;
+// Sx uses the top 7 digit planes (its truncation error 2^(e - 49) enters the
+// centred sums only through Sx^2 / n and Sx Sy / n)
+constexpr int kSxDigits = 7;
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx, double** sq,
                        int32_t** e1, int32_t** e2, double* sxy, int32_t* nn, cudaStream_t s);
 // the large-F Pearson path also takes Sxy and n from int8 digit products (no

@@ -785,16 +785,17 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
     const int32_t* ex = sq_pass ? e2 : e1;
     moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, sq_pass, r0, F * Sp, dig);
     PS_LAUNCHED();
-    for (int d = kDigits; d >= 1; --d) {  // least significant digit first (fixed fold order)
+    const int nd = sq_pass ? kDigits : kSxDigits;  // Sx: the top 7 planes (its error enters only via Sx^2 / n)
+    for (int d = nd; d >= 1; --d) {  // least significant digit first (fixed fold order)
       for (int rect = 0; rect < 2; ++rect) {
         const int64_t ri = rect ? I2 : I0, rn = rect ? nI2 : nI, cn = rect ? nJ2 : nJ;
         if (rn <= 0 || cn <= 0) continue;
         if (mc)
           moment_gemm_mc_kernel<<<grid_mc_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, ri, rn, J0, cn,
-                                                                          ex, d, d == kDigits ? 1 : 0, out, F);
+                                                                          ex, d, d == nd ? 1 : 0, out, F);
         else
           moment_gemm_kernel<<<grid_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, ri, rn, J0, cn, ex, d,
-                                                                    d == kDigits ? 1 : 0, out, F);
+                                                                    d == nd ? 1 : 0, out, F);
         PS_LAUNCHED();
       }
     }
@@ -946,7 +947,8 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
   for (int pass = 0; pass < 2; ++pass) {
     double* out = pass ? j->sq : j->sx;
     const int32_t* ex = pass ? j->e2 : j->e1;
-    for (int d = kDigits; d >= 1; --d) {
+    const int nd = pass ? kDigits : kSxDigits;
+    for (int d = nd; d >= 1; --d) {
       const CUtensorMap& am = pass ? j->a2[d - 1] : j->a1[d - 1];
       // rows [0, J1) x columns [J0, J1), then rows [J0, J1) x columns [0, J0)
       for (int rect = 0; rect < 2; ++rect) {
@@ -954,7 +956,7 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
         const int64_t ci = rect ? 0 : J0, cn = rect ? J0 : J1 - J0;
         if (rn <= 0 || cn <= 0) continue;
         moment_gemm_mc_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMomSmem, s>>>(am, j->bmap_half, j->nk, ri, rn, ci, cn,
-                                                                              ex, d, d == kDigits ? 1 : 0, out, j->F);
+                                                                              ex, d, d == nd ? 1 : 0, out, j->F);
         PS_LAUNCHED();
       }
     }

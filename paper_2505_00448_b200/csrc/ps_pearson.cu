@@ -102,9 +102,10 @@ __device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, d
                                                   int e2g, int e1h, int e2h) {
   if (n <= 1) return false;
   const double fn = (double)n;
-  constexpr int kB = 7 * kMomentDigits - 2;  // 4x the bound
-  const double d1g = ldexp(1.0, e1g - kB), d2g = ldexp(1.0, e2g - kB);
-  const double d1h = ldexp(1.0, e1h - kB), d2h = ldexp(1.0, e2h - kB);
+  constexpr int kB = 7 * kMomentDigits - 2;  // 4x the bound (Sxx: rounded at digit 8)
+  constexpr int kB1 = 7 * kSxDigits - 3;     // 8x the bound (Sx: truncated after digit 7, ~2^(e - 49))
+  const double d1g = ldexp(1.0, e1g - kB1), d2g = ldexp(1.0, e2g - kB);
+  const double d1h = ldexp(1.0, e1h - kB1), d2h = ldexp(1.0, e2h - kB);
   const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
   if (!(sxx > 0.0) || !(syy > 0.0)) return false;  // the degenerate-variance rule replays it anyway
   const double exx = fn * d2g + 2.0 * fabs(sx) * d1g + 1e-15 * qx;
