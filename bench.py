@@ -427,15 +427,15 @@ def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, 
         desc = "4 k_g FP64 flops"
     elif test == "pearson" and moments_path(wl) == 2:
         # every contraction on the int8 tensor cores (prof region pearson_moments):
-        # Sx, Sxx over ordered pairs (8 digits x 2 moments x 2 ops), Sxy over the
-        # triangle (43 digit products x 2 ops), pair counts (2 ops)
+        # Sx, Sxx over ordered pairs (7 + 8 digits x 2 ops), Sxy over the
+        # triangle (36 digit products x 2 ops), pair counts (2 ops)
         F = wl.Fa
-        ops = ((7 + 8) * 2.0 * F * F + (43 * 2.0 + 2.0) * F * (F + 1) / 2) * S / world
+        ops = ((7 + 8) * 2.0 * F * F + (36 * 2.0 + 2.0) * F * (F + 1) / 2) * S / world
         peak = peaks["tcgen05_i8_tops"]
         achieved = ops / (launch_ms / 1e3) / 1e12
         bound, unit = "tensor", "TOPS"
-        desc = ("148 int8 ops per pair-sample (tcgen05 kind::i8 exact digit contractions: Sx, Sy 7 digits, "
-                "Sxx, Syy 8 digits, Sxy 43 digit products, n)")
+        desc = ("134 int8 ops per pair-sample (tcgen05 kind::i8 exact digit contractions: Sx, Sy 7 digits, "
+                "Sxx, Syy 8 digits, Sxy 36 digit products s + t <= 9, n)")
     elif bound == "tensor":
         if test == "pearson" and moments_path(wl) == 1:
             per_ps = 2.0  # Sxy alone on DMMA; Sx, Sxx, Sy, Syy on the int8 tensor cores

@@ -54,6 +54,7 @@ int init_state(ps_device_state* st, int dev) {
   for (auto& w : st->walk) PS_CUDA(cudaStreamCreateWithFlags(&w, cudaStreamNonBlocking));
   for (auto& e : st->walk_ev) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   PS_CUDA(cudaEventCreateWithFlags(&st->alloc_ev, cudaEventDisableTiming));
+  PS_CUDA(cudaEventCreateWithFlags(&st->stat_ev, cudaEventDisableTiming));
   // keep freed workspace cached in the stream-ordered pool between calls
   cudaMemPool_t pool;
   PS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -766,11 +767,13 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     return rc;
   }
   tr.mark("matrices");
+  bool stat_early = false;  // the statistic matrices are final before the p-values
   if (!rc) {
     switch (test) {
       case PS_TEST_PEARSON:
         if (pjob) {
-          rc = ps_pearson_end(pjob, s);
+          rc = ps_pearson_end(pjob, s, st->stat_ev);
+          stat_early = !rc;
           pjob = nullptr;
         } else {
           rc = ps_pearson_run(ma, 0, rows, d_out[0], d_out[1], d_out[2], s);
@@ -819,6 +822,24 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     for (int k = 0; k < 3; ++k)
       if (adj_outs && adj_outs[k]) ps_host_prefault(adj_outs[k], sizeof(double) * cells);
   }
+  // Pearson: r (and r^2) are final before the p-value pass; their D2H runs
+  // on a walk stream while the device evaluates the p-values
+  bool early[4] = {false, false, false, false};
+  if (!rc && stat_early && outs) {
+    void* hd[2];
+    const void* ds_[2];
+    size_t nb[2];
+    for (int q = 0; q < 2; ++q) {
+      const int k = q ? 2 : 0;
+      hd[q] = outs[k];
+      ds_[q] = d_out[k];
+      nb[q] = outs[k] && d_out[k] ? sizeof(double) * cells : 0;
+      early[k] = nb[q] != 0;
+    }
+    cudaError_t e = cudaStreamWaitEvent(st->walk[0], st->stat_ev, 0);
+    rc = e != cudaSuccess ? ps_cuda_check(e, "stat handoff") : ps_stage_d2h_many(2, hd, ds_, nb, st->walk[0]);
+    g_tl.mark("stat d2h done", st->walk[0]);
+  }
   if (!rc) rc = drain_errors(s);
   g_tl.mark("compute done", s);
   tr.mark("compute");
@@ -855,7 +876,7 @@ int ps_run(int test, const ps_matrix_desc* a, const ps_matrix_desc* b, int t_var
     for (int k = 0; k < 4; ++k) {
       hd[k] = outs[k];
       ds_[k] = d_out[k];
-      nb[k] = outs[k] && d_out[k] ? sizeof(double) * cells : 0;
+      nb[k] = outs[k] && d_out[k] && !early[k] ? sizeof(double) * cells : 0;
     }
     rc = ps_stage_d2h_many(4, hd, ds_, nb, s);
   }

@@ -77,6 +77,13 @@ constexpr int kMomentDigits = 8;
 // Sx uses the top 7 digit planes (its truncation error 2^(e - 49) enters the
 // centred sums only through Sx^2 / n and Sx Sy / n)
 constexpr int kSxDigits = 7;
+// Sxy keeps the digit products D_s D_t^T with s + t <= kSxyMaxOrder (36 of
+// the 64).  The dropped ones (s + t >= 10, |d_s d_t| <= 4096) sum to below
+// 7.06 * 2^-58 < 2^-55.1 of 2^(e_g + e_h + 2) per element; with the
+// expansion error 2^(e_g + e_h - 55) the per-element error stays below
+// 2^-54 of 2^(e_g + e_h + 2) (ps_pearson.cu sxy_imprecise).
+constexpr int kSxyMaxOrder = 9;
+constexpr int kSxyProducts = 36;  // pairs s, t in [1, 8] with s + t <= 9
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx, double** sq,
                        int32_t** e1, int32_t** e2, double* sxy, int32_t* nn, cudaStream_t s);
 // the large-F Pearson path also takes Sxy and n from int8 digit products (no
@@ -110,6 +117,7 @@ struct ps_device_state {
   cudaStream_t walk[kWalkStreams] = {};  // incremental rank walks during uploads
   cudaEvent_t walk_ev[kWalkStreams + 1] = {};
   cudaEvent_t alloc_ev = nullptr;  // orders allocations made on `stream` before work on `aux`
+  cudaEvent_t stat_ev = nullptr;   // ps_run: a test's statistic matrix is final (early D2H)
 };
 
 ps_device_state* ps_state();                 // current device's state
@@ -169,7 +177,9 @@ struct ps_pearson_job;
 // Incremental Pearson tiles (outputs must exist when the job begins).
 int ps_pearson_begin(ps_matrix* a, double* stat, double* p, double* r2, cudaStream_t s, ps_pearson_job** job);
 int ps_pearson_upto(ps_pearson_job* job, int64_t h1, cudaStream_t s);
-int ps_pearson_end(ps_pearson_job* job, cudaStream_t s);
+// stat_ready (optional): recorded on s once the statistic and effect-size
+// matrices are final (before the deferred p-value pass)
+int ps_pearson_end(ps_pearson_job* job, cudaStream_t s, cudaEvent_t stat_ready = nullptr);
 void ps_pearson_abort(ps_pearson_job* job, cudaStream_t s);
 struct ps_group_job;
 // Incremental ANOVA / t-test moment contraction (as the Spearman job).

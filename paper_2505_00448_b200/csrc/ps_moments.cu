@@ -31,7 +31,6 @@
 namespace {
 
 constexpr int kDigits = kMomentDigits;
-constexpr int kSxyMaxOrder = 10;  // digit products with s + t <= 10 enter Sxy
 constexpr int QM = 256, QN = 256, QKB = 128;  // tile rows, cols, K bytes per stage
 constexpr int QSTAGES = 3;
 constexpr int QA_BYTES = QM * QKB, QB_BYTES = QN * QKB;
@@ -800,9 +799,9 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
       }
     }
     if (sq_pass == 0 && sxy) {
-      // Sxy = 2^(e_i + e_j + 2) sum_{s + t <= 10} 2^-7(s+t) D_s D_t^T, folded in a
-      // fixed order (smallest weights first); terms with s + t > 10 are below
-      // 2^-60 of the row scales (the pair kernel's bound accounts for them)
+      // Sxy = 2^(e_i + e_j + 2) sum_{s + t <= 9} 2^-7(s+t) D_s D_t^T, folded in a
+      // fixed order (smallest weights first); the terms with s + t >= 10 are
+      // below 2^-55.1 of the row scales (the pair kernel's bound accounts for them)
       int first = 1;
       sxy_groups(S, amap, ahalf, [&](const CrossMaps& cm, double w) {
         cross(cm, w, first, sxy, nullptr);

@@ -78,6 +78,14 @@ struct Outs {
   int32_t* nn = nullptr;
 };
 
+// Pearson p = 2 I_{(1-|r|)/2}(n/2 - 1, n/2 - 1): the division-free continued
+// fraction (PS_P_LENTZ: the reference's Lentz form, for A/B builds)
+#ifdef PS_P_LENTZ
+#define PS_BETA_SYM psf::beta_sym_sf
+#else
+#define PS_BETA_SYM psf::beta_sym_sf_nodiv
+#endif
+
 __device__ __forceinline__ void put(double* o, int64_t F, int64_t g, int64_t h, double v) {
   if (o) {
     o[g * F + h] = v;
@@ -114,10 +122,11 @@ __device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, d
   return exx > 1e-12 * sxx || eyy > 1e-12 * syy || exy > 1e-12 * sqrt(sxx * syy);
 }
 
-// Sxy from int8 digit products (ps_moments.cu, s + t <= 10): per element the
-// expansion errors give |x eps_y| + |y eps_x| <= 2^(e_g + e_h - 55) and the
-// dropped products < 2^(e_g + e_h - 60); the fp64 fold of 43 scaled exact
-// products errs by <= 43 * 2^-53 of the sum of their magnitudes, bounded (Cauchy-
+// Sxy from int8 digit products (ps_moments.cu, s + t <= kSxyMaxOrder = 9): per
+// element the expansion errors give |x eps_y| + |y eps_x| <= 2^(e_g + e_h - 55)
+// and the dropped products < 2^(e_g + e_h - 53.1), together < 2^-54 of
+// ag ah = 2^(e_g + e_h + 2); the fp64 fold of 36 scaled exact
+// products errs by <= 36 * 2^-53 of the sum of their magnitudes, bounded (Cauchy-
 // Schwarz over the joint samples, digit excess delta = 2^-7 of the row scale) by
 // sqrt(qx qy) + delta 2^(e+1) sqrt(n q) terms.  4x margin; replay when the bound
 // exceeds 1e-12 sqrt(sxx syy).
@@ -127,9 +136,9 @@ __device__ __forceinline__ bool sxy_imprecise(int n, double sx, double sy, doubl
   const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
   if (!(sxx > 0.0) || !(syy > 0.0)) return false;  // replayed by the degenerate-variance rule anyway
   const double ag = ldexp(1.0, e1g + 1), ah = ldexp(1.0, e1h + 1), dl = 0.0078125;
-  const double trunc = fn * ag * ah * ldexp(1.0, -55);
+  const double trunc = fn * ag * ah * ldexp(1.0, -54);
   const double mag = sqrt(qx * qy) + dl * ag * sqrt(fn * qy) + dl * ah * sqrt(fn * qx) + fn * dl * dl * ag * ah;
-  const double bound = 4.0 * (trunc + 43.0 * ldexp(mag, -53));
+  const double bound = 4.0 * (trunc + (double)kSxyProducts * ldexp(mag, -53));
   return bound > 1e-12 * sqrt(sxx * syy);
 }
 
@@ -154,7 +163,7 @@ __device__ void pearson_finish(int64_t g, int64_t h, int64_t F, int n, double sx
       if (o.defer_p) {
         p = fn;  // pearson_p_kernel: p from (r, n) at full occupancy
       } else {
-        p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, o.err);
+        p = 2.0 * PS_BETA_SYM(fabs(r), 0.5 * fn - 1.0, o.err);
         if (p > 1.0) p = 1.0;
       }
     }
@@ -187,7 +196,7 @@ __global__ void pearson_p_kernel(const double* __restrict__ stat, double* __rest
     const double fn = pout[g * F + h];
     if (fn != fn) continue;
     const double r = stat[g * F + h];
-    double p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * fn - 1.0, err);
+    double p = 2.0 * PS_BETA_SYM(fabs(r), 0.5 * fn - 1.0, err);
     if (p > 1.0) p = 1.0;
     pout[g * F + h] = p;
     pout[h * F + g] = p;
@@ -738,8 +747,12 @@ __global__ void pearson_replay_kernel(const double* __restrict__ vals, int64_t l
         if (r > 1.0) r = 1.0;
         else if (r < -1.0) r = -1.0;
         if (n != 2) {
-          p = 2.0 * psf::beta_sym_sf(fabs(r), 0.5 * (double)n - 1.0, o.err);
-          if (p > 1.0) p = 1.0;
+          if (o.defer_p) {
+            p = (double)n;  // parked: pearson_p_kernel evaluates the tail from (r, n)
+          } else {
+            p = 2.0 * PS_BETA_SYM(fabs(r), 0.5 * (double)n - 1.0, o.err);
+            if (p > 1.0) p = 1.0;
+          }
         }
       }
     }
@@ -962,14 +975,14 @@ int ps_pearson_run(ps_matrix* a, int64_t lo, int64_t hi, double* stat, double* p
                                                         o);
     PS_LAUNCHED();
   }
-  if (o.defer_p) {
-    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(stat, p, F, lo, hi, ds->d_err);
-    PS_LAUNCHED();
-  }
-  {
+  {  // replays first: with deferred p they park n for the p-value pass
     const int blocks = ds->num_sms * 4;
     pearson_replay_kernel<<<blocks, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, W, a->S, F, o.replay,
                                                 o.replay_count, cap, lo, hi, o);
+    PS_LAUNCHED();
+  }
+  if (o.defer_p) {
+    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(stat, p, F, lo, hi, ds->d_err);
     PS_LAUNCHED();
   }
   ps_free(o.replay, s);
@@ -1125,7 +1138,7 @@ int ps_pearson_upto(ps_pearson_job* j, int64_t h1, cudaStream_t s) {
   return rc;
 }
 
-int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
+int ps_pearson_end(ps_pearson_job* j, cudaStream_t s, cudaEvent_t stat_ready) {
   ps_device_state* ds = ps_state();
   int rc = ps_walk_streams_join(j->nws, s);
   ps_matrix* a = j->a;
@@ -1152,16 +1165,22 @@ int ps_pearson_end(ps_pearson_job* j, cudaStream_t s) {
     ps_free(me1, s);
     ps_free(me2, s);
   }
-  if (!rc && j->o.defer_p) {
-    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
-    ps_count_launch();
-    if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson p launch");
-  }
+  // exact replays first (with deferred p they park n like the tiles), so the
+  // statistic matrices are final before the p-value pass
   if (!rc) {
     pearson_replay_kernel<<<ds->num_sms * 4, 64, 0, s>>>(a->d_vals, a->ld, a->d_mask, a->W, a->S, a->F, j->o.replay,
                                                          j->o.replay_count, j->o.replay_cap, 0, a->F, j->o);
     ps_count_launch();
     if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson replay launch");
+  }
+  if (!rc && stat_ready) {
+    const cudaError_t e = cudaEventRecord(stat_ready, s);
+    if (e != cudaSuccess) rc = ps_cuda_check(e, "pearson stat event");
+  }
+  if (!rc && j->o.defer_p) {
+    pearson_p_kernel<<<ds->num_sms * 16, 128, 0, s>>>(j->o.stat, j->o.p, a->F, 0, a->F, ds->d_err);
+    ps_count_launch();
+    if (cudaGetLastError() != cudaSuccess) rc = ps_fail(PS_ERR_CUDA, "pearson p launch");
   }
   ps_free(j->o.replay, j->home);
   ps_free(j->o.replay_count, j->home);

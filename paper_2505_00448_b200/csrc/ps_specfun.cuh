@@ -72,6 +72,51 @@ static __device__ __noinline__ double beta_cf(double a, double b, double x, int*
   return PS_NAN;
 }
 
+// The same continued fraction without divisions (Pearson p over ~2e8 pairs:
+// the Lentz form spends three fp64 divisions per term).  Convergents A_k / B_k
+// of 1 / (1 + d_1 / (1 + d_2 / ...)) by the forward recurrence, after the
+// equivalence transformation that clears each term's denominator
+// (d_k = num / den: A_k = den A_(k-1) + num A_(k-2), the pair (A_(k-1), B_(k-1))
+// scaled by den as well, so every ratio is kept) and exact power-of-two
+// rescaling once per iteration.  Same stopping rule as beta_cf --
+// |f_k / f_(k-1) - 1| < 1e-15 after each odd term, written without the
+// division.  Differs from the Lentz evaluation only by rounding (a few ulps per
+// term; the stopping iteration can move by a few); a fraction not converged
+// within kNodivIters (n beyond ~1.5e5 joint samples for Pearson) is evaluated
+// by beta_cf itself, so the 300-iteration NonConvergence decision stays the
+// reference's.
+constexpr int kNodivIters = 240;
+static __device__ __noinline__ double beta_cf_nodiv(double a, double b, double x, int* err) {
+  const double eps = 1e-15;
+  const double qab = a + b, qap = a + 1.0, qam = a - 1.0;
+  double A1 = 1.0, A0 = 0.0, B1 = 1.0, B0 = 1.0;  // (A_k, A_(k-1)), (B_k, B_(k-1))
+  auto step = [&](double num, double den) {
+    const double a1 = fma(num, A0, den * A1), b1 = fma(num, B0, den * B1);
+    A0 = den * A1;
+    B0 = den * B1;
+    A1 = a1;
+    B1 = b1;
+  };
+  step(-qab * x, qap);
+#pragma unroll 1
+  for (int m = 1; m <= kNodivIters; ++m) {
+    const double fm = (double)m, m2 = (double)(2 * m);
+    step(fm * (b - fm) * x, (qam + m2) * (a + m2));
+    step(-(a + fm) * (qab + fm) * x, (a + m2) * (qap + m2));
+    if (fabs(fma(A1, B0, -(A0 * B1))) < eps * fabs(A0 * B1)) return A1 / B1;
+    // exact rescale by 2^-e (e: B_k's binary exponent) keeps the terms in range
+    const int e = max(-1000, min(1000, ((__double2hiint(B1) >> 20) & 0x7FF) - 1023));
+    const double sc = __hiloint2double((1023 - e) << 20, 0);
+    A1 *= sc;
+    A0 *= sc;
+    B1 *= sc;
+    B0 *= sc;
+  }
+  // near the cap the rounding of the stopping test could decide NonConvergence
+  // differently from the reference: the Lentz form decides it
+  return beta_cf(a, b, x, err);
+}
+
 __device__ __forceinline__ double reg_inc_beta(double x, double a, double b, int* err) {
   if (a <= 0.0 || b <= 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
   if (x < 0.0 || x > 1.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
@@ -82,6 +127,18 @@ __device__ __forceinline__ double reg_inc_beta(double x, double a, double b, int
   const double front = exp(ln_front);
   if (x < (a + 1.0) / (a + b + 2.0)) return front * beta_cf(a, b, x, err) / a;
   return 1.0 - front * beta_cf(b, a, 1.0 - x, err) / b;
+}
+
+__device__ __forceinline__ double reg_inc_beta_nodiv(double x, double a, double b, int* err) {
+  if (a <= 0.0 || b <= 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
+  if (x < 0.0 || x > 1.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
+  if (x == 0.0) return 0.0;
+  if (x == 1.0) return 1.0;
+  const double ln_front =
+      ln_gamma(a + b, err) - ln_gamma(a, err) - ln_gamma(b, err) + a * log(x) + b * log1p(-x);
+  const double front = exp(ln_front);
+  if (x < (a + 1.0) / (a + b + 2.0)) return front * beta_cf_nodiv(a, b, x, err) / a;
+  return 1.0 - front * beta_cf_nodiv(b, a, 1.0 - x, err) / b;
 }
 
 static __device__ __noinline__ double reg_inc_gamma_upper(double a, double x, int* err) {
@@ -145,6 +202,13 @@ __device__ __forceinline__ double beta_sym_sf(double r_abs, double a, int* err) 
   if (a <= 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
   if (r_abs < 0.0 || r_abs > 1.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
   return reg_inc_beta(0.5 * (1.0 - r_abs), a, a, err);
+}
+
+// beta_sym_sf through the division-free continued fraction (Pearson p)
+__device__ __forceinline__ double beta_sym_sf_nodiv(double r_abs, double a, int* err) {
+  if (a <= 0.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
+  if (r_abs < 0.0 || r_abs > 1.0) { ps_raise(err, PS_ERR_DOMAIN); return PS_NAN; }
+  return reg_inc_beta_nodiv(0.5 * (1.0 - r_abs), a, a, err);
 }
 
 }  // namespace psf
