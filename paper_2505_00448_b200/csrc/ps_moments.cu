@@ -412,10 +412,56 @@ moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_con
 // Up to kCrossGroup digit products of one weight concatenated along K: one
 // exact int32 accumulation per tile (|sum| <= g 4096 S < 2^31), one fold.
 constexpr int kCrossGroup = 4;
+constexpr int kCrossBand = 12;  // tile columns per band of the unit order
 struct CrossMaps {
   CUtensorMap a[kCrossGroup];  // 256-row boxes (own rows)
   CUtensorMap b[kCrossGroup];  // 128-row boxes (multicast halves of the column tile)
   int g;                       // products in the group
+};
+
+// Units of the cross GEMMs: (row pair p, column c = J - I0) with 2p <= c,
+// p < np, over the columns [cb, W0): cb = 0 for a range's whole triangle
+// (Jlo < 0), Jlo - I0 for a column block of the incremental upload.  They are
+// walked in column bands of kCrossBand tiles, row pairs outermost within a
+// band, so a wave of consecutive units covers a compact (row pairs x columns)
+// block whose operand slabs stay in L2 (a row- or column-major wave streams
+// ~3x the tiles from DRAM).
+struct CrossUnits {
+  int64_t I0, np, W0, cb, ubase, nunits;
+  __device__ static int64_t half_sum(int64_t x) { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); }  // sum_{m<x} m/2
+  __device__ int64_t ccum(int64_t x) const {  // units with c < x: sum of min(c / 2 + 1, np)
+    x = x < W0 ? x : W0;
+    return x <= 2 * np ? x + half_sum(x) : 2 * np + half_sum(2 * np) + np * (x - 2 * np);
+  }
+  __device__ CrossUnits(int64_t I0_, int64_t nI, int64_t NT, int64_t Jlo)
+      : I0(I0_), np((nI + 1) / 2), W0(NT - I0_), cb(Jlo < 0 ? 0 : Jlo - I0_) {
+    ubase = ccum(cb);
+    nunits = ccum(W0) - ubase;
+  }
+  __device__ void unit(int64_t u, int64_t& pr, int64_t& J) const {
+    int64_t a = 0, b = (W0 - cb - 1) / kCrossBand;
+    while (a < b) {
+      const int64_t m = (a + b + 1) >> 1;
+      if (ccum(cb + m * kCrossBand) - ubase <= u) a = m;
+      else b = m - 1;
+    }
+    const int64_t c0 = cb + a * kCrossBand, c1 = c0 + kCrossBand < W0 ? c0 + kCrossBand : W0, w = c1 - c0;
+    int64_t rem = u - (ccum(c0) - ubase);
+    const int64_t fr = c0 / 2 + 1 < np ? c0 / 2 + 1 : np;  // row pairs holding the whole band
+    if (rem < fr * w) {
+      pr = rem / w;
+      J = I0 + c0 + rem % w;
+      return;
+    }
+    rem -= fr * w;
+    int64_t p = fr;
+    while (rem >= c1 - 2 * p) {  // at most kCrossBand / 2 partial row pairs
+      rem -= c1 - 2 * p;
+      ++p;
+    }
+    pr = p;
+    J = I0 + 2 * p + rem;
+  }
 };
 
 // Cross products over the upper triangle of tiles: out(i, j) (+)= w rs_i cs_j
@@ -438,35 +484,9 @@ cross_gemm_mc_kernel(const __grid_constant__ CrossMaps maps, int nk,
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (int)tc05::cluster_ctarank();
   const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;
-  // Jlo < 0: row-major over the range's row pairs, columns J >= the pair's
-  // first row, up to NT.  Jlo >= 0 (incremental upload): column-major over the
-  // column block [Jlo, NT), row pairs p with I0 + 2p <= J.
-  const int64_t np = (nI + 1) / 2, W0 = NT - I0;
-  auto cum = [&](int64_t p) { return p * W0 - p * (p - 1); };  // units of row pairs [0, p)
-  auto half_sum = [](int64_t x) -> int64_t { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); };  // sum_{m<x} m/2
-  auto ccum = [&](int64_t J) { return (J - Jlo) + half_sum(J - I0) - half_sum(Jlo - I0); };  // columns [Jlo, J)
-  const int64_t nunits = Jlo < 0 ? cum(np) : ccum(NT);
-  auto unit = [&](int64_t u, int64_t& pr, int64_t& J) {
-    if (Jlo < 0) {
-      int64_t a = 0, b = np - 1;
-      while (a < b) {
-        const int64_t m = (a + b + 1) >> 1;
-        if (cum(m) <= u) a = m;
-        else b = m - 1;
-      }
-      pr = a;
-      J = I0 + 2 * a + (u - cum(a));
-    } else {
-      int64_t a = Jlo, b = NT - 1;
-      while (a < b) {
-        const int64_t m = (a + b + 1) >> 1;
-        if (ccum(m) <= u) a = m;
-        else b = m - 1;
-      }
-      J = a;
-      pr = u - ccum(a);
-    }
-  };
+  const CrossUnits cu(I0, nI, NT, Jlo);
+  const int64_t nunits = cu.nunits;
+  auto unit = [&](int64_t u, int64_t& pr, int64_t& J) { cu.unit(u, pr, J); };
 
   if (warp == 0) tc05::tmem_alloc(&tmem_base_s, 512);
   if (tid == 32) {
@@ -594,6 +614,260 @@ cross_gemm_mc_kernel(const __grid_constant__ CrossMaps maps, int nk,
   if (warp == 0) tc05::tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair forms (tcgen05 cta_group::2): the pair's 512 x 256 block as two
+// M = 256 MMAs per K slice -- rows [128 h, 128 h + 128) of each CTA's own
+// 256-row A tile against the column tile, whose two N halves sit one in each
+// CTA.  Per 128-byte K step a CTA stages 48 KB (its A tile + half of B)
+// instead of 64 KB, and each MMA reads half of B from either SM: four stages
+// fit where three did, and the shared-memory traffic (operand reads + TMA
+// fills) drops from ~156 to ~109 B / clk / SM, under the 128 B / clk port.
+// Same units, same K order, same int32 sums: bitwise the results of the
+// multicast kernels.
+constexpr int Q2STAGES = 4;
+constexpr int Q2STAGE_BYTES = QA_BYTES + QHALF;
+constexpr size_t kMom2Smem = (size_t)Q2STAGES * Q2STAGE_BYTES + 1024;
+
+struct Pipe2 {
+  uint64_t *full, *empty, *accfull, *accempty;
+  uint32_t sbase, tmem, full_leader[Q2STAGES], accempty_leader;
+  int rank;
+};
+
+// producer lane: this CTA's A tile rows and its half of the column tile for K step kx
+__device__ __forceinline__ void pipe2_load(const Pipe2& pp, int64_t q, const CUtensorMap* am, const CUtensorMap* bm,
+                                           int kx, int arow, int brow) {
+  const int st = (int)(q % Q2STAGES), n = (int)(q / Q2STAGES);
+  if (n > 0) tc05::mbar_wait(&pp.empty[st], (uint32_t)((n - 1) & 1));
+  const uint32_t sa = pp.sbase + st * Q2STAGE_BYTES, sb = sa + QA_BYTES;
+  if (pp.rank == 0) tc05::mbar_arrive_expect_tx(&pp.full[st], 2 * Q2STAGE_BYTES);
+  tc05::tma_load_2d_2sm(sa, am, kx, arow, pp.full_leader[st]);
+  tc05::tma_load_2d_2sm(sb, bm, kx, brow, pp.full_leader[st]);
+}
+
+// leader's MMA lane: one staged K step into the two accumulators
+__device__ __forceinline__ void pipe2_mma(const Pipe2& pp, int64_t q, bool first_step) {
+  constexpr uint32_t idesc = tc05::idesc_i8(256, QN, true);
+  const int st = (int)(q % Q2STAGES), n = (int)(q / Q2STAGES);
+  tc05::mbar_wait_cluster(&pp.full[st], (uint32_t)(n & 1));
+  tc05::fence_after_sync();
+  const uint32_t sa = pp.sbase + st * Q2STAGE_BYTES, sb = sa + QA_BYTES;
+#pragma unroll
+  for (int kk = 0; kk < QKB / 32; ++kk) {
+    const uint64_t bd = tc05::sw128_kmajor_desc(sb + kk * 32);
+    const uint32_t acc = (!first_step || kk > 0) ? 1u : 0u;
+    tc05::mma_i8_2sm(pp.tmem, tc05::sw128_kmajor_desc(sa + kk * 32), bd, idesc, acc);
+    tc05::mma_i8_2sm(pp.tmem + 256, tc05::sw128_kmajor_desc(sa + 128 * QKB + kk * 32), bd, idesc, acc);
+  }
+  tc05::commit_2sm(&pp.empty[st], (uint16_t)3);
+}
+
+#define PS_PIPE2_SETUP()                                                                                        \
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];                                                    \
+  __shared__ uint64_t full[Q2STAGES], empty[Q2STAGES], accfull, accempty;                                       \
+  __shared__ uint32_t tmem_base_s;                                                                              \
+  unsigned char* tsm =                                                                                          \
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));       \
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;                                                \
+  Pipe2 pp;                                                                                                     \
+  pp.full = full, pp.empty = empty, pp.accfull = &accfull, pp.accempty = &accempty;                             \
+  pp.sbase = tc05::smem_u32(tsm);                                                                               \
+  pp.rank = (int)tc05::cluster_ctarank();                                                                       \
+  const int rank = pp.rank;                                                                                     \
+  const int64_t ncl = gridDim.x / 2, cl = blockIdx.x / 2;                                                       \
+  if (warp == 0) tc05::tmem_alloc_2sm(&tmem_base_s, 512);                                                       \
+  if (tid == 32) {                                                                                              \
+    for (int i = 0; i < Q2STAGES; ++i) {                                                                        \
+      tc05::mbar_init(&full[i], 1);  /* the leader's expect_tx arrival; both CTAs' bytes */                     \
+      tc05::mbar_init(&empty[i], 1); /* the leader's commit, multicast to both */                               \
+    }                                                                                                           \
+    tc05::mbar_init(&accfull, 1);                                                                               \
+    tc05::mbar_init(&accempty, 256); /* both CTAs' epilogue threads (leader's copy is the one waited on) */     \
+    tc05::fence_barrier_init();                                                                                 \
+  }                                                                                                             \
+  for (int i = 0; i < Q2STAGES; ++i) pp.full_leader[i] = tc05::map_to_rank(&full[i], 0);                        \
+  pp.accempty_leader = tc05::map_to_rank(&accempty, 0);                                                         \
+  tc05::fence_before_sync();                                                                                    \
+  tc05::cluster_sync();                                                                                         \
+  tc05::fence_after_sync();                                                                                     \
+  pp.tmem = tmem_base_s;                                                                                        \
+  const uint32_t tmem = pp.tmem;
+
+#define PS_PIPE2_TEARDOWN()                                                      \
+  tc05::fence_before_sync();                                                     \
+  __syncthreads();                                                               \
+  tc05::cluster_sync(); /* no CTA leaves while the pair's MMAs / commits run */  \
+  if (warp == 0) tc05::tmem_dealloc_2sm(tmem, 512);
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTH, 1)
+moment_gemm_2sm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap, int nk,
+                       int64_t I0, int64_t nI, int64_t J0, int64_t nJ, const int32_t* __restrict__ rexp, int digit,
+                       int first, double* __restrict__ out, int64_t F, int bswap) {
+  PS_PIPE2_SETUP();
+  const int64_t np = (nI + 1) / 2, nunits = np * nJ;
+  if (tid == 4 * 32) {
+    tc05::prefetch_tmap(&amap);
+    tc05::prefetch_tmap(&bmap);
+  }
+  if (warp == 4) {
+    if (lane == 0) {  // TMA producer (both CTAs; a dummy partner's rows are loaded and never stored)
+      int64_t q = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        int64_t pr, cj;
+        band_unit(u, np, nJ, pr, cj);
+        const int I = (int)(I0 + 2 * pr + rank), J = (int)(J0 + cj);
+        for (int kc = 0; kc < nk; ++kc, ++q)
+          pipe2_load(pp, q, &amap, &bmap, kc * QKB, I * QM, J * QN + (rank ^ bswap) * 128);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && rank == 0) {  // MMA issuer of the pair
+      int64_t q = 0;
+      int seg = 0;
+      for (int64_t u = cl; u < nunits; u += ncl, ++seg) {
+        if (seg > 0) {  // both epilogues have drained the previous tiles
+          tc05::mbar_wait_cluster(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        for (int kc = 0; kc < nk; ++kc, ++q) pipe2_mma(pp, q, kc == 0);
+        tc05::commit_2sm(&accfull, (uint16_t)3);
+      }
+    }
+  } else {
+    int seg = 0;
+    for (int64_t u = cl; u < nunits; u += ncl, ++seg) {
+      int64_t pr, cj;
+      band_unit(u, np, nJ, pr, cj);
+      const int64_t ip = 2 * pr + rank;
+      const int64_t I = I0 + ip, J = J0 + cj;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+      if (ip < nI) {
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int64_t r = I * QM + half * 128 + warp * 32 + lane;
+          const bool rok = r < F;
+          const int ex = rok ? rexp[r] : 0;
+          const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+          double* orow = out + (rok ? r : 0) * F;
+#pragma unroll 1
+          for (int cc = 0; cc < QN / 32; ++cc) {
+            uint32_t v[32];
+            tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+            const int64_t c0 = J * QN + cc * 32;
+            if (rok) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int64_t c = c0 + j;
+                if (c < F) {
+                  const double term = (double)(int32_t)v[j] * scale;
+                  orow[c] = first ? term : orow[c] + term;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive_cluster(pp.accempty_leader);
+    }
+  }
+  PS_PIPE2_TEARDOWN();
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(QTH, 1)
+cross_gemm_2sm_kernel(const __grid_constant__ CrossMaps maps, int nk, int64_t I0, int64_t nI, int64_t NT,
+                      const double* __restrict__ rs, const double* __restrict__ cs, double w, int first,
+                      double* __restrict__ out, int32_t* __restrict__ nout, int64_t F, int64_t Jlo, int bswap) {
+  PS_PIPE2_SETUP();
+  const CrossUnits cu(I0, nI, NT, Jlo);
+  const int64_t nunits = cu.nunits;
+  if (tid == 4 * 32)
+    for (int m = 0; m < maps.g; ++m) {
+      tc05::prefetch_tmap(&maps.a[m]);
+      tc05::prefetch_tmap(&maps.b[m]);
+    }
+  const int nkt = nk * maps.g;  // concatenated K steps
+  if (warp == 4) {
+    if (lane == 0) {
+      int64_t q = 0;
+      for (int64_t u = cl; u < nunits; u += ncl) {
+        int64_t pr, J;
+        cu.unit(u, pr, J);
+        const int I = (int)(I0 + 2 * pr + rank);
+        for (int kt = 0; kt < nkt; ++kt, ++q) {
+          const int m = kt / nk, kc = kt - m * nk;
+          pipe2_load(pp, q, &maps.a[m], &maps.b[m], kc * QKB, I * QM, (int)J * QN + (rank ^ bswap) * 128);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && rank == 0) {
+      int64_t q = 0;
+      int seg = 0;
+      for (int64_t u = cl; u < nunits; u += ncl, ++seg) {
+        if (seg > 0) {
+          tc05::mbar_wait_cluster(&accempty, (uint32_t)((seg - 1) & 1));
+          tc05::fence_after_sync();
+        }
+        for (int kt = 0; kt < nkt; ++kt, ++q) pipe2_mma(pp, q, kt == 0);
+        tc05::commit_2sm(&accfull, (uint16_t)3);
+      }
+    }
+  } else {
+    int seg = 0;
+    for (int64_t u = cl; u < nunits; u += ncl, ++seg) {
+      int64_t pr, J;
+      cu.unit(u, pr, J);
+      const int64_t ip = 2 * pr + rank;
+      const int64_t I = I0 + ip;
+      tc05::mbar_wait(&accfull, (uint32_t)(seg & 1));
+      tc05::fence_after_sync();
+      if (ip < nI) {
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+          const int64_t r = I * QM + half * 128 + warp * 32 + lane;
+          const bool rok = r < F;
+          const double rsw = rok && rs ? rs[r] * w : 0.0;
+#pragma unroll 1
+          for (int cc = 0; cc < QN / 32; ++cc) {
+            uint32_t v[32];
+            tc05::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(half * 256 + cc * 32), v);
+            const int64_t c0 = J * QN + cc * 32;
+            if (!rok) continue;
+            if (nout) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j < F) nout[r * F + c0 + j] = (int32_t)v[j];
+            } else {
+              double* orow = out + r * F;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const int64_t c = c0 + j;
+                if (c < F) {
+                  const double term = (double)(int32_t)v[j] * rsw * cs[c];
+                  orow[c] = first ? term : orow[c] + term;
+                }
+              }
+            }
+          }
+        }
+      }
+      tc05::fence_before_sync();
+      tc05::mbar_arrive_cluster(pp.accempty_leader);
+    }
+  }
+  PS_PIPE2_TEARDOWN();
+}
+
+// PS_GEMM_2SM=1 selects the CTA-pair kernels (=2: column halves swapped, a
+// bring-up check that must fail).  Measured equal to the multicast kernels on
+// config 5 (both run at the power cap, DESIGN 4b), which stay the default.
+int gemm_2sm_mode() {
+  const char* e = getenv("PS_GEMM_2SM");
+  return e ? atoi(e) : 0;
+}
+
 // 2^(e1 + 1) per row (NaN for rows holding NaN / inf): the Sxy fold scales
 __global__ void row_scale_kernel(const int32_t* __restrict__ e1, int64_t f0, int64_t n, double* __restrict__ sc) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -695,6 +969,10 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   if (e == cudaSuccess && sxy) e = ps_alloc(&rsc, (size_t)F, s);
   if (e == cudaSuccess && sxy)
     e = cudaFuncSetAttribute(cross_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(cross_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMom2Smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(moment_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMom2Smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kMomSmem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(moment_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -766,7 +1044,11 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
     const int64_t np = (nIt + 1) / 2, W0 = NTt - It0;
     const int64_t units = np * W0 - np * (np - 1);
     const int g = 2 * (int)std::min<int64_t>(units, max_clusters > 0 ? max_clusters : 1);
-    cross_gemm_mc_kernel<<<g, QTH, kMomSmem, s>>>(cm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1);
+    if (gemm_2sm_mode())
+      cross_gemm_2sm_kernel<<<g, QTH, kMom2Smem, s>>>(cm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1,
+                                                      gemm_2sm_mode() == 2);
+    else
+      cross_gemm_mc_kernel<<<g, QTH, kMomSmem, s>>>(cm, nk, It0, nIt, NTt, rsc, rsc, w, first, o, no, F, -1);
     PS_LAUNCHED();
   };
   ps_prof_begin("pearson_moments", s);
@@ -789,7 +1071,10 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
       for (int rect = 0; rect < 2; ++rect) {
         const int64_t ri = rect ? I2 : I0, rn = rect ? nI2 : nI, cn = rect ? nJ2 : nJ;
         if (rn <= 0 || cn <= 0) continue;
-        if (mc)
+        if (mc && gemm_2sm_mode())
+          moment_gemm_2sm_kernel<<<grid_mc_of(rn, cn), QTH, kMom2Smem, s>>>(
+              amap[d - 1], bmap_half, nk, ri, rn, J0, cn, ex, d, d == nd ? 1 : 0, out, F, gemm_2sm_mode() == 2);
+        else if (mc)
           moment_gemm_mc_kernel<<<grid_mc_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, ri, rn, J0, cn,
                                                                           ex, d, d == nd ? 1 : 0, out, F);
         else
@@ -879,6 +1164,10 @@ int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int3
     e = cudaFuncSetAttribute(moment_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(cross_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(cross_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMom2Smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(moment_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMom2Smem);
   if (e != cudaSuccess) {
     job_release(j, s, true);
     return ps_cuda_check(e, "pearson moments setup");
@@ -954,8 +1243,12 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
         const int64_t ri = rect ? J0 : 0, rn = rect ? J1 - J0 : J1;
         const int64_t ci = rect ? 0 : J0, cn = rect ? J0 : J1 - J0;
         if (rn <= 0 || cn <= 0) continue;
-        moment_gemm_mc_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMomSmem, s>>>(am, j->bmap_half, j->nk, ri, rn, ci, cn,
-                                                                              ex, d, d == nd ? 1 : 0, out, j->F);
+        if (gemm_2sm_mode())
+          moment_gemm_2sm_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMom2Smem, s>>>(
+              am, j->bmap_half, j->nk, ri, rn, ci, cn, ex, d, d == nd ? 1 : 0, out, j->F, gemm_2sm_mode() == 2);
+        else
+          moment_gemm_mc_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMomSmem, s>>>(am, j->bmap_half, j->nk, ri, rn, ci, cn,
+                                                                                ex, d, d == nd ? 1 : 0, out, j->F);
         PS_LAUNCHED();
       }
     }
@@ -964,8 +1257,12 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
     auto half_sum = [](int64_t x) -> int64_t { return x <= 0 ? 0 : (x / 2) * ((x - 1) / 2); };
     const int64_t units = (J1 - J0) + half_sum(J1) - half_sum(J0);
     auto cross = [&](const CrossMaps& cm, double w, int first, double* o, int32_t* no) {
-      cross_gemm_mc_kernel<<<gmc(units), QTH, kMomSmem, s>>>(cm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o, no,
-                                                             j->F, J0);
+      if (gemm_2sm_mode())
+        cross_gemm_2sm_kernel<<<gmc(units), QTH, kMom2Smem, s>>>(cm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o, no,
+                                                                 j->F, J0, gemm_2sm_mode() == 2);
+      else
+        cross_gemm_mc_kernel<<<gmc(units), QTH, kMomSmem, s>>>(cm, j->nk, 0, J1, J1, j->rsc, j->rsc, w, first, o, no,
+                                                               j->F, J0);
       PS_LAUNCHED();
     };
     CrossMaps cn1;

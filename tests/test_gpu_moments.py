@@ -133,3 +133,29 @@ def test_moments_outlier_exponent_replayed(oracle, monkeypatch):
     mat = ps.make_matrix(raw, "continuous")
     req = ps.TestRequest("pearson", ("stat", "p"))
     _check(ps.run(req, mat), oracle.oracle_run(req, mat))
+
+
+@pytest.mark.parametrize("F,S", [(600, 900), (1100, 2500)])
+def test_cta_pair_gemms_bitwise_equal_multicast(monkeypatch, F, S):
+    """PS_GEMM_2SM=1 runs the int8 contractions as tcgen05 cta_group::2 pair
+    MMAs (M = 256 across the two SMs of a cluster): same units, K order and
+    int32 sums as the multicast kernels, so every output bit agrees -- on the
+    block path (odd tile-row counts leave a dummy partner CTA) and through
+    ps_run's incremental column blocks."""
+    import torch
+
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    raw = workloads.simulate(F, S, "continuous", na_ratio=0.25, seed=12)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PS_GEMM_2SM", mode)
+        dm = blocks.DeviceMatrix(raw, "continuous", np.nan, None)
+        outs = [torch.full((F, F), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
+        for lo, hi in ((0, 300), (300, F)):
+            blocks.block("pearson", dm, None, lo, hi, outs)
+        blocks.sync()
+        dm.close()
+        full = ps.run(ps.TestRequest("pearson", ("stat", "p")), ps.make_matrix(raw, "continuous"))
+        res[mode] = [o.cpu().numpy() for o in outs] + [full["stat"], full["p"]]
+    for a, b in zip(res["0"], res["1"]):
+        assert bitwise_equal(a, b)

@@ -58,6 +58,27 @@ int main() {
     const double ops = (double)p.multiProcessorCount * iters * 4 * 2.0 * 128 * 256 * 32;
     if (ops / (ms * 1e-3) > best) best = ops / (ms * 1e-3);
   }
-  printf("{\"tcgen05_i8_tops\": %.1f, \"err\": \"%s\"}\n", best / 1e12, cudaGetErrorString(cudaGetLastError()));
+  // sustained: launches back to back for ~4 s (power-capped clocks), rate of the last ~3 s
+  const double ops1 = (double)p.multiProcessorCount * iters * 4 * 2.0 * 128 * 256 * 32;
+  const int per = 50;
+  double sustained = 0, t_total = 0;
+  int counted = 0;
+  double t_counted = 0;
+  while (t_total < 4000.0) {
+    cudaEventRecord(a);
+    for (int r = 0; r < per; ++r) peak_kernel<<<p.multiProcessorCount, 128, 50 * 1024>>>(iters, d);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    t_total += ms;
+    if (t_total > 1000.0) {
+      counted += per;
+      t_counted += ms;
+    }
+  }
+  if (t_counted > 0) sustained = ops1 * counted / (t_counted * 1e-3);
+  printf("{\"tcgen05_i8_tops\": %.1f, \"tcgen05_i8_tops_sustained\": %.1f, \"err\": \"%s\"}\n", best / 1e12,
+         sustained / 1e12, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

@@ -30,7 +30,13 @@ for c in "${CFGL[@]}"; do
   python tools/summarize_launches.py $OUT/launches_$n.csv $OUT/launches_$n.json > $OUT/launches_$n.txt 2>/dev/null
 done
 if [ "${2:-}" = "full" ]; then
-  for spec in "5 --scale 0.15:cross_gemm" "5 --scale 0.15:moment_gemm" "2:spearman_walk" "5s:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm"; do
+  # the int8 GEMMs at half scale (F = 10000: full 74-cluster waves), one mid-run launch each
+  for spec in "cross_gemm:12" "moment_gemm:6"; do
+    k=${spec%%:*}; skip=${spec##*:}
+    timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -s $skip -c 1 \
+      -o $OUT/ncu_5_s0.5_$k python tools/profile_one.py --config 5 --scale 0.5 > $OUT/ncu_5_$k.log 2>&1
+  done
+  for spec in "2:spearman_walk" "5s:spearman_walk" "3:onehot_gemm_mc" "4 --test kruskal:rank_mixed_walk" "4 --test anova:group_gemm"; do
     c=${spec%%:*}; k=${spec##*:}
     n=$(echo $c | sed 's/ --test /_/; s/ --scale /_s/')
     timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 \
