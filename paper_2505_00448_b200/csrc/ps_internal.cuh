@@ -84,6 +84,11 @@ constexpr int kSxDigits = 7;
 // 2^-54 of 2^(e_g + e_h + 2) (ps_pearson.cu sxy_imprecise).
 constexpr int kSxyMaxOrder = 9;
 constexpr int kSxyProducts = 36;  // pairs s, t in [1, 8] with s + t <= 9
+// the symmetric form (S < 2^17) contracts 16 sum planes (D_s + D_t)(D_s + D_t)^T
+// and the 8 squares D_s D_s^T instead: 24 products, 48 roundings in the fold
+constexpr int kSxySymProducts = 24;
+constexpr int kSxyFoldTerms = 48;
+bool ps_sxy_sym(int64_t S);
 int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t hi, double** sx, double** sq,
                        int32_t** e1, int32_t** e2, double* sxy, int32_t* nn, cudaStream_t s);
 // the large-F Pearson path also takes Sxy and n from int8 digit products (no

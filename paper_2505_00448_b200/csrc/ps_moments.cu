@@ -144,6 +144,36 @@ __global__ void presence_i8_kernel(const uint32_t* __restrict__ mask, int64_t W,
   }
 }
 
+// Symmetric form of Sxy.  Over the upper triangle the products D_s D_t^T and
+// D_t D_s^T (s < t) are both needed; with the int8 sum plane E = D_s + D_t
+// (digits lie in [-64, 64]: no overflow)
+//   D_s D_t^T + D_t D_s^T = E E^T - D_s D_s^T - D_t D_t^T,
+// so the 36 products with s + t <= 9 become 16 sum-plane products plus the 8
+// squares D_s D_s^T with the weights c_s collected below: 24 contractions,
+// still exact int32 sums (|E E| <= 2^14 per sample: S < 2^17).
+#define PS_SYM_PAIRS(X)                                                                                   \
+  X(0, 1, 8) X(1, 2, 7) X(2, 3, 6) X(3, 4, 5) X(4, 1, 7) X(5, 2, 6) X(6, 3, 5) X(7, 1, 6) X(8, 2, 5)       \
+  X(9, 3, 4) X(10, 1, 5) X(11, 2, 4) X(12, 1, 4) X(13, 2, 3) X(14, 1, 3) X(15, 1, 2)
+constexpr int kSymPairs = 16;
+static_assert(kDigits == 8 && kSxyMaxOrder == 9, "PS_SYM_PAIRS lists s < t, s + t <= 9 over 8 digits");
+
+// E planes p (out + p * plane) of rows [f0, f0 + gridDim.x) from their digit planes
+__global__ void digit_sum_kernel(const int8_t* __restrict__ dig, int64_t plane, int64_t Sp, int64_t f0,
+                                 int8_t* __restrict__ out) {
+  const int64_t f = f0 + blockIdx.x;
+  for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
+    uint4 d[kDigits];
+#pragma unroll
+    for (int k = 0; k < kDigits; ++k) d[k] = *reinterpret_cast<const uint4*>(dig + k * plane + f * Sp + s0);
+#define PS_SYM_STORE(P, A, B)                                                                             \
+  *reinterpret_cast<uint4*>(out + (int64_t)(P)*plane + f * Sp + s0) =                                     \
+      make_uint4(__vadd4(d[A - 1].x, d[B - 1].x), __vadd4(d[A - 1].y, d[B - 1].y),                        \
+                 __vadd4(d[A - 1].z, d[B - 1].z), __vadd4(d[A - 1].w, d[B - 1].w));
+    PS_SYM_PAIRS(PS_SYM_STORE)
+#undef PS_SYM_STORE
+  }
+}
+
 // out(i, j) (+)= 2^(e_i + 1 - 7 digit) (D M^T)(i, j) over the tiles of rows
 // [I0, I0 + nI) x columns [J0, J0 + nJ) (256 x 256 each; rows / columns past F
 // are zero-filled by TMA and not written).  One persistent CTA per SM takes
@@ -926,6 +956,40 @@ static void sxy_groups(int64_t S, const A& amaps, const B& bmaps, Emit&& emit) {
   }
 }
 
+// Symmetric Sxy: the 16 sum-plane products (smallest weights first), then the
+// squares D_s D_s^T, s = 8 .. 1, with c_s = [2 s <= 9] 2^-14s - sum_{t != s, s + t <= 9} 2^-7(s+t)
+// (each exact in fp64: the powers span at most 49 bits).  One fixed fold order.
+template <class Emit>
+static void sxy_sym_products(const CUtensorMap* emaps, const CUtensorMap* ehalf, const CUtensorMap* amaps,
+                             const CUtensorMap* ahalf, Emit&& emit) {
+  static const int ps_[kSymPairs][2] = {
+#define PS_SYM_ROW(P, S_, T_) {S_, T_},
+      PS_SYM_PAIRS(PS_SYM_ROW)
+#undef PS_SYM_ROW
+  };
+  CrossMaps cm;
+  cm.g = 1;
+  for (int p = 0; p < kSymPairs; ++p) {
+    cm.a[0] = emaps[p];
+    cm.b[0] = ehalf[p];
+    emit(cm, ldexp(1.0, -7 * (ps_[p][0] + ps_[p][1])));
+  }
+  for (int sd = kDigits; sd >= 1; --sd) {
+    double c = 2 * sd <= kSxyMaxOrder ? ldexp(1.0, -14 * sd) : 0.0;
+    for (int td = kDigits; td >= 1; --td)  // smallest first: every partial sum is exact
+      if (td != sd && sd + td <= kSxyMaxOrder) c -= ldexp(1.0, -7 * (sd + td));
+    cm.a[0] = amaps[sd - 1];
+    cm.b[0] = ahalf[sd - 1];
+    emit(cm, c);
+  }
+}
+
+// the symmetric form needs |E E| <= 2^14 per sample in int32 (PS_SXY_SYM=0: the 36 products)
+bool ps_sxy_sym(int64_t S) {
+  const char* e = getenv("PS_SXY_SYM");
+  return !(e && e[0] == '0') && S <= (int64_t)(INT32_MAX / 16384);
+}
+
 // int8 Sxy: each digit product accumulates |d_s d_t| <= 4096 per sample in
 // int32, so the samples are capped at 2^31 / 4096 (the moments' 0/1 operand
 // allows 64x more)
@@ -955,7 +1019,10 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   int8_t *dig = nullptr, *pres = nullptr;
   int32_t *e1 = nullptr, *e2 = nullptr;
   double* rsc = nullptr;  // 2^(e1 + 1) per row (Sxy)
+  int8_t* esum = nullptr;  // the 16 sum planes of the symmetric Sxy
+  const bool sym = sxy && ps_sxy_sym(S);
   auto cleanup = [&]() {
+    ps_free(esum, s);
     ps_free(dig, s);
     ps_free(pres, s);
     ps_free(rsc, s);
@@ -967,6 +1034,7 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   if (e == cudaSuccess) e = ps_alloc(&e1, (size_t)F, s);
   if (e == cudaSuccess) e = ps_alloc(&e2, (size_t)F, s);
   if (e == cudaSuccess && sxy) e = ps_alloc(&rsc, (size_t)F, s);
+  if (e == cudaSuccess && sym) e = ps_alloc(&esum, (size_t)(kSymPairs * F * Sp), s);
   if (e == cudaSuccess && sxy)
     e = cudaFuncSetAttribute(cross_gemm_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMomSmem);
   if (e == cudaSuccess)
@@ -1006,6 +1074,11 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
   if (!rc) rc = make_i8_map(&bmap_half, pres, F, Sp, QN / 2);  // multicast halves
   for (int d = 0; d < kDigits && !rc; ++d) rc = make_i8_map(&amap[d], dig + d * F * Sp, F, Sp);
   for (int d = 0; d < kDigits && !rc && sxy; ++d) rc = make_i8_map(&ahalf[d], dig + d * F * Sp, F, Sp, QN / 2);
+  CUtensorMap emap[kSymPairs], ehalf[kSymPairs];
+  for (int d = 0; d < kSymPairs && !rc && sym; ++d) {
+    rc = make_i8_map(&emap[d], esum + d * F * Sp, F, Sp);
+    if (!rc) rc = make_i8_map(&ehalf[d], esum + d * F * Sp, F, Sp, QN / 2);
+  }
   if (rc) {
     cleanup();
     ps_free(sx, s);
@@ -1088,10 +1161,17 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
       // fixed order (smallest weights first); the terms with s + t >= 10 are
       // below 2^-55.1 of the row scales (the pair kernel's bound accounts for them)
       int first = 1;
-      sxy_groups(S, amap, ahalf, [&](const CrossMaps& cm, double w) {
+      auto emit = [&](const CrossMaps& cm, double w) {
         cross(cm, w, first, sxy, nullptr);
         first = 0;
-      });
+      };
+      if (sym) {
+        digit_sum_kernel<<<(unsigned)nrows, 256, 0, s>>>(dig, F * Sp, Sp, r0, esum);
+        PS_LAUNCHED();
+        sxy_sym_products(emap, ehalf, amap, ahalf, emit);
+      } else {
+        sxy_groups(S, amap, ahalf, emit);
+      }
     }
   }
   ps_prof_end(s);
@@ -1115,11 +1195,12 @@ struct ps_moments_job {
   const double* xc = nullptr;
   int64_t F = 0, S = 0, Sp = 0, NT = 0;
   int nk = 0;
-  int8_t *dig = nullptr, *dig2 = nullptr, *pres = nullptr;
+  int8_t *dig = nullptr, *dig2 = nullptr, *pres = nullptr, *esum = nullptr;
   int32_t *e1 = nullptr, *e2 = nullptr;
   double *rsc = nullptr, *sx = nullptr, *sq = nullptr, *sxy = nullptr;
   int32_t* nn = nullptr;
   CUtensorMap a1[kDigits], a1h[kDigits], a2[kDigits], bmap, bmap_half;
+  CUtensorMap em[kSymPairs], emh[kSymPairs];  // sum planes (symmetric Sxy)
   int64_t rows_done = 0, cols_done = 0;
   int grid_cap = 1;
 };
@@ -1127,6 +1208,7 @@ struct ps_moments_job {
 static void job_release(ps_moments_job* j, cudaStream_t s, bool outputs) {
   ps_free(j->dig, s);
   ps_free(j->dig2, s);
+  ps_free(j->esum, s);
   ps_free(j->pres, s);
   ps_free(j->rsc, s);
   if (outputs) {
@@ -1157,6 +1239,7 @@ int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int3
   if (e == cudaSuccess) e = ps_alloc(&j->dig, (size_t)(kDigits * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&j->dig2, (size_t)(kDigits * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&j->pres, (size_t)(F * Sp), s);
+  if (e == cudaSuccess && sxy && ps_sxy_sym(j->S)) e = ps_alloc(&j->esum, (size_t)(kSymPairs * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&j->e1, (size_t)F, s);
   if (e == cudaSuccess) e = ps_alloc(&j->e2, (size_t)F, s);
   if (e == cudaSuccess) e = ps_alloc(&j->rsc, (size_t)F, s);
@@ -1178,6 +1261,10 @@ int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int3
     rc = make_i8_map(&j->a1[d], j->dig + d * F * Sp, F, Sp);
     if (!rc) rc = make_i8_map(&j->a1h[d], j->dig + d * F * Sp, F, Sp, QN / 2);
     if (!rc) rc = make_i8_map(&j->a2[d], j->dig2 + d * F * Sp, F, Sp);
+  }
+  for (int d = 0; d < kSymPairs && !rc && j->esum; ++d) {
+    rc = make_i8_map(&j->em[d], j->esum + d * F * Sp, F, Sp);
+    if (!rc) rc = make_i8_map(&j->emh[d], j->esum + d * F * Sp, F, Sp, QN / 2);
   }
   if (rc) {
     job_release(j, s, true);
@@ -1218,6 +1305,10 @@ int ps_moments_job_rows(ps_moments_job* j, int64_t r1, cudaStream_t s) {
   PS_LAUNCHED();
   moment_digit_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e2, 1, r0, j->F * j->Sp, j->dig2);
   PS_LAUNCHED();
+  if (j->esum) {
+    digit_sum_kernel<<<(unsigned)n, 256, 0, s>>>(j->dig, j->F * j->Sp, j->Sp, r0, j->esum);
+    PS_LAUNCHED();
+  }
   row_scale_kernel<<<(unsigned)ps_ceil_div(n, 256), 256, 0, s>>>(j->e1, r0, n, j->rsc);
   PS_LAUNCHED();
   j->rows_done = r1;
@@ -1271,10 +1362,12 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
     cn1.b[0] = j->bmap_half;
     cross(cn1, 1.0, 1, nullptr, j->nn);
     int first = 1;
-    sxy_groups(j->S, j->a1, j->a1h, [&](const CrossMaps& cm, double w) {
+    auto emit = [&](const CrossMaps& cm, double w) {
       cross(cm, w, first, j->sxy, nullptr);
       first = 0;
-    });
+    };
+    if (j->esum) sxy_sym_products(j->em, j->emh, j->a1, j->a1h, emit);
+    else sxy_groups(j->S, j->a1, j->a1h, emit);
   }
   ps_prof_end(s);
   j->cols_done = J1;

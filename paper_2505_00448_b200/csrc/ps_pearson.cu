@@ -128,17 +128,20 @@ __device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, d
 // ag ah = 2^(e_g + e_h + 2); the fp64 fold of 36 scaled exact
 // products errs by <= 36 * 2^-53 of the sum of their magnitudes, bounded (Cauchy-
 // Schwarz over the joint samples, digit excess delta = 2^-7 of the row scale) by
-// sqrt(qx qy) + delta 2^(e+1) sqrt(n q) terms.  4x margin; replay when the bound
-// exceeds 1e-12 sqrt(sxx syy).
+// sqrt(qx qy) + delta 2^(e+1) sqrt(n q) terms.  The symmetric form (sum planes,
+// ps_moments.cu: 24 products, each scaled term rounded once more) folds squares
+// that cancel: |w (d_s d_s' + d_t d_t')| <= 2^-7 of ag ah per sample in at most
+// nine partial sums, another n ag ah 2^-56.  The bound covers both forms.  4x
+// margin; replay when it exceeds 1e-12 sqrt(sxx syy).
 __device__ __forceinline__ bool sxy_imprecise(int n, double sx, double sy, double qx, double qy, int e1g, int e1h) {
   if (n <= 1) return false;
   const double fn = (double)n;
   const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
   if (!(sxx > 0.0) || !(syy > 0.0)) return false;  // replayed by the degenerate-variance rule anyway
   const double ag = ldexp(1.0, e1g + 1), ah = ldexp(1.0, e1h + 1), dl = 0.0078125;
-  const double trunc = fn * ag * ah * ldexp(1.0, -54);
+  const double trunc = fn * ag * ah * (ldexp(1.0, -54) + ldexp(1.0, -56));
   const double mag = sqrt(qx * qy) + dl * ag * sqrt(fn * qy) + dl * ah * sqrt(fn * qx) + fn * dl * dl * ag * ah;
-  const double bound = 4.0 * (trunc + (double)kSxyProducts * ldexp(mag, -53));
+  const double bound = 4.0 * (trunc + (double)kSxyFoldTerms * ldexp(mag, -53));
   return bound > 1e-12 * sqrt(sxx * syy);
 }
 

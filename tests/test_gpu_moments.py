@@ -159,3 +159,27 @@ def test_cta_pair_gemms_bitwise_equal_multicast(monkeypatch, F, S):
         res[mode] = [o.cpu().numpy() for o in outs] + [full["stat"], full["p"]]
     for a, b in zip(res["0"], res["1"]):
         assert bitwise_equal(a, b)
+
+
+def test_symmetric_sxy_matches_digit_products(oracle, monkeypatch):
+    """Sxy from 16 sum-plane products (D_s + D_t)(D_s + D_t)^T and the 8 squares
+    (default for S < 2^17) is the same exact integer sum as the 36 digit products
+    (PS_SXY_SYM=0); only the fp64 fold order differs: r within 1e-13, p within
+    1e-9, both inside the oracle tolerances (range / upload-order independence of
+    the default form: test_moments_range_independent, test_gpu_overlap.py)."""
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    F, S = 700, 3000
+    raw = workloads.simulate(F, S, "continuous", na_ratio=0.3, seed=21)
+    raw[5] = raw[5] * 1e6 + 3e6   # large scale, offset of a few sigma
+    raw[9, ::7] = 0.0
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    monkeypatch.setenv("PS_SXY_SYM", "0")
+    plain = ps.run(req, mat)
+    monkeypatch.setenv("PS_SXY_SYM", "1")
+    sym = ps.run(req, mat)
+    assert same_nan(plain["stat"], sym["stat"])
+    m = ~np.isnan(plain["stat"])
+    assert np.max(np.abs(plain["stat"][m] - sym["stat"][m])) <= 1e-13
+    assert p_close(sym["p"], plain["p"], rtol=1e-9)
+    _check(sym, oracle.oracle_run(req, mat))

@@ -24,11 +24,22 @@ def main():
     out = {"note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel: from the "
                    "full-size `ncu --set full` capture where one exists (ncu_summary.json, configs 2, 3, 4:anova, "
                    "4:kruskal, 5s), else averaged over the ncu launch-list pass (launches_<config>.json; "
-                   "config 5: cross_gemm_mc, the int8 Sxy digit-product GEMM of the all-int8 Pearson path)."}
+                   "config 5: every kernel of the int8 contraction phase per step, the region bench.py times)."}
     for name, (key, test) in CONFIGS.items():
         # config 1: split-K cp.async tiles; config 5: the int8 Sxy cross GEMM (all-int8 path)
         kern = "pearson_tile" if name == "1" else "cross_gemm" if name == "5" else KERNEL[test]
         val = None
+        if name == "5":
+            # bench.py's roofline region is the whole int8 contraction phase (one "launch" per step):
+            # every kernel of the phase, summed over the launch list's 2 steps (1 warm-up + 1 timed)
+            lj = pdir / "launches_5.json"
+            if lj.exists():
+                phase = ("cross_gemm", "moment_gemm", "moment_digit", "digit_sum", "presence_i8", "moment_scale",
+                         "row_scale")
+                val = sum(r["launches"] * r["dram_bytes_per_launch"] for r in json.loads(lj.read_text())
+                          if any(k in r["kernel"] for k in phase)) / 2.0
+            out[f"{key}:{test}"] = val
+            continue
         rep = f"ncu_{name}_{kern}.ncu-rep"
         if rep in full:
             d = full[rep]
