@@ -435,13 +435,16 @@ def roofline(wl: Workload, kern_ms: float, kern_n: int, steps: int, world: int, 
         F = wl.Fa
         sym = S <= (2 ** 31 - 1) // 16384 and os.environ.get("PS_SXY_SYM", "1")[:1] != "0"
         nxy = 24 if sym else 36
-        ops = ((7 + 8) * 2.0 * F * F + (nxy * 2.0 + 2.0) * F * (F + 1) / 2) * S / world
+        b256 = S <= (2 ** 31 - 1) // 128 and os.environ.get("PS_MOMENTS_B256", "1")[:1] != "0"
+        nmo = 13 if b256 else 15  # moment planes per ordered pair: base 256 (6 + 7) or base 128 (7 + 8)
+        ops = (nmo * 2.0 * F * F + (nxy * 2.0 + 2.0) * F * (F + 1) / 2) * S / world
         # a ~1 s phase under the power cap: the sustained microbenchmark figure (burst: 4610)
         peak = peaks["tcgen05_i8_tops_sustained"]
         achieved = ops / (launch_ms / 1e3) / 1e12
         bound, unit = "tensor", "TOPS"
-        desc = (f"{2 * (30 + nxy + 1)} int8 ops per pair-sample (tcgen05 kind::i8 exact digit contractions: Sx, Sy 7 "
-                "digits, Sxx, Syy 8 digits, Sxy " + ("16 sum-plane products (D_s + D_t)(D_s + D_t)^T + 8 squares "
+        desc = (f"{2 * (2 * nmo + nxy + 1)} int8 ops per pair-sample (tcgen05 kind::i8 exact digit contractions: "
+                + ("Sx, Sy 6 base-256 digits, Sxx, Syy 7" if b256 else "Sx, Sy 7 base-128 digits, Sxx, Syy 8")
+                + ", Sxy " + ("16 sum-plane products (D_s + D_t)(D_s + D_t)^T + 8 squares "
                 "= the 36 digit products s + t <= 9" if sym else "36 digit products s + t <= 9") + ", n)")
     elif bound == "tensor":
         if test == "pearson" and moments_path(wl) == 1:

@@ -90,9 +90,12 @@ __global__ void moment_scale_kernel(const double* __restrict__ xc, int64_t ld, i
   }
 }
 
-// all kDigits digits of every x' (or x'^2) of rows [f0, f0 + gridDim.x) as
-// int8 planes out + (digit - 1) * plane (F x Sp each), zero past S; one pass
-// over the operand, 16 samples per thread
+// all ND balanced base-2^BITS digits of every x' (or x'^2) of rows [f0, f0 +
+// gridDim.x) as int8 planes out + (digit - 1) * plane (F x Sp each), zero past
+// S; one pass over the operand, 16 samples per thread.  BITS = 7: digits in
+// [-64, 64] (the Sxy planes: sums of two stay int8); BITS = 8: [-128, 127],
+// the moments' planes (their other operand is the 0/1 presence).
+template <int BITS, int ND>
 __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, int64_t S, int64_t Sp,
                                     const int32_t* __restrict__ rexp, int square, int64_t f0, int64_t plane,
                                     int8_t* __restrict__ out) {
@@ -100,11 +103,14 @@ __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, i
   const double* row = xc + f * ld;
   const int e = rexp[f];
   const bool zero = e == kNonFinite;  // (its moments are written as NaN)
-  const int shift = 7 * kDigits - 1 - e;  // u = rint(v 2^(7 kDigits)), v = x / 2^(e + 1): |u| < 2^(7 kDigits - 1)
+  // u = rint(v 2^(BITS ND)), v = x / 2^(e + 1 + G): |u| <= 2^(BITS ND - 1 - G); base 256 takes a guard bit
+  // (G = 1) so the most significant digit stays within +-65 (a full-range top digit could round up to 128)
+  const int shift = BITS * ND - (BITS == 8 ? 2 : 1) - e;
+  constexpr long long kHalf = 1ll << (BITS - 1), kMask = (1ll << BITS) - 1;
   for (int64_t s0 = (int64_t)threadIdx.x * 16; s0 < Sp; s0 += (int64_t)blockDim.x * 16) {
-    uint32_t w[kDigits][4];
+    uint32_t w[ND][4];
 #pragma unroll
-    for (int d = 0; d < kDigits; ++d) w[d][0] = w[d][1] = w[d][2] = w[d][3] = 0u;
+    for (int d = 0; d < ND; ++d) w[d][0] = w[d][1] = w[d][2] = w[d][3] = 0u;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int64_t s = s0 + q;
@@ -112,19 +118,19 @@ __global__ void moment_digit_kernel(const double* __restrict__ xc, int64_t ld, i
         double x = row[s];
         if (square) x = x * x;
         long long u = __double2ll_rn(ldexp(x, shift));
-        // balanced base-128 digits from the least significant one up; the
-        // most significant is what remains (|.| <= 64)
+        // balanced digits from the least significant one up; the most
+        // significant is what remains (|.| <= 64 + carry)
 #pragma unroll
-        for (int d = kDigits - 1; d >= 1; --d) {
-          const long long lo = ((u + 64) & 127) - 64;
-          u = (u - lo) >> 7;
+        for (int d = ND - 1; d >= 1; --d) {
+          const long long lo = ((u + kHalf) & kMask) - kHalf;
+          u = (u - lo) >> BITS;
           w[d][q >> 2] |= (uint32_t)(uint8_t)(int8_t)lo << (8 * (q & 3));
         }
         w[0][q >> 2] |= (uint32_t)(uint8_t)(int8_t)u << (8 * (q & 3));
       }
     }
 #pragma unroll
-    for (int d = 0; d < kDigits; ++d)
+    for (int d = 0; d < ND; ++d)
       *reinterpret_cast<uint4*>(out + d * plane + f * Sp + s0) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
   }
 }
@@ -270,7 +276,7 @@ moment_gemm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_consta
         const int64_t r = I * QM + half * 128 + warp * 32 + lane;
         const bool rok = r < F;
         const int ex = rok ? rexp[r] : 0;
-        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - digit);
         double* orow = out + (rok ? r : 0) * F;
 #pragma unroll 1
         for (int cc = 0; cc < QN / 32; ++cc) {
@@ -409,7 +415,7 @@ moment_gemm_mc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_con
         const int64_t r = I * QM + half * 128 + warp * 32 + lane;
         const bool rok = r < F;
         const int ex = rok ? rexp[r] : 0;
-        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+        const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - digit);
         double* orow = out + (rok ? r : 0) * F;
 #pragma unroll 1
         for (int cc = 0; cc < QN / 32; ++cc) {
@@ -778,7 +784,7 @@ moment_gemm_2sm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_co
           const int64_t r = I * QM + half * 128 + warp * 32 + lane;
           const bool rok = r < F;
           const int ex = rok ? rexp[r] : 0;
-          const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - 7 * digit);
+          const double scale = ex == kNonFinite ? PS_NAN : ldexp(1.0, ex + 1 - digit);
           double* orow = out + (rok ? r : 0) * F;
 #pragma unroll 1
           for (int cc = 0; cc < QN / 32; ++cc) {
@@ -990,6 +996,28 @@ bool ps_sxy_sym(int64_t S) {
   return !(e && e[0] == '0') && S <= (int64_t)(INT32_MAX / 16384);
 }
 
+// Moment planes in balanced base 256 (digits in [-128, 127] against the 0/1
+// presence: |sum| <= 128 S in int32; one guard bit, so x = 2^(e + 2) sum_d
+// D_d 2^-8d): 6 planes carry Sx (rounded at 2^(e - 47)), 7 carry Sxx
+// (2^(e - 55)) -- 13 contractions per ordered pair instead of 15.
+// PS_MOMENTS_B256=0: the base-128 planes (7 + 8).
+constexpr int kSxDigits256 = 6, kSqDigits256 = 7;
+bool ps_moments_b256(int64_t S) {
+  const char* e = getenv("PS_MOMENTS_B256");
+  return !(e && e[0] == '0') && S <= (int64_t)(INT32_MAX / 128);
+}
+// x' (sq = 0) or x'^2 (sq = 1) of rows [r0, r0 + n) into the moments' planes
+static void moment_planes(bool b256, int sq, const double* xc, int64_t ld, int64_t S, int64_t Sp, const int32_t* ex,
+                          int64_t r0, int64_t n, int64_t plane, int8_t* out, cudaStream_t s) {
+  if (!b256)
+    moment_digit_kernel<7, kDigits><<<(unsigned)n, 256, 0, s>>>(xc, ld, S, Sp, ex, sq, r0, plane, out);
+  else if (sq)
+    moment_digit_kernel<8, kSqDigits256><<<(unsigned)n, 256, 0, s>>>(xc, ld, S, Sp, ex, sq, r0, plane, out);
+  else
+    moment_digit_kernel<8, kSxDigits256><<<(unsigned)n, 256, 0, s>>>(xc, ld, S, Sp, ex, sq, r0, plane, out);
+}
+static int moment_digits(bool b256, int sq) { return b256 ? (sq ? kSqDigits256 : kSxDigits256) : (sq ? kDigits : kSxDigits); }
+
 // int8 Sxy: each digit product accumulates |d_s d_t| <= 4096 per sample in
 // int32, so the samples are capped at 2^31 / 4096 (the moments' 0/1 operand
 // allows 64x more)
@@ -1134,43 +1162,51 @@ int ps_pearson_moments(const ps_matrix* a, const double* xc, int64_t lo, int64_t
     row_scale_kernel<<<(unsigned)ps_ceil_div(nrows, 256), 256, 0, s>>>(e1, r0, nrows, rsc);
     PS_LAUNCHED();
   }
+  const bool b256 = ps_moments_b256(S);
+  const int bits = b256 ? 8 : 7;
+  if (sxy) {
+    // Sxy = 2^(e_i + e_j + 2) sum_{s + t <= 9} 2^-7(s+t) D_s D_t^T from the base-128
+    // planes, folded in a fixed order (smallest weights first); the terms with
+    // s + t >= 10 are below 2^-55.1 of the row scales (the pair kernel's bound
+    // accounts for them)
+    moment_digit_kernel<7, kDigits><<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, e1, 0, r0, F * Sp, dig);
+    PS_LAUNCHED();
+    int first = 1;
+    auto emit = [&](const CrossMaps& cm, double w) {
+      cross(cm, w, first, sxy, nullptr);
+      first = 0;
+    };
+    if (sym) {
+      digit_sum_kernel<<<(unsigned)nrows, 256, 0, s>>>(dig, F * Sp, Sp, r0, esum);
+      PS_LAUNCHED();
+      sxy_sym_products(emap, ehalf, amap, ahalf, emit);
+    } else {
+      sxy_groups(S, amap, ahalf, emit);
+    }
+  }
   for (int sq_pass = 0; sq_pass < 2; ++sq_pass) {
     double* out = sq_pass ? sq : sx;
     const int32_t* ex = sq_pass ? e2 : e1;
-    moment_digit_kernel<<<(unsigned)nrows, 256, 0, s>>>(xc, a->ld, S, Sp, ex, sq_pass, r0, F * Sp, dig);
-    PS_LAUNCHED();
-    const int nd = sq_pass ? kDigits : kSxDigits;  // Sx: the top 7 planes (its error enters only via Sx^2 / n)
+    if (sq_pass || b256 || !sxy) {  // (the base-128 planes of x' are in place after Sxy)
+      moment_planes(b256, sq_pass, xc, a->ld, S, Sp, ex, r0, nrows, F * Sp, dig, s);
+      PS_LAUNCHED();
+    }
+    const int nd = moment_digits(b256, sq_pass);  // Sx: its error enters only via Sx^2 / n
     for (int d = nd; d >= 1; --d) {  // least significant digit first (fixed fold order)
       for (int rect = 0; rect < 2; ++rect) {
         const int64_t ri = rect ? I2 : I0, rn = rect ? nI2 : nI, cn = rect ? nJ2 : nJ;
         if (rn <= 0 || cn <= 0) continue;
         if (mc && gemm_2sm_mode())
-          moment_gemm_2sm_kernel<<<grid_mc_of(rn, cn), QTH, kMom2Smem, s>>>(
-              amap[d - 1], bmap_half, nk, ri, rn, J0, cn, ex, d, d == nd ? 1 : 0, out, F, gemm_2sm_mode() == 2);
+          moment_gemm_2sm_kernel<<<grid_mc_of(rn, cn), QTH, kMom2Smem, s>>>(amap[d - 1], bmap_half, nk, ri, rn, J0, cn,
+                                                                            ex, bits * d - (bits == 8), d == nd ? 1 : 0, out, F,
+                                                                            gemm_2sm_mode() == 2);
         else if (mc)
           moment_gemm_mc_kernel<<<grid_mc_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap_half, nk, ri, rn, J0, cn,
-                                                                          ex, d, d == nd ? 1 : 0, out, F);
+                                                                          ex, bits * d - (bits == 8), d == nd ? 1 : 0, out, F);
         else
-          moment_gemm_kernel<<<grid_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, ri, rn, J0, cn, ex, d,
-                                                                    d == nd ? 1 : 0, out, F);
+          moment_gemm_kernel<<<grid_of(rn, cn), QTH, kMomSmem, s>>>(amap[d - 1], bmap, nk, ri, rn, J0, cn, ex,
+                                                                    bits * d - (bits == 8), d == nd ? 1 : 0, out, F);
         PS_LAUNCHED();
-      }
-    }
-    if (sq_pass == 0 && sxy) {
-      // Sxy = 2^(e_i + e_j + 2) sum_{s + t <= 9} 2^-7(s+t) D_s D_t^T, folded in a
-      // fixed order (smallest weights first); the terms with s + t >= 10 are
-      // below 2^-55.1 of the row scales (the pair kernel's bound accounts for them)
-      int first = 1;
-      auto emit = [&](const CrossMaps& cm, double w) {
-        cross(cm, w, first, sxy, nullptr);
-        first = 0;
-      };
-      if (sym) {
-        digit_sum_kernel<<<(unsigned)nrows, 256, 0, s>>>(dig, F * Sp, Sp, r0, esum);
-        PS_LAUNCHED();
-        sxy_sym_products(emap, ehalf, amap, ahalf, emit);
-      } else {
-        sxy_groups(S, amap, ahalf, emit);
       }
     }
   }
@@ -1196,6 +1232,9 @@ struct ps_moments_job {
   int64_t F = 0, S = 0, Sp = 0, NT = 0;
   int nk = 0;
   int8_t *dig = nullptr, *dig2 = nullptr, *pres = nullptr, *esum = nullptr;
+  int8_t* dig1b = nullptr;  // base-256 planes of x' (Sx); dig keeps the base-128 planes of Sxy
+  bool b256 = false;
+  CUtensorMap a1b[kDigits];
   int32_t *e1 = nullptr, *e2 = nullptr;
   double *rsc = nullptr, *sx = nullptr, *sq = nullptr, *sxy = nullptr;
   int32_t* nn = nullptr;
@@ -1209,6 +1248,7 @@ static void job_release(ps_moments_job* j, cudaStream_t s, bool outputs) {
   ps_free(j->dig, s);
   ps_free(j->dig2, s);
   ps_free(j->esum, s);
+  ps_free(j->dig1b, s);
   ps_free(j->pres, s);
   ps_free(j->rsc, s);
   if (outputs) {
@@ -1237,7 +1277,9 @@ int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int3
   cudaError_t e = ps_alloc(&j->sx, (size_t)(F * F), s);
   if (e == cudaSuccess) e = ps_alloc(&j->sq, (size_t)(F * F), s);
   if (e == cudaSuccess) e = ps_alloc(&j->dig, (size_t)(kDigits * F * Sp), s);
-  if (e == cudaSuccess) e = ps_alloc(&j->dig2, (size_t)(kDigits * F * Sp), s);
+  j->b256 = ps_moments_b256(j->S);
+  if (e == cudaSuccess) e = ps_alloc(&j->dig2, (size_t)(moment_digits(j->b256, 1) * F * Sp), s);
+  if (e == cudaSuccess && j->b256) e = ps_alloc(&j->dig1b, (size_t)(kSxDigits256 * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&j->pres, (size_t)(F * Sp), s);
   if (e == cudaSuccess && sxy && ps_sxy_sym(j->S)) e = ps_alloc(&j->esum, (size_t)(kSymPairs * F * Sp), s);
   if (e == cudaSuccess) e = ps_alloc(&j->e1, (size_t)F, s);
@@ -1260,7 +1302,8 @@ int ps_moments_job_begin(const ps_matrix* a, const double* xc, double* sxy, int3
   for (int d = 0; d < kDigits && !rc; ++d) {
     rc = make_i8_map(&j->a1[d], j->dig + d * F * Sp, F, Sp);
     if (!rc) rc = make_i8_map(&j->a1h[d], j->dig + d * F * Sp, F, Sp, QN / 2);
-    if (!rc) rc = make_i8_map(&j->a2[d], j->dig2 + d * F * Sp, F, Sp);
+    if (!rc && d < moment_digits(j->b256, 1)) rc = make_i8_map(&j->a2[d], j->dig2 + d * F * Sp, F, Sp);
+    if (!rc && j->b256 && d < kSxDigits256) rc = make_i8_map(&j->a1b[d], j->dig1b + d * F * Sp, F, Sp);
   }
   for (int d = 0; d < kSymPairs && !rc && j->esum; ++d) {
     rc = make_i8_map(&j->em[d], j->esum + d * F * Sp, F, Sp);
@@ -1301,9 +1344,16 @@ int ps_moments_job_rows(ps_moments_job* j, int64_t r1, cudaStream_t s) {
   PS_LAUNCHED();
   presence_i8_kernel<<<(unsigned)n, 256, 0, s>>>(a->d_mask, a->W, j->S, j->Sp, j->pres, r0);
   PS_LAUNCHED();
-  moment_digit_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e1, 0, r0, j->F * j->Sp, j->dig);
-  PS_LAUNCHED();
-  moment_digit_kernel<<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e2, 1, r0, j->F * j->Sp, j->dig2);
+  if (j->sxy || !j->b256) {
+    moment_digit_kernel<7, kDigits><<<(unsigned)n, 256, 0, s>>>(j->xc, a->ld, j->S, j->Sp, j->e1, 0, r0, j->F * j->Sp,
+                                                                j->dig);
+    PS_LAUNCHED();
+  }
+  if (j->b256) {
+    moment_planes(true, 0, j->xc, a->ld, j->S, j->Sp, j->e1, r0, n, j->F * j->Sp, j->dig1b, s);
+    PS_LAUNCHED();
+  }
+  moment_planes(j->b256, 1, j->xc, a->ld, j->S, j->Sp, j->e2, r0, n, j->F * j->Sp, j->dig2, s);
   PS_LAUNCHED();
   if (j->esum) {
     digit_sum_kernel<<<(unsigned)n, 256, 0, s>>>(j->dig, j->F * j->Sp, j->Sp, r0, j->esum);
@@ -1326,9 +1376,9 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
   for (int pass = 0; pass < 2; ++pass) {
     double* out = pass ? j->sq : j->sx;
     const int32_t* ex = pass ? j->e2 : j->e1;
-    const int nd = pass ? kDigits : kSxDigits;
+    const int nd = moment_digits(j->b256, pass), bits = j->b256 ? 8 : 7;
     for (int d = nd; d >= 1; --d) {
-      const CUtensorMap& am = pass ? j->a2[d - 1] : j->a1[d - 1];
+      const CUtensorMap& am = pass ? j->a2[d - 1] : j->b256 ? j->a1b[d - 1] : j->a1[d - 1];
       // rows [0, J1) x columns [J0, J1), then rows [J0, J1) x columns [0, J0)
       for (int rect = 0; rect < 2; ++rect) {
         const int64_t ri = rect ? J0 : 0, rn = rect ? J1 - J0 : J1;
@@ -1336,10 +1386,10 @@ int ps_moments_job_cols(ps_moments_job* j, int64_t J1, cudaStream_t s) {
         if (rn <= 0 || cn <= 0) continue;
         if (gemm_2sm_mode())
           moment_gemm_2sm_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMom2Smem, s>>>(
-              am, j->bmap_half, j->nk, ri, rn, ci, cn, ex, d, d == nd ? 1 : 0, out, j->F, gemm_2sm_mode() == 2);
+              am, j->bmap_half, j->nk, ri, rn, ci, cn, ex, bits * d - (bits == 8), d == nd ? 1 : 0, out, j->F, gemm_2sm_mode() == 2);
         else
           moment_gemm_mc_kernel<<<gmc(((rn + 1) / 2) * cn), QTH, kMomSmem, s>>>(am, j->bmap_half, j->nk, ri, rn, ci, cn,
-                                                                                ex, d, d == nd ? 1 : 0, out, j->F);
+                                                                                ex, bits * d - (bits == 8), d == nd ? 1 : 0, out, j->F);
         PS_LAUNCHED();
       }
     }

@@ -110,8 +110,11 @@ __device__ __forceinline__ bool moments_imprecise(int n, double sx, double sy, d
                                                   int e2g, int e1h, int e2h) {
   if (n <= 1) return false;
   const double fn = (double)n;
-  constexpr int kB = 7 * kMomentDigits - 2;  // 4x the bound (Sxx: rounded at digit 8)
-  constexpr int kB1 = 7 * kSxDigits - 3;     // 8x the bound (Sx: truncated after digit 7, ~2^(e - 49))
+  // 4x the bound of Sxx: seven base-256 planes with a guard bit round at 2^(e - 55) (eight base-128
+  // digits, PS_MOMENTS_B256=0: 2^(e - 56)); 8x the bound of Sx: six base-256 planes round at 2^(e - 47)
+  // (base 128: truncated after digit 7, ~2^(e - 49)).  One bound for both forms.
+  constexpr int kB = 53;
+  constexpr int kB1 = 44;
   const double d1g = ldexp(1.0, e1g - kB1), d2g = ldexp(1.0, e2g - kB);
   const double d1h = ldexp(1.0, e1h - kB1), d2h = ldexp(1.0, e2h - kB);
   const double sxx = qx - sx * sx / fn, syy = qy - sy * sy / fn;
