@@ -183,3 +183,21 @@ def test_symmetric_sxy_matches_digit_products(oracle, monkeypatch):
     assert np.max(np.abs(plain["stat"][m] - sym["stat"][m])) <= 1e-13
     assert p_close(sym["p"], plain["p"], rtol=1e-9)
     _check(sym, oracle.oracle_run(req, mat))
+
+
+@pytest.mark.parametrize("b256", ["0", "1"])
+def test_moment_plane_bases_match_oracle(oracle, monkeypatch, b256):
+    """The moments from balanced base-256 planes (default: 6 for Sx, 7 for Sxx,
+    one guard bit) and from the base-128 planes (PS_MOMENTS_B256=0: 7 + 8) both
+    meet the oracle tolerances, on rows with large offsets / scales and values
+    at the top of a row's binade (the most significant digit's range)."""
+    monkeypatch.setenv("PS_PEARSON_MOMENTS", "1")
+    monkeypatch.setenv("PS_MOMENTS_B256", b256)
+    F, S = 300, 4000
+    raw = workloads.simulate(F, S, "continuous", na_ratio=0.25, seed=33)
+    raw[2] = raw[2] * 1e-7 - 3e-7
+    raw[4] = np.where(np.isnan(raw[4]), np.nan, np.sign(raw[4]) * (1.0 - 2.0 ** -40))  # |x| just under 2^0
+    raw[6, :50] = 1.9999999 * np.nanmax(np.abs(raw[6]))
+    mat = ps.make_matrix(raw, "continuous")
+    req = ps.TestRequest("pearson", ("stat", "p"))
+    _check(ps.run(req, mat), oracle.oracle_run(req, mat))
